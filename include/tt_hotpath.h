@@ -1,0 +1,152 @@
+/* tt_hotpath.h — C-ABI of the B200 (sm_100a) FP64 tensor-train hot path.
+ *
+ * The operations are the matrix-free building blocks of the TT Newton-system solve of
+ * arXiv 2509.11890 ("An Inexact Tensor-Train Primal-Dual Interior-Point Method for
+ * Semidefinite Programs"); PAPER.md = the paper's LaTeX source, cited by line.
+ *
+ *   TT vector core   x_k in R^{r_k x n_k x r_{k+1}}, r_1 = r_{d+1} = 1
+ *   TT matrix core   A_k in R^{R_k x n_row x n_col x R_{k+1}}
+ *                    (output/row index i first, input/column index j second)
+ *   Block-TT core    X_k in R^{r_k x n_k x nvec x r_{k+1}}
+ *   Interface        Phi in R^{r x R x r}, indices [bra, op, ket]: the interface matrices
+ *                    T^{<k}, T^{>k} sandwiching the operator's partial
+ *                    product, so that the local matvec is the projected operator
+ *                    X_{!=k}^T A X_{!=k} applied to a core.
+ *
+ * Conventions (all calls):
+ *  - Every tensor pointer is DEVICE memory, FP64, C-contiguous in the index order written.
+ *    Shape/size arguments are host int64.  `stream` is a cudaStream_t passed as void*
+ *    (NULL = legacy default stream).
+ *  - Ownership: the caller allocates and owns every buffer, including the workspace.  The
+ *    library never allocates device memory, frees, or retains a pointer past the call.
+ *  - Inputs are never written.  Outputs must not alias inputs (base-pointer equality is
+ *    checked -> TT_ERR_ALIASING).
+ *  - Validation is synchronous; on any error nothing is enqueued.  Execution is
+ *    asynchronous on `stream` (no device synchronisation inside any call), so calls may be
+ *    captured into a CUDA graph.  Launch/configuration failures -> TT_ERR_CUDA; faults
+ *    during execution surface at the caller's next synchronisation.
+ *  - Thread-safe and reentrant; the only mutable state is a thread-local error message.
+ *  - Non-finite inputs are not checked; they propagate.
+ *  - Arithmetic is IEEE FP64 (DMMA tensor-core FMA); summation order differs from the
+ *    paper's plain definition, so results match it to rounding (~1e-15 relative).
+ */
+#ifndef TT_HOTPATH_H
+#define TT_HOTPATH_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  TT_OK = 0,
+  TT_ERR_INVALID_ARGUMENT = 1, /* non-positive extent, r_1/r_{d+1} or R_1/R_{d+1} != 1, bad flag */
+  TT_ERR_NULL_POINTER = 2,
+  TT_ERR_ALIASING = 3,         /* an output base pointer equals an input's or another output's */
+  TT_ERR_WORKSPACE = 4,        /* workspace NULL or smaller than the *_workspace_size() value */
+  TT_ERR_OVERFLOW = 5,         /* an extent product overflows 2^62 elements */
+  TT_ERR_CUDA = 6              /* kernel launch / configuration failure (see message) */
+} tt_status;
+
+const char* tt_status_string(tt_status s);
+/* Detail for the last non-OK status returned on the calling thread ("" if none). */
+const char* tt_last_error_message(void);
+/* Library version string. */
+const char* tt_version(void);
+
+/* ---------------------------------------------------------------------------------------
+ * H1-H3  Local matvec  (master formula (M))
+ *   y[a',i,b'] = sum_{a,alpha,j,beta,b} phiL[a',alpha,a] A[alpha,i,j,beta] phiR[b',beta,b] x[a,j,b]
+ *   phiL (rl,Rl,rl)  A (Rl,n,n,Rr)  phiR (rr,Rr,rr)  x,y (rl,n,rr)
+ * Evaluated as the paper's "three matrix products" on DMMA tensor cores,
+ * intermediates in the caller's workspace.
+ * ------------------------------------------------------------------------------------- */
+size_t tt_local_matvec_workspace_size(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t Rr,
+                                      int64_t nvec);
+tt_status tt_local_matvec(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t Rr,
+                          const double* phiL, const double* A, const double* phiR,
+                          const double* x, double* y,
+                          void* workspace, size_t workspace_bytes, void* stream);
+
+/* H4  Batched Krylov block: the same map on every column m of a Block-TT core
+ *   X, Y (rl, n, nvec, rr)   [PAPER.md:294-300 layout; PAPER.md:488 matrix-free GMRES]
+ * Workspace: tt_local_matvec_workspace_size(rl, n, rr, Rl, Rr, nvec). */
+tt_status tt_local_matvec_batched(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t Rr,
+                                  int64_t nvec, const double* phiL, const double* A,
+                                  const double* phiR, const double* X, double* Y,
+                                  void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------------------
+ * H5/H6  Interface updates (one core of the sweep)
+ *   left : phiL_next[b',beta,b] = sum x[a',i,b'] phiL_prev[a',alpha,a] A[alpha,i,j,beta] x[a,j,b]
+ *          phiL_prev (rl,Rl,rl) -> phiL_next (rr,Rr,rr)
+ *   right: phiR_prev[a',alpha,a] = sum x[a',i,b'] A[alpha,i,j,beta] phiR_next[b',beta,b] x[a,j,b]
+ *          phiR_next (rr,Rr,rr) -> phiR_prev (rl,Rl,rl)
+ * (x is real, so conj(x) = x.)  Workspace: tt_interface_workspace_size(...).
+ * ------------------------------------------------------------------------------------- */
+size_t tt_interface_workspace_size(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t Rr);
+tt_status tt_interface_left(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t Rr,
+                            const double* phiL_prev, const double* A, const double* x,
+                            double* phiL_next,
+                            void* workspace, size_t workspace_bytes, void* stream);
+tt_status tt_interface_right(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t Rr,
+                             const double* phiR_next, const double* A, const double* x,
+                             double* phiR_prev,
+                             void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------------------
+ * H7  Sweep: chain the interface updates over d cores from the boundary values
+ *     T^{<1} = T^{>d} = 1.
+ *   n[d], r[d+1], R[d+1], x_cores[d], A_cores[d], phiL[d+1], phiR[d+1] are HOST arrays; the
+ *   pointers they hold are device pointers.  x_cores[k] (r[k],n[k],r[k+1]),
+ *   A_cores[k] (R[k],n[k],n[k],R[k+1]).
+ *   phiL[k], k=0..d: interface of cores 0..k-1, shape (r[k],R[k],r[k]); phiL[0] is set to 1.
+ *   phiR[k], k=0..d: interface of cores k..d-1, shape (r[k],R[k],r[k]); phiR[d] is set to 1.
+ *   The local matvec at core k uses phiL[k] and phiR[k+1]; phiL[d] == phiR[0] == x^T A x.
+ *   directions: TT_SWEEP_LEFT, TT_SWEEP_RIGHT or TT_SWEEP_BOTH; a NULL phiL / phiR array
+ *   skips that direction.
+ * ------------------------------------------------------------------------------------- */
+enum { TT_SWEEP_LEFT = 1, TT_SWEEP_RIGHT = 2, TT_SWEEP_BOTH = 3 };
+size_t tt_sweep_workspace_size(int64_t d, const int64_t* n, const int64_t* r, const int64_t* R);
+tt_status tt_sweep_interfaces(int64_t d, const int64_t* n, const int64_t* r, const int64_t* R,
+                              const double* const* x_cores, const double* const* A_cores,
+                              double* const* phiL, double* const* phiR, int directions,
+                              void* workspace, size_t workspace_bytes, void* stream);
+
+/* H7 with the local matvecs interleaved: the ALS/AMEn sweep skeleton with the cores held
+ * fixed (SURVEY.md §8(c) reading R9, workload "W5"):
+ *   build phiR[d-1..1] right-to-left; then for k = 0..d-1: Y_fwd[k] = local matvec of
+ *   X_blocks[k] (Block-TT, nvec columns) with phiL[k], A_cores[k], phiR[k+1], then
+ *   phiL[k+1] if k < d-1; then for k = d-1..0: Y_bwd[k] = local matvec, then phiR[k] if k > 0.
+ *   X_blocks[k], Y_fwd[k], Y_bwd[k]: (r[k], n[k], nvec, r[k+1]); Y_bwd may be NULL (the
+ *   backward pass then overwrites Y_fwd).  phiL/phiR as in tt_sweep_interfaces (both required).
+ * Workspace: tt_sweep_als_workspace_size(d, n, r, R, nvec). */
+size_t tt_sweep_als_workspace_size(int64_t d, const int64_t* n, const int64_t* r,
+                                   const int64_t* R, int64_t nvec);
+tt_status tt_sweep_als(int64_t d, const int64_t* n, const int64_t* r, const int64_t* R,
+                       int64_t nvec, const double* const* x_cores,
+                       const double* const* A_cores, const double* const* X_blocks,
+                       double* const* Y_fwd, double* const* Y_bwd,
+                       double* const* phiL, double* const* phiR,
+                       void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------------------
+ * H8  Full unrounded TT-matrix x TT-vector product ("ranks grow"; residuals
+ *     A vec_TT(X)):
+ *   z_k[(a,alpha), i, (b,beta)] = sum_j A_k[alpha,i,j,beta] x_k[a,j,b],
+ *   combined bond index a*R[k] + alpha (vector bond major).
+ *   A_cores[k] (R[k], n_row[k], n_col[k], R[k+1]), x_cores[k] (r[k], n_col[k], r[k+1]),
+ *   z_cores[k] (r[k]*R[k], n_row[k], r[k+1]*R[k+1]).  n_row != n_col allowed.  No workspace.
+ * ------------------------------------------------------------------------------------- */
+tt_status tt_operator_apply(int64_t d, const int64_t* n_row, const int64_t* n_col,
+                            const int64_t* r, const int64_t* R,
+                            const double* const* x_cores, const double* const* A_cores,
+                            double* const* z_cores, void* stream);
+
+/* Number of kernel launches the last successful call on this thread enqueued. */
+int64_t tt_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TT_HOTPATH_H */

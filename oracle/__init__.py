@@ -39,9 +39,11 @@ def lib():
         L.tt_oracle_interface_right.argtypes = [i64] * 5 + [p] * 4
         L.tt_oracle_sweep_interfaces.argtypes = [i64, p, p, p, p, p, p, p, ctypes.c_int]
         L.tt_oracle_operator_apply.argtypes = [i64, p, p, p, p, p, p, p]
+        L.tt_oracle_apply_core.argtypes = [i64] * 6 + [p] * 3
         for f in ("tt_oracle_local_matvec", "tt_oracle_local_matvec_batched",
                   "tt_oracle_interface_left", "tt_oracle_interface_right",
-                  "tt_oracle_sweep_interfaces", "tt_oracle_operator_apply"):
+                  "tt_oracle_sweep_interfaces", "tt_oracle_operator_apply",
+                  "tt_oracle_apply_core"):
             getattr(L, f).restype = ctypes.c_int
         _ = dp
         _lib = L
@@ -135,4 +137,14 @@ def operator_apply(x_cores, A_cores):
     z = [np.empty((r[k] * R[k], n_row[k], r[k + 1] * R[k + 1])) for k in range(d)]
     _check(lib().tt_oracle_operator_apply(d, _p(n_row), _p(n_col), _p(r), _p(R),
                                           _ptr_array(x_cores), _ptr_array(A_cores), _ptr_array(z)))
+    return z
+
+
+def apply_core(x, A):
+    """One core of the unrounded apply: x (rl,nj,rr), A (Rl,ni,nj,Rr) -> (rl*Rl, ni, rr*Rr)."""
+    x, A = _c(x), _c(A)
+    rl, nj, rr = x.shape
+    Rl, ni, _, Rr = A.shape
+    z = np.empty((rl * Rl, ni, rr * Rr))
+    _check(lib().tt_oracle_apply_core(rl, ni, nj, rr, Rl, Rr, _p(x), _p(A), _p(z)))
     return z

@@ -272,11 +272,33 @@ int tt_oracle_sweep_interfaces(int64_t d, const int64_t* n, const int64_t* r, co
  * Unrounded TT-matrix x TT-vector product (AP), PAPER.md:278 (ranks multiply), 440-443:
  *   z_k[(a,alpha), i, (b,beta)] = sum_j A_k[alpha,i,j,beta] x_k[a,j,b]
  * ------------------------------------------------------------------------------------- */
+/* One core of (AP): z[(a,alpha), i, (b,beta)] = sum_j A[alpha,i,j,beta] x[a,j,b]. */
+int tt_oracle_apply_core(int64_t rl, int64_t ni, int64_t nj, int64_t rr, int64_t Rl, int64_t Rr,
+                         const double* x, const double* A, double* z) {
+  int64_t a, al, i, j, b, be, t = 1;
+  if (!x || !A || !z) return OR_NULL;
+  if (rl <= 0 || ni <= 0 || nj <= 0 || rr <= 0 || Rl <= 0 || Rr <= 0) return OR_INVALID;
+  if (!mul_ok(&t, rl) || !mul_ok(&t, Rl) || !mul_ok(&t, ni) || !mul_ok(&t, rr) || !mul_ok(&t, Rr))
+    return OR_OVERFLOW;
+  for (a = 0; a < rl; ++a)
+    for (al = 0; al < Rl; ++al)
+      for (i = 0; i < ni; ++i)
+        for (b = 0; b < rr; ++b)
+          for (be = 0; be < Rr; ++be) {
+            double s = 0.0;
+            for (j = 0; j < nj; ++j)
+              s += A[((al * ni + i) * nj + j) * Rr + be] * x[(a * nj + j) * rr + b];
+            z[(((a * Rl + al) * ni + i) * rr + b) * Rr + be] = s;
+          }
+  return OR_OK;
+}
+
 int tt_oracle_operator_apply(int64_t d, const int64_t* n_row, const int64_t* n_col,
                              const int64_t* r, const int64_t* R,
                              const double* const* x_cores, const double* const* A_cores,
                              double* const* z_cores) {
-  int64_t k, a, al, i, j, b, be;
+  int64_t k;
+  int st;
   if (d <= 0) return OR_INVALID;
   if (!n_row || !n_col || !r || !R || !x_cores || !A_cores || !z_cores) return OR_NULL;
   if (r[0] != 1 || r[d] != 1 || R[0] != 1 || R[d] != 1) return OR_INVALID;
@@ -285,21 +307,9 @@ int tt_oracle_operator_apply(int64_t d, const int64_t* n_row, const int64_t* n_c
     if (!x_cores[k] || !A_cores[k] || !z_cores[k]) return OR_NULL;
   }
   for (k = 0; k < d; ++k) {
-    const int64_t rl = r[k], rr = r[k + 1], Rl = R[k], Rr = R[k + 1];
-    const int64_t ni = n_row[k], nj = n_col[k];
-    const double* x = x_cores[k];
-    const double* A = A_cores[k];
-    double* z = z_cores[k];
-    for (a = 0; a < rl; ++a)
-      for (al = 0; al < Rl; ++al)
-        for (i = 0; i < ni; ++i)
-          for (b = 0; b < rr; ++b)
-            for (be = 0; be < Rr; ++be) {
-              double s = 0.0;
-              for (j = 0; j < nj; ++j)
-                s += A[((al * ni + i) * nj + j) * Rr + be] * x[(a * nj + j) * rr + b];
-              z[(((a * Rl + al) * ni + i) * rr + b) * Rr + be] = s;
-            }
+    st = tt_oracle_apply_core(r[k], n_row[k], n_col[k], r[k + 1], R[k], R[k + 1], x_cores[k],
+                              A_cores[k], z_cores[k]);
+    if (st) return st;
   }
   return OR_OK;
 }

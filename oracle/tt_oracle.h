@@ -59,6 +59,11 @@ int tt_oracle_operator_apply(int64_t d, const int64_t* n_row, const int64_t* n_c
                              const double* const* x_cores, const double* const* A_cores,
                              double* const* z_cores);
 
+/* One core of the product above: x (rl,nj,rr), A (Rl,ni,nj,Rr) -> z (rl*Rl, ni, rr*Rr).
+ * No boundary-rank condition, so a slice x[a0:a1] gives the matching rows of z_k. */
+int tt_oracle_apply_core(int64_t rl, int64_t ni, int64_t nj, int64_t rr, int64_t Rl, int64_t Rr,
+                         const double* x, const double* A, double* z);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,247 @@
+"""B200-native (sm_100a) FP64 tensor-train hot path of arXiv 2509.11890.
+
+Thin ctypes binding of the C-ABI declared in include/tt_hotpath.h: argument marshalling
+only — every step of the path runs in the CUDA kernels of libtt_hotpath.so.  PyTorch is
+used for device memory and streams.  There is NO CPU fallback: importing this package
+without the built library raises, and every call checks that its tensors are CUDA float64.
+
+Function names are the C names.  Tensor shapes (C-contiguous, float64, on one CUDA device):
+  phiL (rl,Rl,rl)  A (Rl,n,n,Rr)  phiR (rr,Rr,rr)  x,y (rl,n,rr)  X,Y (rl,n,nvec,rr)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import List, Optional, Sequence
+
+import torch
+
+__all__ = [
+    "TTError", "lib", "LIB_PATH",
+    "tt_local_matvec_workspace_size", "tt_local_matvec", "tt_local_matvec_batched",
+    "tt_interface_workspace_size", "tt_interface_left", "tt_interface_right",
+    "tt_sweep_workspace_size", "tt_sweep_interfaces", "tt_sweep_als_workspace_size",
+    "tt_sweep_als", "tt_operator_apply", "tt_last_launch_count",
+    "TT_SWEEP_LEFT", "TT_SWEEP_RIGHT", "TT_SWEEP_BOTH",
+]
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libtt_hotpath.so")
+TT_SWEEP_LEFT, TT_SWEEP_RIGHT, TT_SWEEP_BOTH = 1, 2, 3
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+        "(there is no CPU fallback)")
+
+_i64, _p, _sz = ctypes.c_int64, ctypes.c_void_p, ctypes.c_size_t
+lib = ctypes.CDLL(LIB_PATH)
+lib.tt_status_string.restype = ctypes.c_char_p
+lib.tt_status_string.argtypes = [ctypes.c_int]
+lib.tt_last_error_message.restype = ctypes.c_char_p
+lib.tt_version.restype = ctypes.c_char_p
+lib.tt_last_launch_count.restype = ctypes.c_int64
+lib.tt_local_matvec_workspace_size.restype = _sz
+lib.tt_local_matvec_workspace_size.argtypes = [_i64] * 6
+lib.tt_local_matvec.argtypes = [_i64] * 5 + [_p] * 6 + [_sz, _p]
+lib.tt_local_matvec_batched.argtypes = [_i64] * 6 + [_p] * 6 + [_sz, _p]
+lib.tt_interface_workspace_size.restype = _sz
+lib.tt_interface_workspace_size.argtypes = [_i64] * 5
+lib.tt_interface_left.argtypes = [_i64] * 5 + [_p] * 5 + [_sz, _p]
+lib.tt_interface_right.argtypes = [_i64] * 5 + [_p] * 5 + [_sz, _p]
+lib.tt_sweep_workspace_size.restype = _sz
+lib.tt_sweep_workspace_size.argtypes = [_i64, _p, _p, _p]
+lib.tt_sweep_interfaces.argtypes = [_i64, _p, _p, _p, _p, _p, _p, _p, ctypes.c_int, _p, _sz, _p]
+lib.tt_sweep_als_workspace_size.restype = _sz
+lib.tt_sweep_als_workspace_size.argtypes = [_i64, _p, _p, _p, _i64]
+lib.tt_sweep_als.argtypes = [_i64, _p, _p, _p, _i64] + [_p] * 7 + [_p, _sz, _p]
+lib.tt_operator_apply.argtypes = [_i64, _p, _p, _p, _p, _p, _p, _p, _p]
+for _f in ("tt_local_matvec", "tt_local_matvec_batched", "tt_interface_left",
+           "tt_interface_right", "tt_sweep_interfaces", "tt_sweep_als", "tt_operator_apply"):
+    getattr(lib, _f).restype = ctypes.c_int
+
+
+class TTError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        self.status = status
+        super().__init__(f"{lib.tt_status_string(status).decode()}: {msg}")
+
+
+def _check(st: int) -> None:
+    if st != 0:
+        raise TTError(st, lib.tt_last_error_message().decode())
+
+
+def _dev(t: torch.Tensor, name: str) -> int:
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if not t.is_cuda or t.dtype != torch.float64:
+        raise TypeError(f"{name} must be a CUDA float64 tensor (no CPU fallback)")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be C-contiguous")
+    return t.data_ptr()
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _ws(nbytes: int, workspace: Optional[torch.Tensor], device) -> torch.Tensor:
+    if workspace is not None:
+        return workspace
+    return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+
+
+def tt_last_launch_count() -> int:
+    return int(lib.tt_last_launch_count())
+
+
+def tt_local_matvec_workspace_size(rl, n, rr, Rl, Rr, nvec=1) -> int:
+    return int(lib.tt_local_matvec_workspace_size(rl, n, rr, Rl, Rr, nvec))
+
+
+def tt_interface_workspace_size(rl, n, rr, Rl, Rr) -> int:
+    return int(lib.tt_interface_workspace_size(rl, n, rr, Rl, Rr))
+
+
+def tt_local_matvec(phiL, A, phiR, x, y=None, workspace=None, stream=None):
+    """H1-H3: y = local matvec of core x.  Returns y."""
+    rl, n, rr = x.shape
+    Rl, Rr = A.shape[0], A.shape[3]
+    if y is None:
+        y = torch.empty_like(x)
+    ws = _ws(tt_local_matvec_workspace_size(rl, n, rr, Rl, Rr, 1), workspace, x.device)
+    _check(lib.tt_local_matvec(rl, n, rr, Rl, Rr, _dev(phiL, "phiL"), _dev(A, "A"),
+                               _dev(phiR, "phiR"), _dev(x, "x"), _dev(y, "y"), ws.data_ptr(),
+                               ws.numel(), _stream(stream)))
+    return y
+
+
+def tt_local_matvec_batched(phiL, A, phiR, X, Y=None, workspace=None, stream=None):
+    """H4: the local matvec on every column of a Block-TT core X (rl,n,nvec,rr)."""
+    rl, n, nvec, rr = X.shape
+    Rl, Rr = A.shape[0], A.shape[3]
+    if Y is None:
+        Y = torch.empty_like(X)
+    ws = _ws(tt_local_matvec_workspace_size(rl, n, rr, Rl, Rr, nvec), workspace, X.device)
+    _check(lib.tt_local_matvec_batched(rl, n, rr, Rl, Rr, nvec, _dev(phiL, "phiL"), _dev(A, "A"),
+                                       _dev(phiR, "phiR"), _dev(X, "X"), _dev(Y, "Y"),
+                                       ws.data_ptr(), ws.numel(), _stream(stream)))
+    return Y
+
+
+def tt_interface_left(phiL_prev, A, x, out=None, workspace=None, stream=None):
+    """H5: phiL_next (rr,Rr,rr) from phiL_prev (rl,Rl,rl), A_k, x_k."""
+    rl, n, rr = x.shape
+    Rl, Rr = A.shape[0], A.shape[3]
+    if out is None:
+        out = torch.empty((rr, Rr, rr), dtype=x.dtype, device=x.device)
+    ws = _ws(tt_interface_workspace_size(rl, n, rr, Rl, Rr), workspace, x.device)
+    _check(lib.tt_interface_left(rl, n, rr, Rl, Rr, _dev(phiL_prev, "phiL_prev"), _dev(A, "A"),
+                                 _dev(x, "x"), _dev(out, "phiL_next"), ws.data_ptr(), ws.numel(),
+                                 _stream(stream)))
+    return out
+
+
+def tt_interface_right(phiR_next, A, x, out=None, workspace=None, stream=None):
+    """H6: phiR_prev (rl,Rl,rl) from phiR_next (rr,Rr,rr), A_k, x_k."""
+    rl, n, rr = x.shape
+    Rl, Rr = A.shape[0], A.shape[3]
+    if out is None:
+        out = torch.empty((rl, Rl, rl), dtype=x.dtype, device=x.device)
+    ws = _ws(tt_interface_workspace_size(rl, n, rr, Rl, Rr), workspace, x.device)
+    _check(lib.tt_interface_right(rl, n, rr, Rl, Rr, _dev(phiR_next, "phiR_next"), _dev(A, "A"),
+                                  _dev(x, "x"), _dev(out, "phiR_prev"), ws.data_ptr(), ws.numel(),
+                                  _stream(stream)))
+    return out
+
+
+class _Train:
+    """Host-side shape and pointer arrays of a TT train (marshalling only)."""
+
+    def __init__(self, x_cores: Sequence[torch.Tensor], A_cores: Sequence[torch.Tensor]):
+        self.d = len(x_cores)
+        if len(A_cores) != self.d:
+            raise ValueError("x_cores and A_cores must have the same length")
+        self.n = [int(c.shape[1]) for c in x_cores]
+        self.r = [int(c.shape[0]) for c in x_cores] + [int(x_cores[-1].shape[-1])]
+        self.R = [int(c.shape[0]) for c in A_cores] + [int(A_cores[-1].shape[3])]
+        self._n = (ctypes.c_int64 * self.d)(*self.n)
+        self._r = (ctypes.c_int64 * (self.d + 1))(*self.r)
+        self._R = (ctypes.c_int64 * (self.d + 1))(*self.R)
+        self._x = _ptrs(x_cores, "x_cores")
+        self._A = _ptrs(A_cores, "A_cores")
+
+
+def _ptrs(ts: Sequence[torch.Tensor], name: str):
+    return (ctypes.c_void_p * len(ts))(*[_dev(t, f"{name}[{i}]") for i, t in enumerate(ts)])
+
+
+def tt_sweep_workspace_size(tr: _Train) -> int:
+    return int(lib.tt_sweep_workspace_size(tr.d, tr._n, tr._r, tr._R))
+
+
+def tt_sweep_als_workspace_size(tr: _Train, nvec: int) -> int:
+    return int(lib.tt_sweep_als_workspace_size(tr.d, tr._n, tr._r, tr._R, nvec))
+
+
+def alloc_interfaces(x_cores, A_cores) -> List[torch.Tensor]:
+    tr = _Train(x_cores, A_cores)
+    dev = x_cores[0].device
+    return [torch.zeros((tr.r[k], tr.R[k], tr.r[k]), dtype=torch.float64, device=dev)
+            for k in range(tr.d + 1)]
+
+
+def tt_sweep_interfaces(x_cores, A_cores, phiL=None, phiR=None, directions=TT_SWEEP_BOTH,
+                        workspace=None, stream=None):
+    """H7: build phiL[0..d] and/or phiR[0..d] (lists of device tensors).  Returns (phiL, phiR)."""
+    tr = _Train(x_cores, A_cores)
+    if phiL is None and directions & TT_SWEEP_LEFT:
+        phiL = alloc_interfaces(x_cores, A_cores)
+    if phiR is None and directions & TT_SWEEP_RIGHT:
+        phiR = alloc_interfaces(x_cores, A_cores)
+    ws = _ws(tt_sweep_workspace_size(tr), workspace, x_cores[0].device)
+    pl = _ptrs(phiL, "phiL") if phiL is not None else None
+    pr = _ptrs(phiR, "phiR") if phiR is not None else None
+    _check(lib.tt_sweep_interfaces(tr.d, tr._n, tr._r, tr._R, tr._x, tr._A, pl, pr, directions,
+                                   ws.data_ptr(), ws.numel(), _stream(stream)))
+    return phiL, phiR
+
+
+def tt_sweep_als(x_cores, A_cores, X_blocks, Y_fwd=None, Y_bwd=None, phiL=None, phiR=None,
+                 workspace=None, stream=None):
+    """H7 with interleaved batched matvecs (workload W5).  Returns
+    (Y_fwd, Y_bwd, phiL, phiR)."""
+    tr = _Train(x_cores, A_cores)
+    nvec = int(X_blocks[0].shape[2])
+    if Y_fwd is None:
+        Y_fwd = [torch.empty_like(X) for X in X_blocks]
+    if phiL is None:
+        phiL = alloc_interfaces(x_cores, A_cores)
+    if phiR is None:
+        phiR = alloc_interfaces(x_cores, A_cores)
+    ws = _ws(tt_sweep_als_workspace_size(tr, nvec), workspace, x_cores[0].device)
+    _check(lib.tt_sweep_als(tr.d, tr._n, tr._r, tr._R, nvec, tr._x, tr._A,
+                            _ptrs(X_blocks, "X_blocks"), _ptrs(Y_fwd, "Y_fwd"),
+                            _ptrs(Y_bwd, "Y_bwd") if Y_bwd is not None else None,
+                            _ptrs(phiL, "phiL"), _ptrs(phiR, "phiR"), ws.data_ptr(), ws.numel(),
+                            _stream(stream)))
+    return Y_fwd, Y_bwd, phiL, phiR
+
+
+def tt_operator_apply(x_cores, A_cores, z_cores=None, stream=None):
+    """H8: unrounded TT-matrix x TT-vector product; returns z cores (r R, n_row, r' R')."""
+    d = len(x_cores)
+    n_row = [int(c.shape[1]) for c in A_cores]
+    n_col = [int(c.shape[2]) for c in A_cores]
+    r = [int(c.shape[0]) for c in x_cores] + [int(x_cores[-1].shape[2])]
+    R = [int(c.shape[0]) for c in A_cores] + [int(A_cores[-1].shape[3])]
+    if z_cores is None:
+        z_cores = [torch.empty((r[k] * R[k], n_row[k], r[k + 1] * R[k + 1]), dtype=torch.float64,
+                               device=x_cores[0].device) for k in range(d)]
+    a64 = lambda v: (ctypes.c_int64 * len(v))(*v)
+    _check(lib.tt_operator_apply(d, a64(n_row), a64(n_col), a64(r), a64(R),
+                                 _ptrs(x_cores, "x_cores"), _ptrs(A_cores, "A_cores"),
+                                 _ptrs(z_cores, "z_cores"), _stream(stream)))
+    return z_cores

@@ -1,0 +1,759 @@
+// tt_hotpath.cu — C-ABI (include/tt_hotpath.h) and stage plans of the TT hot path, sm_100a.
+//
+// Each ABI operation is a short sequence of kernels on the caller's stream:
+//   * a permutation of the operator core A_k into the (contraction x output) GEMM layout
+//     (a few KB; DESIGN.md §4 "P"),
+//   * three DMMA GEMM stages (tt_gemm.cuh) = the paper's "three matrix products"
+//     (§3.3), with the stage order chosen so that every operand is a plain
+//     2-D view and every intermediate is written directly in the next stage's layout,
+//   * a streaming kernel for the unrounded operator apply (H8).
+// Index letters: a = r_k (rl), b = r_{k+1} (rr), al = R_k (Rl), be = R_{k+1}
+// (Rr), N = mode size n, K = number of Krylov columns (nvec).
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/tt_hotpath.h"
+#include "tt_gemm.cuh"
+
+using tt::GemmParams;
+using tt::IndexMap;
+
+namespace {
+
+thread_local std::string g_msg;
+thread_local int64_t g_launches = 0;
+thread_local int64_t g_launches_last = 0;
+
+tt_status fail(tt_status s, const std::string& m) {
+  g_msg = m;
+  return s;
+}
+
+constexpr long long kMaxElems = (1LL << 62) / 8;
+
+// checked product of positive extents
+bool mulc(long long& acc, long long v) {
+  if (v <= 0) return false;
+  if (acc > kMaxElems / v) return false;
+  acc *= v;
+  return true;
+}
+
+long long prod(std::initializer_list<long long> xs, bool& ok) {
+  long long p = 1;
+  for (long long v : xs)
+    if (!mulc(p, v)) ok = false;
+  return ok ? p : 0;
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Carves 256-byte aligned sub-buffers out of the caller's workspace.
+struct Carver {
+  char* base;
+  size_t cap, off = 0;
+  bool ok = true;
+  double* take(long long elems) {
+    uintptr_t p = reinterpret_cast<uintptr_t>(base) + off;
+    uintptr_t q = (p + 255) & ~uintptr_t(255);
+    size_t need = (q - reinterpret_cast<uintptr_t>(base)) + size_t(elems) * sizeof(double);
+    if (need > cap) {
+      ok = false;
+      return nullptr;
+    }
+    off = need;
+    return reinterpret_cast<double*>(q);
+  }
+};
+
+// bytes of workspace for a list of buffers (each padded to 256 B, plus 256 B base slack)
+size_t ws_bytes(std::initializer_list<long long> elems) {
+  size_t s = 256;
+  for (long long e : elems) s += align_up(size_t(e) * sizeof(double), 256);
+  return s;
+}
+
+// ----------------------------------------------------------------------------------------
+// GEMM launch: tile configuration chosen from the stage's N extent
+// ----------------------------------------------------------------------------------------
+template <int BM, int BN, int BK, int WM, int WN, int ST, bool AK, bool BK_>
+cudaError_t launch_cfg(const GemmParams& p0, cudaStream_t s) {
+  using Cfg = tt::GemmCfg<BM, BN, BK, WM, WN, ST, AK, BK_>;
+  auto kern = tt::dmma_gemm_kernel<BM, BN, BK, WM, WN, ST, AK, BK_>;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] {
+    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)Cfg::kSmemBytes);
+  });
+  if (attr_err != cudaSuccess) return attr_err;
+  GemmParams p = p0;
+  const long long tm = (p.M + BM - 1) / BM;
+  p.tiles_n = (p.N + BN - 1) / BN;
+  const long long tiles = tm * p.tiles_n;
+  if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  kern<<<(unsigned)tiles, Cfg::kThreads, Cfg::kSmemBytes, s>>>(p);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+template <bool AK, bool BK_>
+cudaError_t launch_gemm_l(const GemmParams& p, cudaStream_t s) {
+  // Narrow-N configurations keep the whole N extent of the operator-core stage in one tile
+  // (N = n*R <= 160 in every config: 16, 36, 64, 100, 144); wide N uses 128x128 tiles.
+  if (p.N <= 16) return launch_cfg<128, 16, 16, 8, 1, 4, AK, BK_>(p, s);
+  if (p.N <= 40) return launch_cfg<128, 40, 16, 8, 1, 4, AK, BK_>(p, s);
+  if (p.N <= 64) return launch_cfg<128, 64, 16, 4, 2, 4, AK, BK_>(p, s);
+  if (p.N <= 104) return launch_cfg<128, 104, 16, 8, 1, 4, AK, BK_>(p, s);
+  if (p.N <= 144) return launch_cfg<128, 144, 16, 4, 2, 4, AK, BK_>(p, s);
+  return launch_cfg<128, 128, 16, 2, 4, 4, AK, BK_>(p, s);
+}
+
+cudaError_t launch_gemm(bool a_kc, bool b_kc, const GemmParams& p, cudaStream_t s) {
+  if (p.M <= 0 || p.N <= 0 || p.K <= 0) return cudaSuccess;
+  if (a_kc && b_kc) return launch_gemm_l<true, true>(p, s);
+  if (a_kc && !b_kc) return launch_gemm_l<true, false>(p, s);
+  if (!a_kc && b_kc) return launch_gemm_l<false, true>(p, s);
+  return launch_gemm_l<false, false>(p, s);
+}
+
+GemmParams gp(const double* A, long long lda, const double* B, long long ldb, double* C,
+              long long M, long long N, long long K, IndexMap rm, IndexMap cm) {
+  GemmParams p;
+  p.A = A;
+  p.B = B;
+  p.C = C;
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.lda = lda;
+  p.ldb = ldb;
+  p.rowmap = rm;
+  p.colmap = cm;
+  p.tiles_n = 1;
+  return p;
+}
+
+// ----------------------------------------------------------------------------------------
+// small kernels
+// ----------------------------------------------------------------------------------------
+// Ahat[(al, j), (i, be)] = A[al, i, j, be]   (left / matvec stage S2 operand)
+__global__ void perm_left_kernel(const double* __restrict__ A, double* __restrict__ Ah,
+                                 long long al_n, long long n, long long be_n) {
+  const long long total = al_n * n * n * be_n;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    long long r = e;
+    const long long be = r % be_n; r /= be_n;
+    const long long j = r % n; r /= n;
+    const long long i = r % n; r /= n;
+    const long long al = r;
+    Ah[(al * n + j) * (n * be_n) + i * be_n + be] = A[e];
+  }
+}
+
+// Atil[(j, be), (al, i)] = A[al, i, j, be]   (right interface stage S2'' operand)
+__global__ void perm_right_kernel(const double* __restrict__ A, double* __restrict__ At,
+                                  long long al_n, long long n, long long be_n) {
+  const long long total = al_n * n * n * be_n;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    long long r = e;
+    const long long be = r % be_n; r /= be_n;
+    const long long j = r % n; r /= n;
+    const long long i = r % n; r /= n;
+    const long long al = r;
+    At[(j * be_n + be) * (al_n * n) + al * n + i] = A[e];
+  }
+}
+
+__global__ void set_one_kernel(double* p) { *p = 1.0; }
+
+cudaError_t launch_perm(bool left, const double* A, double* out, long long al, long long n,
+                        long long be, cudaStream_t s) {
+  const long long total = al * n * n * be;
+  const int threads = 256;
+  long long blocks = (total + threads - 1) / threads;
+  if (blocks > 4096) blocks = 4096;
+  if (left)
+    perm_left_kernel<<<(unsigned)blocks, threads, 0, s>>>(A, out, al, n, be);
+  else
+    perm_right_kernel<<<(unsigned)blocks, threads, 0, s>>>(A, out, al, n, be);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_set_one(double* p, cudaStream_t s) {
+  set_one_kernel<<<1, 1, 0, s>>>(p);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+// H8: z[(a,al), i, (b,be)] = sum_j A[al,i,j,be] x[a,j,b].  One CTA per (a, al) pair; the
+// x[a,:,:] and A[al,:,:,:] slices are staged in shared memory; the output rows (one per i,
+// each rr*Rr contiguous doubles) are written with streaming (evict-first) stores.
+__global__ void __launch_bounds__(256) apply_kernel(const double* __restrict__ x,
+                                                    const double* __restrict__ A,
+                                                    double* __restrict__ z, int rl, int ni,
+                                                    int nj, int rr, int Rl, int Rr) {
+  extern __shared__ double sm[];
+  double* xs = sm;                       // [nj][rr]
+  double* As = sm + (size_t)nj * rr;     // [ni][nj][Rr]
+  const long long pair = blockIdx.x;     // a * Rl + al
+  const int a = (int)(pair / Rl), al = (int)(pair % Rl);
+  const int xn = nj * rr, an = ni * nj * Rr;
+  for (int e = threadIdx.x; e < xn; e += blockDim.x) xs[e] = x[(long long)a * xn + e];
+  for (int e = threadIdx.x; e < an; e += blockDim.x) As[e] = A[(long long)al * an + e];
+  __syncthreads();
+  const int L = rr * Rr;
+  const int step_b = blockDim.x / Rr, step_be = blockDim.x % Rr;
+  for (int i = 0; i < ni; ++i) {
+    double* zrow = z + (pair * ni + i) * (long long)L;
+    const double* Ai = As + (size_t)i * nj * Rr;
+    int b = threadIdx.x / Rr, be = threadIdx.x % Rr;
+    for (int e = threadIdx.x; e < L; e += blockDim.x) {
+      double s = 0.0;
+      for (int j = 0; j < nj; ++j) s = fma(Ai[j * Rr + be], xs[j * rr + b], s);
+      __stcs(zrow + e, s);
+      b += step_b;
+      be += step_be;
+      if (be >= Rr) {
+        be -= Rr;
+        ++b;
+      }
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------------------
+// stage plans
+// ----------------------------------------------------------------------------------------
+struct Dims {
+  long long a, n, b, al, be;
+};
+
+bool dims_valid(const Dims& d) { return d.a > 0 && d.n > 0 && d.b > 0 && d.al > 0 && d.be > 0; }
+
+// element counts of the matvec workspace buffers (K columns)
+bool matvec_ws_elems(const Dims& d, long long K, long long& t1, long long& t2, long long& ah) {
+  bool ok = true;
+  t1 = prod({d.a, d.al, d.n, K, d.b}, ok);
+  t2 = prod({d.a, d.n, K, d.be, d.b}, ok);
+  ah = prod({d.al, d.n, d.n, d.be}, ok);
+  return ok;
+}
+
+// Local matvec (K columns, Block-TT layout) — stages S1, S2^T, S3.
+cudaError_t enqueue_matvec(const Dims& d, long long K, const double* phiL, const double* A,
+                           const double* phiR, const double* X, double* Y, double* T1,
+                           double* T2, double* Ah, cudaStream_t s) {
+  const long long a = d.a, b = d.b, al = d.al, be = d.be, N = d.n;
+  cudaError_t e;
+  if ((e = launch_perm(true, A, Ah, al, N, be, s)) != cudaSuccess) return e;
+  // S1: T1(al, j, a', m, b) = phiL[(a' al), a] . X[a, (j m b)]
+  e = launch_gemm(true, false,
+                  gp(phiL, a, X, N * K * b, T1, a * al, N * K * b, a,
+                     tt::map2(al, N * a * K * b, K * b), tt::map2(K * b, 1, a * K * b)),
+                  s);
+  if (e != cudaSuccess) return e;
+  // S2^T: T2(a', m, i, be, b) = T1^T[(a' m b), (al j)] . Ahat[(al j), (i be)]
+  e = launch_gemm(false, false,
+                  gp(T1, a * K * b, Ah, N * be, T2, a * K * b, N * be, al * N,
+                     tt::map2(b, 1, N * be * b), tt::map_plain(b)),
+                  s);
+  if (e != cudaSuccess) return e;
+  // S3: Y(a', i, m, b') = T2[(a' m i), (be b)] . phiR[b', (be b)]^T
+  e = launch_gemm(true, true,
+                  gp(T2, be * b, phiR, be * b, Y, a * K * N, b, be * b,
+                     tt::map3(N, K, K * b, b, N * K * b), tt::map_plain(1)),
+                  s);
+  return e;
+}
+
+bool iface_ws_elems(const Dims& d, long long& t1, long long& t2, long long& ah) {
+  bool ok = true;
+  t1 = prod({d.a, d.al, d.n, d.b}, ok);
+  long long t1r = prod({d.a, d.n, d.b, d.be}, ok);
+  if (t1r > t1) t1 = t1r;
+  t2 = prod({d.a, d.n, d.be, d.b}, ok);
+  long long t2r = prod({d.a, d.al, d.n, d.b}, ok);
+  if (t2r > t2) t2 = t2r;
+  ah = prod({d.al, d.n, d.n, d.be}, ok);
+  return ok;
+}
+
+// Left interface: S1, S2^T (K = 1), S3': phiL_next[b', (be b)] = x^T[b', (a' i)] . T2[(a' i), (be b)]
+cudaError_t enqueue_left(const Dims& d, const double* phiL, const double* A, const double* x,
+                         double* out, double* T1, double* T2, double* Ah, cudaStream_t s) {
+  const long long a = d.a, b = d.b, al = d.al, be = d.be, N = d.n;
+  cudaError_t e;
+  if ((e = launch_perm(true, A, Ah, al, N, be, s)) != cudaSuccess) return e;
+  e = launch_gemm(true, false,
+                  gp(phiL, a, x, N * b, T1, a * al, N * b, a, tt::map2(al, N * a * b, b),
+                     tt::map2(b, 1, a * b)),
+                  s);
+  if (e != cudaSuccess) return e;
+  e = launch_gemm(false, false,
+                  gp(T1, a * b, Ah, N * be, T2, a * b, N * be, al * N, tt::map2(b, 1, N * be * b),
+                     tt::map_plain(b)),
+                  s);
+  if (e != cudaSuccess) return e;
+  return launch_gemm(false, false,
+                     gp(x, b, T2, be * b, out, b, be * b, a * N, tt::map_plain(be * b),
+                        tt::map_plain(1)),
+                     s);
+}
+
+// Right interface: S1'': T1(j, be, a, b') = x[(a j), b] . phiR[(b' be), b]^T
+//                  S2'': T2(i, b', al, a) = T1^T[(a b'), (j be)] . Atil[(j be), (al i)]
+//                  S3'': phiR_prev[a', (al a)] = x[a', (i b')] . T2[(i b'), (al a)]
+cudaError_t enqueue_right(const Dims& d, const double* phiR, const double* A, const double* x,
+                          double* out, double* T1, double* T2, double* At, cudaStream_t s) {
+  const long long a = d.a, b = d.b, al = d.al, be = d.be, N = d.n;
+  cudaError_t e;
+  if ((e = launch_perm(false, A, At, al, N, be, s)) != cudaSuccess) return e;
+  e = launch_gemm(true, true,
+                  gp(x, b, phiR, b, T1, a * N, b * be, b, tt::map2(N, be * a * b, b),
+                     tt::map2(be, a * b, 1)),
+                  s);
+  if (e != cudaSuccess) return e;
+  e = launch_gemm(false, false,
+                  gp(T1, a * b, At, al * N, T2, a * b, al * N, N * be, tt::map2(b, al * a, 1),
+                     tt::map2(N, b * al * a, a)),
+                  s);
+  if (e != cudaSuccess) return e;
+  return launch_gemm(true, false,
+                     gp(x, N * b, T2, al * a, out, a, al * a, N * b, tt::map_plain(al * a),
+                        tt::map_plain(1)),
+                     s);
+}
+
+tt_status cuda_fail(cudaError_t e, const char* where) {
+  return fail(TT_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+struct CallScope {
+  CallScope() {
+    g_msg.clear();
+    g_launches = 0;
+  }
+  ~CallScope() { g_launches_last = g_launches; }
+};
+
+tt_status check_dims(const Dims& d) {
+  if (!dims_valid(d)) return fail(TT_ERR_INVALID_ARGUMENT, "extents must be positive");
+  bool ok = true;
+  prod({d.a, d.al, d.n, d.b}, ok);
+  prod({d.a, d.n, d.be, d.b}, ok);
+  prod({d.al, d.n, d.n, d.be}, ok);
+  prod({d.b, d.be, d.b}, ok);
+  prod({d.a, d.al, d.a}, ok);
+  if (!ok) return fail(TT_ERR_OVERFLOW, "extent product overflows");
+  return TT_OK;
+}
+
+bool same(const void* p, const void* q) { return p != nullptr && p == q; }
+
+}  // namespace
+
+// ========================================================================================
+// C ABI
+// ========================================================================================
+extern "C" {
+
+const char* tt_status_string(tt_status s) {
+  switch (s) {
+    case TT_OK: return "TT_OK";
+    case TT_ERR_INVALID_ARGUMENT: return "TT_ERR_INVALID_ARGUMENT";
+    case TT_ERR_NULL_POINTER: return "TT_ERR_NULL_POINTER";
+    case TT_ERR_ALIASING: return "TT_ERR_ALIASING";
+    case TT_ERR_WORKSPACE: return "TT_ERR_WORKSPACE";
+    case TT_ERR_OVERFLOW: return "TT_ERR_OVERFLOW";
+    case TT_ERR_CUDA: return "TT_ERR_CUDA";
+  }
+  return "TT_UNKNOWN_STATUS";
+}
+
+const char* tt_last_error_message(void) { return g_msg.c_str(); }
+const char* tt_version(void) { return "tt_hotpath 0.1 (sm_100a, FP64 DMMA)"; }
+int64_t tt_last_launch_count(void) { return g_launches_last; }
+
+size_t tt_local_matvec_workspace_size(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t Rr,
+                                      int64_t nvec) {
+  Dims d{rl, n, rr, Rl, Rr};
+  long long t1, t2, ah;
+  if (!dims_valid(d) || nvec <= 0 || !matvec_ws_elems(d, nvec, t1, t2, ah)) return 0;
+  return ws_bytes({t1, t2, ah});
+}
+
+tt_status tt_local_matvec_batched(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t Rr,
+                                  int64_t nvec, const double* phiL, const double* A,
+                                  const double* phiR, const double* X, double* Y,
+                                  void* workspace, size_t workspace_bytes, void* stream) {
+  CallScope scope;
+  Dims d{rl, n, rr, Rl, Rr};
+  tt_status st = check_dims(d);
+  if (st != TT_OK) return st;
+  if (nvec <= 0) return fail(TT_ERR_INVALID_ARGUMENT, "nvec must be positive");
+  if (!phiL || !A || !phiR || !X || !Y) return fail(TT_ERR_NULL_POINTER, "NULL tensor pointer");
+  if (same(Y, phiL) || same(Y, A) || same(Y, phiR) || same(Y, X))
+    return fail(TT_ERR_ALIASING, "output Y aliases an input");
+  long long t1, t2, ah;
+  if (!matvec_ws_elems(d, nvec, t1, t2, ah)) return fail(TT_ERR_OVERFLOW, "workspace overflow");
+  const size_t need = ws_bytes({t1, t2, ah});
+  if (!workspace || workspace_bytes < need)
+    return fail(TT_ERR_WORKSPACE, "workspace NULL or smaller than " + std::to_string(need) + " bytes");
+  if (same(workspace, Y) || same(workspace, X) || same(workspace, phiL) || same(workspace, phiR) ||
+      same(workspace, A))
+    return fail(TT_ERR_ALIASING, "workspace aliases a tensor");
+  Carver c{static_cast<char*>(workspace), workspace_bytes};
+  double* T1 = c.take(t1);
+  double* T2 = c.take(t2);
+  double* Ah = c.take(ah);
+  if (!c.ok) return fail(TT_ERR_WORKSPACE, "workspace too small after alignment");
+  cudaError_t e = enqueue_matvec(d, nvec, phiL, A, phiR, X, Y, T1, T2, Ah,
+                                 static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "tt_local_matvec_batched");
+  return TT_OK;
+}
+
+tt_status tt_local_matvec(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t Rr,
+                          const double* phiL, const double* A, const double* phiR,
+                          const double* x, double* y, void* workspace, size_t workspace_bytes,
+                          void* stream) {
+  return tt_local_matvec_batched(rl, n, rr, Rl, Rr, 1, phiL, A, phiR, x, y, workspace,
+                                 workspace_bytes, stream);
+}
+
+size_t tt_interface_workspace_size(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t Rr) {
+  Dims d{rl, n, rr, Rl, Rr};
+  long long t1, t2, ah;
+  if (!dims_valid(d) || !iface_ws_elems(d, t1, t2, ah)) return 0;
+  return ws_bytes({t1, t2, ah});
+}
+
+static tt_status iface_common(bool left, int64_t rl, int64_t n, int64_t rr, int64_t Rl,
+                              int64_t Rr, const double* phi_in, const double* A,
+                              const double* x, double* phi_out, void* workspace,
+                              size_t workspace_bytes, void* stream) {
+  Dims d{rl, n, rr, Rl, Rr};
+  tt_status st = check_dims(d);
+  if (st != TT_OK) return st;
+  if (!phi_in || !A || !x || !phi_out) return fail(TT_ERR_NULL_POINTER, "NULL tensor pointer");
+  if (same(phi_out, phi_in) || same(phi_out, A) || same(phi_out, x))
+    return fail(TT_ERR_ALIASING, "output interface aliases an input");
+  long long t1, t2, ah;
+  if (!iface_ws_elems(d, t1, t2, ah)) return fail(TT_ERR_OVERFLOW, "workspace overflow");
+  const size_t need = ws_bytes({t1, t2, ah});
+  if (!workspace || workspace_bytes < need)
+    return fail(TT_ERR_WORKSPACE, "workspace NULL or smaller than " + std::to_string(need) + " bytes");
+  if (same(workspace, phi_out) || same(workspace, phi_in) || same(workspace, x) ||
+      same(workspace, A))
+    return fail(TT_ERR_ALIASING, "workspace aliases a tensor");
+  Carver c{static_cast<char*>(workspace), workspace_bytes};
+  double* T1 = c.take(t1);
+  double* T2 = c.take(t2);
+  double* Ah = c.take(ah);
+  if (!c.ok) return fail(TT_ERR_WORKSPACE, "workspace too small after alignment");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = left ? enqueue_left(d, phi_in, A, x, phi_out, T1, T2, Ah, s)
+                       : enqueue_right(d, phi_in, A, x, phi_out, T1, T2, Ah, s);
+  if (e != cudaSuccess) return cuda_fail(e, left ? "tt_interface_left" : "tt_interface_right");
+  return TT_OK;
+}
+
+tt_status tt_interface_left(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t Rr,
+                            const double* phiL_prev, const double* A, const double* x,
+                            double* phiL_next, void* workspace, size_t workspace_bytes,
+                            void* stream) {
+  CallScope scope;
+  return iface_common(true, rl, n, rr, Rl, Rr, phiL_prev, A, x, phiL_next, workspace,
+                      workspace_bytes, stream);
+}
+
+tt_status tt_interface_right(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t Rr,
+                             const double* phiR_next, const double* A, const double* x,
+                             double* phiR_prev, void* workspace, size_t workspace_bytes,
+                             void* stream) {
+  CallScope scope;
+  return iface_common(false, rl, n, rr, Rl, Rr, phiR_next, A, x, phiR_prev, workspace,
+                      workspace_bytes, stream);
+}
+
+// ---- sweeps ------------------------------------------------------------------------------
+static tt_status check_train(int64_t d, const int64_t* n, const int64_t* r, const int64_t* R) {
+  if (d <= 0) return fail(TT_ERR_INVALID_ARGUMENT, "d must be >= 1");
+  if (!n || !r || !R) return fail(TT_ERR_NULL_POINTER, "NULL shape array");
+  if (r[0] != 1 || r[d] != 1) return fail(TT_ERR_INVALID_ARGUMENT, "r_1 and r_{d+1} must be 1");
+  if (R[0] != 1 || R[d] != 1) return fail(TT_ERR_INVALID_ARGUMENT, "R_1 and R_{d+1} must be 1");
+  for (int64_t k = 0; k < d; ++k) {
+    Dims dk{r[k], n[k], r[k + 1], R[k], R[k + 1]};
+    tt_status st = check_dims(dk);
+    if (st != TT_OK) return fail(st, "core " + std::to_string(k) + ": " + g_msg);
+  }
+  return TT_OK;
+}
+
+static size_t sweep_ws(int64_t d, const int64_t* n, const int64_t* r, const int64_t* R,
+                       int64_t nvec) {
+  size_t best = 0;
+  for (int64_t k = 0; k < d; ++k) {
+    Dims dk{r[k], n[k], r[k + 1], R[k], R[k + 1]};
+    long long t1, t2, ah;
+    if (!iface_ws_elems(dk, t1, t2, ah)) return 0;
+    size_t s = ws_bytes({t1, t2, ah});
+    if (s > best) best = s;
+    if (nvec > 0) {
+      if (!matvec_ws_elems(dk, nvec, t1, t2, ah)) return 0;
+      s = ws_bytes({t1, t2, ah});
+      if (s > best) best = s;
+    }
+  }
+  return best;
+}
+
+size_t tt_sweep_workspace_size(int64_t d, const int64_t* n, const int64_t* r, const int64_t* R) {
+  if (d <= 0 || !n || !r || !R) return 0;
+  return sweep_ws(d, n, r, R, 0);
+}
+
+size_t tt_sweep_als_workspace_size(int64_t d, const int64_t* n, const int64_t* r,
+                                   const int64_t* R, int64_t nvec) {
+  if (d <= 0 || !n || !r || !R || nvec <= 0) return 0;
+  return sweep_ws(d, n, r, R, nvec);
+}
+
+// carve the workspace for core k (interface or matvec) and enqueue
+static cudaError_t sweep_left_step(int64_t k, const int64_t* n, const int64_t* r,
+                                   const int64_t* R, const double* const* xc,
+                                   const double* const* Ac, double* const* phiL, void* ws,
+                                   size_t wsb, cudaStream_t s) {
+  Dims dk{r[k], n[k], r[k + 1], R[k], R[k + 1]};
+  long long t1, t2, ah;
+  iface_ws_elems(dk, t1, t2, ah);
+  Carver c{static_cast<char*>(ws), wsb};
+  double* T1 = c.take(t1);
+  double* T2 = c.take(t2);
+  double* Ah = c.take(ah);
+  if (!c.ok) return cudaErrorInvalidValue;
+  return enqueue_left(dk, phiL[k], Ac[k], xc[k], phiL[k + 1], T1, T2, Ah, s);
+}
+
+static cudaError_t sweep_right_step(int64_t k, const int64_t* n, const int64_t* r,
+                                    const int64_t* R, const double* const* xc,
+                                    const double* const* Ac, double* const* phiR, void* ws,
+                                    size_t wsb, cudaStream_t s) {
+  Dims dk{r[k], n[k], r[k + 1], R[k], R[k + 1]};
+  long long t1, t2, ah;
+  iface_ws_elems(dk, t1, t2, ah);
+  Carver c{static_cast<char*>(ws), wsb};
+  double* T1 = c.take(t1);
+  double* T2 = c.take(t2);
+  double* Ah = c.take(ah);
+  if (!c.ok) return cudaErrorInvalidValue;
+  return enqueue_right(dk, phiR[k + 1], Ac[k], xc[k], phiR[k], T1, T2, Ah, s);
+}
+
+static cudaError_t sweep_matvec_step(int64_t k, const int64_t* n, const int64_t* r,
+                                     const int64_t* R, int64_t nvec, const double* const* Ac,
+                                     const double* const* Xb, double* const* Yb,
+                                     double* const* phiL, double* const* phiR, void* ws,
+                                     size_t wsb, cudaStream_t s) {
+  Dims dk{r[k], n[k], r[k + 1], R[k], R[k + 1]};
+  long long t1, t2, ah;
+  matvec_ws_elems(dk, nvec, t1, t2, ah);
+  Carver c{static_cast<char*>(ws), wsb};
+  double* T1 = c.take(t1);
+  double* T2 = c.take(t2);
+  double* Ah = c.take(ah);
+  if (!c.ok) return cudaErrorInvalidValue;
+  return enqueue_matvec(dk, nvec, phiL[k], Ac[k], phiR[k + 1], Xb[k], Yb[k], T1, T2, Ah, s);
+}
+
+static tt_status check_ptrs(int64_t d, const void* const* arr, int64_t count, const char* what) {
+  if (!arr) return fail(TT_ERR_NULL_POINTER, std::string("NULL array ") + what);
+  for (int64_t k = 0; k < count; ++k)
+    if (!arr[k]) return fail(TT_ERR_NULL_POINTER, std::string("NULL entry in ") + what);
+  (void)d;
+  return TT_OK;
+}
+
+// outputs (phi arrays, Y blocks) must not alias inputs (cores, blocks) nor each other
+static tt_status check_outputs(int64_t d, const double* const* xc, const double* const* Ac,
+                               const double* const* Xb,
+                               std::initializer_list<std::pair<double* const*, int64_t>> outs,
+                               void* ws) {
+  std::vector<const void*> ins;
+  for (int64_t k = 0; k < d; ++k) {
+    ins.push_back(xc[k]);
+    ins.push_back(Ac[k]);
+    if (Xb) ins.push_back(Xb[k]);
+  }
+  std::vector<const void*> os;
+  for (auto& pr : outs)
+    if (pr.first)
+      for (int64_t k = 0; k < pr.second; ++k) os.push_back(pr.first[k]);
+  for (size_t i = 0; i < os.size(); ++i) {
+    for (const void* q : ins)
+      if (os[i] == q) return fail(TT_ERR_ALIASING, "an output aliases an input core");
+    for (size_t j = i + 1; j < os.size(); ++j)
+      if (os[i] == os[j]) return fail(TT_ERR_ALIASING, "two outputs alias");
+    if (ws && os[i] == ws) return fail(TT_ERR_ALIASING, "an output aliases the workspace");
+  }
+  return TT_OK;
+}
+
+tt_status tt_sweep_interfaces(int64_t d, const int64_t* n, const int64_t* r, const int64_t* R,
+                              const double* const* x_cores, const double* const* A_cores,
+                              double* const* phiL, double* const* phiR, int directions,
+                              void* workspace, size_t workspace_bytes, void* stream) {
+  CallScope scope;
+  tt_status st = check_train(d, n, r, R);
+  if (st != TT_OK) return st;
+  if (directions < 1 || directions > 3) return fail(TT_ERR_INVALID_ARGUMENT, "bad directions");
+  if ((st = check_ptrs(d, (const void* const*)x_cores, d, "x_cores")) != TT_OK) return st;
+  if ((st = check_ptrs(d, (const void* const*)A_cores, d, "A_cores")) != TT_OK) return st;
+  const bool doL = (directions & TT_SWEEP_LEFT) && phiL;
+  const bool doR = (directions & TT_SWEEP_RIGHT) && phiR;
+  if (doL && (st = check_ptrs(d, (const void* const*)phiL, d + 1, "phiL")) != TT_OK) return st;
+  if (doR && (st = check_ptrs(d, (const void* const*)phiR, d + 1, "phiR")) != TT_OK) return st;
+  if ((st = check_outputs(d, x_cores, A_cores, nullptr,
+                          {{doL ? phiL : nullptr, d + 1}, {doR ? phiR : nullptr, d + 1}},
+                          workspace)) != TT_OK)
+    return st;
+  const size_t need = sweep_ws(d, n, r, R, 0);
+  if (need == 0) return fail(TT_ERR_OVERFLOW, "workspace overflow");
+  if (!workspace || workspace_bytes < need)
+    return fail(TT_ERR_WORKSPACE, "workspace NULL or smaller than " + std::to_string(need) + " bytes");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  if (doL) {
+    if ((e = launch_set_one(phiL[0], s)) != cudaSuccess) return cuda_fail(e, "sweep");
+    for (int64_t k = 0; k < d; ++k)
+      if ((e = sweep_left_step(k, n, r, R, x_cores, A_cores, phiL, workspace, workspace_bytes, s)) !=
+          cudaSuccess)
+        return cuda_fail(e, "sweep left");
+  }
+  if (doR) {
+    if ((e = launch_set_one(phiR[d], s)) != cudaSuccess) return cuda_fail(e, "sweep");
+    for (int64_t k = d - 1; k >= 0; --k)
+      if ((e = sweep_right_step(k, n, r, R, x_cores, A_cores, phiR, workspace, workspace_bytes,
+                                s)) != cudaSuccess)
+        return cuda_fail(e, "sweep right");
+  }
+  return TT_OK;
+}
+
+tt_status tt_sweep_als(int64_t d, const int64_t* n, const int64_t* r, const int64_t* R,
+                       int64_t nvec, const double* const* x_cores,
+                       const double* const* A_cores, const double* const* X_blocks,
+                       double* const* Y_fwd, double* const* Y_bwd, double* const* phiL,
+                       double* const* phiR, void* workspace, size_t workspace_bytes,
+                       void* stream) {
+  CallScope scope;
+  tt_status st = check_train(d, n, r, R);
+  if (st != TT_OK) return st;
+  if (nvec <= 0) return fail(TT_ERR_INVALID_ARGUMENT, "nvec must be positive");
+  if ((st = check_ptrs(d, (const void* const*)x_cores, d, "x_cores")) != TT_OK) return st;
+  if ((st = check_ptrs(d, (const void* const*)A_cores, d, "A_cores")) != TT_OK) return st;
+  if ((st = check_ptrs(d, (const void* const*)X_blocks, d, "X_blocks")) != TT_OK) return st;
+  if ((st = check_ptrs(d, (const void* const*)Y_fwd, d, "Y_fwd")) != TT_OK) return st;
+  if (Y_bwd && (st = check_ptrs(d, (const void* const*)Y_bwd, d, "Y_bwd")) != TT_OK) return st;
+  if ((st = check_ptrs(d, (const void* const*)phiL, d + 1, "phiL")) != TT_OK) return st;
+  if ((st = check_ptrs(d, (const void* const*)phiR, d + 1, "phiR")) != TT_OK) return st;
+  if ((st = check_outputs(d, x_cores, A_cores, X_blocks,
+                          {{Y_fwd, d}, {Y_bwd, d}, {phiL, d + 1}, {phiR, d + 1}}, workspace)) !=
+      TT_OK)
+    return st;
+  const size_t need = sweep_ws(d, n, r, R, nvec);
+  if (need == 0) return fail(TT_ERR_OVERFLOW, "workspace overflow");
+  if (!workspace || workspace_bytes < need)
+    return fail(TT_ERR_WORKSPACE, "workspace NULL or smaller than " + std::to_string(need) + " bytes");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  double* const* Yb = Y_bwd ? Y_bwd : Y_fwd;
+  if ((e = launch_set_one(phiL[0], s)) != cudaSuccess) return cuda_fail(e, "als");
+  if ((e = launch_set_one(phiR[d], s)) != cudaSuccess) return cuda_fail(e, "als");
+  for (int64_t k = d - 1; k >= 1; --k)
+    if ((e = sweep_right_step(k, n, r, R, x_cores, A_cores, phiR, workspace, workspace_bytes, s)) !=
+        cudaSuccess)
+      return cuda_fail(e, "als initial right");
+  for (int64_t k = 0; k < d; ++k) {
+    if ((e = sweep_matvec_step(k, n, r, R, nvec, A_cores, X_blocks, Y_fwd, phiL, phiR, workspace,
+                               workspace_bytes, s)) != cudaSuccess)
+      return cuda_fail(e, "als matvec L->R");
+    if (k < d - 1 &&
+        (e = sweep_left_step(k, n, r, R, x_cores, A_cores, phiL, workspace, workspace_bytes, s)) !=
+            cudaSuccess)
+      return cuda_fail(e, "als left");
+  }
+  for (int64_t k = d - 1; k >= 0; --k) {
+    if ((e = sweep_matvec_step(k, n, r, R, nvec, A_cores, X_blocks, Yb, phiL, phiR, workspace,
+                               workspace_bytes, s)) != cudaSuccess)
+      return cuda_fail(e, "als matvec R->L");
+    if (k > 0 &&
+        (e = sweep_right_step(k, n, r, R, x_cores, A_cores, phiR, workspace, workspace_bytes, s)) !=
+            cudaSuccess)
+      return cuda_fail(e, "als right");
+  }
+  return TT_OK;
+}
+
+// ---- H8 ----------------------------------------------------------------------------------
+tt_status tt_operator_apply(int64_t d, const int64_t* n_row, const int64_t* n_col,
+                            const int64_t* r, const int64_t* R, const double* const* x_cores,
+                            const double* const* A_cores, double* const* z_cores, void* stream) {
+  CallScope scope;
+  if (d <= 0) return fail(TT_ERR_INVALID_ARGUMENT, "d must be >= 1");
+  if (!n_row || !n_col || !r || !R) return fail(TT_ERR_NULL_POINTER, "NULL shape array");
+  if (r[0] != 1 || r[d] != 1) return fail(TT_ERR_INVALID_ARGUMENT, "r_1 and r_{d+1} must be 1");
+  if (R[0] != 1 || R[d] != 1) return fail(TT_ERR_INVALID_ARGUMENT, "R_1 and R_{d+1} must be 1");
+  tt_status st;
+  if ((st = check_ptrs(d, (const void* const*)x_cores, d, "x_cores")) != TT_OK) return st;
+  if ((st = check_ptrs(d, (const void* const*)A_cores, d, "A_cores")) != TT_OK) return st;
+  if ((st = check_ptrs(d, (const void* const*)z_cores, d, "z_cores")) != TT_OK) return st;
+  if ((st = check_outputs(d, x_cores, A_cores, nullptr, {{z_cores, d}}, nullptr)) != TT_OK)
+    return st;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int smem_optin = 0;
+  cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  for (int64_t k = 0; k < d; ++k) {
+    if (n_row[k] <= 0 || n_col[k] <= 0 || r[k] <= 0 || R[k] <= 0)
+      return fail(TT_ERR_INVALID_ARGUMENT, "extents must be positive");
+    bool ok = true;
+    prod({r[k], R[k], n_row[k], r[k + 1], R[k + 1]}, ok);
+    prod({R[k], n_row[k], n_col[k], R[k + 1]}, ok);
+    prod({r[k], n_col[k], r[k + 1]}, ok);
+    if (!ok) return fail(TT_ERR_OVERFLOW, "extent product overflows");
+    const long long smem = 8LL * (n_col[k] * r[k + 1] + n_row[k] * n_col[k] * R[k + 1]);
+    if (smem > smem_optin || r[k + 1] * R[k + 1] > 0x7fffffffLL || r[k] * R[k] > 0x7fffffffLL)
+      return fail(TT_ERR_INVALID_ARGUMENT, "core too large for the apply kernel's staging");
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] {
+    attr_err = cudaFuncSetAttribute(apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    smem_optin);
+  });
+  if (attr_err != cudaSuccess) return cuda_fail(attr_err, "tt_operator_apply attr");
+  for (int64_t k = 0; k < d; ++k) {
+    const long long smem = 8LL * (n_col[k] * r[k + 1] + n_row[k] * n_col[k] * R[k + 1]);
+    const long long blocks = r[k] * R[k];
+    apply_kernel<<<(unsigned)blocks, 256, (size_t)smem, s>>>(
+        x_cores[k], A_cores[k], z_cores[k], (int)r[k], (int)n_row[k], (int)n_col[k],
+        (int)r[k + 1], (int)R[k], (int)R[k + 1]);
+    ++g_launches;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "tt_operator_apply");
+  }
+  return TT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,242 @@
+"""GPU parity: the CUDA path through the C-ABI vs the CPU oracle on the same seeded inputs.
+
+Bar (BASELINE.json north_star, DESIGN.md §3 A8): relative Frobenius error <= 1e-11 per
+output array (each Phi_k, each y_k / Y_k column block, each z_k).  Configs 1-4 are checked
+in full; config 5 (full size, the launch configuration bench.py times: tt_sweep_als with
+K = 32) on sampled Krylov columns of every core plus every interface, and sampled row slices
+of the operator apply.
+"""
+import concurrent.futures as cf
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-11
+
+
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+@pytest.fixture(scope="module")
+def tt():
+    _need_gpu()
+    import paper_2509_11890_b200 as m
+    return m
+
+
+def g(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def h(t):
+    return t.detach().cpu().numpy()
+
+
+def rel(a, b):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    nb = np.linalg.norm(b)
+    if nb == 0:
+        return float(np.linalg.norm(a))
+    return float(np.linalg.norm(a - b) / nb)
+
+
+def test_smoke():
+    _need_gpu()
+    import __graft_entry__
+    __graft_entry__.smoke()
+
+
+# ----------------------------------------------------------------------------------------
+# configs 1-4: full W34 workload (sweep both directions + one matvec per core) + apply
+# ----------------------------------------------------------------------------------------
+@pytest.mark.parametrize("idx", [1, 2, 3, 4])
+def test_config_w34_parity(tt, idx):
+    import oracle
+    import ttgen
+    inp = ttgen.make_inputs(idx)
+    d = inp.cfg.d
+    xs, As = [g(c) for c in inp.x], [g(c) for c in inp.A]
+    phiL, phiR = tt.tt_sweep_interfaces(xs, As)
+    ys = [tt.tt_local_matvec(phiL[k], As[k], phiR[k + 1], xs[k]) for k in range(d)]
+    torch.cuda.synchronize()
+    oL, oR = oracle.sweep_interfaces(inp.x, inp.A)
+    worst = 0.0
+    for k in range(d + 1):
+        worst = max(worst, rel(h(phiL[k]), oL[k]), rel(h(phiR[k]), oR[k]))
+    for k in range(d):
+        oy = oracle.local_matvec(oL[k], inp.A[k], oR[k + 1], inp.x[k])
+        worst = max(worst, rel(h(ys[k]), oy))
+    assert worst <= TOL, worst
+    # energy closure on the GPU side: phiL[d] == phiR[0] == <x_k, y_k>
+    e = h(phiL[d]).item()
+    assert abs(h(phiR[0]).item() - e) <= 1e-12 * abs(e)
+
+
+@pytest.mark.parametrize("idx", [1, 2, 3, 4])
+def test_config_apply_parity(tt, idx):
+    import oracle
+    import ttgen
+    inp = ttgen.make_inputs(idx)
+    zs = tt.tt_operator_apply([g(c) for c in inp.x], [g(c) for c in inp.A])
+    torch.cuda.synchronize()
+    for k in range(inp.cfg.d):
+        oz = oracle.apply_core(inp.x[k], inp.A[k])
+        gz = h(zs[k])
+        zs[k] = None
+        assert gz.shape == oz.shape
+        assert rel(gz, oz) <= TOL, k
+
+
+# ----------------------------------------------------------------------------------------
+# ragged shapes spanning several tiles in every GEMM stage
+# ----------------------------------------------------------------------------------------
+RAGGED = [
+    # rl, n, rr, Rl, Rr, nvec
+    (1, 4, 1, 1, 1, 1),
+    (3, 4, 5, 2, 3, 2),
+    (37, 4, 53, 7, 11, 5),
+    (150, 4, 140, 9, 17, 3),
+    (129, 3, 131, 5, 6, 2),        # odd mode size
+    (64, 4, 200, 30, 41, 1),       # N*Rr = 164 > 160 -> wide-N tiles in S2
+    (257, 2, 33, 3, 2, 4),
+]
+
+
+@pytest.mark.parametrize("shape", RAGGED)
+def test_ragged_batched_matvec(tt, shape):
+    import oracle
+    rl, n, rr, Rl, Rr, nvec = shape
+    rng = np.random.default_rng(sum(shape))
+    phiL = rng.standard_normal((rl, Rl, rl))
+    A = rng.standard_normal((Rl, n, n, Rr))
+    phiR = rng.standard_normal((rr, Rr, rr))
+    X = rng.standard_normal((rl, n, nvec, rr))
+    Y = tt.tt_local_matvec_batched(g(phiL), g(A), g(phiR), g(X))
+    ref = oracle.local_matvec_batched(phiL, A, phiR, X)
+    for m in range(nvec):
+        assert rel(h(Y)[:, :, m, :], ref[:, :, m, :]) <= TOL
+    # single-vector entry point == column of the batched one
+    y0 = tt.tt_local_matvec(g(phiL), g(A), g(phiR), g(np.ascontiguousarray(X[:, :, 0, :])))
+    assert rel(h(y0), ref[:, :, 0, :]) <= TOL
+
+
+@pytest.mark.parametrize("shape", RAGGED)
+def test_ragged_interfaces(tt, shape):
+    import oracle
+    rl, n, rr, Rl, Rr, _ = shape
+    rng = np.random.default_rng(sum(shape) + 1)
+    A = rng.standard_normal((Rl, n, n, Rr))
+    x = rng.standard_normal((rl, n, rr))
+    pl = rng.standard_normal((rl, Rl, rl))
+    pr = rng.standard_normal((rr, Rr, rr))
+    outL = tt.tt_interface_left(g(pl), g(A), g(x))
+    outR = tt.tt_interface_right(g(pr), g(A), g(x))
+    assert rel(h(outL), oracle.interface_left(pl, A, x)) <= TOL
+    assert rel(h(outR), oracle.interface_right(pr, A, x)) <= TOL
+
+
+def test_identity_operator_exact(tt):
+    """Identity operator and identity interfaces: every product is by 0 or 1, so y == x
+    exactly."""
+    rng = np.random.default_rng(9)
+    for rl, n, rr, nvec in [(1, 4, 1, 1), (40, 4, 130, 3), (256, 4, 256, 2)]:
+        X = rng.standard_normal((rl, n, nvec, rr))
+        Y = tt.tt_local_matvec_batched(g(np.eye(rl).reshape(rl, 1, rl)),
+                                       g(np.eye(n).reshape(1, n, n, 1)),
+                                       g(np.eye(rr).reshape(rr, 1, rr)), g(X))
+        assert np.array_equal(h(Y), X)
+
+
+# ----------------------------------------------------------------------------------------
+# config 5 at full size, in bench.py's launch configuration
+# ----------------------------------------------------------------------------------------
+def test_config5_w5_sampled(tt):
+    import oracle
+    import ttgen
+    inp = ttgen.make_inputs(5)
+    d, K = inp.cfg.d, inp.cfg.nvec
+    xs, As, Xs = [g(c) for c in inp.x], [g(c) for c in inp.A], [g(c) for c in inp.X]
+    Yf, Yb, phiL, phiR = tt.tt_sweep_als(xs, As, Xs, Y_bwd=[torch.empty_like(X) for X in Xs])
+    torch.cuda.synchronize()
+    with cf.ThreadPoolExecutor(2) as ex:   # ctypes releases the GIL: the chains run in parallel
+        fl = ex.submit(oracle.sweep_interfaces, inp.x, inp.A, 1)
+        fr = ex.submit(oracle.sweep_interfaces, inp.x, inp.A, 2)
+        oL = fl.result()[0]
+        oR = fr.result()[1]
+    for k in range(1, d + 1):
+        assert rel(h(phiL[k]), oL[k]) <= TOL, ("phiL", k)
+    for k in range(0, d):
+        assert rel(h(phiR[k]), oR[k]) <= TOL, ("phiR", k)
+    cols = [0, K - 1]
+    jobs = {}
+    with cf.ThreadPoolExecutor(min(16, os.cpu_count() or 1)) as ex:
+        for k in range(d):
+            for m in cols:
+                xk = np.ascontiguousarray(inp.X[k][:, :, m, :])
+                jobs[(k, m)] = ex.submit(oracle.local_matvec, oL[k], inp.A[k], oR[k + 1], xk)
+        for (k, m), f in jobs.items():
+            ref = f.result()
+            assert rel(h(Yf[k][:, :, m, :]), ref) <= TOL, ("fwd", k, m)
+            assert rel(h(Yb[k][:, :, m, :]), ref) <= TOL, ("bwd", k, m)
+    # forward and backward passes see identical interfaces -> identical results
+    for k in range(d):
+        assert torch.equal(Yf[k], Yb[k])
+    del Yf, Yb, Xs
+    torch.cuda.empty_cache()
+    zs = tt.tt_operator_apply(xs, As)
+    torch.cuda.synchronize()
+    for k in [0, 3, 6, 11]:
+        rl = inp.x[k].shape[0]
+        Rl = inp.A[k].shape[0]
+        for a0, a1 in [(0, 1), (rl - 1, rl)]:
+            ref = oracle.apply_core(inp.x[k][a0:a1], inp.A[k])
+            assert rel(h(zs[k][a0 * Rl:a1 * Rl]), ref) <= TOL, ("apply", k, a0)
+
+
+# ----------------------------------------------------------------------------------------
+# graph capture, error paths
+# ----------------------------------------------------------------------------------------
+def test_graph_capture_equals_eager(tt):
+    import ttgen
+    inp = ttgen.make_inputs(3)
+    xs, As = [g(c) for c in inp.x], [g(c) for c in inp.A]
+    eL, eR = tt.tt_sweep_interfaces(xs, As)
+    torch.cuda.synchronize()
+    gL = tt.alloc_interfaces(xs, As)
+    gR = tt.alloc_interfaces(xs, As)
+    tr = tt._Train(xs, As)
+    ws = torch.empty(tt.tt_sweep_workspace_size(tr), dtype=torch.uint8, device="cuda")
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(graph, stream=s):
+            tt.tt_sweep_interfaces(xs, As, gL, gR, workspace=ws, stream=s)
+    graph.replay()
+    torch.cuda.synchronize()
+    for a, b in zip(eL + eR, gL + gR):
+        assert torch.equal(a, b)
+
+
+def test_workspace_too_small_enqueues_nothing(tt):
+    x = torch.randn(4, 4, 4, dtype=torch.float64, device="cuda")
+    A = torch.randn(2, 4, 4, 2, dtype=torch.float64, device="cuda")
+    pl = torch.randn(4, 2, 4, dtype=torch.float64, device="cuda")
+    pr = torch.randn(4, 2, 4, dtype=torch.float64, device="cuda")
+    y = torch.full_like(x, 7.0)
+    ws = torch.empty(16, dtype=torch.uint8, device="cuda")
+    with pytest.raises(tt.TTError) as ei:
+        tt.tt_local_matvec(pl, A, pr, x, y, workspace=ws)
+    assert ei.value.status == 4
+    torch.cuda.synchronize()
+    assert bool((y == 7.0).all())
+    with pytest.raises(TypeError):
+        tt.tt_local_matvec(pl.cpu(), A, pr, x)
