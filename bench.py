@@ -1,0 +1,435 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 FP64 TT hot path (BASELINE.json metric, config 5 = W5 workload).
+
+One step = the whole hot path over one batch of synthetic config-5 input, through the C-ABI:
+  tt_sweep_als   (H1-H7: initial right interfaces, L->R sweep with K=32 batched local
+                  matvecs + left interfaces, R->L sweep with batched matvecs + right
+                  interfaces; DESIGN.md §5 workload W5)
+  tt_operator_apply (H8: full unrounded TT-matrix x TT-vector product)
+Value = algorithmic FP64 GFLOP per step / device time per step (CUDA events, max over ranks).
+
+  python bench.py [--gpus N --steps K --warmup W]          # our CUDA path
+  python bench.py --impl reference [--steps K --warmup W]  # the CPU oracle, as it stands
+
+Multi-GPU: replicas only — each rank runs the same workload, no collective on
+the data path; the barrier/all-reduce below is timing plumbing.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import ttgen  # noqa: E402
+
+METRIC = "FP64 GFLOP/s + % FP64 roofline of TT local matvec; full-sweep time at d=12"
+UNIT = "GFLOP/s"
+
+
+# ----------------------------------------------------------------------------------------
+# algorithmic work
+# ----------------------------------------------------------------------------------------
+def f_local(a, N, b, al, be):
+    """FLOPs of one local matvec (per vector) == one interface update: three products."""
+    return 2 * N * (a * a * al * b + a * b * b * be) + 2 * a * b * al * be * N * N
+
+
+def b_local_matvec(a, N, b, al, be, K):
+    return 8 * (a * a * al + b * b * be + al * N * N * be + 2 * K * a * N * b)
+
+
+def f_apply(a, N, b, al, be):
+    return 2 * a * al * N * b * be * N
+
+
+def b_apply(a, N, b, al, be):
+    return 8 * (a * N * b + al * N * N * be + a * al * N * b * be)
+
+
+def w5_work(cfg):
+    d, N, r, R, K = cfg.d, cfg.N, cfg.r, cfg.R, cfg.nvec
+    mv = sum(2 * K * f_local(r[k], N, r[k + 1], R[k], R[k + 1]) for k in range(d))
+    iface = sum(f_local(r[k], N, r[k + 1], R[k], R[k + 1]) for k in range(1, d)) * 2 \
+        + sum(f_local(r[k], N, r[k + 1], R[k], R[k + 1]) for k in range(0, d - 1))
+    ap = sum(f_apply(r[k], N, r[k + 1], R[k], R[k + 1]) for k in range(d))
+    ap_bytes = sum(b_apply(r[k], N, r[k + 1], R[k], R[k + 1]) for k in range(d))
+    return {"matvec_flops": mv, "interface_flops": iface, "apply_flops": ap,
+            "apply_bytes": ap_bytes, "step_flops": mv + iface + ap}
+
+
+# ----------------------------------------------------------------------------------------
+# clocks during the timed region
+# ----------------------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return None
+        sm = [float(p[1]) for p in rows if p[1].replace(".", "").isdigit()]
+        smax = [float(p[2]) for p in rows if p[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for p in rows for i in range(4) if "Active" in p[5 + i]
+                          and "Not" not in p[5 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------------------
+# reference arm: the CPU oracle as it stands
+# ----------------------------------------------------------------------------------------
+def oracle_sample_inputs(seed=7):
+    """Config-5 interior-core shapes (a=b=256, alpha=beta=36, N=4), seeded random values."""
+    cfg = ttgen.CONFIGS[5]
+    k = 6
+    a, b, al, be, N = cfg.r[k], cfg.r[k + 1], cfg.R[k], cfg.R[k + 1], cfg.N
+    rng = np.random.default_rng(seed)
+    return dict(a=a, b=b, al=al, be=be, N=N,
+                phiL=rng.standard_normal((a, al, a)), A=rng.standard_normal((al, N, N, be)),
+                phiR=rng.standard_normal((b, be, b)), x=rng.standard_normal((a, N, b)))
+
+
+def time_oracle_sample(with_interface=True):
+    import oracle
+    s = oracle_sample_inputs()
+    t0 = time.perf_counter()
+    oracle.local_matvec(s["phiL"], s["A"], s["phiR"], s["x"])
+    flops = f_local(s["a"], s["N"], s["b"], s["al"], s["be"])
+    if with_interface:
+        oracle.interface_left(s["phiL"], s["A"], s["x"])
+        flops += f_local(s["a"], s["N"], s["b"], s["al"], s["be"])
+    dt = time.perf_counter() - t0
+    return flops, dt
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    s = oracle_sample_inputs()
+    flops = f_local(s["a"], s["N"], s["b"], s["al"], s["be"])
+    for _ in range(args.warmup):
+        oracle.local_matvec(s["phiL"], s["A"], s["phiR"], s["x"])
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.local_matvec(s["phiL"], s["A"], s["phiR"], s["x"])
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    value = flops * args.steps / total / 1e9
+    sample = ("one Krylov column of the config-5 interior-core (k=6: a=b=256, alpha=beta=36, N=4) "
+              "local matvec per step, tt_oracle_local_matvec, seeded random interfaces")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "config 5 (d=12, r=256, R=36, K=32) W5 - bounded oracle sample",
+                   "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": sample, "cpu": cpu_model(), "compiler": "gcc -O2 -std=c99"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------------------
+# our arm
+# ----------------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-apply", action="store_true", help="debug: skip H8 in the step")
+    ap.add_argument("--verbose", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    import paper_2509_11890_b200 as tt
+
+    cfg = ttgen.CONFIGS[args.config]
+    work = w5_work(cfg)
+    if args.no_apply:
+        work["step_flops"] -= work["apply_flops"]
+    inp = ttgen.make_inputs(args.config, with_block=True)
+    d = cfg.d
+    stream = torch.cuda.current_stream(dev)
+
+    # pinned host copies (e2e source) and resident device copies
+    def pin(a):
+        return torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+
+    hx = [pin(c) for c in inp.x]
+    hA = [pin(c) for c in inp.A]
+    hX = [pin(c) for c in inp.X]
+    xs = [t.to(dev) for t in hx]
+    As = [t.to(dev) for t in hA]
+    Xs = [t.to(dev) for t in hX]
+    Yf = [torch.empty_like(X) for X in Xs]
+    phiL = tt.alloc_interfaces(xs, As)
+    phiR = tt.alloc_interfaces(xs, As)
+    tr = tt._Train(xs, As)
+    ws = torch.empty(tt.tt_sweep_als_workspace_size(tr, cfg.nvec), dtype=torch.uint8, device=dev)
+    zs = None
+    if not args.no_apply:
+        zs = [torch.empty((cfg.r[k] * cfg.R[k], cfg.N, cfg.r[k + 1] * cfg.R[k + 1]),
+                          dtype=torch.float64, device=dev) for k in range(d)]
+    hY = [torch.empty(Y.shape, dtype=torch.float64).pin_memory() for Y in Yf]
+    hE = torch.empty(1, dtype=torch.float64).pin_memory()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
+
+    launches = [0]
+
+    def step():
+        tt.tt_sweep_als(xs, As, Xs, Yf, None, phiL, phiR, workspace=ws, stream=stream)
+        n = tt.tt_last_launch_count()
+        if zs is not None:
+            tt.tt_operator_apply(xs, As, zs, stream=stream)
+            n += tt.tt_last_launch_count()
+        launches[0] += n
+
+    # ---- FP64 peak probe (roofline denominator, measured in this run) ------------------
+    def probe(iters):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fl = tt.tt_fp64_peak_probe(iters, stream=stream)
+        e1.record(stream)
+        e1.synchronize()
+        return fl / (e0.elapsed_time(e1) * 1e-3) / 1e12
+
+    probe(2000)
+    p64_burst = max(probe(40000) for _ in range(3))          # ~20 ms each
+    p64_sustained = probe(2000000)                             # ~1 s back to back
+
+    # ---- warm-up ----------------------------------------------------------------------
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+
+    # ---- timed region -----------------------------------------------------------------
+    tt.tt_trace_enable(400 * (args.steps + 1))
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    launches[0] = 0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.zero_()   # L2 flush between timed steps, outside the step's events
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    clk = clocks.stop()
+    gpu_launches = launches[0]
+    recs = [tt.tt_trace_read(i) for i in range(tt.tt_trace_count())]
+    tt.tt_trace_disable()
+
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = work["step_flops"] * world * args.steps / (total_ms * 1e-3) / 1e9
+
+    # ---- per-stage breakdown from the trace -----------------------------------------------
+    stages = {}
+    for r in recs:
+        s = stages.setdefault(r["stage"], {"launches": 0, "ms": 0.0, "flops": 0.0})
+        s["launches"] += 1
+        s["ms"] += r["ms"]
+        if r["stage"].startswith(("mv_", "il_", "ir_")):
+            s["flops"] += 2.0 * r["M"] * r["N"] * r["K"]
+        elif r["stage"] == "apply":
+            s["flops"] += 2.0 * r["M"] * r["N"]
+    traced_ms = sum(s["ms"] for s in stages.values())
+    for s in stages.values():
+        s["ms_per_step"] = s["ms"] / args.steps
+        s["tflops"] = s["flops"] / (s["ms"] * 1e-3) / 1e12 if s["ms"] > 0 else None
+        s["share"] = s["ms"] / traced_ms if traced_ms else None
+    dom_name = max((n for n in stages if n != "apply"), key=lambda n: stages[n]["ms"])
+    dom = stages[dom_name]
+    mv_ms = sum(stages[n]["ms"] for n in ("mv_s1", "mv_s2", "mv_s3") if n in stages)
+    mv_flops = sum(stages[n]["flops"] for n in ("mv_s1", "mv_s2", "mv_s3") if n in stages)
+    mv_tf = mv_flops / (mv_ms * 1e-3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(dom_name)
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "kernel": f"dmma_gemm ({dom_name})",
+                "achieved": dom["tflops"], "peak": p64_sustained, "unit": "TFLOP/s",
+                "frac": dom["tflops"] / p64_sustained, "traffic": traffic,
+                "peak_source": "FP64 DMMA probe kernel, measured in this run (sustained ~1 s); "
+                               "MEASURED_PEAKS.json has no FP64 entry",
+                "peak_burst": p64_burst}
+    apply_detail = None
+    if "apply" in stages:
+        ap_ms = stages["apply"]["ms"] / args.steps
+        apply_detail = {"ms_per_step": ap_ms, "bytes": work["apply_bytes"],
+                        "gbs": work["apply_bytes"] / (ap_ms * 1e-3) / 1e9}
+
+    # ---- end to end through the public API from pinned host buffers ---------------------
+    e2e = None
+    if not args.no_e2e:
+        h2d = sum(t.numel() * 8 for t in hx + hA + hX)
+        d2h = sum(t.numel() * 8 for t in hY) + 8
+        for _ in range(1):
+            for src, dst in zip(hx + hA + hX, xs + As + Xs):
+                dst.copy_(src, non_blocking=True)
+            step()
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            for src, dst in zip(hx + hA + hX, xs + As + Xs):
+                dst.copy_(src, non_blocking=True)
+            step()
+            for src, dst in zip(Yf, hY):
+                dst.copy_(src, non_blocking=True)
+            hE.copy_(phiL[d].reshape(1), non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        e_ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": work["step_flops"] * world * args.steps / (e_ms * 1e-3) / 1e9,
+               "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": e_ms / args.steps}
+
+    # ---- CPU oracle baseline (rank 0, N=1) ----------------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        fl, dt = time_oracle_sample(True)
+        cpu = {"value": fl / dt / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": "tt_oracle_local_matvec (1 Krylov column) + tt_oracle_interface_left at "
+                         "config-5 interior-core shapes (a=b=256, alpha=beta=36, N=4), "
+                         f"{fl / 1e9:.1f} GFLOP in {dt:.1f} s",
+               "cpu": cpu_model(), "compiler": "gcc -O2 -std=c99"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"config {cfg.index}: d={cfg.d}, N={cfg.N}, r={max(cfg.r)}, "
+                                   f"R={max(cfg.R)}, K={cfg.nvec} Krylov block; W5 two-direction "
+                                   "sweep (tt_sweep_als) + full unrounded apply (tt_operator_apply)",
+                       "step_gflop": work["step_flops"] / 1e9,
+                       "l2": "flushed between timed steps (256 MiB memset outside step events); "
+                             "inputs 0.43 GB > L2",
+                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": gpu_launches,
+            "clocks": clk,
+            "detail": {
+                "full_sweep_ms": (total_ms / args.steps) - (apply_detail["ms_per_step"]
+                                                            if apply_detail else 0.0),
+                "batched_matvec_tflops": mv_tf,
+                "batched_matvec_frac_of_p64": mv_tf / p64_sustained,
+                "p64_tflops_sustained": p64_sustained, "p64_tflops_burst": p64_burst,
+                "apply": apply_detail,
+                "stages": stages,
+                "step_ms": step_ms,
+                "work_gflop": {k: v / 1e9 for k, v in work.items() if k.endswith("flops")},
+            },
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -143,8 +143,35 @@ tt_status tt_operator_apply(int64_t d, const int64_t* n_row, const int64_t* n_co
                             const double* const* x_cores, const double* const* A_cores,
                             double* const* z_cores, void* stream);
 
-/* Number of kernel launches the last successful call on this thread enqueued. */
+/* Number of kernel launches the last call on this thread enqueued. */
 int64_t tt_last_launch_count(void);
+
+/* ---------------------------------------------------------------------------------------
+ * Tracing (measurement support, not part of the math).  While enabled on the calling
+ * thread, every kernel the library launches is bracketed by a pair of CUDA events recorded
+ * on its own stream, and a record {stage, tile, M, N, K} is appended (M,N,K = GEMM extents;
+ * for non-GEMM kernels N = K = 0 and M = elements written).  Do not enable while capturing
+ * a CUDA graph.  tt_trace_read synchronises on record i's end event.
+ *   stage: TT_ST_PERM, TT_ST_SET, TT_ST_MV_S1..S3 (local matvec), TT_ST_IL_S1..S3 (left
+ *   interface), TT_ST_IR_S1..S3 (right interface), TT_ST_APPLY.  tile = the GEMM tile's BN.
+ * ------------------------------------------------------------------------------------- */
+enum {
+  TT_ST_PERM = 0, TT_ST_SET = 1,
+  TT_ST_MV_S1 = 2, TT_ST_MV_S2 = 3, TT_ST_MV_S3 = 4,
+  TT_ST_IL_S1 = 5, TT_ST_IL_S2 = 6, TT_ST_IL_S3 = 7,
+  TT_ST_IR_S1 = 8, TT_ST_IR_S2 = 9, TT_ST_IR_S3 = 10,
+  TT_ST_APPLY = 11
+};
+tt_status tt_trace_enable(int64_t capacity);
+tt_status tt_trace_disable(void);
+int64_t tt_trace_count(void);
+tt_status tt_trace_read(int64_t i, int* stage, int* tile, int64_t* M, int64_t* N, int64_t* K,
+                        float* ms);
+
+/* FP64 DMMA throughput probe (roofline denominator): enqueues one kernel of
+ * `iters` dependent-free mma.m8n8k4.f64 rounds on every SM; returns its FP64 flop count in
+ * *flops.  Time it with events on `stream`. */
+tt_status tt_fp64_peak_probe(int64_t iters, double* flops, void* stream);
 
 #ifdef __cplusplus
 }

@@ -22,8 +22,12 @@ __all__ = [
     "tt_interface_workspace_size", "tt_interface_left", "tt_interface_right",
     "tt_sweep_workspace_size", "tt_sweep_interfaces", "tt_sweep_als_workspace_size",
     "tt_sweep_als", "tt_operator_apply", "tt_last_launch_count",
-    "TT_SWEEP_LEFT", "TT_SWEEP_RIGHT", "TT_SWEEP_BOTH",
+    "TT_SWEEP_LEFT", "TT_SWEEP_RIGHT", "TT_SWEEP_BOTH", "tt_trace_enable", "tt_trace_disable",
+    "tt_trace_count", "tt_trace_read", "tt_fp64_peak_probe", "STAGE_NAMES",
 ]
+
+STAGE_NAMES = {0: "perm", 1: "set", 2: "mv_s1", 3: "mv_s2", 4: "mv_s3", 5: "il_s1", 6: "il_s2",
+               7: "il_s3", 8: "ir_s1", 9: "ir_s2", 10: "ir_s3", 11: "apply"}
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libtt_hotpath.so")
 TT_SWEEP_LEFT, TT_SWEEP_RIGHT, TT_SWEEP_BOTH = 1, 2, 3
@@ -55,6 +59,12 @@ lib.tt_sweep_als_workspace_size.restype = _sz
 lib.tt_sweep_als_workspace_size.argtypes = [_i64, _p, _p, _p, _i64]
 lib.tt_sweep_als.argtypes = [_i64, _p, _p, _p, _i64] + [_p] * 7 + [_p, _sz, _p]
 lib.tt_operator_apply.argtypes = [_i64, _p, _p, _p, _p, _p, _p, _p, _p]
+lib.tt_trace_enable.argtypes = [_i64]
+lib.tt_trace_count.restype = ctypes.c_int64
+lib.tt_trace_read.argtypes = [_i64] + [_p] * 6
+lib.tt_fp64_peak_probe.argtypes = [_i64, _p, _p]
+for _f in ("tt_trace_enable", "tt_trace_disable", "tt_trace_read", "tt_fp64_peak_probe"):
+    getattr(lib, _f).restype = ctypes.c_int
 for _f in ("tt_local_matvec", "tt_local_matvec_batched", "tt_interface_left",
            "tt_interface_right", "tt_sweep_interfaces", "tt_sweep_als", "tt_operator_apply"):
     getattr(lib, _f).restype = ctypes.c_int
@@ -245,3 +255,34 @@ def tt_operator_apply(x_cores, A_cores, z_cores=None, stream=None):
                                  _ptrs(x_cores, "x_cores"), _ptrs(A_cores, "A_cores"),
                                  _ptrs(z_cores, "z_cores"), _stream(stream)))
     return z_cores
+
+
+def tt_trace_enable(capacity: int = 4096) -> None:
+    """Start recording a CUDA-event pair around every library launch on this thread."""
+    _check(lib.tt_trace_enable(int(capacity)))
+
+
+def tt_trace_disable() -> None:
+    _check(lib.tt_trace_disable())
+
+
+def tt_trace_count() -> int:
+    return int(lib.tt_trace_count())
+
+
+def tt_trace_read(i: int) -> dict:
+    """Record i: {stage, tile, M, N, K, ms} (synchronises on the launch's end event)."""
+    st, tile = ctypes.c_int(), ctypes.c_int()
+    M, N, K = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    ms = ctypes.c_float()
+    _check(lib.tt_trace_read(int(i), ctypes.byref(st), ctypes.byref(tile), ctypes.byref(M),
+                             ctypes.byref(N), ctypes.byref(K), ctypes.byref(ms)))
+    return {"stage": STAGE_NAMES.get(st.value, str(st.value)), "tile": tile.value,
+            "M": M.value, "N": N.value, "K": K.value, "ms": ms.value}
+
+
+def tt_fp64_peak_probe(iters: int, stream=None) -> float:
+    """Enqueue the FP64 DMMA probe kernel; returns its flop count (time it on `stream`)."""
+    f = ctypes.c_double()
+    _check(lib.tt_fp64_peak_probe(int(iters), ctypes.byref(f), _stream(stream)))
+    return f.value

@@ -29,6 +29,35 @@ thread_local std::string g_msg;
 thread_local int64_t g_launches = 0;
 thread_local int64_t g_launches_last = 0;
 
+// ---- tracing (tt_trace_*): per-launch CUDA events on the launch stream ----------------
+struct TraceRec {
+  int stage, tile;
+  long long M, N, K;
+  cudaEvent_t e0, e1;
+};
+thread_local bool g_trace_on = false;
+thread_local std::vector<TraceRec> g_trace;
+thread_local std::vector<cudaEvent_t> g_trace_pool;
+thread_local int g_stage = TT_ST_PERM;   // stage tag of the next launch
+
+long long trace_begin(int tile, long long M, long long N, long long K, cudaStream_t s) {
+  if (!g_trace_on || 2 * (g_trace.size() + 1) > g_trace_pool.size()) return -1;
+  TraceRec r;
+  r.stage = g_stage;
+  r.tile = tile;
+  r.M = M;
+  r.N = N;
+  r.K = K;
+  r.e0 = g_trace_pool[2 * g_trace.size()];
+  r.e1 = g_trace_pool[2 * g_trace.size() + 1];
+  cudaEventRecord(r.e0, s);
+  g_trace.push_back(r);
+  return (long long)g_trace.size() - 1;
+}
+void trace_end(long long idx, cudaStream_t s) {
+  if (idx >= 0) cudaEventRecord(g_trace[idx].e1, s);
+}
+
 tt_status fail(tt_status s, const std::string& m) {
   g_msg = m;
   return s;
@@ -97,7 +126,9 @@ cudaError_t launch_cfg(const GemmParams& p0, cudaStream_t s) {
   p.tiles_n = (p.N + BN - 1) / BN;
   const long long tiles = tm * p.tiles_n;
   if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  const long long tr = trace_begin(BN, p.M, p.N, p.K, s);
   kern<<<(unsigned)tiles, Cfg::kThreads, Cfg::kSmemBytes, s>>>(p);
+  trace_end(tr, s);
   ++g_launches;
   return cudaGetLastError();
 }
@@ -180,16 +211,24 @@ cudaError_t launch_perm(bool left, const double* A, double* out, long long al, l
   const int threads = 256;
   long long blocks = (total + threads - 1) / threads;
   if (blocks > 4096) blocks = 4096;
+  const int saved = g_stage;
+  g_stage = TT_ST_PERM;
+  const long long tr = trace_begin(0, total, 0, 0, s);
+  g_stage = saved;
   if (left)
     perm_left_kernel<<<(unsigned)blocks, threads, 0, s>>>(A, out, al, n, be);
   else
     perm_right_kernel<<<(unsigned)blocks, threads, 0, s>>>(A, out, al, n, be);
+  trace_end(tr, s);
   ++g_launches;
   return cudaGetLastError();
 }
 
 cudaError_t launch_set_one(double* p, cudaStream_t s) {
+  g_stage = TT_ST_SET;
+  const long long tr = trace_begin(0, 1, 0, 0, s);
   set_one_kernel<<<1, 1, 0, s>>>(p);
+  trace_end(tr, s);
   ++g_launches;
   return cudaGetLastError();
 }
@@ -230,6 +269,22 @@ __global__ void __launch_bounds__(256) apply_kernel(const double* __restrict__ x
   }
 }
 
+// FP64 DMMA throughput probe: 8 independent accumulator chains per warp.
+__global__ void __launch_bounds__(256) dmma_probe_kernel(double* out, long long iters) {
+  double c[8][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = 0.0;
+  const double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
+  for (long long it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) tt::dmma_8x8x4(c[i], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+  if (s == -1.0) out[threadIdx.x] = s;   // never true; keeps the loop live
+}
+
 // ----------------------------------------------------------------------------------------
 // stage plans
 // ----------------------------------------------------------------------------------------
@@ -256,18 +311,21 @@ cudaError_t enqueue_matvec(const Dims& d, long long K, const double* phiL, const
   cudaError_t e;
   if ((e = launch_perm(true, A, Ah, al, N, be, s)) != cudaSuccess) return e;
   // S1: T1(al, j, a', m, b) = phiL[(a' al), a] . X[a, (j m b)]
+  g_stage = TT_ST_MV_S1;
   e = launch_gemm(true, false,
                   gp(phiL, a, X, N * K * b, T1, a * al, N * K * b, a,
                      tt::map2(al, N * a * K * b, K * b), tt::map2(K * b, 1, a * K * b)),
                   s);
   if (e != cudaSuccess) return e;
   // S2^T: T2(a', m, i, be, b) = T1^T[(a' m b), (al j)] . Ahat[(al j), (i be)]
+  g_stage = TT_ST_MV_S2;
   e = launch_gemm(false, false,
                   gp(T1, a * K * b, Ah, N * be, T2, a * K * b, N * be, al * N,
                      tt::map2(b, 1, N * be * b), tt::map_plain(b)),
                   s);
   if (e != cudaSuccess) return e;
   // S3: Y(a', i, m, b') = T2[(a' m i), (be b)] . phiR[b', (be b)]^T
+  g_stage = TT_ST_MV_S3;
   e = launch_gemm(true, true,
                   gp(T2, be * b, phiR, be * b, Y, a * K * N, b, be * b,
                      tt::map3(N, K, K * b, b, N * K * b), tt::map_plain(1)),
@@ -293,16 +351,19 @@ cudaError_t enqueue_left(const Dims& d, const double* phiL, const double* A, con
   const long long a = d.a, b = d.b, al = d.al, be = d.be, N = d.n;
   cudaError_t e;
   if ((e = launch_perm(true, A, Ah, al, N, be, s)) != cudaSuccess) return e;
+  g_stage = TT_ST_IL_S1;
   e = launch_gemm(true, false,
                   gp(phiL, a, x, N * b, T1, a * al, N * b, a, tt::map2(al, N * a * b, b),
                      tt::map2(b, 1, a * b)),
                   s);
   if (e != cudaSuccess) return e;
+  g_stage = TT_ST_IL_S2;
   e = launch_gemm(false, false,
                   gp(T1, a * b, Ah, N * be, T2, a * b, N * be, al * N, tt::map2(b, 1, N * be * b),
                      tt::map_plain(b)),
                   s);
   if (e != cudaSuccess) return e;
+  g_stage = TT_ST_IL_S3;
   return launch_gemm(false, false,
                      gp(x, b, T2, be * b, out, b, be * b, a * N, tt::map_plain(be * b),
                         tt::map_plain(1)),
@@ -317,16 +378,19 @@ cudaError_t enqueue_right(const Dims& d, const double* phiR, const double* A, co
   const long long a = d.a, b = d.b, al = d.al, be = d.be, N = d.n;
   cudaError_t e;
   if ((e = launch_perm(false, A, At, al, N, be, s)) != cudaSuccess) return e;
+  g_stage = TT_ST_IR_S1;
   e = launch_gemm(true, true,
                   gp(x, b, phiR, b, T1, a * N, b * be, b, tt::map2(N, be * a * b, b),
                      tt::map2(be, a * b, 1)),
                   s);
   if (e != cudaSuccess) return e;
+  g_stage = TT_ST_IR_S2;
   e = launch_gemm(false, false,
                   gp(T1, a * b, At, al * N, T2, a * b, al * N, N * be, tt::map2(b, al * a, 1),
                      tt::map2(N, b * al * a, a)),
                   s);
   if (e != cudaSuccess) return e;
+  g_stage = TT_ST_IR_S3;
   return launch_gemm(true, false,
                      gp(x, N * b, T2, al * a, out, a, al * a, N * b, tt::map_plain(al * a),
                         tt::map_plain(1)),
@@ -746,13 +810,78 @@ tt_status tt_operator_apply(int64_t d, const int64_t* n_row, const int64_t* n_co
   for (int64_t k = 0; k < d; ++k) {
     const long long smem = 8LL * (n_col[k] * r[k + 1] + n_row[k] * n_col[k] * R[k + 1]);
     const long long blocks = r[k] * R[k];
+    g_stage = TT_ST_APPLY;
+    const long long tr = trace_begin(0, r[k] * R[k] * n_row[k] * r[k + 1] * R[k + 1], n_col[k], 0, s);
     apply_kernel<<<(unsigned)blocks, 256, (size_t)smem, s>>>(
         x_cores[k], A_cores[k], z_cores[k], (int)r[k], (int)n_row[k], (int)n_col[k],
         (int)r[k + 1], (int)R[k], (int)R[k + 1]);
+    trace_end(tr, s);
     ++g_launches;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "tt_operator_apply");
   }
+  return TT_OK;
+}
+
+// ---- tracing / probe ----------------------------------------------------------------------
+tt_status tt_trace_enable(int64_t capacity) {
+  g_msg.clear();
+  if (capacity <= 0) return fail(TT_ERR_INVALID_ARGUMENT, "capacity must be positive");
+  tt_trace_disable();
+  g_trace_pool.resize(size_t(2 * capacity));
+  for (auto& ev : g_trace_pool) {
+    cudaError_t e = cudaEventCreate(&ev);
+    if (e != cudaSuccess) {
+      g_trace_pool.clear();
+      return cuda_fail(e, "tt_trace_enable");
+    }
+  }
+  g_trace.clear();
+  g_trace.reserve(size_t(capacity));
+  g_trace_on = true;
+  return TT_OK;
+}
+
+tt_status tt_trace_disable(void) {
+  for (auto& ev : g_trace_pool) cudaEventDestroy(ev);
+  g_trace_pool.clear();
+  g_trace.clear();
+  g_trace_on = false;
+  return TT_OK;
+}
+
+int64_t tt_trace_count(void) { return (int64_t)g_trace.size(); }
+
+tt_status tt_trace_read(int64_t i, int* stage, int* tile, int64_t* M, int64_t* N, int64_t* K,
+                        float* ms) {
+  if (i < 0 || i >= (int64_t)g_trace.size()) return fail(TT_ERR_INVALID_ARGUMENT, "bad index");
+  const TraceRec& r = g_trace[size_t(i)];
+  if (stage) *stage = r.stage;
+  if (tile) *tile = r.tile;
+  if (M) *M = r.M;
+  if (N) *N = r.N;
+  if (K) *K = r.K;
+  if (ms) {
+    cudaError_t e = cudaEventSynchronize(r.e1);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(ms, r.e0, r.e1);
+    if (e != cudaSuccess) return cuda_fail(e, "tt_trace_read");
+  }
+  return TT_OK;
+}
+
+tt_status tt_fp64_peak_probe(int64_t iters, double* flops, void* stream) {
+  CallScope scope;
+  if (iters <= 0) return fail(TT_ERR_INVALID_ARGUMENT, "iters must be positive");
+  if (!flops) return fail(TT_ERR_NULL_POINTER, "flops");
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int blocks = 2 * sms, threads = 256;   // 16 warps per SM
+  dmma_probe_kernel<<<blocks, threads, 0, static_cast<cudaStream_t>(stream)>>>(nullptr, iters);
+  ++g_launches;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "tt_fp64_peak_probe");
+  *flops = 2.0 * 8 * 8 * 4 * 8.0 * double(iters) * blocks * (threads / 32);
   return TT_OK;
 }
 

@@ -171,9 +171,10 @@ def test_config5_w5_sampled(tt):
         fr = ex.submit(oracle.sweep_interfaces, inp.x, inp.A, 2)
         oL = fl.result()[0]
         oR = fr.result()[1]
-    for k in range(1, d + 1):
+    # W5 builds phiL[1..d-1] and phiR[1..d-1] (phiL[d], phiR[0] are not needed by a sweep)
+    assert h(phiL[0]).item() == 1.0 and h(phiR[d]).item() == 1.0
+    for k in range(1, d):
         assert rel(h(phiL[k]), oL[k]) <= TOL, ("phiL", k)
-    for k in range(0, d):
         assert rel(h(phiR[k]), oR[k]) <= TOL, ("phiR", k)
     cols = [0, K - 1]
     jobs = {}
