@@ -145,6 +145,9 @@ tt_status tt_operator_apply(int64_t d, const int64_t* n_row, const int64_t* n_co
 
 /* Number of kernel launches the last call on this thread enqueued. */
 int64_t tt_last_launch_count(void);
+/* Test hook: on != 0 routes every GEMM stage of the calling thread through the generic
+ * (unaligned-capable) kernel instead of the persistent 16-byte-load kernel. */
+void tt_debug_force_v1(int on);
 
 /* ---------------------------------------------------------------------------------------
  * Tracing (measurement support, not part of the math).  While enabled on the calling

@@ -23,7 +23,7 @@ __all__ = [
     "tt_sweep_workspace_size", "tt_sweep_interfaces", "tt_sweep_als_workspace_size",
     "tt_sweep_als", "tt_operator_apply", "tt_last_launch_count",
     "TT_SWEEP_LEFT", "TT_SWEEP_RIGHT", "TT_SWEEP_BOTH", "tt_trace_enable", "tt_trace_disable",
-    "tt_trace_count", "tt_trace_read", "tt_fp64_peak_probe", "STAGE_NAMES",
+    "tt_trace_count", "tt_trace_read", "tt_fp64_peak_probe", "STAGE_NAMES", "tt_debug_force_v1",
 ]
 
 STAGE_NAMES = {0: "perm", 1: "set", 2: "mv_s1", 3: "mv_s2", 4: "mv_s3", 5: "il_s1", 6: "il_s2",
@@ -63,6 +63,8 @@ lib.tt_trace_enable.argtypes = [_i64]
 lib.tt_trace_count.restype = ctypes.c_int64
 lib.tt_trace_read.argtypes = [_i64] + [_p] * 6
 lib.tt_fp64_peak_probe.argtypes = [_i64, _p, _p]
+lib.tt_debug_force_v1.argtypes = [ctypes.c_int]
+lib.tt_debug_force_v1.restype = None
 for _f in ("tt_trace_enable", "tt_trace_disable", "tt_trace_read", "tt_fp64_peak_probe"):
     getattr(lib, _f).restype = ctypes.c_int
 for _f in ("tt_local_matvec", "tt_local_matvec_batched", "tt_interface_left",
@@ -286,3 +288,8 @@ def tt_fp64_peak_probe(iters: int, stream=None) -> float:
     f = ctypes.c_double()
     _check(lib.tt_fp64_peak_probe(int(iters), ctypes.byref(f), _stream(stream)))
     return f.value
+
+
+def tt_debug_force_v1(on: bool) -> None:
+    """Test hook: route this thread's GEMM stages through the generic (v1) kernel."""
+    lib.tt_debug_force_v1(1 if on else 0)

@@ -13,12 +13,14 @@
 
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
 #include <mutex>
 #include <string>
 #include <vector>
 
 #include "../../include/tt_hotpath.h"
 #include "tt_gemm.cuh"
+#include "tt_gemm_v2.cuh"
 
 using tt::GemmParams;
 using tt::IndexMap;
@@ -145,8 +147,88 @@ cudaError_t launch_gemm_l(const GemmParams& p, cudaStream_t s) {
   return launch_cfg<128, 128, 16, 2, 4, 4, AK, BK_>(p, s);
 }
 
+// ---- v2 (persistent, 16 warps, 16-byte loads) --------------------------------------------
+int num_sms() {
+  static int sms = 0;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  });
+  return sms;
+}
+
+template <bool AK, bool BK_, int BN, int WM, int WN>
+cudaError_t launch_v2_cfg(const GemmParams& p0, cudaStream_t s) {
+  constexpr int ST = 4;
+  using Cfg = tt::GemmV2Cfg<AK, BK_, BN, WM, WN, ST>;
+  auto kern = tt::dmma_gemm_v2_kernel<AK, BK_, BN, WM, WN, ST>;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] {
+    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)Cfg::kSmemBytes);
+  });
+  if (attr_err != cudaSuccess) return attr_err;
+  tt::GemmParamsV2 p;
+  p.A = p0.A;
+  p.B = p0.B;
+  p.C = p0.C;
+  p.M = (int)p0.M;
+  p.N = (int)p0.N;
+  p.K = (int)p0.K;
+  p.lda = p0.lda;
+  p.ldb = p0.ldb;
+  p.rowmap = tt::to_map32(p0.rowmap);
+  p.colmap = tt::to_map32(p0.colmap);
+  const long long tm = (p0.M + Cfg::BM - 1) / Cfg::BM;
+  const long long tn = (p0.N + BN - 1) / BN;
+  p.tiles_n = (int)tn;
+  p.total_tiles = (int)(tm * tn);
+  p.KT = (int)((p0.K + Cfg::BK - 1) / Cfg::BK);
+  const int grid = (int)std::min<long long>(tm * tn, num_sms());
+  const long long tr = trace_begin(BN, p0.M, p0.N, p0.K, s);
+  kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes, s>>>(p);
+  trace_end(tr, s);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+template <bool AK, bool BK_>
+cudaError_t launch_v2_l(const GemmParams& p, cudaStream_t s) {
+  if (p.N <= 16) return launch_v2_cfg<AK, BK_, 16, 16, 1>(p, s);
+  if (p.N <= 40) return launch_v2_cfg<AK, BK_, 40, 16, 1>(p, s);
+  if (p.N <= 64) return launch_v2_cfg<AK, BK_, 64, 8, 2>(p, s);
+  if (p.N <= 104) return launch_v2_cfg<AK, BK_, 104, 16, 1>(p, s);
+  if (p.N <= 144) return launch_v2_cfg<AK, BK_, 144, 8, 2>(p, s);
+  return launch_v2_cfg<AK, BK_, 128, 4, 4>(p, s);
+}
+
+bool aligned16(const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; }
+
+// the v2 preconditions (tt_gemm_v2.cuh header)
+bool v2_eligible(bool a_kc, bool b_kc, const GemmParams& p) {
+  const long long lim = (1LL << 31) - 256;
+  if (p.M >= lim || p.N >= lim || p.K >= lim) return false;
+  if (!aligned16(p.A) || !aligned16(p.B) || (p.lda & 1) || (p.ldb & 1)) return false;
+  if (a_kc ? (p.K & 1) : (p.M & 1)) return false;
+  if (b_kc ? (p.K & 1) : (p.N & 1)) return false;
+  const long long tiles = ((p.M + 127) / 128) * ((p.N + 15) / 16);
+  return tiles < lim;
+}
+
+thread_local int g_force_v1 = 0;   // test hook (tt_debug_force_v1)
+
 cudaError_t launch_gemm(bool a_kc, bool b_kc, const GemmParams& p, cudaStream_t s) {
   if (p.M <= 0 || p.N <= 0 || p.K <= 0) return cudaSuccess;
+  if (!g_force_v1 && v2_eligible(a_kc, b_kc, p)) {
+    if (a_kc && b_kc) return launch_v2_l<true, true>(p, s);
+    if (a_kc && !b_kc) return launch_v2_l<true, false>(p, s);
+    if (!a_kc && b_kc) return launch_v2_l<false, true>(p, s);
+    return launch_v2_l<false, false>(p, s);
+  }
   if (a_kc && b_kc) return launch_gemm_l<true, true>(p, s);
   if (a_kc && !b_kc) return launch_gemm_l<true, false>(p, s);
   if (!a_kc && b_kc) return launch_gemm_l<false, true>(p, s);
@@ -446,6 +528,7 @@ const char* tt_status_string(tt_status s) {
 const char* tt_last_error_message(void) { return g_msg.c_str(); }
 const char* tt_version(void) { return "tt_hotpath 0.1 (sm_100a, FP64 DMMA)"; }
 int64_t tt_last_launch_count(void) { return g_launches_last; }
+void tt_debug_force_v1(int on) { g_force_v1 = on; }
 
 size_t tt_local_matvec_workspace_size(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t Rr,
                                       int64_t nvec) {

@@ -57,8 +57,20 @@ def test_smoke():
 # ----------------------------------------------------------------------------------------
 # configs 1-4: full W34 workload (sweep both directions + one matvec per core) + apply
 # ----------------------------------------------------------------------------------------
-@pytest.mark.parametrize("idx", [1, 2, 3, 4])
-def test_config_w34_parity(tt, idx):
+@pytest.mark.parametrize("idx,force_v1", [(1, False), (2, False), (3, False), (4, False),
+                                          (3, True), (4, True)])
+def test_config_w34_parity(tt, idx, force_v1):
+    """force_v1 routes every GEMM through the generic unaligned-capable kernel."""
+    import oracle
+    import ttgen
+    tt.tt_debug_force_v1(force_v1)
+    try:
+        _w34(tt, idx)
+    finally:
+        tt.tt_debug_force_v1(False)
+
+
+def _w34(tt, idx):
     import oracle
     import ttgen
     inp = ttgen.make_inputs(idx)
