@@ -201,6 +201,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-apply", action="store_true", help="debug: skip H8 in the step")
     ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--variant", type=int, default=-1, help="GEMM tiling variant (benchmark hook)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
@@ -221,6 +222,7 @@ def main():
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     import paper_2509_11890_b200 as tt
+    tt.tt_debug_set_variant(args.variant)
 
     cfg = ttgen.CONFIGS[args.config]
     work = w5_work(cfg)

@@ -148,6 +148,12 @@ int64_t tt_last_launch_count(void);
 /* Test hook: on != 0 routes every GEMM stage of the calling thread through the generic
  * (unaligned-capable) kernel instead of the persistent 16-byte-load kernel. */
 void tt_debug_force_v1(int on);
+/* Benchmark hook: GEMM tiling variant of the calling thread (-1 = default; 0 = one 512-thread
+ * CTA per SM; 1 = two 256-thread CTAs per SM). */
+void tt_debug_set_variant(int v);
+/* Benchmark hook (results become WRONG): bit 0 skips the GEMM output stores, bit 1 skips the
+ * operand loads, so the main loop / epilogue / load path can be timed in isolation. */
+void tt_debug_set_flags(int flags);
 
 /* ---------------------------------------------------------------------------------------
  * Tracing (measurement support, not part of the math).  While enabled on the calling

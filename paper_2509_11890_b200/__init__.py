@@ -24,6 +24,7 @@ __all__ = [
     "tt_sweep_als", "tt_operator_apply", "tt_last_launch_count",
     "TT_SWEEP_LEFT", "TT_SWEEP_RIGHT", "TT_SWEEP_BOTH", "tt_trace_enable", "tt_trace_disable",
     "tt_trace_count", "tt_trace_read", "tt_fp64_peak_probe", "STAGE_NAMES", "tt_debug_force_v1",
+    "tt_debug_set_variant", "tt_debug_set_flags",
 ]
 
 STAGE_NAMES = {0: "perm", 1: "set", 2: "mv_s1", 3: "mv_s2", 4: "mv_s3", 5: "il_s1", 6: "il_s2",
@@ -65,6 +66,10 @@ lib.tt_trace_read.argtypes = [_i64] + [_p] * 6
 lib.tt_fp64_peak_probe.argtypes = [_i64, _p, _p]
 lib.tt_debug_force_v1.argtypes = [ctypes.c_int]
 lib.tt_debug_force_v1.restype = None
+lib.tt_debug_set_variant.argtypes = [ctypes.c_int]
+lib.tt_debug_set_variant.restype = None
+lib.tt_debug_set_flags.argtypes = [ctypes.c_int]
+lib.tt_debug_set_flags.restype = None
 for _f in ("tt_trace_enable", "tt_trace_disable", "tt_trace_read", "tt_fp64_peak_probe"):
     getattr(lib, _f).restype = ctypes.c_int
 for _f in ("tt_local_matvec", "tt_local_matvec_batched", "tt_interface_left",
@@ -293,3 +298,13 @@ def tt_fp64_peak_probe(iters: int, stream=None) -> float:
 def tt_debug_force_v1(on: bool) -> None:
     """Test hook: route this thread's GEMM stages through the generic (v1) kernel."""
     lib.tt_debug_force_v1(1 if on else 0)
+
+
+def tt_debug_set_variant(v: int) -> None:
+    """Benchmark hook: GEMM tiling variant for this thread (-1 default, 0, 1)."""
+    lib.tt_debug_set_variant(int(v))
+
+
+def tt_debug_set_flags(flags: int) -> None:
+    """Benchmark hook (results become wrong): 1 = skip GEMM stores, 2 = skip operand loads."""
+    lib.tt_debug_set_flags(int(flags))

@@ -69,11 +69,13 @@ __device__ __forceinline__ long long apply_map32(const IndexMap32& m, uint32_t x
 struct GemmParamsV2 {
   const double* A;
   const double* B;
-  double* C;
+  double* C;        // final output (ksplit == 1) ...
+  double* P;        // ... or partial sums P[split][m][n] (ksplit > 1), reduced afterwards
   int M, N, K;
   long long lda, ldb;
   IndexMap32 rowmap, colmap;
-  int tiles_n, total_tiles, KT;
+  int tiles_n, total_units, KT, ksplit, kt_per_split;
+  int dbg;          // benchmark hook: bit 0 = skip output stores, bit 1 = skip operand loads
 };
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool ok) {
@@ -97,10 +99,9 @@ __device__ __forceinline__ void stg_cs(double* p, double v) {
   asm volatile("st.global.cs.f64 [%0], %1;\n" ::"l"(p), "d"(v));
 }
 
-template <bool A_KC, bool B_KC, int BN, int WARPS_M, int WARPS_N, int STAGES>
+template <bool A_KC, bool B_KC, int BM_, int BN, int WARPS_M, int WARPS_N, int STAGES, int MINB>
 struct GemmV2Cfg {
-  static constexpr int BM = 128, BK = 16, kThreads = 512;
-  static_assert(WARPS_M * WARPS_N == 16, "16 warps");
+  static constexpr int BM = BM_, BK = 16, kThreads = WARPS_M * WARPS_N * 32;
   static constexpr int WTM = BM / WARPS_M, WTN = BN / WARPS_N;
   static_assert(WTM % 8 == 0 && WTN % 8 == 0, "warp tile multiple of 8");
   static constexpr int MI = WTM / 8, NI = WTN / 8;
@@ -114,9 +115,10 @@ struct GemmV2Cfg {
   static constexpr size_t kSmemBytes = sizeof(double) * (size_t)STAGES * (A_ST + B_ST);
 };
 
-template <bool A_KC, bool B_KC, int BN, int WARPS_M, int WARPS_N, int STAGES>
-__global__ void __launch_bounds__(512, 1) dmma_gemm_v2_kernel(const GemmParamsV2 p) {
-  using Cfg = GemmV2Cfg<A_KC, B_KC, BN, WARPS_M, WARPS_N, STAGES>;
+template <bool A_KC, bool B_KC, int BM_, int BN, int WARPS_M, int WARPS_N, int STAGES, int MINB>
+__global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, MINB)
+dmma_gemm_v2_kernel(const GemmParamsV2 p) {
+  using Cfg = GemmV2Cfg<A_KC, B_KC, BM_, BN, WARPS_M, WARPS_N, STAGES, MINB>;
   constexpr int BM = Cfg::BM, BK = Cfg::BK, NT = Cfg::kThreads;
   constexpr int WTM = Cfg::WTM, WTN = Cfg::WTN, MI = Cfg::MI, NI = Cfg::NI;
   constexpr int A_LD = Cfg::A_LD, B_LD = Cfg::B_LD, A_ST = Cfg::A_ST, B_ST = Cfg::B_ST;
@@ -128,12 +130,11 @@ __global__ void __launch_bounds__(512, 1) dmma_gemm_v2_kernel(const GemmParamsV2
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp / WARPS_N, wn = warp % WARPS_N;
   const int g = lane >> 2, t = lane & 3;
-  const int KT = p.KT;
 
-  // ---- loader: stage <- k-tile (tile, kt) -----------------------------------------------
-  auto load = [&](int stage, int tile, int kt) {
-    const int tm = tile / p.tiles_n, tn = tile - tm * p.tiles_n;
-    const int m0 = tm * BM, n0 = tn * BN, k0 = kt * BK;
+  // ---- loader: stage <- k-tile kt of the tile at (m0, n0) ------------------------------
+  auto load = [&](int stage, int m0, int n0, int kt) {
+    if (p.dbg & 2) return;
+    const int k0 = kt * BK;
     double* as = As + stage * A_ST;
     double* bs = Bs + stage * B_ST;
 #pragma unroll
@@ -168,6 +169,21 @@ __global__ void __launch_bounds__(512, 1) dmma_gemm_v2_kernel(const GemmParamsV2
     }
   };
 
+  // work unit u -> (tile, k-split): m0, n0, [kt_begin, kt_end)
+  struct Unit {
+    int m0, n0, kb, ke, split;
+  };
+  auto unit_of = [&](int u) -> Unit {
+    Unit w;
+    const int tile = u / p.ksplit;
+    w.split = u - tile * p.ksplit;
+    const int tm = tile / p.tiles_n;
+    w.m0 = tm * BM;
+    w.n0 = (tile - tm * p.tiles_n) * BN;
+    w.kb = w.split * p.kt_per_split;
+    w.ke = min(p.KT, w.kb + p.kt_per_split);
+    return w;
+  };
   // ---- fragment geometry ---------------------------------------------------------------
   // row (within the CTA tile) of fragment i, lane-group g
   auto frag_row = [&](int i) -> int {
@@ -190,42 +206,51 @@ __global__ void __launch_bounds__(512, 1) dmma_gemm_v2_kernel(const GemmParamsV2
 #pragma unroll
     for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  // this CTA's k-tile stream: tiles blockIdx.x, blockIdx.x + gridDim.x, ...
-  const int my_tiles = (p.total_tiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
-  const long long total = (long long)my_tiles * KT;
-  int l_tile = blockIdx.x, l_kt = 0;
-  long long l_q = 0;
+  // this CTA's k-tile stream over units blockIdx.x, blockIdx.x + gridDim.x, ...
+  int l_u = blockIdx.x;
+  Unit lw = unit_of(l_u < p.total_units ? l_u : 0);
+  int l_kt = lw.kb;
+  int l_stage = 0;
 #pragma unroll 1
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (l_q < total) {
-      load(s, l_tile, l_kt);
-      ++l_q;
-      if (++l_kt == KT) {
-        l_kt = 0;
-        l_tile += gridDim.x;
+    if (l_u < p.total_units) {
+      load(l_stage, lw.m0, lw.n0, l_kt);
+      if (++l_kt == lw.ke) {
+        l_u += gridDim.x;
+        if (l_u < p.total_units) {
+          lw = unit_of(l_u);
+          l_kt = lw.kb;
+        }
       }
     }
+    l_stage = (l_stage + 1 == STAGES) ? 0 : l_stage + 1;
     cp_async_commit();
   }
 
-  int c_tile = blockIdx.x, c_kt = 0;
+  int c_u = blockIdx.x;
+  Unit cw = unit_of(c_u < p.total_units ? c_u : 0);
+  int c_kt = cw.kb;
+  int st = 0;
 #pragma unroll 1
-  for (long long q = 0; q < total; ++q) {
+  while (c_u < p.total_units) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
-    if (l_q < total) {
-      load((int)(l_q % STAGES), l_tile, l_kt);
-      ++l_q;
-      if (++l_kt == KT) {
-        l_kt = 0;
-        l_tile += gridDim.x;
+    if (l_u < p.total_units) {
+      load(l_stage, lw.m0, lw.n0, l_kt);
+      if (++l_kt == lw.ke) {
+        l_u += gridDim.x;
+        if (l_u < p.total_units) {
+          lw = unit_of(l_u);
+          l_kt = lw.kb;
+        }
       }
     }
+    l_stage = (l_stage + 1 == STAGES) ? 0 : l_stage + 1;
     cp_async_commit();
 
-    const int st = (int)(q % STAGES);
     const double* as = As + st * A_ST;
     const double* bs = Bs + st * B_ST;
+    st = (st + 1 == STAGES) ? 0 : st + 1;
 #pragma unroll
     for (int kp = 0; kp < BK / 8; ++kp) {      // pairs of DMMA k-steps
       const int kb = kp * 8;
@@ -265,39 +290,81 @@ __global__ void __launch_bounds__(512, 1) dmma_gemm_v2_kernel(const GemmParamsV2
           for (int j = 0; j < NI; ++j) dmma_8x8x4_nv(acc[i][j], af[s][i], bf[s][j]);
     }
 
-    if (++c_kt == KT) {
-      // ---- epilogue of tile c_tile ------------------------------------------------------
-      const int tm = c_tile / p.tiles_n, tn = c_tile - tm * p.tiles_n;
-      const int m0 = tm * BM, n0 = tn * BN;
-      long long roff[MI];
-      bool rok[MI];
+    if (++c_kt == cw.ke) {
+      // ---- epilogue of unit c_u ---------------------------------------------------------
+      const int m0 = cw.m0, n0 = cw.n0;
+      if (p.dbg & 1) {
+        // skip stores (benchmark hook); keep the accumulators live
+        double sink = 0.0;
 #pragma unroll
-      for (int i = 0; i < MI; ++i) {
-        const int r = m0 + frag_row(i);
-        rok[i] = r < p.M;
-        roff[i] = rok[i] ? apply_map32(p.rowmap, (uint32_t)r) : 0;
-      }
+        for (int i = 0; i < MI; ++i)
 #pragma unroll
-      for (int j = 0; j < NI; ++j)
+          for (int j = 0; j < NI; ++j) sink += acc[i][j][0] + acc[i][j][1];
+        if (sink == 1.2345e-300) p.C[0] = sink;
+      } else if (p.ksplit == 1) {
+        long long roff[MI];
+        bool rok[MI];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int c = n0 + acc_col(j, 2 * t + h);
-          if (c < p.N) {
-            const long long co = apply_map32(p.colmap, (uint32_t)c);
+        for (int i = 0; i < MI; ++i) {
+          const int r = m0 + frag_row(i);
+          rok[i] = r < p.M;
+          roff[i] = rok[i] ? apply_map32(p.rowmap, (uint32_t)r) : 0;
+        }
 #pragma unroll
-            for (int i = 0; i < MI; ++i)
-              if (rok[i]) stg_cs(p.C + roff[i] + co, acc[i][j][h]);
+        for (int j = 0; j < NI; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c = n0 + acc_col(j, 2 * t + h);
+            if (c < p.N) {
+              const long long co = apply_map32(p.colmap, (uint32_t)c);
+#pragma unroll
+              for (int i = 0; i < MI; ++i)
+                if (rok[i]) stg_cs(p.C + roff[i] + co, acc[i][j][h]);
+            }
+          }
+      } else {
+        double* P = p.P + (long long)cw.split * p.M * p.N;
+#pragma unroll
+        for (int i = 0; i < MI; ++i) {
+          const int r = m0 + frag_row(i);
+          if (r < p.M) {
+#pragma unroll
+            for (int j = 0; j < NI; ++j)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int c = n0 + acc_col(j, 2 * t + h);
+                if (c < p.N) P[(long long)r * p.N + c] = acc[i][j][h];
+              }
           }
         }
+      }
 #pragma unroll
       for (int i = 0; i < MI; ++i)
 #pragma unroll
         for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-      c_kt = 0;
-      c_tile += gridDim.x;
+      c_u += gridDim.x;
+      if (c_u < p.total_units) {
+        cw = unit_of(c_u);
+        c_kt = cw.kb;
+      }
     }
   }
   cp_async_wait<0>();
+}
+
+// C[rowmap(m) + colmap(n)] = sum_s P[s][m][n]  (split-K reduction, fixed summation order)
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const double* __restrict__ P,
+                                                            double* __restrict__ C, int M, int N,
+                                                            int ksplit, IndexMap32 rowmap,
+                                                            IndexMap32 colmap) {
+  const long long MN = (long long)M * N;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < MN;
+       e += (long long)gridDim.x * blockDim.x) {
+    double s = P[e];
+    for (int q = 1; q < ksplit; ++q) s += P[q * MN + e];
+    const int m = (int)(e / N), n = (int)(e - (long long)m * N);
+    stg_cs(C + apply_map32(rowmap, (uint32_t)m) + apply_map32(colmap, (uint32_t)n), s);
+  }
 }
 
 }  // namespace tt

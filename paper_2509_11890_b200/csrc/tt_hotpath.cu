@@ -160,11 +160,25 @@ int num_sms() {
   return sms;
 }
 
-template <bool AK, bool BK_, int BN, int WM, int WN>
+thread_local int g_variant = -1;
+thread_local int g_dbg_flags = 0;   // tt_debug_set_flags   // test/benchmark hook (tt_debug_set_variant); -1 = auto
+
+// split-K scratch for the current stage (set by the stage planners; nullptr = no split)
+thread_local double* g_pscratch = nullptr;
+thread_local long long g_pscratch_elems = 0;
+
+constexpr int stages_for(size_t stage_bytes, size_t budget) {
+  return (int)(budget / stage_bytes) > 4 ? 4 : (int)(budget / stage_bytes);
+}
+
+template <bool AK, bool BK_, int BM, int BN, int WM, int WN, int MINB>
 cudaError_t launch_v2_cfg(const GemmParams& p0, cudaStream_t s) {
-  constexpr int ST = 4;
-  using Cfg = tt::GemmV2Cfg<AK, BK_, BN, WM, WN, ST>;
-  auto kern = tt::dmma_gemm_v2_kernel<AK, BK_, BN, WM, WN, ST>;
+  using Probe = tt::GemmV2Cfg<AK, BK_, BM, BN, WM, WN, 1, MINB>;
+  constexpr size_t budget = MINB == 1 ? 220 * 1024 : 110 * 1024;
+  constexpr int ST = stages_for(Probe::kSmemBytes, budget);
+  static_assert(ST >= 2, "shared memory budget");
+  using Cfg = tt::GemmV2Cfg<AK, BK_, BM, BN, WM, WN, ST, MINB>;
+  auto kern = tt::dmma_gemm_v2_kernel<AK, BK_, BM, BN, WM, WN, ST, MINB>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
@@ -176,6 +190,8 @@ cudaError_t launch_v2_cfg(const GemmParams& p0, cudaStream_t s) {
   p.A = p0.A;
   p.B = p0.B;
   p.C = p0.C;
+  p.P = nullptr;
+  p.dbg = g_dbg_flags;
   p.M = (int)p0.M;
   p.N = (int)p0.N;
   p.K = (int)p0.K;
@@ -183,14 +199,43 @@ cudaError_t launch_v2_cfg(const GemmParams& p0, cudaStream_t s) {
   p.ldb = p0.ldb;
   p.rowmap = tt::to_map32(p0.rowmap);
   p.colmap = tt::to_map32(p0.colmap);
-  const long long tm = (p0.M + Cfg::BM - 1) / Cfg::BM;
+  const long long tm = (p0.M + BM - 1) / BM;
   const long long tn = (p0.N + BN - 1) / BN;
+  const long long tiles = tm * tn;
   p.tiles_n = (int)tn;
-  p.total_tiles = (int)(tm * tn);
   p.KT = (int)((p0.K + Cfg::BK - 1) / Cfg::BK);
-  const int grid = (int)std::min<long long>(tm * tn, num_sms());
-  const long long tr = trace_begin(BN, p0.M, p0.N, p0.K, s);
+  // split-K when the tile count quantises badly onto the persistent CTAs (e.g. the
+  // matvec's last stage: 512 tiles on 148 SMs = 3.46 waves) and K is long enough
+  const long long slots = (long long)num_sms() * MINB;
+  int ks = 1;
+  double best = 0.0;
+  for (int cand = 1; cand <= 4; ++cand) {
+    if (cand > 1 && (p.KT / cand < 24 || g_pscratch == nullptr ||
+                     (long long)cand * p0.M * p0.N > g_pscratch_elems))
+      break;
+    const long long units = tiles * cand;
+    const long long waves = (units + slots - 1) / slots;
+    const double eff = (double)units / (double)(waves * slots) * (cand == 1 ? 1.0 : 0.97);
+    if (eff > best + 1e-9) {
+      best = eff;
+      ks = cand;
+    }
+  }
+  p.ksplit = ks;
+  p.kt_per_split = (p.KT + ks - 1) / ks;
+  p.total_units = (int)(tiles * ks);
+  if (ks > 1) p.P = g_pscratch;
+  const int grid = (int)std::min<long long>((long long)p.total_units, slots);
+  const long long tr = trace_begin(BN + 1000 * ks, p0.M, p0.N, p0.K, s);
   kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes, s>>>(p);
+  if (ks > 1) {
+    const long long mn = p0.M * p0.N;
+    long long blocks = (mn + 255) / 256;
+    if (blocks > 8L * num_sms()) blocks = 8L * num_sms();
+    tt::splitk_reduce_kernel<<<(unsigned)blocks, 256, 0, s>>>(p.P, p.C, p.M, p.N, ks, p.rowmap,
+                                                              p.colmap);
+    ++g_launches;
+  }
   trace_end(tr, s);
   ++g_launches;
   return cudaGetLastError();
@@ -198,12 +243,23 @@ cudaError_t launch_v2_cfg(const GemmParams& p0, cudaStream_t s) {
 
 template <bool AK, bool BK_>
 cudaError_t launch_v2_l(const GemmParams& p, cudaStream_t s) {
-  if (p.N <= 16) return launch_v2_cfg<AK, BK_, 16, 16, 1>(p, s);
-  if (p.N <= 40) return launch_v2_cfg<AK, BK_, 40, 16, 1>(p, s);
-  if (p.N <= 64) return launch_v2_cfg<AK, BK_, 64, 8, 2>(p, s);
-  if (p.N <= 104) return launch_v2_cfg<AK, BK_, 104, 16, 1>(p, s);
-  if (p.N <= 144) return launch_v2_cfg<AK, BK_, 144, 8, 2>(p, s);
-  return launch_v2_cfg<AK, BK_, 128, 4, 4>(p, s);
+  const int v = g_variant < 0 ? 1 : g_variant;
+  if (v == 0) {   // one 512-thread CTA per SM, BM = 128
+    if (p.N <= 16) return launch_v2_cfg<AK, BK_, 128, 16, 16, 1, 1>(p, s);
+    if (p.N <= 40) return launch_v2_cfg<AK, BK_, 128, 40, 16, 1, 1>(p, s);
+    if (p.N <= 64) return launch_v2_cfg<AK, BK_, 128, 64, 8, 2, 1>(p, s);
+    if (p.N <= 104) return launch_v2_cfg<AK, BK_, 128, 104, 16, 1, 1>(p, s);
+    if (p.N <= 144) return launch_v2_cfg<AK, BK_, 128, 144, 8, 2, 1>(p, s);
+    return launch_v2_cfg<AK, BK_, 128, 128, 4, 4, 1>(p, s);
+  }
+  // two 256-thread CTAs per SM (independent barriers: one CTA's epilogue and pipeline
+  // bubbles overlap the other's DMMA stream)
+  if (p.N <= 16) return launch_v2_cfg<AK, BK_, 64, 16, 8, 1, 2>(p, s);
+  if (p.N <= 40) return launch_v2_cfg<AK, BK_, 64, 40, 8, 1, 2>(p, s);
+  if (p.N <= 64) return launch_v2_cfg<AK, BK_, 64, 64, 4, 2, 2>(p, s);
+  if (p.N <= 104) return launch_v2_cfg<AK, BK_, 64, 104, 8, 1, 2>(p, s);
+  if (p.N <= 144) return launch_v2_cfg<AK, BK_, 64, 144, 4, 2, 2>(p, s);
+  return launch_v2_cfg<AK, BK_, 128, 64, 4, 2, 2>(p, s);
 }
 
 bool aligned16(const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; }
@@ -377,18 +433,31 @@ struct Dims {
 bool dims_valid(const Dims& d) { return d.a > 0 && d.n > 0 && d.b > 0 && d.al > 0 && d.be > 0; }
 
 // element counts of the matvec workspace buffers (K columns)
-bool matvec_ws_elems(const Dims& d, long long K, long long& t1, long long& t2, long long& ah) {
+bool matvec_ws_elems(const Dims& d, long long K, long long& t1, long long& t2, long long& ah,
+                     long long& pe) {
   bool ok = true;
   t1 = prod({d.a, d.al, d.n, K, d.b}, ok);
   t2 = prod({d.a, d.n, K, d.be, d.b}, ok);
   ah = prod({d.al, d.n, d.n, d.be}, ok);
+  pe = prod({4, d.a, d.n, K, d.b}, ok);   // split-K partials of the last stage
   return ok;
 }
+
+struct SplitScratch {   // scopes the split-K scratch to one stage launch
+  SplitScratch(double* p, long long n) {
+    g_pscratch = p;
+    g_pscratch_elems = n;
+  }
+  ~SplitScratch() {
+    g_pscratch = nullptr;
+    g_pscratch_elems = 0;
+  }
+};
 
 // Local matvec (K columns, Block-TT layout) — stages S1, S2^T, S3.
 cudaError_t enqueue_matvec(const Dims& d, long long K, const double* phiL, const double* A,
                            const double* phiR, const double* X, double* Y, double* T1,
-                           double* T2, double* Ah, cudaStream_t s) {
+                           double* T2, double* Ah, double* P, long long pe, cudaStream_t s) {
   const long long a = d.a, b = d.b, al = d.al, be = d.be, N = d.n;
   cudaError_t e;
   if ((e = launch_perm(true, A, Ah, al, N, be, s)) != cudaSuccess) return e;
@@ -408,6 +477,7 @@ cudaError_t enqueue_matvec(const Dims& d, long long K, const double* phiL, const
   if (e != cudaSuccess) return e;
   // S3: Y(a', i, m, b') = T2[(a' m i), (be b)] . phiR[b', (be b)]^T
   g_stage = TT_ST_MV_S3;
+  SplitScratch scratch(P, pe);
   e = launch_gemm(true, true,
                   gp(T2, be * b, phiR, be * b, Y, a * K * N, b, be * b,
                      tt::map3(N, K, K * b, b, N * K * b), tt::map_plain(1)),
@@ -415,8 +485,9 @@ cudaError_t enqueue_matvec(const Dims& d, long long K, const double* phiL, const
   return e;
 }
 
-bool iface_ws_elems(const Dims& d, long long& t1, long long& t2, long long& ah) {
+bool iface_ws_elems(const Dims& d, long long& t1, long long& t2, long long& ah, long long& pe) {
   bool ok = true;
+  pe = std::max(prod({4, d.b, d.be, d.b}, ok), prod({4, d.a, d.al, d.a}, ok));
   t1 = prod({d.a, d.al, d.n, d.b}, ok);
   long long t1r = prod({d.a, d.n, d.b, d.be}, ok);
   if (t1r > t1) t1 = t1r;
@@ -429,7 +500,8 @@ bool iface_ws_elems(const Dims& d, long long& t1, long long& t2, long long& ah) 
 
 // Left interface: S1, S2^T (K = 1), S3': phiL_next[b', (be b)] = x^T[b', (a' i)] . T2[(a' i), (be b)]
 cudaError_t enqueue_left(const Dims& d, const double* phiL, const double* A, const double* x,
-                         double* out, double* T1, double* T2, double* Ah, cudaStream_t s) {
+                         double* out, double* T1, double* T2, double* Ah, double* P,
+                         long long pe, cudaStream_t s) {
   const long long a = d.a, b = d.b, al = d.al, be = d.be, N = d.n;
   cudaError_t e;
   if ((e = launch_perm(true, A, Ah, al, N, be, s)) != cudaSuccess) return e;
@@ -446,6 +518,7 @@ cudaError_t enqueue_left(const Dims& d, const double* phiL, const double* A, con
                   s);
   if (e != cudaSuccess) return e;
   g_stage = TT_ST_IL_S3;
+  SplitScratch scratch(P, pe);
   return launch_gemm(false, false,
                      gp(x, b, T2, be * b, out, b, be * b, a * N, tt::map_plain(be * b),
                         tt::map_plain(1)),
@@ -456,7 +529,8 @@ cudaError_t enqueue_left(const Dims& d, const double* phiL, const double* A, con
 //                  S2'': T2(i, b', al, a) = T1^T[(a b'), (j be)] . Atil[(j be), (al i)]
 //                  S3'': phiR_prev[a', (al a)] = x[a', (i b')] . T2[(i b'), (al a)]
 cudaError_t enqueue_right(const Dims& d, const double* phiR, const double* A, const double* x,
-                          double* out, double* T1, double* T2, double* At, cudaStream_t s) {
+                          double* out, double* T1, double* T2, double* At, double* P,
+                          long long pe, cudaStream_t s) {
   const long long a = d.a, b = d.b, al = d.al, be = d.be, N = d.n;
   cudaError_t e;
   if ((e = launch_perm(false, A, At, al, N, be, s)) != cudaSuccess) return e;
@@ -473,6 +547,7 @@ cudaError_t enqueue_right(const Dims& d, const double* phiR, const double* A, co
                   s);
   if (e != cudaSuccess) return e;
   g_stage = TT_ST_IR_S3;
+  SplitScratch scratch(P, pe);
   return launch_gemm(true, false,
                      gp(x, N * b, T2, al * a, out, a, al * a, N * b, tt::map_plain(al * a),
                         tt::map_plain(1)),
@@ -529,13 +604,15 @@ const char* tt_last_error_message(void) { return g_msg.c_str(); }
 const char* tt_version(void) { return "tt_hotpath 0.1 (sm_100a, FP64 DMMA)"; }
 int64_t tt_last_launch_count(void) { return g_launches_last; }
 void tt_debug_force_v1(int on) { g_force_v1 = on; }
+void tt_debug_set_variant(int v) { g_variant = v; }
+void tt_debug_set_flags(int f) { g_dbg_flags = f; }
 
 size_t tt_local_matvec_workspace_size(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t Rr,
                                       int64_t nvec) {
   Dims d{rl, n, rr, Rl, Rr};
-  long long t1, t2, ah;
-  if (!dims_valid(d) || nvec <= 0 || !matvec_ws_elems(d, nvec, t1, t2, ah)) return 0;
-  return ws_bytes({t1, t2, ah});
+  long long t1, t2, ah, pe;
+  if (!dims_valid(d) || nvec <= 0 || !matvec_ws_elems(d, nvec, t1, t2, ah, pe)) return 0;
+  return ws_bytes({t1, t2, ah, pe});
 }
 
 tt_status tt_local_matvec_batched(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t Rr,
@@ -550,9 +627,9 @@ tt_status tt_local_matvec_batched(int64_t rl, int64_t n, int64_t rr, int64_t Rl,
   if (!phiL || !A || !phiR || !X || !Y) return fail(TT_ERR_NULL_POINTER, "NULL tensor pointer");
   if (same(Y, phiL) || same(Y, A) || same(Y, phiR) || same(Y, X))
     return fail(TT_ERR_ALIASING, "output Y aliases an input");
-  long long t1, t2, ah;
-  if (!matvec_ws_elems(d, nvec, t1, t2, ah)) return fail(TT_ERR_OVERFLOW, "workspace overflow");
-  const size_t need = ws_bytes({t1, t2, ah});
+  long long t1, t2, ah, pe;
+  if (!matvec_ws_elems(d, nvec, t1, t2, ah, pe)) return fail(TT_ERR_OVERFLOW, "workspace overflow");
+  const size_t need = ws_bytes({t1, t2, ah, pe});
   if (!workspace || workspace_bytes < need)
     return fail(TT_ERR_WORKSPACE, "workspace NULL or smaller than " + std::to_string(need) + " bytes");
   if (same(workspace, Y) || same(workspace, X) || same(workspace, phiL) || same(workspace, phiR) ||
@@ -562,8 +639,9 @@ tt_status tt_local_matvec_batched(int64_t rl, int64_t n, int64_t rr, int64_t Rl,
   double* T1 = c.take(t1);
   double* T2 = c.take(t2);
   double* Ah = c.take(ah);
+  double* Pp = c.take(pe);
   if (!c.ok) return fail(TT_ERR_WORKSPACE, "workspace too small after alignment");
-  cudaError_t e = enqueue_matvec(d, nvec, phiL, A, phiR, X, Y, T1, T2, Ah,
+  cudaError_t e = enqueue_matvec(d, nvec, phiL, A, phiR, X, Y, T1, T2, Ah, Pp, pe,
                                  static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "tt_local_matvec_batched");
   return TT_OK;
@@ -579,9 +657,9 @@ tt_status tt_local_matvec(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t
 
 size_t tt_interface_workspace_size(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t Rr) {
   Dims d{rl, n, rr, Rl, Rr};
-  long long t1, t2, ah;
-  if (!dims_valid(d) || !iface_ws_elems(d, t1, t2, ah)) return 0;
-  return ws_bytes({t1, t2, ah});
+  long long t1, t2, ah, pe;
+  if (!dims_valid(d) || !iface_ws_elems(d, t1, t2, ah, pe)) return 0;
+  return ws_bytes({t1, t2, ah, pe});
 }
 
 static tt_status iface_common(bool left, int64_t rl, int64_t n, int64_t rr, int64_t Rl,
@@ -594,9 +672,9 @@ static tt_status iface_common(bool left, int64_t rl, int64_t n, int64_t rr, int6
   if (!phi_in || !A || !x || !phi_out) return fail(TT_ERR_NULL_POINTER, "NULL tensor pointer");
   if (same(phi_out, phi_in) || same(phi_out, A) || same(phi_out, x))
     return fail(TT_ERR_ALIASING, "output interface aliases an input");
-  long long t1, t2, ah;
-  if (!iface_ws_elems(d, t1, t2, ah)) return fail(TT_ERR_OVERFLOW, "workspace overflow");
-  const size_t need = ws_bytes({t1, t2, ah});
+  long long t1, t2, ah, pe;
+  if (!iface_ws_elems(d, t1, t2, ah, pe)) return fail(TT_ERR_OVERFLOW, "workspace overflow");
+  const size_t need = ws_bytes({t1, t2, ah, pe});
   if (!workspace || workspace_bytes < need)
     return fail(TT_ERR_WORKSPACE, "workspace NULL or smaller than " + std::to_string(need) + " bytes");
   if (same(workspace, phi_out) || same(workspace, phi_in) || same(workspace, x) ||
@@ -606,10 +684,11 @@ static tt_status iface_common(bool left, int64_t rl, int64_t n, int64_t rr, int6
   double* T1 = c.take(t1);
   double* T2 = c.take(t2);
   double* Ah = c.take(ah);
+  double* Pp = c.take(pe);
   if (!c.ok) return fail(TT_ERR_WORKSPACE, "workspace too small after alignment");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  cudaError_t e = left ? enqueue_left(d, phi_in, A, x, phi_out, T1, T2, Ah, s)
-                       : enqueue_right(d, phi_in, A, x, phi_out, T1, T2, Ah, s);
+  cudaError_t e = left ? enqueue_left(d, phi_in, A, x, phi_out, T1, T2, Ah, Pp, pe, s)
+                       : enqueue_right(d, phi_in, A, x, phi_out, T1, T2, Ah, Pp, pe, s);
   if (e != cudaSuccess) return cuda_fail(e, left ? "tt_interface_left" : "tt_interface_right");
   return TT_OK;
 }
@@ -651,13 +730,13 @@ static size_t sweep_ws(int64_t d, const int64_t* n, const int64_t* r, const int6
   size_t best = 0;
   for (int64_t k = 0; k < d; ++k) {
     Dims dk{r[k], n[k], r[k + 1], R[k], R[k + 1]};
-    long long t1, t2, ah;
-    if (!iface_ws_elems(dk, t1, t2, ah)) return 0;
-    size_t s = ws_bytes({t1, t2, ah});
+    long long t1, t2, ah, pe;
+    if (!iface_ws_elems(dk, t1, t2, ah, pe)) return 0;
+    size_t s = ws_bytes({t1, t2, ah, pe});
     if (s > best) best = s;
     if (nvec > 0) {
-      if (!matvec_ws_elems(dk, nvec, t1, t2, ah)) return 0;
-      s = ws_bytes({t1, t2, ah});
+      if (!matvec_ws_elems(dk, nvec, t1, t2, ah, pe)) return 0;
+      s = ws_bytes({t1, t2, ah, pe});
       if (s > best) best = s;
     }
   }
@@ -681,14 +760,15 @@ static cudaError_t sweep_left_step(int64_t k, const int64_t* n, const int64_t* r
                                    const double* const* Ac, double* const* phiL, void* ws,
                                    size_t wsb, cudaStream_t s) {
   Dims dk{r[k], n[k], r[k + 1], R[k], R[k + 1]};
-  long long t1, t2, ah;
-  iface_ws_elems(dk, t1, t2, ah);
+  long long t1, t2, ah, pe;
+  iface_ws_elems(dk, t1, t2, ah, pe);
   Carver c{static_cast<char*>(ws), wsb};
   double* T1 = c.take(t1);
   double* T2 = c.take(t2);
   double* Ah = c.take(ah);
+  double* Pp = c.take(pe);
   if (!c.ok) return cudaErrorInvalidValue;
-  return enqueue_left(dk, phiL[k], Ac[k], xc[k], phiL[k + 1], T1, T2, Ah, s);
+  return enqueue_left(dk, phiL[k], Ac[k], xc[k], phiL[k + 1], T1, T2, Ah, Pp, pe, s);
 }
 
 static cudaError_t sweep_right_step(int64_t k, const int64_t* n, const int64_t* r,
@@ -696,14 +776,15 @@ static cudaError_t sweep_right_step(int64_t k, const int64_t* n, const int64_t* 
                                     const double* const* Ac, double* const* phiR, void* ws,
                                     size_t wsb, cudaStream_t s) {
   Dims dk{r[k], n[k], r[k + 1], R[k], R[k + 1]};
-  long long t1, t2, ah;
-  iface_ws_elems(dk, t1, t2, ah);
+  long long t1, t2, ah, pe;
+  iface_ws_elems(dk, t1, t2, ah, pe);
   Carver c{static_cast<char*>(ws), wsb};
   double* T1 = c.take(t1);
   double* T2 = c.take(t2);
   double* Ah = c.take(ah);
+  double* Pp = c.take(pe);
   if (!c.ok) return cudaErrorInvalidValue;
-  return enqueue_right(dk, phiR[k + 1], Ac[k], xc[k], phiR[k], T1, T2, Ah, s);
+  return enqueue_right(dk, phiR[k + 1], Ac[k], xc[k], phiR[k], T1, T2, Ah, Pp, pe, s);
 }
 
 static cudaError_t sweep_matvec_step(int64_t k, const int64_t* n, const int64_t* r,
@@ -712,14 +793,15 @@ static cudaError_t sweep_matvec_step(int64_t k, const int64_t* n, const int64_t*
                                      double* const* phiL, double* const* phiR, void* ws,
                                      size_t wsb, cudaStream_t s) {
   Dims dk{r[k], n[k], r[k + 1], R[k], R[k + 1]};
-  long long t1, t2, ah;
-  matvec_ws_elems(dk, nvec, t1, t2, ah);
+  long long t1, t2, ah, pe;
+  matvec_ws_elems(dk, nvec, t1, t2, ah, pe);
   Carver c{static_cast<char*>(ws), wsb};
   double* T1 = c.take(t1);
   double* T2 = c.take(t2);
   double* Ah = c.take(ah);
+  double* Pp = c.take(pe);
   if (!c.ok) return cudaErrorInvalidValue;
-  return enqueue_matvec(dk, nvec, phiL[k], Ac[k], phiR[k + 1], Xb[k], Yb[k], T1, T2, Ah, s);
+  return enqueue_matvec(dk, nvec, phiL[k], Ac[k], phiR[k + 1], Xb[k], Yb[k], T1, T2, Ah, Pp, pe, s);
 }
 
 static tt_status check_ptrs(int64_t d, const void* const* arr, int64_t count, const char* what) {
