@@ -148,8 +148,8 @@ int64_t tt_last_launch_count(void);
 /* Test hook: on != 0 routes every GEMM stage of the calling thread through the generic
  * (unaligned-capable) kernel instead of the persistent 16-byte-load kernel. */
 void tt_debug_force_v1(int on);
-/* Benchmark hook: GEMM tiling variant of the calling thread (-1 = default; 0 = one 512-thread
- * CTA per SM; 1 = two 256-thread CTAs per SM). */
+/* Benchmark hook: GEMM engine of the calling thread (-1 = default = 2; 0 = cp.async, one
+ * 512-thread CTA per SM; 1 = cp.async, two 256-thread CTAs per SM; 2 = TMA + mbarrier). */
 void tt_debug_set_variant(int v);
 /* Benchmark hook (results become WRONG): bit 0 skips the GEMM output stores, bit 1 skips the
  * operand loads, so the main loop / epilogue / load path can be timed in isolation. */

@@ -1,0 +1,342 @@
+// tt_gemm_v3.cuh — TMA + mbarrier FP64 DMMA GEMM for the TT contraction stages (sm_100a).
+//
+// Same contract as tt_gemm.cuh / tt_gemm_v2.cuh (C[m,n] = sum_k A[m,k] B[k,n] over plain 2-D
+// operand views, 3-level output index maps, optional split-K), with the operand path moved
+// to the Blackwell copy engine:
+//  * operand tiles arrive by TMA (cp.async.bulk.tensor.2d, SWIZZLE_128B, OOB zero-fill),
+//    issued by one thread; per-stage `full` mbarriers carry the transaction count, per-stage
+//    `empty` mbarriers collect one arrival per consumer warp.  There is no CTA-wide barrier
+//    in the main loop: each warp runs ahead as soon as its stage is full, so one warp's
+//    epilogue or fragment-load latency overlaps the other warps' DMMA stream.
+//  * two 256-thread CTAs per SM (4 warps per sub-partition), persistent over work units,
+//    the k-tile stream continuing across tiles.
+//  * fragment loads are 128-bit and bank-conflict-free under the 128-byte swizzle:
+//      K-contiguous tiles (rows of 16 doubles = 128 B): fragment row g <-> tile row
+//        8i + 4(g&1) + (g>>1), so the two rows a quarter-warp reads differ by 4 mod 8 and the
+//        XOR swizzle sends them to disjoint 64-byte halves; one LDS.128 = two DMMA k-steps
+//        (lane t <-> k = 2t + s).
+//      M/N-contiguous tiles (16-wide boxes of 16 k-rows): fragment pair (2p, 2p+1) <-> rows
+//        (16p+2g, 16p+2g+1); the quarter-warp's four k-rows 2t+s carry XOR keys 2t+s, so the
+//        eight 16-byte chunks are distinct.
+// Preconditions (host-checked; else tt_gemm_v2/v1): 16-byte aligned bases, even leading
+// dimensions, even contiguous extents, M/N-contiguous tile extents multiples of 16.
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "tt_gemm_v2.cuh"
+
+namespace tt {
+
+struct GemmParamsV3 {
+  double* C;
+  double* P;
+  int M, N, K;
+  IndexMap32 rowmap, colmap;
+  int tiles_n, total_units, KT, ksplit, kt_per_split;
+  int dbg;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <bool A_KC, bool B_KC, int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, int MINB>
+struct GemmV3Cfg {
+  static constexpr int BK = 16, kThreads = WARPS_M * WARPS_N * 32, kWarps = WARPS_M * WARPS_N;
+  static constexpr int WTM = BM / WARPS_M, WTN = BN / WARPS_N;
+  static_assert(WTM % 8 == 0 && WTN % 8 == 0, "warp tile multiple of 8");
+  static_assert(A_KC || BM % 16 == 0, "M-contiguous A needs 16-wide boxes");
+  static_assert(B_KC || BN % 16 == 0, "N-contiguous B needs 16-wide boxes");
+  static constexpr int MI = WTM / 8, NI = WTN / 8;
+  static constexpr int A_BYTES = BM * 128, B_BYTES = BN * 128;   // 16 doubles per row/column
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static_assert(A_BYTES % 1024 == 0 || BM % 8 == 0, "");
+  // +1024 alignment slack for the 128-byte swizzle atoms
+  static constexpr size_t kSmemBytes = (size_t)STAGES * STAGE_BYTES + 1024;
+};
+
+template <bool A_KC, bool B_KC, int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, int MINB>
+__global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, MINB)
+dmma_gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const GemmParamsV3 p) {
+  using Cfg = GemmV3Cfg<A_KC, B_KC, BM, BN, WARPS_M, WARPS_N, STAGES, MINB>;
+  constexpr int WTM = Cfg::WTM, WTN = Cfg::WTN, MI = Cfg::MI, NI = Cfg::NI;
+  constexpr int A_BYTES = Cfg::A_BYTES, STAGE_BYTES = Cfg::STAGE_BYTES;
+
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES];
+  // align to the 1 KB swizzle atom by integer offset so the compiler keeps the shared
+  // address space (generic pointer arithmetic would turn every LDS into a generic LD)
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp / WARPS_N, wn = warp % WARPS_N;
+  const int g = lane >> 2, t = lane & 3;
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], Cfg::kWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  auto unit_of = [&](int u, int& m0, int& n0, int& kb, int& ke, int& split) {
+    const int tile = u / p.ksplit;
+    split = u - tile * p.ksplit;
+    const int tm = tile / p.tiles_n;
+    m0 = tm * BM;
+    n0 = (tile - tm * p.tiles_n) * BN;
+    kb = split * p.kt_per_split;
+    ke = min(p.KT, kb + p.kt_per_split);
+  };
+
+  // ---- producer state (thread 0 only; kept in shared memory to spare registers) ---------
+  __shared__ int prod_state[7];   // u, m0, n0, kt, ke, split, q
+  if (tid == 0) {
+    int* ps = prod_state;
+    ps[0] = blockIdx.x;
+    ps[6] = 0;
+    if (ps[0] < p.total_units) unit_of(ps[0], ps[1], ps[2], ps[3], ps[4], ps[5]);
+  }
+  auto produce_one = [&]() {   // thread 0: issue the next k-tile of the stream, if any
+    int* ps = prod_state;
+    if (ps[0] >= p.total_units) return;
+    const uint32_t lq = (uint32_t)ps[6];
+    const int s = (int)(lq % STAGES);
+    if (lq >= (uint32_t)STAGES) mbar_wait(&empty_bar[s], ((lq / STAGES) - 1) & 1);
+    unsigned char* as = smem + s * STAGE_BYTES;
+    unsigned char* bs = as + A_BYTES;
+    const int k0 = ps[3] * Cfg::BK, m0 = ps[1], n0 = ps[2];
+    mbar_expect_tx(&full_bar[s], STAGE_BYTES);
+    if (!(p.dbg & 2)) {
+      if (A_KC) {
+        tma_load_2d(as, &tmA, k0, m0, &full_bar[s]);
+      } else {
+#pragma unroll
+        for (int b = 0; b < BM / 16; ++b) tma_load_2d(as + b * 2048, &tmA, m0 + 16 * b, k0, &full_bar[s]);
+      }
+      if (B_KC) {
+        tma_load_2d(bs, &tmB, k0, n0, &full_bar[s]);
+      } else {
+#pragma unroll
+        for (int b = 0; b < BN / 16; ++b) tma_load_2d(bs + b * 2048, &tmB, n0 + 16 * b, k0, &full_bar[s]);
+      }
+    } else {
+      // benchmark hook: no loads; complete the transaction count locally
+      asm volatile("mbarrier.complete_tx.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&full_bar[s])),
+                   "r"((uint32_t)STAGE_BYTES)
+                   : "memory");
+    }
+    ps[6] = (int)(lq + 1);
+    if (++ps[3] == ps[4]) {
+      ps[0] += gridDim.x;
+      if (ps[0] < p.total_units) unit_of(ps[0], ps[1], ps[2], ps[3], ps[4], ps[5]);
+    }
+  };
+  if (tid == 0) {
+    for (int s = 0; s < STAGES - 1; ++s) produce_one();
+  }
+
+  // ---- fragment geometry ---------------------------------------------------------------
+  auto frag_row = [&](int i) -> int {   // tile row of fragment i, lane group g
+    if (A_KC) return wm * WTM + i * 8 + 4 * (g & 1) + (g >> 1);
+    if ((MI & 1) && i == MI - 1) return wm * WTM + (i >> 1) * 16 + g;
+    return wm * WTM + (i >> 1) * 16 + 2 * g + (i & 1);
+  };
+  auto acc_col = [&](int j, int c) -> int {   // tile column of accumulator column c of fragment j
+    if (B_KC) return wn * WTN + j * 8 + 4 * (c & 1) + (c >> 1);
+    if ((NI & 1) && j == NI - 1) return wn * WTN + (j >> 1) * 16 + c;
+    return wn * WTN + (j >> 1) * 16 + 2 * c + (j & 1);
+  };
+  // ---- per-lane shared-memory byte offsets (loop invariant) ------------------------------
+  // K-contiguous tile, rows R0 + 8i + Rg (Rg = 4(g&1) + (g>>1)), k = kb + 2t:
+  //   off = (R0 + Rg)*128 + ((t ^ Rg) << 4) + i*1024, and the kb = 8 half is off ^ 64.
+  const int Rg = 4 * (g & 1) + (g >> 1);
+  const int a_kc = (wm * WTM + Rg) * 128 + ((t ^ Rg) << 4);
+  const int b_kc = (wn * WTN + Rg) * 128 + ((t ^ Rg) << 4);
+  // M/N-contiguous tile of 16-wide boxes, k-row kb + 2t + s2, column m:
+  //   off = (m >> 4)*2048 + (kb + 2t + s2)*128 + ((((m & 15) >> 1) ^ (2t + s2)) << 4) + (m & 1)*8
+  // pair p of a warp tile starting at column C0 uses m = C0 + 16p + 2g (-> + p*2048).
+  auto mn_off = [&](int m, int s2) -> int {
+    const int k = 2 * t + s2;
+    return (m >> 4) * 2048 + k * 128 + ((((m & 15) >> 1) ^ k) << 4) + (m & 1) * 8;
+  };
+  const int a_mn0 = mn_off(wm * WTM + 2 * g, 0), a_mn1 = mn_off(wm * WTM + 2 * g, 1);
+  const int b_mn0 = mn_off(wn * WTN + 2 * g, 0), b_mn1 = mn_off(wn * WTN + 2 * g, 1);
+  const int a_lo0 = mn_off(wm * WTM + (MI / 2) * 16 + g, 0), a_lo1 = mn_off(wm * WTM + (MI / 2) * 16 + g, 1);
+  const int b_lo0 = mn_off(wn * WTN + (NI / 2) * 16 + g, 0), b_lo1 = mn_off(wn * WTN + (NI / 2) * 16 + g, 1);
+
+  double acc[MI][NI][2];
+#pragma unroll
+  for (int i = 0; i < MI; ++i)
+#pragma unroll
+    for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  int c_u = blockIdx.x, c_m0 = 0, c_n0 = 0, c_kt = 0, c_ke = 0, c_split = 0;
+  if (c_u < p.total_units) unit_of(c_u, c_m0, c_n0, c_kt, c_ke, c_split);
+  uint32_t q = 0;
+#pragma unroll 1
+  while (c_u < p.total_units) {
+    const int s = (int)(q % STAGES);
+    mbar_wait(&full_bar[s], (q / STAGES) & 1);
+    const unsigned char* as = smem + s * STAGE_BYTES;
+    const unsigned char* bs = as + A_BYTES;
+#pragma unroll
+    for (int kp = 0; kp < 2; ++kp) {   // two pairs of DMMA k-steps per 16-deep k-tile
+      // K-contiguous operands: one LDS.128 yields both k-steps of the pair
+      double akc[A_KC ? 2 : 1][A_KC ? MI : 1], bkc[B_KC ? 2 : 1][B_KC ? NI : 1];
+      if (A_KC) {
+        const unsigned char* base = as + (kp ? (a_kc ^ 64) : a_kc);
+#pragma unroll
+        for (int i = 0; i < MI; ++i) {
+          const double2 v = *reinterpret_cast<const double2*>(base + i * 1024);
+          akc[0][i] = v.x;
+          akc[A_KC ? 1 : 0][i] = v.y;
+        }
+      }
+      if (B_KC) {
+        const unsigned char* base = bs + (kp ? (b_kc ^ 64) : b_kc);
+#pragma unroll
+        for (int j = 0; j < NI; ++j) {
+          const double2 v = *reinterpret_cast<const double2*>(base + j * 1024);
+          bkc[0][j] = v.x;
+          bkc[B_KC ? 1 : 0][j] = v.y;
+        }
+      }
+#pragma unroll
+      for (int s2 = 0; s2 < 2; ++s2) {
+        // M/N-contiguous operands: loaded per k-step (fewer live registers)
+        double af[MI], bf[NI];
+        if (A_KC) {
+#pragma unroll
+          for (int i = 0; i < MI; ++i) af[i] = akc[A_KC ? s2 : 0][i];
+        } else {
+          const unsigned char* base = as + (s2 ? a_mn1 : a_mn0) + kp * 1024;
+#pragma unroll
+          for (int pr = 0; pr < MI / 2; ++pr) {
+            const double2 v = *reinterpret_cast<const double2*>(base + pr * 2048);
+            af[2 * pr] = v.x;
+            af[2 * pr + 1] = v.y;
+          }
+          if (MI & 1) af[MI - 1] = *reinterpret_cast<const double*>(as + (s2 ? a_lo1 : a_lo0) + kp * 1024);
+        }
+        if (B_KC) {
+#pragma unroll
+          for (int j = 0; j < NI; ++j) bf[j] = bkc[B_KC ? s2 : 0][j];
+        } else {
+          const unsigned char* base = bs + (s2 ? b_mn1 : b_mn0) + kp * 1024;
+#pragma unroll
+          for (int q2 = 0; q2 < NI / 2; ++q2) {
+            const double2 v = *reinterpret_cast<const double2*>(base + q2 * 2048);
+            bf[2 * q2] = v.x;
+            bf[2 * q2 + 1] = v.y;
+          }
+          if (NI & 1) bf[NI - 1] = *reinterpret_cast<const double*>(bs + (s2 ? b_lo1 : b_lo0) + kp * 1024);
+        }
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+          for (int j = 0; j < NI; ++j) dmma_8x8x4_nv(acc[i][j], af[i], bf[j]);
+      }
+    }
+    // release the stage (one arrival per warp), then thread 0 refills the stream
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[s]);
+    if (tid == 0) produce_one();
+    __syncwarp();
+    ++q;
+
+    if (++c_kt == c_ke) {
+      // ---- epilogue of unit c_u (registers -> global) --------------------------------
+      if (p.dbg & 1) {
+        double sink = 0.0;
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+          for (int j = 0; j < NI; ++j) sink += acc[i][j][0] + acc[i][j][1];
+        if (sink == 1.2345e-300) p.C[0] = sink;
+      } else if (p.ksplit == 1) {
+        long long roff[MI];
+        bool rok[MI];
+#pragma unroll
+        for (int i = 0; i < MI; ++i) {
+          const int r = c_m0 + frag_row(i);
+          rok[i] = r < p.M;
+          roff[i] = rok[i] ? apply_map32(p.rowmap, (uint32_t)r) : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < NI; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c = c_n0 + acc_col(j, 2 * t + h);
+            if (c < p.N) {
+              const long long co = apply_map32(p.colmap, (uint32_t)c);
+#pragma unroll
+              for (int i = 0; i < MI; ++i)
+                if (rok[i]) stg_cs(p.C + roff[i] + co, acc[i][j][h]);
+            }
+          }
+      } else {
+        double* P = p.P + (long long)c_split * p.M * p.N;
+#pragma unroll
+        for (int i = 0; i < MI; ++i) {
+          const int r = c_m0 + frag_row(i);
+          if (r < p.M) {
+#pragma unroll
+            for (int j = 0; j < NI; ++j)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int c = c_n0 + acc_col(j, 2 * t + h);
+                if (c < p.N) P[(long long)r * p.N + c] = acc[i][j][h];
+              }
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      c_u += gridDim.x;
+      if (c_u < p.total_units) unit_of(c_u, c_m0, c_n0, c_kt, c_ke, c_split);
+    }
+  }
+  // drain: thread 0 may still owe nothing (every issued stage was consumed)
+}
+
+}  // namespace tt

@@ -21,6 +21,8 @@
 #include "../../include/tt_hotpath.h"
 #include "tt_gemm.cuh"
 #include "tt_gemm_v2.cuh"
+#include "tt_gemm_v3.cuh"
+#include <cudaTypedefs.h>
 
 using tt::GemmParams;
 using tt::IndexMap;
@@ -262,6 +264,120 @@ cudaError_t launch_v2_l(const GemmParams& p, cudaStream_t s) {
   return launch_v2_cfg<AK, BK_, 128, 64, 4, 2, 2>(p, s);
 }
 
+// ---- v3 (TMA + mbarrier pipeline) ---------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  });
+  return fn;
+}
+
+// 2-D FP64 tensor map of a plain view: inner extent `inner` (unit stride), outer extent
+// `outer` with stride `ld` doubles; box {16, box_outer}, 128-byte swizzle, zero OOB fill.
+bool make_map(CUtensorMap* m, const double* base, long long inner, long long outer, long long ld,
+              int box_outer) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 8)};
+  cuuint32_t box[2] = {16u, (cuuint32_t)box_outer};
+  cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <bool AK, bool BK_, int BM, int BN, int WM, int WN, int MINB>
+cudaError_t launch_v3_cfg(const GemmParams& p0, cudaStream_t s, bool& ok) {
+  using Probe = tt::GemmV3Cfg<AK, BK_, BM, BN, WM, WN, 1, MINB>;
+  constexpr size_t budget = (MINB == 1 ? 224 : 110) * 1024 - 1024;
+  constexpr int ST0 = (int)(budget / Probe::STAGE_BYTES);
+  constexpr int ST = ST0 > 6 ? 6 : ST0;
+  static_assert(ST >= 2, "shared memory budget");
+  using Cfg = tt::GemmV3Cfg<AK, BK_, BM, BN, WM, WN, ST, MINB>;
+  ok = false;
+  CUtensorMap ta, tb;
+  // A: K-contiguous -> inner K, outer M (box rows BM); M-contiguous -> inner M, outer K (box 16)
+  if (!(AK ? make_map(&ta, p0.A, p0.K, p0.M, p0.lda, BM) : make_map(&ta, p0.A, p0.M, p0.K, p0.lda, 16)))
+    return cudaSuccess;
+  if (!(BK_ ? make_map(&tb, p0.B, p0.K, p0.N, p0.ldb, BN) : make_map(&tb, p0.B, p0.N, p0.K, p0.ldb, 16)))
+    return cudaSuccess;
+  ok = true;
+  auto kern = tt::dmma_gemm_v3_kernel<AK, BK_, BM, BN, WM, WN, ST, MINB>;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] {
+    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)Cfg::kSmemBytes);
+  });
+  if (attr_err != cudaSuccess) return attr_err;
+  tt::GemmParamsV3 p;
+  p.C = p0.C;
+  p.P = nullptr;
+  p.dbg = g_dbg_flags;
+  p.M = (int)p0.M;
+  p.N = (int)p0.N;
+  p.K = (int)p0.K;
+  p.rowmap = tt::to_map32(p0.rowmap);
+  p.colmap = tt::to_map32(p0.colmap);
+  const long long tm = (p0.M + BM - 1) / BM;
+  const long long tn = (p0.N + BN - 1) / BN;
+  const long long tiles = tm * tn;
+  p.tiles_n = (int)tn;
+  p.KT = (int)((p0.K + Cfg::BK - 1) / Cfg::BK);
+  const long long slots = (long long)num_sms() * MINB;
+  int ks = 1;
+  double best = 0.0;
+  for (int cand = 1; cand <= 4; ++cand) {
+    if (cand > 1 && (p.KT / cand < 24 || g_pscratch == nullptr ||
+                     (long long)cand * p0.M * p0.N > g_pscratch_elems))
+      break;
+    const long long units = tiles * cand;
+    const long long waves = (units + slots - 1) / slots;
+    const double eff = (double)units / (double)(waves * slots) * (cand == 1 ? 1.0 : 0.97);
+    if (eff > best + 1e-9) {
+      best = eff;
+      ks = cand;
+    }
+  }
+  p.ksplit = ks;
+  p.kt_per_split = (p.KT + ks - 1) / ks;
+  p.total_units = (int)(tiles * ks);
+  if (ks > 1) p.P = g_pscratch;
+  const int grid = (int)std::min<long long>((long long)p.total_units, slots);
+  const long long tr = trace_begin(BN + 1000 * ks + 100000, p0.M, p0.N, p0.K, s);
+  kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes, s>>>(ta, tb, p);
+  if (ks > 1) {
+    const long long mn = p0.M * p0.N;
+    long long blocks = (mn + 255) / 256;
+    if (blocks > 8L * num_sms()) blocks = 8L * num_sms();
+    tt::splitk_reduce_kernel<<<(unsigned)blocks, 256, 0, s>>>(p.P, p.C, p.M, p.N, ks, p.rowmap,
+                                                              p.colmap);
+    ++g_launches;
+  }
+  trace_end(tr, s);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+template <bool AK, bool BK_>
+cudaError_t launch_v3_l(const GemmParams& p, cudaStream_t s, bool& ok) {
+  if (p.N <= 16) return launch_v3_cfg<AK, BK_, 64, 16, 8, 1, 2>(p, s, ok);
+  if (p.N <= 48) return launch_v3_cfg<AK, BK_, 64, 48, 8, 1, 2>(p, s, ok);
+  if (p.N <= 64) return launch_v3_cfg<AK, BK_, 64, 64, 4, 2, 2>(p, s, ok);
+  if (p.N <= 112) return launch_v3_cfg<AK, BK_, 64, 112, 8, 1, 2>(p, s, ok);
+  if (p.N <= 144) return launch_v3_cfg<AK, BK_, 64, 144, 4, 2, 2>(p, s, ok);
+  return launch_v3_cfg<AK, BK_, 128, 64, 4, 2, 2>(p, s, ok);
+}
+
 bool aligned16(const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; }
 
 // the v2 preconditions (tt_gemm_v2.cuh header)
@@ -279,6 +395,16 @@ thread_local int g_force_v1 = 0;   // test hook (tt_debug_force_v1)
 
 cudaError_t launch_gemm(bool a_kc, bool b_kc, const GemmParams& p, cudaStream_t s) {
   if (p.M <= 0 || p.N <= 0 || p.K <= 0) return cudaSuccess;
+  const int v = g_variant < 0 ? 2 : g_variant;
+  if (!g_force_v1 && v == 2 && v2_eligible(a_kc, b_kc, p)) {
+    bool ok = false;
+    cudaError_t e;
+    if (a_kc && b_kc) e = launch_v3_l<true, true>(p, s, ok);
+    else if (a_kc && !b_kc) e = launch_v3_l<true, false>(p, s, ok);
+    else if (!a_kc && b_kc) e = launch_v3_l<false, true>(p, s, ok);
+    else e = launch_v3_l<false, false>(p, s, ok);
+    if (ok || e != cudaSuccess) return e;
+  }
   if (!g_force_v1 && v2_eligible(a_kc, b_kc, p)) {
     if (a_kc && b_kc) return launch_v2_l<true, true>(p, s);
     if (a_kc && !b_kc) return launch_v2_l<true, false>(p, s);
