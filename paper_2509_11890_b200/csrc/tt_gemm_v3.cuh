@@ -35,8 +35,14 @@ struct GemmParamsV3 {
   int M, N, K;
   IndexMap32 rowmap, colmap;
   int tiles_n, total_units, KT, ksplit, kt_per_split;
+  int store_mode;   // 0 scalar; 1 column pairs (N-contiguous B, output contiguous along n);
+                    // 2 row pairs (M-contiguous A, output contiguous along m) -> 16-byte stores
   int dbg;
 };
+
+__device__ __forceinline__ void stg_cs2(double* p, double a, double b) {
+  asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};\n" ::"l"(p), "d"(a), "d"(b));
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -291,6 +297,76 @@ dmma_gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
 #pragma unroll
           for (int j = 0; j < NI; ++j) sink += acc[i][j][0] + acc[i][j][1];
         if (sink == 1.2345e-300) p.C[0] = sink;
+      } else if (p.ksplit == 1 && !B_KC && p.store_mode == 1) {
+        // fragments 2q and 2q+1 hold adjacent output columns: one 16-byte store per pair
+        long long roff[MI];
+        bool rok[MI];
+#pragma unroll
+        for (int i = 0; i < MI; ++i) {
+          const int r = c_m0 + frag_row(i);
+          rok[i] = r < p.M;
+          roff[i] = rok[i] ? apply_map32(p.rowmap, (uint32_t)r) : 0;
+        }
+#pragma unroll
+        for (int j = 0; j + 1 < NI; j += 2)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c = c_n0 + acc_col(j, 2 * t + h);
+            if (c < p.N) {
+              const long long co = apply_map32(p.colmap, (uint32_t)c);
+#pragma unroll
+              for (int i = 0; i < MI; ++i)
+                if (rok[i]) stg_cs2(p.C + roff[i] + co, acc[i][j][h], acc[i][j + 1][h]);
+            }
+          }
+        if (NI & 1) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c = c_n0 + acc_col(NI - 1, 2 * t + h);
+            if (c < p.N) {
+              const long long co = apply_map32(p.colmap, (uint32_t)c);
+#pragma unroll
+              for (int i = 0; i < MI; ++i)
+                if (rok[i]) stg_cs(p.C + roff[i] + co, acc[i][NI - 1][h]);
+            }
+          }
+        }
+      } else if (p.ksplit == 1 && !A_KC && p.store_mode == 2) {
+        // fragments 2p and 2p+1 hold adjacent output rows: one 16-byte store per pair
+        constexpr int MP = MI / 2;
+        long long rpo[MP > 0 ? MP : 1];
+        bool rpk[MP > 0 ? MP : 1];
+#pragma unroll
+        for (int ip = 0; ip < MP; ++ip) {
+          const int r = c_m0 + frag_row(2 * ip);
+          rpk[ip] = r < p.M;
+          rpo[ip] = rpk[ip] ? apply_map32(p.rowmap, (uint32_t)r) : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < NI; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c = c_n0 + acc_col(j, 2 * t + h);
+            if (c < p.N) {
+              const long long co = apply_map32(p.colmap, (uint32_t)c);
+#pragma unroll
+              for (int ip = 0; ip < MP; ++ip)
+                if (rpk[ip]) stg_cs2(p.C + rpo[ip] + co, acc[2 * ip][j][h], acc[2 * ip + 1][j][h]);
+            }
+          }
+        if (MI & 1) {
+          const int r = c_m0 + frag_row(MI - 1);
+          if (r < p.M) {
+            const long long ro = apply_map32(p.rowmap, (uint32_t)r);
+#pragma unroll
+            for (int j = 0; j < NI; ++j)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int c = c_n0 + acc_col(j, 2 * t + h);
+                if (c < p.N) stg_cs(p.C + ro + apply_map32(p.colmap, (uint32_t)c), acc[MI - 1][j][h]);
+              }
+          }
+        }
       } else if (p.ksplit == 1) {
         long long roff[MI];
         bool rok[MI];

@@ -295,6 +295,23 @@ bool make_map(CUtensorMap* m, const double* base, long long inner, long long out
   return r == CUDA_SUCCESS;
 }
 
+bool even_strides(const IndexMap& m) {
+  return ((m.s0 | m.s1 | m.s2) & 1) == 0;
+}
+// 16-byte epilogue stores (tt_gemm_v3.cuh store_mode): the output must be contiguous in
+// pairs along the paired fragment dimension, with every other offset even and C aligned.
+int store_mode(bool a_kc, bool b_kc, const GemmParams& p) {
+  if (reinterpret_cast<uintptr_t>(p.C) & 15) return 0;
+  const IndexMap &r = p.rowmap, &c = p.colmap;
+  if (!b_kc && c.s0 == 1 && (c.d0 & 1) == 0 && ((c.s1 | c.s2) & 1) == 0 && even_strides(r) &&
+      (p.N & 1) == 0)
+    return 1;
+  if (!a_kc && r.s0 == 1 && (r.d0 & 1) == 0 && ((r.s1 | r.s2) & 1) == 0 && even_strides(c) &&
+      (p.M & 1) == 0)
+    return 2;
+  return 0;
+}
+
 template <bool AK, bool BK_, int BM, int BN, int WM, int WN, int MINB>
 cudaError_t launch_v3_cfg(const GemmParams& p0, cudaStream_t s, bool& ok) {
   using Probe = tt::GemmV3Cfg<AK, BK_, BM, BN, WM, WN, 1, MINB>;
@@ -328,6 +345,8 @@ cudaError_t launch_v3_cfg(const GemmParams& p0, cudaStream_t s, bool& ok) {
   p.K = (int)p0.K;
   p.rowmap = tt::to_map32(p0.rowmap);
   p.colmap = tt::to_map32(p0.colmap);
+  p.store_mode = store_mode(AK, BK_, p0);
+  p.store_mode = store_mode(AK, BK_, p0);
   const long long tm = (p0.M + BM - 1) / BM;
   const long long tn = (p0.N + BN - 1) / BN;
   const long long tiles = tm * tn;
