@@ -552,6 +552,61 @@ __global__ void __launch_bounds__(256) apply_kernel(const double* __restrict__ x
   }
 }
 
+// H8, register-blocked: thread <-> one output column e = (b, beta) of the z rows; the thread
+// keeps x[a, :, b] for AB consecutive a in registers and walks (alpha, i), reading the nj
+// operator values A[alpha, i, :, beta] (L1-resident, coalesced across the warp's betas) once
+// per AB outputs.  Every warp store is 32 consecutive doubles of one z row (evict-first).
+template <int NJ, int AB>
+__global__ void __launch_bounds__(256) apply_reg_kernel(const double* __restrict__ x,
+                                                        const double* __restrict__ A,
+                                                        double* __restrict__ z, int rl, int ni,
+                                                        int rr, int Rl, int Rr, int az) {
+  const long long L = (long long)rr * Rr;
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= L) return;
+  const int b = (int)(e / Rr), be = (int)(e - (long long)b * Rr);
+  const int a0 = blockIdx.y * AB;
+  // operator bond indices [al0, al1): split over blockIdx.z when the core is small
+  const int al0 = blockIdx.z * az, al1 = min(Rl, al0 + az);
+  double xv[AB][NJ];
+#pragma unroll
+  for (int u = 0; u < AB; ++u)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+      xv[u][j] = (a0 + u < rl) ? __ldg(x + ((long long)(a0 + u) * NJ + j) * rr + b) : 0.0;
+  for (int al = al0; al < al1; ++al)
+  for (int i = 0; i < ni; ++i) {
+    double av[NJ];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) av[j] = __ldg(A + ((long long)(al * ni + i) * NJ + j) * Rr + be);
+#pragma unroll
+    for (int u = 0; u < AB; ++u) {
+      if (a0 + u < rl) {
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) s = fma(av[j], xv[u][j], s);
+        __stcs(z + (((long long)(a0 + u) * Rl + al) * ni + i) * L + e, s);
+      }
+    }
+  }
+}
+
+template <int NJ>
+cudaError_t launch_apply_reg(const double* x, const double* A, double* z, long long rl,
+                             long long ni, long long rr, long long Rl, long long Rr,
+                             cudaStream_t s) {
+  constexpr int AB = 4;
+  const long long L = rr * Rr;
+  const long long gx = (L + 255) / 256, gy = (rl + AB - 1) / AB;
+  // enough CTAs to fill the machine, but as many bond indices per thread as possible
+  long long az = (gx * gy * Rl) / 4096;
+  az = az < 1 ? 1 : (az > Rl ? Rl : az);
+  dim3 grid((unsigned)gx, (unsigned)gy, (unsigned)((Rl + az - 1) / az));
+  apply_reg_kernel<NJ, AB><<<grid, 256, 0, s>>>(x, A, z, (int)rl, (int)ni, (int)rr, (int)Rl,
+                                                (int)Rr, (int)az);
+  return cudaGetLastError();
+}
+
 // FP64 DMMA throughput probe: 8 independent accumulator chains per warp.
 __global__ void __launch_bounds__(256) dmma_probe_kernel(double* out, long long iters) {
   double c[8][2];
@@ -1122,12 +1177,23 @@ tt_status tt_operator_apply(int64_t d, const int64_t* n_row, const int64_t* n_co
     const long long blocks = r[k] * R[k];
     g_stage = TT_ST_APPLY;
     const long long tr = trace_begin(0, r[k] * R[k] * n_row[k] * r[k + 1] * R[k + 1], n_col[k], 0, s);
-    apply_kernel<<<(unsigned)blocks, 256, (size_t)smem, s>>>(
-        x_cores[k], A_cores[k], z_cores[k], (int)r[k], (int)n_row[k], (int)n_col[k],
-        (int)r[k + 1], (int)R[k], (int)R[k + 1]);
+    cudaError_t e = cudaSuccess;
+    const long long L = r[k + 1] * R[k + 1];
+    if (n_col[k] <= 4 && L >= 256 && (r[k] + 3) / 4 <= 65535 && R[k] <= 65535) {
+      switch (n_col[k]) {
+        case 1: e = launch_apply_reg<1>(x_cores[k], A_cores[k], z_cores[k], r[k], n_row[k], r[k + 1], R[k], R[k + 1], s); break;
+        case 2: e = launch_apply_reg<2>(x_cores[k], A_cores[k], z_cores[k], r[k], n_row[k], r[k + 1], R[k], R[k + 1], s); break;
+        case 3: e = launch_apply_reg<3>(x_cores[k], A_cores[k], z_cores[k], r[k], n_row[k], r[k + 1], R[k], R[k + 1], s); break;
+        default: e = launch_apply_reg<4>(x_cores[k], A_cores[k], z_cores[k], r[k], n_row[k], r[k + 1], R[k], R[k + 1], s); break;
+      }
+    } else {
+      apply_kernel<<<(unsigned)blocks, 256, (size_t)smem, s>>>(
+          x_cores[k], A_cores[k], z_cores[k], (int)r[k], (int)n_row[k], (int)n_col[k],
+          (int)r[k + 1], (int)R[k], (int)R[k + 1]);
+      e = cudaGetLastError();
+    }
     trace_end(tr, s);
     ++g_launches;
-    cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "tt_operator_apply");
   }
   return TT_OK;
