@@ -151,8 +151,9 @@ void tt_debug_force_v1(int on);
 /* Benchmark hook: GEMM engine of the calling thread (-1 = default = 2; 0 = cp.async, one
  * 512-thread CTA per SM; 1 = cp.async, two 256-thread CTAs per SM; 2 = TMA + mbarrier). */
 void tt_debug_set_variant(int v);
-/* Benchmark hook (results become WRONG): bit 0 skips the GEMM output stores, bit 1 skips the
- * operand loads, so the main loop / epilogue / load path can be timed in isolation. */
+/* Benchmark hooks: bit 0 skips the GEMM output stores and bit 1 the operand loads (results
+ * become WRONG; times the main loop / epilogue / load path in isolation); bit 3 computes the
+ * right interface update directly instead of as the mirrored left update (same result). */
 void tt_debug_set_flags(int flags);
 
 /* ---------------------------------------------------------------------------------------

@@ -488,6 +488,63 @@ __global__ void perm_right_kernel(const double* __restrict__ A, double* __restri
 
 __global__ void set_one_kernel(double* p) { *p = 1.0; }
 
+// xt[b, j, a] = x[a, j, b]: 32x32 shared-memory tiles per mode index j (coalesced both ways)
+__global__ void transpose_core_kernel(const double* __restrict__ x, double* __restrict__ xt,
+                                      int a_n, int n, int b_n) {
+  __shared__ double tile[32][33];
+  const int j = blockIdx.z;
+  const int a0 = blockIdx.y * 32, b0 = blockIdx.x * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int a = a0 + r, b = b0 + threadIdx.x;
+    if (a < a_n && b < b_n) tile[r][threadIdx.x] = x[((long long)a * n + j) * b_n + b];
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int b = b0 + r, a = a0 + threadIdx.x;
+    if (a < a_n && b < b_n) xt[((long long)b * n + j) * a_n + a] = tile[threadIdx.x][r];
+  }
+}
+
+// Per-core operand preparation for a sweep (one launch per core, reused by every stage
+// of every pass): Ahl[(al,j),(i,be)] = A[al,i,j,be] (matvec / left update),
+// Ahr[(be,j),(i,al)] = A[al,i,j,be] (mirrored right update), xt[b,j,a] = x[a,j,b].
+__global__ void prep_core_kernel(const double* __restrict__ A, const double* __restrict__ x,
+                                 double* __restrict__ Ahl, double* __restrict__ Ahr,
+                                 double* __restrict__ xt, long long al_n, long long n,
+                                 long long be_n, long long a_n, long long b_n) {
+  const long long tA = al_n * n * n * be_n, tx = a_n * n * b_n;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tA + tx;
+       e += (long long)gridDim.x * blockDim.x) {
+    if (e < tA) {
+      long long r = e;
+      const long long be = r % be_n; r /= be_n;
+      const long long j = r % n; r /= n;
+      const long long i = r % n;
+      const long long al = r / n;
+      const double v = A[e];
+      Ahl[(al * n + j) * (n * be_n) + i * be_n + be] = v;
+      Ahr[(be * n + j) * (n * al_n) + i * al_n + al] = v;
+    } else {
+      const long long f = e - tA;   // f = (a * n + j) * b_n + b
+      const long long b = f % b_n, r = f / b_n;
+      const long long j = r % n, a = r / n;
+      xt[(b * n + j) * a_n + a] = x[f];
+    }
+  }
+}
+
+// At[be, i, j, al] = A[al, i, j, be]  (operator core with its two bonds swapped)
+__global__ void swap_bonds_kernel(const double* __restrict__ A, double* __restrict__ At,
+                                  long long al_n, long long nn, long long be_n) {
+  const long long total = al_n * nn * be_n;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long be = e % be_n, r = e / be_n;
+    const long long ij = r % nn, al = r / nn;
+    At[(be * nn + ij) * al_n + al] = A[e];
+  }
+}
+
 cudaError_t launch_perm(bool left, const double* A, double* out, long long al, long long n,
                         long long be, cudaStream_t s) {
   const long long total = al * n * n * be;
@@ -657,10 +714,14 @@ struct SplitScratch {   // scopes the split-K scratch to one stage launch
 // Local matvec (K columns, Block-TT layout) — stages S1, S2^T, S3.
 cudaError_t enqueue_matvec(const Dims& d, long long K, const double* phiL, const double* A,
                            const double* phiR, const double* X, double* Y, double* T1,
-                           double* T2, double* Ah, double* P, long long pe, cudaStream_t s) {
+                           double* T2, double* Ah, double* P, long long pe, cudaStream_t s,
+                           const double* Ah_pre = nullptr) {
   const long long a = d.a, b = d.b, al = d.al, be = d.be, N = d.n;
   cudaError_t e;
-  if ((e = launch_perm(true, A, Ah, al, N, be, s)) != cudaSuccess) return e;
+  if (Ah_pre)
+    Ah = const_cast<double*>(Ah_pre);
+  else if ((e = launch_perm(true, A, Ah, al, N, be, s)) != cudaSuccess)
+    return e;
   // S1: T1(al, j, a', m, b) = phiL[(a' al), a] . X[a, (j m b)]
   g_stage = TT_ST_MV_S1;
   e = launch_gemm(true, false,
@@ -687,6 +748,7 @@ cudaError_t enqueue_matvec(const Dims& d, long long K, const double* phiL, const
 
 bool iface_ws_elems(const Dims& d, long long& t1, long long& t2, long long& ah, long long& pe) {
   bool ok = true;
+  // ah also holds the mirrored right update's swapped operator core and transposed core
   pe = std::max(prod({4, d.b, d.be, d.b}, ok), prod({4, d.a, d.al, d.a}, ok));
   t1 = prod({d.a, d.al, d.n, d.b}, ok);
   long long t1r = prod({d.a, d.n, d.b, d.be}, ok);
@@ -694,30 +756,34 @@ bool iface_ws_elems(const Dims& d, long long& t1, long long& t2, long long& ah, 
   t2 = prod({d.a, d.n, d.be, d.b}, ok);
   long long t2r = prod({d.a, d.al, d.n, d.b}, ok);
   if (t2r > t2) t2 = t2r;
-  ah = prod({d.al, d.n, d.n, d.be}, ok);
+  ah = prod({3, d.al, d.n, d.n, d.be}, ok) + prod({d.a, d.n, d.b}, ok);
   return ok;
 }
 
 // Left interface: S1, S2^T (K = 1), S3': phiL_next[b', (be b)] = x^T[b', (a' i)] . T2[(a' i), (be b)]
 cudaError_t enqueue_left(const Dims& d, const double* phiL, const double* A, const double* x,
                          double* out, double* T1, double* T2, double* Ah, double* P,
-                         long long pe, cudaStream_t s) {
+                         long long pe, cudaStream_t s, int tag_s1 = TT_ST_IL_S1,
+                         const double* Ah_pre = nullptr) {
   const long long a = d.a, b = d.b, al = d.al, be = d.be, N = d.n;
   cudaError_t e;
-  if ((e = launch_perm(true, A, Ah, al, N, be, s)) != cudaSuccess) return e;
-  g_stage = TT_ST_IL_S1;
+  if (Ah_pre)
+    Ah = const_cast<double*>(Ah_pre);
+  else if ((e = launch_perm(true, A, Ah, al, N, be, s)) != cudaSuccess)
+    return e;
+  g_stage = tag_s1;
   e = launch_gemm(true, false,
                   gp(phiL, a, x, N * b, T1, a * al, N * b, a, tt::map2(al, N * a * b, b),
                      tt::map2(b, 1, a * b)),
                   s);
   if (e != cudaSuccess) return e;
-  g_stage = TT_ST_IL_S2;
+  g_stage = tag_s1 + 1;
   e = launch_gemm(false, false,
                   gp(T1, a * b, Ah, N * be, T2, a * b, N * be, al * N, tt::map2(b, 1, N * be * b),
                      tt::map_plain(b)),
                   s);
   if (e != cudaSuccess) return e;
-  g_stage = TT_ST_IL_S3;
+  g_stage = tag_s1 + 2;
   SplitScratch scratch(P, pe);
   return launch_gemm(false, false,
                      gp(x, b, T2, be * b, out, b, be * b, a * N, tt::map_plain(be * b),
@@ -728,6 +794,50 @@ cudaError_t enqueue_left(const Dims& d, const double* phiL, const double* A, con
 // Right interface: S1'': T1(j, be, a, b') = x[(a j), b] . phiR[(b' be), b]^T
 //                  S2'': T2(i, b', al, a) = T1^T[(a b'), (j be)] . Atil[(j be), (al i)]
 //                  S3'': phiR_prev[a', (al a)] = x[a', (i b')] . T2[(i b'), (al a)]
+// Right interface as the mirror image of the left one: with
+// xt[b, j, a] = x[a, j, b] and At[be, i, j, al] = A[al, i, j, be],
+//   phiR_prev[a', al, a] = sum x[a',i,b'] A[al,i,j,be] phiR[b',be,b] x[a,j,b]
+//                        = (left update of phiR through At, xt)[a', al, a],
+// so the right update runs on the left update's stage kernels (their layouts give 16-byte
+// epilogue stores and M/N-contiguous TMA operands).  Ah holds [perm | At | xt].
+cudaError_t enqueue_right_mirror(const Dims& d, const double* phiR, const double* A,
+                                 const double* x, double* out, double* T1, double* T2,
+                                 double* Ah, double* P, long long pe, cudaStream_t s,
+                                 const double* Ahr_pre = nullptr, const double* xt_pre = nullptr) {
+  const long long a = d.a, b = d.b, al = d.al, be = d.be, N = d.n;
+  if (Ahr_pre && xt_pre) {
+    const Dims dm{b, N, a, be, al};
+    return enqueue_left(dm, phiR, nullptr, xt_pre, out, T1, T2, Ah, P, pe, s, TT_ST_IR_S1,
+                        Ahr_pre);
+  }
+  double* At = Ah + al * N * N * be;
+  double* xt = At + al * N * N * be;
+  {
+    const long long total = al * N * N * be;
+    long long blocks = (total + 255) / 256;
+    if (blocks > 4096) blocks = 4096;
+    g_stage = TT_ST_PERM;
+    const long long tr = trace_begin(0, total, 0, 0, s);
+    swap_bonds_kernel<<<(unsigned)blocks, 256, 0, s>>>(A, At, al, N * N, be);
+    trace_end(tr, s);
+    ++g_launches;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  {
+    dim3 grid((unsigned)((b + 31) / 32), (unsigned)((a + 31) / 32), (unsigned)N);
+    g_stage = TT_ST_PERM;
+    const long long tr = trace_begin(0, a * N * b, 0, 0, s);
+    transpose_core_kernel<<<grid, dim3(32, 8), 0, s>>>(x, xt, (int)a, (int)N, (int)b);
+    trace_end(tr, s);
+    ++g_launches;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  const Dims dm{b, N, a, be, al};
+  return enqueue_left(dm, phiR, At, xt, out, T1, T2, Ah, P, pe, s, TT_ST_IR_S1);
+}
+
 cudaError_t enqueue_right(const Dims& d, const double* phiR, const double* A, const double* x,
                           double* out, double* T1, double* T2, double* At, double* P,
                           long long pe, cudaStream_t s) {
@@ -888,7 +998,8 @@ static tt_status iface_common(bool left, int64_t rl, int64_t n, int64_t rr, int6
   if (!c.ok) return fail(TT_ERR_WORKSPACE, "workspace too small after alignment");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t e = left ? enqueue_left(d, phi_in, A, x, phi_out, T1, T2, Ah, Pp, pe, s)
-                       : enqueue_right(d, phi_in, A, x, phi_out, T1, T2, Ah, Pp, pe, s);
+                       : (g_dbg_flags & 8) ? enqueue_right(d, phi_in, A, x, phi_out, T1, T2, Ah, Pp, pe, s)
+                                            : enqueue_right_mirror(d, phi_in, A, x, phi_out, T1, T2, Ah, Pp, pe, s);
   if (e != cudaSuccess) return cuda_fail(e, left ? "tt_interface_left" : "tt_interface_right");
   return TT_OK;
 }
@@ -925,8 +1036,67 @@ static tt_status check_train(int64_t d, const int64_t* n, const int64_t* r, cons
   return TT_OK;
 }
 
+// Sweep workspace = [per-stage scratch (max over cores and stage kinds)] [prepared operands
+// of every core: Ahl, Ahr (alpha n^2 beta each), xt (r_k n r_{k+1})].
+static long long prep_elems(const Dims& d) {
+  return 2 * d.al * d.n * d.n * d.be + d.a * d.n * d.b;
+}
+static size_t sweep_step_ws(int64_t d, const int64_t* n, const int64_t* r, const int64_t* R,
+                            int64_t nvec);
 static size_t sweep_ws(int64_t d, const int64_t* n, const int64_t* r, const int64_t* R,
                        int64_t nvec) {
+  size_t base = sweep_step_ws(d, n, r, R, nvec);
+  if (base == 0) return 0;
+  for (int64_t k = 0; k < d; ++k) {
+    Dims dk{r[k], n[k], r[k + 1], R[k], R[k + 1]};
+    base += align_up(size_t(prep_elems(dk)) * sizeof(double), 256) + 256;
+  }
+  return base;
+}
+struct Prep {
+  const double *Ahl, *Ahr, *xt;
+};
+// pointers of core k's prepared operands inside the workspace
+static Prep prep_ptrs(int64_t k, int64_t d, const int64_t* n, const int64_t* r, const int64_t* R,
+                      int64_t nvec, void* ws) {
+  size_t off = sweep_step_ws(d, n, r, R, nvec);
+  char* base = static_cast<char*>(ws);
+  for (int64_t q = 0; q <= k; ++q) {
+    Dims dq{r[q], n[q], r[q + 1], R[q], R[q + 1]};
+    uintptr_t p = (reinterpret_cast<uintptr_t>(base) + off + 255) & ~uintptr_t(255);
+    if (q == k) {
+      const double* Ahl = reinterpret_cast<const double*>(p);
+      const double* Ahr = Ahl + dq.al * dq.n * dq.n * dq.be;
+      const double* xt = Ahr + dq.al * dq.n * dq.n * dq.be;
+      return Prep{Ahl, Ahr, xt};
+    }
+    off = (p - reinterpret_cast<uintptr_t>(base)) + size_t(prep_elems(dq)) * sizeof(double);
+  }
+  return Prep{nullptr, nullptr, nullptr};
+}
+static cudaError_t launch_prep(int64_t d, const int64_t* n, const int64_t* r, const int64_t* R,
+                               int64_t nvec, const double* const* xc, const double* const* Ac,
+                               void* ws, cudaStream_t s) {
+  for (int64_t k = 0; k < d; ++k) {
+    Dims dk{r[k], n[k], r[k + 1], R[k], R[k + 1]};
+    Prep pp = prep_ptrs(k, d, n, r, R, nvec, ws);
+    const long long total = prep_elems(dk);
+    long long blocks = (total + 255) / 256;
+    if (blocks > 2048) blocks = 2048;
+    g_stage = TT_ST_PERM;
+    const long long tr = trace_begin(0, total, 0, 0, s);
+    prep_core_kernel<<<(unsigned)blocks, 256, 0, s>>>(
+        Ac[k], xc[k], const_cast<double*>(pp.Ahl), const_cast<double*>(pp.Ahr),
+        const_cast<double*>(pp.xt), dk.al, dk.n, dk.be, dk.a, dk.b);
+    trace_end(tr, s);
+    ++g_launches;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+static size_t sweep_step_ws(int64_t d, const int64_t* n, const int64_t* r, const int64_t* R,
+                            int64_t nvec) {
   size_t best = 0;
   for (int64_t k = 0; k < d; ++k) {
     Dims dk{r[k], n[k], r[k + 1], R[k], R[k + 1]};
@@ -955,8 +1125,8 @@ size_t tt_sweep_als_workspace_size(int64_t d, const int64_t* n, const int64_t* r
 }
 
 // carve the workspace for core k (interface or matvec) and enqueue
-static cudaError_t sweep_left_step(int64_t k, const int64_t* n, const int64_t* r,
-                                   const int64_t* R, const double* const* xc,
+static cudaError_t sweep_left_step(int64_t k, int64_t d, int64_t nvec, const int64_t* n,
+                                   const int64_t* r, const int64_t* R, const double* const* xc,
                                    const double* const* Ac, double* const* phiL, void* ws,
                                    size_t wsb, cudaStream_t s) {
   Dims dk{r[k], n[k], r[k + 1], R[k], R[k + 1]};
@@ -968,11 +1138,13 @@ static cudaError_t sweep_left_step(int64_t k, const int64_t* n, const int64_t* r
   double* Ah = c.take(ah);
   double* Pp = c.take(pe);
   if (!c.ok) return cudaErrorInvalidValue;
-  return enqueue_left(dk, phiL[k], Ac[k], xc[k], phiL[k + 1], T1, T2, Ah, Pp, pe, s);
+  const Prep pp = prep_ptrs(k, d, n, r, R, nvec, ws);
+  return enqueue_left(dk, phiL[k], Ac[k], xc[k], phiL[k + 1], T1, T2, Ah, Pp, pe, s,
+                      TT_ST_IL_S1, pp.Ahl);
 }
 
-static cudaError_t sweep_right_step(int64_t k, const int64_t* n, const int64_t* r,
-                                    const int64_t* R, const double* const* xc,
+static cudaError_t sweep_right_step(int64_t k, int64_t d, int64_t nvec, const int64_t* n,
+                                    const int64_t* r, const int64_t* R, const double* const* xc,
                                     const double* const* Ac, double* const* phiR, void* ws,
                                     size_t wsb, cudaStream_t s) {
   Dims dk{r[k], n[k], r[k + 1], R[k], R[k + 1]};
@@ -984,10 +1156,13 @@ static cudaError_t sweep_right_step(int64_t k, const int64_t* n, const int64_t* 
   double* Ah = c.take(ah);
   double* Pp = c.take(pe);
   if (!c.ok) return cudaErrorInvalidValue;
-  return enqueue_right(dk, phiR[k + 1], Ac[k], xc[k], phiR[k], T1, T2, Ah, Pp, pe, s);
+  if (g_dbg_flags & 8) return enqueue_right(dk, phiR[k + 1], Ac[k], xc[k], phiR[k], T1, T2, Ah, Pp, pe, s);
+  const Prep pp = prep_ptrs(k, d, n, r, R, nvec, ws);
+  return enqueue_right_mirror(dk, phiR[k + 1], Ac[k], xc[k], phiR[k], T1, T2, Ah, Pp, pe, s,
+                              pp.Ahr, pp.xt);
 }
 
-static cudaError_t sweep_matvec_step(int64_t k, const int64_t* n, const int64_t* r,
+static cudaError_t sweep_matvec_step(int64_t k, int64_t d, const int64_t* n, const int64_t* r,
                                      const int64_t* R, int64_t nvec, const double* const* Ac,
                                      const double* const* Xb, double* const* Yb,
                                      double* const* phiL, double* const* phiR, void* ws,
@@ -1001,7 +1176,9 @@ static cudaError_t sweep_matvec_step(int64_t k, const int64_t* n, const int64_t*
   double* Ah = c.take(ah);
   double* Pp = c.take(pe);
   if (!c.ok) return cudaErrorInvalidValue;
-  return enqueue_matvec(dk, nvec, phiL[k], Ac[k], phiR[k + 1], Xb[k], Yb[k], T1, T2, Ah, Pp, pe, s);
+  const Prep pp = prep_ptrs(k, d, n, r, R, nvec, ws);
+  return enqueue_matvec(dk, nvec, phiL[k], Ac[k], phiR[k + 1], Xb[k], Yb[k], T1, T2, Ah, Pp, pe,
+                        s, pp.Ahl);
 }
 
 static tt_status check_ptrs(int64_t d, const void* const* arr, int64_t count, const char* what) {
@@ -1061,17 +1238,19 @@ tt_status tt_sweep_interfaces(int64_t d, const int64_t* n, const int64_t* r, con
     return fail(TT_ERR_WORKSPACE, "workspace NULL or smaller than " + std::to_string(need) + " bytes");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t e;
+  if ((doL || doR) && (e = launch_prep(d, n, r, R, 0, x_cores, A_cores, workspace, s)) != cudaSuccess)
+    return cuda_fail(e, "sweep prep");
   if (doL) {
     if ((e = launch_set_one(phiL[0], s)) != cudaSuccess) return cuda_fail(e, "sweep");
     for (int64_t k = 0; k < d; ++k)
-      if ((e = sweep_left_step(k, n, r, R, x_cores, A_cores, phiL, workspace, workspace_bytes, s)) !=
+      if ((e = sweep_left_step(k, d, 0, n, r, R, x_cores, A_cores, phiL, workspace, workspace_bytes, s)) !=
           cudaSuccess)
         return cuda_fail(e, "sweep left");
   }
   if (doR) {
     if ((e = launch_set_one(phiR[d], s)) != cudaSuccess) return cuda_fail(e, "sweep");
     for (int64_t k = d - 1; k >= 0; --k)
-      if ((e = sweep_right_step(k, n, r, R, x_cores, A_cores, phiR, workspace, workspace_bytes,
+      if ((e = sweep_right_step(k, d, 0, n, r, R, x_cores, A_cores, phiR, workspace, workspace_bytes,
                                 s)) != cudaSuccess)
         return cuda_fail(e, "sweep right");
   }
@@ -1106,27 +1285,29 @@ tt_status tt_sweep_als(int64_t d, const int64_t* n, const int64_t* r, const int6
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t e;
   double* const* Yb = Y_bwd ? Y_bwd : Y_fwd;
+  if ((e = launch_prep(d, n, r, R, nvec, x_cores, A_cores, workspace, s)) != cudaSuccess)
+    return cuda_fail(e, "als prep");
   if ((e = launch_set_one(phiL[0], s)) != cudaSuccess) return cuda_fail(e, "als");
   if ((e = launch_set_one(phiR[d], s)) != cudaSuccess) return cuda_fail(e, "als");
   for (int64_t k = d - 1; k >= 1; --k)
-    if ((e = sweep_right_step(k, n, r, R, x_cores, A_cores, phiR, workspace, workspace_bytes, s)) !=
+    if ((e = sweep_right_step(k, d, nvec, n, r, R, x_cores, A_cores, phiR, workspace, workspace_bytes, s)) !=
         cudaSuccess)
       return cuda_fail(e, "als initial right");
   for (int64_t k = 0; k < d; ++k) {
-    if ((e = sweep_matvec_step(k, n, r, R, nvec, A_cores, X_blocks, Y_fwd, phiL, phiR, workspace,
+    if ((e = sweep_matvec_step(k, d, n, r, R, nvec, A_cores, X_blocks, Y_fwd, phiL, phiR, workspace,
                                workspace_bytes, s)) != cudaSuccess)
       return cuda_fail(e, "als matvec L->R");
     if (k < d - 1 &&
-        (e = sweep_left_step(k, n, r, R, x_cores, A_cores, phiL, workspace, workspace_bytes, s)) !=
+        (e = sweep_left_step(k, d, nvec, n, r, R, x_cores, A_cores, phiL, workspace, workspace_bytes, s)) !=
             cudaSuccess)
       return cuda_fail(e, "als left");
   }
   for (int64_t k = d - 1; k >= 0; --k) {
-    if ((e = sweep_matvec_step(k, n, r, R, nvec, A_cores, X_blocks, Yb, phiL, phiR, workspace,
+    if ((e = sweep_matvec_step(k, d, n, r, R, nvec, A_cores, X_blocks, Yb, phiL, phiR, workspace,
                                workspace_bytes, s)) != cudaSuccess)
       return cuda_fail(e, "als matvec R->L");
     if (k > 0 &&
-        (e = sweep_right_step(k, n, r, R, x_cores, A_cores, phiR, workspace, workspace_bytes, s)) !=
+        (e = sweep_right_step(k, d, nvec, n, r, R, x_cores, A_cores, phiR, workspace, workspace_bytes, s)) !=
             cudaSuccess)
       return cuda_fail(e, "als right");
   }

@@ -57,17 +57,19 @@ def test_smoke():
 # ----------------------------------------------------------------------------------------
 # configs 1-4: full W34 workload (sweep both directions + one matvec per core) + apply
 # ----------------------------------------------------------------------------------------
-@pytest.mark.parametrize("idx,force_v1", [(1, False), (2, False), (3, False), (4, False),
-                                          (3, True), (4, True)])
-def test_config_w34_parity(tt, idx, force_v1):
-    """force_v1 routes every GEMM through the generic unaligned-capable kernel."""
-    import oracle
-    import ttgen
-    tt.tt_debug_force_v1(force_v1)
+@pytest.mark.parametrize("idx,engine", [(1, "default"), (2, "default"), (3, "default"),
+                                        (4, "default"), (3, "v1"), (4, "v1"), (3, "v2"),
+                                        (4, "v2")])
+def test_config_w34_parity(tt, idx, engine):
+    """engine: default = TMA/mbarrier kernel (v3) where eligible; v1 = the generic
+    unaligned-capable kernel for every GEMM; v2 = the cp.async persistent kernel."""
+    tt.tt_debug_force_v1(engine == "v1")
+    tt.tt_debug_set_variant(1 if engine == "v2" else -1)
     try:
         _w34(tt, idx)
     finally:
         tt.tt_debug_force_v1(False)
+        tt.tt_debug_set_variant(-1)
 
 
 def _w34(tt, idx):
@@ -140,8 +142,19 @@ def test_ragged_batched_matvec(tt, shape):
     assert rel(h(y0), ref[:, :, 0, :]) <= TOL
 
 
+@pytest.mark.parametrize("direct_right", [False, True])
 @pytest.mark.parametrize("shape", RAGGED)
-def test_ragged_interfaces(tt, shape):
+def test_ragged_interfaces(tt, shape, direct_right):
+    """direct_right: the right update computed directly (debug flag 8) instead of as the
+    mirrored left update; both must match the oracle."""
+    tt.tt_debug_set_flags(8 if direct_right else 0)
+    try:
+        _ragged_interfaces(tt, shape)
+    finally:
+        tt.tt_debug_set_flags(0)
+
+
+def _ragged_interfaces(tt, shape):
     import oracle
     rl, n, rr, Rl, Rr, _ = shape
     rng = np.random.default_rng(sum(shape) + 1)
