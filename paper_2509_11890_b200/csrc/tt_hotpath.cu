@@ -389,11 +389,26 @@ cudaError_t launch_v3_cfg(const GemmParams& p0, cudaStream_t s, bool& ok) {
 
 template <bool AK, bool BK_>
 cudaError_t launch_v3_l(const GemmParams& p, cudaStream_t s, bool& ok) {
+  if (g_variant == 4) {   // all two-CTA tiles (previous default), kept for comparison
+    if (p.N <= 16) return launch_v3_cfg<AK, BK_, 64, 16, 8, 1, 2>(p, s, ok);
+    if (p.N <= 48) return launch_v3_cfg<AK, BK_, 64, 48, 8, 1, 2>(p, s, ok);
+    if (p.N <= 64) return launch_v3_cfg<AK, BK_, 64, 64, 4, 2, 2>(p, s, ok);
+    if (p.N <= 112) return launch_v3_cfg<AK, BK_, 64, 112, 8, 1, 2>(p, s, ok);
+    if (p.N <= 144) return launch_v3_cfg<AK, BK_, 64, 144, 4, 2, 2>(p, s, ok);
+    return launch_v3_cfg<AK, BK_, 128, 64, 4, 2, 2>(p, s, ok);
+  }
+  // Measured per stage shape (tools/stage_probe.py, config-5 interior core):
+  //  * narrow N (the operator-core stage, N = n R <= 144): one 16-warp CTA per SM with a
+  //    128 x N tile and a 6-deep TMA ring (the streamed operand comes from HBM);
+  //  * wide N with a K-contiguous B (the last matvec stage): one 16-warp CTA per SM,
+  //    128 x 128 tiles (+ split-K), 95% of the DMMA peak;
+  //  * wide N with an N-contiguous B (the first stage): two 8-warp CTAs per SM, 128 x 64.
   if (p.N <= 16) return launch_v3_cfg<AK, BK_, 64, 16, 8, 1, 2>(p, s, ok);
   if (p.N <= 48) return launch_v3_cfg<AK, BK_, 64, 48, 8, 1, 2>(p, s, ok);
-  if (p.N <= 64) return launch_v3_cfg<AK, BK_, 64, 64, 4, 2, 2>(p, s, ok);
-  if (p.N <= 112) return launch_v3_cfg<AK, BK_, 64, 112, 8, 1, 2>(p, s, ok);
-  if (p.N <= 144) return launch_v3_cfg<AK, BK_, 64, 144, 4, 2, 2>(p, s, ok);
+  if (p.N <= 64) return launch_v3_cfg<AK, BK_, 128, 64, 8, 2, 1>(p, s, ok);
+  if (p.N <= 112) return launch_v3_cfg<AK, BK_, 128, 112, 8, 2, 1>(p, s, ok);
+  if (p.N <= 144) return launch_v3_cfg<AK, BK_, 128, 144, 8, 2, 1>(p, s, ok);
+  if (BK_) return launch_v3_cfg<AK, BK_, 128, 128, 4, 4, 1>(p, s, ok);
   return launch_v3_cfg<AK, BK_, 128, 64, 4, 2, 2>(p, s, ok);
 }
 
@@ -415,7 +430,7 @@ thread_local int g_force_v1 = 0;   // test hook (tt_debug_force_v1)
 cudaError_t launch_gemm(bool a_kc, bool b_kc, const GemmParams& p, cudaStream_t s) {
   if (p.M <= 0 || p.N <= 0 || p.K <= 0) return cudaSuccess;
   const int v = g_variant < 0 ? 2 : g_variant;
-  if (!g_force_v1 && v == 2 && v2_eligible(a_kc, b_kc, p)) {
+  if (!g_force_v1 && v >= 2 && v2_eligible(a_kc, b_kc, p)) {
     bool ok = false;
     cudaError_t e;
     if (a_kc && b_kc) e = launch_v3_l<true, true>(p, s, ok);
