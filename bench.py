@@ -68,6 +68,25 @@ def w5_work(cfg):
 
 
 # ----------------------------------------------------------------------------------------
+# multi-rank plumbing (replicas only: no collective on the data path)
+# ----------------------------------------------------------------------------------------
+def max_over_ranks(ms: float, device) -> float:
+    """Max of a per-rank device time over all ranks (timing plumbing; identity at N=1)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return ms
+    t = torch.tensor([ms], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def whole_job_rate(work_per_step: float, world: int, steps: int, max_ms: float) -> float:
+    """Whole-job throughput: all ranks' work / the slowest rank's time (GFLOP/s)."""
+    return work_per_step * world * steps / (max_ms * 1e-3) / 1e9
+
+
+# ----------------------------------------------------------------------------------------
 # clocks during the timed region
 # ----------------------------------------------------------------------------------------
 class ClockSampler:
@@ -308,13 +327,9 @@ def main():
     recs = [tt.tt_trace_read(i) for i in range(tt.tt_trace_count())]
     tt.tt_trace_disable()
 
-    total_ms = sum(step_ms)
-    if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = max_over_ranks(sum(step_ms), dev)
     ms_per_step = total_ms / args.steps
-    value = work["step_flops"] * world * args.steps / (total_ms * 1e-3) / 1e9
+    value = whole_job_rate(work["step_flops"], world, args.steps, total_ms)
 
     # ---- per-stage breakdown from the trace -----------------------------------------------
     stages = {}
@@ -414,12 +429,8 @@ def main():
         stream.wait_event(out_done[(args.steps - 1) % 2])
         e1.record(stream)
         torch.cuda.synchronize(dev)
-        e_ms = e0.elapsed_time(e1)
-        if world > 1:
-            t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e_ms = float(t.item())
-        e2e = {"value": work["step_flops"] * world * args.steps / (e_ms * 1e-3) / 1e9,
+        e_ms = max_over_ranks(e0.elapsed_time(e1), dev)
+        e2e = {"value": whole_job_rate(work["step_flops"], world, args.steps, e_ms),
                "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": e_ms / args.steps,
                "note": "H2D of x, A and the Krylov block and D2H of the Y blocks every step, "
