@@ -86,6 +86,45 @@ def whole_job_rate(work_per_step: float, world: int, steps: int, max_ms: float) 
     return work_per_step * world * steps / (max_ms * 1e-3) / 1e9
 
 
+def bench_w34_flops(cfg):
+    """W34 = (d-1) right + (d-1) left interface updates + one local matvec per core."""
+    d, N, r, R = cfg.d, cfg.N, cfg.r, cfg.R
+    f = [f_local(r[k], N, r[k + 1], R[k], R[k + 1]) for k in range(d)]
+    return sum(f[1:]) + sum(f[:-1]) + sum(f)
+
+
+def time_sweep(tt, fn, stream, dev, reps=5):
+    """Median/best device time of `fn` run eagerly and replayed from a captured CUDA graph."""
+    import torch
+    fn(stream)
+    torch.cuda.synchronize(dev)
+    eager = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn(stream)
+        e1.record(stream)
+        e1.synchronize()
+        eager.append(e0.elapsed_time(e1))
+    graph = torch.cuda.CUDAGraph()
+    cap = torch.cuda.Stream(dev)
+    cap.wait_stream(stream)
+    with torch.cuda.stream(cap):
+        with torch.cuda.graph(graph, stream=cap):
+            fn(cap)
+    torch.cuda.synchronize(dev)
+    graphed = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        graph.replay()
+        e1.record(stream)
+        e1.synchronize()
+        graphed.append(e0.elapsed_time(e1))
+    return {"eager_ms_median": statistics.median(eager), "eager_ms_best": min(eager),
+            "graph_ms_median": statistics.median(graphed), "graph_ms_best": min(graphed)}
+
+
 # ----------------------------------------------------------------------------------------
 # clocks during the timed region
 # ----------------------------------------------------------------------------------------
@@ -219,6 +258,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-apply", action="store_true", help="debug: skip H8 in the step")
+    ap.add_argument("--no-sweeps", action="store_true", help="skip the d=12 sweep timings")
     ap.add_argument("--verbose", action="store_true")
     ap.add_argument("--variant", type=int, default=-1, help="GEMM tiling variant (benchmark hook)")
     args = ap.parse_args()
@@ -436,6 +476,35 @@ def main():
                "note": "H2D of x, A and the Krylov block and D2H of the Y blocks every step, "
                        "double-buffered on two copy streams (overlapping compute)"}
 
+    # ---- full sweeps at d = 12 (metric's second half), eager and as a CUDA graph ---------
+    sweeps = None
+    if not args.no_sweeps:
+        sweeps = {}
+        # config 5, W5 (tt_sweep_als) without the apply: the timed step's sweep part
+        def w5(st):
+            tt.tt_sweep_als(xs, As, Xs, Yf, None, phiL, phiR, workspace=ws, stream=st)
+        sweeps["config5_W5"] = time_sweep(tt, w5, stream, dev, reps=3)
+        # config 4, W34: all right interfaces, all left interfaces, one matvec per core
+        inp4 = ttgen.make_inputs(4)
+        x4 = [torch.from_numpy(c).to(dev) for c in inp4.x]
+        A4 = [torch.from_numpy(c).to(dev) for c in inp4.A]
+        pl4 = tt.alloc_interfaces(x4, A4)
+        pr4 = tt.alloc_interfaces(x4, A4)
+        y4 = [torch.empty_like(c) for c in x4]
+        tr4 = tt._Train(x4, A4)
+        ws4 = torch.empty(tt.tt_sweep_workspace_size(tr4), dtype=torch.uint8, device=dev)
+        wsm4 = torch.empty(max(tt.tt_local_matvec_workspace_size(c.shape[0], c.shape[1], c.shape[2],
+                                                                 A.shape[0], A.shape[3], 1)
+                               for c, A in zip(x4, A4)), dtype=torch.uint8, device=dev)
+
+        def w34(st):
+            tt.tt_sweep_interfaces(x4, A4, pl4, pr4, workspace=ws4, stream=st)
+            for k in range(len(x4)):
+                tt.tt_local_matvec(pl4[k], A4[k], pr4[k + 1], x4[k], y4[k], workspace=wsm4,
+                                   stream=st)
+        sweeps["config4_W34"] = time_sweep(tt, w34, stream, dev, reps=20)
+        sweeps["config4_W34"]["gflop"] = bench_w34_flops(ttgen.CONFIGS[4]) / 1e9
+
     # ---- CPU oracle baseline (rank 0, N=1) ----------------------------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -464,6 +533,7 @@ def main():
             "e2e": e2e,
             "gpu_launches": gpu_launches,
             "clocks": clk,
+            "sweeps_d12": sweeps,
             "detail": {
                 "full_sweep_ms": (total_ms / args.steps) - (apply_detail["ms_per_step"]
                                                             if apply_detail else 0.0),
