@@ -353,18 +353,27 @@ cudaError_t launch_v3_cfg(const GemmParams& p0, cudaStream_t s, bool& ok) {
   p.tiles_n = (int)tn;
   p.KT = (int)((p0.K + Cfg::BK - 1) / Cfg::BK);
   const long long slots = (long long)num_sms() * MINB;
+  // Split-K choice from a small cost model: GEMM time = waves x (k-tiles per unit) x
+  // (k-tile time), plus the deterministic reduction (reads ks*M*N, writes M*N doubles).
+  // Big stages rarely split (only to fix wave quantisation); skinny ones (few output tiles,
+  // long K — e.g. config 4's last matvec stage, 4 tiles x 200 k-tiles) split up to 64 ways.
   int ks = 1;
-  double best = 0.0;
-  for (int cand = 1; cand <= 4; ++cand) {
-    if (cand > 1 && (p.KT / cand < 24 || g_pscratch == nullptr ||
-                     (long long)cand * p0.M * p0.N > g_pscratch_elems))
-      break;
-    const long long units = tiles * cand;
-    const long long waves = (units + slots - 1) / slots;
-    const double eff = (double)units / (double)(waves * slots) * (cand == 1 ? 1.0 : 0.97);
-    if (eff > best + 1e-9) {
-      best = eff;
-      ks = cand;
+  {
+    const double ktile_s = 2.0 * BM * BN * Cfg::BK / (37.0e12 / (double)slots);
+    double best_t = 1e30;
+    for (int cand = 1; cand <= 64; ++cand) {
+      if (cand > 1 && (p.KT < 4 * cand || g_pscratch == nullptr ||
+                       (long long)cand * p0.M * p0.N > g_pscratch_elems))
+        break;
+      const long long units = tiles * cand;
+      const long long waves = (units + slots - 1) / slots;
+      const long long kper = (p.KT + cand - 1) / cand;
+      double t = (double)waves * (double)kper * ktile_s + 2.0e-6 * waves;
+      if (cand > 1) t += (double)(cand + 1) * p0.M * p0.N * 8.0 / 5.0e12 + 3.0e-6;
+      if (t < best_t * 0.98) {
+        best_t = t;
+        ks = cand;
+      }
     }
   }
   p.ksplit = ks;
@@ -405,6 +414,13 @@ cudaError_t launch_v3_l(const GemmParams& p, cudaStream_t s, bool& ok) {
   //  * wide N with an N-contiguous B (the first stage): two 8-warp CTAs per SM, 128 x 64.
   if (p.N <= 16) return launch_v3_cfg<AK, BK_, 64, 16, 8, 1, 2>(p, s, ok);
   if (p.N <= 48) return launch_v3_cfg<AK, BK_, 64, 48, 8, 1, 2>(p, s, ok);
+  // small problems: 64-row tiles on two CTAs per SM double the tile count
+  const bool small = (p.M + 127) / 128 < (long long)num_sms() && p.N <= 144;
+  if (small) {
+    if (p.N <= 64) return launch_v3_cfg<AK, BK_, 64, 64, 4, 2, 2>(p, s, ok);
+    if (p.N <= 112) return launch_v3_cfg<AK, BK_, 64, 112, 8, 1, 2>(p, s, ok);
+    return launch_v3_cfg<AK, BK_, 64, 144, 4, 2, 2>(p, s, ok);
+  }
   if (p.N <= 64) return launch_v3_cfg<AK, BK_, 128, 64, 8, 2, 1>(p, s, ok);
   if (p.N <= 112) return launch_v3_cfg<AK, BK_, 128, 112, 8, 2, 1>(p, s, ok);
   if (p.N <= 144) return launch_v3_cfg<AK, BK_, 128, 144, 8, 2, 1>(p, s, ok);
@@ -711,7 +727,11 @@ bool matvec_ws_elems(const Dims& d, long long K, long long& t1, long long& t2, l
   t1 = prod({d.a, d.al, d.n, K, d.b}, ok);
   t2 = prod({d.a, d.n, K, d.be, d.b}, ok);
   ah = prod({d.al, d.n, d.n, d.be}, ok);
-  pe = prod({4, d.a, d.n, K, d.b}, ok);   // split-K partials of the last stage
+  // split-K partials of the last stage: 4 slices, or up to 64 for small outputs (<= 128 MB)
+  {
+    const long long out = prod({d.a, d.n, K, d.b}, ok);
+    pe = std::max(4 * out, std::min(64 * out, 16LL << 20));
+  }
   return ok;
 }
 
@@ -764,7 +784,10 @@ cudaError_t enqueue_matvec(const Dims& d, long long K, const double* phiL, const
 bool iface_ws_elems(const Dims& d, long long& t1, long long& t2, long long& ah, long long& pe) {
   bool ok = true;
   // ah also holds the mirrored right update's swapped operator core and transposed core
-  pe = std::max(prod({4, d.b, d.be, d.b}, ok), prod({4, d.a, d.al, d.a}, ok));
+  {
+    const long long out = std::max(prod({d.b, d.be, d.b}, ok), prod({d.a, d.al, d.a}, ok));
+    pe = std::max(4 * out, std::min(64 * out, 16LL << 20));
+  }
   t1 = prod({d.a, d.al, d.n, d.b}, ok);
   long long t1r = prod({d.a, d.n, d.b, d.be}, ok);
   if (t1r > t1) t1 = t1r;
