@@ -44,6 +44,36 @@ thread_local std::vector<TraceRec> g_trace;
 thread_local std::vector<cudaEvent_t> g_trace_pool;
 thread_local int g_stage = TT_ST_PERM;   // stage tag of the next launch
 
+// ---- side stream for the sweeps' concurrent interface chains (per thread, per device) ------
+struct SideStream {
+  int dev = -1;
+  cudaStream_t s = nullptr;
+  cudaEvent_t ev[64] = {};
+  unsigned next = 0;
+};
+thread_local SideStream g_side;
+
+cudaError_t side_stream(cudaStream_t* out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (g_side.dev != dev) {
+    if ((e = cudaStreamCreateWithFlags(&g_side.s, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    for (auto& ev : g_side.ev)
+      if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return e;
+    g_side.dev = dev;
+  }
+  *out = g_side.s;
+  return cudaSuccess;
+}
+// `to` waits for all work enqueued on `from` so far (graph-capture compatible)
+cudaError_t stream_dep(cudaStream_t from, cudaStream_t to) {
+  cudaEvent_t ev = g_side.ev[g_side.next++ % 64];
+  cudaError_t e = cudaEventRecord(ev, from);
+  if (e != cudaSuccess) return e;
+  return cudaStreamWaitEvent(to, ev, 0);
+}
+
 long long trace_begin(int tile, long long M, long long N, long long K, cudaStream_t s) {
   if (!g_trace_on || 2 * (g_trace.size() + 1) > g_trace_pool.size()) return -1;
   TraceRec r;
@@ -1081,9 +1111,18 @@ static long long prep_elems(const Dims& d) {
 }
 static size_t sweep_step_ws(int64_t d, const int64_t* n, const int64_t* r, const int64_t* R,
                             int64_t nvec);
+// [main-stream scratch: max over cores of the interface / matvec stage scratch]
+// [side-stream scratch: max over cores of the interface stage scratch] [prepared operands]
+static size_t sweep_prep_offset(int64_t d, const int64_t* n, const int64_t* r, const int64_t* R,
+                                int64_t nvec) {
+  const size_t main_b = sweep_step_ws(d, n, r, R, nvec);
+  const size_t side_b = sweep_step_ws(d, n, r, R, 0);
+  if (main_b == 0 || side_b == 0) return 0;
+  return align_up(main_b, 256) + align_up(side_b, 256);
+}
 static size_t sweep_ws(int64_t d, const int64_t* n, const int64_t* r, const int64_t* R,
                        int64_t nvec) {
-  size_t base = sweep_step_ws(d, n, r, R, nvec);
+  size_t base = sweep_prep_offset(d, n, r, R, nvec);
   if (base == 0) return 0;
   for (int64_t k = 0; k < d; ++k) {
     Dims dk{r[k], n[k], r[k + 1], R[k], R[k + 1]};
@@ -1097,7 +1136,7 @@ struct Prep {
 // pointers of core k's prepared operands inside the workspace
 static Prep prep_ptrs(int64_t k, int64_t d, const int64_t* n, const int64_t* r, const int64_t* R,
                       int64_t nvec, void* ws) {
-  size_t off = sweep_step_ws(d, n, r, R, nvec);
+  size_t off = sweep_prep_offset(d, n, r, R, nvec);
   char* base = static_cast<char*>(ws);
   for (int64_t q = 0; q <= k; ++q) {
     Dims dq{r[q], n[q], r[q + 1], R[q], R[q + 1]};
@@ -1163,14 +1202,14 @@ size_t tt_sweep_als_workspace_size(int64_t d, const int64_t* n, const int64_t* r
 }
 
 // carve the workspace for core k (interface or matvec) and enqueue
-static cudaError_t sweep_left_step(int64_t k, int64_t d, int64_t nvec, const int64_t* n,
+static cudaError_t sweep_left_step(int64_t k, int64_t d, int64_t nvec, void* scratch, const int64_t* n,
                                    const int64_t* r, const int64_t* R, const double* const* xc,
                                    const double* const* Ac, double* const* phiL, void* ws,
                                    size_t wsb, cudaStream_t s) {
   Dims dk{r[k], n[k], r[k + 1], R[k], R[k + 1]};
   long long t1, t2, ah, pe;
   iface_ws_elems(dk, t1, t2, ah, pe);
-  Carver c{static_cast<char*>(ws), wsb};
+  Carver c{static_cast<char*>(scratch), wsb};
   double* T1 = c.take(t1);
   double* T2 = c.take(t2);
   double* Ah = c.take(ah);
@@ -1181,14 +1220,14 @@ static cudaError_t sweep_left_step(int64_t k, int64_t d, int64_t nvec, const int
                       TT_ST_IL_S1, pp.Ahl);
 }
 
-static cudaError_t sweep_right_step(int64_t k, int64_t d, int64_t nvec, const int64_t* n,
+static cudaError_t sweep_right_step(int64_t k, int64_t d, int64_t nvec, void* scratch, const int64_t* n,
                                     const int64_t* r, const int64_t* R, const double* const* xc,
                                     const double* const* Ac, double* const* phiR, void* ws,
                                     size_t wsb, cudaStream_t s) {
   Dims dk{r[k], n[k], r[k + 1], R[k], R[k + 1]};
   long long t1, t2, ah, pe;
   iface_ws_elems(dk, t1, t2, ah, pe);
-  Carver c{static_cast<char*>(ws), wsb};
+  Carver c{static_cast<char*>(scratch), wsb};
   double* T1 = c.take(t1);
   double* T2 = c.take(t2);
   double* Ah = c.take(ah);
@@ -1200,7 +1239,7 @@ static cudaError_t sweep_right_step(int64_t k, int64_t d, int64_t nvec, const in
                               pp.Ahr, pp.xt);
 }
 
-static cudaError_t sweep_matvec_step(int64_t k, int64_t d, const int64_t* n, const int64_t* r,
+static cudaError_t sweep_matvec_step(int64_t k, int64_t d, void* scratch, const int64_t* n, const int64_t* r,
                                      const int64_t* R, int64_t nvec, const double* const* Ac,
                                      const double* const* Xb, double* const* Yb,
                                      double* const* phiL, double* const* phiR, void* ws,
@@ -1208,7 +1247,7 @@ static cudaError_t sweep_matvec_step(int64_t k, int64_t d, const int64_t* n, con
   Dims dk{r[k], n[k], r[k + 1], R[k], R[k + 1]};
   long long t1, t2, ah, pe;
   matvec_ws_elems(dk, nvec, t1, t2, ah, pe);
-  Carver c{static_cast<char*>(ws), wsb};
+  Carver c{static_cast<char*>(scratch), wsb};
   double* T1 = c.take(t1);
   double* T2 = c.take(t2);
   double* Ah = c.take(ah);
@@ -1276,22 +1315,34 @@ tt_status tt_sweep_interfaces(int64_t d, const int64_t* n, const int64_t* r, con
     return fail(TT_ERR_WORKSPACE, "workspace NULL or smaller than " + std::to_string(need) + " bytes");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t e;
+  char* wsb = static_cast<char*>(workspace);
+  const size_t main_b = sweep_step_ws(d, n, r, R, 0);
+  void* ws_main = wsb;
+  void* ws_side = wsb + align_up(main_b, 256);
   if ((doL || doR) && (e = launch_prep(d, n, r, R, 0, x_cores, A_cores, workspace, s)) != cudaSuccess)
     return cuda_fail(e, "sweep prep");
+  // the two chains are independent: left on the caller's stream, right on the side stream
+  cudaStream_t sr = s;
+  if (doL && doR) {
+    if ((e = side_stream(&sr)) != cudaSuccess) return cuda_fail(e, "side stream");
+    if ((e = stream_dep(s, sr)) != cudaSuccess) return cuda_fail(e, "fork");
+  }
   if (doL) {
     if ((e = launch_set_one(phiL[0], s)) != cudaSuccess) return cuda_fail(e, "sweep");
     for (int64_t k = 0; k < d; ++k)
-      if ((e = sweep_left_step(k, d, 0, n, r, R, x_cores, A_cores, phiL, workspace, workspace_bytes, s)) !=
-          cudaSuccess)
+      if ((e = sweep_left_step(k, d, 0, ws_main, n, r, R, x_cores, A_cores, phiL, workspace,
+                               main_b, s)) != cudaSuccess)
         return cuda_fail(e, "sweep left");
   }
   if (doR) {
-    if ((e = launch_set_one(phiR[d], s)) != cudaSuccess) return cuda_fail(e, "sweep");
+    void* wr = (sr == s) ? ws_main : ws_side;
+    if ((e = launch_set_one(phiR[d], sr)) != cudaSuccess) return cuda_fail(e, "sweep");
     for (int64_t k = d - 1; k >= 0; --k)
-      if ((e = sweep_right_step(k, d, 0, n, r, R, x_cores, A_cores, phiR, workspace, workspace_bytes,
-                                s)) != cudaSuccess)
+      if ((e = sweep_right_step(k, d, 0, wr, n, r, R, x_cores, A_cores, phiR, workspace, main_b,
+                                sr)) != cudaSuccess)
         return cuda_fail(e, "sweep right");
   }
+  if (sr != s && (e = stream_dep(sr, s)) != cudaSuccess) return cuda_fail(e, "join");
   return TT_OK;
 }
 
@@ -1323,32 +1374,46 @@ tt_status tt_sweep_als(int64_t d, const int64_t* n, const int64_t* r, const int6
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t e;
   double* const* Yb = Y_bwd ? Y_bwd : Y_fwd;
+  char* wsb = static_cast<char*>(workspace);
+  const size_t main_b = sweep_step_ws(d, n, r, R, nvec);
+  const size_t side_b = sweep_step_ws(d, n, r, R, 0);
+  void* ws_main = wsb;
+  void* ws_side = wsb + align_up(main_b, 256);
+  cudaStream_t ss;
+  if ((e = side_stream(&ss)) != cudaSuccess) return cuda_fail(e, "side stream");
   if ((e = launch_prep(d, n, r, R, nvec, x_cores, A_cores, workspace, s)) != cudaSuccess)
     return cuda_fail(e, "als prep");
   if ((e = launch_set_one(phiL[0], s)) != cudaSuccess) return cuda_fail(e, "als");
   if ((e = launch_set_one(phiR[d], s)) != cudaSuccess) return cuda_fail(e, "als");
   for (int64_t k = d - 1; k >= 1; --k)
-    if ((e = sweep_right_step(k, d, nvec, n, r, R, x_cores, A_cores, phiR, workspace, workspace_bytes, s)) !=
-        cudaSuccess)
+    if ((e = sweep_right_step(k, d, nvec, ws_main, n, r, R, x_cores, A_cores, phiR, workspace,
+                              main_b, s)) != cudaSuccess)
       return cuda_fail(e, "als initial right");
+  // L->R: the left-interface chain runs on the side stream, one step ahead of the matvecs,
+  // which wait only for the interface they read (matvec(k) needs phiL[k] = IL(k-1)).
+  if ((e = stream_dep(s, ss)) != cudaSuccess) return cuda_fail(e, "fork");
   for (int64_t k = 0; k < d; ++k) {
-    if ((e = sweep_matvec_step(k, d, n, r, R, nvec, A_cores, X_blocks, Y_fwd, phiL, phiR, workspace,
-                               workspace_bytes, s)) != cudaSuccess)
+    if (k > 0 && (e = stream_dep(ss, s)) != cudaSuccess) return cuda_fail(e, "dep");
+    if ((e = sweep_matvec_step(k, d, ws_main, n, r, R, nvec, A_cores, X_blocks, Y_fwd, phiL, phiR,
+                               workspace, main_b, s)) != cudaSuccess)
       return cuda_fail(e, "als matvec L->R");
-    if (k < d - 1 &&
-        (e = sweep_left_step(k, d, nvec, n, r, R, x_cores, A_cores, phiL, workspace, workspace_bytes, s)) !=
-            cudaSuccess)
+    if (k < d - 1 && (e = sweep_left_step(k, d, nvec, ws_side, n, r, R, x_cores, A_cores, phiL,
+                                          workspace, side_b, ss)) != cudaSuccess)
       return cuda_fail(e, "als left");
   }
+  // R->L: the right chain recomputes phiR[k] (k = d-1..1) on the side stream; matvec(k)
+  // needs phiR[k+1] = IR(k+1).  Both streams first wait for the whole L->R pass.
+  if ((e = stream_dep(s, ss)) != cudaSuccess) return cuda_fail(e, "fork");
   for (int64_t k = d - 1; k >= 0; --k) {
-    if ((e = sweep_matvec_step(k, d, n, r, R, nvec, A_cores, X_blocks, Yb, phiL, phiR, workspace,
-                               workspace_bytes, s)) != cudaSuccess)
+    if (k < d - 1 && (e = stream_dep(ss, s)) != cudaSuccess) return cuda_fail(e, "dep");
+    if ((e = sweep_matvec_step(k, d, ws_main, n, r, R, nvec, A_cores, X_blocks, Yb, phiL, phiR,
+                               workspace, main_b, s)) != cudaSuccess)
       return cuda_fail(e, "als matvec R->L");
-    if (k > 0 &&
-        (e = sweep_right_step(k, d, nvec, n, r, R, x_cores, A_cores, phiR, workspace, workspace_bytes, s)) !=
-            cudaSuccess)
+    if (k > 0 && (e = sweep_right_step(k, d, nvec, ws_side, n, r, R, x_cores, A_cores, phiR,
+                                       workspace, side_b, ss)) != cudaSuccess)
       return cuda_fail(e, "als right");
   }
+  if ((e = stream_dep(ss, s)) != cudaSuccess) return cuda_fail(e, "join");
   return TT_OK;
 }
 
