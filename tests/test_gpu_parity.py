@@ -266,3 +266,96 @@ def test_workspace_too_small_enqueues_nothing(tt):
     assert bool((y == 7.0).all())
     with pytest.raises(TypeError):
         tt.tt_local_matvec(pl.cpu(), A, pr, x)
+
+
+# ----------------------------------------------------------------------------------------
+# more paths: small W5 sweeps, d = 1, rectangular apply, sweep graph capture, errors
+# ----------------------------------------------------------------------------------------
+@pytest.mark.parametrize("with_bwd", [True, False])
+def test_sweep_als_small_vs_oracle(tt, with_bwd):
+    """tt_sweep_als (W5) on config-3 shapes with a 3-column block, both passes vs oracle."""
+    import oracle
+    import ttgen
+    inp = ttgen.make_inputs(3)
+    d = inp.cfg.d
+    rng = np.random.default_rng(33)
+    X = ttgen.random_block(rng, inp.cfg.N, inp.cfg.r, 3)
+    xs, As, Xs = [g(c) for c in inp.x], [g(c) for c in inp.A], [g(c) for c in X]
+    Yb = [torch.empty_like(t) for t in Xs] if with_bwd else None
+    Yf, Yb, phiL, phiR = tt.tt_sweep_als(xs, As, Xs, Y_bwd=Yb)
+    torch.cuda.synchronize()
+    oL, oR = oracle.sweep_interfaces(inp.x, inp.A)
+    for k in range(1, d):
+        assert rel(h(phiL[k]), oL[k]) <= TOL and rel(h(phiR[k]), oR[k]) <= TOL
+    for k in range(d):
+        ref = oracle.local_matvec_batched(oL[k], inp.A[k], oR[k + 1], X[k])
+        assert rel(h(Yf[k]), ref) <= TOL
+        if with_bwd:
+            assert torch.equal(Yf[k], Yb[k])
+
+
+def test_single_core_train(tt):
+    """d = 1: the interfaces are the boundary values and phiL[1] = phiR[0] = x^T A x."""
+    import oracle
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((1, 6, 1))
+    A = rng.standard_normal((1, 6, 6, 1))
+    pl, pr = tt.tt_sweep_interfaces([g(x)], [g(A)])
+    oL, oR = oracle.sweep_interfaces([x], [A])
+    assert rel(h(pl[1]), oL[1]) <= TOL and rel(h(pr[0]), oR[0]) <= TOL
+    z = tt.tt_operator_apply([g(x)], [g(A)])
+    assert rel(h(z[0]), oracle.apply_core(x, A)) <= TOL
+
+
+@pytest.mark.parametrize("shapes,rs", [
+    ([(1, 5, 3, 2), (2, 2, 3, 4), (4, 4, 3, 1)], [1, 3, 9, 1]),       # small: shared-memory kernel
+    ([(1, 3, 3, 30), (30, 2, 3, 20), (20, 5, 3, 1)], [1, 16, 24, 1]),  # r R >= 256: register kernel
+])
+def test_rectangular_apply(tt, shapes, rs):
+    import oracle
+    rng = np.random.default_rng(71)
+    x = [rng.standard_normal((rs[k], shapes[k][2], rs[k + 1])) for k in range(3)]
+    A = [rng.standard_normal(s) for s in shapes]
+    z = tt.tt_operator_apply([g(c) for c in x], [g(c) for c in A])
+    for k in range(3):
+        assert rel(h(z[k]), oracle.apply_core(x[k], A[k])) <= TOL
+
+
+def test_sweep_als_graph_capture_equals_eager(tt):
+    """The W5 sweep forks a side stream internally; it must capture into one CUDA graph."""
+    import ttgen
+    inp = ttgen.make_inputs(3)
+    rng = np.random.default_rng(44)
+    X = ttgen.random_block(rng, inp.cfg.N, inp.cfg.r, 2)
+    xs, As, Xs = [g(c) for c in inp.x], [g(c) for c in inp.A], [g(c) for c in X]
+    Ye, _, pLe, pRe = tt.tt_sweep_als(xs, As, Xs)
+    torch.cuda.synchronize()
+    tr = tt._Train(xs, As)
+    ws = torch.empty(tt.tt_sweep_als_workspace_size(tr, 2), dtype=torch.uint8, device="cuda")
+    Yg = [torch.zeros_like(t) for t in Xs]
+    pLg, pRg = tt.alloc_interfaces(xs, As), tt.alloc_interfaces(xs, As)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(graph, stream=s):
+            tt.tt_sweep_als(xs, As, Xs, Yg, None, pLg, pRg, workspace=ws, stream=s)
+    graph.replay()
+    torch.cuda.synchronize()
+    for a, b in zip(Ye + pLe[:-1] + pRe[1:], Yg + pLg[:-1] + pRg[1:]):
+        assert torch.equal(a, b)
+
+
+def test_sweep_workspace_errors(tt):
+    import ttgen
+    inp = ttgen.make_inputs(1)
+    xs, As = [g(c) for c in inp.x], [g(c) for c in inp.A]
+    small = torch.empty(64, dtype=torch.uint8, device="cuda")
+    with pytest.raises(tt.TTError) as ei:
+        tt.tt_sweep_interfaces(xs, As, workspace=small)
+    assert ei.value.status == 4
+    with pytest.raises(tt.TTError) as ei:   # aliasing: output interface == input core
+        pl = tt.alloc_interfaces(xs, As)
+        pl[2] = xs[1]
+        tt.tt_sweep_interfaces(xs, As, phiL=pl, directions=tt.TT_SWEEP_LEFT)
+    assert ei.value.status in (3, 1)
