@@ -6,7 +6,7 @@ import sys
 from collections import OrderedDict
 
 
-def main(path, per_step=None):
+def main(path, per_step=None, skip=0):
     rows = []
     with open(path) as f:
         lines = [l for l in f if l.startswith('"')]
@@ -15,13 +15,13 @@ def main(path, per_step=None):
     ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
     for r in rd:
         name = r[ki]
-        if not re.search(r"dmma_gemm|apply_kernel|perm_|set_one|splitk", name):
+        if not re.search(r"dmma_gemm|apply_|perm_|set_one|splitk|prep_core|transpose_core|swap_bonds", name):
             continue
         v = float(r[vi].replace(",", ""))
         v = v / 1e6 if r[ui] == "ns" else (v / 1e3 if r[ui] == "us" else v)
         rows.append((name, v))
     if per_step:
-        rows = rows[-per_step:]
+        rows = rows[skip:skip + per_step] if skip else rows[-per_step:]
     agg = OrderedDict()
     for name, ms in rows:
         short = re.sub(r"\(.*", "", name)
@@ -36,4 +36,5 @@ def main(path, per_step=None):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else None)
+    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else None,
+         int(sys.argv[3]) if len(sys.argv) > 3 else 0)
