@@ -143,6 +143,28 @@ tt_status tt_operator_apply(int64_t d, const int64_t* n_row, const int64_t* n_co
                             const double* const* x_cores, const double* const* A_cores,
                             double* const* z_cores, void* stream);
 
+/* ---------------------------------------------------------------------------------------
+ * matrix-free local solve: restarted GMRES(m) on the projected local
+ * operator ("solve them in a matrix-free fashion via GMRES ... perform the
+ * constituent multiplications sequentially"), for nvec <= 64 independent right-hand sides:
+ *   (X_{!=k}^T A X_{!=k}) y_j = f_j,  F, X in the Block-TT layout (rl, n, nvec, rr).
+ * Every Arnoldi step is one batched local matvec (H4); orthogonalisation is classical
+ * Gram-Schmidt with one re-orthogonalisation pass; Givens rotations per column.  X holds
+ * the initial guess on entry and the iterate after `cycles` restart cycles of m steps on
+ * exit; a column whose Givens residual estimate |g_{i+1}| / ||f_j|| drops to <= tol is
+ * frozen.  rel_res (device, nvec doubles): final relative residual estimate per column;
+ * iters (device, nvec int64): Arnoldi steps taken per column.  Fully asynchronous (a fixed
+ * launch sequence; no host synchronisation), graph-capturable.
+ * Workspace: tt_local_gmres_workspace_size(...) (basis of m+1 Block-TT vectors + matvec).
+ * ------------------------------------------------------------------------------------- */
+size_t tt_local_gmres_workspace_size(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t Rr,
+                                     int64_t nvec, int64_t m);
+tt_status tt_local_gmres(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t Rr, int64_t nvec,
+                         int64_t m, int64_t cycles, double tol, const double* phiL,
+                         const double* A, const double* phiR, const double* F, double* X,
+                         double* rel_res, int64_t* iters, void* workspace,
+                         size_t workspace_bytes, void* stream);
+
 /* Number of kernel launches the last call on this thread enqueued. */
 int64_t tt_last_launch_count(void);
 /* Test hook: on != 0 routes every GEMM stage of the calling thread through the generic

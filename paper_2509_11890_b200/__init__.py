@@ -24,7 +24,7 @@ __all__ = [
     "tt_sweep_als", "tt_operator_apply", "tt_last_launch_count",
     "TT_SWEEP_LEFT", "TT_SWEEP_RIGHT", "TT_SWEEP_BOTH", "tt_trace_enable", "tt_trace_disable",
     "tt_trace_count", "tt_trace_read", "tt_fp64_peak_probe", "STAGE_NAMES", "tt_debug_force_v1",
-    "tt_debug_set_variant", "tt_debug_set_flags",
+    "tt_debug_set_variant", "tt_debug_set_flags", "tt_local_gmres", "tt_local_gmres_workspace_size",
 ]
 
 STAGE_NAMES = {0: "perm", 1: "set", 2: "mv_s1", 3: "mv_s2", 4: "mv_s3", 5: "il_s1", 6: "il_s2",
@@ -64,6 +64,10 @@ lib.tt_trace_enable.argtypes = [_i64]
 lib.tt_trace_count.restype = ctypes.c_int64
 lib.tt_trace_read.argtypes = [_i64] + [_p] * 6
 lib.tt_fp64_peak_probe.argtypes = [_i64, _p, _p]
+lib.tt_local_gmres_workspace_size.restype = _sz
+lib.tt_local_gmres_workspace_size.argtypes = [_i64] * 7
+lib.tt_local_gmres.argtypes = [_i64] * 8 + [ctypes.c_double] + [_p] * 7 + [_sz, _p]
+lib.tt_local_gmres.restype = ctypes.c_int
 lib.tt_debug_force_v1.argtypes = [ctypes.c_int]
 lib.tt_debug_force_v1.restype = None
 lib.tt_debug_set_variant.argtypes = [ctypes.c_int]
@@ -308,3 +312,30 @@ def tt_debug_set_variant(v: int) -> None:
 def tt_debug_set_flags(flags: int) -> None:
     """Benchmark hook (results become wrong): 1 = skip GEMM stores, 2 = skip operand loads."""
     lib.tt_debug_set_flags(int(flags))
+
+
+def tt_local_gmres_workspace_size(rl, n, rr, Rl, Rr, nvec, m) -> int:
+    return int(lib.tt_local_gmres_workspace_size(rl, n, rr, Rl, Rr, nvec, m))
+
+
+def tt_local_gmres(phiL, A, phiR, F, X=None, m=20, cycles=1, tol=0.0, rel_res=None, iters=None,
+                   workspace=None, stream=None):
+    """Restarted GMRES(m) on the projected local operator for every column of the Block-TT
+    right-hand side F (rl, n, nvec, rr).  X: initial guess (zeros if None),
+    overwritten with the iterate.  Returns (X, rel_res, iters) (device tensors)."""
+    rl, n, nvec, rr = F.shape
+    Rl, Rr = A.shape[0], A.shape[3]
+    if X is None:
+        X = torch.zeros_like(F)
+    if rel_res is None:
+        rel_res = torch.empty(nvec, dtype=torch.float64, device=F.device)
+    if iters is None:
+        iters = torch.empty(nvec, dtype=torch.int64, device=F.device)
+    ws = _ws(tt_local_gmres_workspace_size(rl, n, rr, Rl, Rr, nvec, m), workspace, F.device)
+    if iters.dtype != torch.int64 or not iters.is_cuda:
+        raise TypeError("iters must be a CUDA int64 tensor")
+    _check(lib.tt_local_gmres(rl, n, rr, Rl, Rr, nvec, m, cycles, float(tol), _dev(phiL, "phiL"),
+                              _dev(A, "A"), _dev(phiR, "phiR"), _dev(F, "F"), _dev(X, "X"),
+                              _dev(rel_res, "rel_res"), iters.data_ptr(), ws.data_ptr(),
+                              ws.numel(), _stream(stream)))
+    return X, rel_res, iters

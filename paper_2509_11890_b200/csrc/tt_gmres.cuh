@@ -1,0 +1,352 @@
+// tt_gmres.cuh — GPU-resident restarted GMRES(m) on the projected local operator
+// ("we can solve them in a matrix-free fashion via
+// GMRES ... perform the constituent multiplications sequentially").
+//
+// nvec independent right-hand sides (the columns of a Block-TT core, layout (rl,n,nvec,rr))
+// are solved in lock step: every Arnoldi step is ONE batched local matvec (the hot path,
+// enqueue_matvec) plus column-wise reductions.  Orthogonalisation is classical Gram-Schmidt
+// with one re-orthogonalisation pass (CGS2; equal in exact arithmetic to the modified
+// Gram-Schmidt of the textbook algorithm).  The Hessenberg least-squares problem of every column is updated by Givens
+// rotations in a one-thread-per-column kernel; converged columns are frozen by a device-side
+// flag, so the whole solve is a fixed sequence of launches (asynchronous, graph-capturable).
+// Included by tt_hotpath.cu inside its anonymous namespace.
+
+constexpr int kMaxL = 32;   // basis vectors per reduction pass
+
+// Column-segmented reduction: part[(l*K + j)*chunks + c] = sum over the rows of chunk c of
+// sum_b A_l[row, j, b] * B[row, j, b], for l < L (A_l = A + l*S).  Grid (chunks, K).
+__global__ void __launch_bounds__(256) colreduce_kernel(const double* __restrict__ A, long long S,
+                                                        int L, const double* __restrict__ B,
+                                                        long long rows, int K, int rr,
+                                                        long long rows_per_chunk,
+                                                        double* __restrict__ part) {
+  const int c = blockIdx.x, j = blockIdx.y, chunks = gridDim.x;
+  const long long r0 = c * rows_per_chunk;
+  const long long r1 = min(rows, r0 + rows_per_chunk);
+  double acc[kMaxL];
+#pragma unroll
+  for (int l = 0; l < kMaxL; ++l) acc[l] = 0.0;
+  const long long nel = (r1 - r0) * rr;
+  for (long long t = threadIdx.x; t < nel; t += blockDim.x) {
+    const long long row = r0 + t / rr;
+    const long long e = (row * K + j) * rr + (t % rr);
+    const double b = B[e];
+#pragma unroll
+    for (int l = 0; l < kMaxL; ++l)
+      if (l < L) acc[l] = fma(A[l * S + e], b, acc[l]);
+  }
+  __shared__ double red[8][kMaxL];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int l = 0; l < kMaxL; ++l) {
+    if (l < L) {
+      double v = acc[l];
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+      if (lane == 0) red[warp][l] = v;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < L) {
+    double v = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += red[w][threadIdx.x];
+    part[((long long)threadIdx.x * K + j) * chunks + c] = v;
+  }
+}
+
+// out[l*K + j] = sum_c part[(l*K + j)*chunks + c]   (fixed order: deterministic)
+__global__ void colreduce_finish_kernel(const double* __restrict__ part, int LK, int chunks,
+                                        double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= LK) return;
+  double v = 0.0;
+  for (int c = 0; c < chunks; ++c) v += part[(long long)i * chunks + c];
+  out[i] = v;
+}
+
+// B[e] += sign * sum_{l<L} coef[l*K + j(e)] * A_l[e]
+__global__ void __launch_bounds__(256) colaxpy_kernel(const double* __restrict__ A, long long S,
+                                                      int L, const double* __restrict__ coef,
+                                                      double sign, double* __restrict__ B,
+                                                      int K, int rr) {
+  __shared__ double cf[kMaxL * 64];
+  for (int i = threadIdx.x; i < L * K; i += blockDim.x) cf[i] = sign * coef[i];
+  __syncthreads();
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < S;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)((e / rr) % K);
+    double v = B[e];
+    for (int l = 0; l < L; ++l) v = fma(cf[l * K + j], A[l * S + e], v);
+    B[e] = v;
+  }
+}
+
+// dst[e] = src[e] * s[j(e)];  dst2 (optional) = src - dst2 (residual form: dst = F - W)
+__global__ void colscale_kernel(const double* __restrict__ src, const double* __restrict__ s,
+                                double* __restrict__ dst, long long S, int K, int rr) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < S;
+       e += (long long)gridDim.x * blockDim.x)
+    dst[e] = src[e] * s[(e / rr) % K];
+}
+__global__ void sub_kernel(const double* __restrict__ F, double* __restrict__ W, long long S) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < S;
+       e += (long long)gridDim.x * blockDim.x)
+    W[e] = F[e] - W[e];
+}
+
+// Per-column GMRES state.
+struct GmresState {
+  double* H;      // [K][m+1][m]  Hessenberg (rotated in place)
+  double* cs;     // [K][m]
+  double* sn;     // [K][m]
+  double* g;      // [K][m+1]
+  double* fnorm;  // [K]
+  double* rel;    // [K]   current relative residual estimate (output)
+  double* scale;  // [K]   per-column scale for the next basis vector
+  double* coef;   // [m][K] back-substitution result y (for the solution update)
+  int* active;    // [K]
+  int* kcyc;      // [K]   Arnoldi steps in the current cycle
+  long long* its; // [K]   total Arnoldi steps (output)
+};
+
+// cycle start: beta = ||r_j|| (true residual of the current iterate)
+__global__ void gmres_cycle_init_kernel(GmresState st, const double* __restrict__ nrm2,
+                                        int K, int m, double tol) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= K) return;
+  const double beta = sqrt(nrm2[j]);
+  const double fn = st.fnorm[j];
+  const double rel = fn > 0.0 ? beta / fn : 0.0;
+  st.rel[j] = rel;
+  const int act = (fn > 0.0) && (rel > tol) && (beta > 0.0);
+  st.active[j] = act;
+  st.kcyc[j] = 0;
+  for (int i = 0; i <= m; ++i) st.g[(long long)j * (m + 1) + i] = 0.0;
+  st.g[(long long)j * (m + 1)] = beta;
+  st.scale[j] = act ? 1.0 / beta : 0.0;
+}
+
+__global__ void gmres_set_fnorm_kernel(GmresState st, const double* __restrict__ nrm2, int K) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= K) return;
+  st.fnorm[j] = sqrt(nrm2[j]);
+  st.its[j] = 0;
+  st.rel[j] = 0.0;
+}
+
+// Arnoldi step i: column of H from the two Gram-Schmidt passes (h1 + h2, rows 0..i) and
+// ||w||^2; previous rotations, new rotation, residual estimate, convergence flag, and the
+// scale 1/H[i+1,i] of the next basis vector (0 for frozen columns or breakdown).
+__global__ void gmres_arnoldi_kernel(GmresState st, const double* __restrict__ h1,
+                                     const double* __restrict__ h2,
+                                     const double* __restrict__ wn2, int K, int m, int i,
+                                     double tol) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= K) return;
+  if (!st.active[j]) {
+    st.scale[j] = 0.0;
+    return;
+  }
+  double* H = st.H + (long long)j * (m + 1) * m;
+  double* cs = st.cs + (long long)j * m;
+  double* sn = st.sn + (long long)j * m;
+  double* g = st.g + (long long)j * (m + 1);
+  for (int l = 0; l <= i; ++l) H[l * m + i] = h1[l * K + j] + h2[l * K + j];
+  const double hn = sqrt(wn2[j]);
+  H[(i + 1) * m + i] = hn;
+  for (int l = 0; l < i; ++l) {
+    const double a = H[l * m + i], b = H[(l + 1) * m + i];
+    H[l * m + i] = cs[l] * a + sn[l] * b;
+    H[(l + 1) * m + i] = -sn[l] * a + cs[l] * b;
+  }
+  const double a = H[i * m + i], b = H[(i + 1) * m + i];
+  const double den = hypot(a, b);
+  cs[i] = a / den;
+  sn[i] = b / den;
+  H[i * m + i] = den;
+  H[(i + 1) * m + i] = 0.0;
+  g[i + 1] = -sn[i] * g[i];
+  g[i] = cs[i] * g[i];
+  st.kcyc[j] = i + 1;
+  st.its[j] += 1;
+  const double rel = fabs(g[i + 1]) / st.fnorm[j];
+  st.rel[j] = rel;
+  const bool done = (rel <= tol) || !(hn > 0.0);
+  if (done) st.active[j] = 0;
+  st.scale[j] = (!done && hn > 0.0) ? 1.0 / hn : 0.0;
+}
+
+// back substitution H[:k,:k] y = g[:k] per column -> coef[l*K + j] (0 beyond k)
+__global__ void gmres_backsolve_kernel(GmresState st, int K, int m) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= K) return;
+  const int k = st.kcyc[j];
+  const double* H = st.H + (long long)j * (m + 1) * m;
+  const double* g = st.g + (long long)j * (m + 1);
+  for (int l = m - 1; l >= 0; --l) {
+    double y = 0.0;
+    if (l < k) {
+      y = g[l];
+      for (int q = l + 1; q < k; ++q) y -= H[l * m + q] * st.coef[q * K + j];
+      y /= H[l * m + l];
+    }
+    st.coef[l * K + j] = y;
+  }
+}
+
+struct GmresDims {
+  long long S;      // elements of one Block-TT vector (rl n K rr)
+  long long rows;   // rl * n
+  int K, rr;
+  int chunks;
+  long long rows_per_chunk;
+};
+
+GmresDims gmres_dims(const Dims& d, long long K) {
+  GmresDims g;
+  g.rows = d.a * d.n;
+  g.K = (int)K;
+  g.rr = (int)d.b;
+  g.S = g.rows * K * d.b;
+  // ~ 4 blocks per SM across (chunks x K)
+  long long want = (4LL * num_sms() + K - 1) / K;
+  if (want < 1) want = 1;
+  if (want > g.rows) want = g.rows;
+  g.rows_per_chunk = (g.rows + want - 1) / want;
+  g.chunks = (int)((g.rows + g.rows_per_chunk - 1) / g.rows_per_chunk);
+  return g;
+}
+
+// out[l*K+j] = <A_l[:,j], B[:,j]> for l < L (L any size; passes of kMaxL)
+cudaError_t launch_coldots(const GmresDims& gd, const double* A, int L, const double* B,
+                           double* part, double* out, cudaStream_t s) {
+  for (int l0 = 0; l0 < L; l0 += kMaxL) {
+    const int Lp = std::min(kMaxL, L - l0);
+    dim3 grid(gd.chunks, gd.K);
+    colreduce_kernel<<<grid, 256, 0, s>>>(A + l0 * gd.S, gd.S, Lp, B, gd.rows, gd.K, gd.rr,
+                                          gd.rows_per_chunk, part);
+    ++g_launches;
+    const int LK = Lp * gd.K;
+    colreduce_finish_kernel<<<(LK + 255) / 256, 256, 0, s>>>(part, LK, gd.chunks,
+                                                            out + (long long)l0 * gd.K);
+    ++g_launches;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_colaxpy(const GmresDims& gd, const double* A, int L, const double* coef,
+                           double sign, double* B, cudaStream_t s) {
+  long long blocks = (gd.S + 255) / 256;
+  if (blocks > 8LL * num_sms()) blocks = 8LL * num_sms();
+  for (int l0 = 0; l0 < L; l0 += kMaxL) {
+    const int Lp = std::min(kMaxL, L - l0);
+    colaxpy_kernel<<<(unsigned)blocks, 256, 0, s>>>(A + l0 * gd.S, gd.S, Lp,
+                                                     coef + (long long)l0 * gd.K, sign, B, gd.K,
+                                                     gd.rr);
+    ++g_launches;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_elementwise(int kind, const double* a, const double* sc, double* b,
+                               const GmresDims& gd, cudaStream_t s) {
+  long long blocks = (gd.S + 255) / 256;
+  if (blocks > 8LL * num_sms()) blocks = 8LL * num_sms();
+  if (kind == 0)
+    colscale_kernel<<<(unsigned)blocks, 256, 0, s>>>(a, sc, b, gd.S, gd.K, gd.rr);
+  else
+    sub_kernel<<<(unsigned)blocks, 256, 0, s>>>(a, b, gd.S);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+// element counts of the GMRES workspace beyond the matvec's own
+struct GmresWs {
+  long long basis, w, part, small;
+};
+bool gmres_ws_elems(const Dims& d, long long K, long long m, GmresWs& g) {
+  bool ok = true;
+  const long long S = prod({d.a, d.n, K, d.b}, ok);
+  g.basis = prod({m + 1, S}, ok);
+  g.w = S;
+  GmresDims gd = gmres_dims(d, K);
+  g.part = (long long)kMaxL * K * gd.chunks;
+  // H, cs, sn, g, fnorm, rel, scale, coef, h1, h2, wn2 (doubles) + active, kcyc, its
+  g.small = K * ((m + 1) * m + 2 * m + (m + 1) + 4 + m) + 2 * (m + 1) * K + K + 3 * K + 8;
+  return ok;
+}
+
+// The solve (host-side launch sequence; no synchronisation).
+cudaError_t enqueue_gmres(const Dims& d, long long K, long long m, long long cycles, double tol,
+                          const double* phiL, const double* A, const double* phiR,
+                          const double* F, double* X, double* rel_out, long long* its_out,
+                          void* workspace, size_t workspace_bytes, cudaStream_t s) {
+  long long t1, t2, ah, pe;
+  matvec_ws_elems(d, K, t1, t2, ah, pe);
+  GmresWs gw;
+  gmres_ws_elems(d, K, m, gw);
+  Carver c{static_cast<char*>(workspace), workspace_bytes};
+  double* T1 = c.take(t1);
+  double* T2 = c.take(t2);
+  double* Ah = c.take(ah);
+  double* Pp = c.take(pe);
+  double* V = c.take(gw.basis);
+  double* W = c.take(gw.w);
+  double* part = c.take(gw.part);
+  double* sm = c.take(gw.small);
+  if (!c.ok) return cudaErrorInvalidValue;
+  GmresState st;
+  st.H = sm;
+  st.cs = st.H + K * (m + 1) * m;
+  st.sn = st.cs + K * m;
+  st.g = st.sn + K * m;
+  st.fnorm = st.g + K * (m + 1);
+  st.rel = rel_out;
+  st.scale = st.fnorm + K;
+  st.coef = st.scale + K;
+  double* h1 = st.coef + m * K;
+  double* h2 = h1 + (m + 1) * K;
+  double* wn2 = h2 + (m + 1) * K;
+  st.active = reinterpret_cast<int*>(wn2 + K);
+  st.kcyc = st.active + K;
+  st.its = its_out;
+  const GmresDims gd = gmres_dims(d, K);
+  const int kb = (int)((K + 127) / 128), kt = 128;
+  cudaError_t e;
+  g_stage = TT_ST_PERM;
+  if ((e = launch_perm(true, A, Ah, d.al, d.n, d.be, s)) != cudaSuccess) return e;
+  // ||f||
+  if ((e = launch_coldots(gd, F, 1, F, part, wn2, s)) != cudaSuccess) return e;
+  gmres_set_fnorm_kernel<<<kb, kt, 0, s>>>(st, wn2, (int)K);
+  ++g_launches;
+  for (long long cyc = 0; cyc < cycles; ++cyc) {
+    // r = f - L(x), beta = ||r||, v0 = r / beta
+    if ((e = enqueue_matvec(d, K, phiL, A, phiR, X, W, T1, T2, Ah, Pp, pe, s, Ah)) != cudaSuccess)
+      return e;
+    if ((e = launch_elementwise(1, F, nullptr, W, gd, s)) != cudaSuccess) return e;
+    if ((e = launch_coldots(gd, W, 1, W, part, wn2, s)) != cudaSuccess) return e;
+    gmres_cycle_init_kernel<<<kb, kt, 0, s>>>(st, wn2, (int)K, (int)m, tol);
+    ++g_launches;
+    if ((e = launch_elementwise(0, W, st.scale, V, gd, s)) != cudaSuccess) return e;
+    for (long long i = 0; i < m; ++i) {
+      const double* Vi = V + i * gd.S;
+      if ((e = enqueue_matvec(d, K, phiL, A, phiR, Vi, W, T1, T2, Ah, Pp, pe, s, Ah)) !=
+          cudaSuccess)
+        return e;
+      const int L = (int)(i + 1);
+      // CGS2: two classical Gram-Schmidt passes against v_0..v_i
+      if ((e = launch_coldots(gd, V, L, W, part, h1, s)) != cudaSuccess) return e;
+      if ((e = launch_colaxpy(gd, V, L, h1, -1.0, W, s)) != cudaSuccess) return e;
+      if ((e = launch_coldots(gd, V, L, W, part, h2, s)) != cudaSuccess) return e;
+      if ((e = launch_colaxpy(gd, V, L, h2, -1.0, W, s)) != cudaSuccess) return e;
+      if ((e = launch_coldots(gd, W, 1, W, part, wn2, s)) != cudaSuccess) return e;
+      gmres_arnoldi_kernel<<<kb, kt, 0, s>>>(st, h1, h2, wn2, (int)K, (int)m, (int)i, tol);
+      ++g_launches;
+      if ((e = launch_elementwise(0, W, st.scale, V + (i + 1) * gd.S, gd, s)) != cudaSuccess)
+        return e;
+    }
+    gmres_backsolve_kernel<<<kb, kt, 0, s>>>(st, (int)K, (int)m);
+    ++g_launches;
+    if ((e = launch_colaxpy(gd, V, (int)m, st.coef, 1.0, X, s)) != cudaSuccess) return e;
+  }
+  return cudaGetLastError();
+}

@@ -958,6 +958,8 @@ tt_status check_dims(const Dims& d) {
 
 bool same(const void* p, const void* q) { return p != nullptr && p == q; }
 
+#include "tt_gmres.cuh"
+
 }  // namespace
 
 // ========================================================================================
@@ -1480,6 +1482,49 @@ tt_status tt_operator_apply(int64_t d, const int64_t* n_row, const int64_t* n_co
     ++g_launches;
     if (e != cudaSuccess) return cuda_fail(e, "tt_operator_apply");
   }
+  return TT_OK;
+}
+
+// ---- local GMRES --------------------------------------------------
+size_t tt_local_gmres_workspace_size(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t Rr,
+                                     int64_t nvec, int64_t m) {
+  Dims d{rl, n, rr, Rl, Rr};
+  long long t1, t2, ah, pe;
+  GmresWs gw;
+  if (!dims_valid(d) || nvec <= 0 || nvec > 64 || m <= 0 || !matvec_ws_elems(d, nvec, t1, t2, ah, pe) ||
+      !gmres_ws_elems(d, nvec, m, gw))
+    return 0;
+  return ws_bytes({t1, t2, ah, pe, gw.basis, gw.w, gw.part, gw.small});
+}
+
+tt_status tt_local_gmres(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t Rr, int64_t nvec,
+                         int64_t m, int64_t cycles, double tol, const double* phiL,
+                         const double* A, const double* phiR, const double* F, double* X,
+                         double* rel_res, int64_t* iters, void* workspace,
+                         size_t workspace_bytes, void* stream) {
+  CallScope scope;
+  Dims d{rl, n, rr, Rl, Rr};
+  tt_status st = check_dims(d);
+  if (st != TT_OK) return st;
+  if (nvec <= 0 || nvec > 64) return fail(TT_ERR_INVALID_ARGUMENT, "nvec must be in [1, 64]");
+  if (m <= 0 || m > 512 || cycles < 0 || !(tol >= 0.0))
+    return fail(TT_ERR_INVALID_ARGUMENT, "need 0 < m <= 512, cycles >= 0, tol >= 0");
+  if (!phiL || !A || !phiR || !F || !X || !rel_res || !iters)
+    return fail(TT_ERR_NULL_POINTER, "NULL pointer");
+  for (const void* o : {(const void*)X, (const void*)rel_res, (const void*)iters})
+    for (const void* i : {(const void*)phiL, (const void*)A, (const void*)phiR, (const void*)F})
+      if (o == i) return fail(TT_ERR_ALIASING, "an output aliases an input");
+  if ((const void*)X == (const void*)rel_res || (const void*)X == (const void*)iters ||
+      (const void*)rel_res == (const void*)iters)
+    return fail(TT_ERR_ALIASING, "two outputs alias");
+  const size_t need = tt_local_gmres_workspace_size(rl, n, rr, Rl, Rr, nvec, m);
+  if (need == 0) return fail(TT_ERR_OVERFLOW, "workspace overflow");
+  if (!workspace || workspace_bytes < need)
+    return fail(TT_ERR_WORKSPACE, "workspace NULL or smaller than " + std::to_string(need) + " bytes");
+  cudaError_t e = enqueue_gmres(d, nvec, m, cycles, tol, phiL, A, phiR, F, X, rel_res,
+                                reinterpret_cast<long long*>(iters), workspace, workspace_bytes,
+                                static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "tt_local_gmres");
   return TT_OK;
 }
 

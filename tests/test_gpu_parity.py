@@ -359,3 +359,66 @@ def test_sweep_workspace_errors(tt):
         pl[2] = xs[1]
         tt.tt_sweep_interfaces(xs, As, phiL=pl, directions=tt.TT_SWEEP_LEFT)
     assert ei.value.status in (3, 1)
+
+
+# ----------------------------------------------------------------------------------------
+# matrix-free local GMRES vs the oracle GMRES
+# ----------------------------------------------------------------------------------------
+def _mixed_canonical_system(idx, k, seed=3):
+    import oracle
+    import ttgen
+    inp = ttgen.make_inputs(idx)
+    xl = ttgen.left_orthonormalise(inp.x)
+    xr = ttgen.right_orthonormalise(inp.x)
+    mixed = xl[:k] + [inp.x[k]] + xr[k + 1:]
+    pl, _ = oracle.sweep_interfaces(mixed, inp.A, 1)
+    _, pr = oracle.sweep_interfaces(mixed, inp.A, 2)
+    return mixed, inp.A, pl[k], pr[k + 1], np.random.default_rng(seed)
+
+
+@pytest.mark.parametrize("idx,k,K,m,cycles", [(2, 3, 4, 12, 2), (4, 5, 3, 8, 1), (3, 1, 5, 10, 2)])
+def test_local_gmres_vs_oracle(tt, idx, k, K, m, cycles):
+    """Fixed m, cycles and tol = 0 on both sides: the iterates must agree (<= 1e-11)."""
+    from oracle.gmres import local_gmres_batched
+    mixed, A, phiL, phiR, rng = _mixed_canonical_system(idx, k)
+    rl, n, rr = mixed[k].shape
+    F = rng.standard_normal((rl, n, K, rr))
+    X0 = 0.1 * rng.standard_normal((rl, n, K, rr))
+    Xo, relo, itso = local_gmres_batched(phiL, A[k], phiR, F, X0, m=m, cycles=cycles, tol=0.0)
+    Xg, relg, itsg = tt.tt_local_gmres(g(phiL), g(A[k]), g(phiR), g(F), g(X0.copy()), m=m,
+                                       cycles=cycles, tol=0.0)
+    torch.cuda.synchronize()
+    for j in range(K):
+        assert rel(h(Xg)[:, :, j, :], Xo[:, :, j, :]) <= TOL, j
+    assert (h(itsg) == itso).all()
+    assert np.allclose(h(relg), relo, rtol=1e-6, atol=1e-14)
+
+
+def test_local_gmres_converges_to_dense_solution(tt):
+    """SPD Kronecker-sum operator, orthonormal frame (config-2 core 3): GMRES to tol 1e-13
+    reproduces the dense solve of the projected system."""
+    from dense_ref import full_matrix, projected_operator
+    mixed, A, phiL, phiR, rng = _mixed_canonical_system(2, 2)
+    rl, n, rr = mixed[2].shape
+    F = rng.standard_normal((rl, n, 2, rr))
+    Xg, relg, itsg = tt.tt_local_gmres(g(phiL), g(A[2]), g(phiR), g(F), m=30, cycles=4,
+                                       tol=1e-13)
+    torch.cuda.synchronize()
+    L = projected_operator(mixed, full_matrix(A), 2)
+    for j in range(2):
+        ref = np.linalg.solve(L, F[:, :, j, :].ravel())
+        assert rel(h(Xg)[:, :, j, :].ravel(), ref) <= 1e-11
+    assert (h(relg) <= 1e-13).all()
+
+
+def test_local_gmres_errors(tt):
+    F = torch.zeros(2, 4, 65, 2, dtype=torch.float64, device="cuda")
+    A = torch.zeros(1, 4, 4, 1, dtype=torch.float64, device="cuda")
+    P = torch.zeros(2, 1, 2, dtype=torch.float64, device="cuda")
+    with pytest.raises(tt.TTError) as ei:
+        tt.tt_local_gmres(P, A, P, F, m=4)
+    assert ei.value.status == 1
+    F = torch.zeros(2, 4, 3, 2, dtype=torch.float64, device="cuda")
+    X, rr_, it = tt.tt_local_gmres(P, A, P, F, m=4, cycles=2, tol=1e-12)   # zero rhs -> zero
+    torch.cuda.synchronize()
+    assert not h(X).any() and (h(it) == 0).all()
