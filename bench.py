@@ -476,6 +476,34 @@ def main():
                "note": "H2D of x, A and the Krylov block and D2H of the Y blocks every step, "
                        "double-buffered on two copy streams (overlapping compute)"}
 
+    # ---- local GMRES on the interior core (m = 10, one cycle) ----------
+    gm = None
+    if not args.no_sweeps:
+        k = cfg.d // 2
+        m_g = 10
+        rl, nn, rr = cfg.r[k], cfg.N, cfg.r[k + 1]
+        Rl, Rr = cfg.R[k], cfg.R[k + 1]
+        Fg = Xs[k]
+        Xg = torch.zeros_like(Fg)
+        wsg = torch.empty(tt.tt_local_gmres_workspace_size(rl, nn, rr, Rl, Rr, cfg.nvec, m_g),
+                          dtype=torch.uint8, device=dev)
+        relg = torch.empty(cfg.nvec, dtype=torch.float64, device=dev)
+        itg = torch.empty(cfg.nvec, dtype=torch.int64, device=dev)
+
+        def gmres_run(st):
+            Xg.zero_()
+            tt.tt_local_gmres(phiL[k], As[k], phiR[k + 1], Fg, Xg, m=m_g, cycles=1, tol=0.0,
+                              rel_res=relg, iters=itg, workspace=wsg, stream=st)
+        t = time_sweep(tt, gmres_run, stream, dev, reps=3)
+        mv_f = (m_g + 1) * cfg.nvec * f_local(rl, nn, rr, Rl, Rr)
+        S = rl * nn * cfg.nvec * rr
+        orth_f = sum(2 * 2 * 2 * (i + 1) * S for i in range(m_g))   # CGS2: 2 passes x (dot + axpy)
+        gm = {"core": k, "nvec": cfg.nvec, "m": m_g, "cycles": 1,
+              "ms": t["graph_ms_median"], "ms_eager": t["eager_ms_median"],
+              "gflop": (mv_f + orth_f) / 1e9,
+              "tflops": (mv_f + orth_f) / (t["graph_ms_median"] * 1e-3) / 1e12,
+              "matvec_share_of_flops": mv_f / (mv_f + orth_f)}
+
     # ---- full sweeps at d = 12 (metric's second half), eager and as a CUDA graph ---------
     sweeps = None
     if not args.no_sweeps:
@@ -534,6 +562,7 @@ def main():
             "gpu_launches": gpu_launches,
             "clocks": clk,
             "sweeps_d12": sweeps,
+            "local_gmres": gm,
             "detail": {
                 "full_sweep_ms": (total_ms / args.steps) - (apply_detail["ms_per_step"]
                                                             if apply_detail else 0.0),

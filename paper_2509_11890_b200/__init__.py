@@ -66,7 +66,7 @@ lib.tt_trace_read.argtypes = [_i64] + [_p] * 6
 lib.tt_fp64_peak_probe.argtypes = [_i64, _p, _p]
 lib.tt_local_gmres_workspace_size.restype = _sz
 lib.tt_local_gmres_workspace_size.argtypes = [_i64] * 7
-lib.tt_local_gmres.argtypes = [_i64] * 8 + [ctypes.c_double] + [_p] * 7 + [_sz, _p]
+lib.tt_local_gmres.argtypes = [_i64] * 8 + [ctypes.c_double] + [_p] * 8 + [_sz, _p]
 lib.tt_local_gmres.restype = ctypes.c_int
 lib.tt_debug_force_v1.argtypes = [ctypes.c_int]
 lib.tt_debug_force_v1.restype = None

@@ -92,3 +92,28 @@ def test_no_oracle_in_product_path():
             if fn.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 s = open(os.path.join(dirpath, fn)).read()
                 assert "oracle" not in s.replace("no oracle", ""), fn
+
+
+def _header_param_counts():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    out = {}
+    for m in re.finditer(r"\b(tt_[a-z_0-9]+)\s*\(([^;{]*?)\)\s*;", src, flags=re.S):
+        params = m.group(2).strip()
+        out[m.group(1)] = 0 if params in ("", "void") else params.count(",") + 1
+    return out
+
+
+def test_binding_argtypes_match_header():
+    """Every ctypes prototype of the binding has exactly the header's parameter count (a
+    missing entry silently truncates a 64-bit argument, e.g. the stream)."""
+    import paper_2509_11890_b200 as tt
+    counts = _header_param_counts()
+    checked = 0
+    for name, n in counts.items():
+        fn = getattr(tt.lib, name)
+        if fn.argtypes is None:
+            continue
+        assert len(fn.argtypes) == n, (name, len(fn.argtypes), n)
+        checked += 1
+    assert checked >= 12
