@@ -144,6 +144,24 @@ tt_status tt_operator_apply(int64_t d, const int64_t* n_row, const int64_t* n_co
                             double* const* z_cores, void* stream);
 
 /* ---------------------------------------------------------------------------------------
+ * two-site (DMRG supercore) local matvec: the projected operator of a
+ * PAIR of neighbouring cores ("operates on pairs of neighbouring cores simultaneously",
+ * PAPER.md:556-567) applied to nvec supercores:
+ *   Y[a',i1,i2,m,b'] = sum phiL[a',al,a] A1[al,i1,j1,g] A2[g,i2,j2,be] phiR[b',be,b] W[a,j1,j2,m,b]
+ *   phiL (rl,Rl,rl), A1 (Rl,n1,n1,Rm), A2 (Rm,n2,n2,Rr), phiR (rr,Rr,rr),
+ *   W, Y (rl, n1, n2, nvec, rr) (Block-TT layout of the supercore).
+ * Evaluated by merging the two operator cores (a small kernel) and running the single-site
+ * batched matvec with mode n1*n2.  Workspace: tt_local_matvec_two_site_workspace_size(...).
+ * ------------------------------------------------------------------------------------- */
+size_t tt_local_matvec_two_site_workspace_size(int64_t rl, int64_t n1, int64_t n2, int64_t rr,
+                                               int64_t Rl, int64_t Rm, int64_t Rr, int64_t nvec);
+tt_status tt_local_matvec_two_site(int64_t rl, int64_t n1, int64_t n2, int64_t rr, int64_t Rl,
+                                   int64_t Rm, int64_t Rr, int64_t nvec, const double* phiL,
+                                   const double* A1, const double* A2, const double* phiR,
+                                   const double* W, double* Y, void* workspace,
+                                   size_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------------------
  * matrix-free local solve: restarted GMRES(m) on the projected local
  * operator ("solve them in a matrix-free fashion via GMRES ... perform the
  * constituent multiplications sequentially"), for nvec <= 64 independent right-hand sides:

@@ -40,10 +40,11 @@ def lib():
         L.tt_oracle_sweep_interfaces.argtypes = [i64, p, p, p, p, p, p, p, ctypes.c_int]
         L.tt_oracle_operator_apply.argtypes = [i64, p, p, p, p, p, p, p]
         L.tt_oracle_apply_core.argtypes = [i64] * 6 + [p] * 3
+        L.tt_oracle_local_matvec_two_site.argtypes = [i64] * 7 + [p] * 6
         for f in ("tt_oracle_local_matvec", "tt_oracle_local_matvec_batched",
                   "tt_oracle_interface_left", "tt_oracle_interface_right",
                   "tt_oracle_sweep_interfaces", "tt_oracle_operator_apply",
-                  "tt_oracle_apply_core"):
+                  "tt_oracle_apply_core", "tt_oracle_local_matvec_two_site"):
             getattr(L, f).restype = ctypes.c_int
         _ = dp
         _lib = L
@@ -148,3 +149,14 @@ def apply_core(x, A):
     z = np.empty((rl * Rl, ni, rr * Rr))
     _check(lib().tt_oracle_apply_core(rl, ni, nj, rr, Rl, Rr, _p(x), _p(A), _p(z)))
     return z
+
+
+def local_matvec_two_site(phiL, A1, A2, phiR, w):
+    """Two-site local matvec on a supercore w (rl, n1, n2, rr)."""
+    phiL, A1, A2, phiR, w = map(_c, (phiL, A1, A2, phiR, w))
+    rl, n1, n2, rr = w.shape
+    Rl, Rm, Rr = A1.shape[0], A1.shape[3], A2.shape[3]
+    y = np.empty_like(w)
+    _check(lib().tt_oracle_local_matvec_two_site(rl, n1, n2, rr, Rl, Rm, Rr, _p(phiL), _p(A1),
+                                                 _p(A2), _p(phiR), _p(w), _p(y)))
+    return y

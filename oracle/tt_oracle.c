@@ -313,3 +313,80 @@ int tt_oracle_operator_apply(int64_t d, const int64_t* n_row, const int64_t* n_c
   }
   return OR_OK;
 }
+
+/* ---------------------------------------------------------------------------------------
+ * Two-site (DMRG supercore) local matvec, SURVEY.md 8(f) row 4 ("the
+ * algorithm operates on pairs of neighbouring cores simultaneously"): the projected operator
+ * X_{!=k,k+1}^T A X_{!=k,k+1} applied to a supercore w[a, j1, j2, b], as four products:
+ *   S1  T1[a',al,j1,j2,b] = sum_a          phiL[a',al,a] w[a,j1,j2,b]
+ *   S2  T2[a',i1,g,j2,b]  = sum_{al,j1}    A1[al,i1,j1,g] T1[a',al,j1,j2,b]
+ *   S3  T3[a',i1,i2,be,b] = sum_{g,j2}     A2[g,i2,j2,be] T2[a',i1,g,j2,b]
+ *   S4  y[a',i1,i2,b']    = sum_{be,b}     T3[a',i1,i2,be,b] phiR[b',be,b]
+ * phiL (rl,Rl,rl), A1 (Rl,n1,n1,Rm), A2 (Rm,n2,n2,Rr), phiR (rr,Rr,rr), w,y (rl,n1,n2,rr).
+ * ------------------------------------------------------------------------------------- */
+int tt_oracle_local_matvec_two_site(int64_t rl, int64_t n1, int64_t n2, int64_t rr, int64_t Rl,
+                                    int64_t Rm, int64_t Rr, const double* phiL, const double* A1,
+                                    const double* A2, const double* phiR, const double* w,
+                                    double* y) {
+  int64_t t = 1, u = 1, v = 1;
+  int64_t ap, al, a, j1, j2, b, i1, i2, g, be, bp;
+  double *T1, *T2, *T3;
+  if (!phiL || !A1 || !A2 || !phiR || !w || !y) return OR_NULL;
+  if (rl <= 0 || n1 <= 0 || n2 <= 0 || rr <= 0 || Rl <= 0 || Rm <= 0 || Rr <= 0) return OR_INVALID;
+  if (!mul_ok(&t, rl) || !mul_ok(&t, Rl) || !mul_ok(&t, n1) || !mul_ok(&t, n2) || !mul_ok(&t, rr))
+    return OR_OVERFLOW;
+  if (!mul_ok(&u, rl) || !mul_ok(&u, n1) || !mul_ok(&u, Rm) || !mul_ok(&u, n2) || !mul_ok(&u, rr))
+    return OR_OVERFLOW;
+  if (!mul_ok(&v, rl) || !mul_ok(&v, n1) || !mul_ok(&v, n2) || !mul_ok(&v, Rr) || !mul_ok(&v, rr))
+    return OR_OVERFLOW;
+  T1 = (double*)calloc((size_t)t, sizeof(double));
+  T2 = (double*)calloc((size_t)u, sizeof(double));
+  T3 = (double*)calloc((size_t)v, sizeof(double));
+  if (!T1 || !T2 || !T3) { free(T1); free(T2); free(T3); return OR_NOMEM; }
+  for (ap = 0; ap < rl; ++ap)
+    for (al = 0; al < Rl; ++al)
+      for (a = 0; a < rl; ++a) {
+        const double f = phiL[(ap * Rl + al) * rl + a];
+        for (j1 = 0; j1 < n1; ++j1)
+          for (j2 = 0; j2 < n2; ++j2)
+            for (b = 0; b < rr; ++b)
+              T1[(((ap * Rl + al) * n1 + j1) * n2 + j2) * rr + b] +=
+                  f * w[((a * n1 + j1) * n2 + j2) * rr + b];
+      }
+  for (ap = 0; ap < rl; ++ap)
+    for (al = 0; al < Rl; ++al)
+      for (i1 = 0; i1 < n1; ++i1)
+        for (j1 = 0; j1 < n1; ++j1)
+          for (g = 0; g < Rm; ++g) {
+            const double f = A1[((al * n1 + i1) * n1 + j1) * Rm + g];
+            for (j2 = 0; j2 < n2; ++j2)
+              for (b = 0; b < rr; ++b)
+                T2[(((ap * n1 + i1) * Rm + g) * n2 + j2) * rr + b] +=
+                    f * T1[(((ap * Rl + al) * n1 + j1) * n2 + j2) * rr + b];
+          }
+  for (ap = 0; ap < rl; ++ap)
+    for (i1 = 0; i1 < n1; ++i1)
+      for (g = 0; g < Rm; ++g)
+        for (i2 = 0; i2 < n2; ++i2)
+          for (j2 = 0; j2 < n2; ++j2)
+            for (be = 0; be < Rr; ++be) {
+              const double f = A2[((g * n2 + i2) * n2 + j2) * Rr + be];
+              for (b = 0; b < rr; ++b)
+                T3[(((ap * n1 + i1) * n2 + i2) * Rr + be) * rr + b] +=
+                    f * T2[(((ap * n1 + i1) * Rm + g) * n2 + j2) * rr + b];
+            }
+  for (ap = 0; ap < rl; ++ap)
+    for (i1 = 0; i1 < n1; ++i1)
+      for (i2 = 0; i2 < n2; ++i2)
+        for (bp = 0; bp < rr; ++bp) {
+          double sum = 0.0;
+          for (be = 0; be < Rr; ++be)
+            for (b = 0; b < rr; ++b)
+              sum += T3[(((ap * n1 + i1) * n2 + i2) * Rr + be) * rr + b] * phiR[(bp * Rr + be) * rr + b];
+          y[((ap * n1 + i1) * n2 + i2) * rr + bp] = sum;
+        }
+  free(T1);
+  free(T2);
+  free(T3);
+  return OR_OK;
+}

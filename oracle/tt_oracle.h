@@ -64,6 +64,14 @@ int tt_oracle_operator_apply(int64_t d, const int64_t* n_row, const int64_t* n_c
 int tt_oracle_apply_core(int64_t rl, int64_t ni, int64_t nj, int64_t rr, int64_t Rl, int64_t Rr,
                          const double* x, const double* A, double* z);
 
+/* Two-site (DMRG supercore) local matvec:
+ * y[a',i1,i2,b'] = sum phiL[a',al,a] A1[al,i1,j1,g] A2[g,i2,j2,be] phiR[b',be,b] w[a,j1,j2,b]
+ * phiL (rl,Rl,rl), A1 (Rl,n1,n1,Rm), A2 (Rm,n2,n2,Rr), phiR (rr,Rr,rr), w,y (rl,n1,n2,rr). */
+int tt_oracle_local_matvec_two_site(int64_t rl, int64_t n1, int64_t n2, int64_t rr, int64_t Rl,
+                                    int64_t Rm, int64_t Rr, const double* phiL, const double* A1,
+                                    const double* A2, const double* phiR, const double* w,
+                                    double* y);
+
 #ifdef __cplusplus
 }
 #endif

@@ -25,6 +25,7 @@ __all__ = [
     "TT_SWEEP_LEFT", "TT_SWEEP_RIGHT", "TT_SWEEP_BOTH", "tt_trace_enable", "tt_trace_disable",
     "tt_trace_count", "tt_trace_read", "tt_fp64_peak_probe", "STAGE_NAMES", "tt_debug_force_v1",
     "tt_debug_set_variant", "tt_debug_set_flags", "tt_local_gmres", "tt_local_gmres_workspace_size",
+    "tt_local_matvec_two_site", "tt_local_matvec_two_site_workspace_size",
 ]
 
 STAGE_NAMES = {0: "perm", 1: "set", 2: "mv_s1", 3: "mv_s2", 4: "mv_s3", 5: "il_s1", 6: "il_s2",
@@ -64,6 +65,10 @@ lib.tt_trace_enable.argtypes = [_i64]
 lib.tt_trace_count.restype = ctypes.c_int64
 lib.tt_trace_read.argtypes = [_i64] + [_p] * 6
 lib.tt_fp64_peak_probe.argtypes = [_i64, _p, _p]
+lib.tt_local_matvec_two_site_workspace_size.restype = _sz
+lib.tt_local_matvec_two_site_workspace_size.argtypes = [_i64] * 8
+lib.tt_local_matvec_two_site.argtypes = [_i64] * 8 + [_p] * 7 + [_sz, _p]
+lib.tt_local_matvec_two_site.restype = ctypes.c_int
 lib.tt_local_gmres_workspace_size.restype = _sz
 lib.tt_local_gmres_workspace_size.argtypes = [_i64] * 7
 lib.tt_local_gmres.argtypes = [_i64] * 8 + [ctypes.c_double] + [_p] * 8 + [_sz, _p]
@@ -339,3 +344,24 @@ def tt_local_gmres(phiL, A, phiR, F, X=None, m=20, cycles=1, tol=0.0, rel_res=No
                               _dev(rel_res, "rel_res"), iters.data_ptr(), ws.data_ptr(),
                               ws.numel(), _stream(stream)))
     return X, rel_res, iters
+
+
+def tt_local_matvec_two_site_workspace_size(rl, n1, n2, rr, Rl, Rm, Rr, nvec) -> int:
+    return int(lib.tt_local_matvec_two_site_workspace_size(rl, n1, n2, rr, Rl, Rm, Rr, nvec))
+
+
+def tt_local_matvec_two_site(phiL, A1, A2, phiR, W, Y=None, workspace=None, stream=None):
+    """Two-site (DMRG supercore) local matvec; W, Y (rl, n1, n2, nvec, rr) or (rl, n1, n2, rr)."""
+    single = W.dim() == 4
+    Wv = W.unsqueeze(3) if single else W
+    rl, n1, n2, nvec, rr = Wv.shape
+    Rl, Rm, Rr = A1.shape[0], A1.shape[3], A2.shape[3]
+    if Y is None:
+        Y = torch.empty_like(W)
+    ws = _ws(tt_local_matvec_two_site_workspace_size(rl, n1, n2, rr, Rl, Rm, Rr, nvec), workspace,
+             W.device)
+    _check(lib.tt_local_matvec_two_site(rl, n1, n2, rr, Rl, Rm, Rr, nvec, _dev(phiL, "phiL"),
+                                        _dev(A1, "A1"), _dev(A2, "A2"), _dev(phiR, "phiR"),
+                                        _dev(W, "W"), _dev(Y, "Y"), ws.data_ptr(), ws.numel(),
+                                        _stream(stream)))
+    return Y

@@ -960,6 +960,28 @@ bool same(const void* p, const void* q) { return p != nullptr && p == q; }
 
 #include "tt_gmres.cuh"
 
+// Two-site supercore operator: A12[al, (i1 i2), (j1 j2), be] = sum_g A1[al,i1,j1,g] A2[g,i2,j2,be]
+// (the local operator of a pair of cores; tiny, one thread per output)
+__global__ void merge_cores_kernel(const double* __restrict__ A1, const double* __restrict__ A2,
+                                   double* __restrict__ A12, long long Rl, long long n1,
+                                   long long n2, long long Rm, long long Rr) {
+  const long long total = Rl * n1 * n2 * n1 * n2 * Rr;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    long long r = e;
+    const long long be = r % Rr; r /= Rr;
+    const long long j2 = r % n2; r /= n2;
+    const long long j1 = r % n1; r /= n1;
+    const long long i2 = r % n2; r /= n2;
+    const long long i1 = r % n1;
+    const long long al = r / n1;
+    double s = 0.0;
+    for (long long g = 0; g < Rm; ++g)
+      s = fma(A1[((al * n1 + i1) * n1 + j1) * Rm + g], A2[((g * n2 + i2) * n2 + j2) * Rr + be], s);
+    A12[e] = s;
+  }
+}
+
 }  // namespace
 
 // ========================================================================================
@@ -1482,6 +1504,60 @@ tt_status tt_operator_apply(int64_t d, const int64_t* n_row, const int64_t* n_co
     ++g_launches;
     if (e != cudaSuccess) return cuda_fail(e, "tt_operator_apply");
   }
+  return TT_OK;
+}
+
+// ---- two-site local matvec ------------------------------------------
+size_t tt_local_matvec_two_site_workspace_size(int64_t rl, int64_t n1, int64_t n2, int64_t rr,
+                                               int64_t Rl, int64_t Rm, int64_t Rr, int64_t nvec) {
+  if (n1 <= 0 || n2 <= 0 || Rm <= 0 || nvec <= 0) return 0;
+  Dims d{rl, n1 * n2, rr, Rl, Rr};
+  long long t1, t2, ah, pe;
+  if (!dims_valid(d) || !matvec_ws_elems(d, nvec, t1, t2, ah, pe)) return 0;
+  return ws_bytes({t1, t2, ah, pe, d.al * d.n * d.n * d.be});
+}
+
+tt_status tt_local_matvec_two_site(int64_t rl, int64_t n1, int64_t n2, int64_t rr, int64_t Rl,
+                                   int64_t Rm, int64_t Rr, int64_t nvec, const double* phiL,
+                                   const double* A1, const double* A2, const double* phiR,
+                                   const double* W, double* Y, void* workspace,
+                                   size_t workspace_bytes, void* stream) {
+  CallScope scope;
+  if (n1 <= 0 || n2 <= 0 || Rm <= 0 || nvec <= 0)
+    return fail(TT_ERR_INVALID_ARGUMENT, "extents must be positive");
+  bool ok = true;
+  const long long N = prod({n1, n2}, ok);
+  if (!ok) return fail(TT_ERR_OVERFLOW, "extent product overflows");
+  Dims d{rl, N, rr, Rl, Rr};
+  tt_status st = check_dims(d);
+  if (st != TT_OK) return st;
+  if (!phiL || !A1 || !A2 || !phiR || !W || !Y) return fail(TT_ERR_NULL_POINTER, "NULL pointer");
+  if (same(Y, phiL) || same(Y, A1) || same(Y, A2) || same(Y, phiR) || same(Y, W))
+    return fail(TT_ERR_ALIASING, "output Y aliases an input");
+  long long t1, t2, ah, pe;
+  if (!matvec_ws_elems(d, nvec, t1, t2, ah, pe)) return fail(TT_ERR_OVERFLOW, "workspace overflow");
+  const long long a12 = d.al * d.n * d.n * d.be;
+  const size_t need = ws_bytes({t1, t2, ah, pe, a12});
+  if (!workspace || workspace_bytes < need)
+    return fail(TT_ERR_WORKSPACE, "workspace NULL or smaller than " + std::to_string(need) + " bytes");
+  Carver c{static_cast<char*>(workspace), workspace_bytes};
+  double* T1 = c.take(t1);
+  double* T2 = c.take(t2);
+  double* Ah = c.take(ah);
+  double* Pp = c.take(pe);
+  double* A12 = c.take(a12);
+  if (!c.ok) return fail(TT_ERR_WORKSPACE, "workspace too small after alignment");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  long long blocks = (a12 + 255) / 256;
+  if (blocks > 2048) blocks = 2048;
+  g_stage = TT_ST_PERM;
+  const long long tr = trace_begin(0, a12, 0, 0, s);
+  merge_cores_kernel<<<(unsigned)blocks, 256, 0, s>>>(A1, A2, A12, Rl, n1, n2, Rm, Rr);
+  trace_end(tr, s);
+  ++g_launches;
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = enqueue_matvec(d, nvec, phiL, A12, phiR, W, Y, T1, T2, Ah, Pp, pe, s);
+  if (e != cudaSuccess) return cuda_fail(e, "tt_local_matvec_two_site");
   return TT_OK;
 }
 

@@ -422,3 +422,29 @@ def test_local_gmres_errors(tt):
     X, rr_, it = tt.tt_local_gmres(P, A, P, F, m=4, cycles=2, tol=1e-12)   # zero rhs -> zero
     torch.cuda.synchronize()
     assert not h(X).any() and (h(it) == 0).all()
+
+
+# ----------------------------------------------------------------------------------------
+# two-site (DMRG supercore) local matvec vs the oracle
+# ----------------------------------------------------------------------------------------
+@pytest.mark.parametrize("shape", [
+    # rl, n1, n2, rr, Rl, Rm, Rr, nvec
+    (3, 2, 2, 5, 2, 3, 2, 1),
+    (37, 2, 2, 45, 6, 9, 5, 3),
+    (64, 2, 3, 40, 16, 12, 8, 2),
+    (128, 2, 2, 128, 25, 25, 25, 4),
+])
+def test_two_site_matvec_vs_oracle(tt, shape):
+    import oracle
+    rl, n1, n2, rr, Rl, Rm, Rr, nvec = shape
+    rng = np.random.default_rng(sum(shape))
+    phiL = rng.standard_normal((rl, Rl, rl))
+    A1 = rng.standard_normal((Rl, n1, n1, Rm))
+    A2 = rng.standard_normal((Rm, n2, n2, Rr))
+    phiR = rng.standard_normal((rr, Rr, rr))
+    W = rng.standard_normal((rl, n1, n2, nvec, rr))
+    Y = tt.tt_local_matvec_two_site(g(phiL), g(A1), g(A2), g(phiR), g(W))
+    torch.cuda.synchronize()
+    for m in range(nvec):
+        ref = oracle.local_matvec_two_site(phiL, A1, A2, phiR, np.ascontiguousarray(W[:, :, :, m, :]))
+        assert rel(h(Y)[:, :, :, m, :], ref) <= TOL, m

@@ -392,3 +392,41 @@ def test_oracle_rejects_bad_arguments():
     assert L.tt_oracle_local_matvec(0, 4, 1, 1, 1, p, p, p, p, p) == 1
     assert L.tt_oracle_local_matvec(1, 4, 1, -1, 1, p, p, p, p, p) == 1
     assert L.tt_oracle_local_matvec(1 << 40, 1 << 20, 1 << 20, 1, 1, p, p, p, p, p) == 5
+
+
+# --------------------------------------------------------------------------------------
+# two-site (DMRG supercore) local matvec — SURVEY.md 8(f) row 4
+# --------------------------------------------------------------------------------------
+def _two_site_frame(x, k):
+    """X_{!=k,k+1} = T^{<k} (x) I_{n_k} (x) I_{n_{k+1}} (x) T^{>k+1} (Def. Frame, two sites)."""
+    from dense_ref import left_interface, right_interface
+    n1, n2 = x[k].shape[1], x[k + 1].shape[1]
+    return np.kron(np.kron(left_interface(x, k), np.eye(n1 * n2)), right_interface(x, k + 1))
+
+
+@pytest.mark.parametrize("case", [(91, 4, 3, [1, 3, 4, 5, 1], [1, 2, 3, 2, 1]),
+                                  (92, 5, 2, [1, 2, 4, 4, 2, 1], [1, 3, 2, 3, 2, 1])])
+def test_two_site_matvec_projected_operator(case):
+    seed, d, N, r, R = case
+    x, A, _ = _rand_tt(seed, d, N, r, R)
+    Af = full_matrix(A)
+    pl, pr = oracle.sweep_interfaces(x, A)
+    rng = np.random.default_rng(seed)
+    for k in range(d - 1):
+        w = rng.standard_normal((r[k], N, N, r[k + 2]))
+        y = oracle.local_matvec_two_site(pl[k], A[k], A[k + 1], pr[k + 2], w)
+        F = _two_site_frame(x, k)
+        ref = F.T @ Af @ F @ w.reshape(-1)
+        assert rel_fro(y.reshape(-1), ref) < TOL_DENSE, k
+
+
+def test_two_site_merged_supercore_energy():
+    """With w = the merged supercore x_k x_{k+1}, <w, y> = x^T A x (restricted energy)."""
+    x, A, _ = _rand_tt(93, 4, 4, [1, 4, 6, 4, 1], [1, 3, 3, 3, 1])
+    v = full_vector(x)
+    e = v @ full_matrix(A) @ v
+    pl, pr = oracle.sweep_interfaces(x, A)
+    for k in range(3):
+        w = np.einsum("aib,bjc->aijc", x[k], x[k + 1])
+        y = oracle.local_matvec_two_site(pl[k], A[k], A[k + 1], pr[k + 2], w)
+        assert abs(np.vdot(w, y) - e) <= 1e-12 * abs(e)
