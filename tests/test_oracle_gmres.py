@@ -105,3 +105,51 @@ def test_local_gmres_restarts_converge_spd():
 def test_zero_rhs():
     x, rel, its = gmres(lambda v: 2 * v, np.zeros(5), np.ones(5), m=3, cycles=2, tol=1e-12)
     assert not x.any() and rel == 0.0 and its == 0
+
+
+# --------------------------------------------------------------------------------------
+# accelerated GMRES (LGMRES, Baker et al. 2005) — PAPER.md:488 "accelerated GMRES"
+# --------------------------------------------------------------------------------------
+def test_lgmres_first_cycle_is_gmres():
+    rng = np.random.default_rng(11)
+    n = 30
+    M = rng.standard_normal((n, n)) + 6 * np.eye(n)
+    f = rng.standard_normal(n)
+    a = gmres(lambda v: M @ v, f, np.zeros(n), m=6, cycles=1, tol=0.0, k=0)
+    b = gmres(lambda v: M @ v, f, np.zeros(n), m=6, cycles=1, tol=0.0, k=2)
+    assert np.array_equal(a[0], b[0]) and a[2] == b[2]
+
+
+def test_lgmres_cycle_minimises_over_augmented_space():
+    """The second cycle's iterate minimises ||f - M x|| over x1 + span(K_m(M, r1) + z1) with
+    z1 = x1 - x0 (dense least squares on an explicit basis)."""
+    rng = np.random.default_rng(12)
+    n, m = 40, 5
+    M = rng.standard_normal((n, n)) + 7 * np.eye(n)
+    f = rng.standard_normal(n)
+    x0 = np.zeros(n)
+    x1, _, _ = gmres(lambda v: M @ v, f, x0, m=m, cycles=1, tol=0.0, k=1)
+    x2, rel2, _ = gmres(lambda v: M @ v, f, x0, m=m, cycles=2, tol=0.0, k=1)
+    r1 = f - M @ x1
+    K = [r1]
+    for _ in range(m - 1):
+        K.append(M @ K[-1])
+    W = np.linalg.qr(np.column_stack(K + [x1 - x0]))[0]
+    y = np.linalg.lstsq(M @ W, r1, rcond=None)[0]
+    best = np.linalg.norm(r1 - M @ W @ y)
+    got = np.linalg.norm(f - M @ x2)
+    assert abs(got - best) <= 1e-10 * np.linalg.norm(f)
+    assert abs(rel2 - got / np.linalg.norm(f)) <= 1e-10
+
+
+def test_lgmres_converges_to_dense_solve():
+    mixed, A, k, phiL, phiR, rng = _spd_local_system(seed=13)
+    shape = mixed[k].shape
+    F = rng.standard_normal((shape[0], shape[1], 2, shape[2]))
+    X, rel, its = local_gmres_batched(phiL, A[k], phiR, F, np.zeros_like(F), m=4, cycles=60,
+                                      tol=1e-12, k=2)
+    assert (rel <= 1e-12).all()
+    Ldense = projected_operator(mixed, full_matrix(A), k)
+    for j in range(2):
+        ref = np.linalg.solve(Ldense, F[:, :, j, :].ravel())
+        assert np.linalg.norm(X[:, :, j, :].ravel() - ref) / np.linalg.norm(ref) < 1e-10
