@@ -162,9 +162,12 @@ tt_status tt_local_matvec_two_site(int64_t rl, int64_t n1, int64_t n2, int64_t r
                                    size_t workspace_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------------------
- * matrix-free local solve: restarted GMRES(m) on the projected local
- * operator ("solve them in a matrix-free fashion via GMRES ... perform the
- * constituent multiplications sequentially"), for nvec <= 64 independent right-hand sides:
+ * matrix-free local solve: restarted GMRES(m), or its accelerated
+ * variant LGMRES(m, k_aug) ("we employ the accelerated GMRES method [Baker 2005]":
+ * each cycle's search space is augmented with the k_aug most recent cycle corrections), on
+ * the projected local operator ("solve them in a matrix-free fashion via GMRES
+ * ... perform the constituent multiplications sequentially"), for nvec <= 64 independent
+ * right-hand sides:
  *   (X_{!=k}^T A X_{!=k}) y_j = f_j,  F, X in the Block-TT layout (rl, n, nvec, rr).
  * Every Arnoldi step is one batched local matvec (H4); orthogonalisation is classical
  * Gram-Schmidt with one re-orthogonalisation pass; Givens rotations per column.  X holds
@@ -176,9 +179,9 @@ tt_status tt_local_matvec_two_site(int64_t rl, int64_t n1, int64_t n2, int64_t r
  * Workspace: tt_local_gmres_workspace_size(...) (basis of m+1 Block-TT vectors + matvec).
  * ------------------------------------------------------------------------------------- */
 size_t tt_local_gmres_workspace_size(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t Rr,
-                                     int64_t nvec, int64_t m);
+                                     int64_t nvec, int64_t m, int64_t k_aug);
 tt_status tt_local_gmres(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t Rr, int64_t nvec,
-                         int64_t m, int64_t cycles, double tol, const double* phiL,
+                         int64_t m, int64_t k_aug, int64_t cycles, double tol, const double* phiL,
                          const double* A, const double* phiR, const double* F, double* X,
                          double* rel_res, int64_t* iters, void* workspace,
                          size_t workspace_bytes, void* stream);

@@ -70,8 +70,8 @@ lib.tt_local_matvec_two_site_workspace_size.argtypes = [_i64] * 8
 lib.tt_local_matvec_two_site.argtypes = [_i64] * 8 + [_p] * 7 + [_sz, _p]
 lib.tt_local_matvec_two_site.restype = ctypes.c_int
 lib.tt_local_gmres_workspace_size.restype = _sz
-lib.tt_local_gmres_workspace_size.argtypes = [_i64] * 7
-lib.tt_local_gmres.argtypes = [_i64] * 8 + [ctypes.c_double] + [_p] * 8 + [_sz, _p]
+lib.tt_local_gmres_workspace_size.argtypes = [_i64] * 8
+lib.tt_local_gmres.argtypes = [_i64] * 9 + [ctypes.c_double] + [_p] * 8 + [_sz, _p]
 lib.tt_local_gmres.restype = ctypes.c_int
 lib.tt_debug_force_v1.argtypes = [ctypes.c_int]
 lib.tt_debug_force_v1.restype = None
@@ -319,15 +319,16 @@ def tt_debug_set_flags(flags: int) -> None:
     lib.tt_debug_set_flags(int(flags))
 
 
-def tt_local_gmres_workspace_size(rl, n, rr, Rl, Rr, nvec, m) -> int:
-    return int(lib.tt_local_gmres_workspace_size(rl, n, rr, Rl, Rr, nvec, m))
+def tt_local_gmres_workspace_size(rl, n, rr, Rl, Rr, nvec, m, k_aug=0) -> int:
+    return int(lib.tt_local_gmres_workspace_size(rl, n, rr, Rl, Rr, nvec, m, k_aug))
 
 
 def tt_local_gmres(phiL, A, phiR, F, X=None, m=20, cycles=1, tol=0.0, rel_res=None, iters=None,
-                   workspace=None, stream=None):
-    """Restarted GMRES(m) on the projected local operator for every column of the Block-TT
-    right-hand side F (rl, n, nvec, rr).  X: initial guess (zeros if None),
-    overwritten with the iterate.  Returns (X, rel_res, iters) (device tensors)."""
+                   workspace=None, stream=None, k_aug=0):
+    """Restarted GMRES(m) (k_aug = 0) or accelerated LGMRES(m, k_aug) on the projected local
+    operator for every column of the Block-TT right-hand side F (rl, n, nvec, rr)
+    (PAPER.md:488).  X: initial guess (zeros if None), overwritten with the iterate.
+    Returns (X, rel_res, iters) (device tensors)."""
     rl, n, nvec, rr = F.shape
     Rl, Rr = A.shape[0], A.shape[3]
     if X is None:
@@ -336,10 +337,10 @@ def tt_local_gmres(phiL, A, phiR, F, X=None, m=20, cycles=1, tol=0.0, rel_res=No
         rel_res = torch.empty(nvec, dtype=torch.float64, device=F.device)
     if iters is None:
         iters = torch.empty(nvec, dtype=torch.int64, device=F.device)
-    ws = _ws(tt_local_gmres_workspace_size(rl, n, rr, Rl, Rr, nvec, m), workspace, F.device)
+    ws = _ws(tt_local_gmres_workspace_size(rl, n, rr, Rl, Rr, nvec, m, k_aug), workspace, F.device)
     if iters.dtype != torch.int64 or not iters.is_cuda:
         raise TypeError("iters must be a CUDA int64 tensor")
-    _check(lib.tt_local_gmres(rl, n, rr, Rl, Rr, nvec, m, cycles, float(tol), _dev(phiL, "phiL"),
+    _check(lib.tt_local_gmres(rl, n, rr, Rl, Rr, nvec, m, k_aug, cycles, float(tol), _dev(phiL, "phiL"),
                               _dev(A, "A"), _dev(phiR, "phiR"), _dev(F, "F"), _dev(X, "X"),
                               _dev(rel_res, "rel_res"), iters.data_ptr(), ws.data_ptr(),
                               ws.numel(), _stream(stream)))

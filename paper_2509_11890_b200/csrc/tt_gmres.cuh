@@ -87,6 +87,16 @@ __global__ void colscale_kernel(const double* __restrict__ src, const double* __
        e += (long long)gridDim.x * blockDim.x)
     dst[e] = src[e] * s[(e / rr) % K];
 }
+__global__ void add_kernel(const double* __restrict__ C, double* __restrict__ X, long long S) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < S;
+       e += (long long)gridDim.x * blockDim.x)
+    X[e] += C[e];
+}
+// per-column 1 / ||c|| (0 for a zero column)
+__global__ void inv_norm_kernel(const double* __restrict__ nrm2, double* __restrict__ sc, int K) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < K) sc[j] = nrm2[j] > 0.0 ? 1.0 / sqrt(nrm2[j]) : 0.0;
+}
 __global__ void sub_kernel(const double* __restrict__ F, double* __restrict__ W, long long S) {
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < S;
        e += (long long)gridDim.x * blockDim.x)
@@ -253,8 +263,10 @@ cudaError_t launch_elementwise(int kind, const double* a, const double* sc, doub
   if (blocks > 8LL * num_sms()) blocks = 8LL * num_sms();
   if (kind == 0)
     colscale_kernel<<<(unsigned)blocks, 256, 0, s>>>(a, sc, b, gd.S, gd.K, gd.rr);
-  else
+  else if (kind == 1)
     sub_kernel<<<(unsigned)blocks, 256, 0, s>>>(a, b, gd.S);
+  else
+    add_kernel<<<(unsigned)blocks, 256, 0, s>>>(a, b, gd.S);
   ++g_launches;
   return cudaGetLastError();
 }
@@ -263,10 +275,12 @@ cudaError_t launch_elementwise(int kind, const double* a, const double* sc, doub
 struct GmresWs {
   long long basis, w, part, small;
 };
-bool gmres_ws_elems(const Dims& d, long long K, long long m, GmresWs& g) {
+// m = Krylov steps per cycle plus augmentation vectors (the Hessenberg dimension); the
+// basis holds m+1 orthonormal vectors, the k_aug error approximations and one correction.
+bool gmres_ws_elems(const Dims& d, long long K, long long m, GmresWs& g, long long kaug = 0) {
   bool ok = true;
   const long long S = prod({d.a, d.n, K, d.b}, ok);
-  g.basis = prod({m + 1, S}, ok);
+  g.basis = prod({m + 1 + kaug + 1, S}, ok);
   g.w = S;
   GmresDims gd = gmres_dims(d, K);
   g.part = (long long)kMaxL * K * gd.chunks;
@@ -275,41 +289,50 @@ bool gmres_ws_elems(const Dims& d, long long K, long long m, GmresWs& g) {
   return ok;
 }
 
-// The solve (host-side launch sequence; no synchronisation).
-cudaError_t enqueue_gmres(const Dims& d, long long K, long long m, long long cycles, double tol,
-                          const double* phiL, const double* A, const double* phiR,
-                          const double* F, double* X, double* rel_out, long long* its_out,
-                          void* workspace, size_t workspace_bytes, cudaStream_t s) {
+// The solve (host-side launch sequence; no synchronisation).  kaug > 0: LGMRES(m, kaug)
+// (Baker, Jessup & Manteuffel 2005): each cycle's search space is [v_0..v_{m-1}] plus the
+// kaug most recent normalised corrections z (newest first), orthonormalised into the
+// growing Arnoldi basis; the new correction becomes the newest z.
+cudaError_t enqueue_gmres(const Dims& d, long long K, long long m, long long kaug,
+                          long long cycles, double tol, const double* phiL, const double* A,
+                          const double* phiR, const double* F, double* X, double* rel_out,
+                          long long* its_out, void* workspace, size_t workspace_bytes,
+                          cudaStream_t s) {
+  const long long ms = m + kaug;   // Hessenberg dimension
   long long t1, t2, ah, pe;
   matvec_ws_elems(d, K, t1, t2, ah, pe);
   GmresWs gw;
-  gmres_ws_elems(d, K, m, gw);
+  gmres_ws_elems(d, K, ms, gw, kaug);
   Carver c{static_cast<char*>(workspace), workspace_bytes};
   double* T1 = c.take(t1);
   double* T2 = c.take(t2);
   double* Ah = c.take(ah);
   double* Pp = c.take(pe);
-  double* V = c.take(gw.basis);
+  double* V = c.take(gw.basis);   // (ms + 2) vectors: ms + 1 basis, then Z slots / correction
   double* W = c.take(gw.w);
   double* part = c.take(gw.part);
   double* sm = c.take(gw.small);
   if (!c.ok) return cudaErrorInvalidValue;
   GmresState st;
   st.H = sm;
-  st.cs = st.H + K * (m + 1) * m;
-  st.sn = st.cs + K * m;
-  st.g = st.sn + K * m;
-  st.fnorm = st.g + K * (m + 1);
+  st.cs = st.H + K * (ms + 1) * ms;
+  st.sn = st.cs + K * ms;
+  st.g = st.sn + K * ms;
+  st.fnorm = st.g + K * (ms + 1);
   st.rel = rel_out;
   st.scale = st.fnorm + K;
   st.coef = st.scale + K;
-  double* h1 = st.coef + m * K;
-  double* h2 = h1 + (m + 1) * K;
-  double* wn2 = h2 + (m + 1) * K;
+  double* h1 = st.coef + ms * K;
+  double* h2 = h1 + (ms + 1) * K;
+  double* wn2 = h2 + (ms + 1) * K;
   st.active = reinterpret_cast<int*>(wn2 + K);
   st.kcyc = st.active + K;
   st.its = its_out;
   const GmresDims gd = gmres_dims(d, K);
+  // vector slots: V_0..V_{m+nz} (Arnoldi basis, at most ms + 1), then the kaug Z slots
+  double* Zs = V + (ms + 1) * gd.S;
+  double* C = W;   // the correction reuses W after the cycle's last Arnoldi step
+  std::vector<int> zorder;   // Z slot indices, newest first
   const int kb = (int)((K + 127) / 128), kt = 128;
   cudaError_t e;
   g_stage = TT_ST_PERM;
@@ -319,17 +342,18 @@ cudaError_t enqueue_gmres(const Dims& d, long long K, long long m, long long cyc
   gmres_set_fnorm_kernel<<<kb, kt, 0, s>>>(st, wn2, (int)K);
   ++g_launches;
   for (long long cyc = 0; cyc < cycles; ++cyc) {
+    const long long nz = (long long)zorder.size();
     // r = f - L(x), beta = ||r||, v0 = r / beta
     if ((e = enqueue_matvec(d, K, phiL, A, phiR, X, W, T1, T2, Ah, Pp, pe, s, Ah)) != cudaSuccess)
       return e;
     if ((e = launch_elementwise(1, F, nullptr, W, gd, s)) != cudaSuccess) return e;
     if ((e = launch_coldots(gd, W, 1, W, part, wn2, s)) != cudaSuccess) return e;
-    gmres_cycle_init_kernel<<<kb, kt, 0, s>>>(st, wn2, (int)K, (int)m, tol);
+    gmres_cycle_init_kernel<<<kb, kt, 0, s>>>(st, wn2, (int)K, (int)ms, tol);
     ++g_launches;
     if ((e = launch_elementwise(0, W, st.scale, V, gd, s)) != cudaSuccess) return e;
-    for (long long i = 0; i < m; ++i) {
-      const double* Vi = V + i * gd.S;
-      if ((e = enqueue_matvec(d, K, phiL, A, phiR, Vi, W, T1, T2, Ah, Pp, pe, s, Ah)) !=
+    for (long long i = 0; i < m + nz; ++i) {
+      const double* in = (i < m) ? V + i * gd.S : Zs + (long long)zorder[i - m] * gd.S;
+      if ((e = enqueue_matvec(d, K, phiL, A, phiR, in, W, T1, T2, Ah, Pp, pe, s, Ah)) !=
           cudaSuccess)
         return e;
       const int L = (int)(i + 1);
@@ -339,14 +363,32 @@ cudaError_t enqueue_gmres(const Dims& d, long long K, long long m, long long cyc
       if ((e = launch_coldots(gd, V, L, W, part, h2, s)) != cudaSuccess) return e;
       if ((e = launch_colaxpy(gd, V, L, h2, -1.0, W, s)) != cudaSuccess) return e;
       if ((e = launch_coldots(gd, W, 1, W, part, wn2, s)) != cudaSuccess) return e;
-      gmres_arnoldi_kernel<<<kb, kt, 0, s>>>(st, h1, h2, wn2, (int)K, (int)m, (int)i, tol);
+      gmres_arnoldi_kernel<<<kb, kt, 0, s>>>(st, h1, h2, wn2, (int)K, (int)ms, (int)i, tol);
       ++g_launches;
       if ((e = launch_elementwise(0, W, st.scale, V + (i + 1) * gd.S, gd, s)) != cudaSuccess)
         return e;
     }
-    gmres_backsolve_kernel<<<kb, kt, 0, s>>>(st, (int)K, (int)m);
+    gmres_backsolve_kernel<<<kb, kt, 0, s>>>(st, (int)K, (int)ms);
     ++g_launches;
-    if ((e = launch_colaxpy(gd, V, (int)m, st.coef, 1.0, X, s)) != cudaSuccess) return e;
+    // correction C = sum_{i<m} y_i v_i + sum_{j<nz} y_{m+j} z_j;  x += C
+    if ((e = cudaMemsetAsync(C, 0, sizeof(double) * gd.S, s)) != cudaSuccess) return e;
+    if ((e = launch_colaxpy(gd, V, (int)m, st.coef, 1.0, C, s)) != cudaSuccess) return e;
+    for (long long j = 0; j < nz; ++j)
+      if ((e = launch_colaxpy(gd, Zs + (long long)zorder[j] * gd.S, 1, st.coef + (m + j) * K, 1.0,
+                              C, s)) != cudaSuccess)
+        return e;
+    if ((e = launch_elementwise(2, C, nullptr, X, gd, s)) != cudaSuccess) return e;
+    if (kaug > 0) {   // newest error approximation z = C / ||C||
+      if ((e = launch_coldots(gd, C, 1, C, part, wn2, s)) != cudaSuccess) return e;
+      inv_norm_kernel<<<kb, kt, 0, s>>>(wn2, st.scale, (int)K);
+      ++g_launches;
+      const int slot = (nz < kaug) ? (int)nz : zorder.back();
+      if ((e = launch_elementwise(0, C, st.scale, Zs + (long long)slot * gd.S, gd, s)) !=
+          cudaSuccess)
+        return e;
+      if (nz == kaug) zorder.pop_back();
+      zorder.insert(zorder.begin(), slot);
+    }
   }
   return cudaGetLastError();
 }

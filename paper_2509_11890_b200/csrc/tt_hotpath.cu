@@ -1563,18 +1563,18 @@ tt_status tt_local_matvec_two_site(int64_t rl, int64_t n1, int64_t n2, int64_t r
 
 // ---- local GMRES --------------------------------------------------
 size_t tt_local_gmres_workspace_size(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t Rr,
-                                     int64_t nvec, int64_t m) {
+                                     int64_t nvec, int64_t m, int64_t k_aug) {
   Dims d{rl, n, rr, Rl, Rr};
   long long t1, t2, ah, pe;
   GmresWs gw;
-  if (!dims_valid(d) || nvec <= 0 || nvec > 64 || m <= 0 || !matvec_ws_elems(d, nvec, t1, t2, ah, pe) ||
-      !gmres_ws_elems(d, nvec, m, gw))
+  if (!dims_valid(d) || nvec <= 0 || nvec > 64 || m <= 0 || k_aug < 0 ||
+      !matvec_ws_elems(d, nvec, t1, t2, ah, pe) || !gmres_ws_elems(d, nvec, m + k_aug, gw, k_aug))
     return 0;
   return ws_bytes({t1, t2, ah, pe, gw.basis, gw.w, gw.part, gw.small});
 }
 
 tt_status tt_local_gmres(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t Rr, int64_t nvec,
-                         int64_t m, int64_t cycles, double tol, const double* phiL,
+                         int64_t m, int64_t k_aug, int64_t cycles, double tol, const double* phiL,
                          const double* A, const double* phiR, const double* F, double* X,
                          double* rel_res, int64_t* iters, void* workspace,
                          size_t workspace_bytes, void* stream) {
@@ -1583,8 +1583,9 @@ tt_status tt_local_gmres(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t 
   tt_status st = check_dims(d);
   if (st != TT_OK) return st;
   if (nvec <= 0 || nvec > 64) return fail(TT_ERR_INVALID_ARGUMENT, "nvec must be in [1, 64]");
-  if (m <= 0 || m > 512 || cycles < 0 || !(tol >= 0.0))
-    return fail(TT_ERR_INVALID_ARGUMENT, "need 0 < m <= 512, cycles >= 0, tol >= 0");
+  if (m <= 0 || m > 512 || k_aug < 0 || k_aug > 64 || cycles < 0 || !(tol >= 0.0))
+    return fail(TT_ERR_INVALID_ARGUMENT,
+                "need 0 < m <= 512, 0 <= k_aug <= 64, cycles >= 0, tol >= 0");
   if (!phiL || !A || !phiR || !F || !X || !rel_res || !iters)
     return fail(TT_ERR_NULL_POINTER, "NULL pointer");
   for (const void* o : {(const void*)X, (const void*)rel_res, (const void*)iters})
@@ -1593,11 +1594,11 @@ tt_status tt_local_gmres(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t 
   if ((const void*)X == (const void*)rel_res || (const void*)X == (const void*)iters ||
       (const void*)rel_res == (const void*)iters)
     return fail(TT_ERR_ALIASING, "two outputs alias");
-  const size_t need = tt_local_gmres_workspace_size(rl, n, rr, Rl, Rr, nvec, m);
+  const size_t need = tt_local_gmres_workspace_size(rl, n, rr, Rl, Rr, nvec, m, k_aug);
   if (need == 0) return fail(TT_ERR_OVERFLOW, "workspace overflow");
   if (!workspace || workspace_bytes < need)
     return fail(TT_ERR_WORKSPACE, "workspace NULL or smaller than " + std::to_string(need) + " bytes");
-  cudaError_t e = enqueue_gmres(d, nvec, m, cycles, tol, phiL, A, phiR, F, X, rel_res,
+  cudaError_t e = enqueue_gmres(d, nvec, m, k_aug, cycles, tol, phiL, A, phiR, F, X, rel_res,
                                 reinterpret_cast<long long*>(iters), workspace, workspace_bytes,
                                 static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "tt_local_gmres");

@@ -376,17 +376,21 @@ def _mixed_canonical_system(idx, k, seed=3):
     return mixed, inp.A, pl[k], pr[k + 1], np.random.default_rng(seed)
 
 
-@pytest.mark.parametrize("idx,k,K,m,cycles", [(2, 3, 4, 12, 2), (4, 5, 3, 8, 1), (3, 1, 5, 10, 2)])
-def test_local_gmres_vs_oracle(tt, idx, k, K, m, cycles):
-    """Fixed m, cycles and tol = 0 on both sides: the iterates must agree (<= 1e-11)."""
+@pytest.mark.parametrize("idx,k,K,m,cycles,kaug", [(2, 3, 4, 12, 2, 0), (4, 5, 3, 8, 1, 0),
+                                                  (3, 1, 5, 10, 2, 0), (2, 3, 4, 5, 4, 2),
+                                                  (3, 5, 3, 6, 3, 1)])
+def test_local_gmres_vs_oracle(tt, idx, k, K, m, cycles, kaug):
+    """Fixed m, cycles (and augmentation k for LGMRES) and tol = 0 on both sides: the
+    iterates must agree (<= 1e-11) and take the same number of Arnoldi steps."""
     from oracle.gmres import local_gmres_batched
     mixed, A, phiL, phiR, rng = _mixed_canonical_system(idx, k)
     rl, n, rr = mixed[k].shape
     F = rng.standard_normal((rl, n, K, rr))
     X0 = 0.1 * rng.standard_normal((rl, n, K, rr))
-    Xo, relo, itso = local_gmres_batched(phiL, A[k], phiR, F, X0, m=m, cycles=cycles, tol=0.0)
+    Xo, relo, itso = local_gmres_batched(phiL, A[k], phiR, F, X0, m=m, cycles=cycles, tol=0.0,
+                                         k=kaug)
     Xg, relg, itsg = tt.tt_local_gmres(g(phiL), g(A[k]), g(phiR), g(F), g(X0.copy()), m=m,
-                                       cycles=cycles, tol=0.0)
+                                       cycles=cycles, tol=0.0, k_aug=kaug)
     torch.cuda.synchronize()
     for j in range(K):
         assert rel(h(Xg)[:, :, j, :], Xo[:, :, j, :]) <= TOL, j
