@@ -144,6 +144,30 @@ tt_status tt_operator_apply(int64_t d, const int64_t* n_row, const int64_t* n_co
                             double* const* z_cores, void* stream);
 
 /* ---------------------------------------------------------------------------------------
+ * projected KKT block system action: several
+ * operators sharing one frame W_{!=k} act on a Block-TT core whose block index is the KKT
+ * component (Delta X_k, Delta Y_k, Delta T_k):
+ *   Y[:, :, row, :] = sum_{terms with this row} coeff * L_op( L_op2( X[:, :, col, :] ) )
+ * with L_o the projected operator of operator o (its own interfaces phiL[o] (rl,Rl[o],rl),
+ * phiR[o] (rr,Rr[o],rr) and core A[o] (Rl[o],n,n,Rr[o])); op2 = -1 means a single operator,
+ * op2 >= 0 a product of two projected operators, e.g. (W^T L_X W)(W^T A_eq^T W).
+ *   X, Y (rl, n, nblocks, rr); Rl, Rr, phiL, A, phiR, terms are HOST arrays (pointers in
+ *   them are device pointers).  Workspace: tt_block_local_matvec_workspace_size(...).
+ * ------------------------------------------------------------------------------------- */
+typedef struct {
+  int64_t row, col, op, op2;
+  double coeff;
+} tt_block_term;
+size_t tt_block_local_matvec_workspace_size(int64_t rl, int64_t n, int64_t rr, int64_t nops,
+                                            const int64_t* Rl, const int64_t* Rr);
+tt_status tt_block_local_matvec(int64_t rl, int64_t n, int64_t rr, int64_t nblocks, int64_t nops,
+                                const int64_t* Rl, const int64_t* Rr, const double* const* phiL,
+                                const double* const* A, const double* const* phiR,
+                                int64_t nterms, const tt_block_term* terms, const double* X,
+                                double* Y, void* workspace, size_t workspace_bytes,
+                                void* stream);
+
+/* ---------------------------------------------------------------------------------------
  * two-site (DMRG supercore) local matvec: the projected operator of a
  * PAIR of neighbouring cores ("operates on pairs of neighbouring cores simultaneously",
  * PAPER.md:556-567) applied to nvec supercores:

@@ -160,3 +160,20 @@ def local_matvec_two_site(phiL, A1, A2, phiR, w):
     _check(lib().tt_oracle_local_matvec_two_site(rl, n1, n2, rr, Rl, Rm, Rr, _p(phiL), _p(A1),
                                                  _p(A2), _p(phiR), _p(w), _p(y)))
     return y
+
+
+def block_local_matvec(ops, terms, X):
+    """the projected KKT block system acting on a
+    Block-TT core X (rl, n, nblocks, rr) whose block index is the KKT component:
+        Y[:, :, row, :] = sum over terms (row, col, op, op2, coeff) of
+                          coeff * L_op( L_op2( X[:, :, col, :] ) )   (op2 = -1: L_op only)
+    where L_o is the projected operator of ops[o] = (phiL, A, phiR) (all sharing the frame).
+    Plain loops over the terms; each L_o is tt_oracle_local_matvec."""
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    Y = np.zeros_like(X)
+    for (row, col, op, op2, coeff) in terms:
+        v = np.ascontiguousarray(X[:, :, col, :])
+        if op2 >= 0:
+            v = local_matvec(*ops[op2], v)
+        Y[:, :, row, :] += coeff * local_matvec(*ops[op], v)
+    return Y

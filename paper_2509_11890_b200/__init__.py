@@ -26,6 +26,7 @@ __all__ = [
     "tt_trace_count", "tt_trace_read", "tt_fp64_peak_probe", "STAGE_NAMES", "tt_debug_force_v1",
     "tt_debug_set_variant", "tt_debug_set_flags", "tt_local_gmres", "tt_local_gmres_workspace_size",
     "tt_local_matvec_two_site", "tt_local_matvec_two_site_workspace_size",
+    "tt_block_local_matvec", "tt_block_local_matvec_workspace_size", "TTBlockTerm",
 ]
 
 STAGE_NAMES = {0: "perm", 1: "set", 2: "mv_s1", 3: "mv_s2", 4: "mv_s3", 5: "il_s1", 6: "il_s2",
@@ -65,6 +66,16 @@ lib.tt_trace_enable.argtypes = [_i64]
 lib.tt_trace_count.restype = ctypes.c_int64
 lib.tt_trace_read.argtypes = [_i64] + [_p] * 6
 lib.tt_fp64_peak_probe.argtypes = [_i64, _p, _p]
+class TTBlockTerm(ctypes.Structure):
+    """tt_block_term: Y[row] += coeff * L_op(L_op2(X[col])) (op2 = -1: single operator)."""
+    _fields_ = [("row", ctypes.c_int64), ("col", ctypes.c_int64), ("op", ctypes.c_int64),
+                ("op2", ctypes.c_int64), ("coeff", ctypes.c_double)]
+
+
+lib.tt_block_local_matvec_workspace_size.restype = _sz
+lib.tt_block_local_matvec_workspace_size.argtypes = [_i64] * 4 + [_p, _p]
+lib.tt_block_local_matvec.argtypes = [_i64] * 5 + [_p] * 5 + [_i64, _p, _p, _p, _p, _sz, _p]
+lib.tt_block_local_matvec.restype = ctypes.c_int
 lib.tt_local_matvec_two_site_workspace_size.restype = _sz
 lib.tt_local_matvec_two_site_workspace_size.argtypes = [_i64] * 8
 lib.tt_local_matvec_two_site.argtypes = [_i64] * 8 + [_p] * 7 + [_sz, _p]
@@ -365,4 +376,30 @@ def tt_local_matvec_two_site(phiL, A1, A2, phiR, W, Y=None, workspace=None, stre
                                         _dev(A1, "A1"), _dev(A2, "A2"), _dev(phiR, "phiR"),
                                         _dev(W, "W"), _dev(Y, "Y"), ws.data_ptr(), ws.numel(),
                                         _stream(stream)))
+    return Y
+
+
+def tt_block_local_matvec_workspace_size(rl, n, rr, Rl, Rr) -> int:
+    a64 = lambda v: (ctypes.c_int64 * len(v))(*v)
+    return int(lib.tt_block_local_matvec_workspace_size(rl, n, rr, len(Rl), a64(Rl), a64(Rr)))
+
+
+def tt_block_local_matvec(ops, terms, X, Y=None, workspace=None, stream=None):
+    """Projected KKT block action.  ops: list of (phiL, A, phiR) device
+    tensors sharing the frame; terms: list of (row, col, op, op2, coeff); X (rl, n, nb, rr)."""
+    rl, n, nb, rr = X.shape
+    Rl = [int(o[1].shape[0]) for o in ops]
+    Rr = [int(o[1].shape[3]) for o in ops]
+    if Y is None:
+        Y = torch.empty_like(X)
+    a64 = lambda v: (ctypes.c_int64 * len(v))(*v)
+    T = (TTBlockTerm * max(len(terms), 1))(*[TTBlockTerm(int(r), int(c), int(o), int(o2), float(cf))
+                                             for (r, c, o, o2, cf) in terms])
+    ws = _ws(tt_block_local_matvec_workspace_size(rl, n, rr, Rl, Rr), workspace, X.device)
+    _check(lib.tt_block_local_matvec(rl, n, rr, nb, len(ops), a64(Rl), a64(Rr),
+                                     _ptrs([o[0] for o in ops], "phiL"),
+                                     _ptrs([o[1] for o in ops], "A"),
+                                     _ptrs([o[2] for o in ops], "phiR"), len(terms), T,
+                                     _dev(X, "X"), _dev(Y, "Y"), ws.data_ptr(), ws.numel(),
+                                     _stream(stream)))
     return Y

@@ -960,6 +960,27 @@ bool same(const void* p, const void* q) { return p != nullptr && p == q; }
 
 #include "tt_gmres.cuh"
 
+// Block-TT column gather / scaled scatter-add: column `col` of X (rows, nb, rr) <-> v (rows, rr)
+__global__ void gather_col_kernel(const double* __restrict__ X, double* __restrict__ v,
+                                  long long rows, int nb, int rr, int col) {
+  const long long tot = rows * rr;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long row = e / rr, b = e - row * rr;
+    v[e] = X[(row * nb + col) * rr + b];
+  }
+}
+__global__ void scatter_add_col_kernel(const double* __restrict__ v, double* __restrict__ Y,
+                                       long long rows, int nb, int rr, int row_blk, double c) {
+  const long long tot = rows * rr;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long row = e / rr, b = e - row * rr;
+    double* y = Y + (row * nb + row_blk) * rr + b;
+    *y = fma(c, v[e], *y);
+  }
+}
+
 // Two-site supercore operator: A12[al, (i1 i2), (j1 j2), be] = sum_g A1[al,i1,j1,g] A2[g,i2,j2,be]
 // (the local operator of a pair of cores; tiny, one thread per output)
 __global__ void merge_cores_kernel(const double* __restrict__ A1, const double* __restrict__ A2,
@@ -1504,6 +1525,102 @@ tt_status tt_operator_apply(int64_t d, const int64_t* n_row, const int64_t* n_co
     ++g_launches;
     if (e != cudaSuccess) return cuda_fail(e, "tt_operator_apply");
   }
+  return TT_OK;
+}
+
+// ---- projected KKT block system action -----------------------------
+static bool block_ws(int64_t rl, int64_t n, int64_t rr, int64_t nops, const int64_t* Rl,
+                     const int64_t* Rr, long long& t1, long long& t2, long long& ah, long long& pe,
+                     long long& vec) {
+  t1 = t2 = ah = pe = 0;
+  bool ok = true;
+  for (int64_t o = 0; o < nops; ++o) {
+    Dims d{rl, n, rr, Rl[o], Rr[o]};
+    long long a, b, c, e;
+    if (!dims_valid(d) || !matvec_ws_elems(d, 1, a, b, c, e)) return false;
+    t1 = std::max(t1, a);
+    t2 = std::max(t2, b);
+    ah = std::max(ah, c);
+    pe = std::max(pe, e);
+  }
+  vec = prod({rl, n, rr}, ok);
+  return ok;
+}
+
+size_t tt_block_local_matvec_workspace_size(int64_t rl, int64_t n, int64_t rr, int64_t nops,
+                                            const int64_t* Rl, const int64_t* Rr) {
+  if (nops <= 0 || !Rl || !Rr) return 0;
+  long long t1, t2, ah, pe, vec;
+  if (!block_ws(rl, n, rr, nops, Rl, Rr, t1, t2, ah, pe, vec)) return 0;
+  return ws_bytes({t1, t2, ah, pe, vec, vec, vec});
+}
+
+tt_status tt_block_local_matvec(int64_t rl, int64_t n, int64_t rr, int64_t nblocks, int64_t nops,
+                                const int64_t* Rl, const int64_t* Rr, const double* const* phiL,
+                                const double* const* A, const double* const* phiR,
+                                int64_t nterms, const tt_block_term* terms, const double* X,
+                                double* Y, void* workspace, size_t workspace_bytes,
+                                void* stream) {
+  CallScope scope;
+  if (rl <= 0 || n <= 0 || rr <= 0 || nblocks <= 0 || nops <= 0 || nterms < 0)
+    return fail(TT_ERR_INVALID_ARGUMENT, "extents must be positive");
+  if (!Rl || !Rr || !phiL || !A || !phiR || !X || !Y || (nterms > 0 && !terms))
+    return fail(TT_ERR_NULL_POINTER, "NULL argument");
+  for (int64_t o = 0; o < nops; ++o) {
+    if (!phiL[o] || !A[o] || !phiR[o]) return fail(TT_ERR_NULL_POINTER, "NULL operator entry");
+    tt_status st = check_dims(Dims{rl, n, rr, Rl[o], Rr[o]});
+    if (st != TT_OK) return st;
+    if (same(Y, phiL[o]) || same(Y, A[o]) || same(Y, phiR[o]))
+      return fail(TT_ERR_ALIASING, "output Y aliases an operator");
+  }
+  if (same(Y, X)) return fail(TT_ERR_ALIASING, "output Y aliases X");
+  for (int64_t t = 0; t < nterms; ++t) {
+    const tt_block_term& tm = terms[t];
+    if (tm.row < 0 || tm.row >= nblocks || tm.col < 0 || tm.col >= nblocks || tm.op < 0 ||
+        tm.op >= nops || tm.op2 < -1 || tm.op2 >= nops)
+      return fail(TT_ERR_INVALID_ARGUMENT, "term " + std::to_string(t) + " out of range");
+  }
+  long long t1, t2, ah, pe, vec;
+  if (!block_ws(rl, n, rr, nops, Rl, Rr, t1, t2, ah, pe, vec))
+    return fail(TT_ERR_OVERFLOW, "workspace overflow");
+  const size_t need = ws_bytes({t1, t2, ah, pe, vec, vec, vec});
+  if (!workspace || workspace_bytes < need)
+    return fail(TT_ERR_WORKSPACE, "workspace NULL or smaller than " + std::to_string(need) + " bytes");
+  Carver c{static_cast<char*>(workspace), workspace_bytes};
+  double* T1 = c.take(t1);
+  double* T2 = c.take(t2);
+  double* Ah = c.take(ah);
+  double* Pp = c.take(pe);
+  double* G = c.take(vec);
+  double* G2 = c.take(vec);
+  double* Tv = c.take(vec);
+  if (!c.ok) return fail(TT_ERR_WORKSPACE, "workspace too small after alignment");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const long long rows = rl * n;
+  long long blocks = (vec + 255) / 256;
+  if (blocks > 4L * num_sms()) blocks = 4L * num_sms();
+  cudaError_t e = cudaMemsetAsync(Y, 0, sizeof(double) * rows * nblocks * rr, s);
+  for (int64_t t = 0; t < nterms && e == cudaSuccess; ++t) {
+    const tt_block_term& tm = terms[t];
+    gather_col_kernel<<<(unsigned)blocks, 256, 0, s>>>(X, G, rows, (int)nblocks, (int)rr,
+                                                       (int)tm.col);
+    ++g_launches;
+    const double* in = G;
+    if (tm.op2 >= 0) {
+      const Dims d2{rl, n, rr, Rl[tm.op2], Rr[tm.op2]};
+      e = enqueue_matvec(d2, 1, phiL[tm.op2], A[tm.op2], phiR[tm.op2], G, G2, T1, T2, Ah, Pp, pe, s);
+      in = G2;
+    }
+    if (e != cudaSuccess) break;
+    const Dims d1{rl, n, rr, Rl[tm.op], Rr[tm.op]};
+    e = enqueue_matvec(d1, 1, phiL[tm.op], A[tm.op], phiR[tm.op], in, Tv, T1, T2, Ah, Pp, pe, s);
+    if (e != cudaSuccess) break;
+    scatter_add_col_kernel<<<(unsigned)blocks, 256, 0, s>>>(Tv, Y, rows, (int)nblocks, (int)rr,
+                                                            (int)tm.row, tm.coeff);
+    ++g_launches;
+    e = cudaGetLastError();
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "tt_block_local_matvec");
   return TT_OK;
 }
 

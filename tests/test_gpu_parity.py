@@ -452,3 +452,29 @@ def test_two_site_matvec_vs_oracle(tt, shape):
     for m in range(nvec):
         ref = oracle.local_matvec_two_site(phiL, A1, A2, phiR, np.ascontiguousarray(W[:, :, :, m, :]))
         assert rel(h(Y)[:, :, :, m, :], ref) <= TOL, m
+
+
+# ----------------------------------------------------------------------------------------
+# projected KKT block system action vs the oracle
+# ----------------------------------------------------------------------------------------
+KKT_TERMS = [(0, 0, 0, -1, -1.0), (0, 1, 1, -1, 1.0), (1, 0, 2, -1, -1.0), (1, 2, 3, -1, 1.0),
+             (2, 0, 4, -1, 1.0), (2, 1, 5, 6, 1.0), (2, 2, 5, 7, 1.0)]
+
+
+@pytest.mark.parametrize("rl,n,rr,Rmax", [(5, 4, 7, 3), (64, 4, 96, 16), (129, 4, 128, 25)])
+def test_block_local_matvec_vs_oracle(tt, rl, n, rr, Rmax):
+    import oracle
+    rng = np.random.default_rng(rl + rr)
+    ops_h, ops_d = [], []
+    for o in range(8):
+        Rl_, Rr_ = int(rng.integers(1, Rmax + 1)), int(rng.integers(1, Rmax + 1))
+        op = (rng.standard_normal((rl, Rl_, rl)), rng.standard_normal((Rl_, n, n, Rr_)),
+              rng.standard_normal((rr, Rr_, rr)))
+        ops_h.append(op)
+        ops_d.append(tuple(g(a) for a in op))
+    X = rng.standard_normal((rl, n, 3, rr))
+    Y = tt.tt_block_local_matvec(ops_d, KKT_TERMS, g(X))
+    torch.cuda.synchronize()
+    ref = oracle.block_local_matvec(ops_h, KKT_TERMS, X)
+    for b in range(3):
+        assert rel(h(Y)[:, :, b, :], ref[:, :, b, :]) <= TOL, b

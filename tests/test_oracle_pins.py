@@ -430,3 +430,48 @@ def test_two_site_merged_supercore_energy():
         w = np.einsum("aib,bjc->aijc", x[k], x[k + 1])
         y = oracle.local_matvec_two_site(pl[k], A[k], A[k + 1], pr[k + 2], w)
         assert abs(np.vdot(w, y) - e) <= 1e-12 * abs(e)
+
+
+# --------------------------------------------------------------------------------------
+# projected KKT block system
+# --------------------------------------------------------------------------------------
+KKT_TERMS = [  # (row, col, op, op2, coeff): the 3x3 system of PAPER.md:460-472
+    (0, 0, 0, -1, -1.0),   # -W^T A_eq W
+    (0, 1, 1, -1, 1.0),    #  W^T K_Y W
+    (1, 0, 2, -1, -1.0),   # -W^T T A_ineq W
+    (1, 2, 3, -1, 1.0),    #  W^T (R_ineq + K_T) W
+    (2, 0, 4, -1, 1.0),    #  W^T L_Z W
+    (2, 1, 5, 6, 1.0),     # (W^T L_X W)(W^T A_eq^T W)
+    (2, 2, 5, 7, 1.0),     # (W^T L_X W)(W^T A_ineq^T W)
+]
+
+
+def test_block_local_matvec_dense():
+    """The block action equals the dense 3x3 block matrix of projected operators (each
+    X_{!=k}^T A_o X_{!=k} with the shared frame) times the block vector."""
+    rng = np.random.default_rng(101)
+    d, N = 4, 4
+    r = [1, 4, 6, 4, 1]
+    x = ttgen.gaussian_tt_vector(rng, N, r)
+    Rs = [[1, 2, 3, 2, 1], [1, 1, 2, 1, 1], [1, 3, 2, 3, 1], [1, 2, 2, 2, 1],
+          [1, 2, 3, 2, 1], [1, 3, 3, 3, 1], [1, 2, 1, 2, 1], [1, 1, 3, 1, 1]]
+    Aops = [ttgen.gaussian_tt_matrix(rng, N, N, R) for R in Rs]
+    k = 2
+    ops = []
+    dense = []
+    for A in Aops:
+        pl, pr = oracle.sweep_interfaces(x, A)
+        ops.append((pl[k], A[k], pr[k + 1]))
+        dense.append(projected_operator(x, full_matrix(A), k))
+    nb = 3
+    X = rng.standard_normal((r[k], N, nb, r[k + 1]))
+    Y = oracle.block_local_matvec(ops, KKT_TERMS, X)
+    m = r[k] * N * r[k + 1]
+    big = np.zeros((nb * m, nb * m))
+    for (row, col, op, op2, c) in KKT_TERMS:
+        blk = dense[op] @ (dense[op2] if op2 >= 0 else np.eye(m))
+        big[row * m:(row + 1) * m, col * m:(col + 1) * m] += c * blk
+    xv = np.concatenate([X[:, :, b, :].ravel() for b in range(nb)])
+    yv = big @ xv
+    for b in range(nb):
+        assert rel_fro(Y[:, :, b, :].ravel(), yv[b * m:(b + 1) * m]) < TOL_DENSE
