@@ -504,6 +504,41 @@ def main():
               "tflops": (mv_f + orth_f) / (t["graph_ms_median"] * 1e-3) / 1e12,
               "matvec_share_of_flops": mv_f / (mv_f + orth_f)}
 
+    # ---- SURVEY 8(f) rows 2 and 4 on the interior core: KKT block action, two-site matvec --
+    kkt = two = None
+    if not args.no_sweeps:
+        k = cfg.d // 2
+        rl, nn, rr = cfg.r[k], cfg.N, cfg.r[k + 1]
+        Rl, Rr = cfg.R[k], cfg.R[k + 1]
+        gen = torch.Generator(device=dev).manual_seed(11)
+        rnd = lambda *sh: torch.randn(*sh, dtype=torch.float64, device=dev, generator=gen)
+        ops = [(rnd(rl, Rl, rl), rnd(Rl, nn, nn, Rr), rnd(rr, Rr, rr)) for _ in range(8)]
+        terms = [(0, 0, 0, -1, -1.0), (0, 1, 1, -1, 1.0), (1, 0, 2, -1, -1.0),
+                 (1, 2, 3, -1, 1.0), (2, 0, 4, -1, 1.0), (2, 1, 5, 6, 1.0), (2, 2, 5, 7, 1.0)]
+        Xk = rnd(rl, nn, 3, rr)
+        Yk = torch.empty_like(Xk)
+        wsk = torch.empty(tt.tt_block_local_matvec_workspace_size(rl, nn, rr, [Rl] * 8, [Rr] * 8),
+                          dtype=torch.uint8, device=dev)
+        t = time_sweep(tt, lambda st: tt.tt_block_local_matvec(ops, terms, Xk, Yk, workspace=wsk,
+                                                              stream=st), stream, dev, reps=5)
+        f9 = 9 * f_local(rl, nn, rr, Rl, Rr)
+        kkt = {"core": k, "operators": 8, "terms": len(terms), "matvecs": 9,
+               "ms": t["graph_ms_median"], "gflop": f9 / 1e9,
+               "tflops": f9 / (t["graph_ms_median"] * 1e-3) / 1e12}
+        # two-site (DMRG supercore) matvec: 2x2 modes (N = 4), bonds of the interior core
+        A1, A2 = rnd(Rl, 2, 2, Rl), rnd(Rl, 2, 2, Rr)
+        W2 = rnd(rl, 2, 2, cfg.nvec, rr)
+        Y2 = torch.empty_like(W2)
+        ws2 = torch.empty(tt.tt_local_matvec_two_site_workspace_size(rl, 2, 2, rr, Rl, Rl, Rr,
+                                                                     cfg.nvec),
+                          dtype=torch.uint8, device=dev)
+        t = time_sweep(tt, lambda st: tt.tt_local_matvec_two_site(phiL[k], A1, A2, phiR[k + 1], W2,
+                                                                  Y2, workspace=ws2, stream=st),
+                       stream, dev, reps=5)
+        f2 = cfg.nvec * f_local(rl, 4, rr, Rl, Rr)
+        two = {"core": k, "n1": 2, "n2": 2, "nvec": cfg.nvec, "ms": t["graph_ms_median"],
+               "gflop": f2 / 1e9, "tflops": f2 / (t["graph_ms_median"] * 1e-3) / 1e12}
+
     # ---- full sweeps at d = 12 (metric's second half), eager and as a CUDA graph ---------
     sweeps = None
     if not args.no_sweeps:
@@ -563,6 +598,8 @@ def main():
             "clocks": clk,
             "sweeps_d12": sweeps,
             "local_gmres": gm,
+            "kkt_block_action": kkt,
+            "two_site_matvec": two,
             "detail": {
                 "full_sweep_ms": (total_ms / args.steps) - (apply_detail["ms_per_step"]
                                                             if apply_detail else 0.0),
