@@ -144,6 +144,31 @@ tt_status tt_operator_apply(int64_t d, const int64_t* n_row, const int64_t* n_co
                             double* const* z_cores, void* stream);
 
 /* ---------------------------------------------------------------------------------------
+ * TT rounding ("TT rounding ... to construct an
+ * approximation subject to a specified error tolerance delta"; one of its steps moves the
+ * block index between cores): Oseledets' algorithm, right-to-left
+ * orthonormalisation then left-to-right truncation with per-core threshold
+ * delta / sqrt(d-1) * ||T||_F (optionally capped at max_rank > 0), so that
+ * ||T - round(T)||_F <= delta ||T||_F.  Every SVD is taken through the core unfolding's Gram
+ * matrix (DMMA GEMM + a one-CTA parallel Jacobi eigensolver); numerically zero directions
+ * (Gram eigenvalue <= 1e-14 of the largest) are dropped, which bounds the attainable
+ * accuracy at ~1e-7 relative (fine for the paper's delta = 1e-4).
+ * cores_in[k] (r_in[k], n[k], r_in[k+1]) device, not modified; cores_out[k] device buffers of
+ * at least the input core's size; r_out[d+1] (host) receives the new ranks.  Ranks <= 512.
+ * SYNCHRONOUS: the truncation ranks are data dependent (one host read per core).
+ * ------------------------------------------------------------------------------------- */
+size_t tt_round_workspace_size(int64_t d, const int64_t* n, const int64_t* r);
+/* Test hook: eigendecomposition of a symmetric n x n matrix G (overwritten; n <= 512) by the
+ * rounding's parallel Jacobi solver: V columns = eigenvectors, lam descending.  Workspace
+ * >= (n^2 + n) doubles. */
+tt_status tt_debug_sym_eigen(int64_t n, double* G, double* V, double* lam, void* workspace,
+                             size_t workspace_bytes, void* stream);
+tt_status tt_round(int64_t d, const int64_t* n, const int64_t* r_in,
+                   const double* const* cores_in, double delta, int64_t max_rank, int64_t* r_out,
+                   double* const* cores_out, void* workspace, size_t workspace_bytes,
+                   void* stream);
+
+/* ---------------------------------------------------------------------------------------
  * projected KKT block system action: several
  * operators sharing one frame W_{!=k} act on a Block-TT core whose block index is the KKT
  * component (Delta X_k, Delta Y_k, Delta T_k):

@@ -27,6 +27,7 @@ __all__ = [
     "tt_debug_set_variant", "tt_debug_set_flags", "tt_local_gmres", "tt_local_gmres_workspace_size",
     "tt_local_matvec_two_site", "tt_local_matvec_two_site_workspace_size",
     "tt_block_local_matvec", "tt_block_local_matvec_workspace_size", "TTBlockTerm",
+    "tt_round", "tt_round_workspace_size", "tt_debug_sym_eigen",
 ]
 
 STAGE_NAMES = {0: "perm", 1: "set", 2: "mv_s1", 3: "mv_s2", 4: "mv_s3", 5: "il_s1", 6: "il_s2",
@@ -72,6 +73,12 @@ class TTBlockTerm(ctypes.Structure):
                 ("op2", ctypes.c_int64), ("coeff", ctypes.c_double)]
 
 
+lib.tt_round_workspace_size.restype = _sz
+lib.tt_round_workspace_size.argtypes = [_i64, _p, _p]
+lib.tt_round.argtypes = [_i64, _p, _p, _p, ctypes.c_double, _i64, _p, _p, _p, _sz, _p]
+lib.tt_round.restype = ctypes.c_int
+lib.tt_debug_sym_eigen.argtypes = [_i64, _p, _p, _p, _p, _sz, _p]
+lib.tt_debug_sym_eigen.restype = ctypes.c_int
 lib.tt_block_local_matvec_workspace_size.restype = _sz
 lib.tt_block_local_matvec_workspace_size.argtypes = [_i64] * 4 + [_p, _p]
 lib.tt_block_local_matvec.argtypes = [_i64] * 5 + [_p] * 5 + [_i64, _p, _p, _p, _p, _sz, _p]
@@ -403,3 +410,38 @@ def tt_block_local_matvec(ops, terms, X, Y=None, workspace=None, stream=None):
                                      _dev(X, "X"), _dev(Y, "Y"), ws.data_ptr(), ws.numel(),
                                      _stream(stream)))
     return Y
+
+
+def tt_round(cores, delta, max_rank=0, workspace=None, stream=None):
+    """TT rounding of a TT vector (list of device cores (r_k, n_k, r_{k+1})) to relative
+    accuracy delta.  Synchronous.  Returns the list of rounded cores."""
+    d = len(cores)
+    a64 = lambda v: (ctypes.c_int64 * len(v))(*v)
+    n = [int(c.shape[1]) for c in cores]
+    r = [int(c.shape[0]) for c in cores] + [int(cores[-1].shape[2])]
+    outs = [torch.empty_like(c) for c in cores]
+    rout = (ctypes.c_int64 * (d + 1))()
+    ws = _ws(int(lib.tt_round_workspace_size(d, a64(n), a64(r))), workspace, cores[0].device)
+    _check(lib.tt_round(d, a64(n), a64(r), _ptrs(cores, "cores"), float(delta), int(max_rank),
+                        rout, _ptrs(outs, "cores_out"), ws.data_ptr(), ws.numel(), _stream(stream)))
+    ro = list(rout)
+    return [outs[k].reshape(-1)[: ro[k] * n[k] * ro[k + 1]].reshape(ro[k], n[k], ro[k + 1])
+            for k in range(d)]
+
+
+def tt_round_workspace_size(n, r) -> int:
+    a64 = lambda v: (ctypes.c_int64 * len(v))(*v)
+    return int(lib.tt_round_workspace_size(len(n), a64(n), a64(r)))
+
+
+def tt_debug_sym_eigen(G, stream=None):
+    """Eigendecomposition of a symmetric CUDA float64 matrix by the rounding's Jacobi solver.
+    Returns (lam descending, V)."""
+    n = int(G.shape[0])
+    Gc = G.clone()
+    V = torch.empty_like(Gc)
+    lam = torch.empty(n, dtype=torch.float64, device=G.device)
+    ws = torch.empty((n * n + n) * 8, dtype=torch.uint8, device=G.device)
+    _check(lib.tt_debug_sym_eigen(n, _dev(Gc, "G"), _dev(V, "V"), _dev(lam, "lam"), ws.data_ptr(),
+                                  ws.numel(), _stream(stream)))
+    return lam, V

@@ -959,6 +959,23 @@ tt_status check_dims(const Dims& d) {
 bool same(const void* p, const void* q) { return p != nullptr && p == q; }
 
 #include "tt_gmres.cuh"
+#include "tt_round.cuh"
+
+// Symmetric eigendecomposition of the n x n Gram matrix G (overwritten): lam (descending)
+// and V (columns) in the caller's buffers; d, Vtmp are scratch.
+cudaError_t launch_sym_eigen(double* G, double* Vtmp, double* V, double* d, double* lam, int n,
+                             cudaStream_t s) {
+  const int np = (n + 1) & ~1;
+  const size_t smem = (size_t)np / 2 * (2 * sizeof(double) + 2 * sizeof(int));
+  g_stage = TT_ST_PERM;
+  const long long tr = trace_begin(0, (long long)n * n, 0, 0, s);
+  jacobi_eigen_kernel<<<1, 1024, smem, s>>>(G, Vtmp, n, 30);
+  diag_kernel<<<(n + 255) / 256, 256, 0, s>>>(G, d, n);
+  sort_eigvecs_kernel<<<(n + 255) / 256, 256, 0, s>>>(Vtmp, d, V, lam, n);
+  trace_end(tr, s);
+  g_launches += 3;
+  return cudaGetLastError();
+}
 
 // Block-TT column gather / scaled scatter-add: column `col` of X (rows, nb, rr) <-> v (rows, rr)
 __global__ void gather_col_kernel(const double* __restrict__ X, double* __restrict__ v,
@@ -1525,6 +1542,182 @@ tt_status tt_operator_apply(int64_t d, const int64_t* n_row, const int64_t* n_co
     ++g_launches;
     if (e != cudaSuccess) return cuda_fail(e, "tt_operator_apply");
   }
+  return TT_OK;
+}
+
+// test hook: symmetric eigendecomposition of an n x n matrix (G overwritten), lam descending
+tt_status tt_debug_sym_eigen(int64_t n, double* G, double* V, double* lam, void* workspace,
+                             size_t workspace_bytes, void* stream) {
+  CallScope scope;
+  if (n <= 0 || n > 512) return fail(TT_ERR_INVALID_ARGUMENT, "0 < n <= 512");
+  if (!G || !V || !lam || !workspace) return fail(TT_ERR_NULL_POINTER, "NULL pointer");
+  if (workspace_bytes < (size_t)(n * n + n) * 8) return fail(TT_ERR_WORKSPACE, "workspace");
+  double* Vt = static_cast<double*>(workspace);
+  double* dg = Vt + n * n;
+  cudaError_t e = launch_sym_eigen(G, Vt, V, dg, lam, (int)n, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "tt_debug_sym_eigen");
+  return TT_OK;
+}
+
+// ---- TT rounding ------------------------------------------------------
+size_t tt_round_workspace_size(int64_t d, const int64_t* n, const int64_t* r) {
+  if (d <= 0 || !n || !r) return 0;
+  long long core_max = 0, rmax = 0, tot = 0;
+  bool ok = true;
+  for (int64_t k = 0; k < d; ++k) {
+    const long long sz = prod({r[k], n[k], r[k + 1]}, ok);
+    core_max = std::max(core_max, sz);
+    tot += align_up((size_t)sz * 8, 256) / 8 + 32;
+  }
+  for (int64_t k = 0; k <= d; ++k) rmax = std::max<long long>(rmax, r[k]);
+  if (!ok) return 0;
+  // working cores, one temp core, G, Vtmp, V, Bm (rmax^2 each), d, lam (rmax)
+  return ws_bytes({tot, core_max, rmax * rmax, rmax * rmax, rmax * rmax, rmax * rmax, rmax, rmax});
+}
+
+tt_status tt_round(int64_t d, const int64_t* n, const int64_t* r_in,
+                   const double* const* cores_in, double delta, int64_t max_rank, int64_t* r_out,
+                   double* const* cores_out, void* workspace, size_t workspace_bytes,
+                   void* stream) {
+  CallScope scope;
+  if (d <= 0) return fail(TT_ERR_INVALID_ARGUMENT, "d must be >= 1");
+  if (!n || !r_in || !cores_in || !r_out || !cores_out) return fail(TT_ERR_NULL_POINTER, "NULL array");
+  if (r_in[0] != 1 || r_in[d] != 1) return fail(TT_ERR_INVALID_ARGUMENT, "r_1 and r_{d+1} must be 1");
+  if (!(delta >= 0.0)) return fail(TT_ERR_INVALID_ARGUMENT, "delta must be >= 0");
+  long long rmax = 0;
+  for (int64_t k = 0; k < d; ++k) {
+    if (n[k] <= 0 || r_in[k] <= 0) return fail(TT_ERR_INVALID_ARGUMENT, "extents must be positive");
+    if (!cores_in[k] || !cores_out[k]) return fail(TT_ERR_NULL_POINTER, "NULL core");
+    for (int64_t q = 0; q < d; ++q)
+      if ((const void*)cores_out[k] == (const void*)cores_in[q])
+        return fail(TT_ERR_ALIASING, "an output core aliases an input core");
+    rmax = std::max<long long>(rmax, r_in[k]);
+  }
+  if (rmax > 512) return fail(TT_ERR_INVALID_ARGUMENT, "ranks above 512 are not supported");
+  const size_t need = tt_round_workspace_size(d, n, r_in);
+  if (need == 0) return fail(TT_ERR_OVERFLOW, "workspace overflow");
+  if (!workspace || workspace_bytes < need)
+    return fail(TT_ERR_WORKSPACE, "workspace NULL or smaller than " + std::to_string(need) + " bytes");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Carver c{static_cast<char*>(workspace), workspace_bytes};
+  std::vector<double*> W(d);
+  long long core_max = 0;
+  for (int64_t k = 0; k < d; ++k) {
+    const long long sz = r_in[k] * n[k] * r_in[k + 1];
+    W[k] = c.take(sz);
+    core_max = std::max(core_max, sz);
+  }
+  double* Tmp = c.take(core_max);
+  double* G = c.take(rmax * rmax);
+  double* Vt = c.take(rmax * rmax);
+  double* V = c.take(rmax * rmax);
+  double* Bm = c.take(rmax * rmax);
+  double* dg = c.take(rmax);
+  double* lam = c.take(rmax);
+  if (!c.ok) return fail(TT_ERR_WORKSPACE, "workspace too small after alignment");
+  std::vector<long long> r(r_in, r_in + d + 1);
+  cudaError_t e = cudaSuccess;
+  for (int64_t k = 0; k < d && e == cudaSuccess; ++k)
+    e = cudaMemcpyAsync(W[k], cores_in[k], sizeof(double) * r[k] * n[k] * r[k + 1],
+                        cudaMemcpyDeviceToDevice, s);
+  std::vector<double> hl(rmax);
+  auto eig = [&](int m) -> cudaError_t {   // G (m x m) -> V, lam (host copy in hl)
+    cudaError_t er = launch_sym_eigen(G, Vt, V, dg, lam, m, s);
+    if (er != cudaSuccess) return er;
+    er = cudaMemcpyAsync(hl.data(), lam, sizeof(double) * m, cudaMemcpyDeviceToHost, s);
+    if (er != cudaSuccess) return er;
+    return cudaStreamSynchronize(s);
+  };
+  // scaled copies of the leading eigenvector columns: Bm[:, :s] = V[:, :s] * f
+  std::vector<double> hf(rmax);
+  auto scaled = [&](int m, int cols, const std::vector<double>& f) -> cudaError_t {
+    cudaError_t er = cudaMemcpyAsync(dg, f.data(), sizeof(double) * cols, cudaMemcpyHostToDevice, s);
+    if (er != cudaSuccess) return er;
+    scale_cols_kernel<<<(m * cols + 255) / 256, 256, 0, s>>>(V, dg, Bm, m, cols);
+    ++g_launches;
+    return cudaGetLastError();
+  };
+  const double zero_rel = 1e-14;   // relative eigenvalue floor (numerical zero of the Gram)
+  // right-to-left orthonormalisation: W_k = (V S)(S^-1 V^T W_k), W_{k-1} <- W_{k-1} V S
+  for (int64_t k = d - 1; k >= 1 && e == cudaSuccess; --k) {
+    const long long rk = r[k], q = n[k] * r[k + 1];
+    g_stage = TT_ST_IL_S1;
+    e = launch_gemm(true, true, gp(W[k], q, W[k], q, G, rk, rk, q, tt::map_plain(rk),
+                                   tt::map_plain(1)), s);
+    if (e == cudaSuccess) e = eig((int)rk);
+    if (e != cudaSuccess) break;
+    int sk = 0;
+    for (long long i = 0; i < rk; ++i)
+      if (hl[i] > zero_rel * hl[0] && hl[i] > 0.0) ++sk;
+    if (sk == 0) sk = 1;
+    for (int i = 0; i < sk; ++i) hf[i] = 1.0 / std::sqrt(std::max(hl[i], 1e-300));
+    if ((e = scaled((int)rk, sk, hf)) != cudaSuccess) break;
+    // Tmp (sk x q) = (V S^-1)^T W_k
+    e = launch_gemm(false, false, gp(Bm, sk, W[k], q, Tmp, sk, q, rk, tt::map_plain(q),
+                                     tt::map_plain(1)), s);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(W[k], Tmp, sizeof(double) * sk * q, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) break;
+    for (int i = 0; i < sk; ++i) hf[i] = std::sqrt(std::max(hl[i], 0.0));
+    if ((e = scaled((int)rk, sk, hf)) != cudaSuccess) break;
+    // W_{k-1} (r_{k-1} n x sk) = W_{k-1} (r_{k-1} n x rk) . (V S)
+    const long long m1 = r[k - 1] * n[k - 1];
+    e = launch_gemm(true, false, gp(W[k - 1], rk, Bm, sk, Tmp, m1, sk, rk, tt::map_plain(sk),
+                                    tt::map_plain(1)), s);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(W[k - 1], Tmp, sizeof(double) * m1 * sk, cudaMemcpyDeviceToDevice, s);
+    r[k] = sk;
+  }
+  // left-to-right truncation with threshold delta / sqrt(d-1) ||T||
+  double thr = 0.0;
+  for (int64_t k = 0; k < d - 1 && e == cudaSuccess; ++k) {
+    const long long m = r[k] * n[k], rk1 = r[k + 1];
+    g_stage = TT_ST_IL_S2;
+    e = launch_gemm(false, false, gp(W[k], rk1, W[k], rk1, G, rk1, rk1, m, tt::map_plain(rk1),
+                                     tt::map_plain(1)), s);
+    if (e == cudaSuccess) e = eig((int)rk1);
+    if (e != cudaSuccess) break;
+    if (k == 0) {
+      double nrm2 = 0.0;
+      for (long long i = 0; i < rk1; ++i) nrm2 += std::max(hl[i], 0.0);
+      thr = delta / std::sqrt((double)std::max<int64_t>(d - 1, 1)) * std::sqrt(nrm2);
+    }
+    // smallest rank whose discarded tail has Frobenius norm <= thr; drop numerical zeros
+    int nz = 0;
+    for (long long i = 0; i < rk1; ++i)
+      if (hl[i] > zero_rel * hl[0] && hl[i] > 0.0) ++nz;
+    if (nz == 0) nz = 1;
+    int sk = nz;
+    double tail = 0.0;
+    for (int i = nz - 1; i >= 1; --i) {
+      tail += std::max(hl[i], 0.0);
+      if (std::sqrt(tail) <= thr) sk = i; else break;
+    }
+    if (max_rank > 0 && sk > max_rank) sk = (int)max_rank;
+    for (int i = 0; i < sk; ++i) hf[i] = 1.0 / std::sqrt(std::max(hl[i], 1e-300));
+    if ((e = scaled((int)rk1, sk, hf)) != cudaSuccess) break;
+    // U (m x sk) = W_k . (V S^-1)
+    e = launch_gemm(true, false, gp(W[k], rk1, Bm, sk, Tmp, m, sk, rk1, tt::map_plain(sk),
+                                    tt::map_plain(1)), s);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(W[k], Tmp, sizeof(double) * m * sk, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) break;
+    for (int i = 0; i < sk; ++i) hf[i] = std::sqrt(std::max(hl[i], 0.0));
+    if ((e = scaled((int)rk1, sk, hf)) != cudaSuccess) break;
+    // W_{k+1} (sk x q) = (V S)^T . W_{k+1} (rk1 x q)
+    const long long q = n[k + 1] * r[k + 2];
+    e = launch_gemm(false, false, gp(Bm, sk, W[k + 1], q, Tmp, sk, q, rk1, tt::map_plain(q),
+                                     tt::map_plain(1)), s);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(W[k + 1], Tmp, sizeof(double) * sk * q, cudaMemcpyDeviceToDevice, s);
+    r[k + 1] = sk;
+  }
+  for (int64_t k = 0; k < d && e == cudaSuccess; ++k)
+    e = cudaMemcpyAsync(cores_out[k], W[k], sizeof(double) * r[k] * n[k] * r[k + 1],
+                        cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "tt_round");
+  for (int64_t k = 0; k <= d; ++k) r_out[k] = r[k];
   return TT_OK;
 }
 

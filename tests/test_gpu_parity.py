@@ -478,3 +478,64 @@ def test_block_local_matvec_vs_oracle(tt, rl, n, rr, Rmax):
     ref = oracle.block_local_matvec(ops_h, KKT_TERMS, X)
     for b in range(3):
         assert rel(h(Y)[:, :, b, :], ref[:, :, b, :]) <= TOL, b
+
+
+# ----------------------------------------------------------------------------------------
+# TT rounding vs the oracle (Oseledets Alg. 2)
+# ----------------------------------------------------------------------------------------
+def _tt_sum(a, b, sb=1.0):
+    d = len(a)
+    out = []
+    for k in range(d):
+        ca, cb = a[k], (sb * b[k] if k == 0 else b[k])
+        if d == 1:
+            out.append(ca + cb)
+        elif k == 0:
+            out.append(np.concatenate([ca, cb], axis=2))
+        elif k == d - 1:
+            out.append(np.concatenate([ca, cb], axis=0))
+        else:
+            c = np.zeros((ca.shape[0] + cb.shape[0], ca.shape[1], ca.shape[2] + cb.shape[2]))
+            c[:ca.shape[0], :, :ca.shape[2]] = ca
+            c[ca.shape[0]:, :, ca.shape[2]:] = cb
+            out.append(c)
+    return out
+
+
+@pytest.mark.parametrize("case", ["random", "sum", "config3"])
+@pytest.mark.parametrize("delta", [1e-2, 1e-6])
+def test_tt_round_vs_oracle(tt, case, delta):
+    import ttgen
+    from oracle.rounding import tt_round as oracle_round
+    rng = np.random.default_rng(5)
+    if case == "random":
+        x = ttgen.gaussian_tt_vector(rng, 4, [1, 4, 12, 16, 9, 3, 1])
+    elif case == "sum":
+        base = ttgen.gaussian_tt_vector(rng, 4, [1, 4, 6, 6, 4, 1])
+        x = _tt_sum(base, ttgen.gaussian_tt_vector(rng, 4, [1, 3, 5, 5, 3, 1]))
+        x = _tt_sum(x, base)                       # exactly rank-deficient formal sum
+    else:
+        x = ttgen.make_inputs(3).x
+    from dense_ref import full_vector
+    yo = oracle_round(x, delta)
+    yg = [h(c) for c in tt.tt_round([g(c) for c in x], delta)]
+    assert [c.shape for c in yg] == [c.shape for c in yo]
+    # dense reconstructions (config 3: 4^10 entries); a TT inner-product difference would
+    # cancel catastrophically at this accuracy
+    v, vo, vg = full_vector(x), full_vector(yo), full_vector(yg)
+    assert rel(vg, vo) <= TOL
+    assert np.linalg.norm(vg - v) / np.linalg.norm(v) <= delta * (1 + 1e-6)
+
+
+@pytest.mark.parametrize("n", [1, 2, 7, 64, 129, 256])
+def test_jacobi_eigen_vs_numpy(tt, n):
+    rng = np.random.default_rng(n)
+    M = rng.standard_normal((n, n))
+    G = M @ M.T
+    lam, V = tt.tt_debug_sym_eigen(g(G))
+    torch.cuda.synchronize()
+    ref = np.linalg.eigvalsh(G)[::-1]
+    assert np.allclose(h(lam), ref, rtol=1e-12, atol=1e-12 * ref[0])
+    Vh = h(V)
+    assert np.allclose(Vh.T @ Vh, np.eye(n), atol=1e-12)
+    assert np.allclose(G @ Vh, Vh * h(lam), atol=1e-10 * ref[0])
