@@ -539,6 +539,20 @@ def main():
         two = {"core": k, "n1": 2, "n2": 2, "nvec": cfg.nvec, "ms": t["graph_ms_median"],
                "gflop": f2 / 1e9, "tflops": f2 / (t["graph_ms_median"] * 1e-3) / 1e12}
 
+    # ---- TT rounding of the config-5 vector train (delta = 1e-4) --------
+    rnd_info = None
+    if not args.no_sweeps:
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        rounded = tt.tt_round(xs, 1e-4)
+        t1 = time.perf_counter()
+        rounded = tt.tt_round(xs, 1e-4)
+        t2 = time.perf_counter()
+        rnd_info = {"delta": 1e-4, "ranks_in": list(cfg.r),
+                    "ranks_out": [1] + [int(c.shape[2]) for c in rounded],
+                    "ms": (t2 - t1) * 1e3, "ms_first": (t1 - t0) * 1e3,
+                    "note": "synchronous (data-dependent ranks); host wall time"}
+
     # ---- full sweeps at d = 12 (metric's second half), eager and as a CUDA graph ---------
     sweeps = None
     if not args.no_sweeps:
@@ -600,6 +614,7 @@ def main():
             "local_gmres": gm,
             "kkt_block_action": kkt,
             "two_site_matvec": two,
+            "tt_round": rnd_info,
             "detail": {
                 "full_sweep_ms": (total_ms / args.steps) - (apply_detail["ms_per_step"]
                                                             if apply_detail else 0.0),

@@ -160,7 +160,7 @@ tt_status tt_operator_apply(int64_t d, const int64_t* n_row, const int64_t* n_co
 size_t tt_round_workspace_size(int64_t d, const int64_t* n, const int64_t* r);
 /* Test hook: eigendecomposition of a symmetric n x n matrix G (overwritten; n <= 512) by the
  * rounding's parallel Jacobi solver: V columns = eigenvectors, lam descending.  Workspace
- * >= (n^2 + n) doubles. */
+ * >= 4 (n+1)^2 + 8200 doubles. */
 tt_status tt_debug_sym_eigen(int64_t n, double* G, double* V, double* lam, void* workspace,
                              size_t workspace_bytes, void* stream);
 tt_status tt_round(int64_t d, const int64_t* n, const int64_t* r_in,

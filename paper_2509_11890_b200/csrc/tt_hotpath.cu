@@ -23,6 +23,7 @@
 #include "tt_gemm_v2.cuh"
 #include "tt_gemm_v3.cuh"
 #include <cudaTypedefs.h>
+#include <cooperative_groups.h>
 
 using tt::GemmParams;
 using tt::IndexMap;
@@ -961,19 +962,46 @@ bool same(const void* p, const void* q) { return p != nullptr && p == q; }
 #include "tt_gmres.cuh"
 #include "tt_round.cuh"
 
-// Symmetric eigendecomposition of the n x n Gram matrix G (overwritten): lam (descending)
-// and V (columns) in the caller's buffers; d, Vtmp are scratch.
-cudaError_t launch_sym_eigen(double* G, double* Vtmp, double* V, double* d, double* lam, int n,
+// Symmetric eigendecomposition of the n x n Gram matrix G: lam (descending) and V (columns)
+// in the caller's buffers.  Scratch: 4 padded (np x np) buffers + partials (np = n rounded up
+// to even) carved from `scratch` (sym_eigen_scratch(n) doubles).
+long long sym_eigen_scratch(long long n) {
+  const long long np = (n + 1) & ~1LL;
+  return 4 * np * np + 2 * 4096 + 8;
+}
+cudaError_t launch_sym_eigen(const double* G, double* V, double* lam, int n, double* scratch,
                              cudaStream_t s) {
   const int np = (n + 1) & ~1;
-  const size_t smem = (size_t)np / 2 * (2 * sizeof(double) + 2 * sizeof(int));
+  const long long NN = (long long)np * np;
+  double* G0 = scratch;
+  double* G1 = G0 + NN;
+  double* V0 = G1 + NN;
+  double* V1 = V0 + NN;
+  double* part = V1 + NN;
+  int* which = reinterpret_cast<int*>(part + 2 * 4096);
   g_stage = TT_ST_PERM;
   const long long tr = trace_begin(0, (long long)n * n, 0, 0, s);
-  jacobi_eigen_kernel<<<1, 1024, smem, s>>>(G, Vtmp, n, 30);
-  diag_kernel<<<(n + 255) / 256, 256, 0, s>>>(G, d, n);
-  sort_eigvecs_kernel<<<(n + 255) / 256, 256, 0, s>>>(Vtmp, d, V, lam, n);
+  long long eb = (NN + 255) / 256;
+  if (eb > 4096) eb = 4096;
+  embed_kernel<<<(unsigned)eb, 256, 0, s>>>(G, G0, n, np);
+  ++g_launches;
+  int dev = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  const size_t smem = (size_t)np / 2 * (2 * sizeof(double) + 2 * sizeof(int));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_coop_kernel, 256, smem);
+  int grid = num_sms() * std::max(per_sm, 1);
+  const long long want = std::max<long long>(1, ((long long)(np / 2) * (np / 2) + 255) / 256);
+  if (grid > want) grid = (int)want;
+  if (grid > 4096) grid = 4096;
+  int sweeps = 25;
+  void* args[] = {&G0, &G1, &V0, &V1, (void*)&np, &sweeps, &part, &which};
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)jacobi_coop_kernel, grid, 256, args,
+                                              smem, s);
+  ++g_launches;
+  if (e != cudaSuccess) return e;
+  sort_padded_kernel<<<(n + 255) / 256, 256, 0, s>>>(G0, G1, V0, V1, which, V, lam, n, np);
+  ++g_launches;
   trace_end(tr, s);
-  g_launches += 3;
   return cudaGetLastError();
 }
 
@@ -1551,10 +1579,9 @@ tt_status tt_debug_sym_eigen(int64_t n, double* G, double* V, double* lam, void*
   CallScope scope;
   if (n <= 0 || n > 512) return fail(TT_ERR_INVALID_ARGUMENT, "0 < n <= 512");
   if (!G || !V || !lam || !workspace) return fail(TT_ERR_NULL_POINTER, "NULL pointer");
-  if (workspace_bytes < (size_t)(n * n + n) * 8) return fail(TT_ERR_WORKSPACE, "workspace");
-  double* Vt = static_cast<double*>(workspace);
-  double* dg = Vt + n * n;
-  cudaError_t e = launch_sym_eigen(G, Vt, V, dg, lam, (int)n, static_cast<cudaStream_t>(stream));
+  if (workspace_bytes < (size_t)sym_eigen_scratch(n) * 8) return fail(TT_ERR_WORKSPACE, "workspace");
+  cudaError_t e = launch_sym_eigen(G, V, lam, (int)n, static_cast<double*>(workspace),
+                                   static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "tt_debug_sym_eigen");
   return TT_OK;
 }
@@ -1571,8 +1598,9 @@ size_t tt_round_workspace_size(int64_t d, const int64_t* n, const int64_t* r) {
   }
   for (int64_t k = 0; k <= d; ++k) rmax = std::max<long long>(rmax, r[k]);
   if (!ok) return 0;
-  // working cores, one temp core, G, Vtmp, V, Bm (rmax^2 each), d, lam (rmax)
-  return ws_bytes({tot, core_max, rmax * rmax, rmax * rmax, rmax * rmax, rmax * rmax, rmax, rmax});
+  // working cores, one temp core, G, V, Bm (rmax^2 each), d, lam (rmax), eigen scratch
+  return ws_bytes({tot, core_max, rmax * rmax, rmax * rmax, rmax * rmax, rmax, rmax,
+                   sym_eigen_scratch(rmax)});
 }
 
 tt_status tt_round(int64_t d, const int64_t* n, const int64_t* r_in,
@@ -1609,11 +1637,11 @@ tt_status tt_round(int64_t d, const int64_t* n, const int64_t* r_in,
   }
   double* Tmp = c.take(core_max);
   double* G = c.take(rmax * rmax);
-  double* Vt = c.take(rmax * rmax);
   double* V = c.take(rmax * rmax);
   double* Bm = c.take(rmax * rmax);
   double* dg = c.take(rmax);
   double* lam = c.take(rmax);
+  double* esc = c.take(sym_eigen_scratch(rmax));
   if (!c.ok) return fail(TT_ERR_WORKSPACE, "workspace too small after alignment");
   std::vector<long long> r(r_in, r_in + d + 1);
   cudaError_t e = cudaSuccess;
@@ -1622,7 +1650,7 @@ tt_status tt_round(int64_t d, const int64_t* n, const int64_t* r_in,
                         cudaMemcpyDeviceToDevice, s);
   std::vector<double> hl(rmax);
   auto eig = [&](int m) -> cudaError_t {   // G (m x m) -> V, lam (host copy in hl)
-    cudaError_t er = launch_sym_eigen(G, Vt, V, dg, lam, m, s);
+    cudaError_t er = launch_sym_eigen(G, V, lam, m, esc, s);
     if (er != cudaSuccess) return er;
     er = cudaMemcpyAsync(hl.data(), lam, sizeof(double) * m, cudaMemcpyDeviceToHost, s);
     if (er != cudaSuccess) return er;
