@@ -245,7 +245,9 @@ void tt_debug_force_v1(int on);
 void tt_debug_set_variant(int v);
 /* Benchmark hooks: bit 0 skips the GEMM output stores and bit 1 the operand loads (results
  * become WRONG; times the main loop / epilogue / load path in isolation); bit 3 computes the
- * right interface update directly instead of as the mirrored left update (same result). */
+ * right interface update directly instead of as the mirrored left update (same result); bit 4
+ * disables the TMA L2 cache-policy hints, bit 5 only the evict_first ones, bit 6 only the
+ * evict_last ones (same results). */
 void tt_debug_set_flags(int flags);
 
 /* ---------------------------------------------------------------------------------------

@@ -35,6 +35,8 @@ struct GemmParamsV3 {
   int M, N, K;
   IndexMap32 rowmap, colmap;
   int tiles_n, total_units, KT, ksplit, kt_per_split;
+  int l2_a, l2_b;   // TMA L2 policy per operand: 0 default, 1 evict_last (reused, L2-sized),
+                    // 2 evict_first (streamed once, larger than L2)
   int store_mode;   // 0 scalar; 1 column pairs (N-contiguous B, output contiguous along n);
                     // 2 row pairs (M-contiguous A, output contiguous along m) -> 16-byte stores
   int dbg;
@@ -69,6 +71,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "r"(a), "r"(parity)
         : "memory");
   } while (!done);
+}
+__device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* map, int c0, int c1,
+                                                 uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t l2_policy(int kind) {
+  uint64_t pol = 0;
+  if (kind == 1)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
 }
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
                                             uint64_t* bar) {
@@ -132,6 +150,8 @@ dmma_gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     ke = min(p.KT, kb + p.kt_per_split);
   };
 
+  const uint64_t pol_a = (tid == 0 && p.l2_a) ? l2_policy(p.l2_a) : 0;
+  const uint64_t pol_b = (tid == 0 && p.l2_b) ? l2_policy(p.l2_b) : 0;
   // ---- producer state (thread 0 only; kept in shared memory to spare registers) ---------
   __shared__ int prod_state[7];   // u, m0, n0, kt, ke, split, q
   if (tid == 0) {
@@ -152,16 +172,24 @@ dmma_gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     mbar_expect_tx(&full_bar[s], STAGE_BYTES);
     if (!(p.dbg & 2)) {
       if (A_KC) {
-        tma_load_2d(as, &tmA, k0, m0, &full_bar[s]);
+        if (p.l2_a) tma_load_2d_hint(as, &tmA, k0, m0, &full_bar[s], pol_a);
+        else tma_load_2d(as, &tmA, k0, m0, &full_bar[s]);
       } else {
 #pragma unroll
-        for (int b = 0; b < BM / 16; ++b) tma_load_2d(as + b * 2048, &tmA, m0 + 16 * b, k0, &full_bar[s]);
+        for (int b = 0; b < BM / 16; ++b) {
+          if (p.l2_a) tma_load_2d_hint(as + b * 2048, &tmA, m0 + 16 * b, k0, &full_bar[s], pol_a);
+          else tma_load_2d(as + b * 2048, &tmA, m0 + 16 * b, k0, &full_bar[s]);
+        }
       }
       if (B_KC) {
-        tma_load_2d(bs, &tmB, k0, n0, &full_bar[s]);
+        if (p.l2_b) tma_load_2d_hint(bs, &tmB, k0, n0, &full_bar[s], pol_b);
+        else tma_load_2d(bs, &tmB, k0, n0, &full_bar[s]);
       } else {
 #pragma unroll
-        for (int b = 0; b < BN / 16; ++b) tma_load_2d(bs + b * 2048, &tmB, n0 + 16 * b, k0, &full_bar[s]);
+        for (int b = 0; b < BN / 16; ++b) {
+          if (p.l2_b) tma_load_2d_hint(bs + b * 2048, &tmB, n0 + 16 * b, k0, &full_bar[s], pol_b);
+          else tma_load_2d(bs + b * 2048, &tmB, n0 + 16 * b, k0, &full_bar[s]);
+        }
       }
     } else {
       // benchmark hook: no loads; complete the transaction count locally

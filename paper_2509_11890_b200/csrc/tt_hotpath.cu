@@ -377,6 +377,34 @@ cudaError_t launch_v3_cfg(const GemmParams& p0, cudaStream_t s, bool& ok) {
   p.rowmap = tt::to_map32(p0.rowmap);
   p.colmap = tt::to_map32(p0.colmap);
   p.store_mode = store_mode(AK, BK_, p0);
+  // L2 policies: an operand that fits comfortably in L2 and is re-read by many tiles is kept
+  // (evict_last); an operand larger than L2 is streamed (evict_first) when that protects a
+  // kept partner of some size (a streamed operand with a tiny partner gains nothing and was
+  // measured to lose ~1% on config 5's S2).  Config 5: S3 +1.5% (T2 streamed, PhiR kept),
+  // S2 +0.6% (A-hat kept).
+  {
+    const long long a_bytes = 8LL * (AK ? p0.M * p0.lda : p0.K * p0.lda);
+    const long long b_bytes = 8LL * (BK_ ? p0.N * p0.ldb : p0.K * p0.ldb);
+    const long long a_reads = (p0.N + BN - 1) / BN, b_reads = (p0.M + BM - 1) / BM;
+    const long long l2_keep = 80LL << 20, l2_size = 126LL << 20;
+    p.l2_a = (g_dbg_flags & 16) || a_reads < 2 || a_bytes > l2_keep ? 0 : 1;
+    p.l2_b = (g_dbg_flags & 16) || b_reads < 2 || b_bytes > l2_keep ? 0 : 1;
+    if (p.l2_a == 1 && p.l2_b == 1 && a_bytes + b_bytes > l2_keep) {
+      if (a_bytes > b_bytes) p.l2_a = 0; else p.l2_b = 0;
+    }
+    const long long min_protect = 4LL << 20;
+    if (!(g_dbg_flags & 16)) {
+      if (a_bytes > l2_size && p.l2_b == 1 && b_bytes >= min_protect) p.l2_a = 2;
+      if (b_bytes > l2_size && p.l2_a == 1 && a_bytes >= min_protect) p.l2_b = 2;
+    }
+    if (g_dbg_flags & 32) { if (p.l2_a == 2) p.l2_a = 0; if (p.l2_b == 2) p.l2_b = 0; }
+    if (g_dbg_flags & 64) { if (p.l2_a == 1) p.l2_a = 0; if (p.l2_b == 1) p.l2_b = 0; }
+    static const bool l2_debug = getenv("TT_L2_DEBUG") != nullptr;
+    if (l2_debug)
+      fprintf(stderr, "v3 %dx%d M=%lld N=%lld K=%lld AK=%d BK=%d a=%lldMB(r%lld,p%d) b=%lldMB(r%lld,p%d)\n",
+              BM, BN, (long long)p0.M, (long long)p0.N, (long long)p0.K, AK, BK_, a_bytes >> 20,
+              a_reads, p.l2_a, b_bytes >> 20, b_reads, p.l2_b);
+  }
   p.store_mode = store_mode(AK, BK_, p0);
   const long long tm = (p0.M + BM - 1) / BM;
   const long long tn = (p0.N + BN - 1) / BN;
