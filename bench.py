@@ -539,6 +539,52 @@ def main():
         two = {"core": k, "n1": 2, "n2": 2, "nvec": cfg.nvec, "ms": t["graph_ms_median"],
                "gflop": f2 / 1e9, "tflops": f2 / (t["graph_ms_median"] * 1e-3) / 1e12}
 
+    # ---- block LOBPCG of the step-length eigenproblem (interior core) ---
+    lob = None
+    if not args.no_sweeps:
+        k = cfg.d // 2
+        rl, nn, rr = cfg.r[k], cfg.N, cfg.r[k + 1]
+        Rl, Rr = cfg.R[k], cfg.R[k + 1]
+        gen = torch.Generator(device=dev).manual_seed(12)
+        rnd = lambda *sh: torch.randn(*sh, dtype=torch.float64, device=dev, generator=gen)
+        sym_if = lambda r, R: (lambda t: (t + t.transpose(0, 2)) / 2)(rnd(r, R, r))
+        sym_core = lambda: (lambda t: (t + t.transpose(1, 2)) / 2)(rnd(Rl, nn, nn, Rr))
+        opA = (sym_if(rl, Rl), sym_core(), sym_if(rr, Rr))
+        # L_B = I + 0.01 (symmetric perturbation): SPD, operator ranks as the interior core's
+        pLB, ALB, pRB = 0.1 * sym_if(rl, Rl), 0.1 * sym_core(), 0.1 * sym_if(rr, Rr)
+        pLB[:, 0, :] += torch.eye(rl, dtype=torch.float64, device=dev)
+        pRB[:, 0, :] += torch.eye(rr, dtype=torch.float64, device=dev)
+        ALB[0, :, :, 0] = torch.eye(nn, dtype=torch.float64, device=dev)
+        ALB[0, :, :, 1:] = 0.0
+        ALB[1:, :, :, 0] = 0.0
+        opB = (pLB, ALB, pRB)
+        nb_l, its_l = 8, 20
+        lob = {"core": k, "nb": nb_l, "iterations": its_l, "refresh": 20}
+        for name, oB in (("standard", None), ("generalised", opB)):
+            X0 = rnd(rl, nn, nb_l, rr)
+            Xl = X0.clone()
+            RlB, RrB = (Rl, Rr) if oB is not None else (0, 0)
+            wsl = torch.empty(tt.tt_local_lobpcg_workspace_size(rl, nn, rr, Rl, Rr, RlB, RrB, nb_l),
+                              dtype=torch.uint8, device=dev)
+            bufs = [torch.empty(nb_l, dtype=torch.float64, device=dev) for _ in range(2)]
+            itl = torch.empty(1, dtype=torch.int64, device=dev)
+            stl = torch.empty(1, dtype=torch.float64, device=dev)
+
+            def lob_run(st, oB=oB, Xl=Xl, X0=X0, wsl=wsl, bufs=bufs, itl=itl, stl=stl):
+                Xl.copy_(X0)
+                tt.tt_local_lobpcg(opA, Xl, opB=oB, maxiter=its_l, tol=0.0, lam=bufs[0],
+                                   res=bufs[1], iters=itl, step=stl, workspace=wsl, stream=st,
+                                   refresh=20)
+            t = time_sweep(tt, lob_run, stream, dev, reps=3)
+            nops = 2 if oB is not None else 1
+            # matvecs: initial (1 block), one per iteration, refresh (2 blocks) every 20
+            nblocks = 1 + its_l + 2 * ((its_l - 1) // 20)
+            mv_f = nops * nblocks * nb_l * f_local(rl, nn, rr, Rl, Rr)
+            lob[name] = {"ms": t["graph_ms_median"], "ms_eager": t["eager_ms_median"],
+                         "ms_per_iteration": t["graph_ms_median"] / its_l,
+                         "matvec_gflop": mv_f / 1e9,
+                         "matvec_tflops_over_total_time": mv_f / (t["graph_ms_median"] * 1e-3) / 1e12}
+
     # ---- TT rounding of the config-5 vector train (delta = 1e-4) --------
     rnd_info = None
     if not args.no_sweeps:
@@ -615,6 +661,7 @@ def main():
             "kkt_block_action": kkt,
             "two_site_matvec": two,
             "tt_round": rnd_info,
+            "local_lobpcg": lob,
             "detail": {
                 "full_sweep_ms": (total_ms / args.steps) - (apply_detail["ms_per_step"]
                                                             if apply_detail else 0.0),

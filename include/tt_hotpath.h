@@ -235,6 +235,47 @@ tt_status tt_local_gmres(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t 
                          double* rel_res, int64_t* iters, void* workspace,
                          size_t workspace_bytes, void* stream);
 
+/* -------------------------------------------------------------------------------------
+ * NEXT row 4: matrix-free block LOBPCG for the step-length local
+ * generalised eigenproblem ("we minimise -<E, M E> / <E, dM E> via the
+ * local eigenvalue problem max vec(E_k)^T E_{!=k}^T dM E_{!=k} vec(E_k) s.t.
+ * vec(E_k)^T E_{!=k}^T M E_{!=k} vec(E_k) = 1 ... it can also be implemented in a
+ * matrix-free fashion by using iterative eigenvalue solvers (such as LOBPCG [Knyazev 2001])").
+ *
+ * Computes the nb LARGEST eigenpairs of the pencil (L_A, L_B), L_A = X_{!=k}^T A X_{!=k}
+ * (operator A: phiL_A (rl,RlA,rl), A_A (RlA,n,n,RrA), phiR_A (rr,RrA,rr)), L_B likewise from
+ * operator B, which must make L_B symmetric positive definite; L_A must be symmetric.
+ * phiL_B = A_B = phiR_B = NULL selects L_B = I (RlB, RrB ignored); otherwise all three are
+ * required.  For the two-site (DMRG) eigenproblem pass supercore operators merged by
+ * tt_merge_operator_cores and n = n1 n2.
+ *   X (device, Block-TT layout (rl, n, nb, rr)): initial block on entry (must be L_B-linearly
+ *     independent); the L_B-orthonormal Ritz vectors on exit, column j for lam[j].
+ *   lam (device, nb): Ritz values, descending.  res (device, nb): ||L_A x - lam L_B x|| /
+ *     (||L_A x|| + |lam| ||L_B x||) per column.  iters (device, 1 int64): iterations done.
+ *   step (device, 1 double, may be NULL): min(1, 1 / lam[0]) if lam[0] > 0 else 1 -- the
+ *     step length of PAPER.md:561-563 when A = -dM, B = M (reading R12).
+ * Stops when max_j res_j <= tol or after maxiter iterations; each iteration is one batched
+ * local matvec (H4) per operator on nb columns, the residual block L_B-orthogonalised
+ * against X, Gram matrices and an on-device Rayleigh-Ritz step (P kept L_B-orthonormal and
+ * L_B-orthogonal to X).  refresh > 0: every `refresh` iterations the carried images L_A X,
+ * L_B X, L_A P, L_B P are recomputed by matvecs (recommended 20; 0 = never).
+ * Fully asynchronous (device-side convergence flag; no host synchronisation), graph-capturable.
+ * Workspace: tt_local_lobpcg_workspace_size(...) (RlB = RrB = 0 for B = I).  nb <= 32.
+ * ------------------------------------------------------------------------------------- */
+size_t tt_local_lobpcg_workspace_size(int64_t rl, int64_t n, int64_t rr, int64_t RlA, int64_t RrA,
+                                      int64_t RlB, int64_t RrB, int64_t nb);
+tt_status tt_local_lobpcg(int64_t rl, int64_t n, int64_t rr, int64_t RlA, int64_t RrA,
+                          int64_t RlB, int64_t RrB, int64_t nb, int64_t maxiter,
+                          int64_t refresh, double tol, const double* phiL_A, const double* A_A, const double* phiR_A,
+                          const double* phiL_B, const double* A_B, const double* phiR_B,
+                          double* X, double* lam, double* res, int64_t* iters, double* step,
+                          void* workspace, size_t workspace_bytes, void* stream);
+/* Two-site supercore operator ("operates on pairs of neighbouring cores"):
+ * A12[al, (i1 i2), (j1 j2), be] = sum_g A1[al, i1, j1, g] A2[g, i2, j2, be];
+ * A1 (Rl,n1,n1,Rm), A2 (Rm,n2,n2,Rr), A12 (Rl, n1 n2, n1 n2, Rr), device.  No workspace. */
+tt_status tt_merge_operator_cores(int64_t Rl, int64_t n1, int64_t n2, int64_t Rm, int64_t Rr,
+                                  const double* A1, const double* A2, double* A12, void* stream);
+
 /* Number of kernel launches the last call on this thread enqueued. */
 int64_t tt_last_launch_count(void);
 /* Test hook: on != 0 routes every GEMM stage of the calling thread through the generic

@@ -28,6 +28,7 @@ __all__ = [
     "tt_local_matvec_two_site", "tt_local_matvec_two_site_workspace_size",
     "tt_block_local_matvec", "tt_block_local_matvec_workspace_size", "TTBlockTerm",
     "tt_round", "tt_round_workspace_size", "tt_debug_sym_eigen",
+    "tt_local_lobpcg", "tt_local_lobpcg_workspace_size", "tt_merge_operator_cores",
 ]
 
 STAGE_NAMES = {0: "perm", 1: "set", 2: "mv_s1", 3: "mv_s2", 4: "mv_s3", 5: "il_s1", 6: "il_s2",
@@ -91,6 +92,12 @@ lib.tt_local_gmres_workspace_size.restype = _sz
 lib.tt_local_gmres_workspace_size.argtypes = [_i64] * 8
 lib.tt_local_gmres.argtypes = [_i64] * 9 + [ctypes.c_double] + [_p] * 8 + [_sz, _p]
 lib.tt_local_gmres.restype = ctypes.c_int
+lib.tt_local_lobpcg_workspace_size.restype = _sz
+lib.tt_local_lobpcg_workspace_size.argtypes = [_i64] * 8
+lib.tt_local_lobpcg.argtypes = [_i64] * 10 + [ctypes.c_double] + [_p] * 12 + [_sz, _p]
+lib.tt_local_lobpcg.restype = ctypes.c_int
+lib.tt_merge_operator_cores.argtypes = [_i64] * 5 + [_p] * 4
+lib.tt_merge_operator_cores.restype = ctypes.c_int
 lib.tt_debug_force_v1.argtypes = [ctypes.c_int]
 lib.tt_debug_force_v1.restype = None
 lib.tt_debug_set_variant.argtypes = [ctypes.c_int]
@@ -363,6 +370,54 @@ def tt_local_gmres(phiL, A, phiR, F, X=None, m=20, cycles=1, tol=0.0, rel_res=No
                               _dev(rel_res, "rel_res"), iters.data_ptr(), ws.data_ptr(),
                               ws.numel(), _stream(stream)))
     return X, rel_res, iters
+
+
+def tt_local_lobpcg_workspace_size(rl, n, rr, RlA, RrA, RlB, RrB, nb) -> int:
+    return int(lib.tt_local_lobpcg_workspace_size(rl, n, rr, RlA, RrA, RlB, RrB, nb))
+
+
+def tt_local_lobpcg(opA, X, opB=None, maxiter=100, tol=1e-10, lam=None, res=None, iters=None,
+                    step=None, workspace=None, stream=None, refresh=20):
+    """Block LOBPCG for the nb largest eigenpairs of the projected pencil (L_A, L_B)
+    (PAPER.md:556-567).  opA, opB: (phiL, A, phiR) triplets of device tensors; opB None means
+    L_B = I.  X (rl, n, nb, rr): initial block, overwritten with the Ritz vectors.
+    Returns (X, lam, res, iters, step) (device tensors; step = min(1, 1/lam[0]) or 1)."""
+    rl, n, nb, rr = X.shape
+    phiLA, AA, phiRA = opA
+    RlA, RrA = AA.shape[0], AA.shape[3]
+    if opB is not None:
+        phiLB, AB, phiRB = opB
+        RlB, RrB = AB.shape[0], AB.shape[3]
+        pB = (_dev(phiLB, "phiL_B"), _dev(AB, "A_B"), _dev(phiRB, "phiR_B"))
+    else:
+        RlB = RrB = 0
+        pB = (None, None, None)
+    dev = X.device
+    lam = torch.empty(nb, dtype=torch.float64, device=dev) if lam is None else lam
+    res = torch.empty(nb, dtype=torch.float64, device=dev) if res is None else res
+    iters = torch.empty(1, dtype=torch.int64, device=dev) if iters is None else iters
+    step = torch.empty(1, dtype=torch.float64, device=dev) if step is None else step
+    if iters.dtype != torch.int64 or not iters.is_cuda:
+        raise TypeError("iters must be a CUDA int64 tensor")
+    ws = _ws(tt_local_lobpcg_workspace_size(rl, n, rr, RlA, RrA, RlB, RrB, nb), workspace, dev)
+    _check(lib.tt_local_lobpcg(rl, n, rr, RlA, RrA, RlB, RrB, nb, int(maxiter), int(refresh),
+                               float(tol),
+                               _dev(phiLA, "phiL_A"), _dev(AA, "A_A"), _dev(phiRA, "phiR_A"),
+                               pB[0], pB[1], pB[2], _dev(X, "X"), _dev(lam, "lam"),
+                               _dev(res, "res"), iters.data_ptr(), _dev(step, "step"),
+                               ws.data_ptr(), ws.numel(), _stream(stream)))
+    return X, lam, res, iters, step
+
+
+def tt_merge_operator_cores(A1, A2, A12=None, stream=None):
+    """Two-site supercore operator A12 (Rl, n1 n2, n1 n2, Rr) from A1 (Rl,n1,n1,Rm), A2 (Rm,n2,n2,Rr)."""
+    Rl, n1, _, Rm = A1.shape
+    _, n2, _, Rr = A2.shape
+    if A12 is None:
+        A12 = torch.empty((Rl, n1 * n2, n1 * n2, Rr), dtype=torch.float64, device=A1.device)
+    _check(lib.tt_merge_operator_cores(Rl, n1, n2, Rm, Rr, _dev(A1, "A1"), _dev(A2, "A2"),
+                                       _dev(A12, "A12"), _stream(stream)))
+    return A12
 
 
 def tt_local_matvec_two_site_workspace_size(rl, n1, n2, rr, Rl, Rm, Rr, nvec) -> int:

@@ -45,6 +45,7 @@ struct GemmParams {
   long long lda, ldb;   // A: (m,k) at m*lda+k if A_KC else k*lda+m;  B: (k,n) at n*ldb+k if B_KC else k*ldb+n
   IndexMap rowmap, colmap;
   long long tiles_n;
+  const int* gate;   // optional device flag: nonzero -> the launch is a no-op (iterative solvers)
 };
 
 __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool ok) {
@@ -82,6 +83,7 @@ struct GemmCfg {
 template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool A_KC, bool B_KC>
 __global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, 1)
 dmma_gemm_kernel(const GemmParams p) {
+  if (p.gate && *p.gate) return;
   using Cfg = GemmCfg<BM, BN, BK, WARPS_M, WARPS_N, STAGES, A_KC, B_KC>;
   constexpr int NT = Cfg::kThreads;
   constexpr int WTM = Cfg::WTM, WTN = Cfg::WTN, MI = Cfg::MI, NI = Cfg::NI;

@@ -76,6 +76,7 @@ struct GemmParamsV2 {
   IndexMap32 rowmap, colmap;
   int tiles_n, total_units, KT, ksplit, kt_per_split;
   int dbg;          // benchmark hook: bit 0 = skip output stores, bit 1 = skip operand loads
+  const int* gate;  // optional device flag: nonzero -> no-op
 };
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool ok) {
@@ -118,6 +119,7 @@ struct GemmV2Cfg {
 template <bool A_KC, bool B_KC, int BM_, int BN, int WARPS_M, int WARPS_N, int STAGES, int MINB>
 __global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, MINB)
 dmma_gemm_v2_kernel(const GemmParamsV2 p) {
+  if (p.gate && *p.gate) return;
   using Cfg = GemmV2Cfg<A_KC, B_KC, BM_, BN, WARPS_M, WARPS_N, STAGES, MINB>;
   constexpr int BM = Cfg::BM, BK = Cfg::BK, NT = Cfg::kThreads;
   constexpr int WTM = Cfg::WTM, WTN = Cfg::WTN, MI = Cfg::MI, NI = Cfg::NI;
@@ -356,7 +358,9 @@ dmma_gemm_v2_kernel(const GemmParamsV2 p) {
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const double* __restrict__ P,
                                                             double* __restrict__ C, int M, int N,
                                                             int ksplit, IndexMap32 rowmap,
-                                                            IndexMap32 colmap) {
+                                                            IndexMap32 colmap,
+                                                            const int* gate) {
+  if (gate && *gate) return;
   const long long MN = (long long)M * N;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < MN;
        e += (long long)gridDim.x * blockDim.x) {

@@ -40,6 +40,7 @@ struct GemmParamsV3 {
   int store_mode;   // 0 scalar; 1 column pairs (N-contiguous B, output contiguous along n);
                     // 2 row pairs (M-contiguous A, output contiguous along m) -> 16-byte stores
   int dbg;
+  const int* gate;  // optional device flag: nonzero -> no-op
 };
 
 __device__ __forceinline__ void stg_cs2(double* p, double a, double b) {
@@ -116,6 +117,7 @@ template <bool A_KC, bool B_KC, int BM, int BN, int WARPS_M, int WARPS_N, int ST
 __global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, MINB)
 dmma_gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const GemmParamsV3 p) {
+  if (p.gate && *p.gate) return;
   using Cfg = GemmV3Cfg<A_KC, B_KC, BM, BN, WARPS_M, WARPS_N, STAGES, MINB>;
   constexpr int WTM = Cfg::WTM, WTN = Cfg::WTN, MI = Cfg::MI, NI = Cfg::NI;
   constexpr int A_BYTES = Cfg::A_BYTES, STAGE_BYTES = Cfg::STAGE_BYTES;

@@ -194,6 +194,9 @@ int num_sms() {
 }
 
 thread_local int g_variant = -1;
+// device flag gating every GEMM launch of the calling thread (set by the iterative solvers
+// around their matvecs so that iterations after convergence cost launches only)
+thread_local const int* g_gate = nullptr;
 thread_local int g_dbg_flags = 0;   // tt_debug_set_flags   // test/benchmark hook (tt_debug_set_variant); -1 = auto
 
 // split-K scratch for the current stage (set by the stage planners; nullptr = no split)
@@ -225,6 +228,7 @@ cudaError_t launch_v2_cfg(const GemmParams& p0, cudaStream_t s) {
   p.C = p0.C;
   p.P = nullptr;
   p.dbg = g_dbg_flags;
+  p.gate = p0.gate;
   p.M = (int)p0.M;
   p.N = (int)p0.N;
   p.K = (int)p0.K;
@@ -266,7 +270,7 @@ cudaError_t launch_v2_cfg(const GemmParams& p0, cudaStream_t s) {
     long long blocks = (mn + 255) / 256;
     if (blocks > 8L * num_sms()) blocks = 8L * num_sms();
     tt::splitk_reduce_kernel<<<(unsigned)blocks, 256, 0, s>>>(p.P, p.C, p.M, p.N, ks, p.rowmap,
-                                                              p.colmap);
+                                                              p.colmap, p.gate);
     ++g_launches;
   }
   trace_end(tr, s);
@@ -371,6 +375,7 @@ cudaError_t launch_v3_cfg(const GemmParams& p0, cudaStream_t s, bool& ok) {
   p.C = p0.C;
   p.P = nullptr;
   p.dbg = g_dbg_flags;
+  p.gate = p0.gate;
   p.M = (int)p0.M;
   p.N = (int)p0.N;
   p.K = (int)p0.K;
@@ -447,7 +452,7 @@ cudaError_t launch_v3_cfg(const GemmParams& p0, cudaStream_t s, bool& ok) {
     long long blocks = (mn + 255) / 256;
     if (blocks > 8L * num_sms()) blocks = 8L * num_sms();
     tt::splitk_reduce_kernel<<<(unsigned)blocks, 256, 0, s>>>(p.P, p.C, p.M, p.N, ks, p.rowmap,
-                                                              p.colmap);
+                                                              p.colmap, p.gate);
     ++g_launches;
   }
   trace_end(tr, s);
@@ -540,6 +545,7 @@ GemmParams gp(const double* A, long long lda, const double* B, long long ldb, do
   p.rowmap = rm;
   p.colmap = cm;
   p.tiles_n = 1;
+  p.gate = g_gate;
   return p;
 }
 
@@ -989,6 +995,7 @@ bool same(const void* p, const void* q) { return p != nullptr && p == q; }
 
 #include "tt_gmres.cuh"
 #include "tt_round.cuh"
+#include "tt_lobpcg.cuh"
 
 // Symmetric eigendecomposition of the n x n Gram matrix G: lam (descending) and V (columns)
 // in the caller's buffers.  Scratch: 4 padded (np x np) buffers + partials (np = n rounded up
@@ -1968,6 +1975,85 @@ tt_status tt_local_gmres(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t 
                                 reinterpret_cast<long long*>(iters), workspace, workspace_bytes,
                                 static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "tt_local_gmres");
+  return TT_OK;
+}
+
+// ---- LOBPCG ---------------------------------------------------------
+size_t tt_local_lobpcg_workspace_size(int64_t rl, int64_t n, int64_t rr, int64_t RlA, int64_t RrA,
+                                      int64_t RlB, int64_t RrB, int64_t nb) {
+  Dims dA{rl, n, rr, RlA, RrA};
+  const bool has_B = RlB > 0 || RrB > 0;
+  Dims dB{rl, n, rr, has_B ? RlB : 1, has_B ? RrB : 1};
+  if (!dims_valid(dA) || !dims_valid(dB) || nb <= 0 || nb > kLobMaxNb) return 0;
+  long long t1a, t2a, aha, pea, t1b = 0, t2b = 0, ahb = 0, peb = 0;
+  if (!matvec_ws_elems(dA, nb, t1a, t2a, aha, pea)) return 0;
+  if (has_B && !matvec_ws_elems(dB, nb, t1b, t2b, ahb, peb)) return 0;
+  LobWs lw;
+  if (!lob_ws_elems(dA, nb, lw)) return 0;
+  return ws_bytes({std::max(t1a, t1b), std::max(t2a, t2b), std::max(pea, peb), aha, ahb, lw.blocks,
+                   lw.part, lw.gpart, lw.G, lw.Y, lw.small});
+}
+
+tt_status tt_local_lobpcg(int64_t rl, int64_t n, int64_t rr, int64_t RlA, int64_t RrA,
+                          int64_t RlB, int64_t RrB, int64_t nb, int64_t maxiter,
+                          int64_t refresh, double tol, const double* phiLA, const double* AA, const double* phiRA,
+                          const double* phiLB, const double* AB, const double* phiRB, double* X,
+                          double* lam, double* res, int64_t* iters, double* step,
+                          void* workspace, size_t workspace_bytes, void* stream) {
+  CallScope scope;
+  const bool has_B = phiLB || AB || phiRB;
+  if (has_B && (!phiLB || !AB || !phiRB))
+    return fail(TT_ERR_NULL_POINTER, "operator B needs all of phiL_B, A_B, phiR_B (or none: B = I)");
+  Dims dA{rl, n, rr, RlA, RrA};
+  tt_status st = check_dims(dA);
+  if (st != TT_OK) return st;
+  Dims dB{rl, n, rr, has_B ? RlB : 1, has_B ? RrB : 1};
+  if ((st = check_dims(dB)) != TT_OK) return st;
+  if (nb <= 0 || nb > kLobMaxNb) return fail(TT_ERR_INVALID_ARGUMENT, "nb must be in [1, 32]");
+  if (nb > rl * n * rr) return fail(TT_ERR_INVALID_ARGUMENT, "nb exceeds the local dimension");
+  if (maxiter < 0 || refresh < 0 || !(tol >= 0.0))
+    return fail(TT_ERR_INVALID_ARGUMENT, "need maxiter >= 0, refresh >= 0, tol >= 0");
+  if (!phiLA || !AA || !phiRA || !X || !lam || !res || !iters)
+    return fail(TT_ERR_NULL_POINTER, "NULL pointer");
+  const void* outs[] = {X, lam, res, iters, step};
+  const void* ins[] = {phiLA, AA, phiRA, phiLB, AB, phiRB};
+  for (const void* o : outs) {
+    for (const void* i : ins)
+      if (same(o, i)) return fail(TT_ERR_ALIASING, "an output aliases an input");
+    for (const void* o2 : outs)
+      if (o != o2 && same(o, o2)) return fail(TT_ERR_ALIASING, "two outputs alias");
+  }
+  const size_t need = tt_local_lobpcg_workspace_size(rl, n, rr, RlA, RrA, has_B ? RlB : 0,
+                                                     has_B ? RrB : 0, nb);
+  if (need == 0) return fail(TT_ERR_OVERFLOW, "workspace overflow");
+  if (!workspace || workspace_bytes < need)
+    return fail(TT_ERR_WORKSPACE, "workspace NULL or smaller than " + std::to_string(need) + " bytes");
+  cudaError_t e = enqueue_lobpcg(dA, dB, has_B, nb, maxiter, refresh, tol, phiLA, AA, phiRA, phiLB, AB,
+                                 phiRB, X, lam, res, reinterpret_cast<long long*>(iters), step,
+                                 workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "tt_local_lobpcg");
+  return TT_OK;
+}
+
+tt_status tt_merge_operator_cores(int64_t Rl, int64_t n1, int64_t n2, int64_t Rm, int64_t Rr,
+                                  const double* A1, const double* A2, double* A12, void* stream) {
+  CallScope scope;
+  if (Rl <= 0 || n1 <= 0 || n2 <= 0 || Rm <= 0 || Rr <= 0)
+    return fail(TT_ERR_INVALID_ARGUMENT, "extents must be positive");
+  bool ok = true;
+  const long long total = prod({Rl, n1, n2, n1, n2, Rr}, ok);
+  prod({Rl, n1, n1, Rm}, ok);
+  prod({Rm, n2, n2, Rr}, ok);
+  if (!ok) return fail(TT_ERR_OVERFLOW, "extent product overflows");
+  if (!A1 || !A2 || !A12) return fail(TT_ERR_NULL_POINTER, "NULL pointer");
+  if (same(A12, A1) || same(A12, A2)) return fail(TT_ERR_ALIASING, "output A12 aliases an input");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  long long blocks = (total + 255) / 256;
+  if (blocks > 4096) blocks = 4096;
+  merge_cores_kernel<<<(unsigned)blocks, 256, 0, s>>>(A1, A2, A12, Rl, n1, n2, Rm, Rr);
+  ++g_launches;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "tt_merge_operator_cores");
   return TT_OK;
 }
 

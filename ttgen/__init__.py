@@ -189,6 +189,17 @@ def spd_factor(rng: np.random.Generator, d: int, n: int, rank: int):
     return _tt_sum(g, ident)
 
 
+def symmetric_tt_matrix(rng: np.random.Generator, d: int, n: int, rank: int, fro: float = 1.0):
+    """A symmetric (indefinite) TT matrix of n^d x n^d: core-wise symmetrised N(0,1) cores of
+    rank `rank` (capped), scaled to Frobenius norm `fro` (the search direction dX of the
+    step-length eigenproblem; reading R12)."""
+    rg = capped_ranks(d, n * n, rank)
+    g = gaussian_tt_matrix(rng, n, n, rg, scale=False)
+    g = [(c + c.transpose(0, 2, 1, 3)) / 2.0 for c in g]
+    g[0] = g[0] * (fro / _tt_matrix_fro_norm(g))
+    return g
+
+
 def kron_sum_operator(X, Z, n: int):
     """A = X (x) I + I (x) Z (the L_X-like Kronecker sum of PAPER.md:449), built exactly with
     the core-wise Kronecker product and TT addition; stored rank r_X + r_Z."""
