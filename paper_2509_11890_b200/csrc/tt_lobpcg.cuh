@@ -164,15 +164,43 @@ struct GramArgs {
   const int* gate;
 };
 
-template <int IU, int JV>
+// Thread layout: G = 256 / (TU TV) groups split the 32 contraction indices of a staged chunk;
+// inside a group a TU x TV grid of threads owns IU x JV outputs each (rows tu + TU i, columns
+// tv + TV j); the G partial tiles are summed in shared memory in a fixed order.
+template <int TU, int TV, int IU, int JV>
+struct GramCfg {
+  static constexpr int G = 256 / (TU * TV), KB = 32, LD = KB + 1;
+  static size_t smem(int su, int sv) {
+    const size_t stage = (size_t)(su + sv) * LD, red = G > 1 ? (size_t)G * su * sv : 0;
+    return sizeof(double) * std::max(stage, red) + sizeof(long long) * (KB + su + sv);
+  }
+};
+
+template <int TU, int TV, int IU, int JV>
 __global__ void __launch_bounds__(256) lob_gram_kernel(const GramArgs g, double* __restrict__ part) {
   if (g.gate && *g.gate) return;
-  constexpr int KB = 32, LD = KB + 1;
+  using Cfg = GramCfg<TU, TV, IU, JV>;
+  constexpr int G = Cfg::G, KB = Cfg::KB, LD = Cfg::LD;
   extern __shared__ double gsm[];
   const int su = g.nu * g.nb, sv = g.nv * g.nb;
+  const size_t stage = (size_t)(su + sv) * LD, redsz = G > 1 ? (size_t)G * su * sv : 0;
+  const size_t dbl = stage > redsz ? stage : redsz;
   double* Us = gsm;              // [su][LD]
   double* Vs = gsm + su * LD;    // [sv][LD]
-  const int tid = threadIdx.x, tu = tid & 15, tv = tid >> 4;
+  long long* koff = reinterpret_cast<long long*>(gsm + dbl);   // [KB] element offsets
+  const double** rptr = reinterpret_cast<const double**>(koff + KB);   // [su + sv] columns
+  const int tid = threadIdx.x, grp = tid / (TU * TV), t2 = tid - grp * (TU * TV);
+  const int tu = t2 % TU, tv = t2 / TU;
+  // column r of the staged operand: block pointer index and in-block column offset
+  if (tid == 0) {   // column r of the staged operands: its block's base + column offset
+    for (int r = 0; r < su + sv; ++r) {
+      const int q = (r < su ? r : r - su) / g.nb, p = (r < su ? r : r - su) - q * g.nb;
+      const double* base = r < su ? (q == 0 ? g.U[0] : q == 1 ? g.U[1] : g.U[2])
+                                  : (q == 0 ? g.V[0] : q == 1 ? g.V[1] : q == 2 ? g.V[2]
+                                     : q == 3 ? g.V[3] : q == 4 ? g.V[4] : g.V[5]);
+      rptr[r] = base + (long long)p * g.rr;
+    }
+  }
   double acc[IU][JV];
 #pragma unroll
   for (int i = 0; i < IU; ++i)
@@ -181,26 +209,25 @@ __global__ void __launch_bounds__(256) lob_gram_kernel(const GramArgs g, double*
   const long long k0 = blockIdx.x * g.k_per_chunk;
   const long long k1 = min(g.kt, k0 + g.k_per_chunk);
   for (long long kb = k0; kb < k1; kb += KB) {
+    if (tid < KB) {
+      const long long k = kb + tid;
+      koff[tid] = k < k1 ? (k / g.rr) * g.nb * g.rr + (k % g.rr) : -1;
+    }
+    __syncthreads();
     for (int idx = tid; idx < (su + sv) * KB; idx += 256) {
-      const int r = idx / KB, bb = idx - r * KB;
-      const long long k = kb + bb;
-      double v = 0.0;
-      if (k < k1) {
-        const long long row = k / g.rr, b = k - row * g.rr;
-        const double* src = r < su ? g.U[r / g.nb] : g.V[(r - su) / g.nb];
-        const int p = (r < su ? r : r - su) % g.nb;
-        v = src[(row * g.nb + p) * g.rr + b];
-      }
+      const int r = idx >> 5, bb = idx & 31;
+      const long long off = koff[bb];
+      const double v = off >= 0 ? rptr[r][off] : 0.0;
       (r < su ? Us + r * LD : Vs + (r - su) * LD)[bb] = v;
     }
     __syncthreads();
-#pragma unroll 4
-    for (int bb = 0; bb < KB; ++bb) {
+#pragma unroll 2
+    for (int bb = grp; bb < KB; bb += G) {
       double u[IU], v[JV];
 #pragma unroll
-      for (int i = 0; i < IU; ++i) u[i] = (tu + 16 * i < su) ? Us[(tu + 16 * i) * LD + bb] : 0.0;
+      for (int i = 0; i < IU; ++i) u[i] = (tu + TU * i < su) ? Us[(tu + TU * i) * LD + bb] : 0.0;
 #pragma unroll
-      for (int j = 0; j < JV; ++j) v[j] = (tv + 16 * j < sv) ? Vs[(tv + 16 * j) * LD + bb] : 0.0;
+      for (int j = 0; j < JV; ++j) v[j] = (tv + TV * j < sv) ? Vs[(tv + TV * j) * LD + bb] : 0.0;
 #pragma unroll
       for (int i = 0; i < IU; ++i)
 #pragma unroll
@@ -209,11 +236,27 @@ __global__ void __launch_bounds__(256) lob_gram_kernel(const GramArgs g, double*
     __syncthreads();
   }
   double* out = part + (long long)blockIdx.x * su * sv;
+  if (G == 1) {
+#pragma unroll
+    for (int i = 0; i < IU; ++i)
+#pragma unroll
+      for (int j = 0; j < JV; ++j)
+        if (tu + TU * i < su && tv + TV * j < sv) out[(tu + TU * i) * sv + tv + TV * j] = acc[i][j];
+    return;
+  }
+  double* red = gsm;   // [G][su][sv] (the staging area is free after the last barrier)
 #pragma unroll
   for (int i = 0; i < IU; ++i)
 #pragma unroll
     for (int j = 0; j < JV; ++j)
-      if (tu + 16 * i < su && tv + 16 * j < sv) out[(tu + 16 * i) * sv + tv + 16 * j] = acc[i][j];
+      if (tu + TU * i < su && tv + TV * j < sv)
+        red[((size_t)grp * su + tu + TU * i) * sv + tv + TV * j] = acc[i][j];
+  __syncthreads();
+  for (int e = tid; e < su * sv; e += 256) {
+    double v = 0.0;
+    for (int q = 0; q < G; ++q) v += red[(size_t)q * su * sv + e];
+    out[e] = v;
+  }
 }
 
 // G[e] = sum_c part[c][e]  (fixed order: deterministic)
@@ -233,9 +276,14 @@ __global__ void lob_gram_finish_kernel(const double* __restrict__ part, int chun
 __device__ void lob_jacobi_cta(double* M, double* V, int np, double* cs, double* sn, int* pp,
                                int* qq, double* red) {
   const int tid = threadIdx.x, nt = blockDim.x, h = np / 2;
+  __shared__ int nrot;
   for (int e = tid; e < np * np; e += nt) V[e] = (e / np == e % np) ? 1.0 : 0.0;
+  if (tid == 0) nrot = 1;
   __syncthreads();
   for (int sw = 0; sw < 60; ++sw) {
+    // a sweep that applied no rotation (every off-diagonal entry negligible against its
+    // diagonal pair) ends the iteration; so does a negligible off-diagonal mass
+    if (nrot == 0) break;
     double off = 0.0, dia = 0.0;
     for (int e = tid; e < np * np; e += nt) {
       const double v = M[e];
@@ -257,6 +305,8 @@ __device__ void lob_jacobi_cta(double* M, double* V, int np, double* cs, double*
     }
     __syncthreads();
     if (!(offs > 1e-30 * dias)) break;   // also stops on an all-zero matrix
+    if (tid == 0) nrot = 0;
+    __syncthreads();
     for (int step = 0; step < np - 1; ++step) {
       for (int k = tid; k < h; k += nt) {
         int a = (k == 0) ? 0 : 1 + (k - 1 + step) % (np - 1);
@@ -265,12 +315,15 @@ __device__ void lob_jacobi_cta(double* M, double* V, int np, double* cs, double*
         pp[k] = a;
         qq[k] = b;
         double c = 1.0, s = 0.0;
-        const double apq = M[a * np + b];
-        if (apq != 0.0) {
-          const double tau = (M[b * np + b] - M[a * np + a]) / (2.0 * apq);
+        const double apq = M[a * np + b], app = M[a * np + a], aqq = M[b * np + b];
+        if (fabs(apq) > 1e-18 * sqrt(fabs(app * aqq))) {
+          const double tau = (aqq - app) / (2.0 * apq);
           const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-          c = 1.0 / sqrt(1.0 + t * t);
-          s = t * c;
+          if (t != 0.0) {
+            c = 1.0 / sqrt(1.0 + t * t);
+            s = t * c;
+            atomicAdd(&nrot, 1);
+          }
         }
         cs[k] = c;
         sn[k] = s;
@@ -280,6 +333,7 @@ __device__ void lob_jacobi_cta(double* M, double* V, int np, double* cs, double*
         const int kr = e / h, kc = e - kr * h;
         const int p = pp[kr], q = qq[kr], u = pp[kc], w = qq[kc];
         const double cr = cs[kr], sr = sn[kr], cc = cs[kc], sc = sn[kc];
+        if (sr == 0.0 && sc == 0.0) continue;
         const double mpu = M[p * np + u], mpw = M[p * np + w];
         const double mqu = M[q * np + u], mqw = M[q * np + w];
         const double rpu = cr * mpu - sr * mqu, rpw = cr * mpw - sr * mqw;
@@ -359,28 +413,98 @@ __global__ void __launch_bounds__(256) lob_rr_kernel(const double* __restrict__ 
     Dg[i] = gb > 0.0 ? 1.0 / sqrt(gb) : 0.0;
   }
   __syncthreads();
-  // equilibrated G_B (unit diagonal on nonzero columns), zero-padded to np
-  for (int e = tid; e < np * np; e += nt) {
-    const int i = e / np, j = e - i * np;
-    M0[e] = (i < s && j < s) ? GB(i, j) * Dg[i] * Dg[j] : 0.0;
-  }
-  __syncthreads();
-  lob_jacobi_cta(M0, M1, np, cs, sn, pp, qq, red);
-  __syncthreads();
+  // T with T^T G_B' T = I over the kept directions (G_B' = D G_B D, unit diagonal).  First
+  // try a Cholesky factorisation G_B' = L L^T (T = L^{-T}; the basis is kept well conditioned
+  // by construction: X L_B-orthonormal, W and P L_B-orthogonal to X, P L_B-orthonormal); on a
+  // pivot below 1e-8 fall back to the eigen-decomposition G_B' = U mu U^T, T = U mu^{-1/2},
+  // dropping mu <= 1e-12 mu_max (SVQB).  Zero columns (D = 0) are excluded either way.
+  __shared__ int chol_ok;
   if (tid == 0) {
-    double mx = 0.0;
-    for (int i = 0; i < np; ++i) mx = fmax(mx, M0[i * np + i]);
     int k = 0;
-    for (int i = 0; i < np; ++i)
-      if (mx > 0.0 && M0[i * np + i] > 1e-12 * mx) keep[k++] = i;
+    for (int i = 0; i < s; ++i)
+      if (Dg[i] > 0.0) keep[k++] = i;
     k_sh = k;
+    chol_ok = 1;
   }
   __syncthreads();
-  const int k = k_sh, kp = (k + 1) & ~1;
-  // T = U[:, keep] mu^{-1/2}  -> M2 (np x kp, zero-padded)
-  for (int e = tid; e < np * kp; e += nt) {
-    const int i = e / kp, c = e - i * kp;
-    M2[e] = c < k ? M1[i * np + keep[c]] / sqrt(M0[keep[c] * np + keep[c]]) : 0.0;
+  {
+    const int kc = k_sh;
+    // compacted equilibrated G_B over the nonzero columns -> M0 (kc x kc, ld np)
+    for (int e = tid; e < kc * kc; e += nt) {
+      const int i = e / kc, j = e - i * kc;
+      M0[i * np + j] = GB(keep[i], keep[j]) * Dg[keep[i]] * Dg[keep[j]];
+    }
+    __syncthreads();
+    for (int c = 0; c < kc; ++c) {   // right-looking Cholesky, lower triangle in place
+      if (tid == 0) {
+        const double d = M0[c * np + c];
+        if (!(d > 1e-8)) chol_ok = 0;
+        M0[c * np + c] = d > 0.0 ? sqrt(d) : 1.0;
+      }
+      __syncthreads();
+      if (!chol_ok) break;
+      const double piv = M0[c * np + c];
+      for (int i = c + 1 + tid; i < kc; i += nt) M0[i * np + c] /= piv;
+      __syncthreads();
+      for (int e = tid; e < (kc - c - 1) * (kc - c - 1); e += nt) {
+        const int i = c + 1 + e / (kc - c - 1), j = c + 1 + e % (kc - c - 1);
+        if (j <= i) M0[i * np + j] = fma(-M0[i * np + c], M0[j * np + c], M0[i * np + j]);
+      }
+      __syncthreads();
+    }
+    if (chol_ok) {
+      // Z = L^{-1} (forward substitution, one column per thread) -> M1;  T = Z^T -> M2
+      for (int j = tid; j < kc; j += nt) {
+        for (int i = 0; i < kc; ++i) {
+          double v = (i == j) ? 1.0 : 0.0;
+          if (i >= j) {
+            for (int l = j; l < i; ++l) v = fma(-M0[i * np + l], M1[l * np + j], v);
+            v /= M0[i * np + i];
+          } else {
+            v = 0.0;
+          }
+          M1[i * np + j] = v;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  int k, kp;
+  if (chol_ok) {
+    k = k_sh;
+    kp = (k + 1) & ~1;
+    // T[q][c] = Z[c][pos(q)] for kept q (Z^T: row index of T is the original column q)
+    for (int e = tid; e < np * kp; e += nt) M2[e] = 0.0;
+    __syncthreads();
+    for (int e = tid; e < k * k; e += nt) {
+      const int r = e / k, c = e - r * k;   // r: position of the original column keep[r]
+      M2[keep[r] * kp + c] = M1[c * np + r];
+    }
+  } else {
+    // SVQB fallback: equilibrated G_B (unit diagonal on nonzero columns), zero-padded to np
+    for (int e = tid; e < np * np; e += nt) {
+      const int i = e / np, j = e - i * np;
+      M0[e] = (i < s && j < s) ? GB(i, j) * Dg[i] * Dg[j] : 0.0;
+    }
+    __syncthreads();
+    lob_jacobi_cta(M0, M1, np, cs, sn, pp, qq, red);
+    __syncthreads();
+    if (tid == 0) {
+      double mx = 0.0;
+      for (int i = 0; i < np; ++i) mx = fmax(mx, M0[i * np + i]);
+      int kk = 0;
+      for (int i = 0; i < np; ++i)
+        if (mx > 0.0 && M0[i * np + i] > 1e-12 * mx) keep[kk++] = i;
+      k_sh = kk;
+    }
+    __syncthreads();
+    k = k_sh;
+    kp = (k + 1) & ~1;
+    // T = U[:, keep] mu^{-1/2}  -> M2 (np x kp, zero-padded)
+    for (int e = tid; e < np * kp; e += nt) {
+      const int i = e / kp, c = e - i * kp;
+      M2[e] = c < k ? M1[i * np + keep[c]] / sqrt(M0[keep[c] * np + keep[c]]) : 0.0;
+    }
   }
   __syncthreads();
   // equilibrated G_A -> M0
@@ -538,49 +662,70 @@ struct CombineArgs {
   const int* gate;
 };
 
+// NBT: compile-time bound on nb (accumulators); TB: consecutive b positions per thread
+// (TB = 2 uses 16-byte loads/stores; needs rr even)
+template <int NBT, int TB>
 __global__ void __launch_bounds__(128) lob_combine_kernel(const CombineArgs a) {
   if (a.gate && *a.gate) return;
   extern __shared__ double csm[];
-  const int s = a.nblk * a.nb;
+  const int s = a.nblk * a.nb, nb = a.nb;
   double* Ys = csm;
-  double* Yps = csm + s * a.nb;
-  for (int i = threadIdx.x; i < s * a.nb; i += blockDim.x) {
+  double* Yps = csm + s * nb;
+  for (int i = threadIdx.x; i < s * nb; i += blockDim.x) {
     Ys[i] = a.Y[i];
     if (a.Yp) Yps[i] = a.Yp[i];
   }
   __syncthreads();
-  const long long total = a.rows * a.rr;
+  const long long rrt = a.rr / TB, total = a.rows * rrt;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
-    const long long row = e / a.rr, b = e - row * a.rr;
+    const long long row = e / rrt, b = (e - row * rrt) * TB;
     for (int f = 0; f < a.nfam; ++f) {
-      double ax[kLobMaxNb], ap[kLobMaxNb];
+      double ax[NBT][TB], ap[NBT][TB];
 #pragma unroll
-      for (int m = 0; m < kLobMaxNb; ++m) ax[m] = ap[m] = 0.0;
+      for (int m = 0; m < NBT; ++m)
+#pragma unroll
+        for (int t = 0; t < TB; ++t) ax[m][t] = ap[m][t] = 0.0;
       for (int q = 0; q < a.nblk; ++q) {
-        const double* src = a.S[f][q] + row * a.nb * a.rr + b;
-        for (int p = 0; p < a.nb; ++p) {
-          const double v = src[(long long)p * a.rr];
-          const double* y = Ys + (q * a.nb + p) * a.nb;
-          const double* yp = Yps + (q * a.nb + p) * a.nb;
+        const double* src = a.S[f][q] + row * nb * a.rr + b;
+        for (int p = 0; p < nb; ++p) {
+          double v[TB];
+          if (TB == 2) {
+            const double2 w = *reinterpret_cast<const double2*>(src + (long long)p * a.rr);
+            v[0] = w.x;
+            v[TB - 1] = w.y;
+          } else {
+            v[0] = src[(long long)p * a.rr];
+          }
+          const double* y = Ys + (q * nb + p) * nb;
+          const double* yp = Yps + (q * nb + p) * nb;
 #pragma unroll
-          for (int m = 0; m < kLobMaxNb; ++m)
-            if (m < a.nb) {
-              ax[m] = fma(v, y[m], ax[m]);
-              if (a.Yp) ap[m] = fma(v, yp[m], ap[m]);
+          for (int m = 0; m < NBT; ++m)
+            if (m < nb) {
+              const double ym = y[m];
+#pragma unroll
+              for (int t = 0; t < TB; ++t) ax[m][t] = fma(v[t], ym, ax[m][t]);
+              if (a.Yp) {
+                const double ypm = yp[m];
+#pragma unroll
+                for (int t = 0; t < TB; ++t) ap[m][t] = fma(v[t], ypm, ap[m][t]);
+              }
             }
         }
       }
-      double* xo = a.Xn[f] + row * a.nb * a.rr + b;
+      double* xo = a.Xn[f] + row * nb * a.rr + b;
+      double* po = a.Yp ? a.Pn[f] + row * nb * a.rr + b : nullptr;
 #pragma unroll
-      for (int m = 0; m < kLobMaxNb; ++m)
-        if (m < a.nb) xo[(long long)m * a.rr] = ax[m];
-      if (a.Yp) {
-        double* po = a.Pn[f] + row * a.nb * a.rr + b;
-#pragma unroll
-        for (int m = 0; m < kLobMaxNb; ++m)
-          if (m < a.nb) po[(long long)m * a.rr] = ap[m];
-      }
+      for (int m = 0; m < NBT; ++m)
+        if (m < nb) {
+          if (TB == 2) {
+            *reinterpret_cast<double2*>(xo + (long long)m * a.rr) = make_double2(ax[m][0], ax[m][TB - 1]);
+            if (po) *reinterpret_cast<double2*>(po + (long long)m * a.rr) = make_double2(ap[m][0], ap[m][TB - 1]);
+          } else {
+            xo[(long long)m * a.rr] = ax[m][0];
+            if (po) po[(long long)m * a.rr] = ap[m][0];
+          }
+        }
     }
   }
 }
@@ -647,14 +792,20 @@ cudaError_t lob_set_smem_attrs() {
   static std::once_flag once;
   static cudaError_t err = cudaSuccess;
   std::call_once(once, [] {
-    err = cudaFuncSetAttribute(lob_gram_kernel<6, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)(sizeof(double) * 3 * kLobMaxS * 33));
+    err = cudaFuncSetAttribute(lob_gram_kernel<16, 16, 6, 12>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)GramCfg<16, 16, 6, 12>::smem(kLobMaxS, 2 * kLobMaxS));
+    if (err == cudaSuccess)
+      err = cudaFuncSetAttribute(lob_gram_kernel<16, 8, 3, 12>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)GramCfg<16, 8, 3, 12>::smem(48, 96));
     if (err == cudaSuccess)
       err = cudaFuncSetAttribute(lob_rr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)lob_rr_smem(kLobMaxS, kLobMaxNb));
-    if (err == cudaSuccess)
-      err = cudaFuncSetAttribute(lob_combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(sizeof(double) * 2 * kLobMaxS * kLobMaxNb));
+    for (auto fn : {lob_combine_kernel<16, 1>, lob_combine_kernel<16, 2>, lob_combine_kernel<32, 1>})
+      if (err == cudaSuccess)
+        err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(sizeof(double) * 2 * kLobMaxS * kLobMaxNb));
   });
   return err;
 }
@@ -753,16 +904,19 @@ cudaError_t enqueue_lobpcg(const Dims& dA, const Dims& dB, bool has_B, long long
     ga.k_per_chunk = L.k_per_gchunk;
     ga.gate = gate;
     const int su = nu * (int)nb, sv = nv * (int)nb;
-    const size_t smem = sizeof(double) * (size_t)(su + sv) * 33;
-    const int mx = std::max(su, (sv + 1) / 2);
-    if (mx <= 16)
-      lob_gram_kernel<1, 2><<<L.gchunks, 256, smem, s>>>(ga, gpart);
-    else if (mx <= 32)
-      lob_gram_kernel<2, 4><<<L.gchunks, 256, smem, s>>>(ga, gpart);
-    else if (mx <= 48)
-      lob_gram_kernel<3, 6><<<L.gchunks, 256, smem, s>>>(ga, gpart);
-    else
-      lob_gram_kernel<6, 12><<<L.gchunks, 256, smem, s>>>(ga, gpart);
+    if (su <= 12 && sv <= 24) {
+      using C = GramCfg<4, 4, 3, 6>;
+      lob_gram_kernel<4, 4, 3, 6><<<L.gchunks, 256, C::smem(su, sv), s>>>(ga, gpart);
+    } else if (su <= 24 && sv <= 48) {
+      using C = GramCfg<8, 8, 3, 6>;
+      lob_gram_kernel<8, 8, 3, 6><<<L.gchunks, 256, C::smem(su, sv), s>>>(ga, gpart);
+    } else if (su <= 48 && sv <= 96) {
+      using C = GramCfg<16, 8, 3, 12>;
+      lob_gram_kernel<16, 8, 3, 12><<<L.gchunks, 256, C::smem(su, sv), s>>>(ga, gpart);
+    } else {
+      using C = GramCfg<16, 16, 6, 12>;
+      lob_gram_kernel<16, 16, 6, 12><<<L.gchunks, 256, C::smem(su, sv), s>>>(ga, gpart);
+    }
     ++g_launches;
     const int n = su * sv;
     lob_gram_finish_kernel<<<(n + 255) / 256, 256, 0, s>>>(gpart, L.gchunks, n, out, gate);
@@ -805,7 +959,19 @@ cudaError_t enqueue_lobpcg(const Dims& dA, const Dims& dB, bool has_B, long long
     ca.Yp = nblk > 1 ? Yp : nullptr;
     ca.gate = gate;
     const size_t smem = sizeof(double) * 2 * (size_t)nblk * nb * nb;
-    lob_combine_kernel<<<(unsigned)cb, 128, smem, s>>>(ca);
+    const bool tb2 = (L.rr % 2) == 0 && nb <= 16;   // 32 x 2 accumulators would spill
+    long long cb2 = (L.rows * (tb2 ? L.rr / 2 : L.rr) + 127) / 128;
+    cb2 = std::min<long long>(std::max(1LL, cb2), 16LL * num_sms());
+#define LOB_COMBINE(NBT)                                                              \
+  do {                                                                                \
+    if (tb2) lob_combine_kernel<NBT, 2><<<(unsigned)cb2, 128, smem, s>>>(ca);          \
+    else lob_combine_kernel<NBT, 1><<<(unsigned)cb2, 128, smem, s>>>(ca);              \
+  } while (0)
+    if (nb <= 4) LOB_COMBINE(4);
+    else if (nb <= 8) LOB_COMBINE(8);
+    else if (nb <= 16) LOB_COMBINE(16);
+    else lob_combine_kernel<32, 1><<<(unsigned)cb2, 128, smem, s>>>(ca);
+#undef LOB_COMBINE
     ++g_launches;
     double* dst[6] = {X, AX, BX, P, AP, BP};
     double* src[6] = {nX, nAX, nBX, nP, nAP, nBP};
