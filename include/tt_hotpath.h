@@ -276,6 +276,47 @@ tt_status tt_local_lobpcg(int64_t rl, int64_t n, int64_t rr, int64_t RlA, int64_
 tt_status tt_merge_operator_cores(int64_t Rl, int64_t n1, int64_t n2, int64_t Rm, int64_t Rr,
                                   const double* A1, const double* A2, double* A12, void* stream);
 
+/* -------------------------------------------------------------------------------------
+ * NEXT row 3: core orthonormalisation and the block-index move.
+ *
+ * tt_orthonormalise: left- (TT_SWEEP_LEFT: cores 0..d-2 left-orthonormal, sum_{a,i}
+ * x[a,i,b] x[a,i,b'] = delta_{bb'}, the norm carried into core d-1) or right-
+ * (TT_SWEEP_RIGHT: cores 1..d-1 right-orthonormal, the norm carried into core 0)
+ * orthonormalisation of a TT vector, the represented tensor unchanged.  Every factorisation
+ * goes through the unfolding's Gram matrix and its eigendecomposition (as tt_round); exactly
+ * rank-deficient bonds shrink (r_out).  Arguments and workspace as tt_round.  Synchronous.
+ *
+ * tt_block_move_right / _left: "move the block index l to W_{k+1} or W_{k-1} ... by realising
+ * one step of the TT rounding procedure".  Right: Wk_hat (r0,n0,l,r1) and
+ * Wk1 (r1,n1,r2) -> Wk_out (r0,n0,s) left-orthonormal and Wk1_hat_out (s,n1,l,r2), from the
+ * SVD of the (r0 n0) x (l r1) unfolding truncated to the smallest s with
+ * ||sigma_{s:}||_2 <= delta ||sigma||_2 (s <= max_rank if max_rank > 0; numerical zeros
+ * dropped), so the block tensors W_l are reproduced to relative Frobenius error <= delta.
+ * Left: Wkm1 (r0,n0,r1) and Wk_hat (r1,n1,l,r2) -> Wkm1_hat_out (r0,n0,l,s) and Wk_out
+ * (s,n1,r2) right-orthonormal, from the (r1 l) x (n1 r2) unfolding.  Outputs are written
+ * with the returned extent s (*s_out, host); the caller sizes them for s = min of the
+ * unfolding's sides.  The smaller side must be <= 2048.  Synchronous (data-dependent s).
+ * Workspace: tt_block_move_workspace_size(r0, n0, l, r1, n1, r2) for the right move with
+ * those extents; for the left move pass (r0, n0, l, r1, n1, r2) of its own arguments.
+ * ------------------------------------------------------------------------------------- */
+size_t tt_orthonormalise_workspace_size(int64_t d, const int64_t* n, const int64_t* r);
+tt_status tt_orthonormalise(int64_t d, const int64_t* n, const int64_t* r_in,
+                            const double* const* cores_in, int direction, int64_t* r_out,
+                            double* const* cores_out, void* workspace, size_t workspace_bytes,
+                            void* stream);
+size_t tt_block_move_workspace_size(int64_t r0, int64_t n0, int64_t l, int64_t r1, int64_t n1,
+                                    int64_t r2);
+tt_status tt_block_move_right(int64_t r0, int64_t n0, int64_t l, int64_t r1, int64_t n1,
+                              int64_t r2, double delta, int64_t max_rank, const double* Wk_hat,
+                              const double* Wk1, double* Wk_out, double* Wk1_hat_out,
+                              int64_t* s_out, void* workspace, size_t workspace_bytes,
+                              void* stream);
+tt_status tt_block_move_left(int64_t r0, int64_t n0, int64_t r1, int64_t n1, int64_t l,
+                             int64_t r2, double delta, int64_t max_rank, const double* Wkm1,
+                             const double* Wk_hat, double* Wkm1_hat_out, double* Wk_out,
+                             int64_t* s_out, void* workspace, size_t workspace_bytes,
+                             void* stream);
+
 /* Number of kernel launches the last call on this thread enqueued. */
 int64_t tt_last_launch_count(void);
 /* Test hook: on != 0 routes every GEMM stage of the calling thread through the generic

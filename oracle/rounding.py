@@ -82,3 +82,42 @@ def tt_round(cores, delta: float, max_rank: int | None = None):
         SV = S[:rnew, None] * Vt[:rnew]
         cores[k + 1] = np.tensordot(SV, cores[k + 1], axes=(1, 0))
     return cores
+
+
+def _svd_rank(S: np.ndarray, delta: float, max_rank: int | None) -> int:
+    """Smallest s with ||S[s:]||_2 <= delta ||S||_2 (then capped at max_rank)."""
+    thr = delta * float(np.linalg.norm(S))
+    tail = np.sqrt(np.cumsum(S[::-1] ** 2))[::-1]      # tail[i] = ||S[i:]||
+    s = len(S)
+    for i in range(1, len(S) + 1):
+        if i == len(S) or tail[i] <= thr:
+            s = i
+            break
+    if max_rank:
+        s = min(s, max_rank)
+    return s
+
+
+def block_move_right(Wk_hat, Wk1, delta: float = 0.0, max_rank: int | None = None):
+    """Move the block index l of the Block-TT core Wk_hat (r0, n0, l, r1) into the next core
+    Wk1 (r1, n1, r2) by one SVD step of TT rounding (Def. Block TT PAPER.md:294-300):
+    Wk_hat[(a,i), (l,b)] = U S V^T, truncated to s; returns Wk = U_s (r0, n0, s) and
+    Wk1_hat[s, j, l, c] = sum_b (S V^T)_s[s, (l, b)] Wk1[b, j, c]."""
+    r0, n0, l, r1 = Wk_hat.shape
+    M = np.asarray(Wk_hat, dtype=np.float64).reshape(r0 * n0, l * r1)
+    U, S, Vt = np.linalg.svd(M, full_matrices=False)
+    s = _svd_rank(S, delta, max_rank)
+    C = (S[:s, None] * Vt[:s]).reshape(s, l, r1)
+    return U[:, :s].reshape(r0, n0, s), np.einsum("slb,bjc->sjlc", C, Wk1)
+
+
+def block_move_left(Wkm1, Wk_hat, delta: float = 0.0, max_rank: int | None = None):
+    """Mirror: move l of Wk_hat (r1, n1, l, r2) into the previous core Wkm1 (r0, n0, r1):
+    Wk_hat[(a,l), (j,c)] = U S V^T truncated to s; returns Wkm1_hat (r0, n0, l, s) =
+    Wkm1 x (U S)_s and Wk = V^T_s (s, n1, r2)."""
+    r1, n1, l, r2 = Wk_hat.shape
+    M = np.asarray(Wk_hat, dtype=np.float64).transpose(0, 2, 1, 3).reshape(r1 * l, n1 * r2)
+    U, S, Vt = np.linalg.svd(M, full_matrices=False)
+    s = _svd_rank(S, delta, max_rank)
+    C = (U[:, :s] * S[:s]).reshape(r1, l, s)
+    return np.einsum("ajb,bls->ajls", Wkm1, C), Vt[:s].reshape(s, n1, r2)

@@ -29,6 +29,8 @@ __all__ = [
     "tt_block_local_matvec", "tt_block_local_matvec_workspace_size", "TTBlockTerm",
     "tt_round", "tt_round_workspace_size", "tt_debug_sym_eigen",
     "tt_local_lobpcg", "tt_local_lobpcg_workspace_size", "tt_merge_operator_cores",
+    "tt_orthonormalise", "tt_orthonormalise_workspace_size", "tt_block_move_right",
+    "tt_block_move_left", "tt_block_move_workspace_size",
 ]
 
 STAGE_NAMES = {0: "perm", 1: "set", 2: "mv_s1", 3: "mv_s2", 4: "mv_s3", 5: "il_s1", 6: "il_s2",
@@ -97,6 +99,16 @@ lib.tt_local_lobpcg_workspace_size.argtypes = [_i64] * 8
 lib.tt_local_lobpcg.argtypes = [_i64] * 10 + [ctypes.c_double] + [_p] * 12 + [_sz, _p]
 lib.tt_local_lobpcg.restype = ctypes.c_int
 lib.tt_merge_operator_cores.argtypes = [_i64] * 5 + [_p] * 4
+lib.tt_orthonormalise_workspace_size.restype = _sz
+lib.tt_orthonormalise_workspace_size.argtypes = [_i64, _p, _p]
+lib.tt_orthonormalise.argtypes = [_i64, _p, _p, _p, ctypes.c_int, _p, _p, _p, _sz, _p]
+lib.tt_orthonormalise.restype = ctypes.c_int
+lib.tt_block_move_workspace_size.restype = _sz
+lib.tt_block_move_workspace_size.argtypes = [_i64] * 6
+lib.tt_block_move_right.argtypes = [_i64] * 6 + [ctypes.c_double, _i64] + [_p] * 6 + [_sz, _p]
+lib.tt_block_move_right.restype = ctypes.c_int
+lib.tt_block_move_left.argtypes = [_i64] * 6 + [ctypes.c_double, _i64] + [_p] * 6 + [_sz, _p]
+lib.tt_block_move_left.restype = ctypes.c_int
 lib.tt_merge_operator_cores.restype = ctypes.c_int
 lib.tt_debug_force_v1.argtypes = [ctypes.c_int]
 lib.tt_debug_force_v1.restype = None
@@ -482,6 +494,71 @@ def tt_round(cores, delta, max_rank=0, workspace=None, stream=None):
     ro = list(rout)
     return [outs[k].reshape(-1)[: ro[k] * n[k] * ro[k + 1]].reshape(ro[k], n[k], ro[k + 1])
             for k in range(d)]
+
+
+def tt_orthonormalise_workspace_size(n, r) -> int:
+    a64 = lambda v: (ctypes.c_int64 * len(v))(*v)
+    return int(lib.tt_orthonormalise_workspace_size(len(n), a64(n), a64(r)))
+
+
+def tt_orthonormalise(cores, direction=TT_SWEEP_LEFT, workspace=None, stream=None):
+    """Left- (TT_SWEEP_LEFT) or right- (TT_SWEEP_RIGHT) orthonormalisation of a TT vector
+    (SURVEY.md 8(f) row 3); the represented tensor is unchanged.  Synchronous.  Returns the
+    list of cores (bonds shrink only where the train is exactly rank deficient)."""
+    d = len(cores)
+    a64 = lambda v: (ctypes.c_int64 * len(v))(*v)
+    n = [int(c.shape[1]) for c in cores]
+    r = [int(c.shape[0]) for c in cores] + [int(cores[-1].shape[2])]
+    outs = [torch.empty_like(c) for c in cores]
+    rout = (ctypes.c_int64 * (d + 1))()
+    ws = _ws(int(lib.tt_orthonormalise_workspace_size(d, a64(n), a64(r))), workspace,
+             cores[0].device)
+    _check(lib.tt_orthonormalise(d, a64(n), a64(r), _ptrs(cores, "cores"), int(direction), rout,
+                                 _ptrs(outs, "cores_out"), ws.data_ptr(), ws.numel(),
+                                 _stream(stream)))
+    ro = list(rout)
+    return [outs[k].reshape(-1)[: ro[k] * n[k] * ro[k + 1]].reshape(ro[k], n[k], ro[k + 1])
+            for k in range(d)]
+
+
+def tt_block_move_workspace_size(r0, n0, l, r1, n1, r2) -> int:
+    return int(lib.tt_block_move_workspace_size(r0, n0, l, r1, n1, r2))
+
+
+def tt_block_move_right(Wk_hat, Wk1, delta=0.0, max_rank=0, workspace=None, stream=None):
+    """Move the block index of Wk_hat (r0,n0,l,r1) into Wk1 (r1,n1,r2) by one truncated SVD
+    step (PAPER.md:303).  Returns (Wk (r0,n0,s) left-orthonormal, Wk1_hat (s,n1,l,r2))."""
+    r0, n0, l, r1 = Wk_hat.shape
+    _, n1, r2 = Wk1.shape
+    smax = min(r0 * n0, l * r1)
+    Wk = torch.empty(r0 * n0 * smax, dtype=torch.float64, device=Wk_hat.device)
+    W1 = torch.empty(smax * n1 * l * r2, dtype=torch.float64, device=Wk_hat.device)
+    s_out = ctypes.c_int64()
+    ws = _ws(tt_block_move_workspace_size(r0, n0, l, r1, n1, r2), workspace, Wk_hat.device)
+    _check(lib.tt_block_move_right(r0, n0, l, r1, n1, r2, float(delta), int(max_rank),
+                                   _dev(Wk_hat, "Wk_hat"), _dev(Wk1, "Wk1"), _dev(Wk, "Wk_out"),
+                                   _dev(W1, "Wk1_hat_out"), ctypes.byref(s_out), ws.data_ptr(),
+                                   ws.numel(), _stream(stream)))
+    sk = s_out.value
+    return (Wk[: r0 * n0 * sk].reshape(r0, n0, sk), W1[: sk * n1 * l * r2].reshape(sk, n1, l, r2))
+
+
+def tt_block_move_left(Wkm1, Wk_hat, delta=0.0, max_rank=0, workspace=None, stream=None):
+    """Move the block index of Wk_hat (r1,n1,l,r2) into Wkm1 (r0,n0,r1).
+    Returns (Wkm1_hat (r0,n0,l,s), Wk (s,n1,r2) right-orthonormal)."""
+    r0, n0, r1 = Wkm1.shape
+    _, n1, l, r2 = Wk_hat.shape
+    smax = min(r1 * l, n1 * r2)
+    Wh = torch.empty(r0 * n0 * l * smax, dtype=torch.float64, device=Wk_hat.device)
+    Wk = torch.empty(smax * n1 * r2, dtype=torch.float64, device=Wk_hat.device)
+    s_out = ctypes.c_int64()
+    ws = _ws(tt_block_move_workspace_size(r0, n0, l, r1, n1, r2), workspace, Wk_hat.device)
+    _check(lib.tt_block_move_left(r0, n0, r1, n1, l, r2, float(delta), int(max_rank),
+                                  _dev(Wkm1, "Wkm1"), _dev(Wk_hat, "Wk_hat"), _dev(Wh, "Wkm1_hat_out"),
+                                  _dev(Wk, "Wk_out"), ctypes.byref(s_out), ws.data_ptr(),
+                                  ws.numel(), _stream(stream)))
+    sk = s_out.value
+    return (Wh[: r0 * n0 * l * sk].reshape(r0, n0, l, sk), Wk[: sk * n1 * r2].reshape(sk, n1, r2))
 
 
 def tt_round_workspace_size(n, r) -> int:

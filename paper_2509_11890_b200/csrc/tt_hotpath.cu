@@ -1061,6 +1061,42 @@ __global__ void scatter_add_col_kernel(const double* __restrict__ v, double* __r
   }
 }
 
+// W[r, c] = V[r * ldv + c] * f[c], r < rows, c < s
+__global__ void scale_cols_ld_kernel(const double* __restrict__ V, long long ldv,
+                                     const double* __restrict__ f, double* __restrict__ W,
+                                     long long rows, int s) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < rows * s;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long r = e / s;
+    const int c = (int)(e - r * s);
+    W[e] = V[r * ldv + c] * f[c];
+  }
+}
+
+// out (cols x rows) = in (rows x cols)^T, both row-major
+__global__ void transpose2d_kernel(const double* __restrict__ in, double* __restrict__ out,
+                                   long long rows, long long cols) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < rows * cols;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long i = e / cols, j = e - i * cols;
+    out[j * rows + i] = in[e];
+  }
+}
+// out (a, l, i, b) = in (a, i, l, b)   (the block index moved next to the left bond)
+__global__ void swap_mid_kernel(const double* __restrict__ in, double* __restrict__ out,
+                                long long a, long long ni, long long nl, long long b) {
+  const long long total = a * ni * nl * b;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    long long r = e;
+    const long long bb = r % b; r /= b;
+    const long long l = r % nl; r /= nl;
+    const long long i = r % ni;
+    const long long aa = r / ni;
+    out[((aa * nl + l) * ni + i) * b + bb] = in[e];
+  }
+}
+
 // Two-site supercore operator: A12[al, (i1 i2), (j1 j2), be] = sum_g A1[al,i1,j1,g] A2[g,i2,j2,be]
 // (the local operator of a pair of cores; tiny, one thread per output)
 __global__ void merge_cores_kernel(const double* __restrict__ A1, const double* __restrict__ A2,
@@ -1638,11 +1674,12 @@ size_t tt_round_workspace_size(int64_t d, const int64_t* n, const int64_t* r) {
                    sym_eigen_scratch(rmax)});
 }
 
-tt_status tt_round(int64_t d, const int64_t* n, const int64_t* r_in,
-                   const double* const* cores_in, double delta, int64_t max_rank, int64_t* r_out,
-                   double* const* cores_out, void* workspace, size_t workspace_bytes,
-                   void* stream) {
-  CallScope scope;
+// phases: bit 0 = right-to-left orthonormalisation, bit 1 = left-to-right truncation
+// (delta = 0, max_rank = 0: plain left-to-right orthonormalisation)
+static tt_status round_impl(int64_t d, const int64_t* n, const int64_t* r_in,
+                            const double* const* cores_in, double delta, int64_t max_rank,
+                            int64_t* r_out, double* const* cores_out, void* workspace,
+                            size_t workspace_bytes, void* stream, int phases, const char* who) {
   if (d <= 0) return fail(TT_ERR_INVALID_ARGUMENT, "d must be >= 1");
   if (!n || !r_in || !cores_in || !r_out || !cores_out) return fail(TT_ERR_NULL_POINTER, "NULL array");
   if (r_in[0] != 1 || r_in[d] != 1) return fail(TT_ERR_INVALID_ARGUMENT, "r_1 and r_{d+1} must be 1");
@@ -1702,7 +1739,7 @@ tt_status tt_round(int64_t d, const int64_t* n, const int64_t* r_in,
   };
   const double zero_rel = 1e-14;   // relative eigenvalue floor (numerical zero of the Gram)
   // right-to-left orthonormalisation: W_k = (V S)(S^-1 V^T W_k), W_{k-1} <- W_{k-1} V S
-  for (int64_t k = d - 1; k >= 1 && e == cudaSuccess; --k) {
+  for (int64_t k = d - 1; (phases & 1) && k >= 1 && e == cudaSuccess; --k) {
     const long long rk = r[k], q = n[k] * r[k + 1];
     g_stage = TT_ST_IL_S1;
     e = launch_gemm(true, true, gp(W[k], q, W[k], q, G, rk, rk, q, tt::map_plain(rk),
@@ -1733,7 +1770,7 @@ tt_status tt_round(int64_t d, const int64_t* n, const int64_t* r_in,
   }
   // left-to-right truncation with threshold delta / sqrt(d-1) ||T||
   double thr = 0.0;
-  for (int64_t k = 0; k < d - 1 && e == cudaSuccess; ++k) {
+  for (int64_t k = 0; (phases & 2) && k < d - 1 && e == cudaSuccess; ++k) {
     const long long m = r[k] * n[k], rk1 = r[k + 1];
     g_stage = TT_ST_IL_S2;
     e = launch_gemm(false, false, gp(W[k], rk1, W[k], rk1, G, rk1, rk1, m, tt::map_plain(rk1),
@@ -1779,8 +1816,238 @@ tt_status tt_round(int64_t d, const int64_t* n, const int64_t* r_in,
     e = cudaMemcpyAsync(cores_out[k], W[k], sizeof(double) * r[k] * n[k] * r[k + 1],
                         cudaMemcpyDeviceToDevice, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  if (e != cudaSuccess) return cuda_fail(e, "tt_round");
+  if (e != cudaSuccess) return cuda_fail(e, who);
   for (int64_t k = 0; k <= d; ++k) r_out[k] = r[k];
+  return TT_OK;
+}
+
+tt_status tt_round(int64_t d, const int64_t* n, const int64_t* r_in,
+                   const double* const* cores_in, double delta, int64_t max_rank, int64_t* r_out,
+                   double* const* cores_out, void* workspace, size_t workspace_bytes,
+                   void* stream) {
+  CallScope scope;
+  return round_impl(d, n, r_in, cores_in, delta, max_rank, r_out, cores_out, workspace,
+                    workspace_bytes, stream, 3, "tt_round");
+}
+
+size_t tt_orthonormalise_workspace_size(int64_t d, const int64_t* n, const int64_t* r) {
+  return tt_round_workspace_size(d, n, r);
+}
+
+tt_status tt_orthonormalise(int64_t d, const int64_t* n, const int64_t* r_in,
+                            const double* const* cores_in, int direction, int64_t* r_out,
+                            double* const* cores_out, void* workspace, size_t workspace_bytes,
+                            void* stream) {
+  CallScope scope;
+  if (direction != TT_SWEEP_LEFT && direction != TT_SWEEP_RIGHT)
+    return fail(TT_ERR_INVALID_ARGUMENT, "direction must be TT_SWEEP_LEFT or TT_SWEEP_RIGHT");
+  return round_impl(d, n, r_in, cores_in, 0.0, 0, r_out, cores_out, workspace, workspace_bytes,
+                    stream, direction == TT_SWEEP_LEFT ? 2 : 1, "tt_orthonormalise");
+}
+
+// ---- block-index move ---------------------------------
+// Thin SVD of an m x q matrix M through the Gram matrix of its smaller side: the leading s
+// left singular vectors Us (m x s) and right singular vectors Vs (q x s), truncated at
+// ||sigma_{s:}|| <= delta ||sigma|| (numerical zeros lambda <= 1e-14 lambda_max dropped) and
+// s <= max_rank.  One host synchronisation (the truncation is data dependent).
+struct SvdBufs {
+  double *G, *E, *lam, *esc, *f, *Us, *Vs;
+};
+static long long svd_ws_elems(long long m, long long q) {
+  const long long k = std::min(m, q), big = std::max(m, q);
+  // G, E (<= k^2 + big k), lam, eigen scratch, f, Us + Vs (<= 2 big k), alignment slack
+  return 2 * k * k + 3 * big * k + 3 * k + 128 + sym_eigen_scratch(k) + 12 * 32;
+}
+static cudaError_t svd_gram(const double* M, long long m, long long q, double delta,
+                            long long max_rank, SvdBufs& b, int& s_out, cudaStream_t s) {
+  const bool left = m <= q;   // Gram of the smaller side
+  const long long k = left ? m : q;
+  cudaError_t e;
+  g_stage = TT_ST_IL_S1;
+  if (left)   // G = M M^T (m x m)
+    e = launch_gemm(true, true, gp(M, q, M, q, b.G, m, m, q, tt::map_plain(m), tt::map_plain(1)), s);
+  else        // G = M^T M (q x q)
+    e = launch_gemm(false, false, gp(M, q, M, q, b.G, q, q, m, tt::map_plain(q), tt::map_plain(1)), s);
+  if (e != cudaSuccess) return e;
+  if ((e = launch_sym_eigen(b.G, b.E, b.lam, (int)k, b.esc, s)) != cudaSuccess) return e;
+  std::vector<double> hl(k);
+  if ((e = cudaMemcpyAsync(hl.data(), b.lam, sizeof(double) * k, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+    return e;
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+  double tot = 0.0;
+  int nz = 0;
+  for (long long i = 0; i < k; ++i) {
+    tot += std::max(hl[i], 0.0);
+    if (hl[i] > 1e-14 * hl[0] && hl[i] > 0.0) ++nz;
+  }
+  if (nz == 0) nz = 1;
+  const double thr = delta * std::sqrt(tot);
+  int sk = nz;
+  double tail = 0.0;
+  for (int i = nz - 1; i >= 1; --i) {
+    tail += std::max(hl[i], 0.0);
+    if (std::sqrt(tail) <= thr) sk = i; else break;
+  }
+  if (max_rank > 0 && sk > max_rank) sk = (int)max_rank;
+  s_out = sk;
+  // E[:, :sk] (k x sk) -> the singular vectors of the Gram side; the other side by a GEMM
+  std::vector<double> hf(sk);
+  for (int i = 0; i < sk; ++i) hf[i] = 1.0;
+  if ((e = cudaMemcpyAsync(b.f, hf.data(), sizeof(double) * sk, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+    return e;
+  double* side = left ? b.Us : b.Vs;
+  scale_cols_kernel<<<(unsigned)((k * sk + 255) / 256), 256, 0, s>>>(b.E, b.f, side, (int)k, sk);
+  ++g_launches;
+  for (int i = 0; i < sk; ++i) hf[i] = 1.0 / std::sqrt(std::max(hl[i], 1e-300));
+  double* fin = b.f + 32 * ((sk + 31) / 32);
+  if ((e = cudaMemcpyAsync(fin, hf.data(), sizeof(double) * sk, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+    return e;
+  // the other side: Vs = M^T Us Sigma^-1  or  Us = M Vs Sigma^-1 (scale columns afterwards)
+  double* other = left ? b.Vs : b.Us;
+  if (left)   // Vs (q x sk) = M^T (q x m) . Us (m x sk)
+    e = launch_gemm(false, false, gp(M, q, b.Us, sk, b.E, q, sk, m, tt::map_plain(sk), tt::map_plain(1)), s);
+  else        // Us (m x sk) = M (m x q) . Vs (q x sk)
+    e = launch_gemm(true, false, gp(M, q, b.Vs, sk, b.E, m, sk, q, tt::map_plain(sk), tt::map_plain(1)), s);
+  if (e != cudaSuccess) return e;
+  const long long ob = left ? q : m;
+  scale_cols_ld_kernel<<<(unsigned)std::min<long long>(4096, (ob * sk + 255) / 256), 256, 0, s>>>(
+      b.E, sk, fin, other, ob, sk);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+static bool block_move_ws(long long m, long long q, long long extra, long long& total) {
+  total = svd_ws_elems(m, q) + m * q + extra;
+  return m > 0 && q > 0;
+}
+
+size_t tt_block_move_workspace_size(int64_t r0, int64_t n0, int64_t l, int64_t r1, int64_t n1,
+                                    int64_t r2) {
+  if (r0 <= 0 || n0 <= 0 || l <= 0 || r1 <= 0 || n1 <= 0 || r2 <= 0) return 0;
+  bool ok = true;
+  // right move: M = (r0 n0) x (l r1);  left move: M = (r0 l) x (n0 r1) with (r0,n0,l,r1) the
+  // core carrying the block index -- size for the larger of the two views
+  const long long m1 = prod({r0, n0}, ok), q1 = prod({l, r1}, ok);
+  const long long m2 = prod({r1, l}, ok), q2 = prod({n1, r2}, ok);
+  const long long out = prod({std::max(m1, q1), std::max(n1 * r2, r0 * n0), l}, ok);
+  if (!ok) return 0;
+  long long a, b;
+  block_move_ws(m1, q1, out, a);
+  block_move_ws(m2, q2, out, b);
+  return ws_bytes({std::max(a, b)});
+}
+
+tt_status tt_block_move_right(int64_t r0, int64_t n0, int64_t l, int64_t r1, int64_t n1,
+                              int64_t r2, double delta, int64_t max_rank, const double* Wk_hat,
+                              const double* Wk1, double* Wk_out, double* Wk1_hat_out,
+                              int64_t* s_out, void* workspace, size_t workspace_bytes,
+                              void* stream) {
+  CallScope scope;
+  if (r0 <= 0 || n0 <= 0 || l <= 0 || r1 <= 0 || n1 <= 0 || r2 <= 0)
+    return fail(TT_ERR_INVALID_ARGUMENT, "extents must be positive");
+  if (!(delta >= 0.0) || max_rank < 0) return fail(TT_ERR_INVALID_ARGUMENT, "need delta >= 0, max_rank >= 0");
+  if (!Wk_hat || !Wk1 || !Wk_out || !Wk1_hat_out || !s_out) return fail(TT_ERR_NULL_POINTER, "NULL pointer");
+  for (const void* o : {(const void*)Wk_out, (const void*)Wk1_hat_out})
+    if (same(o, Wk_hat) || same(o, Wk1)) return fail(TT_ERR_ALIASING, "an output aliases an input");
+  if (same(Wk_out, Wk1_hat_out)) return fail(TT_ERR_ALIASING, "two outputs alias");
+  const long long m = r0 * n0, q = l * r1;
+  if (std::min(m, q) > 2048)
+    return fail(TT_ERR_INVALID_ARGUMENT, "min(r0 n0, l r1) above 2048 is not supported");
+  const size_t need = tt_block_move_workspace_size(r0, n0, l, r1, n1, r2);
+  if (need == 0) return fail(TT_ERR_OVERFLOW, "workspace overflow");
+  if (!workspace || workspace_bytes < need)
+    return fail(TT_ERR_WORKSPACE, "workspace NULL or smaller than " + std::to_string(need) + " bytes");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const long long k = std::min(m, q), big = std::max(m, q);
+  Carver c{static_cast<char*>(workspace), workspace_bytes};
+  SvdBufs b;
+  b.G = c.take(k * k);
+  b.E = c.take(std::max(k * k, big * k));
+  b.lam = c.take(k);
+  b.esc = c.take(sym_eigen_scratch(k));
+  b.f = c.take(2 * (k + 64));
+  b.Us = c.take(m * k);
+  b.Vs = c.take(q * k);
+  double* C = c.take(k * q);
+  if (!c.ok) return fail(TT_ERR_WORKSPACE, "workspace too small after alignment");
+  int sk = 0;
+  cudaError_t e = svd_gram(Wk_hat, m, q, delta, max_rank, b, sk, s);
+  // Wk_out = Us (m x sk);  C (sk x q) = Us^T M
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(Wk_out, b.Us, sizeof(double) * m * sk, cudaMemcpyDeviceToDevice, s);
+  g_stage = TT_ST_IL_S2;
+  if (e == cudaSuccess)
+    e = launch_gemm(false, false, gp(b.Us, sk, Wk_hat, q, C, sk, q, m, tt::map_plain(q),
+                                     tt::map_plain(1)), s);
+  // Wk1_hat_out[s, j, l, c] = sum_b C[s, l, b] Wk1[b, j, c]: rows (s, l), cols (j, c)
+  if (e == cudaSuccess)
+    e = launch_gemm(true, false, gp(C, r1, Wk1, n1 * r2, Wk1_hat_out, sk * l, n1 * r2, r1,
+                                    tt::map2(l, r2, n1 * l * r2), tt::map2(r2, 1, l * r2)), s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "tt_block_move_right");
+  *s_out = sk;
+  return TT_OK;
+}
+
+tt_status tt_block_move_left(int64_t r0, int64_t n0, int64_t r1, int64_t n1, int64_t l,
+                             int64_t r2, double delta, int64_t max_rank, const double* Wkm1,
+                             const double* Wk_hat, double* Wkm1_hat_out, double* Wk_out,
+                             int64_t* s_out, void* workspace, size_t workspace_bytes,
+                             void* stream) {
+  CallScope scope;
+  if (r0 <= 0 || n0 <= 0 || l <= 0 || r1 <= 0 || n1 <= 0 || r2 <= 0)
+    return fail(TT_ERR_INVALID_ARGUMENT, "extents must be positive");
+  if (!(delta >= 0.0) || max_rank < 0) return fail(TT_ERR_INVALID_ARGUMENT, "need delta >= 0, max_rank >= 0");
+  if (!Wkm1 || !Wk_hat || !Wk_out || !Wkm1_hat_out || !s_out) return fail(TT_ERR_NULL_POINTER, "NULL pointer");
+  for (const void* o : {(const void*)Wk_out, (const void*)Wkm1_hat_out})
+    if (same(o, Wk_hat) || same(o, Wkm1)) return fail(TT_ERR_ALIASING, "an output aliases an input");
+  if (same(Wk_out, Wkm1_hat_out)) return fail(TT_ERR_ALIASING, "two outputs alias");
+  const long long m = r1 * l, q = n1 * r2;
+  if (std::min(m, q) > 2048)
+    return fail(TT_ERR_INVALID_ARGUMENT, "min(r1 l, n1 r2) above 2048 is not supported");
+  const size_t need = tt_block_move_workspace_size(r0, n0, l, r1, n1, r2);
+  if (need == 0) return fail(TT_ERR_OVERFLOW, "workspace overflow");
+  if (!workspace || workspace_bytes < need)
+    return fail(TT_ERR_WORKSPACE, "workspace NULL or smaller than " + std::to_string(need) + " bytes");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const long long k = std::min(m, q), big = std::max(m, q);
+  Carver c{static_cast<char*>(workspace), workspace_bytes};
+  SvdBufs b;
+  b.G = c.take(k * k);
+  b.E = c.take(std::max(k * k, big * k));
+  b.lam = c.take(k);
+  b.esc = c.take(sym_eigen_scratch(k));
+  b.f = c.take(2 * (k + 64));
+  b.Us = c.take(m * k);
+  b.Vs = c.take(q * k);
+  double* Mp = c.take(m * q);
+  double* C = c.take(m * k);
+  if (!c.ok) return fail(TT_ERR_WORKSPACE, "workspace too small after alignment");
+  long long blocks = std::min<long long>(4096, (m * q + 255) / 256);
+  // M (r1 l) x (n1 r2) from Wk_hat (r1, n1, l, r2)
+  swap_mid_kernel<<<(unsigned)blocks, 256, 0, s>>>(Wk_hat, Mp, r1, n1, l, r2);
+  ++g_launches;
+  int sk = 0;
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = svd_gram(Mp, m, q, delta, max_rank, b, sk, s);
+  // Wk_out (sk x q) = Vs^T;  C (m x sk) = M Vs = Us Sigma
+  if (e == cudaSuccess) {
+    transpose2d_kernel<<<(unsigned)std::min<long long>(4096, (q * sk + 255) / 256), 256, 0, s>>>(
+        b.Vs, Wk_out, q, sk);
+    ++g_launches;
+    e = cudaGetLastError();
+  }
+  g_stage = TT_ST_IL_S2;
+  if (e == cudaSuccess)
+    e = launch_gemm(true, false, gp(Mp, q, b.Vs, sk, C, m, sk, q, tt::map_plain(sk),
+                                    tt::map_plain(1)), s);
+  // Wkm1_hat_out (r0 n0) x (l sk) = Wkm1 (r0 n0 x r1) . C (r1 x (l sk))
+  if (e == cudaSuccess)
+    e = launch_gemm(true, false, gp(Wkm1, r1, C, l * sk, Wkm1_hat_out, r0 * n0, l * sk, r1,
+                                    tt::map_plain(l * sk), tt::map_plain(1)), s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "tt_block_move_left");
+  *s_out = sk;
   return TT_OK;
 }
 

@@ -1,0 +1,150 @@
+"""GPU parity for SURVEY.md §8(f) row 3 beyond rounding: core orthonormalisation and the
+block-index move against oracle/rounding.py.
+
+SVD factors are unique only up to signs/rotations, so the comparisons are on what is unique:
+the represented (block) tensors, the truncation rank, orthonormality, and orthogonal
+projectors onto the kept singular subspaces (gapped spectra)."""
+import numpy as np
+import pytest
+
+import ttgen
+from dense_ref import full_vector, left_interface, rel_fro
+from oracle.rounding import (block_move_left, block_move_right, orthonormalise_left,
+                             orthonormalise_right)
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tt():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2509_11890_b200 as m
+    return m
+
+
+def g(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def h(t):
+    return t.detach().cpu().numpy()
+
+
+def _graded(rng, m, q, sig):
+    U = np.linalg.qr(rng.standard_normal((m, len(sig))))[0]
+    V = np.linalg.qr(rng.standard_normal((q, len(sig))))[0]
+    return (U * sig) @ V.T
+
+
+@pytest.mark.parametrize("direction", ["left", "right"])
+def test_orthonormalise_vs_oracle(tt, direction):
+    rng = np.random.default_rng(31)
+    d, N = 6, 4
+    x = ttgen.gaussian_tt_vector(rng, N, ttgen.capped_ranks(d, N, 12))
+    flag = tt.TT_SWEEP_LEFT if direction == "left" else tt.TT_SWEEP_RIGHT
+    out = [h(c) for c in tt.tt_orthonormalise([g(c) for c in x], flag)]
+    ref = orthonormalise_left(x) if direction == "left" else orthonormalise_right(x)
+    assert [c.shape for c in out] == [c.shape for c in ref]
+    assert rel_fro(full_vector(out), full_vector(x)) <= 1e-11
+    ks = range(d - 1) if direction == "left" else range(1, d)
+    for k in ks:
+        c = out[k]
+        M = c.reshape(-1, c.shape[2]) if direction == "left" else c.reshape(c.shape[0], -1).T
+        # the factorisations go through Gram matrices: orthonormality to ~ eps kappa^2
+        assert np.abs(M.T @ M - np.eye(M.shape[1])).max() <= 1e-11
+    if direction == "left":   # the left interfaces span the same subspaces as the oracle's
+        for k in (1, 2, 3):
+            A, B = left_interface(out, k), left_interface(ref, k)
+            assert np.abs(A @ A.T - B @ B.T).max() <= 1e-11
+
+
+@pytest.mark.parametrize("shape", [(3, 4, 4, 5, 4, 2), (16, 4, 2, 40, 4, 8), (8, 4, 4, 4, 4, 16)])
+def test_block_move_right_exact(tt, shape):
+    r0, n0, l, r1, n1, r2 = shape
+    rng = np.random.default_rng(32)
+    Wk_hat = rng.standard_normal((r0, n0, l, r1))
+    Wk1 = rng.standard_normal((r1, n1, r2))
+    Wk, W1 = tt.tt_block_move_right(g(Wk_hat), g(Wk1))
+    Wk, W1 = h(Wk), h(W1)
+    rk, r1k = block_move_right(Wk_hat, Wk1)
+    assert Wk.shape == rk.shape and W1.shape == r1k.shape
+    M = Wk.reshape(r0 * n0, -1)
+    assert np.abs(M.T @ M - np.eye(M.shape[1])).max() <= 1e-11
+    T0 = np.einsum("ailb,bjc->ailjc", Wk_hat, Wk1)
+    assert rel_fro(np.einsum("ais,sjlc->ailjc", Wk, W1), T0) <= 1e-11
+
+
+@pytest.mark.parametrize("delta", [1e-2, 1e-4])
+@pytest.mark.parametrize("m_lt_q", [True, False])
+def test_block_move_right_truncated(tt, delta, m_lt_q):
+    rng = np.random.default_rng(33)
+    r0, n0, l, r1, n1, r2 = (4, 4, 4, 8, 4, 3) if m_lt_q else (16, 4, 2, 6, 4, 3)
+    sig = np.array([3.0, 2.0, 1.0, 0.5, 1e-3, 5e-4, 1e-6, 1e-7])
+    Wk_hat = _graded(rng, r0 * n0, l * r1, sig).reshape(r0, n0, l, r1)
+    Wk1 = rng.standard_normal((r1, n1, r2))
+    Wk, W1 = (h(t) for t in tt.tt_block_move_right(g(Wk_hat), g(Wk1), delta))
+    rk, r1k = block_move_right(Wk_hat, Wk1, delta)
+    assert Wk.shape == rk.shape
+    P, Pr = Wk.reshape(r0 * n0, -1), rk.reshape(r0 * n0, -1)
+    # the kept singular subspace through the Gram matrix: accurate to ~ eps kappa^2,
+    # kappa = sigma_max / sigma_min(kept)
+    kappa = sig[0] / sig[Wk.shape[2] - 1]
+    assert np.abs(P @ P.T - Pr @ Pr.T).max() <= 1e-13 * kappa ** 2
+    T = np.einsum("ais,sjlc->ailjc", Wk, W1)
+    Tr = np.einsum("ais,sjlc->ailjc", rk, r1k)
+    assert rel_fro(T, Tr) <= 1e-10
+
+
+@pytest.mark.parametrize("shape", [(2, 4, 5, 4, 3, 6), (8, 4, 32, 4, 4, 8)])
+def test_block_move_left_vs_oracle(tt, shape):
+    r0, n0, r1, n1, l, r2 = shape
+    rng = np.random.default_rng(34)
+    Wkm1 = rng.standard_normal((r0, n0, r1))
+    Wk_hat = rng.standard_normal((r1, n1, l, r2))
+    Wh, Wk = (h(t) for t in tt.tt_block_move_left(g(Wkm1), g(Wk_hat)))
+    rh, rk = block_move_left(Wkm1, Wk_hat)
+    assert Wh.shape == rh.shape and Wk.shape == rk.shape
+    R = Wk.reshape(Wk.shape[0], -1)
+    assert np.abs(R @ R.T - np.eye(R.shape[0])).max() <= 1e-11
+    T0 = np.einsum("ajb,bilc->ajilc", Wkm1, Wk_hat)
+    assert rel_fro(np.einsum("ajls,sic->ajilc", Wh, Wk), T0) <= 1e-11
+
+
+def test_block_move_config5_size(tt):
+    """Interior core of config 5 with the 4-component KKT block index:
+    (256, 4, 4, 256) -> 1024 x 1024 unfolding, delta = 1e-6 on a graded spectrum."""
+    rng = np.random.default_rng(35)
+    r0 = r1 = 256
+    sig = np.concatenate([np.geomspace(1.0, 1e-3, 200), np.geomspace(1e-9, 1e-12, 56)])
+    Wk_hat = _graded(rng, r0 * 4, 4 * r1, sig).reshape(r0, 4, 4, r1)
+    Q = np.linalg.qr(rng.standard_normal((4 * 1024, r1)))[0]    # (n1 r2) x r1, orthonormal
+    Wk1 = np.ascontiguousarray(Q.T.reshape(r1, 4, 1024))
+    Wk, W1 = (h(t) for t in tt.tt_block_move_right(g(Wk_hat), g(np.ascontiguousarray(Wk1)),
+                                                   1e-6))
+    rk, r1k = block_move_right(Wk_hat, Wk1, 1e-6)
+    assert Wk.shape[2] == rk.shape[2] == 200
+    P, Pr = Wk.reshape(1024, -1), rk.reshape(1024, -1)
+    kappa = 1e3
+    assert np.abs(P.T @ P - np.eye(200)).max() <= 1e-13 * kappa ** 2
+    assert np.abs(P @ P.T - Pr @ Pr.T).max() <= 1e-13 * kappa ** 2
+    T = np.einsum("ais,sjlc->ailjc", Wk, W1)
+    Tr = np.einsum("ais,sjlc->ailjc", rk, r1k)
+    assert rel_fro(T, Tr) <= 1e-10
+
+
+def test_block_move_errors(tt):
+    import ctypes
+    buf = torch.zeros(16, dtype=torch.float64, device="cuda")
+    p = buf.data_ptr()
+    s_out = ctypes.c_int64()
+    # both sides of the unfolding above 2048: refused before the workspace is examined
+    assert tt.lib.tt_block_move_right(64, 64, 64, 64, 2, 2, 0.0, 0, p, p + 8, p + 16, p + 24,
+                                      ctypes.byref(s_out), None, 0, None) == 1
+    # NULL workspace
+    assert tt.lib.tt_block_move_right(3, 4, 2, 5, 4, 2, 0.0, 0, p, p + 8, p + 16, p + 24,
+                                      ctypes.byref(s_out), None, 0, None) == 4
+    # aliasing output/input
+    assert tt.lib.tt_block_move_left(3, 4, 5, 4, 2, 2, 0.0, 0, p, p + 8, p, p + 24,
+                                     ctypes.byref(s_out), None, 0, None) == 3

@@ -77,3 +77,86 @@ def test_round_rank_one_stays_rank_one():
     y = tt_round(_tt_sum(ones, ones), 1e-12)
     assert all(c.shape[0] == 1 and c.shape[2] == 1 for c in y)
     assert rel_fro(full_vector(y), 2 * full_vector(ones)) < 1e-13
+
+
+# --------------------------------------------------------------------------------------
+# block-index move: one SVD step of TT rounding
+# --------------------------------------------------------------------------------------
+from oracle.rounding import block_move_left, block_move_right  # noqa: E402
+
+
+def _pair_right(Wk_hat, Wk1):
+    """Block tensors of the pair: T[a, i, l, j, c] = sum_b Wk_hat[a,i,l,b] Wk1[b,j,c]."""
+    return np.einsum("ailb,bjc->ailjc", Wk_hat, Wk1)
+
+
+def _pair_after_right(Wk, Wk1_hat):
+    return np.einsum("ais,sjlc->ailjc", Wk, Wk1_hat)
+
+
+def _graded(rng, m, q, sig):
+    """m x q matrix with prescribed singular values (random orthonormal factors)."""
+    U = np.linalg.qr(rng.standard_normal((m, len(sig))))[0]
+    V = np.linalg.qr(rng.standard_normal((q, len(sig))))[0]
+    return (U * sig) @ V.T
+
+
+def test_block_move_right_exact_and_orthonormal():
+    rng = np.random.default_rng(21)
+    Wk_hat = rng.standard_normal((3, 4, 4, 5))
+    Wk1 = rng.standard_normal((5, 4, 2))
+    Wk, W1 = block_move_right(Wk_hat, Wk1)
+    assert Wk.shape == (3, 4, 12) and W1.shape == (12, 4, 4, 2)
+    M = Wk.reshape(12, 12)
+    assert np.allclose(M.T @ M, np.eye(12), atol=1e-13)
+    T0, T1 = _pair_right(Wk_hat, Wk1), _pair_after_right(Wk, W1)
+    assert rel_fro(T1, T0) <= 1e-13
+
+
+def test_block_move_truncation_is_eckart_young():
+    """With Wk1 right-orthonormal the pair's error equals the discarded singular values
+    (Eckart-Young), is <= delta, and one rank fewer would exceed delta."""
+    rng = np.random.default_rng(22)
+    r0, n0, l, r1 = 4, 4, 4, 6
+    sig = np.array([3.0, 2.0, 1.0, 0.5, 1e-3, 5e-4, 1e-5, 1e-6])
+    Wk_hat = _graded(rng, r0 * n0, l * r1, sig).reshape(r0, n0, l, r1)
+    Q = np.linalg.qr(rng.standard_normal((4 * 3, r1)))[0]        # (n1 r2) x r1, orthonormal
+    Wk1 = Q.T.reshape(r1, 4, 3)
+    T0 = _pair_right(Wk_hat, Wk1)
+    for delta, s_exp in ((1e-2, 4), (1e-4, 6), (1e-6, 7)):
+        Wk, W1 = block_move_right(Wk_hat, Wk1, delta)
+        assert Wk.shape[2] == s_exp
+        err = np.linalg.norm(_pair_after_right(Wk, W1) - T0)
+        tail = np.linalg.norm(sig[s_exp:])
+        assert abs(err - tail) <= 1e-12 * np.linalg.norm(sig)
+        assert err <= delta * np.linalg.norm(sig) + 1e-14
+        if s_exp > 1:
+            assert np.linalg.norm(sig[s_exp - 1:]) > delta * np.linalg.norm(sig)
+    Wk, W1 = block_move_right(Wk_hat, Wk1, 0.0, max_rank=3)
+    assert Wk.shape[2] == 3
+
+
+def test_block_move_left_exact_and_orthonormal():
+    rng = np.random.default_rng(23)
+    Wkm1 = rng.standard_normal((2, 4, 5))
+    Wk_hat = rng.standard_normal((5, 4, 3, 6))
+    Wh, Wk = block_move_left(Wkm1, Wk_hat)
+    s = Wk.shape[0]
+    assert s == min(5 * 3, 4 * 6) and Wh.shape == (2, 4, 3, s)
+    R = Wk.reshape(s, 24)
+    assert np.allclose(R @ R.T, np.eye(s), atol=1e-13)
+    T0 = np.einsum("ajb,bilc->ajilc", Wkm1, Wk_hat)
+    T1 = np.einsum("ajls,sic->ajilc", Wh, Wk)
+    assert rel_fro(T1, T0) <= 1e-13
+
+
+def test_block_move_round_trip():
+    """Moving right then back left reproduces the block tensors (delta = 0)."""
+    rng = np.random.default_rng(24)
+    Wk_hat = rng.standard_normal((3, 4, 2, 5))
+    Wk1 = rng.standard_normal((5, 4, 3))
+    Wk, W1 = block_move_right(Wk_hat, Wk1)
+    Wh, Wk1b = block_move_left(Wk, W1)
+    T0 = _pair_right(Wk_hat, Wk1)
+    T2 = np.einsum("ails,sjc->ailjc", Wh, Wk1b)
+    assert rel_fro(T2, T0) <= 1e-12
