@@ -35,6 +35,7 @@ struct GemmParamsV3 {
   int M, N, K;
   IndexMap32 rowmap, colmap;
   int tiles_n, total_units, KT, ksplit, kt_per_split;
+  int a3d, b3d;     // MN-contiguous operand described by a 3-D map (one TMA per stage)
   int l2_a, l2_b;   // TMA L2 policy per operand: 0 default, 1 evict_last (reused, L2-sized),
                     // 2 evict_first (streamed once, larger than L2)
   int store_mode;   // 0 scalar; 1 column pairs (N-contiguous B, output contiguous along n);
@@ -80,6 +81,24 @@ __device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* m
       " [%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
+}
+// 3-D box {16 (m_lo), 16 (k), nslab (m_hi)}: the BM/16 swizzled 2 KB slabs of an
+// M-contiguous operand tile in one instruction (same shared-memory layout as nslab 2-D boxes)
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, uint64_t* bar, uint64_t pol, bool hint) {
+  if (hint)
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4}], [%5], %6;\n" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)),
+        "l"(pol)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
 }
 __device__ __forceinline__ uint64_t l2_policy(int kind) {
   uint64_t pol = 0;
@@ -176,6 +195,8 @@ dmma_gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       if (A_KC) {
         if (p.l2_a) tma_load_2d_hint(as, &tmA, k0, m0, &full_bar[s], pol_a);
         else tma_load_2d(as, &tmA, k0, m0, &full_bar[s]);
+      } else if (p.a3d) {
+        tma_load_3d(as, &tmA, 0, k0, m0 / 16, &full_bar[s], pol_a, p.l2_a != 0);
       } else {
 #pragma unroll
         for (int b = 0; b < BM / 16; ++b) {
@@ -186,6 +207,8 @@ dmma_gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       if (B_KC) {
         if (p.l2_b) tma_load_2d_hint(bs, &tmB, k0, n0, &full_bar[s], pol_b);
         else tma_load_2d(bs, &tmB, k0, n0, &full_bar[s]);
+      } else if (p.b3d) {
+        tma_load_3d(bs, &tmB, 0, k0, n0 / 16, &full_bar[s], pol_b, p.l2_b != 0);
       } else {
 #pragma unroll
         for (int b = 0; b < BN / 16; ++b) {

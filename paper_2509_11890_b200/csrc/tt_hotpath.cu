@@ -330,6 +330,24 @@ bool make_map(CUtensorMap* m, const double* base, long long inner, long long out
   return r == CUDA_SUCCESS;
 }
 
+// 3-D view of an MN-contiguous operand: dims {16 (m_lo), K, M/16 (m_hi)}, strides
+// {ld, 16} doubles, box {16, 16, nslab}: one TMA loads a whole BM x 16 tile as nslab
+// swizzled 2 KB slabs.  Needs M % 16 == 0 (no element past M is ever addressed).
+bool make_map3(CUtensorMap* m, const double* base, long long M, long long K, long long ld,
+               int nslab) {
+  if (M % 16 != 0 || (ld * 8) % 16 != 0) return false;
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {16u, (cuuint64_t)K, (cuuint64_t)(M / 16)};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * 8), 128u};
+  cuuint32_t box[3] = {16u, 16u, (cuuint32_t)nslab};
+  cuuint32_t estr[3] = {1u, 1u, 1u};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 bool even_strides(const IndexMap& m) {
   return ((m.s0 | m.s1 | m.s2) & 1) == 0;
 }
@@ -358,9 +376,14 @@ cudaError_t launch_v3_cfg(const GemmParams& p0, cudaStream_t s, bool& ok) {
   ok = false;
   CUtensorMap ta, tb;
   // A: K-contiguous -> inner K, outer M (box rows BM); M-contiguous -> inner M, outer K (box 16)
-  if (!(AK ? make_map(&ta, p0.A, p0.K, p0.M, p0.lda, BM) : make_map(&ta, p0.A, p0.M, p0.K, p0.lda, 16)))
+  const bool use3d = !(g_dbg_flags & 128);
+  const bool a3d = !AK && use3d && make_map3(&ta, p0.A, p0.M, p0.K, p0.lda, BM / 16);
+  const bool b3d = !BK_ && use3d && make_map3(&tb, p0.B, p0.N, p0.K, p0.ldb, BN / 16);
+  if (!a3d &&
+      !(AK ? make_map(&ta, p0.A, p0.K, p0.M, p0.lda, BM) : make_map(&ta, p0.A, p0.M, p0.K, p0.lda, 16)))
     return cudaSuccess;
-  if (!(BK_ ? make_map(&tb, p0.B, p0.K, p0.N, p0.ldb, BN) : make_map(&tb, p0.B, p0.N, p0.K, p0.ldb, 16)))
+  if (!b3d &&
+      !(BK_ ? make_map(&tb, p0.B, p0.K, p0.N, p0.ldb, BN) : make_map(&tb, p0.B, p0.N, p0.K, p0.ldb, 16)))
     return cudaSuccess;
   ok = true;
   auto kern = tt::dmma_gemm_v3_kernel<AK, BK_, BM, BN, WM, WN, ST, MINB>;
@@ -382,6 +405,8 @@ cudaError_t launch_v3_cfg(const GemmParams& p0, cudaStream_t s, bool& ok) {
   p.rowmap = tt::to_map32(p0.rowmap);
   p.colmap = tt::to_map32(p0.colmap);
   p.store_mode = store_mode(AK, BK_, p0);
+  p.a3d = a3d ? 1 : 0;
+  p.b3d = b3d ? 1 : 0;
   // L2 policies: an operand that fits comfortably in L2 and is re-read by many tiles is kept
   // (evict_last); an operand larger than L2 is streamed (evict_first) when that protects a
   // kept partner of some size (a streamed operand with a tiny partner gains nothing and was
