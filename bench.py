@@ -189,9 +189,28 @@ def oracle_sample_inputs(seed=7):
                 phiR=rng.standard_normal((b, be, b)), x=rng.standard_normal((a, N, b)))
 
 
+class pinned_one_core:
+    """the oracle is timed single-threaded, pinned to one core."""
+    def __enter__(self):
+        self.prev = None
+        try:
+            self.prev = os.sched_getaffinity(0)
+            self.core = max(self.prev)
+            os.sched_setaffinity(0, {self.core})
+        except (AttributeError, OSError):
+            self.core = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.prev is not None:
+            os.sched_setaffinity(0, self.prev)
+        return False
+
+
 def time_oracle_sample(with_interface=True):
     import oracle
     s = oracle_sample_inputs()
+    oracle.build()
     t0 = time.perf_counter()
     oracle.local_matvec(s["phiL"], s["A"], s["phiR"], s["x"])
     flops = f_local(s["a"], s["N"], s["b"], s["al"], s["be"])
@@ -219,13 +238,14 @@ def run_reference(args, rank):
     oracle.build()
     s = oracle_sample_inputs()
     flops = f_local(s["a"], s["N"], s["b"], s["al"], s["be"])
-    for _ in range(args.warmup):
-        oracle.local_matvec(s["phiL"], s["A"], s["phiR"], s["x"])
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        oracle.local_matvec(s["phiL"], s["A"], s["phiR"], s["x"])
-        times.append(time.perf_counter() - t0)
+    with pinned_one_core() as pin:
+        for _ in range(args.warmup):
+            oracle.local_matvec(s["phiL"], s["A"], s["phiR"], s["x"])
+        times = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            oracle.local_matvec(s["phiL"], s["A"], s["phiR"], s["x"])
+            times.append(time.perf_counter() - t0)
     total = sum(times)
     value = flops * args.steps / total / 1e9
     sample = ("one Krylov column of the config-5 interior-core (k=6: a=b=256, alpha=beta=36, N=4) "
@@ -238,7 +258,8 @@ def run_reference(args, rank):
         "config": {"workload": "config 5 (d=12, r=256, R=36, K=32) W5 - bounded oracle sample",
                    "sample": sample},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": sample, "cpu": cpu_model(), "compiler": "gcc -O2 -std=c99"},
+                         "sample": sample, "cpu": cpu_model(), "compiler": "gcc -O2 -std=c99",
+                         "pinned_core": pin.core},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -403,7 +424,11 @@ def main():
                 "frac": dom["tflops"] / p64_sustained, "traffic": traffic,
                 "peak_source": "FP64 DMMA probe kernel, measured in this run (sustained ~1 s); "
                                "MEASURED_PEAKS.json has no FP64 entry",
-                "peak_burst": p64_burst}
+                "peak_burst": p64_burst,
+                # second line against the datasheet (HGX B200: 296 TFLOP/s
+                # FP64 Tensor Core per 8 GPUs = 37 per GPU)
+                "datasheet_peak": 37.0,
+                "frac_vs_datasheet": dom["tflops"] / 37.0}
     apply_detail = None
     if "apply" in stages:
         ap_ms = stages["apply"]["ms"] / args.steps
@@ -631,12 +656,13 @@ def main():
     # ---- CPU oracle baseline (rank 0, N=1) ----------------------------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        fl, dt = time_oracle_sample(True)
+        with pinned_one_core() as pin:
+            fl, dt = time_oracle_sample(True)
         cpu = {"value": fl / dt / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
                "sample": "tt_oracle_local_matvec (1 Krylov column) + tt_oracle_interface_left at "
                          "config-5 interior-core shapes (a=b=256, alpha=beta=36, N=4), "
                          f"{fl / 1e9:.1f} GFLOP in {dt:.1f} s",
-               "cpu": cpu_model(), "compiler": "gcc -O2 -std=c99"}
+               "cpu": cpu_model(), "compiler": "gcc -O2 -std=c99", "pinned_core": pin.core}
 
     if rank == 0:
         line = {
