@@ -317,6 +317,48 @@ tt_status tt_block_move_left(int64_t r0, int64_t n0, int64_t r1, int64_t n1, int
                              int64_t* s_out, void* workspace, size_t workspace_bytes,
                              void* stream);
 
+/* -------------------------------------------------------------------------------------
+ * Petrov-Galerkin local operations: the bra train Z differs from the ket train X (ranks
+ * rl_bra / rr_bra vs rl / rr).  Interfaces are [bra, op, ket] as everywhere:
+ *   phiL (rl_bra, Rl, rl), phiR (rr_bra, Rr, rr).
+ * tt_local_matvec_pg: Y = (Z_{!=k}^T A X_{!=k}) X_k column by column, X (rl, n, nvec, rr),
+ *   Y (rl_bra, n, nvec, rr_bra) -- with an identity operator core (Rl = Rr = 1) and the
+ *   right-hand side train as ket this is the projected right-hand side X_{!=k}^T vec(B) of
+ *   the local system; with Z the approximate residual it is the AMEn residual
+ *   core.
+ * tt_interface_left_pg:  phiL_next (rr_bra, Rr, rr) = sum z[a',i,b'] phiL_prev[a',al,a]
+ *   A[al,i,j,be] x[a,j,b];  x_bra = z (rl_bra, n, rr_bra), x_ket = x (rl, n, rr).
+ * tt_interface_right_pg: phiR_prev (rl_bra, Rl, rl) = sum z[a',i,b'] A[al,i,j,be]
+ *   phiR_next[b',be,b] x[a,j,b].
+ * Same conventions as the square calls; one workspace size covers all three.
+ * ------------------------------------------------------------------------------------- */
+size_t tt_pg_workspace_size(int64_t rl_bra, int64_t rl, int64_t n, int64_t rr_bra, int64_t rr,
+                            int64_t Rl, int64_t Rr, int64_t nvec);
+tt_status tt_local_matvec_pg(int64_t rl_bra, int64_t rl, int64_t n, int64_t rr_bra, int64_t rr,
+                             int64_t Rl, int64_t Rr, int64_t nvec, const double* phiL,
+                             const double* A, const double* phiR, const double* X, double* Y,
+                             void* workspace, size_t workspace_bytes, void* stream);
+tt_status tt_interface_left_pg(int64_t rl_bra, int64_t rl, int64_t n, int64_t rr_bra, int64_t rr,
+                               int64_t Rl, int64_t Rr, const double* phiL_prev, const double* A,
+                               const double* x_bra, const double* x_ket, double* phiL_next,
+                               void* workspace, size_t workspace_bytes, void* stream);
+tt_status tt_interface_right_pg(int64_t rl_bra, int64_t rl, int64_t n, int64_t rr_bra, int64_t rr,
+                                int64_t Rl, int64_t Rr, const double* phiR_next, const double* A,
+                                const double* x_bra, const double* x_ket, double* phiR_prev,
+                                void* workspace, size_t workspace_bytes, void* stream);
+/* AMEn enrichment (Dolgov & Savostyanov 2014): x_k (rl, n, rx) and the
+ * residual core z_k (rl, n, rz) are concatenated along the right bond, x_{k+1} (rx, n1, r2)
+ * gets rz zero rows (the represented tensor is unchanged), and the enlarged core is
+ * re-orthonormalised by one truncated SVD step (tt_block_move_right with l = 1; delta,
+ * max_rank as there): x_k_out (rl, n, s) left-orthonormal, x_k1_out (s, n1, r2), s in *s_out
+ * (host), s <= min(rl n, rx + rz).  Synchronous. */
+size_t tt_enrich_right_workspace_size(int64_t rl, int64_t n, int64_t rx, int64_t rz, int64_t n1,
+                                      int64_t r2);
+tt_status tt_enrich_right(int64_t rl, int64_t n, int64_t rx, int64_t rz, int64_t n1, int64_t r2,
+                          double delta, int64_t max_rank, const double* x_k, const double* z_k,
+                          const double* x_k1, double* x_k_out, double* x_k1_out, int64_t* s_out,
+                          void* workspace, size_t workspace_bytes, void* stream);
+
 /* Number of kernel launches the last call on this thread enqueued. */
 int64_t tt_last_launch_count(void);
 /* Test hook: on != 0 routes every GEMM stage of the calling thread through the generic

@@ -30,7 +30,9 @@ __all__ = [
     "tt_round", "tt_round_workspace_size", "tt_debug_sym_eigen",
     "tt_local_lobpcg", "tt_local_lobpcg_workspace_size", "tt_merge_operator_cores",
     "tt_orthonormalise", "tt_orthonormalise_workspace_size", "tt_block_move_right",
-    "tt_block_move_left", "tt_block_move_workspace_size",
+    "tt_block_move_left", "tt_block_move_workspace_size", "tt_pg_workspace_size",
+    "tt_local_matvec_pg", "tt_interface_left_pg", "tt_interface_right_pg", "tt_enrich_right",
+    "tt_enrich_right_workspace_size",
 ]
 
 STAGE_NAMES = {0: "perm", 1: "set", 2: "mv_s1", 3: "mv_s2", 4: "mv_s3", 5: "il_s1", 6: "il_s2",
@@ -109,6 +111,18 @@ lib.tt_block_move_right.argtypes = [_i64] * 6 + [ctypes.c_double, _i64] + [_p] *
 lib.tt_block_move_right.restype = ctypes.c_int
 lib.tt_block_move_left.argtypes = [_i64] * 6 + [ctypes.c_double, _i64] + [_p] * 6 + [_sz, _p]
 lib.tt_block_move_left.restype = ctypes.c_int
+lib.tt_pg_workspace_size.restype = _sz
+lib.tt_pg_workspace_size.argtypes = [_i64] * 8
+lib.tt_local_matvec_pg.argtypes = [_i64] * 8 + [_p] * 6 + [_sz, _p]
+lib.tt_local_matvec_pg.restype = ctypes.c_int
+lib.tt_interface_left_pg.argtypes = [_i64] * 7 + [_p] * 6 + [_sz, _p]
+lib.tt_interface_left_pg.restype = ctypes.c_int
+lib.tt_interface_right_pg.argtypes = [_i64] * 7 + [_p] * 6 + [_sz, _p]
+lib.tt_interface_right_pg.restype = ctypes.c_int
+lib.tt_enrich_right_workspace_size.restype = _sz
+lib.tt_enrich_right_workspace_size.argtypes = [_i64] * 6
+lib.tt_enrich_right.argtypes = [_i64] * 6 + [ctypes.c_double, _i64] + [_p] * 7 + [_sz, _p]
+lib.tt_enrich_right.restype = ctypes.c_int
 lib.tt_merge_operator_cores.restype = ctypes.c_int
 lib.tt_debug_force_v1.argtypes = [ctypes.c_int]
 lib.tt_debug_force_v1.restype = None
@@ -559,6 +573,79 @@ def tt_block_move_left(Wkm1, Wk_hat, delta=0.0, max_rank=0, workspace=None, stre
                                   ws.numel(), _stream(stream)))
     sk = s_out.value
     return (Wh[: r0 * n0 * l * sk].reshape(r0, n0, l, sk), Wk[: sk * n1 * r2].reshape(sk, n1, r2))
+
+
+def tt_pg_workspace_size(rl_bra, rl, n, rr_bra, rr, Rl, Rr, nvec=1) -> int:
+    return int(lib.tt_pg_workspace_size(rl_bra, rl, n, rr_bra, rr, Rl, Rr, nvec))
+
+
+def tt_local_matvec_pg(phiL, A, phiR, X, Y=None, workspace=None, stream=None):
+    """Petrov-Galerkin local matvec (bra train != ket train): phiL (rl_bra, Rl, rl),
+    phiR (rr_bra, Rr, rr), X (rl, n, nvec, rr) or (rl, n, rr) -> Y (rl_bra, n, [nvec,] rr_bra)."""
+    single = X.dim() == 3
+    Xv = X.unsqueeze(2) if single else X
+    rl, n, nvec, rr = Xv.shape
+    rlb, rrb = phiL.shape[0], phiR.shape[0]
+    Rl, Rr = A.shape[0], A.shape[3]
+    if Y is None:
+        shape = (rlb, n, rrb) if single else (rlb, n, nvec, rrb)
+        Y = torch.empty(shape, dtype=torch.float64, device=X.device)
+    ws = _ws(tt_pg_workspace_size(rlb, rl, n, rrb, rr, Rl, Rr, nvec), workspace, X.device)
+    _check(lib.tt_local_matvec_pg(rlb, rl, n, rrb, rr, Rl, Rr, nvec, _dev(phiL, "phiL"), _dev(A, "A"),
+                                  _dev(phiR, "phiR"), _dev(X, "X"), _dev(Y, "Y"), ws.data_ptr(),
+                                  ws.numel(), _stream(stream)))
+    return Y
+
+
+def tt_interface_left_pg(phiL_prev, A, x_bra, x_ket, out=None, workspace=None, stream=None):
+    rlb, n, rrb = x_bra.shape
+    rl, _, rr = x_ket.shape
+    Rl, Rr = A.shape[0], A.shape[3]
+    if out is None:
+        out = torch.empty((rrb, Rr, rr), dtype=torch.float64, device=x_ket.device)
+    ws = _ws(tt_pg_workspace_size(rlb, rl, n, rrb, rr, Rl, Rr, 1), workspace, x_ket.device)
+    _check(lib.tt_interface_left_pg(rlb, rl, n, rrb, rr, Rl, Rr, _dev(phiL_prev, "phiL_prev"),
+                                    _dev(A, "A"), _dev(x_bra, "x_bra"), _dev(x_ket, "x_ket"),
+                                    _dev(out, "phiL_next"), ws.data_ptr(), ws.numel(),
+                                    _stream(stream)))
+    return out
+
+
+def tt_interface_right_pg(phiR_next, A, x_bra, x_ket, out=None, workspace=None, stream=None):
+    rlb, n, rrb = x_bra.shape
+    rl, _, rr = x_ket.shape
+    Rl, Rr = A.shape[0], A.shape[3]
+    if out is None:
+        out = torch.empty((rlb, Rl, rl), dtype=torch.float64, device=x_ket.device)
+    ws = _ws(tt_pg_workspace_size(rlb, rl, n, rrb, rr, Rl, Rr, 1), workspace, x_ket.device)
+    _check(lib.tt_interface_right_pg(rlb, rl, n, rrb, rr, Rl, Rr, _dev(phiR_next, "phiR_next"),
+                                     _dev(A, "A"), _dev(x_bra, "x_bra"), _dev(x_ket, "x_ket"),
+                                     _dev(out, "phiR_prev"), ws.data_ptr(), ws.numel(),
+                                     _stream(stream)))
+    return out
+
+
+def tt_enrich_right_workspace_size(rl, n, rx, rz, n1, r2) -> int:
+    return int(lib.tt_enrich_right_workspace_size(rl, n, rx, rz, n1, r2))
+
+
+def tt_enrich_right(x_k, z_k, x_k1, delta=0.0, max_rank=0, workspace=None, stream=None):
+    """AMEn enrichment: [x_k | z_k] re-orthonormalised, x_{k+1} padded and
+    rotated.  Returns (x_k' (rl, n, s) left-orthonormal, x_{k+1}' (s, n1, r2))."""
+    rl, n, rx = x_k.shape
+    rz = z_k.shape[2]
+    _, n1, r2 = x_k1.shape
+    smax = min(rl * n, rx + rz)
+    xo = torch.empty(rl * n * smax, dtype=torch.float64, device=x_k.device)
+    x1o = torch.empty(smax * n1 * r2, dtype=torch.float64, device=x_k.device)
+    s_out = ctypes.c_int64()
+    ws = _ws(tt_enrich_right_workspace_size(rl, n, rx, rz, n1, r2), workspace, x_k.device)
+    _check(lib.tt_enrich_right(rl, n, rx, rz, n1, r2, float(delta), int(max_rank), _dev(x_k, "x_k"),
+                               _dev(z_k, "z_k"), _dev(x_k1, "x_k1"), _dev(xo, "x_k_out"),
+                               _dev(x1o, "x_k1_out"), ctypes.byref(s_out), ws.data_ptr(),
+                               ws.numel(), _stream(stream)))
+    sk = s_out.value
+    return xo[: rl * n * sk].reshape(rl, n, sk), x1o[: sk * n1 * r2].reshape(sk, n1, r2)
 
 
 def tt_round_workspace_size(n, r) -> int:

@@ -514,6 +514,9 @@ cudaError_t launch_v3_l(const GemmParams& p, cudaStream_t s, bool& ok) {
   if (p.N <= 112) return launch_v3_cfg<AK, BK_, 128, 112, 8, 2, 1>(p, s, ok);
   if (p.N <= 144) return launch_v3_cfg<AK, BK_, 128, 144, 8, 2, 1>(p, s, ok);
   if (BK_) return launch_v3_cfg<AK, BK_, 128, 128, 4, 4, 1>(p, s, ok);
+  if (g_variant == 5) return launch_v3_cfg<AK, BK_, 128, 128, 4, 4, 1>(p, s, ok);   // probes
+  if (g_variant == 6) return launch_v3_cfg<AK, BK_, 128, 128, 8, 2, 1>(p, s, ok);
+  if (g_variant == 7) return launch_v3_cfg<AK, BK_, 64, 128, 2, 4, 2>(p, s, ok);
   return launch_v3_cfg<AK, BK_, 128, 64, 4, 2, 2>(p, s, ok);
 }
 
@@ -988,6 +991,114 @@ cudaError_t enqueue_right(const Dims& d, const double* phiR, const double* A, co
   SplitScratch scratch(P, pe);
   return launch_gemm(true, false,
                      gp(x, N * b, T2, al * a, out, a, al * a, N * b, tt::map_plain(al * a),
+                        tt::map_plain(1)),
+                     s);
+}
+
+// ---- Petrov-Galerkin (bra train != ket train) variants --------------------------------------
+// The same three-GEMM stage plans with the bra ranks (ap = a', bp = b') decoupled from the ket
+// ranks (a, b): the local operator Z_{!=k}^T A X_{!=k} of two different trains, the projected
+// right-hand side X_{!=k}^T b (identity operator) and the AMEn residual frame
+// (PAPER.md:303).  Interfaces are [bra, op, ket]: phiL (ap, al, a), phiR (bp, be, b).
+struct DimsPG {
+  long long ap, a, n, bp, b, al, be;
+};
+bool dims_pg_valid(const DimsPG& d) {
+  return d.ap > 0 && d.a > 0 && d.n > 0 && d.bp > 0 && d.b > 0 && d.al > 0 && d.be > 0;
+}
+// element counts for the matvec (K columns) and both interface updates
+bool pg_ws_elems(const DimsPG& d, long long K, long long& t1, long long& t2, long long& ah,
+                 long long& pe) {
+  bool ok = true;
+  t1 = std::max({prod({d.ap, d.al, d.n, K, d.b}, ok), prod({d.a, d.n, d.bp, d.be}, ok)});
+  t2 = std::max({prod({d.ap, d.n, K, d.be, d.b}, ok), prod({d.n, d.bp, d.al, d.a}, ok)});
+  ah = prod({d.al, d.n, d.n, d.be}, ok);
+  const long long out = std::max({prod({d.ap, d.n, K, d.bp}, ok), prod({d.bp, d.be, d.b}, ok),
+                                  prod({d.ap, d.al, d.a}, ok)});
+  pe = std::max(4 * out, std::min(64 * out, 16LL << 20));
+  return ok;
+}
+
+// Y (ap, n, K, bp) = phiL (ap, al, a) x A x phiR (bp, be, b) applied to X (a, n, K, b)
+cudaError_t enqueue_matvec_pg(const DimsPG& d, long long K, const double* phiL, const double* A,
+                              const double* phiR, const double* X, double* Y, double* T1,
+                              double* T2, double* Ah, double* P, long long pe, cudaStream_t s) {
+  const long long ap = d.ap, a = d.a, bp = d.bp, b = d.b, al = d.al, be = d.be, N = d.n;
+  cudaError_t e;
+  if ((e = launch_perm(true, A, Ah, al, N, be, s)) != cudaSuccess) return e;
+  // S1: T1(al, j, a', m, b) = phiL[(a' al), a] . X[a, (j m b)]
+  g_stage = TT_ST_MV_S1;
+  e = launch_gemm(true, false,
+                  gp(phiL, a, X, N * K * b, T1, ap * al, N * K * b, a,
+                     tt::map2(al, N * ap * K * b, K * b), tt::map2(K * b, 1, ap * K * b)),
+                  s);
+  if (e != cudaSuccess) return e;
+  // S2: T2(a', m, i, be, b) = T1^T[(a' m b), (al j)] . Ahat[(al j), (i be)]
+  g_stage = TT_ST_MV_S2;
+  e = launch_gemm(false, false,
+                  gp(T1, ap * K * b, Ah, N * be, T2, ap * K * b, N * be, al * N,
+                     tt::map2(b, 1, N * be * b), tt::map_plain(b)),
+                  s);
+  if (e != cudaSuccess) return e;
+  // S3: Y(a', i, m, b') = T2[(a' m i), (be b)] . phiR[b', (be b)]^T
+  g_stage = TT_ST_MV_S3;
+  SplitScratch scratch(P, pe);
+  return launch_gemm(true, true,
+                     gp(T2, be * b, phiR, be * b, Y, ap * K * N, bp, be * b,
+                        tt::map3(N, K, K * bp, bp, N * K * bp), tt::map_plain(1)),
+                     s);
+}
+
+// phiL_next (bp, be, b) = sum x_bra[a', i, b'] phiL[a', al, a] A[al, i, j, be] x_ket[a, j, b]
+cudaError_t enqueue_left_pg(const DimsPG& d, const double* phiL, const double* A,
+                            const double* xb, const double* xk, double* out, double* T1,
+                            double* T2, double* Ah, double* P, long long pe, cudaStream_t s) {
+  const long long ap = d.ap, a = d.a, bp = d.bp, b = d.b, al = d.al, be = d.be, N = d.n;
+  cudaError_t e;
+  if ((e = launch_perm(true, A, Ah, al, N, be, s)) != cudaSuccess) return e;
+  g_stage = TT_ST_IL_S1;   // T1(al, j, a', b) = phiL[(a' al), a] . x_ket[a, (j b)]
+  e = launch_gemm(true, false,
+                  gp(phiL, a, xk, N * b, T1, ap * al, N * b, a, tt::map2(al, N * ap * b, b),
+                     tt::map2(b, 1, ap * b)),
+                  s);
+  if (e != cudaSuccess) return e;
+  g_stage = TT_ST_IL_S2;   // T2(a', i, be, b) = T1^T[(a' b), (al j)] . Ahat[(al j), (i be)]
+  e = launch_gemm(false, false,
+                  gp(T1, ap * b, Ah, N * be, T2, ap * b, N * be, al * N, tt::map2(b, 1, N * be * b),
+                     tt::map_plain(b)),
+                  s);
+  if (e != cudaSuccess) return e;
+  g_stage = TT_ST_IL_S3;   // out[b', (be b)] = x_bra^T[b', (a' i)] . T2[(a' i), (be b)]
+  SplitScratch scratch(P, pe);
+  return launch_gemm(false, false,
+                     gp(xb, bp, T2, be * b, out, bp, be * b, ap * N, tt::map_plain(be * b),
+                        tt::map_plain(1)),
+                     s);
+}
+
+// phiR_prev (ap, al, a) = sum x_bra[a', i, b'] A[al, i, j, be] phiR[b', be, b] x_ket[a, j, b]
+cudaError_t enqueue_right_pg(const DimsPG& d, const double* phiR, const double* A,
+                             const double* xb, const double* xk, double* out, double* T1,
+                             double* T2, double* At, double* P, long long pe, cudaStream_t s) {
+  const long long ap = d.ap, a = d.a, bp = d.bp, b = d.b, al = d.al, be = d.be, N = d.n;
+  cudaError_t e;
+  if ((e = launch_perm(false, A, At, al, N, be, s)) != cudaSuccess) return e;
+  g_stage = TT_ST_IR_S1;   // T1(j, be, a, b') = x_ket[(a j), b] . phiR[(b' be), b]^T
+  e = launch_gemm(true, true,
+                  gp(xk, b, phiR, b, T1, a * N, bp * be, b, tt::map2(N, be * a * bp, bp),
+                     tt::map2(be, a * bp, 1)),
+                  s);
+  if (e != cudaSuccess) return e;
+  g_stage = TT_ST_IR_S2;   // T2(i, b', al, a) = T1^T[(a b'), (j be)] . Atil[(j be), (al i)]
+  e = launch_gemm(false, false,
+                  gp(T1, a * bp, At, al * N, T2, a * bp, al * N, N * be, tt::map2(bp, al * a, 1),
+                     tt::map2(N, bp * al * a, a)),
+                  s);
+  if (e != cudaSuccess) return e;
+  g_stage = TT_ST_IR_S3;   // out[a', (al a)] = x_bra[a', (i b')] . T2[(i b'), (al a)]
+  SplitScratch scratch(P, pe);
+  return launch_gemm(true, false,
+                     gp(xb, N * bp, T2, al * a, out, ap, al * a, N * bp, tt::map_plain(al * a),
                         tt::map_plain(1)),
                      s);
 }
@@ -2076,6 +2187,79 @@ tt_status tt_block_move_left(int64_t r0, int64_t n0, int64_t r1, int64_t n1, int
   return TT_OK;
 }
 
+// ---- AMEn enrichment ("enrichment of the TT cores by TT cores of the
+// approximate residual, as in the AMEn algorithm") -----------------------------------------
+// x_k (rl, n, rx) and the residual core z_k (rl, n, rz) are concatenated along the right bond,
+// x_{k+1} (rx, n1, r2) is padded with rz zero rows (the represented tensor is unchanged), and
+// the enlarged core is re-orthonormalised by one truncated SVD step (tt_block_move_right with
+// l = 1): x_k' (rl, n, s) left-orthonormal, x_{k+1}' (s, n1, r2).
+__global__ void enrich_concat_kernel(const double* __restrict__ x, const double* __restrict__ z,
+                                     const double* __restrict__ x1, double* __restrict__ cat,
+                                     double* __restrict__ cat1, long long rows, long long rx,
+                                     long long rz, long long q1) {
+  const long long r = rx + rz;
+  const long long n0 = rows * r, n1 = r * q1;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n0 + n1;
+       e += (long long)gridDim.x * blockDim.x) {
+    if (e < n0) {
+      const long long i = e / r, c = e - i * r;
+      cat[e] = c < rx ? x[i * rx + c] : z[i * rz + (c - rx)];
+    } else {
+      const long long f = e - n0, row = f / q1;
+      cat1[f] = row < rx ? x1[f] : 0.0;
+    }
+  }
+}
+
+size_t tt_enrich_right_workspace_size(int64_t rl, int64_t n, int64_t rx, int64_t rz, int64_t n1,
+                                      int64_t r2) {
+  if (rl <= 0 || n <= 0 || rx <= 0 || rz <= 0 || n1 <= 0 || r2 <= 0) return 0;
+  bool ok = true;
+  const long long cat = prod({rl, n, rx + rz}, ok), cat1 = prod({rx + rz, n1, r2}, ok);
+  if (!ok) return 0;
+  const size_t mv = tt_block_move_workspace_size(rl, n, 1, rx + rz, n1, r2);
+  if (mv == 0) return 0;
+  return mv + ws_bytes({cat, cat1});
+}
+
+tt_status tt_enrich_right(int64_t rl, int64_t n, int64_t rx, int64_t rz, int64_t n1, int64_t r2,
+                          double delta, int64_t max_rank, const double* x_k, const double* z_k,
+                          const double* x_k1, double* x_k_out, double* x_k1_out, int64_t* s_out,
+                          void* workspace, size_t workspace_bytes, void* stream) {
+  CallScope scope;
+  if (rl <= 0 || n <= 0 || rx <= 0 || rz <= 0 || n1 <= 0 || r2 <= 0)
+    return fail(TT_ERR_INVALID_ARGUMENT, "extents must be positive");
+  if (!x_k || !z_k || !x_k1 || !x_k_out || !x_k1_out || !s_out)
+    return fail(TT_ERR_NULL_POINTER, "NULL pointer");
+  for (const void* o : {(const void*)x_k_out, (const void*)x_k1_out})
+    if (same(o, x_k) || same(o, z_k) || same(o, x_k1))
+      return fail(TT_ERR_ALIASING, "an output aliases an input");
+  const size_t need = tt_enrich_right_workspace_size(rl, n, rx, rz, n1, r2);
+  if (need == 0) return fail(TT_ERR_OVERFLOW, "workspace overflow");
+  if (!workspace || workspace_bytes < need)
+    return fail(TT_ERR_WORKSPACE, "workspace NULL or smaller than " + std::to_string(need) + " bytes");
+  const size_t mv = tt_block_move_workspace_size(rl, n, 1, rx + rz, n1, r2);
+  char* base = static_cast<char*>(workspace);
+  Carver c{base + mv, workspace_bytes - mv};
+  const long long r = rx + rz;
+  double* cat = c.take(rl * n * r);
+  double* cat1 = c.take(r * n1 * r2);
+  if (!c.ok) return fail(TT_ERR_WORKSPACE, "workspace too small after alignment");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const long long tot = rl * n * r + r * n1 * r2;
+  enrich_concat_kernel<<<(unsigned)std::min<long long>(4096, (tot + 255) / 256), 256, 0, s>>>(
+      x_k, z_k, x_k1, cat, cat1, rl * n, rx, rz, n1 * r2);
+  ++g_launches;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "tt_enrich_right");
+  const int64_t launches = g_launches;
+  tt_status st = tt_block_move_right(rl, n, 1, r, n1, r2, delta, max_rank, cat, cat1, x_k_out,
+                                     x_k1_out, s_out, base, mv, stream);
+  g_launches += launches;
+  g_launches_last = g_launches;
+  return st;
+}
+
 // ---- projected KKT block system action -----------------------------
 static bool block_ws(int64_t rl, int64_t n, int64_t rr, int64_t nops, const int64_t* Rl,
                      const int64_t* Rr, long long& t1, long long& t2, long long& ah, long long& pe,
@@ -2269,6 +2453,98 @@ tt_status tt_local_gmres(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t 
   if (e != cudaSuccess) return cuda_fail(e, "tt_local_gmres");
   return TT_OK;
 }
+
+// ---- Petrov-Galerkin local operations (bra != ket) and AMEn enrichment ---------------------
+static tt_status check_pg(const DimsPG& d) {
+  if (!dims_pg_valid(d)) return fail(TT_ERR_INVALID_ARGUMENT, "extents must be positive");
+  long long t1, t2, ah, pe;
+  if (!pg_ws_elems(d, 1, t1, t2, ah, pe)) return fail(TT_ERR_OVERFLOW, "extent product overflows");
+  return TT_OK;
+}
+
+size_t tt_pg_workspace_size(int64_t rl_bra, int64_t rl, int64_t n, int64_t rr_bra, int64_t rr,
+                            int64_t Rl, int64_t Rr, int64_t nvec) {
+  DimsPG d{rl_bra, rl, n, rr_bra, rr, Rl, Rr};
+  long long t1, t2, ah, pe;
+  if (!dims_pg_valid(d) || nvec <= 0 || !pg_ws_elems(d, nvec, t1, t2, ah, pe)) return 0;
+  return ws_bytes({t1, t2, ah, pe});
+}
+
+#define TT_PG_CARVE()                                                                      \
+  long long t1, t2, ah, pe;                                                                \
+  if (!pg_ws_elems(d, K, t1, t2, ah, pe)) return fail(TT_ERR_OVERFLOW, "workspace overflow"); \
+  const size_t need = ws_bytes({t1, t2, ah, pe});                                          \
+  if (!workspace || workspace_bytes < need)                                                \
+    return fail(TT_ERR_WORKSPACE, "workspace NULL or smaller than " + std::to_string(need) + " bytes"); \
+  Carver c{static_cast<char*>(workspace), workspace_bytes};                                \
+  double* T1 = c.take(t1);                                                                 \
+  double* T2 = c.take(t2);                                                                 \
+  double* Ah = c.take(ah);                                                                 \
+  double* Pp = c.take(pe);                                                                 \
+  if (!c.ok) return fail(TT_ERR_WORKSPACE, "workspace too small after alignment");
+
+tt_status tt_local_matvec_pg(int64_t rl_bra, int64_t rl, int64_t n, int64_t rr_bra, int64_t rr,
+                             int64_t Rl, int64_t Rr, int64_t nvec, const double* phiL,
+                             const double* A, const double* phiR, const double* X, double* Y,
+                             void* workspace, size_t workspace_bytes, void* stream) {
+  CallScope scope;
+  DimsPG d{rl_bra, rl, n, rr_bra, rr, Rl, Rr};
+  tt_status st = check_pg(d);
+  if (st != TT_OK) return st;
+  if (nvec <= 0) return fail(TT_ERR_INVALID_ARGUMENT, "nvec must be positive");
+  if (!phiL || !A || !phiR || !X || !Y) return fail(TT_ERR_NULL_POINTER, "NULL tensor pointer");
+  if (same(Y, phiL) || same(Y, A) || same(Y, phiR) || same(Y, X))
+    return fail(TT_ERR_ALIASING, "output Y aliases an input");
+  const long long K = nvec;
+  TT_PG_CARVE();
+  cudaError_t e = enqueue_matvec_pg(d, K, phiL, A, phiR, X, Y, T1, T2, Ah, Pp, pe,
+                                    static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "tt_local_matvec_pg");
+  return TT_OK;
+}
+
+tt_status tt_interface_left_pg(int64_t rl_bra, int64_t rl, int64_t n, int64_t rr_bra, int64_t rr,
+                               int64_t Rl, int64_t Rr, const double* phiL_prev, const double* A,
+                               const double* x_bra, const double* x_ket, double* phiL_next,
+                               void* workspace, size_t workspace_bytes, void* stream) {
+  CallScope scope;
+  DimsPG d{rl_bra, rl, n, rr_bra, rr, Rl, Rr};
+  tt_status st = check_pg(d);
+  if (st != TT_OK) return st;
+  if (!phiL_prev || !A || !x_bra || !x_ket || !phiL_next)
+    return fail(TT_ERR_NULL_POINTER, "NULL tensor pointer");
+  if (same(phiL_next, phiL_prev) || same(phiL_next, A) || same(phiL_next, x_bra) ||
+      same(phiL_next, x_ket))
+    return fail(TT_ERR_ALIASING, "output aliases an input");
+  const long long K = 1;
+  TT_PG_CARVE();
+  cudaError_t e = enqueue_left_pg(d, phiL_prev, A, x_bra, x_ket, phiL_next, T1, T2, Ah, Pp, pe,
+                                  static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "tt_interface_left_pg");
+  return TT_OK;
+}
+
+tt_status tt_interface_right_pg(int64_t rl_bra, int64_t rl, int64_t n, int64_t rr_bra, int64_t rr,
+                                int64_t Rl, int64_t Rr, const double* phiR_next, const double* A,
+                                const double* x_bra, const double* x_ket, double* phiR_prev,
+                                void* workspace, size_t workspace_bytes, void* stream) {
+  CallScope scope;
+  DimsPG d{rl_bra, rl, n, rr_bra, rr, Rl, Rr};
+  tt_status st = check_pg(d);
+  if (st != TT_OK) return st;
+  if (!phiR_next || !A || !x_bra || !x_ket || !phiR_prev)
+    return fail(TT_ERR_NULL_POINTER, "NULL tensor pointer");
+  if (same(phiR_prev, phiR_next) || same(phiR_prev, A) || same(phiR_prev, x_bra) ||
+      same(phiR_prev, x_ket))
+    return fail(TT_ERR_ALIASING, "output aliases an input");
+  const long long K = 1;
+  TT_PG_CARVE();
+  cudaError_t e = enqueue_right_pg(d, phiR_next, A, x_bra, x_ket, phiR_prev, T1, T2, Ah, Pp, pe,
+                                   static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "tt_interface_right_pg");
+  return TT_OK;
+}
+#undef TT_PG_CARVE
 
 // ---- LOBPCG ---------------------------------------------------------
 size_t tt_local_lobpcg_workspace_size(int64_t rl, int64_t n, int64_t rr, int64_t RlA, int64_t RrA,
