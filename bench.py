@@ -623,6 +623,26 @@ def main():
                     "ranks_out": [1] + [int(c.shape[2]) for c in rounded],
                     "ms": (t2 - t1) * 1e3, "ms_first": (t1 - t0) * 1e3,
                     "note": "synchronous (data-dependent ranks); host wall time"}
+        # the other row-3 steps at the interior core: left orthonormalisation of the train,
+        # the block-index move with the 4-component KKT block index, AMEn enrichment
+        def wall(fn, reps=2):
+            fn()
+            torch.cuda.synchronize(dev)
+            t = time.perf_counter()
+            for _ in range(reps):
+                fn()
+            torch.cuda.synchronize(dev)
+            return (time.perf_counter() - t) / reps * 1e3
+        k = cfg.d // 2
+        gen = torch.Generator(device=dev).manual_seed(13)
+        rnd = lambda *sh: torch.randn(*sh, dtype=torch.float64, device=dev, generator=gen)
+        Wh = rnd(cfg.r[k], cfg.N, 4, cfg.r[k + 1])
+        zk = rnd(cfg.r[k], cfg.N, 32)
+        rnd_info["orthonormalise_left_ms"] = wall(lambda: tt.tt_orthonormalise(xs, tt.TT_SWEEP_LEFT))
+        rnd_info["block_move_right_ms"] = wall(lambda: tt.tt_block_move_right(Wh, xs[k + 1], 1e-6))
+        rnd_info["enrich_right_ms"] = wall(lambda: tt.tt_enrich_right(xs[k], zk, xs[k + 1]))
+        rnd_info["row3_shapes"] = {"block_move": [cfg.r[k], cfg.N, 4, cfg.r[k + 1]],
+                                   "enrich": [cfg.r[k], cfg.N, cfg.r[k + 1], 32]}
 
     # ---- full sweeps at d = 12 (metric's second half), eager and as a CUDA graph ---------
     sweeps = None
