@@ -670,8 +670,30 @@ def main():
             for k in range(len(x4)):
                 tt.tt_local_matvec(pl4[k], A4[k], pr4[k + 1], x4[k], y4[k], workspace=wsm4,
                                    stream=st)
-        sweeps["config4_W34"] = time_sweep(tt, w34, stream, dev, reps=20)
-        sweeps["config4_W34"]["gflop"] = bench_w34_flops(ttgen.CONFIGS[4]) / 1e9
+        sweeps["config4_W34_separate_calls"] = time_sweep(tt, w34, stream, dev, reps=20)
+        # the same workload as one DAG-scheduled call (matvecs overlap the interface chains)
+        ws34 = torch.empty(tt.tt_sweep_w34_workspace_size(tr4), dtype=torch.uint8, device=dev)
+
+        def w34_dag(st):
+            tt.tt_sweep_w34(x4, A4, pl4, pr4, y4, workspace=ws34, stream=st)
+        sweeps["config4_W34"] = time_sweep(tt, w34_dag, stream, dev, reps=20)
+        f34 = bench_w34_flops(ttgen.CONFIGS[4])
+        sweeps["config4_W34"]["gflop"] = f34 / 1e9
+        sweeps["config4_W34"]["tflops_graph"] = f34 / (sweeps["config4_W34"]["graph_ms_median"] * 1e-3) / 1e12
+        sweeps["config4_W34"]["frac_of_p64"] = sweeps["config4_W34"]["tflops_graph"] / p64_sustained
+        # config 3 (d = 10) W34 as well
+        inp3 = ttgen.make_inputs(3)
+        x3 = [torch.from_numpy(c).to(dev) for c in inp3.x]
+        A3 = [torch.from_numpy(c).to(dev) for c in inp3.A]
+        pl3, pr3 = tt.alloc_interfaces(x3, A3), tt.alloc_interfaces(x3, A3)
+        y3 = [torch.empty_like(c) for c in x3]
+        ws3 = torch.empty(tt.tt_sweep_w34_workspace_size(tt._Train(x3, A3)), dtype=torch.uint8,
+                          device=dev)
+
+        def w34_c3(st):
+            tt.tt_sweep_w34(x3, A3, pl3, pr3, y3, workspace=ws3, stream=st)
+        sweeps["config3_W34"] = time_sweep(tt, w34_c3, stream, dev, reps=20)
+        sweeps["config3_W34"]["gflop"] = bench_w34_flops(ttgen.CONFIGS[3]) / 1e9
 
     # ---- CPU oracle baseline (rank 0, N=1) ----------------------------------------------
     cpu = None

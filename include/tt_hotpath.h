@@ -359,6 +359,19 @@ tt_status tt_enrich_right(int64_t rl, int64_t n, int64_t rx, int64_t rz, int64_t
                           const double* x_k1, double* x_k_out, double* x_k1_out, int64_t* s_out,
                           void* workspace, size_t workspace_bytes, void* stream);
 
+/* Workload W34 as one call: all interfaces (as
+ * tt_sweep_interfaces with TT_SWEEP_BOTH: phiL[0..d], phiR[0..d]) and y_k = local matvec of
+ * x_k with phiL[k], phiR[k+1] for every core (y_cores[k] shaped like x_cores[k]).  The two
+ * chains run concurrently and each matvec starts as soon as its two interfaces exist (event
+ * dependencies, pool streams, middle cores first); the caller's stream waits for all of it.
+ * Asynchronous, graph-capturable.  Workspace: tt_sweep_w34_workspace_size. */
+size_t tt_sweep_w34_workspace_size(int64_t d, const int64_t* n, const int64_t* r,
+                                   const int64_t* R);
+tt_status tt_sweep_w34(int64_t d, const int64_t* n, const int64_t* r, const int64_t* R,
+                       const double* const* x_cores, const double* const* A_cores,
+                       double* const* phiL, double* const* phiR, double* const* y_cores,
+                       void* workspace, size_t workspace_bytes, void* stream);
+
 /* Number of kernel launches the last call on this thread enqueued. */
 int64_t tt_last_launch_count(void);
 /* Test hook: on != 0 routes every GEMM stage of the calling thread through the generic

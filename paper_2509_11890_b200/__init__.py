@@ -32,7 +32,7 @@ __all__ = [
     "tt_orthonormalise", "tt_orthonormalise_workspace_size", "tt_block_move_right",
     "tt_block_move_left", "tt_block_move_workspace_size", "tt_pg_workspace_size",
     "tt_local_matvec_pg", "tt_interface_left_pg", "tt_interface_right_pg", "tt_enrich_right",
-    "tt_enrich_right_workspace_size",
+    "tt_enrich_right_workspace_size", "tt_sweep_w34", "tt_sweep_w34_workspace_size",
 ]
 
 STAGE_NAMES = {0: "perm", 1: "set", 2: "mv_s1", 3: "mv_s2", 4: "mv_s3", 5: "il_s1", 6: "il_s2",
@@ -111,6 +111,10 @@ lib.tt_block_move_right.argtypes = [_i64] * 6 + [ctypes.c_double, _i64] + [_p] *
 lib.tt_block_move_right.restype = ctypes.c_int
 lib.tt_block_move_left.argtypes = [_i64] * 6 + [ctypes.c_double, _i64] + [_p] * 6 + [_sz, _p]
 lib.tt_block_move_left.restype = ctypes.c_int
+lib.tt_sweep_w34_workspace_size.restype = _sz
+lib.tt_sweep_w34_workspace_size.argtypes = [_i64, _p, _p, _p]
+lib.tt_sweep_w34.argtypes = [_i64, _p, _p, _p, _p, _p, _p, _p, _p, _p, _sz, _p]
+lib.tt_sweep_w34.restype = ctypes.c_int
 lib.tt_pg_workspace_size.restype = _sz
 lib.tt_pg_workspace_size.argtypes = [_i64] * 8
 lib.tt_local_matvec_pg.argtypes = [_i64] * 8 + [_p] * 6 + [_sz, _p]
@@ -284,6 +288,28 @@ def tt_sweep_interfaces(x_cores, A_cores, phiL=None, phiR=None, directions=TT_SW
     _check(lib.tt_sweep_interfaces(tr.d, tr._n, tr._r, tr._R, tr._x, tr._A, pl, pr, directions,
                                    ws.data_ptr(), ws.numel(), _stream(stream)))
     return phiL, phiR
+
+
+def tt_sweep_w34_workspace_size(tr: _Train) -> int:
+    return int(lib.tt_sweep_w34_workspace_size(tr.d, tr._n, tr._r, tr._R))
+
+
+def tt_sweep_w34(x_cores, A_cores, phiL=None, phiR=None, y_cores=None, workspace=None,
+                 stream=None):
+    """Workload W34 in one DAG-scheduled call: all interfaces and one local matvec per core.
+    Returns (y_cores, phiL, phiR)."""
+    tr = _Train(x_cores, A_cores)
+    if phiL is None:
+        phiL = alloc_interfaces(x_cores, A_cores)
+    if phiR is None:
+        phiR = alloc_interfaces(x_cores, A_cores)
+    if y_cores is None:
+        y_cores = [torch.empty_like(c) for c in x_cores]
+    ws = _ws(tt_sweep_w34_workspace_size(tr), workspace, x_cores[0].device)
+    _check(lib.tt_sweep_w34(tr.d, tr._n, tr._r, tr._R, tr._x, tr._A, _ptrs(phiL, "phiL"),
+                            _ptrs(phiR, "phiR"), _ptrs(y_cores, "y_cores"), ws.data_ptr(),
+                            ws.numel(), _stream(stream)))
+    return y_cores, phiL, phiR
 
 
 def tt_sweep_als(x_cores, A_cores, X_blocks, Y_fwd=None, Y_bwd=None, phiL=None, phiR=None,

@@ -75,6 +75,32 @@ cudaError_t stream_dep(cudaStream_t from, cudaStream_t to) {
   return cudaStreamWaitEvent(to, ev, 0);
 }
 
+// ---- stream pool + dependency events for DAG-scheduled sweeps (per thread, per device) ----
+constexpr int kPoolStreams = 4;
+struct StreamPool {
+  int dev = -1;
+  cudaStream_t s[kPoolStreams] = {};
+  std::vector<cudaEvent_t> ev;
+};
+thread_local StreamPool g_pool;
+cudaError_t pool_init(size_t nevents) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (g_pool.dev != dev) {
+    for (auto& st : g_pool.s)
+      if ((e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    g_pool.ev.clear();
+    g_pool.dev = dev;
+  }
+  while (g_pool.ev.size() < nevents) {
+    cudaEvent_t ev;
+    if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return e;
+    g_pool.ev.push_back(ev);
+  }
+  return cudaSuccess;
+}
+
 long long trace_begin(int tile, long long M, long long N, long long K, cudaStream_t s) {
   if (!g_trace_on || 2 * (g_trace.size() + 1) > g_trace_pool.size()) return -1;
   TraceRec r;
@@ -1640,6 +1666,121 @@ tt_status tt_sweep_interfaces(int64_t d, const int64_t* n, const int64_t* r, con
         return cuda_fail(e, "sweep right");
   }
   if (sr != s && (e = stream_dep(sr, s)) != cudaSuccess) return cuda_fail(e, "join");
+  return TT_OK;
+}
+
+// ---- W34 as one DAG-scheduled call: both interface chains and one matvec per core ---------
+// Workspace: [sweep workspace (chain scratch x2, prepared operands)] [kPoolStreams matvec
+// scratches].  The left chain runs on the caller's stream, the right chain on the side
+// stream, and core k's matvec on a pool stream as soon as phiL[k] and phiR[k+1] exist
+// (events), middle cores first -- so the matvecs overlap the chains.
+static size_t w34_mv_scratch(int64_t d, const int64_t* n, const int64_t* r, const int64_t* R) {
+  size_t best = 0;
+  for (int64_t k = 0; k < d; ++k) {
+    Dims dk{r[k], n[k], r[k + 1], R[k], R[k + 1]};
+    long long t1, t2, ah, pe;
+    if (!matvec_ws_elems(dk, 1, t1, t2, ah, pe)) return 0;
+    best = std::max(best, ws_bytes({t1, t2, ah, pe}));
+  }
+  return best;
+}
+
+size_t tt_sweep_w34_workspace_size(int64_t d, const int64_t* n, const int64_t* r,
+                                   const int64_t* R) {
+  if (d <= 0 || !n || !r || !R) return 0;
+  const size_t base = sweep_ws(d, n, r, R, 0), mv = w34_mv_scratch(d, n, r, R);
+  if (base == 0 || mv == 0) return 0;
+  return align_up(base, 256) + kPoolStreams * align_up(mv, 256) + 256;
+}
+
+tt_status tt_sweep_w34(int64_t d, const int64_t* n, const int64_t* r, const int64_t* R,
+                       const double* const* x_cores, const double* const* A_cores,
+                       double* const* phiL, double* const* phiR, double* const* y_cores,
+                       void* workspace, size_t workspace_bytes, void* stream) {
+  CallScope scope;
+  tt_status st = check_train(d, n, r, R);
+  if (st != TT_OK) return st;
+  if ((st = check_ptrs(d, (const void* const*)x_cores, d, "x_cores")) != TT_OK) return st;
+  if ((st = check_ptrs(d, (const void* const*)A_cores, d, "A_cores")) != TT_OK) return st;
+  if ((st = check_ptrs(d, (const void* const*)phiL, d + 1, "phiL")) != TT_OK) return st;
+  if ((st = check_ptrs(d, (const void* const*)phiR, d + 1, "phiR")) != TT_OK) return st;
+  if ((st = check_ptrs(d, (const void* const*)y_cores, d, "y_cores")) != TT_OK) return st;
+  if ((st = check_outputs(d, x_cores, A_cores, nullptr, {{phiL, d + 1}, {phiR, d + 1}, {y_cores, d}},
+                          workspace)) != TT_OK)
+    return st;
+  const size_t need = tt_sweep_w34_workspace_size(d, n, r, R);
+  if (need == 0) return fail(TT_ERR_OVERFLOW, "workspace overflow");
+  if (!workspace || workspace_bytes < need)
+    return fail(TT_ERR_WORKSPACE, "workspace NULL or smaller than " + std::to_string(need) + " bytes");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  char* wsb = static_cast<char*>(workspace);
+  const size_t main_b = sweep_step_ws(d, n, r, R, 0);
+  void* ws_main = wsb;
+  void* ws_side = wsb + align_up(main_b, 256);
+  const size_t mv_b = w34_mv_scratch(d, n, r, R);
+  char* mv_base = wsb + align_up(sweep_ws(d, n, r, R, 0), 256);
+  if ((e = pool_init(size_t(2 * (d + 1) + kPoolStreams + 4))) != cudaSuccess) return cuda_fail(e, "pool");
+  cudaEvent_t* evL = g_pool.ev.data();         // evL[k]: phiL[k] ready
+  cudaEvent_t* evR = evL + (d + 1);            // evR[k]: phiR[k] ready
+  cudaEvent_t* evJ = evR + (d + 1);            // joins
+  if ((e = launch_prep(d, n, r, R, 0, x_cores, A_cores, workspace, s)) != cudaSuccess)
+    return cuda_fail(e, "sweep prep");
+  cudaStream_t sr;
+  if ((e = side_stream(&sr)) != cudaSuccess) return cuda_fail(e, "side stream");
+  if ((e = stream_dep(s, sr)) != cudaSuccess) return cuda_fail(e, "fork");
+  for (int q = 0; q < kPoolStreams; ++q)
+    if ((e = stream_dep(s, g_pool.s[q])) != cudaSuccess) return cuda_fail(e, "fork");
+  // the two chains
+  if ((e = launch_set_one(phiL[0], s)) != cudaSuccess) return cuda_fail(e, "sweep");
+  if ((e = cudaEventRecord(evL[0], s)) != cudaSuccess) return cuda_fail(e, "event");
+  for (int64_t k = 0; k < d; ++k) {
+    if ((e = sweep_left_step(k, d, 0, ws_main, n, r, R, x_cores, A_cores, phiL, workspace, main_b,
+                             s)) != cudaSuccess)
+      return cuda_fail(e, "sweep left");
+    if ((e = cudaEventRecord(evL[k + 1], s)) != cudaSuccess) return cuda_fail(e, "event");
+  }
+  if ((e = launch_set_one(phiR[d], sr)) != cudaSuccess) return cuda_fail(e, "sweep");
+  if ((e = cudaEventRecord(evR[d], sr)) != cudaSuccess) return cuda_fail(e, "event");
+  for (int64_t k = d - 1; k >= 0; --k) {
+    if ((e = sweep_right_step(k, d, 0, ws_side, n, r, R, x_cores, A_cores, phiR, workspace,
+                              main_b, sr)) != cudaSuccess)
+      return cuda_fail(e, "sweep right");
+    if ((e = cudaEventRecord(evR[k], sr)) != cudaSuccess) return cuda_fail(e, "event");
+  }
+  // matvecs in readiness order (core k needs k left steps and d-1-k right steps)
+  std::vector<int64_t> order(d);
+  for (int64_t k = 0; k < d; ++k) order[k] = k;
+  std::stable_sort(order.begin(), order.end(), [&](int64_t p, int64_t q) {
+    return std::max(p, d - 1 - p) < std::max(q, d - 1 - q);
+  });
+  for (int64_t i = 0; i < d; ++i) {
+    const int64_t k = order[i];
+    const int q = (int)(i % kPoolStreams);
+    cudaStream_t ps = g_pool.s[q];
+    if ((e = cudaStreamWaitEvent(ps, evL[k], 0)) != cudaSuccess) return cuda_fail(e, "wait");
+    if ((e = cudaStreamWaitEvent(ps, evR[k + 1], 0)) != cudaSuccess) return cuda_fail(e, "wait");
+    Dims dk{r[k], n[k], r[k + 1], R[k], R[k + 1]};
+    long long t1, t2, ah, pe;
+    matvec_ws_elems(dk, 1, t1, t2, ah, pe);
+    Carver c{mv_base + q * align_up(mv_b, 256), mv_b};
+    double* T1 = c.take(t1);
+    double* T2 = c.take(t2);
+    double* Ah = c.take(ah);
+    double* Pp = c.take(pe);
+    if (!c.ok) return fail(TT_ERR_WORKSPACE, "workspace too small after alignment");
+    const Prep pp = prep_ptrs(k, d, n, r, R, 0, workspace);
+    if ((e = enqueue_matvec(dk, 1, phiL[k], A_cores[k], phiR[k + 1], x_cores[k], y_cores[k], T1,
+                            T2, Ah, Pp, pe, ps, pp.Ahl)) != cudaSuccess)
+      return cuda_fail(e, "sweep matvec");
+  }
+  // join everything back into the caller's stream
+  if ((e = cudaEventRecord(evJ[0], sr)) != cudaSuccess || (e = cudaStreamWaitEvent(s, evJ[0], 0)) != cudaSuccess)
+    return cuda_fail(e, "join");
+  for (int q = 0; q < kPoolStreams; ++q)
+    if ((e = cudaEventRecord(evJ[1 + q], g_pool.s[q])) != cudaSuccess ||
+        (e = cudaStreamWaitEvent(s, evJ[1 + q], 0)) != cudaSuccess)
+      return cuda_fail(e, "join");
   return TT_OK;
 }
 

@@ -539,3 +539,53 @@ def test_jacobi_eigen_vs_numpy(tt, n):
     Vh = h(V)
     assert np.allclose(Vh.T @ Vh, np.eye(n), atol=1e-12)
     assert np.allclose(G @ Vh, Vh * h(lam), atol=1e-10 * ref[0])
+
+
+# ----------------------------------------------------------------------------------------
+# W34 as one DAG-scheduled call (tt_sweep_w34)
+# ----------------------------------------------------------------------------------------
+@pytest.mark.parametrize("idx", [1, 2, 3, 4])
+def test_sweep_w34_call_vs_oracle_and_separate_calls(tt, idx):
+    import oracle
+    import ttgen
+    inp = ttgen.make_inputs(idx)
+    x = [g(c) for c in inp.x]
+    A = [g(c) for c in inp.A]
+    y, pl, pr = tt.tt_sweep_w34(x, A)
+    torch.cuda.synchronize()
+    # identical to the separate calls (same kernels, deterministic)
+    pl2, pr2 = tt.alloc_interfaces(x, A), tt.alloc_interfaces(x, A)
+    tt.tt_sweep_interfaces(x, A, pl2, pr2)
+    for k in range(len(x)):
+        y2 = tt.tt_local_matvec(pl2[k], A[k], pr2[k + 1], x[k])
+        assert torch.equal(y[k], y2)
+    for a, b in zip(pl + pr, pl2 + pr2):
+        assert torch.equal(a, b)
+    # and the oracle
+    opl, opr = oracle.sweep_interfaces(inp.x, inp.A, 3)
+    for k in range(len(x)):
+        ref = oracle.local_matvec(opl[k], inp.A[k], opr[k + 1], inp.x[k])
+        assert rel(h(y[k]), ref) <= TOL
+        assert rel(h(pl[k + 1]), opl[k + 1]) <= TOL and rel(h(pr[k]), opr[k]) <= TOL
+
+
+def test_sweep_w34_graph_capture(tt):
+    import ttgen
+    inp = ttgen.make_inputs(3)
+    x = [g(c) for c in inp.x]
+    A = [g(c) for c in inp.A]
+    y0, _, _ = tt.tt_sweep_w34(x, A)
+    torch.cuda.synchronize()
+    pl, pr = tt.alloc_interfaces(x, A), tt.alloc_interfaces(x, A)
+    y = [torch.zeros_like(c) for c in x]
+    tr = tt._Train(x, A)
+    ws = torch.empty(tt.tt_sweep_w34_workspace_size(tr), dtype=torch.uint8, device="cuda")
+    s = torch.cuda.Stream()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(graph, stream=s):
+            tt.tt_sweep_w34(x, A, pl, pr, y, workspace=ws, stream=s)
+    graph.replay()
+    torch.cuda.synchronize()
+    for a, b in zip(y, y0):
+        assert torch.equal(a, b)
