@@ -527,7 +527,8 @@ def main():
               "ms": t["graph_ms_median"], "ms_eager": t["eager_ms_median"],
               "gflop": (mv_f + orth_f) / 1e9,
               "tflops": (mv_f + orth_f) / (t["graph_ms_median"] * 1e-3) / 1e12,
-              "matvec_share_of_flops": mv_f / (mv_f + orth_f)}
+              "matvec_share_of_flops": mv_f / (mv_f + orth_f),
+              "frac_of_p64": (mv_f + orth_f) / (t["graph_ms_median"] * 1e-3) / 1e12 / p64_sustained}
 
     # ---- SURVEY 8(f) rows 2 and 4 on the interior core: KKT block action, two-site matvec --
     kkt = two = None
@@ -549,7 +550,8 @@ def main():
         f9 = 9 * f_local(rl, nn, rr, Rl, Rr)
         kkt = {"core": k, "operators": 8, "terms": len(terms), "matvecs": 9,
                "ms": t["graph_ms_median"], "gflop": f9 / 1e9,
-               "tflops": f9 / (t["graph_ms_median"] * 1e-3) / 1e12}
+               "tflops": f9 / (t["graph_ms_median"] * 1e-3) / 1e12,
+               "frac_of_p64": f9 / (t["graph_ms_median"] * 1e-3) / 1e12 / p64_sustained}
         # two-site (DMRG supercore) matvec: 2x2 modes (N = 4), bonds of the interior core
         A1, A2 = rnd(Rl, 2, 2, Rl), rnd(Rl, 2, 2, Rr)
         W2 = rnd(rl, 2, 2, cfg.nvec, rr)
@@ -562,7 +564,8 @@ def main():
                        stream, dev, reps=5)
         f2 = cfg.nvec * f_local(rl, 4, rr, Rl, Rr)
         two = {"core": k, "n1": 2, "n2": 2, "nvec": cfg.nvec, "ms": t["graph_ms_median"],
-               "gflop": f2 / 1e9, "tflops": f2 / (t["graph_ms_median"] * 1e-3) / 1e12}
+               "gflop": f2 / 1e9, "tflops": f2 / (t["graph_ms_median"] * 1e-3) / 1e12,
+               "frac_of_p64": f2 / (t["graph_ms_median"] * 1e-3) / 1e12 / p64_sustained}
 
     # ---- block LOBPCG of the step-length eigenproblem (interior core) ---
     lob = None
@@ -608,7 +611,8 @@ def main():
             lob[name] = {"ms": t["graph_ms_median"], "ms_eager": t["eager_ms_median"],
                          "ms_per_iteration": t["graph_ms_median"] / its_l,
                          "matvec_gflop": mv_f / 1e9,
-                         "matvec_tflops_over_total_time": mv_f / (t["graph_ms_median"] * 1e-3) / 1e12}
+                         "matvec_tflops_over_total_time": mv_f / (t["graph_ms_median"] * 1e-3) / 1e12,
+                         "frac_of_p64": mv_f / (t["graph_ms_median"] * 1e-3) / 1e12 / p64_sustained}
 
     # ---- TT rounding of the config-5 vector train (delta = 1e-4) --------
     rnd_info = None

@@ -38,7 +38,11 @@ def run(variant, flags, a=256, b=256, al=36, be=36, n=4, K=32, reps=3):
 
 if __name__ == "__main__":
     for variant in [int(v) for v in (sys.argv[1:] or ['1', '2'])]:
-        for flags, name in ((0, "normal"), (16, "no-L2-hints"), (32, "no-evict-first"), (64, "no-evict-last"), (128, "2d-boxes"), (1, "no-stores"), (2, "no-loads"), (3, "compute-only")):
+        sets = ((0, "normal"), (16, "no-L2-hints"), (32, "no-evict-first"), (64, "no-evict-last"),
+                (128, "2d-boxes"), (1, "no-stores"), (2, "no-loads"), (3, "compute-only"))
+        if os.environ.get("PROBE_QUICK"):
+            sets = ((0, "normal"), (3, "compute-only"))
+        for flags, name in sets:
             res = run(variant, flags)
             print(f"variant {variant} {name:13s} " + "  ".join(
                 f"{k}: {ms:.3f} ms {tf:.2f} TF" for k, (ms, tf) in sorted(res.items())), flush=True)
