@@ -19,7 +19,9 @@ __global__ void __launch_bounds__(256) colreduce_kernel(const double* __restrict
                                                         int L, const double* __restrict__ B,
                                                         long long rows, int K, int rr,
                                                         long long rows_per_chunk,
-                                                        double* __restrict__ part) {
+                                                        double* __restrict__ part,
+                                                        const int* __restrict__ gate) {
+  if (gate && *gate) return;
   const int c = blockIdx.x, j = blockIdx.y, chunks = gridDim.x;
   const long long r0 = c * rows_per_chunk;
   const long long r1 = min(rows, r0 + rows_per_chunk);
@@ -55,7 +57,8 @@ __global__ void __launch_bounds__(256) colreduce_kernel(const double* __restrict
 
 // out[l*K + j] = sum_c part[(l*K + j)*chunks + c]   (fixed order: deterministic)
 __global__ void colreduce_finish_kernel(const double* __restrict__ part, int LK, int chunks,
-                                        double* __restrict__ out) {
+                                        double* __restrict__ out, const int* __restrict__ gate) {
+  if (gate && *gate) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= LK) return;
   double v = 0.0;
@@ -67,7 +70,8 @@ __global__ void colreduce_finish_kernel(const double* __restrict__ part, int LK,
 __global__ void __launch_bounds__(256) colaxpy_kernel(const double* __restrict__ A, long long S,
                                                       int L, const double* __restrict__ coef,
                                                       double sign, double* __restrict__ B,
-                                                      int K, int rr) {
+                                                      int K, int rr, const int* __restrict__ gate) {
+  if (gate && *gate) return;
   __shared__ double cf[kMaxL * 64];
   for (int i = threadIdx.x; i < L * K; i += blockDim.x) cf[i] = sign * coef[i];
   __syncthreads();
@@ -82,7 +86,9 @@ __global__ void __launch_bounds__(256) colaxpy_kernel(const double* __restrict__
 
 // dst[e] = src[e] * s[j(e)];  dst2 (optional) = src - dst2 (residual form: dst = F - W)
 __global__ void colscale_kernel(const double* __restrict__ src, const double* __restrict__ s,
-                                double* __restrict__ dst, long long S, int K, int rr) {
+                                double* __restrict__ dst, long long S, int K, int rr,
+                                const int* __restrict__ gate) {
+  if (gate && *gate) return;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < S;
        e += (long long)gridDim.x * blockDim.x)
     dst[e] = src[e] * s[(e / rr) % K];
@@ -116,6 +122,7 @@ struct GmresState {
   int* active;    // [K]
   int* kcyc;      // [K]   Arnoldi steps in the current cycle
   long long* its; // [K]   total Arnoldi steps (output)
+  int* done;      // [1]   all columns inactive in the current cycle
 };
 
 // cycle start: beta = ||r_j|| (true residual of the current iterate)
@@ -185,6 +192,13 @@ __global__ void gmres_arnoldi_kernel(GmresState st, const double* __restrict__ h
   st.scale[j] = (!done && hn > 0.0) ? 1.0 / hn : 0.0;
 }
 
+// *done = no column is active (gates the rest of the cycle's Arnoldi steps)
+__global__ void gmres_alldone_kernel(const int* __restrict__ active, int K, int* __restrict__ done) {
+  int any = 0;
+  for (int j = 0; j < K; ++j) any |= active[j];
+  *done = !any;
+}
+
 // back substitution H[:k,:k] y = g[:k] per column -> coef[l*K + j] (0 beyond k)
 __global__ void gmres_backsolve_kernel(GmresState st, int K, int m) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -233,11 +247,11 @@ cudaError_t launch_coldots(const GmresDims& gd, const double* A, int L, const do
     const int Lp = std::min(kMaxL, L - l0);
     dim3 grid(gd.chunks, gd.K);
     colreduce_kernel<<<grid, 256, 0, s>>>(A + l0 * gd.S, gd.S, Lp, B, gd.rows, gd.K, gd.rr,
-                                          gd.rows_per_chunk, part);
+                                          gd.rows_per_chunk, part, g_gate);
     ++g_launches;
     const int LK = Lp * gd.K;
     colreduce_finish_kernel<<<(LK + 255) / 256, 256, 0, s>>>(part, LK, gd.chunks,
-                                                            out + (long long)l0 * gd.K);
+                                                            out + (long long)l0 * gd.K, g_gate);
     ++g_launches;
   }
   return cudaGetLastError();
@@ -251,7 +265,7 @@ cudaError_t launch_colaxpy(const GmresDims& gd, const double* A, int L, const do
     const int Lp = std::min(kMaxL, L - l0);
     colaxpy_kernel<<<(unsigned)blocks, 256, 0, s>>>(A + l0 * gd.S, gd.S, Lp,
                                                      coef + (long long)l0 * gd.K, sign, B, gd.K,
-                                                     gd.rr);
+                                                     gd.rr, g_gate);
     ++g_launches;
   }
   return cudaGetLastError();
@@ -262,7 +276,7 @@ cudaError_t launch_elementwise(int kind, const double* a, const double* sc, doub
   long long blocks = (gd.S + 255) / 256;
   if (blocks > 8LL * num_sms()) blocks = 8LL * num_sms();
   if (kind == 0)
-    colscale_kernel<<<(unsigned)blocks, 256, 0, s>>>(a, sc, b, gd.S, gd.K, gd.rr);
+    colscale_kernel<<<(unsigned)blocks, 256, 0, s>>>(a, sc, b, gd.S, gd.K, gd.rr, g_gate);
   else if (kind == 1)
     sub_kernel<<<(unsigned)blocks, 256, 0, s>>>(a, b, gd.S);
   else
@@ -327,6 +341,7 @@ cudaError_t enqueue_gmres(const Dims& d, long long K, long long m, long long kau
   double* wn2 = h2 + (ms + 1) * K;
   st.active = reinterpret_cast<int*>(wn2 + K);
   st.kcyc = st.active + K;
+  st.done = st.kcyc + K;
   st.its = its_out;
   const GmresDims gd = gmres_dims(d, K);
   // vector slots: V_0..V_{m+nz} (Arnoldi basis, at most ms + 1), then the kaug Z slots
@@ -350,7 +365,15 @@ cudaError_t enqueue_gmres(const Dims& d, long long K, long long m, long long kau
     if ((e = launch_coldots(gd, W, 1, W, part, wn2, s)) != cudaSuccess) return e;
     gmres_cycle_init_kernel<<<kb, kt, 0, s>>>(st, wn2, (int)K, (int)ms, tol);
     ++g_launches;
+    gmres_alldone_kernel<<<1, 1, 0, s>>>(st.active, (int)K, st.done);
+    ++g_launches;
     if ((e = launch_elementwise(0, W, st.scale, V, gd, s)) != cudaSuccess) return e;
+    // once every column has converged the rest of the cycle's Arnoldi steps are no-ops
+    // (device flag read by every launch of the step, the matvec's GEMMs included)
+    struct GateScope {
+      GateScope(const int* g) { g_gate = g; }
+      ~GateScope() { g_gate = nullptr; }
+    } gscope(st.done);
     for (long long i = 0; i < m + nz; ++i) {
       const double* in = (i < m) ? V + i * gd.S : Zs + (long long)zorder[i - m] * gd.S;
       if ((e = enqueue_matvec(d, K, phiL, A, phiR, in, W, T1, T2, Ah, Pp, pe, s, Ah)) !=
@@ -365,9 +388,12 @@ cudaError_t enqueue_gmres(const Dims& d, long long K, long long m, long long kau
       if ((e = launch_coldots(gd, W, 1, W, part, wn2, s)) != cudaSuccess) return e;
       gmres_arnoldi_kernel<<<kb, kt, 0, s>>>(st, h1, h2, wn2, (int)K, (int)ms, (int)i, tol);
       ++g_launches;
+      gmres_alldone_kernel<<<1, 1, 0, s>>>(st.active, (int)K, st.done);
+      ++g_launches;
       if ((e = launch_elementwise(0, W, st.scale, V + (i + 1) * gd.S, gd, s)) != cudaSuccess)
         return e;
     }
+    g_gate = nullptr;
     gmres_backsolve_kernel<<<kb, kt, 0, s>>>(st, (int)K, (int)ms);
     ++g_launches;
     // correction C = sum_{i<m} y_i v_i + sum_{j<nz} y_{m+j} z_j;  x += C

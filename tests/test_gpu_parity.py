@@ -589,3 +589,34 @@ def test_sweep_w34_graph_capture(tt):
     torch.cuda.synchronize()
     for a, b in zip(y, y0):
         assert torch.equal(a, b)
+
+
+def test_local_gmres_converged_cycle_is_gated(tt):
+    """Once every column has converged, the rest of the cycle's Arnoldi steps are device-gated
+    no-ops: a solve that converges early costs far less than the same launch sequence with
+    tol = 0, and its result equals the oracle's."""
+    from oracle.gmres import local_gmres_batched
+    mixed, A, phiL, phiR, rng = _mixed_canonical_system(2, 3)
+    k = 3
+    shape = mixed[k].shape
+    F = rng.standard_normal((shape[0], shape[1], 4, shape[2]))
+    args = (g(phiL), g(A[k]), g(phiR), g(F))
+
+    def run(tol):
+        X = torch.zeros_like(args[3])
+        tt.tt_local_gmres(*args, X, m=60, cycles=1, tol=tol)   # warm
+        X.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        out = tt.tt_local_gmres(*args, X, m=60, cycles=1, tol=tol)
+        e1.record()
+        torch.cuda.synchronize()
+        return out, e0.elapsed_time(e1)
+    (X1, rel1, it1), t_conv = run(1e-8)
+    (_, _, it0), t_full = run(0.0)
+    assert int(h(it1).max()) < 60 and int(h(it0).min()) == 60
+    assert t_conv < 0.8 * t_full
+    Xo, relo, ito = local_gmres_batched(phiL, A[k], phiR, F, np.zeros_like(F), m=60, cycles=1,
+                                        tol=1e-8)
+    assert np.array_equal(h(it1), ito)
+    assert rel(h(X1), Xo) <= 1e-9
