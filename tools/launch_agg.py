@@ -21,7 +21,8 @@ for r in rows:
     key = m.group(1) if m else name[:40]
     v = float(d["Metric Value"].replace(",", ""))
     unit = d["Metric Unit"]
-    v = v / 1e3 if unit == "nsecond" else v * 1e3 if unit == "msecond" else v
+    scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}
+    v *= scale.get(unit, 1.0)   # -> microseconds
     agg[key][0] += 1
     agg[key][1] += v
 tot = sum(v[1] for v in agg.values())
