@@ -14,7 +14,11 @@
 constexpr int kMaxL = 32;   // basis vectors per reduction pass
 
 // Column-segmented reduction: part[(l*K + j)*chunks + c] = sum over the rows of chunk c of
-// sum_b A_l[row, j, b] * B[row, j, b], for l < L (A_l = A + l*S).  Grid (chunks, K).
+// sum_b A_l[row, j, b] * B[row, j, b], for l < L <= LMAX (A_l = A + l*S).  Grid (chunks, K).
+// Column j of a row is the contiguous run [(row K + j) rr, + rr); with VEC = 2 a thread
+// reads b pairs as 16-byte loads (rr even).  LMAX bounds the accumulators: fewer registers,
+// more resident warps, more loads in flight (the kernel is HBM-bound).
+template <int LMAX, int VEC>
 __global__ void __launch_bounds__(256) colreduce_kernel(const double* __restrict__ A, long long S,
                                                         int L, const double* __restrict__ B,
                                                         long long rows, int K, int rr,
@@ -25,22 +29,40 @@ __global__ void __launch_bounds__(256) colreduce_kernel(const double* __restrict
   const int c = blockIdx.x, j = blockIdx.y, chunks = gridDim.x;
   const long long r0 = c * rows_per_chunk;
   const long long r1 = min(rows, r0 + rows_per_chunk);
-  double acc[kMaxL];
+  double acc[LMAX];
 #pragma unroll
-  for (int l = 0; l < kMaxL; ++l) acc[l] = 0.0;
-  const long long nel = (r1 - r0) * rr;
-  for (long long t = threadIdx.x; t < nel; t += blockDim.x) {
-    const long long row = r0 + t / rr;
-    const long long e = (row * K + j) * rr + (t % rr);
-    const double b = B[e];
+  for (int l = 0; l < LMAX; ++l) acc[l] = 0.0;
+  if (VEC == 2) {
+    const int half = rr / 2;
+    for (long long row = r0; row < r1; ++row) {
+      const long long base = (row * K + j) * rr;
+      for (int bb = threadIdx.x; bb < half; bb += blockDim.x) {
+        const long long e = base + 2 * bb;
+        const double2 bv = *reinterpret_cast<const double2*>(B + e);
+        double2 av[LMAX];
 #pragma unroll
-    for (int l = 0; l < kMaxL; ++l)
-      if (l < L) acc[l] = fma(A[l * S + e], b, acc[l]);
+        for (int l = 0; l < LMAX; ++l)
+          if (l < L) av[l] = *reinterpret_cast<const double2*>(A + l * S + e);
+#pragma unroll
+        for (int l = 0; l < LMAX; ++l)
+          if (l < L) acc[l] = fma(av[l].y, bv.y, fma(av[l].x, bv.x, acc[l]));
+      }
+    }
+  } else {
+    const unsigned nel = (unsigned)((r1 - r0) * rr);
+    for (unsigned t = threadIdx.x; t < nel; t += blockDim.x) {
+      const unsigned rowo = t / (unsigned)rr, bb = t - rowo * (unsigned)rr;
+      const long long e = ((r0 + rowo) * K + j) * rr + bb;
+      const double bv = B[e];
+#pragma unroll
+      for (int l = 0; l < LMAX; ++l)
+        if (l < L) acc[l] = fma(A[l * S + e], bv, acc[l]);
+    }
   }
-  __shared__ double red[8][kMaxL];
+  __shared__ double red[8][LMAX];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-  for (int l = 0; l < kMaxL; ++l) {
+  for (int l = 0; l < LMAX; ++l) {
     if (l < L) {
       double v = acc[l];
       for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
@@ -75,12 +97,18 @@ __global__ void __launch_bounds__(256) colaxpy_kernel(const double* __restrict__
   __shared__ double cf[kMaxL * 64];
   for (int i = threadIdx.x; i < L * K; i += blockDim.x) cf[i] = sign * coef[i];
   __syncthreads();
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < S;
-       e += (long long)gridDim.x * blockDim.x) {
-    const int j = (int)((e / rr) % K);
-    double v = B[e];
-    for (int l = 0; l < L; ++l) v = fma(cf[l * K + j], A[l * S + e], v);
-    B[e] = v;
+  // one (row, column) run of rr contiguous doubles per block iteration (no per-element
+  // 64-bit division)
+  const long long runs = S / rr;
+  for (long long rc = blockIdx.x; rc < runs; rc += gridDim.x) {
+    const int j = (int)(rc % K);
+    const long long base = rc * rr;
+    for (int bb = threadIdx.x; bb < rr; bb += blockDim.x) {
+      const long long e = base + bb;
+      double v = B[e];
+      for (int l = 0; l < L; ++l) v = fma(cf[l * K + j], A[l * S + e], v);
+      B[e] = v;
+    }
   }
 }
 
@@ -243,11 +271,24 @@ GmresDims gmres_dims(const Dims& d, long long K) {
 // out[l*K+j] = <A_l[:,j], B[:,j]> for l < L (L any size; passes of kMaxL)
 cudaError_t launch_coldots(const GmresDims& gd, const double* A, int L, const double* B,
                            double* part, double* out, cudaStream_t s) {
-  for (int l0 = 0; l0 < L; l0 += kMaxL) {
-    const int Lp = std::min(kMaxL, L - l0);
+  constexpr int kPass = 16;   // accumulators per pass (colreduce_kernel LMAX)
+  for (int l0 = 0; l0 < L; l0 += kPass) {
+    const int Lp = std::min(kPass, L - l0);
     dim3 grid(gd.chunks, gd.K);
-    colreduce_kernel<<<grid, 256, 0, s>>>(A + l0 * gd.S, gd.S, Lp, B, gd.rows, gd.K, gd.rr,
-                                          gd.rows_per_chunk, part, g_gate);
+    const double* Al = A + l0 * gd.S;
+    const bool v2 = (gd.rr % 2 == 0) && (gd.S % 2 == 0) &&
+                    ((reinterpret_cast<uintptr_t>(Al) | reinterpret_cast<uintptr_t>(B)) & 15) == 0;
+#define TT_COLRED(LM)                                                                         \
+  do {                                                                                        \
+    if (v2) colreduce_kernel<LM, 2><<<grid, 256, 0, s>>>(Al, gd.S, Lp, B, gd.rows, gd.K, gd.rr, \
+                                                         gd.rows_per_chunk, part, g_gate);      \
+    else colreduce_kernel<LM, 1><<<grid, 256, 0, s>>>(Al, gd.S, Lp, B, gd.rows, gd.K, gd.rr,    \
+                                                      gd.rows_per_chunk, part, g_gate);         \
+  } while (0)
+    if (Lp <= 4) TT_COLRED(4);
+    else if (Lp <= 8) TT_COLRED(8);
+    else TT_COLRED(16);
+#undef TT_COLRED
     ++g_launches;
     const int LK = Lp * gd.K;
     colreduce_finish_kernel<<<(LK + 255) / 256, 256, 0, s>>>(part, LK, gd.chunks,
