@@ -158,9 +158,11 @@ tt_status tt_operator_apply(int64_t d, const int64_t* n_row, const int64_t* n_co
  * SYNCHRONOUS: the truncation ranks are data dependent (one host read per core).
  * ------------------------------------------------------------------------------------- */
 size_t tt_round_workspace_size(int64_t d, const int64_t* n, const int64_t* r);
-/* Test hook: eigendecomposition of a symmetric n x n matrix G (overwritten; n <= 512) by the
- * rounding's parallel Jacobi solver: V columns = eigenvectors, lam descending.  Workspace
- * >= 4 (n+1)^2 + 8200 doubles. */
+/* Test hook: eigendecomposition of a symmetric n x n matrix G (overwritten; n <= 2048) by the
+ * rounding's parallel Jacobi solver (element-wise for n <= 64, block Jacobi above; debug flag
+ * 256 forces the element-wise kernel): V columns = eigenvectors, lam descending.  Workspace
+ * >= max(4 ne^2, 2 nb^2 + 32 nb) + 8200 doubles, ne = n rounded up to even, nb = n rounded
+ * up to a multiple of 32. */
 tt_status tt_debug_sym_eigen(int64_t n, double* G, double* V, double* lam, void* workspace,
                              size_t workspace_bytes, void* stream);
 tt_status tt_round(int64_t d, const int64_t* n, const int64_t* r_in,

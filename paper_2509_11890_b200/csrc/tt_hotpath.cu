@@ -1160,14 +1160,53 @@ bool same(const void* p, const void* q) { return p != nullptr && p == q; }
 #include "tt_lobpcg.cuh"
 
 // Symmetric eigendecomposition of the n x n Gram matrix G: lam (descending) and V (columns)
-// in the caller's buffers.  Scratch: 4 padded (np x np) buffers + partials (np = n rounded up
-// to even) carved from `scratch` (sym_eigen_scratch(n) doubles).
+// in the caller's buffers.  n <= 64: element-wise cooperative Jacobi (4 padded np x np
+// buffers, np = n rounded up to even); larger n: block Jacobi (G and V padded to a multiple
+// of 32 plus the per-pair rotations).  Scratch: sym_eigen_scratch(n) doubles.
+constexpr int kBlockJacobiMin = 65;
 long long sym_eigen_scratch(long long n) {
   const long long np = (n + 1) & ~1LL;
-  return 4 * np * np + 2 * 4096 + 8;
+  const long long nb = (n + kJB2 - 1) / kJB2 * kJB2;
+  const long long elem = 4 * np * np, blk = 2 * nb * nb + (nb / kJB2) * kJB2 * kJB2;
+  return std::max(elem, blk) + 2 * 4096 + 8;
 }
+thread_local int g_eigen_elementwise = 0;   // test hook: force the element-wise kernel
 cudaError_t launch_sym_eigen(const double* G, double* V, double* lam, int n, double* scratch,
                              cudaStream_t s) {
+  g_stage = TT_ST_PERM;
+  const long long tr = trace_begin(0, (long long)n * n, 0, 0, s);
+  int dev = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaError_t e;
+  if (n >= kBlockJacobiMin && !g_eigen_elementwise) {
+    const int np = (n + kJB2 - 1) / kJB2 * kJB2;
+    const long long NN = (long long)np * np;
+    double* G0 = scratch;
+    double* V0 = G0 + NN;
+    double* Rbuf = V0 + NN;
+    const int m = np / kJB2;   // block pairs per step
+    double* part = Rbuf + (long long)m * kJB2 * kJB2;
+    int* which = reinterpret_cast<int*>(part + 2 * 4096);
+    long long eb = std::min<long long>(4096, (NN + 255) / 256);
+    embed_kernel<<<(unsigned)eb, 256, 0, s>>>(G, G0, n, np);
+    ++g_launches;
+    if ((e = cudaMemsetAsync(which, 0, sizeof(int), s)) != cudaSuccess) return e;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_block_coop_kernel, 256, 0);
+    int grid = num_sms() * std::max(per_sm, 1);
+    const int tasks = m * m + (np / kJB2) * m;
+    if (grid > tasks) grid = tasks;
+    if (grid > 4096) grid = 4096;
+    int sweeps = 30;
+    int npi = np;
+    void* args[] = {&G0, &V0, (void*)&npi, &sweeps, &Rbuf, &part};
+    e = cudaLaunchCooperativeKernel((const void*)jacobi_block_coop_kernel, grid, 256, args, 0, s);
+    ++g_launches;
+    if (e != cudaSuccess) return e;
+    sort_padded_kernel<<<(n + 255) / 256, 256, 0, s>>>(G0, G0, V0, V0, which, V, lam, n, np);
+    ++g_launches;
+    trace_end(tr, s);
+    return cudaGetLastError();
+  }
   const int np = (n + 1) & ~1;
   const long long NN = (long long)np * np;
   double* G0 = scratch;
@@ -1176,14 +1215,10 @@ cudaError_t launch_sym_eigen(const double* G, double* V, double* lam, int n, dou
   double* V1 = V0 + NN;
   double* part = V1 + NN;
   int* which = reinterpret_cast<int*>(part + 2 * 4096);
-  g_stage = TT_ST_PERM;
-  const long long tr = trace_begin(0, (long long)n * n, 0, 0, s);
   long long eb = (NN + 255) / 256;
   if (eb > 4096) eb = 4096;
   embed_kernel<<<(unsigned)eb, 256, 0, s>>>(G, G0, n, np);
   ++g_launches;
-  int dev = 0, per_sm = 0;
-  cudaGetDevice(&dev);
   const size_t smem = (size_t)np / 2 * (2 * sizeof(double) + 2 * sizeof(int));
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_coop_kernel, 256, smem);
   int grid = num_sms() * std::max(per_sm, 1);
@@ -1192,8 +1227,7 @@ cudaError_t launch_sym_eigen(const double* G, double* V, double* lam, int n, dou
   if (grid > 4096) grid = 4096;
   int sweeps = 25;
   void* args[] = {&G0, &G1, &V0, &V1, (void*)&np, &sweeps, &part, &which};
-  cudaError_t e = cudaLaunchCooperativeKernel((const void*)jacobi_coop_kernel, grid, 256, args,
-                                              smem, s);
+  e = cudaLaunchCooperativeKernel((const void*)jacobi_coop_kernel, grid, 256, args, smem, s);
   ++g_launches;
   if (e != cudaSuccess) return e;
   sort_padded_kernel<<<(n + 255) / 256, 256, 0, s>>>(G0, G1, V0, V1, which, V, lam, n, np);
@@ -1925,11 +1959,13 @@ tt_status tt_operator_apply(int64_t d, const int64_t* n_row, const int64_t* n_co
 tt_status tt_debug_sym_eigen(int64_t n, double* G, double* V, double* lam, void* workspace,
                              size_t workspace_bytes, void* stream) {
   CallScope scope;
-  if (n <= 0 || n > 512) return fail(TT_ERR_INVALID_ARGUMENT, "0 < n <= 512");
+  if (n <= 0 || n > 2048) return fail(TT_ERR_INVALID_ARGUMENT, "0 < n <= 2048");
   if (!G || !V || !lam || !workspace) return fail(TT_ERR_NULL_POINTER, "NULL pointer");
   if (workspace_bytes < (size_t)sym_eigen_scratch(n) * 8) return fail(TT_ERR_WORKSPACE, "workspace");
+  g_eigen_elementwise = (g_dbg_flags & 256) ? 1 : 0;
   cudaError_t e = launch_sym_eigen(G, V, lam, (int)n, static_cast<double*>(workspace),
                                    static_cast<cudaStream_t>(stream));
+  g_eigen_elementwise = 0;
   if (e != cudaSuccess) return cuda_fail(e, "tt_debug_sym_eigen");
   return TT_OK;
 }

@@ -123,6 +123,200 @@ __global__ void __launch_bounds__(256) jacobi_coop_kernel(double* __restrict__ G
   if (gt == 0) result_buf[0] = cur;   // which buffer holds the result
 }
 
+// Block Jacobi (cooperative launch): the np x np matrix (np a multiple of 2 BS) is split into
+// 2m blocks of BS indices, paired round-robin.  In each step every pair (P, Q) of blocks is
+// handled by one CTA, which runs one cyclic Jacobi sweep on its 2BS x 2BS diagonal block in
+// shared memory and records the accumulated rotation R_PQ; after a grid barrier every
+// 2BS x 2BS block of G is replaced by R_rows^T G_blk R_cols and every 2BS-row slab of V by
+// V R (each block is owned by one task, so the update is in place); a second barrier ends the
+// step.  2m - 1 steps per sweep: two grid barriers per BS-wide pair instead of one per index
+// pair, i.e. ~BS/2 times fewer barriers than the element-wise kernel above.
+constexpr int kJBS = 16, kJB2 = 2 * kJBS;
+__global__ void __launch_bounds__(256) jacobi_block_coop_kernel(double* __restrict__ G,
+                                                                double* __restrict__ V, int np,
+                                                                int sweeps,
+                                                                double* __restrict__ Rbuf,
+                                                                double* __restrict__ part) {
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  __shared__ double S[kJB2][kJB2 + 1];
+  __shared__ double R[kJB2][kJB2 + 1];
+  __shared__ double T[kJB2][kJB2 + 1];
+  __shared__ double cs[kJBS], sn[kJBS];
+  __shared__ int pp[kJBS], qq[kJBS];
+  __shared__ double red[16];
+  __shared__ int pb[2];
+  const int tid = threadIdx.x, nt = blockDim.x, bid = blockIdx.x, nb = gridDim.x;
+  const int nblk = np / kJBS, m = nblk / 2;
+  const long long gt = (long long)bid * nt + tid, gstride = (long long)nb * nt;
+  const long long NN = (long long)np * np;
+  for (long long e = gt; e < NN; e += gstride) V[e] = (e / np == e % np) ? 1.0 : 0.0;
+  grid.sync();
+  auto pair_of = [&](int k, int step, int& a, int& b) {   // round-robin over nblk blocks
+    a = (k == 0) ? 0 : 1 + (k - 1 + step) % (nblk - 1);
+    b = 1 + (nblk - 2 - k + step) % (nblk - 1);
+    if (a > b) { const int t = a; a = b; b = t; }
+  };
+  for (int sw = 0; sw < sweeps; ++sw) {
+    double off = 0.0, dia = 0.0;
+    for (long long e = gt; e < NN; e += gstride) {
+      const double v = G[e];
+      if (e / np == e % np) dia += v * v; else off += v * v;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      off += __shfl_down_sync(0xffffffffu, off, o);
+      dia += __shfl_down_sync(0xffffffffu, dia, o);
+    }
+    if ((tid & 31) == 0) {
+      red[(tid >> 5) * 2] = off;
+      red[(tid >> 5) * 2 + 1] = dia;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double a = 0.0, b = 0.0;
+      for (int w = 0; w < nt / 32; ++w) {
+        a += red[2 * w];
+        b += red[2 * w + 1];
+      }
+      part[2 * bid] = a;
+      part[2 * bid + 1] = b;
+    }
+    grid.sync();
+    double offs = 0.0, dias = 0.0;
+    for (int c = 0; c < nb; ++c) {
+      offs += part[2 * c];
+      dias += part[2 * c + 1];
+    }
+    grid.sync();
+    if (offs <= 1e-26 * dias) break;
+    for (int step = 0; step < nblk - 1; ++step) {
+      // ---- phase A: one inner Jacobi sweep per block pair -> R_PQ ----
+      for (int k = bid; k < m; k += nb) {
+        if (tid == 0) pair_of(k, step, pb[0], pb[1]);
+        __syncthreads();
+        const int P = pb[0], Q = pb[1];
+        for (int e = tid; e < kJB2 * kJB2; e += nt) {
+          const int i = e / kJB2, j = e % kJB2;
+          const int gi = (i < kJBS ? P * kJBS + i : Q * kJBS + i - kJBS);
+          const int gj = (j < kJBS ? P * kJBS + j : Q * kJBS + j - kJBS);
+          S[i][j] = G[(long long)gi * np + gj];
+          R[i][j] = (i == j) ? 1.0 : 0.0;
+        }
+        __syncthreads();
+        for (int st = 0; st < kJB2 - 1; ++st) {
+          if (tid < kJBS) {
+            int a = (tid == 0) ? 0 : 1 + (tid - 1 + st) % (kJB2 - 1);
+            int b = 1 + (kJB2 - 2 - tid + st) % (kJB2 - 1);
+            if (a > b) { const int t = a; a = b; b = t; }
+            pp[tid] = a;
+            qq[tid] = b;
+            double c = 1.0, sv = 0.0;
+            const double apq = S[a][b], app = S[a][a], aqq = S[b][b];
+            if (fabs(apq) > 1e-300) {
+              const double tau = (aqq - app) / (2.0 * apq);
+              const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+              c = 1.0 / sqrt(1.0 + t * t);
+              sv = t * c;
+            }
+            cs[tid] = c;
+            sn[tid] = sv;
+          }
+          __syncthreads();
+          for (int e = tid; e < kJBS * kJBS; e += nt) {   // 2x2 blocks of J^T S J (in place)
+            const int kr = e / kJBS, kc = e % kJBS;
+            const int p = pp[kr], q = qq[kr], u = pp[kc], w = qq[kc];
+            const double cr = cs[kr], sr = sn[kr], cc = cs[kc], sc = sn[kc];
+            const double mpu = S[p][u], mpw = S[p][w], mqu = S[q][u], mqw = S[q][w];
+            const double rpu = cr * mpu - sr * mqu, rpw = cr * mpw - sr * mqw;
+            const double rqu = sr * mpu + cr * mqu, rqw = sr * mpw + cr * mqw;
+            S[p][u] = cc * rpu - sc * rpw;
+            S[p][w] = sc * rpu + cc * rpw;
+            S[q][u] = cc * rqu - sc * rqw;
+            S[q][w] = sc * rqu + cc * rqw;
+          }
+          for (int e = tid; e < kJB2 * kJBS; e += nt) {   // R <- R J
+            const int i = e / kJBS, kc = e % kJBS;
+            const int u = pp[kc], w = qq[kc];
+            const double ru = R[i][u], rw = R[i][w];
+            R[i][u] = cs[kc] * ru - sn[kc] * rw;
+            R[i][w] = sn[kc] * ru + cs[kc] * rw;
+          }
+          __syncthreads();
+        }
+        double* Rg = Rbuf + (long long)k * kJB2 * kJB2;
+        for (int e = tid; e < kJB2 * kJB2; e += nt) Rg[e] = R[e / kJB2][e % kJB2];
+        __syncthreads();
+      }
+      grid.sync();
+      // ---- phase B: G[PQ, RS] <- R_PQ^T G[PQ, RS] R_RS;  V[rows, PQ] <- V[rows, PQ] R_PQ ----
+      const int gtasks = m * m, vtasks = (np / kJB2) * m;
+      for (int task = bid; task < gtasks + vtasks; task += nb) {
+        const bool isG = task < gtasks;
+        const int t2 = isG ? task : task - gtasks;
+        const int kr = isG ? t2 / m : -1, kc = t2 % m;
+        const int rb = isG ? -1 : t2 / m;   // V row slab
+        if (tid == 0) {
+          int a, b;
+          pair_of(kc, step, a, b);
+          pb[0] = a * 32768 + b;   // column pair
+          if (isG) {
+            pair_of(kr, step, a, b);
+            pb[1] = a * 32768 + b;
+          }
+        }
+        __syncthreads();
+        const int Pc = pb[0] / 32768, Qc = pb[0] % 32768;
+        const int Pr = isG ? pb[1] / 32768 : 0, Qr = isG ? pb[1] % 32768 : 0;
+        const double* Rc = Rbuf + (long long)kc * kJB2 * kJB2;
+        for (int e = tid; e < kJB2 * kJB2; e += nt) {
+          const int i = e / kJB2, j = e % kJB2;
+          const int gj = (j < kJBS ? Pc * kJBS + j : Qc * kJBS + j - kJBS);
+          int gi;
+          if (isG) gi = (i < kJBS ? Pr * kJBS + i : Qr * kJBS + i - kJBS);
+          else gi = rb * kJB2 + i;
+          S[i][j] = isG ? G[(long long)gi * np + gj] : V[(long long)gi * np + gj];
+          R[i][j] = Rc[e];
+        }
+        __syncthreads();
+        // T = S R_cols
+        for (int e = tid; e < kJB2 * kJB2; e += nt) {
+          const int i = e / kJB2, j = e % kJB2;
+          double v = 0.0;
+#pragma unroll 8
+          for (int q = 0; q < kJB2; ++q) v = fma(S[i][q], R[q][j], v);
+          T[i][j] = v;
+        }
+        __syncthreads();
+        if (isG) {   // S = R_rows^T T
+          const double* Rr = Rbuf + (long long)kr * kJB2 * kJB2;
+          for (int e = tid; e < kJB2 * kJB2; e += nt) R[e / kJB2][e % kJB2] = Rr[e];
+          __syncthreads();
+          for (int e = tid; e < kJB2 * kJB2; e += nt) {
+            const int i = e / kJB2, j = e % kJB2;
+            double v = 0.0;
+#pragma unroll 8
+            for (int q = 0; q < kJB2; ++q) v = fma(R[q][i], T[q][j], v);
+            S[i][j] = v;
+          }
+          __syncthreads();
+        }
+        double (*Out)[kJB2 + 1] = isG ? S : T;
+        for (int e = tid; e < kJB2 * kJB2; e += nt) {
+          const int i = e / kJB2, j = e % kJB2;
+          const int gj = (j < kJBS ? Pc * kJBS + j : Qc * kJBS + j - kJBS);
+          if (isG) {
+            const int gi = (i < kJBS ? Pr * kJBS + i : Qr * kJBS + i - kJBS);
+            G[(long long)gi * np + gj] = Out[i][j];
+          } else {
+            V[(long long)(rb * kJB2 + i) * np + gj] = Out[i][j];
+          }
+        }
+        __syncthreads();
+      }
+      grid.sync();
+    }
+  }
+}
+
 // copy an n x n matrix into the top-left of an np x np zero-padded buffer
 __global__ void embed_kernel(const double* __restrict__ G, double* __restrict__ P, int n, int np) {
   const long long NN = (long long)np * np;

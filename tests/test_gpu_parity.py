@@ -527,7 +527,7 @@ def test_tt_round_vs_oracle(tt, case, delta):
     assert np.linalg.norm(vg - v) / np.linalg.norm(v) <= delta * (1 + 1e-6)
 
 
-@pytest.mark.parametrize("n", [1, 2, 7, 64, 129, 256])
+@pytest.mark.parametrize("n", [1, 2, 7, 64, 65, 129, 256, 300, 1024])
 def test_jacobi_eigen_vs_numpy(tt, n):
     rng = np.random.default_rng(n)
     M = rng.standard_normal((n, n))
@@ -539,6 +539,25 @@ def test_jacobi_eigen_vs_numpy(tt, n):
     Vh = h(V)
     assert np.allclose(Vh.T @ Vh, np.eye(n), atol=1e-12)
     assert np.allclose(G @ Vh, Vh * h(lam), atol=1e-10 * ref[0])
+
+
+def test_block_and_elementwise_jacobi_agree(tt):
+    """The block-Jacobi kernel (n > 64) and the element-wise kernel (debug flag 256) give the
+    same spectrum, including exactly repeated and zero eigenvalues."""
+    rng = np.random.default_rng(9)
+    Q = np.linalg.qr(rng.standard_normal((200, 200)))[0]
+    lamv = np.concatenate([np.repeat([5.0, 2.0], 40), rng.uniform(0.1, 1.0, 100), np.zeros(20)])
+    G = (Q * lamv) @ Q.T
+    lb, Vb = tt.tt_debug_sym_eigen(g(G))
+    tt.tt_debug_set_flags(256)
+    le, Ve = tt.tt_debug_sym_eigen(g(G))
+    tt.tt_debug_set_flags(0)
+    torch.cuda.synchronize()
+    ref = np.sort(lamv)[::-1]
+    assert np.allclose(h(lb), ref, atol=1e-12 * 5) and np.allclose(h(le), ref, atol=1e-12 * 5)
+    for V, lam in ((h(Vb), h(lb)), (h(Ve), h(le))):
+        assert np.allclose(V.T @ V, np.eye(200), atol=1e-12)
+        assert np.allclose(G @ V, V * lam, atol=1e-10 * 5)
 
 
 # ----------------------------------------------------------------------------------------
