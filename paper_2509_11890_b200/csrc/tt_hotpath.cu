@@ -1196,7 +1196,7 @@ cudaError_t launch_sym_eigen(const double* G, double* V, double* lam, int n, dou
     const int tasks = m * m + (np / kJB2) * m;
     if (grid > tasks) grid = tasks;
     if (grid > 4096) grid = 4096;
-    int sweeps = 30;
+    int sweeps = 40;
     int npi = np;
     void* args[] = {&G0, &V0, (void*)&npi, &sweeps, &Rbuf, &part};
     e = cudaLaunchCooperativeKernel((const void*)jacobi_block_coop_kernel, grid, 256, args, 0, s);

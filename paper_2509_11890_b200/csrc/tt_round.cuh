@@ -151,6 +151,7 @@ __global__ void __launch_bounds__(256) jacobi_block_coop_kernel(double* __restri
   const long long NN = (long long)np * np;
   for (long long e = gt; e < NN; e += gstride) V[e] = (e / np == e % np) ? 1.0 : 0.0;
   grid.sync();
+  int extra = 0;
   auto pair_of = [&](int k, int step, int& a, int& b) {   // round-robin over nblk blocks
     a = (k == 0) ? 0 : 1 + (k - 1 + step) % (nblk - 1);
     b = 1 + (nblk - 2 - k + step) % (nblk - 1);
@@ -187,7 +188,10 @@ __global__ void __launch_bounds__(256) jacobi_block_coop_kernel(double* __restri
       dias += part[2 * c + 1];
     }
     grid.sync();
-    if (offs <= 1e-26 * dias) break;
+    // below 1e-13 relative off-diagonal mass, two more sweeps: the one-sweep inner solves
+    // converge more slowly than the element-wise kernel, and eigenvectors of eigenvalues
+    // ~1e-6 of the largest need the off-diagonal mass near the rounding floor
+    if (offs <= 1e-26 * dias && ++extra > 2) break;
     for (int step = 0; step < nblk - 1; ++step) {
       // ---- phase A: one inner Jacobi sweep per block pair -> R_PQ ----
       for (int k = bid; k < m; k += nb) {
