@@ -386,7 +386,8 @@ void tt_debug_set_variant(int v);
  * become WRONG; times the main loop / epilogue / load path in isolation); bit 3 computes the
  * right interface update directly instead of as the mirrored left update (same result); bit 4
  * disables the TMA L2 cache-policy hints, bit 5 only the evict_first ones, bit 6 only the
- * evict_last ones (same results). */
+ * evict_last ones, bit 7 issues M/N-contiguous tiles as 2-D boxes, bits 9/10 order the tiles
+ * M-grouped by 8 / M-fastest, bit 8 forces the element-wise Jacobi (same results). */
 void tt_debug_set_flags(int flags);
 
 /* ---------------------------------------------------------------------------------------

@@ -36,6 +36,8 @@ struct GemmParamsV3 {
   IndexMap32 rowmap, colmap;
   int tiles_n, total_units, KT, ksplit, kt_per_split;
   int a3d, b3d;     // MN-contiguous operand described by a 3-D map (one TMA per stage)
+  int tiles_m, group_m;   // tile order: groups of group_m M-tiles, M fastest inside a group
+                          // (group_m = 1: N-fastest rows of tiles)
   int l2_a, l2_b;   // TMA L2 policy per operand: 0 default, 1 evict_last (reused, L2-sized),
                     // 2 evict_first (streamed once, larger than L2)
   int store_mode;   // 0 scalar; 1 column pairs (N-contiguous B, output contiguous along n);
@@ -164,9 +166,20 @@ dmma_gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   auto unit_of = [&](int u, int& m0, int& n0, int& kb, int& ke, int& split) {
     const int tile = u / p.ksplit;
     split = u - tile * p.ksplit;
-    const int tm = tile / p.tiles_n;
+    int tm, tn;
+    if (p.group_m <= 1) {
+      tm = tile / p.tiles_n;
+      tn = tile - tm * p.tiles_n;
+    } else {
+      const int per_group = p.group_m * p.tiles_n;
+      const int grp = tile / per_group, first = grp * p.group_m;
+      const int gsz = min(p.tiles_m - first, p.group_m);
+      const int r = tile - grp * per_group;
+      tm = first + r % gsz;
+      tn = r / gsz;
+    }
     m0 = tm * BM;
-    n0 = (tile - tm * p.tiles_n) * BN;
+    n0 = tn * BN;
     kb = split * p.kt_per_split;
     ke = min(p.KT, kb + p.kt_per_split);
   };
