@@ -49,22 +49,31 @@ thread_local int g_stage = TT_ST_PERM;   // stage tag of the next launch
 struct SideStream {
   int dev = -1;
   cudaStream_t s = nullptr;
+  cudaStream_t s_lo = nullptr;   // same, lowest priority (A/B hook: debug flag 2048)
   cudaEvent_t ev[64] = {};
   unsigned next = 0;
 };
 thread_local SideStream g_side;
+thread_local int g_side_lowprio = 0;
 
 cudaError_t side_stream(cudaStream_t* out) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   if (g_side.dev != dev) {
-    if ((e = cudaStreamCreateWithFlags(&g_side.s, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    // the side stream carries the interface chains, the sweeps' critical path: give it the
+    // highest priority so its small GEMMs are scheduled ahead of the concurrent matvecs
+    int lo = 0, hi = 0;
+    if ((e = cudaDeviceGetStreamPriorityRange(&lo, &hi)) != cudaSuccess) return e;
+    if ((e = cudaStreamCreateWithPriority(&g_side.s, cudaStreamNonBlocking, hi)) != cudaSuccess)
+      return e;
+    if ((e = cudaStreamCreateWithPriority(&g_side.s_lo, cudaStreamNonBlocking, lo)) != cudaSuccess)
+      return e;
     for (auto& ev : g_side.ev)
       if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return e;
     g_side.dev = dev;
   }
-  *out = g_side.s;
+  *out = g_side_lowprio ? g_side.s_lo : g_side.s;
   return cudaSuccess;
 }
 // `to` waits for all work enqueued on `from` so far (graph-capture compatible)
@@ -80,6 +89,7 @@ constexpr int kPoolStreams = 4;
 struct StreamPool {
   int dev = -1;
   cudaStream_t s[kPoolStreams] = {};
+  cudaStream_t chain = nullptr;   // high priority (the W34 left chain)
   std::vector<cudaEvent_t> ev;
 };
 thread_local StreamPool g_pool;
@@ -88,8 +98,12 @@ cudaError_t pool_init(size_t nevents) {
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   if (g_pool.dev != dev) {
+    int lo = 0, hi = 0;
+    if ((e = cudaDeviceGetStreamPriorityRange(&lo, &hi)) != cudaSuccess) return e;
     for (auto& st : g_pool.s)
-      if ((e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)) != cudaSuccess) return e;
+      if ((e = cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, lo)) != cudaSuccess) return e;
+    if ((e = cudaStreamCreateWithPriority(&g_pool.chain, cudaStreamNonBlocking, hi)) != cudaSuccess)
+      return e;
     g_pool.ev.clear();
     g_pool.dev = dev;
   }
@@ -1342,7 +1356,10 @@ const char* tt_version(void) { return "tt_hotpath 0.1 (sm_100a, FP64 DMMA)"; }
 int64_t tt_last_launch_count(void) { return g_launches_last; }
 void tt_debug_force_v1(int on) { g_force_v1 = on; }
 void tt_debug_set_variant(int v) { g_variant = v; }
-void tt_debug_set_flags(int f) { g_dbg_flags = f; }
+void tt_debug_set_flags(int f) {
+  g_dbg_flags = f;
+  g_side_lowprio = (f & 2048) ? 1 : 0;
+}
 
 size_t tt_local_matvec_workspace_size(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t Rr,
                                       int64_t nvec) {
@@ -1767,14 +1784,16 @@ tt_status tt_sweep_w34(int64_t d, const int64_t* n, const int64_t* r, const int6
   if ((e = stream_dep(s, sr)) != cudaSuccess) return cuda_fail(e, "fork");
   for (int q = 0; q < kPoolStreams; ++q)
     if ((e = stream_dep(s, g_pool.s[q])) != cudaSuccess) return cuda_fail(e, "fork");
-  // the two chains
-  if ((e = launch_set_one(phiL[0], s)) != cudaSuccess) return cuda_fail(e, "sweep");
-  if ((e = cudaEventRecord(evL[0], s)) != cudaSuccess) return cuda_fail(e, "event");
+  // the two chains, on high-priority streams (the critical path)
+  cudaStream_t sl = g_pool.chain;
+  if ((e = stream_dep(s, sl)) != cudaSuccess) return cuda_fail(e, "fork");
+  if ((e = launch_set_one(phiL[0], sl)) != cudaSuccess) return cuda_fail(e, "sweep");
+  if ((e = cudaEventRecord(evL[0], sl)) != cudaSuccess) return cuda_fail(e, "event");
   for (int64_t k = 0; k < d; ++k) {
     if ((e = sweep_left_step(k, d, 0, ws_main, n, r, R, x_cores, A_cores, phiL, workspace, main_b,
-                             s)) != cudaSuccess)
+                             sl)) != cudaSuccess)
       return cuda_fail(e, "sweep left");
-    if ((e = cudaEventRecord(evL[k + 1], s)) != cudaSuccess) return cuda_fail(e, "event");
+    if ((e = cudaEventRecord(evL[k + 1], sl)) != cudaSuccess) return cuda_fail(e, "event");
   }
   if ((e = launch_set_one(phiR[d], sr)) != cudaSuccess) return cuda_fail(e, "sweep");
   if ((e = cudaEventRecord(evR[d], sr)) != cudaSuccess) return cuda_fail(e, "event");
@@ -1812,6 +1831,9 @@ tt_status tt_sweep_w34(int64_t d, const int64_t* n, const int64_t* r, const int6
   }
   // join everything back into the caller's stream
   if ((e = cudaEventRecord(evJ[0], sr)) != cudaSuccess || (e = cudaStreamWaitEvent(s, evJ[0], 0)) != cudaSuccess)
+    return cuda_fail(e, "join");
+  if ((e = cudaEventRecord(evJ[1 + kPoolStreams], sl)) != cudaSuccess ||
+      (e = cudaStreamWaitEvent(s, evJ[1 + kPoolStreams], 0)) != cudaSuccess)
     return cuda_fail(e, "join");
   for (int q = 0; q < kPoolStreams; ++q)
     if ((e = cudaEventRecord(evJ[1 + q], g_pool.s[q])) != cudaSuccess ||

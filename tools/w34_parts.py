@@ -64,4 +64,7 @@ for idx in [int(a) for a in (sys.argv[1:] or ["3", "4"])]:
     res = {name: graph_ms(f) for name, f in (("both_chains", chains), ("left_chain", left),
                                              ("matvecs", mvs), ("w34", w34),
                                              ("w34_dag", w34_dag))}
+    tt.tt_debug_set_flags(2048)   # chains at the lowest priority (A/B)
+    res["w34_dag_lowprio_side"] = graph_ms(w34_dag)
+    tt.tt_debug_set_flags(0)
     print(f"config {idx}: " + "  ".join(f"{k} {v:.3f} ms" for k, v in res.items()), flush=True)
