@@ -26,6 +26,12 @@
 // Included by tt_hotpath.cu inside its anonymous namespace.
 
 constexpr int kLobMaxNb = 32;
+// Cholesky pivot floor of the equilibrated Gram matrix (squared norm of the new direction a
+// column adds): below it the Rayleigh-Ritz step restarts without P / falls back to SVQB
+#ifndef TT_LOB_PIVOT
+#define TT_LOB_PIVOT 1e-4
+#endif
+constexpr double kLobPivot = TT_LOB_PIVOT;
 constexpr int kLobMaxS = 3 * kLobMaxNb;   // Rayleigh-Ritz basis [X W P]
 
 struct LobDims {
@@ -419,15 +425,19 @@ __global__ void __launch_bounds__(256) lob_rr_kernel(const double* __restrict__ 
   // pivot below 1e-8 fall back to the eigen-decomposition G_B' = U mu U^T, T = U mu^{-1/2},
   // dropping mu <= 1e-12 mu_max (SVQB).  Zero columns (D = 0) are excluded either way.
   __shared__ int chol_ok;
-  if (tid == 0) {
-    int k = 0;
-    for (int i = 0; i < s; ++i)
-      if (Dg[i] > 0.0) keep[k++] = i;
-    k_sh = k;
-    chol_ok = 1;
-  }
-  __syncthreads();
-  {
+  // attempt 0 on [X W P]; if G_B is too ill-conditioned for the Cholesky pivot test and P is
+  // present, attempt 1 restarts without P (its columns get Dg = 0: excluded everywhere below,
+  // so its Ritz coefficients are zero) -- the classical LOBPCG restart, which keeps runs past
+  // convergence from drifting (nb = 32 on a 192-dimensional problem otherwise diverges)
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    if (tid == 0) {
+      int k = 0;
+      for (int i = 0; i < s; ++i)
+        if (Dg[i] > 0.0) keep[k++] = i;
+      k_sh = k;
+      chol_ok = 1;
+    }
+    __syncthreads();
     const int kc = k_sh;
     // compacted equilibrated G_B over the nonzero columns -> M0 (kc x kc, ld np)
     for (int e = tid; e < kc * kc; e += nt) {
@@ -438,7 +448,7 @@ __global__ void __launch_bounds__(256) lob_rr_kernel(const double* __restrict__ 
     for (int c = 0; c < kc; ++c) {   // right-looking Cholesky, lower triangle in place
       if (tid == 0) {
         const double d = M0[c * np + c];
-        if (!(d > 1e-8)) chol_ok = 0;
+        if (!(d > kLobPivot)) chol_ok = 0;
         M0[c * np + c] = d > 0.0 ? sqrt(d) : 1.0;
       }
       __syncthreads();
@@ -466,7 +476,11 @@ __global__ void __launch_bounds__(256) lob_rr_kernel(const double* __restrict__ 
           M1[i * np + j] = v;
         }
       }
+      break;
     }
+    if (s <= 2 * nb) break;
+    for (int i = 2 * nb + tid; i < s; i += nt) Dg[i] = 0.0;   // restart without P
+    __syncthreads();
   }
   __syncthreads();
   int k, kp;

@@ -260,3 +260,20 @@ def test_lobpcg_errors(tt):
     assert lib.tt_local_lobpcg(*args((None, None, None), need - 1)) == 4            # WORKSPACE
     assert lib.tt_local_lobpcg(*args((None, None, None), need)) == 0
     torch.cuda.synchronize()
+
+
+def test_lobpcg_max_block(tt):
+    """nb = 32 (the largest block): Rayleigh-Ritz on s = 96 columns in one CTA."""
+    rng, mixed, A, _ = step_system(59, d=8, rE=12)
+    k = 4
+    phiL, phiR = local_triplets(mixed, A, k)
+    op = (phiL, A[k], phiR)
+    rl, rr = phiL.shape[0], phiR.shape[0]
+    nb = 32
+    X0 = rng.standard_normal((rl, 2, nb, rr))
+    X, lam, res, its, step = tt.tt_local_lobpcg(tuple(g(t) for t in op), g(X0), maxiter=400,
+                                                tol=1e-10)
+    torch.cuda.synchronize()
+    ref, _ = local_geneig(op, None, nb)
+    assert np.allclose(h(lam), ref, rtol=0, atol=1e-9 * np.abs(ref).max())
+    check_pairs(local_operator_dense(*op), None, block_columns(h(X)), h(lam), 1e-9)
