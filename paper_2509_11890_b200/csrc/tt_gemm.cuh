@@ -48,6 +48,17 @@ struct GemmParams {
   const int* gate;   // optional device flag: nonzero -> the launch is a no-op (iterative solvers)
 };
 
+// Programmatic dependent launch (PDL).  Every kernel the library may launch with the
+// programmatic-serialisation attribute waits for its stream predecessor here, before its
+// first global-memory access (read or write) and before any early return, so completion stays
+// transitive along the stream; it then lets its own successor be launched, whose CTAs run
+// their prologue (barrier init, descriptor prefetch) on SMs this grid leaves idle.
+// Both instructions are no-ops for a normal launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+
 __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool ok) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
   const int sz = ok ? 8 : 0;
@@ -83,6 +94,8 @@ struct GemmCfg {
 template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool A_KC, bool B_KC>
 __global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, 1)
 dmma_gemm_kernel(const GemmParams p) {
+  pdl_wait();
+  pdl_trigger();
   if (p.gate && *p.gate) return;
   using Cfg = GemmCfg<BM, BN, BK, WARPS_M, WARPS_N, STAGES, A_KC, B_KC>;
   constexpr int NT = Cfg::kThreads;

@@ -119,6 +119,8 @@ struct GemmV2Cfg {
 template <bool A_KC, bool B_KC, int BM_, int BN, int WARPS_M, int WARPS_N, int STAGES, int MINB>
 __global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, MINB)
 dmma_gemm_v2_kernel(const GemmParamsV2 p) {
+  pdl_wait();
+  pdl_trigger();
   if (p.gate && *p.gate) return;
   using Cfg = GemmV2Cfg<A_KC, B_KC, BM_, BN, WARPS_M, WARPS_N, STAGES, MINB>;
   constexpr int BM = Cfg::BM, BK = Cfg::BK, NT = Cfg::kThreads;
@@ -360,6 +362,8 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const double* __rest
                                                             int ksplit, IndexMap32 rowmap,
                                                             IndexMap32 colmap,
                                                             const int* gate) {
+  pdl_wait();
+  pdl_trigger();
   if (gate && *gate) return;
   const long long MN = (long long)M * N;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < MN;

@@ -138,7 +138,6 @@ template <bool A_KC, bool B_KC, int BM, int BN, int WARPS_M, int WARPS_N, int ST
 __global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, MINB)
 dmma_gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const GemmParamsV3 p) {
-  if (p.gate && *p.gate) return;
   using Cfg = GemmV3Cfg<A_KC, B_KC, BM, BN, WARPS_M, WARPS_N, STAGES, MINB>;
   constexpr int WTM = Cfg::WTM, WTN = Cfg::WTN, MI = Cfg::MI, NI = Cfg::NI;
   constexpr int A_BYTES = Cfg::A_BYTES, STAGE_BYTES = Cfg::STAGE_BYTES;
@@ -160,8 +159,14 @@ dmma_gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
   }
   __syncthreads();
+  // PDL: the barrier setup above overlaps the predecessor's tail (tt_gemm.cuh)
+  pdl_wait();
+  pdl_trigger();
+  if (p.gate && *p.gate) return;
 
   auto unit_of = [&](int u, int& m0, int& n0, int& kb, int& ke, int& split) {
     const int tile = u / p.ksplit;

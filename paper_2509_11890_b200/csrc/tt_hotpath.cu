@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/tt_hotpath.h"
@@ -182,6 +183,28 @@ size_t ws_bytes(std::initializer_list<long long> elems) {
   return s;
 }
 
+thread_local int g_dbg_flags = 0;   // tt_debug_set_flags (bits listed in the header)
+
+// Launch with programmatic stream serialisation (PDL, tt_gemm.cuh pdl_wait/pdl_trigger): the
+// kernel may be scheduled while its stream predecessor drains and waits for it on the device.
+// Only kernels that call pdl_wait() before touching global memory are launched this way.
+// Debug flag 4096 restores plain launches (A/B).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (g_dbg_flags & 4096) ? 0 : 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // ----------------------------------------------------------------------------------------
 // GEMM launch: tile configuration chosen from the stage's N extent
 // ----------------------------------------------------------------------------------------
@@ -202,7 +225,8 @@ cudaError_t launch_cfg(const GemmParams& p0, cudaStream_t s) {
   const long long tiles = tm * p.tiles_n;
   if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
   const long long tr = trace_begin(BN, p.M, p.N, p.K, s);
-  kern<<<(unsigned)tiles, Cfg::kThreads, Cfg::kSmemBytes, s>>>(p);
+  if (cudaError_t e = launch_pdl(kern, dim3((unsigned)tiles), dim3(Cfg::kThreads), Cfg::kSmemBytes, s, p))
+    return e;
   trace_end(tr, s);
   ++g_launches;
   return cudaGetLastError();
@@ -234,10 +258,10 @@ int num_sms() {
 }
 
 thread_local int g_variant = -1;
+thread_local int g_force_ks = 0;   // probe hook: split-K factor forced by tt_debug_set_variant
 // device flag gating every GEMM launch of the calling thread (set by the iterative solvers
 // around their matvecs so that iterations after convergence cost launches only)
 thread_local const int* g_gate = nullptr;
-thread_local int g_dbg_flags = 0;   // tt_debug_set_flags   // test/benchmark hook (tt_debug_set_variant); -1 = auto
 
 // split-K scratch for the current stage (set by the stage planners; nullptr = no split)
 thread_local double* g_pscratch = nullptr;
@@ -298,19 +322,24 @@ cudaError_t launch_v2_cfg(const GemmParams& p0, cudaStream_t s) {
       ks = cand;
     }
   }
+  // no empty K-split: the unit stream assumes every unit has at least one k-tile
+  ks = (p.KT + (p.KT + ks - 1) / ks - 1) / ((p.KT + ks - 1) / ks);
   p.ksplit = ks;
   p.kt_per_split = (p.KT + ks - 1) / ks;
   p.total_units = (int)(tiles * ks);
   if (ks > 1) p.P = g_pscratch;
   const int grid = (int)std::min<long long>((long long)p.total_units, slots);
   const long long tr = trace_begin(BN + 1000 * ks, p0.M, p0.N, p0.K, s);
-  kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes, s>>>(p);
+  if (cudaError_t e = launch_pdl(kern, dim3(grid), dim3(Cfg::kThreads), Cfg::kSmemBytes, s, p))
+    return e;
   if (ks > 1) {
     const long long mn = p0.M * p0.N;
     long long blocks = (mn + 255) / 256;
     if (blocks > 8L * num_sms()) blocks = 8L * num_sms();
-    tt::splitk_reduce_kernel<<<(unsigned)blocks, 256, 0, s>>>(p.P, p.C, p.M, p.N, ks, p.rowmap,
-                                                              p.colmap, p.gate);
+    if (cudaError_t e = launch_pdl(tt::splitk_reduce_kernel, dim3((unsigned)blocks), dim3(256), 0,
+                                   s, (const double*)p.P, p.C, p.M, p.N, ks, p.rowmap, p.colmap,
+                                   p.gate))
+      return e;
     ++g_launches;
   }
   trace_end(tr, s);
@@ -408,7 +437,7 @@ int store_mode(bool a_kc, bool b_kc, const GemmParams& p) {
 template <bool AK, bool BK_, int BM, int BN, int WM, int WN, int MINB>
 cudaError_t launch_v3_cfg(const GemmParams& p0, cudaStream_t s, bool& ok) {
   using Probe = tt::GemmV3Cfg<AK, BK_, BM, BN, WM, WN, 1, MINB>;
-  constexpr size_t budget = (MINB == 1 ? 224 : 110) * 1024 - 1024;
+  constexpr size_t budget = (MINB == 1 ? 224 : MINB == 2 ? 110 : 54) * 1024 - 1024;
   constexpr int ST0 = (int)(budget / Probe::STAGE_BYTES);
   constexpr int ST = ST0 > 6 ? 6 : ST0;
   static_assert(ST >= 2, "shared memory budget");
@@ -489,7 +518,12 @@ cudaError_t launch_v3_cfg(const GemmParams& p0, cudaStream_t s, bool& ok) {
   // Big stages rarely split (only to fix wave quantisation); skinny ones (few output tiles,
   // long K — e.g. config 4's last matvec stage, 4 tiles x 200 k-tiles) split up to 64 ways.
   int ks = 1;
-  {
+  if (g_force_ks > 0) {   // probe hook (tt_debug_set_variant >= 100)
+    ks = g_force_ks;
+    while (ks > 1 && (p.KT < ks || g_pscratch == nullptr ||
+                      (long long)ks * p0.M * p0.N > g_pscratch_elems))
+      --ks;
+  } else {
     const double ktile_s = 2.0 * BM * BN * Cfg::BK / (37.0e12 / (double)slots);
     double best_t = 1e30;
     for (int cand = 1; cand <= 64; ++cand) {
@@ -507,19 +541,24 @@ cudaError_t launch_v3_cfg(const GemmParams& p0, cudaStream_t s, bool& ok) {
       }
     }
   }
+  // no empty K-split: the unit stream assumes every unit has at least one k-tile
+  ks = (p.KT + (p.KT + ks - 1) / ks - 1) / ((p.KT + ks - 1) / ks);
   p.ksplit = ks;
   p.kt_per_split = (p.KT + ks - 1) / ks;
   p.total_units = (int)(tiles * ks);
   if (ks > 1) p.P = g_pscratch;
   const int grid = (int)std::min<long long>((long long)p.total_units, slots);
   const long long tr = trace_begin(BN + 1000 * ks + 100000, p0.M, p0.N, p0.K, s);
-  kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes, s>>>(ta, tb, p);
+  if (cudaError_t e = launch_pdl(kern, dim3(grid), dim3(Cfg::kThreads), Cfg::kSmemBytes, s, ta, tb, p))
+    return e;
   if (ks > 1) {
     const long long mn = p0.M * p0.N;
     long long blocks = (mn + 255) / 256;
     if (blocks > 8L * num_sms()) blocks = 8L * num_sms();
-    tt::splitk_reduce_kernel<<<(unsigned)blocks, 256, 0, s>>>(p.P, p.C, p.M, p.N, ks, p.rowmap,
-                                                              p.colmap, p.gate);
+    if (cudaError_t e = launch_pdl(tt::splitk_reduce_kernel, dim3((unsigned)blocks), dim3(256), 0,
+                                   s, (const double*)p.P, p.C, p.M, p.N, ks, p.rowmap, p.colmap,
+                                   p.gate))
+      return e;
     ++g_launches;
   }
   trace_end(tr, s);
@@ -527,8 +566,111 @@ cudaError_t launch_v3_cfg(const GemmParams& p0, cudaStream_t s, bool& ok) {
   return cudaGetLastError();
 }
 
+// ---- latency policy for small stage GEMMs (configs 3/4, boundary cores) -------------------
+// A stage of a few tens of MFLOP is bound by how many SMs it occupies (one SM retires
+// 37.2 TF / 148 = 251 GFLOP/s of DMMA), not by tile efficiency: config 3's interior left-update
+// stages (~34 MFLOP) ran as 32-64 CTAs of 128 x 64.  For GEMMs below kLatencyFlops the tile
+// configuration and split-K factor are chosen by a small model over a candidate list:
+//   t = ceil(units / SMs) x k-tiles per unit x 2 BM BN 16 / (251 GF/s x eff x occ)
+//       + split-K reduction (reads ks M N, writes M N doubles) + a fixed 3 us if ks > 1,
+// eff = the configuration's measured fraction of peak at scale (tools/stage_probe.py, config-5
+// interior shapes) and occ the warp-occupancy factor of a sparsely filled SM (a DMMA blocks
+// its warp ~16 cycles; fewer than 2 warps per sub-partition leave the pipe idle).
+// Debug flag 8192 disables it (A/B).
+struct TileCand {
+  int id, bm, bn, warps, minb;
+  double eff;
+};
+constexpr double kLatencyFlops = 1.5e9;
+constexpr TileCand kLatencyCands[] = {
+    {10, 128, 64, 8, 2, 0.90}, {11, 64, 64, 8, 2, 0.83}, {12, 64, 64, 4, 4, 0.85},
+    {13, 64, 32, 4, 4, 0.82},  {14, 32, 64, 4, 4, 0.82}, {15, 32, 32, 4, 4, 0.75},
+    {16, 64, 112, 8, 2, 0.80}, {21, 64, 144, 8, 2, 0.85}, {17, 64, 48, 8, 2, 0.78},
+};
+
+double latency_estimate(const TileCand& c, long long M, long long N, long long K, int ks) {
+  const long long sms = num_sms();
+  const long long tiles = ((M + c.bm - 1) / c.bm) * ((N + c.bn - 1) / c.bn);
+  const long long KT = (K + 15) / 16;
+  const long long kper = (KT + ks - 1) / ks;
+  const long long units = tiles * ks;
+  const long long grid = std::min<long long>(units, sms * c.minb);
+  const long long per_sm = (units + sms - 1) / sms;
+  const long long ctas_per_sm = std::min<long long>(c.minb, (grid + sms - 1) / sms);
+  const long long w = ctas_per_sm * c.warps;
+  const double occ = w >= 12 ? 1.0 : w >= 8 ? 0.9 : w >= 4 ? 0.6 : 0.35;
+  double t = (double)per_sm * (double)kper * 2.0 * c.bm * c.bn * 16.0 / (251.0e9 * c.eff * occ);
+  if (ks > 1) t += (double)(ks + 1) * M * N * 8.0 / 5.0e12 + 3.0e-6;
+  return t;
+}
+
+// best (candidate index, ks) for a small GEMM, or -1 when the stage is not small
+int latency_choice(const GemmParams& p, bool a_kc, bool b_kc, int& ks_out) {
+  if (g_dbg_flags & 8192) return -1;
+  if (2.0 * p.M * p.N * p.K > kLatencyFlops) return -1;
+  double best = 1e30;
+  int bi = -1;
+  const long long KT = (p.K + 15) / 16;
+  for (int i = 0; i < (int)(sizeof(kLatencyCands) / sizeof(kLatencyCands[0])); ++i) {
+    const TileCand& c = kLatencyCands[i];
+    (void)a_kc; (void)b_kc;   // every candidate's BM, BN are multiples of 16 (any operand layout)
+    for (int ks = 1; ks <= 16; ks *= 2) {
+      if (ks > 1 && (KT < 2 * ks || g_pscratch == nullptr || (long long)ks * p.M * p.N > g_pscratch_elems))
+        break;
+      const double t = latency_estimate(c, p.M, p.N, p.K, ks);
+      if (t < best * 0.97) {
+        best = t;
+        bi = i;
+        ks_out = ks;
+      }
+    }
+  }
+  return bi;
+}
+
 template <bool AK, bool BK_>
 cudaError_t launch_v3_l(const GemmParams& p, cudaStream_t s, bool& ok) {
+  {
+    int ks = 1;
+    const int li = g_variant < 0 ? latency_choice(p, AK, BK_, ks) : -1;
+    if (li >= 0) {
+      struct KsScope {   // the planned split-K factor, for this launch only
+        int saved;
+        explicit KsScope(int k) : saved(g_force_ks) { g_force_ks = k; }
+        ~KsScope() { g_force_ks = saved; }
+      } ks_scope(ks);
+      switch (kLatencyCands[li].id) {
+        case 10: return launch_v3_cfg<AK, BK_, 128, 64, 4, 2, 2>(p, s, ok);
+        case 11: return launch_v3_cfg<AK, BK_, 64, 64, 4, 2, 2>(p, s, ok);
+        case 12: return launch_v3_cfg<AK, BK_, 64, 64, 2, 2, 4>(p, s, ok);
+        case 13: return launch_v3_cfg<AK, BK_, 64, 32, 2, 2, 4>(p, s, ok);
+        case 14: return launch_v3_cfg<AK, BK_, 32, 64, 2, 2, 4>(p, s, ok);
+        case 15: return launch_v3_cfg<AK, BK_, 32, 32, 2, 2, 4>(p, s, ok);
+        case 16: return launch_v3_cfg<AK, BK_, 64, 112, 8, 1, 2>(p, s, ok);
+        case 17: return launch_v3_cfg<AK, BK_, 64, 48, 8, 1, 2>(p, s, ok);
+        case 21: return launch_v3_cfg<AK, BK_, 64, 144, 4, 2, 2>(p, s, ok);
+        default: break;
+      }
+    }
+  }
+  if (g_variant >= 10) {   // probe hook: forced tile configuration (variant % 100)
+    switch (g_variant % 100) {
+      case 10: return launch_v3_cfg<AK, BK_, 128, 64, 4, 2, 2>(p, s, ok);
+      case 11: return launch_v3_cfg<AK, BK_, 64, 64, 4, 2, 2>(p, s, ok);
+      case 12: return launch_v3_cfg<AK, BK_, 64, 64, 2, 2, 4>(p, s, ok);
+      case 13: return launch_v3_cfg<AK, BK_, 64, 32, 2, 2, 4>(p, s, ok);
+      case 14: return launch_v3_cfg<AK, BK_, 32, 64, 2, 2, 4>(p, s, ok);
+      case 15: return launch_v3_cfg<AK, BK_, 32, 32, 2, 2, 4>(p, s, ok);
+      case 16: return launch_v3_cfg<AK, BK_, 64, 112, 8, 1, 2>(p, s, ok);
+      case 17: return launch_v3_cfg<AK, BK_, 64, 48, 8, 1, 2>(p, s, ok);
+      case 18: return launch_v3_cfg<AK, BK_, 128, 128, 4, 4, 1>(p, s, ok);
+      case 19: return launch_v3_cfg<AK, BK_, 64, 128, 2, 4, 2>(p, s, ok);
+      case 20: return launch_v3_cfg<AK, BK_, 128, 32, 4, 2, 2>(p, s, ok);
+      case 21: return launch_v3_cfg<AK, BK_, 64, 144, 4, 2, 2>(p, s, ok);
+      case 22: return launch_v3_cfg<AK, BK_, 32, 112, 2, 2, 4>(p, s, ok);
+      default: break;
+    }
+  }
   if (g_variant == 4) {   // all two-CTA tiles (previous default), kept for comparison
     if (p.N <= 16) return launch_v3_cfg<AK, BK_, 64, 16, 8, 1, 2>(p, s, ok);
     if (p.N <= 48) return launch_v3_cfg<AK, BK_, 64, 48, 8, 1, 2>(p, s, ok);
@@ -652,7 +794,6 @@ __global__ void perm_right_kernel(const double* __restrict__ A, double* __restri
   }
 }
 
-__global__ void set_one_kernel(double* p) { *p = 1.0; }
 
 // xt[b, j, a] = x[a, j, b]: 32x32 shared-memory tiles per mode index j (coalesced both ways)
 __global__ void transpose_core_kernel(const double* __restrict__ x, double* __restrict__ xt,
@@ -671,16 +812,42 @@ __global__ void transpose_core_kernel(const double* __restrict__ x, double* __re
   }
 }
 
-// Per-core operand preparation for a sweep (one launch per core, reused by every stage
-// of every pass): Ahl[(al,j),(i,be)] = A[al,i,j,be] (matvec / left update),
-// Ahr[(be,j),(i,al)] = A[al,i,j,be] (mirrored right update), xt[b,j,a] = x[a,j,b].
-__global__ void prep_core_kernel(const double* __restrict__ A, const double* __restrict__ x,
-                                 double* __restrict__ Ahl, double* __restrict__ Ahr,
-                                 double* __restrict__ xt, long long al_n, long long n,
-                                 long long be_n, long long a_n, long long b_n) {
+// All cores of a sweep prepared by ONE launch (a dependent launch costs ~4 us on the
+// critical path of the small-rank sweeps): block range [start[c], start[c+1]) works on core c;
+// the first block also writes the trivial boundary interfaces when given.
+constexpr int kPrepMax = 40;
+struct PrepTable {
+  const double* A[kPrepMax];
+  const double* x[kPrepMax];
+  double* Ahl[kPrepMax];
+  double* Ahr[kPrepMax];
+  double* xt[kPrepMax];
+  int al[kPrepMax], n[kPrepMax], be[kPrepMax], a[kPrepMax], b[kPrepMax];
+  int start[kPrepMax + 1];
+  int cores;
+  double* one0;
+  double* one1;
+};
+
+__global__ void __launch_bounds__(256) prep_all_kernel(const __grid_constant__ PrepTable t) {
+  tt::pdl_wait();
+  tt::pdl_trigger();
+  int c = 0;
+  while (c + 1 < t.cores && (int)blockIdx.x >= t.start[c + 1]) ++c;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (t.one0) *t.one0 = 1.0;
+    if (t.one1) *t.one1 = 1.0;
+  }
+  const long long al_n = t.al[c], n = t.n[c], be_n = t.be[c], a_n = t.a[c], b_n = t.b[c];
+  const double* __restrict__ A = t.A[c];
+  const double* __restrict__ x = t.x[c];
+  double* __restrict__ Ahl = t.Ahl[c];
+  double* __restrict__ Ahr = t.Ahr[c];
+  double* __restrict__ xt = t.xt[c];
   const long long tA = al_n * n * n * be_n, tx = a_n * n * b_n;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tA + tx;
-       e += (long long)gridDim.x * blockDim.x) {
+  const long long nb = t.start[c + 1] - t.start[c];
+  for (long long e = (blockIdx.x - t.start[c]) * (long long)blockDim.x + threadIdx.x; e < tA + tx;
+       e += nb * blockDim.x) {
     if (e < tA) {
       long long r = e;
       const long long be = r % be_n; r /= be_n;
@@ -691,7 +858,7 @@ __global__ void prep_core_kernel(const double* __restrict__ A, const double* __r
       Ahl[(al * n + j) * (n * be_n) + i * be_n + be] = v;
       Ahr[(be * n + j) * (n * al_n) + i * al_n + al] = v;
     } else {
-      const long long f = e - tA;   // f = (a * n + j) * b_n + b
+      const long long f = e - tA;
       const long long b = f % b_n, r = f / b_n;
       const long long j = r % n, a = r / n;
       xt[(b * n + j) * a_n + a] = x[f];
@@ -730,14 +897,6 @@ cudaError_t launch_perm(bool left, const double* A, double* out, long long al, l
   return cudaGetLastError();
 }
 
-cudaError_t launch_set_one(double* p, cudaStream_t s) {
-  g_stage = TT_ST_SET;
-  const long long tr = trace_begin(0, 1, 0, 0, s);
-  set_one_kernel<<<1, 1, 0, s>>>(p);
-  trace_end(tr, s);
-  ++g_launches;
-  return cudaGetLastError();
-}
 
 // H8: z[(a,al), i, (b,be)] = sum_j A[al,i,j,be] x[a,j,b].  One CTA per (a, al) pair; the
 // x[a,:,:] and A[al,:,:,:] slices are staged in shared memory; the output rows (one per i,
@@ -1355,7 +1514,10 @@ const char* tt_last_error_message(void) { return g_msg.c_str(); }
 const char* tt_version(void) { return "tt_hotpath 0.1 (sm_100a, FP64 DMMA)"; }
 int64_t tt_last_launch_count(void) { return g_launches_last; }
 void tt_debug_force_v1(int on) { g_force_v1 = on; }
-void tt_debug_set_variant(int v) { g_variant = v; }
+void tt_debug_set_variant(int v) {
+  g_variant = v;
+  g_force_ks = v >= 10 ? v / 100 : 0;
+}
 void tt_debug_set_flags(int f) {
   g_dbg_flags = f;
   g_side_lowprio = (f & 2048) ? 1 : 0;
@@ -1527,20 +1689,38 @@ static Prep prep_ptrs(int64_t k, int64_t d, const int64_t* n, const int64_t* r, 
   }
   return Prep{nullptr, nullptr, nullptr};
 }
+// one launch per kPrepMax cores (all of them in practice); one0/one1 (nullable) are set to 1
 static cudaError_t launch_prep(int64_t d, const int64_t* n, const int64_t* r, const int64_t* R,
                                int64_t nvec, const double* const* xc, const double* const* Ac,
-                               void* ws, cudaStream_t s) {
-  for (int64_t k = 0; k < d; ++k) {
-    Dims dk{r[k], n[k], r[k + 1], R[k], R[k + 1]};
-    Prep pp = prep_ptrs(k, d, n, r, R, nvec, ws);
-    const long long total = prep_elems(dk);
-    long long blocks = (total + 255) / 256;
-    if (blocks > 2048) blocks = 2048;
+                               void* ws, cudaStream_t s, double* one0 = nullptr,
+                               double* one1 = nullptr) {
+  for (int64_t k0 = 0; k0 < d; k0 += kPrepMax) {
+    PrepTable t;
+    t.cores = (int)std::min<int64_t>(kPrepMax, d - k0);
+    t.one0 = k0 == 0 ? one0 : nullptr;
+    t.one1 = k0 == 0 ? one1 : nullptr;
+    long long blocks = 0, total = 0;
+    for (int c = 0; c < t.cores; ++c) {
+      const int64_t k = k0 + c;
+      Dims dk{r[k], n[k], r[k + 1], R[k], R[k + 1]};
+      Prep pp = prep_ptrs(k, d, n, r, R, nvec, ws);
+      t.A[c] = Ac[k];
+      t.x[c] = xc[k];
+      t.Ahl[c] = const_cast<double*>(pp.Ahl);
+      t.Ahr[c] = const_cast<double*>(pp.Ahr);
+      t.xt[c] = const_cast<double*>(pp.xt);
+      t.al[c] = (int)dk.al; t.n[c] = (int)dk.n; t.be[c] = (int)dk.be;
+      t.a[c] = (int)dk.a; t.b[c] = (int)dk.b;
+      const long long el = prep_elems(dk);
+      total += el;
+      t.start[c] = (int)blocks;
+      blocks += std::min<long long>(2048, (el + 255) / 256);
+    }
+    t.start[t.cores] = (int)blocks;
     g_stage = TT_ST_PERM;
     const long long tr = trace_begin(0, total, 0, 0, s);
-    prep_core_kernel<<<(unsigned)blocks, 256, 0, s>>>(
-        Ac[k], xc[k], const_cast<double*>(pp.Ahl), const_cast<double*>(pp.Ahr),
-        const_cast<double*>(pp.xt), dk.al, dk.n, dk.be, dk.a, dk.b);
+    if (cudaError_t e = launch_pdl(prep_all_kernel, dim3((unsigned)blocks), dim3(256), 0, s, t))
+      return e;
     trace_end(tr, s);
     ++g_launches;
     cudaError_t e = cudaGetLastError();
@@ -1695,7 +1875,8 @@ tt_status tt_sweep_interfaces(int64_t d, const int64_t* n, const int64_t* r, con
   const size_t main_b = sweep_step_ws(d, n, r, R, 0);
   void* ws_main = wsb;
   void* ws_side = wsb + align_up(main_b, 256);
-  if ((doL || doR) && (e = launch_prep(d, n, r, R, 0, x_cores, A_cores, workspace, s)) != cudaSuccess)
+  if ((doL || doR) && (e = launch_prep(d, n, r, R, 0, x_cores, A_cores, workspace, s,
+                                      doL ? phiL[0] : nullptr, doR ? phiR[d] : nullptr)) != cudaSuccess)
     return cuda_fail(e, "sweep prep");
   // the two chains are independent: left on the caller's stream, right on the side stream
   cudaStream_t sr = s;
@@ -1704,7 +1885,6 @@ tt_status tt_sweep_interfaces(int64_t d, const int64_t* n, const int64_t* r, con
     if ((e = stream_dep(s, sr)) != cudaSuccess) return cuda_fail(e, "fork");
   }
   if (doL) {
-    if ((e = launch_set_one(phiL[0], s)) != cudaSuccess) return cuda_fail(e, "sweep");
     for (int64_t k = 0; k < d; ++k)
       if ((e = sweep_left_step(k, d, 0, ws_main, n, r, R, x_cores, A_cores, phiL, workspace,
                                main_b, s)) != cudaSuccess)
@@ -1712,7 +1892,6 @@ tt_status tt_sweep_interfaces(int64_t d, const int64_t* n, const int64_t* r, con
   }
   if (doR) {
     void* wr = (sr == s) ? ws_main : ws_side;
-    if ((e = launch_set_one(phiR[d], sr)) != cudaSuccess) return cuda_fail(e, "sweep");
     for (int64_t k = d - 1; k >= 0; --k)
       if ((e = sweep_right_step(k, d, 0, wr, n, r, R, x_cores, A_cores, phiR, workspace, main_b,
                                 sr)) != cudaSuccess)
@@ -1777,7 +1956,7 @@ tt_status tt_sweep_w34(int64_t d, const int64_t* n, const int64_t* r, const int6
   cudaEvent_t* evL = g_pool.ev.data();         // evL[k]: phiL[k] ready
   cudaEvent_t* evR = evL + (d + 1);            // evR[k]: phiR[k] ready
   cudaEvent_t* evJ = evR + (d + 1);            // joins
-  if ((e = launch_prep(d, n, r, R, 0, x_cores, A_cores, workspace, s)) != cudaSuccess)
+  if ((e = launch_prep(d, n, r, R, 0, x_cores, A_cores, workspace, s, phiL[0], phiR[d])) != cudaSuccess)
     return cuda_fail(e, "sweep prep");
   cudaStream_t sr;
   if ((e = side_stream(&sr)) != cudaSuccess) return cuda_fail(e, "side stream");
@@ -1787,7 +1966,6 @@ tt_status tt_sweep_w34(int64_t d, const int64_t* n, const int64_t* r, const int6
   // the two chains, on high-priority streams (the critical path)
   cudaStream_t sl = g_pool.chain;
   if ((e = stream_dep(s, sl)) != cudaSuccess) return cuda_fail(e, "fork");
-  if ((e = launch_set_one(phiL[0], sl)) != cudaSuccess) return cuda_fail(e, "sweep");
   if ((e = cudaEventRecord(evL[0], sl)) != cudaSuccess) return cuda_fail(e, "event");
   for (int64_t k = 0; k < d; ++k) {
     if ((e = sweep_left_step(k, d, 0, ws_main, n, r, R, x_cores, A_cores, phiL, workspace, main_b,
@@ -1795,7 +1973,6 @@ tt_status tt_sweep_w34(int64_t d, const int64_t* n, const int64_t* r, const int6
       return cuda_fail(e, "sweep left");
     if ((e = cudaEventRecord(evL[k + 1], sl)) != cudaSuccess) return cuda_fail(e, "event");
   }
-  if ((e = launch_set_one(phiR[d], sr)) != cudaSuccess) return cuda_fail(e, "sweep");
   if ((e = cudaEventRecord(evR[d], sr)) != cudaSuccess) return cuda_fail(e, "event");
   for (int64_t k = d - 1; k >= 0; --k) {
     if ((e = sweep_right_step(k, d, 0, ws_side, n, r, R, x_cores, A_cores, phiR, workspace,
@@ -1877,10 +2054,9 @@ tt_status tt_sweep_als(int64_t d, const int64_t* n, const int64_t* r, const int6
   void* ws_side = wsb + align_up(main_b, 256);
   cudaStream_t ss;
   if ((e = side_stream(&ss)) != cudaSuccess) return cuda_fail(e, "side stream");
-  if ((e = launch_prep(d, n, r, R, nvec, x_cores, A_cores, workspace, s)) != cudaSuccess)
+  if ((e = launch_prep(d, n, r, R, nvec, x_cores, A_cores, workspace, s, phiL[0], phiR[d])) !=
+      cudaSuccess)
     return cuda_fail(e, "als prep");
-  if ((e = launch_set_one(phiL[0], s)) != cudaSuccess) return cuda_fail(e, "als");
-  if ((e = launch_set_one(phiR[d], s)) != cudaSuccess) return cuda_fail(e, "als");
   for (int64_t k = d - 1; k >= 1; --k)
     if ((e = sweep_right_step(k, d, nvec, ws_main, n, r, R, x_cores, A_cores, phiR, workspace,
                               main_b, s)) != cudaSuccess)

@@ -639,3 +639,55 @@ def test_local_gmres_converged_cycle_is_gated(tt):
                                         tol=1e-8)
     assert np.array_equal(h(it1), ito)
     assert rel(h(X1), Xo) <= 1e-9
+
+
+# Every tile configuration of the v3 engine the latency policy (or a probe) can select, with
+# forced split-K factors that leave ragged K ranges (KT = 25 k-tiles split 3 / 8 / 16 ways):
+# interface update + single-vector matvec vs the oracle.  Guards the 4-warp / 4-CTA-per-SM
+# configurations and the no-empty-split clamp of the split-K planner.
+@pytest.mark.timeout(120)
+@pytest.mark.parametrize("cfg", list(range(10, 23)))
+@pytest.mark.parametrize("ks", [1, 3, 8, 16])
+def test_forced_tile_configs(tt, cfg, ks):
+    import oracle
+    rl, n, rr, Rl, Rr = 100, 4, 36, 5, 7     # S1 K = 100, S3' K = rl*n = 400 (25 k-tiles)
+    rng = np.random.default_rng(cfg * 100 + ks)
+    phiL = rng.standard_normal((rl, Rl, rl))
+    A = rng.standard_normal((Rl, n, n, Rr))
+    phiR = rng.standard_normal((rr, Rr, rr))
+    x = rng.standard_normal((rl, n, rr))
+    tt.tt_debug_set_variant(cfg + 100 * ks)
+    try:
+        out = tt.tt_interface_left(g(phiL), g(A), g(x))
+        y = tt.tt_local_matvec(g(phiL), g(A), g(phiR), g(x))
+        torch.cuda.synchronize()
+    finally:
+        tt.tt_debug_set_variant(-1)
+    assert rel(h(out), oracle.interface_left(phiL, A, x)) <= TOL
+    assert rel(h(y), oracle.local_matvec(phiL, A, phiR, x)) <= TOL
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("idx", [3, 4])
+def test_latency_policy_w34_vs_default_policy(tt, idx):
+    """The small-GEMM latency policy (tile + split-K model) against the default tile policy
+    (debug flag 8192) on the config-3/4 W34 DAG: same interfaces and matvecs (<= 1e-11)."""
+    import ttgen
+    inp = ttgen.make_inputs(idx)
+    x = [g(c) for c in inp.x]
+    A = [g(c) for c in inp.A]
+    outs = []
+    for flags in (0, 8192):
+        tt.tt_debug_set_flags(flags)
+        try:
+            pl, pr = tt.alloc_interfaces(x, A), tt.alloc_interfaces(x, A)
+            y = [torch.empty_like(c) for c in x]
+            tr = tt._Train(x, A)
+            ws = torch.empty(tt.tt_sweep_w34_workspace_size(tr), dtype=torch.uint8, device="cuda")
+            tt.tt_sweep_w34(x, A, pl, pr, y, workspace=ws)
+            torch.cuda.synchronize()
+        finally:
+            tt.tt_debug_set_flags(0)
+        outs.append([h(t) for t in pl + pr + y])
+    for a, b in zip(*outs):
+        assert rel(a, b) <= TOL

@@ -66,5 +66,11 @@ for idx in [int(a) for a in (sys.argv[1:] or ["3", "4"])]:
                                              ("w34_dag", w34_dag))}
     tt.tt_debug_set_flags(2048)   # chains at the lowest priority (A/B)
     res["w34_dag_lowprio_side"] = graph_ms(w34_dag)
+    tt.tt_debug_set_flags(4096)   # plain launches instead of PDL (A/B)
+    res["w34_dag_no_pdl"] = graph_ms(w34_dag)
+    res["left_chain_no_pdl"] = graph_ms(left)
+    tt.tt_debug_set_flags(8192)   # default tile policy for small GEMMs (A/B)
+    res["w34_dag_no_latency_tiles"] = graph_ms(w34_dag)
+    res["left_chain_no_latency_tiles"] = graph_ms(left)
     tt.tt_debug_set_flags(0)
     print(f"config {idx}: " + "  ".join(f"{k} {v:.3f} ms" for k, v in res.items()), flush=True)
