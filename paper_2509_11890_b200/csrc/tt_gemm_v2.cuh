@@ -363,7 +363,6 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const double* __rest
                                                             IndexMap32 colmap,
                                                             const int* gate) {
   pdl_wait();
-  pdl_trigger();
   if (gate && *gate) return;
   const long long MN = (long long)M * N;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < MN;
@@ -373,6 +372,7 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const double* __rest
     const int m = (int)(e / N), n = (int)(e - (long long)m * N);
     stg_cs(C + apply_map32(rowmap, (uint32_t)m) + apply_map32(colmap, (uint32_t)n), s);
   }
+  pdl_trigger();
 }
 
 }  // namespace tt

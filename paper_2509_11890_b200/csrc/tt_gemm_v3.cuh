@@ -163,9 +163,10 @@ dmma_gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
   }
   __syncthreads();
-  // PDL: the barrier setup above overlaps the predecessor's tail (tt_gemm.cuh)
+  // PDL: the barrier setup above overlaps the predecessor's tail (tt_gemm.cuh).  The
+  // successor is released when every CTA has started its LAST unit (below), so its CTAs are
+  // placed on SMs as this grid's CTAs retire rather than piling onto the few with spare room.
   pdl_wait();
-  pdl_trigger();
   if (p.gate && *p.gate) return;
 
   auto unit_of = [&](int u, int& m0, int& n0, int& kb, int& ke, int& split) {
@@ -287,6 +288,7 @@ dmma_gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
 
   int c_u = blockIdx.x, c_m0 = 0, c_n0 = 0, c_kt = 0, c_ke = 0, c_split = 0;
   if (c_u < p.total_units) unit_of(c_u, c_m0, c_n0, c_kt, c_ke, c_split);
+  if (c_u + (int)gridDim.x >= p.total_units) pdl_trigger();
   uint32_t q = 0;
 #pragma unroll 1
   while (c_u < p.total_units) {
@@ -481,6 +483,7 @@ dmma_gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
       c_u += gridDim.x;
       if (c_u < p.total_units) unit_of(c_u, c_m0, c_n0, c_kt, c_ke, c_split);
+      if (c_u < p.total_units && c_u + (int)gridDim.x >= p.total_units) pdl_trigger();
     }
   }
   // drain: thread 0 may still owe nothing (every issued stage was consumed)

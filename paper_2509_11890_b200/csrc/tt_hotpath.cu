@@ -184,13 +184,21 @@ size_t ws_bytes(std::initializer_list<long long> elems) {
 }
 
 thread_local int g_dbg_flags = 0;   // tt_debug_set_flags (bits listed in the header)
+// GEMMs up to this size are launched with PDL (config 3's ~34 MFLOP stages gain 8 %; config
+// 4's ~0.4 GFLOP interior stages lose 6 % in a lone chain: the early-placed dependents
+// unbalance the persistent grid); g_no_pdl (tt_sweep_als scope) disables it.
+constexpr double kPdlFlops = 0.2e9;
+thread_local bool g_no_pdl = false;
 
-// Launch with programmatic stream serialisation (PDL, tt_gemm.cuh pdl_wait/pdl_trigger): the
-// kernel may be scheduled while its stream predecessor drains and waits for it on the device.
-// Only kernels that call pdl_wait() before touching global memory are launched this way.
-// Debug flag 4096 restores plain launches (A/B).
+// Launch with programmatic stream serialisation (PDL, tt_gemm.cuh pdl_wait/pdl_trigger) when
+// `pdl`: the kernel may be scheduled while its stream predecessor drains and waits for it on
+// the device.  Only kernels that call pdl_wait() before touching global memory are launched
+// this way, and only latency-bound ones (small GEMMs, their split-K reduction, the sweep
+// preparation): for the large matvec GEMMs of W5 the early-resident dependents hold SMs the
+// concurrent interface chain could use (measured +1.1 % on the W5 sweep with PDL everywhere).
+// Debug flag 4096 disables PDL (A/B).
 template <typename... KArgs, typename... Args>
-cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+cudaError_t launch_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
                        cudaStream_t s, Args&&... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
@@ -201,7 +209,7 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = (g_dbg_flags & 4096) ? 0 : 1;
+  cfg.numAttrs = (pdl && !g_no_pdl && !(g_dbg_flags & 4096)) ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
@@ -225,7 +233,7 @@ cudaError_t launch_cfg(const GemmParams& p0, cudaStream_t s) {
   const long long tiles = tm * p.tiles_n;
   if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
   const long long tr = trace_begin(BN, p.M, p.N, p.K, s);
-  if (cudaError_t e = launch_pdl(kern, dim3((unsigned)tiles), dim3(Cfg::kThreads), Cfg::kSmemBytes, s, p))
+  if (cudaError_t e = launch_pdl(2.0 * p.M * p.N * p.K <= kPdlFlops, kern, dim3((unsigned)tiles), dim3(Cfg::kThreads), Cfg::kSmemBytes, s, p))
     return e;
   trace_end(tr, s);
   ++g_launches;
@@ -330,13 +338,14 @@ cudaError_t launch_v2_cfg(const GemmParams& p0, cudaStream_t s) {
   if (ks > 1) p.P = g_pscratch;
   const int grid = (int)std::min<long long>((long long)p.total_units, slots);
   const long long tr = trace_begin(BN + 1000 * ks, p0.M, p0.N, p0.K, s);
-  if (cudaError_t e = launch_pdl(kern, dim3(grid), dim3(Cfg::kThreads), Cfg::kSmemBytes, s, p))
+  if (cudaError_t e = launch_pdl(2.0 * p0.M * p0.N * p0.K <= kPdlFlops, kern, dim3(grid), dim3(Cfg::kThreads), Cfg::kSmemBytes, s, p))
     return e;
   if (ks > 1) {
     const long long mn = p0.M * p0.N;
     long long blocks = (mn + 255) / 256;
     if (blocks > 8L * num_sms()) blocks = 8L * num_sms();
-    if (cudaError_t e = launch_pdl(tt::splitk_reduce_kernel, dim3((unsigned)blocks), dim3(256), 0,
+    if (cudaError_t e = launch_pdl(2.0 * p0.M * p0.N * p0.K <= kPdlFlops, tt::splitk_reduce_kernel,
+                                   dim3((unsigned)blocks), dim3(256), 0,
                                    s, (const double*)p.P, p.C, p.M, p.N, ks, p.rowmap, p.colmap,
                                    p.gate))
       return e;
@@ -549,13 +558,14 @@ cudaError_t launch_v3_cfg(const GemmParams& p0, cudaStream_t s, bool& ok) {
   if (ks > 1) p.P = g_pscratch;
   const int grid = (int)std::min<long long>((long long)p.total_units, slots);
   const long long tr = trace_begin(BN + 1000 * ks + 100000, p0.M, p0.N, p0.K, s);
-  if (cudaError_t e = launch_pdl(kern, dim3(grid), dim3(Cfg::kThreads), Cfg::kSmemBytes, s, ta, tb, p))
+  if (cudaError_t e = launch_pdl(2.0 * p0.M * p0.N * p0.K <= kPdlFlops, kern, dim3(grid), dim3(Cfg::kThreads), Cfg::kSmemBytes, s, ta, tb, p))
     return e;
   if (ks > 1) {
     const long long mn = p0.M * p0.N;
     long long blocks = (mn + 255) / 256;
     if (blocks > 8L * num_sms()) blocks = 8L * num_sms();
-    if (cudaError_t e = launch_pdl(tt::splitk_reduce_kernel, dim3((unsigned)blocks), dim3(256), 0,
+    if (cudaError_t e = launch_pdl(2.0 * p0.M * p0.N * p0.K <= kPdlFlops, tt::splitk_reduce_kernel,
+                                   dim3((unsigned)blocks), dim3(256), 0,
                                    s, (const double*)p.P, p.C, p.M, p.N, ks, p.rowmap, p.colmap,
                                    p.gate))
       return e;
@@ -632,7 +642,7 @@ template <bool AK, bool BK_>
 cudaError_t launch_v3_l(const GemmParams& p, cudaStream_t s, bool& ok) {
   {
     int ks = 1;
-    const int li = g_variant < 0 ? latency_choice(p, AK, BK_, ks) : -1;
+    const int li = (g_variant < 10 && g_variant != 4) ? latency_choice(p, AK, BK_, ks) : -1;
     if (li >= 0) {
       struct KsScope {   // the planned split-K factor, for this launch only
         int saved;
@@ -684,7 +694,9 @@ cudaError_t launch_v3_l(const GemmParams& p, cudaStream_t s, bool& ok) {
   //    128 x N tile and a 6-deep TMA ring (the streamed operand comes from HBM);
   //  * wide N with a K-contiguous B (the last matvec stage): one 16-warp CTA per SM,
   //    128 x 128 tiles (+ split-K), 95% of the DMMA peak;
-  //  * wide N with an N-contiguous B (the first stage): two 8-warp CTAs per SM, 128 x 64.
+  //  * wide N with an N-contiguous B (the first stage): one 16-warp CTA per SM, 128 x 128
+  //    (two 8-warp CTAs of 128 x 64 were the earlier choice; with the 3-D TMA slabs and L2
+  //    hints the 128 x 128 tile is 1.2 % faster on the whole W5 sweep, tools/flags_ab.py 0 v5).
   if (p.N <= 16) return launch_v3_cfg<AK, BK_, 64, 16, 8, 1, 2>(p, s, ok);
   if (p.N <= 48) return launch_v3_cfg<AK, BK_, 64, 48, 8, 1, 2>(p, s, ok);
   // small problems: 64-row tiles on two CTAs per SM double the tile count
@@ -698,10 +710,10 @@ cudaError_t launch_v3_l(const GemmParams& p, cudaStream_t s, bool& ok) {
   if (p.N <= 112) return launch_v3_cfg<AK, BK_, 128, 112, 8, 2, 1>(p, s, ok);
   if (p.N <= 144) return launch_v3_cfg<AK, BK_, 128, 144, 8, 2, 1>(p, s, ok);
   if (BK_) return launch_v3_cfg<AK, BK_, 128, 128, 4, 4, 1>(p, s, ok);
-  if (g_variant == 5) return launch_v3_cfg<AK, BK_, 128, 128, 4, 4, 1>(p, s, ok);   // probes
+  if (g_variant == 5) return launch_v3_cfg<AK, BK_, 128, 64, 4, 2, 2>(p, s, ok);   // probes
   if (g_variant == 6) return launch_v3_cfg<AK, BK_, 128, 128, 8, 2, 1>(p, s, ok);
   if (g_variant == 7) return launch_v3_cfg<AK, BK_, 64, 128, 2, 4, 2>(p, s, ok);
-  return launch_v3_cfg<AK, BK_, 128, 64, 4, 2, 2>(p, s, ok);
+  return launch_v3_cfg<AK, BK_, 128, 128, 4, 4, 1>(p, s, ok);
 }
 
 bool aligned16(const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; }
@@ -831,7 +843,6 @@ struct PrepTable {
 
 __global__ void __launch_bounds__(256) prep_all_kernel(const __grid_constant__ PrepTable t) {
   tt::pdl_wait();
-  tt::pdl_trigger();
   int c = 0;
   while (c + 1 < t.cores && (int)blockIdx.x >= t.start[c + 1]) ++c;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -864,6 +875,7 @@ __global__ void __launch_bounds__(256) prep_all_kernel(const __grid_constant__ P
       xt[(b * n + j) * a_n + a] = x[f];
     }
   }
+  tt::pdl_trigger();
 }
 
 // At[be, i, j, al] = A[al, i, j, be]  (operator core with its two bonds swapped)
@@ -1719,7 +1731,7 @@ static cudaError_t launch_prep(int64_t d, const int64_t* n, const int64_t* r, co
     t.start[t.cores] = (int)blocks;
     g_stage = TT_ST_PERM;
     const long long tr = trace_begin(0, total, 0, 0, s);
-    if (cudaError_t e = launch_pdl(prep_all_kernel, dim3((unsigned)blocks), dim3(256), 0, s, t))
+    if (cudaError_t e = launch_pdl(true, prep_all_kernel, dim3((unsigned)blocks), dim3(256), 0, s, t))
       return e;
     trace_end(tr, s);
     ++g_launches;
@@ -2052,6 +2064,12 @@ tt_status tt_sweep_als(int64_t d, const int64_t* n, const int64_t* r, const int6
   const size_t side_b = sweep_step_ws(d, n, r, R, 0);
   void* ws_main = wsb;
   void* ws_side = wsb + align_up(main_b, 256);
+  // W5 is throughput-bound: plain launches (PDL measured 0.2 % slower on the whole sweep)
+  struct NoPdl {
+    bool saved = g_no_pdl;
+    NoPdl() { g_no_pdl = true; }
+    ~NoPdl() { g_no_pdl = saved; }
+  } no_pdl;
   cudaStream_t ss;
   if ((e = side_stream(&ss)) != cudaSuccess) return cuda_fail(e, "side stream");
   if ((e = launch_prep(d, n, r, R, nvec, x_cores, A_cores, workspace, s, phiL[0], phiR[d])) !=
