@@ -387,7 +387,11 @@ void tt_debug_set_variant(int v);
  * right interface update directly instead of as the mirrored left update (same result); bit 4
  * disables the TMA L2 cache-policy hints, bit 5 only the evict_first ones, bit 6 only the
  * evict_last ones, bit 7 issues M/N-contiguous tiles as 2-D boxes, bits 9/10 order the tiles
- * M-grouped by 8 / M-fastest, bit 8 forces the element-wise Jacobi (same results). */
+ * M-grouped by 8 / M-fastest, bit 8 forces the element-wise Jacobi (same results), bit 11
+ * runs the W34 interface chains at the lowest stream priority, bit 12 disables programmatic
+ * dependent launch, bit 13 the small-GEMM latency tile policy, bit 14 the one-k-tile warp skew
+ * of the 16-warp GEMM tiles (bit 15: two k-tiles).  tt_debug_set_variant(v): v >= 10 forces
+ * the GEMM tile configuration v % 100 (probe list in tt_hotpath.cu) and split-K factor v / 100. */
 void tt_debug_set_flags(int flags);
 
 /* ---------------------------------------------------------------------------------------

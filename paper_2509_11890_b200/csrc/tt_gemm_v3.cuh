@@ -43,6 +43,7 @@ struct GemmParamsV3 {
   int store_mode;   // 0 scalar; 1 column pairs (N-contiguous B, output contiguous along n);
                     // 2 row pairs (M-contiguous A, output contiguous along m) -> 16-byte stores
   int dbg;
+  int skew;         // k-tiles by which the second half of the warps trails the first (0 = off)
   const int* gate;  // optional device flag: nonzero -> no-op
 };
 
@@ -247,9 +248,17 @@ dmma_gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       if (ps[0] < p.total_units) unit_of(ps[0], ps[1], ps[2], ps[3], ps[4], ps[5]);
     }
   };
+  // Warp skew: when every warp reaches a unit's epilogue at once, the DMMA pipe idles for the
+  // epilogue's duration (S1 / S2 of the matvec switch units every 9-16 k-tiles).  With skew L
+  // the second half of the warps starts L k-tiles after the first (named barrier 1), so the two
+  // halves' epilogues fall on each other's DMMA stream; the producer then runs only
+  // STAGES-1-L k-tiles ahead so that refilling a stage never waits for the trailing half.
+  const int skew = p.skew;
+  const bool trail = skew > 0 && warp >= Cfg::kWarps / 2;
   if (tid == 0) {
-    for (int s = 0; s < STAGES - 1; ++s) produce_one();
+    for (int s = 0; s < STAGES - 1 - skew; ++s) produce_one();
   }
+  if (trail) asm volatile("bar.sync 1, %0;\n" ::"r"(Cfg::kThreads) : "memory");
 
   // ---- fragment geometry ---------------------------------------------------------------
   auto frag_row = [&](int i) -> int {   // tile row of fragment i, lane group g
@@ -360,6 +369,8 @@ dmma_gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     if (tid == 0) produce_one();
     __syncwarp();
     ++q;
+    if (skew > 0 && !trail && q == (uint32_t)skew)
+      asm volatile("bar.arrive 1, %0;\n" ::"r"(Cfg::kThreads) : "memory");
 
     if (++c_kt == c_ke) {
       // ---- epilogue of unit c_u (registers -> global) --------------------------------
@@ -486,6 +497,8 @@ dmma_gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       if (c_u < p.total_units && c_u + (int)gridDim.x >= p.total_units) pdl_trigger();
     }
   }
+  if (skew > 0 && !trail && q < (uint32_t)skew)   // fewer k-tiles than the skew: release
+    asm volatile("bar.arrive 1, %0;\n" ::"r"(Cfg::kThreads) : "memory");
   // drain: thread 0 may still owe nothing (every issued stage was consumed)
 }
 

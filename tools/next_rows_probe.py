@@ -1,5 +1,5 @@
 """One run of a NEXT-row workload at the config-5 interior-core size, for ncu launch lists
-(python tools/next_rows_probe.py gmres|lobpcg|kkt|round|w34)."""
+(python tools/next_rows_probe.py gmres|lobpcg|kkt|round|w34 [config])."""
 import os
 import sys
 
@@ -32,7 +32,7 @@ elif what == "round":
     inp = ttgen.make_inputs(5, with_block=False)
     tt.tt_round([torch.from_numpy(c).to(dev) for c in inp.x], 1e-4)
 elif what == "w34":
-    inp = ttgen.make_inputs(4)
+    inp = ttgen.make_inputs(int(sys.argv[2]) if len(sys.argv) > 2 else 4)
     tt.tt_sweep_w34([torch.from_numpy(c).to(dev) for c in inp.x],
                     [torch.from_numpy(c).to(dev) for c in inp.A])
 torch.cuda.synchronize()
