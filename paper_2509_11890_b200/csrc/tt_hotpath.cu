@@ -267,21 +267,6 @@ int num_sms() {
 }
 
 thread_local int g_variant = -1;
-// SM budget of the GEMM planner on this thread (0 = the whole GPU): two concurrent interface
-// chains each size their persistent grids for half the SMs instead of queueing their CTAs
-// behind each other (SmBudget scope in the sweeps; debug flag 65536 disables it)
-thread_local int g_sm_budget = 0;
-int plan_sms() {
-  const int n = num_sms();
-  return (g_sm_budget > 0 && g_sm_budget < n) ? g_sm_budget : n;
-}
-struct SmBudget {
-  int saved;
-  explicit SmBudget(int b) : saved(g_sm_budget) {
-    if (!(g_dbg_flags & 65536)) g_sm_budget = b;
-  }
-  ~SmBudget() { g_sm_budget = saved; }
-};
 thread_local int g_force_ks = 0;   // probe hook: split-K factor forced by tt_debug_set_variant
 // device flag gating every GEMM launch of the calling thread (set by the iterative solvers
 // around their matvecs so that iterations after convergence cost launches only)
@@ -541,7 +526,7 @@ cudaError_t launch_v3_cfg(const GemmParams& p0, cudaStream_t s, bool& ok) {
   p.tiles_m = (int)tm;
   p.group_m = (g_dbg_flags & 512) ? 8 : (g_dbg_flags & 1024) ? (int)tm : 1;
   p.KT = (int)((p0.K + Cfg::BK - 1) / Cfg::BK);
-  const long long slots = (long long)plan_sms() * MINB;
+  const long long slots = (long long)num_sms() * MINB;
   // Split-K choice from a small cost model: GEMM time = waves x (k-tiles per unit) x
   // (k-tile time), plus the deterministic reduction (reads ks*M*N, writes M*N doubles).
   // Big stages rarely split (only to fix wave quantisation); skinny ones (few output tiles,
@@ -619,7 +604,7 @@ constexpr TileCand kLatencyCands[] = {
 };
 
 double latency_estimate(const TileCand& c, long long M, long long N, long long K, int ks) {
-  const long long sms = plan_sms();
+  const long long sms = num_sms();
   const long long tiles = ((M + c.bm - 1) / c.bm) * ((N + c.bn - 1) / c.bn);
   const long long KT = (K + 15) / 16;
   const long long kper = (KT + ks - 1) / ks;
@@ -1916,7 +1901,6 @@ tt_status tt_sweep_interfaces(int64_t d, const int64_t* n, const int64_t* r, con
     if ((e = side_stream(&sr)) != cudaSuccess) return cuda_fail(e, "side stream");
     if ((e = stream_dep(s, sr)) != cudaSuccess) return cuda_fail(e, "fork");
   }
-  SmBudget half(doL && doR ? num_sms() / 2 : 0);   // concurrent chains share the GPU
   if (doL) {
     for (int64_t k = 0; k < d; ++k)
       if ((e = sweep_left_step(k, d, 0, ws_main, n, r, R, x_cores, A_cores, phiL, workspace,
@@ -2000,7 +1984,6 @@ tt_status tt_sweep_w34(int64_t d, const int64_t* n, const int64_t* r, const int6
   cudaStream_t sl = g_pool.chain;
   if ((e = stream_dep(s, sl)) != cudaSuccess) return cuda_fail(e, "fork");
   if ((e = cudaEventRecord(evL[0], sl)) != cudaSuccess) return cuda_fail(e, "event");
-  std::unique_ptr<SmBudget> half(new SmBudget(num_sms() / 2));   // the two chains share the GPU
   for (int64_t k = 0; k < d; ++k) {
     if ((e = sweep_left_step(k, d, 0, ws_main, n, r, R, x_cores, A_cores, phiL, workspace, main_b,
                              sl)) != cudaSuccess)
@@ -2014,7 +1997,6 @@ tt_status tt_sweep_w34(int64_t d, const int64_t* n, const int64_t* r, const int6
       return cuda_fail(e, "sweep right");
     if ((e = cudaEventRecord(evR[k], sr)) != cudaSuccess) return cuda_fail(e, "event");
   }
-  half.reset();
   // matvecs in readiness order (core k needs k left steps and d-1-k right steps)
   std::vector<int64_t> order(d);
   for (int64_t k = 0; k < d; ++k) order[k] = k;
