@@ -176,8 +176,9 @@ struct GramArgs {
 template <int TU, int TV, int IU, int JV>
 struct GramCfg {
   static constexpr int G = 256 / (TU * TV), KB = 32, LD = KB + 1;
+  // two staging buffers (cp.async double buffering), reused for the group reduction
   static size_t smem(int su, int sv) {
-    const size_t stage = (size_t)(su + sv) * LD, red = G > 1 ? (size_t)G * su * sv : 0;
+    const size_t stage = 2 * (size_t)(su + sv) * LD, red = G > 1 ? (size_t)G * su * sv : 0;
     return sizeof(double) * std::max(stage, red) + sizeof(long long) * (KB + su + sv);
   }
 };
@@ -190,14 +191,11 @@ __global__ void __launch_bounds__(256) lob_gram_kernel(const GramArgs g, double*
   extern __shared__ double gsm[];
   const int su = g.nu * g.nb, sv = g.nv * g.nb;
   const size_t stage = (size_t)(su + sv) * LD, redsz = G > 1 ? (size_t)G * su * sv : 0;
-  const size_t dbl = stage > redsz ? stage : redsz;
-  double* Us = gsm;              // [su][LD]
-  double* Vs = gsm + su * LD;    // [sv][LD]
-  long long* koff = reinterpret_cast<long long*>(gsm + dbl);   // [KB] element offsets
+  const size_t dbl = 2 * stage > redsz ? 2 * stage : redsz;
+  long long* koff = reinterpret_cast<long long*>(gsm + dbl);   // (unused slot kept for layout)
   const double** rptr = reinterpret_cast<const double**>(koff + KB);   // [su + sv] columns
   const int tid = threadIdx.x, grp = tid / (TU * TV), t2 = tid - grp * (TU * TV);
   const int tu = t2 % TU, tv = t2 / TU;
-  // column r of the staged operand: block pointer index and in-block column offset
   if (tid == 0) {   // column r of the staged operands: its block's base + column offset
     for (int r = 0; r < su + sv; ++r) {
       const int q = (r < su ? r : r - su) / g.nb, p = (r < su ? r : r - su) - q * g.nb;
@@ -207,6 +205,7 @@ __global__ void __launch_bounds__(256) lob_gram_kernel(const GramArgs g, double*
       rptr[r] = base + (long long)p * g.rr;
     }
   }
+  __syncthreads();
   double acc[IU][JV];
 #pragma unroll
   for (int i = 0; i < IU; ++i)
@@ -214,19 +213,32 @@ __global__ void __launch_bounds__(256) lob_gram_kernel(const GramArgs g, double*
     for (int j = 0; j < JV; ++j) acc[i][j] = 0.0;
   const long long k0 = blockIdx.x * g.k_per_chunk;
   const long long k1 = min(g.kt, k0 + g.k_per_chunk);
-  for (long long kb = k0; kb < k1; kb += KB) {
-    if (tid < KB) {
-      const long long k = kb + tid;
-      koff[tid] = k < k1 ? (k / g.rr) * g.nb * g.rr + (k % g.rr) : -1;
+  // Chunk kb -> staging buffer: every thread always stages contraction index bb = tid % 32 of
+  // columns r = tid / 32 + 8 i (coalesced 256-byte runs along the b index), by 8-byte
+  // cp.async with zero fill past k1; the next chunk's copies fly while this one is reduced.
+  const int bb_t = tid & 31, r_t = tid >> 5;
+  auto stage_chunk = [&](long long kb, double* buf) {
+    const long long k = kb + bb_t;
+    const bool in = k < k1;
+    const long long off = in ? (k / g.rr) * (long long)g.nb * g.rr + (k % g.rr) : 0;
+    for (int r = r_t; r < su + sv; r += 8) {
+      double* dst = (r < su ? buf + r * LD : buf + su * LD + (r - su) * LD) + bb_t;
+      tt::cp_async8(dst, rptr[r] + off, in);
+    }
+    tt::cp_async_commit();
+  };
+  if (k0 < k1) stage_chunk(k0, gsm);
+  int cur = 0;
+  for (long long kb = k0; kb < k1; kb += KB, cur ^= 1) {
+    if (kb + KB < k1) {
+      stage_chunk(kb + KB, gsm + (cur ^ 1) * stage);
+      tt::cp_async_wait<1>();
+    } else {
+      tt::cp_async_wait<0>();
     }
     __syncthreads();
-    for (int idx = tid; idx < (su + sv) * KB; idx += 256) {
-      const int r = idx >> 5, bb = idx & 31;
-      const long long off = koff[bb];
-      const double v = off >= 0 ? rptr[r][off] : 0.0;
-      (r < su ? Us + r * LD : Vs + (r - su) * LD)[bb] = v;
-    }
-    __syncthreads();
+    const double* Us = gsm + cur * stage;
+    const double* Vs = Us + su * LD;
 #pragma unroll 2
     for (int bb = grp; bb < KB; bb += G) {
       double u[IU], v[JV];
@@ -266,14 +278,17 @@ __global__ void __launch_bounds__(256) lob_gram_kernel(const GramArgs g, double*
 }
 
 // G[e] = sum_c part[c][e]  (fixed order: deterministic)
+// One warp per entry: lane l sums chunks l, l + 32, ... and the 32 partials are combined by a
+// fixed shuffle tree (the summation order is fixed, so the result is deterministic).
 __global__ void lob_gram_finish_kernel(const double* __restrict__ part, int chunks, int n,
                                        double* __restrict__ G, const int* __restrict__ gate) {
   if (gate && *gate) return;
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  const int e = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x & 31;
   if (e >= n) return;
   double v = 0.0;
-  for (int c = 0; c < chunks; ++c) v += part[(long long)c * n + e];
-  G[e] = v;
+  for (int c = lane; c < chunks; c += 32) v += part[(long long)c * n + e];
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if (lane == 0) G[e] = v;
 }
 
 // Cyclic parallel Jacobi on a symmetric np x np matrix (np even) in shared memory, one CTA:
@@ -933,7 +948,7 @@ cudaError_t enqueue_lobpcg(const Dims& dA, const Dims& dB, bool has_B, long long
     }
     ++g_launches;
     const int n = su * sv;
-    lob_gram_finish_kernel<<<(n + 255) / 256, 256, 0, s>>>(gpart, L.gchunks, n, out, gate);
+    lob_gram_finish_kernel<<<(n + 7) / 8, 256, 0, s>>>(gpart, L.gchunks, n, out, gate);
     ++g_launches;
     return cudaGetLastError();
   };
