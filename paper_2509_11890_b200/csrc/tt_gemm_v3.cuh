@@ -41,12 +41,18 @@ struct GemmParamsV3 {
   int l2_a, l2_b;   // TMA L2 policy per operand: 0 default, 1 evict_last (reused, L2-sized),
                     // 2 evict_first (streamed once, larger than L2)
   int store_mode;   // 0 scalar; 1 column pairs (N-contiguous B, output contiguous along n);
-                    // 2 row pairs (M-contiguous A, output contiguous along m) -> 16-byte stores
+                    // 2 row pairs (M-contiguous A, output contiguous along m) -> 16-byte stores;
+                    // 3 column quads (as 1, contiguous in fours) -> 32-byte stores
   int dbg;
   int skew;         // k-tiles by which the second half of the warps trails the first (0 = off)
   const int* gate;  // optional device flag: nonzero -> no-op
 };
 
+// 32-byte store (sm_100: STG.E.EF.256)
+__device__ __forceinline__ void stg_cs4(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};\n" ::"l"(p), "d"(a), "d"(b), "d"(c),
+               "d"(d));
+}
 __device__ __forceinline__ void stg_cs2(double* p, double a, double b) {
   asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};\n" ::"l"(p), "d"(a), "d"(b));
 }
@@ -381,7 +387,30 @@ dmma_gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
 #pragma unroll
           for (int j = 0; j < NI; ++j) sink += acc[i][j][0] + acc[i][j][1];
         if (sink == 1.2345e-300) p.C[0] = sink;
-      } else if (p.ksplit == 1 && !B_KC && p.store_mode == 1) {
+      } else if (p.ksplit == 1 && !B_KC && p.store_mode == 3 && NI % 2 == 0 && WTN % 16 == 0) {
+        // lane t holds output columns 4t..4t+3 of every 16-column group (fragments 2q, 2q+1,
+        // both accumulator halves): one 32-byte store per row and group (full sectors)
+        long long roff[MI];
+        bool rok[MI];
+#pragma unroll
+        for (int i = 0; i < MI; ++i) {
+          const int r = c_m0 + frag_row(i);
+          rok[i] = r < p.M;
+          roff[i] = rok[i] ? apply_map32(p.rowmap, (uint32_t)r) : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < NI; j += 2) {
+          const int c = c_n0 + acc_col(j, 2 * t);
+          if (c < p.N) {
+            const long long co = apply_map32(p.colmap, (uint32_t)c);
+#pragma unroll
+            for (int i = 0; i < MI; ++i)
+              if (rok[i])
+                stg_cs4(p.C + roff[i] + co, acc[i][j][0], acc[i][j + 1][0], acc[i][j][1],
+                        acc[i][j + 1][1]);
+          }
+        }
+      } else if (p.ksplit == 1 && !B_KC && (p.store_mode == 1 || p.store_mode == 3)) {
         // fragments 2q and 2q+1 hold adjacent output columns: one 16-byte store per pair
         long long roff[MI];
         bool rok[MI];

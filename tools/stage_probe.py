@@ -42,6 +42,8 @@ if __name__ == "__main__":
                 (128, "2d-boxes"), (1, "no-stores"), (2, "no-loads"), (3, "compute-only"))
         if os.environ.get("PROBE_QUICK"):
             sets = ((0, "normal"), (3, "compute-only"))
+        if os.environ.get("PROBE_QUAD"):
+            sets = ((0, "quad-stores"), (131072, "pair-stores"), (1, "no-stores"), (0, "quad-stores"))
         if os.environ.get("PROBE_SKEW"):
             sets = ((0, "skew0"), (16384, "skew1"), (32768, "skew2"), (0, "skew0"))
         if os.environ.get("PROBE_RASTER"):
