@@ -159,6 +159,17 @@ dmma_gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   const int wm = warp / WARPS_N, wn = warp % WARPS_N;
   const int g = lane >> 2, t = lane & 3;
 
+  // Column offsets of the output map: when the whole N extent is one tile (the operator-core
+  // stage, N = n R <= 144) every unit has c_n0 = 0, so the BN offsets are evaluated once into
+  // shared memory instead of two magic divisions per column per unit in the epilogue.
+  __shared__ long long ctab[BN];
+  const bool col_cached = p.tiles_n == 1 && !(p.dbg & 262144);
+  if (col_cached)
+    for (int c = threadIdx.x; c < BN; c += blockDim.x)
+      ctab[c] = c < p.N ? apply_map32(p.colmap, (uint32_t)c) : 0;
+  auto col_off = [&](int c) -> long long {
+    return col_cached ? ctab[c] : apply_map32(p.colmap, (uint32_t)c);
+  };
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
@@ -402,7 +413,7 @@ dmma_gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         for (int j = 0; j < NI; j += 2) {
           const int c = c_n0 + acc_col(j, 2 * t);
           if (c < p.N) {
-            const long long co = apply_map32(p.colmap, (uint32_t)c);
+            const long long co = col_off(c);
 #pragma unroll
             for (int i = 0; i < MI; ++i)
               if (rok[i])
@@ -426,7 +437,7 @@ dmma_gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           for (int h = 0; h < 2; ++h) {
             const int c = c_n0 + acc_col(j, 2 * t + h);
             if (c < p.N) {
-              const long long co = apply_map32(p.colmap, (uint32_t)c);
+              const long long co = col_off(c);
 #pragma unroll
               for (int i = 0; i < MI; ++i)
                 if (rok[i]) stg_cs2(p.C + roff[i] + co, acc[i][j][h], acc[i][j + 1][h]);
@@ -437,7 +448,7 @@ dmma_gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           for (int h = 0; h < 2; ++h) {
             const int c = c_n0 + acc_col(NI - 1, 2 * t + h);
             if (c < p.N) {
-              const long long co = apply_map32(p.colmap, (uint32_t)c);
+              const long long co = col_off(c);
 #pragma unroll
               for (int i = 0; i < MI; ++i)
                 if (rok[i]) stg_cs(p.C + roff[i] + co, acc[i][NI - 1][h]);
@@ -461,7 +472,7 @@ dmma_gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           for (int h = 0; h < 2; ++h) {
             const int c = c_n0 + acc_col(j, 2 * t + h);
             if (c < p.N) {
-              const long long co = apply_map32(p.colmap, (uint32_t)c);
+              const long long co = col_off(c);
 #pragma unroll
               for (int ip = 0; ip < MP; ++ip)
                 if (rpk[ip]) stg_cs2(p.C + rpo[ip] + co, acc[2 * ip][j][h], acc[2 * ip + 1][j][h]);
@@ -476,7 +487,7 @@ dmma_gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
                 const int c = c_n0 + acc_col(j, 2 * t + h);
-                if (c < p.N) stg_cs(p.C + ro + apply_map32(p.colmap, (uint32_t)c), acc[MI - 1][j][h]);
+                if (c < p.N) stg_cs(p.C + ro + col_off(c), acc[MI - 1][j][h]);
               }
           }
         }
@@ -495,7 +506,7 @@ dmma_gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           for (int h = 0; h < 2; ++h) {
             const int c = c_n0 + acc_col(j, 2 * t + h);
             if (c < p.N) {
-              const long long co = apply_map32(p.colmap, (uint32_t)c);
+              const long long co = col_off(c);
 #pragma unroll
               for (int i = 0; i < MI; ++i)
                 if (rok[i]) stg_cs(p.C + roff[i] + co, acc[i][j][h]);
