@@ -391,7 +391,8 @@ void tt_debug_set_variant(int v);
  * runs the W34 interface chains at the lowest stream priority, bit 12 disables programmatic
  * dependent launch, bit 13 the small-GEMM latency tile policy, bit 14 the one-k-tile warp skew
  * of the 16-warp GEMM tiles (bit 15: two k-tiles), bit 17 the 32-byte epilogue stores, bit 18
- * the shared-memory column-offset table of single-N-tile GEMMs.
+ * the shared-memory column-offset table of single-N-tile GEMMs, bit 19 the division-free unit
+ * decode (ksplit == 1 / one N tile).
  * tt_debug_set_variant(v): v >= 10 forces
  * the GEMM tile configuration v % 100 (probe list in tt_hotpath.cu) and split-K factor v / 100. */
 void tt_debug_set_flags(int flags);

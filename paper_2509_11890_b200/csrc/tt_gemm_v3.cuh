@@ -187,11 +187,17 @@ dmma_gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   pdl_wait();
   if (p.gate && *p.gate) return;
 
+  // (the common cases ksplit == 1 and a single N tile skip the integer divisions: the
+  // operator-core stage switches units every 9 k-tiles; debug bit 19 forces the generic path)
+  const bool fast_units = !(p.dbg & 524288);
   auto unit_of = [&](int u, int& m0, int& n0, int& kb, int& ke, int& split) {
-    const int tile = u / p.ksplit;
+    const int tile = (fast_units && p.ksplit == 1) ? u : u / p.ksplit;
     split = u - tile * p.ksplit;
     int tm, tn;
-    if (p.group_m <= 1) {
+    if (fast_units && p.group_m <= 1 && p.tiles_n == 1) {
+      tm = tile;
+      tn = 0;
+    } else if (p.group_m <= 1) {
       tm = tile / p.tiles_n;
       tn = tile - tm * p.tiles_n;
     } else {

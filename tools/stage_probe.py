@@ -42,6 +42,8 @@ if __name__ == "__main__":
                 (128, "2d-boxes"), (1, "no-stores"), (2, "no-loads"), (3, "compute-only"))
         if os.environ.get("PROBE_QUICK"):
             sets = ((0, "normal"), (3, "compute-only"))
+        if os.environ.get("PROBE_UNITS"):
+            sets = ((0, "fast-units"), (524288, "div-units"), (0, "fast-units"), (524288, "div-units"))
         if os.environ.get("PROBE_CTAB"):
             sets = ((0, "col-table"), (262144, "col-map"), (0, "col-table"), (262144, "col-map"))
         if os.environ.get("PROBE_QUAD"):
