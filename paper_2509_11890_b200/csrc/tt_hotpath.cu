@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <algorithm>
 #include <memory>
@@ -597,7 +598,8 @@ cudaError_t launch_v3_cfg(const GemmParams& p0, cudaStream_t s, bool& ok) {
 // stages (~34 MFLOP) ran as 32-64 CTAs of 128 x 64.  For GEMMs below kLatencyFlops the tile
 // configuration and split-K factor are chosen by a small model over a candidate list:
 //   t = ceil(units / SMs) x k-tiles per unit x 2 BM BN 16 / (251 GF/s x eff x occ)
-//       + split-K reduction (reads ks M N, writes M N doubles) + a fixed 3 us if ks > 1,
+//       + ceil(units / SMs) x 3 us + split-K reduction (reads ks M N, writes M N doubles)
+//       + a fixed 3 us if ks > 1,
 // eff = the configuration's measured fraction of peak at scale (tools/stage_probe.py, config-5
 // interior shapes) and occ the warp-occupancy factor of a sparsely filled SM (a DMMA blocks
 // its warp ~16 cycles; fewer than 2 warps per sub-partition leave the pipe idle).
@@ -613,6 +615,26 @@ constexpr TileCand kLatencyCands[] = {
     {16, 64, 112, 8, 2, 0.80}, {21, 64, 144, 8, 2, 0.85}, {17, 64, 48, 8, 2, 0.78},
 };
 
+// model knobs (probe overrides: TT_LAT_FLOPS, TT_LAT_UNIT_US, TT_LAT_MASK = candidate bitmask
+// to exclude), read once
+struct LatKnobs {
+  // unit_s: a per-unit cost (epilogue, pipeline refill, the smaller tiles' lower efficiency)
+  // that favours fewer, larger units; swept on the W34 DAG (tools/w34_knobs.py): config 4
+  // 0.808 ms (0 us) -> 0.761 (1 us) -> 0.750 (3 us), config 3 unchanged (0.173-0.176 ms)
+  double flops = kLatencyFlops, unit_s = 3.0e-6;
+  unsigned mask = 0;
+};
+const LatKnobs& lat_knobs() {
+  static LatKnobs k = [] {
+    LatKnobs r;
+    if (const char* e = getenv("TT_LAT_FLOPS")) r.flops = atof(e);
+    if (const char* e = getenv("TT_LAT_UNIT_US")) r.unit_s = atof(e) * 1e-6;
+    if (const char* e = getenv("TT_LAT_MASK")) r.mask = (unsigned)strtoul(e, nullptr, 0);
+    return r;
+  }();
+  return k;
+}
+
 double latency_estimate(const TileCand& c, long long M, long long N, long long K, int ks) {
   const long long sms = num_sms();
   const long long tiles = ((M + c.bm - 1) / c.bm) * ((N + c.bn - 1) / c.bn);
@@ -625,6 +647,7 @@ double latency_estimate(const TileCand& c, long long M, long long N, long long K
   const long long w = ctas_per_sm * c.warps;
   const double occ = w >= 12 ? 1.0 : w >= 8 ? 0.9 : w >= 4 ? 0.6 : 0.35;
   double t = (double)per_sm * (double)kper * 2.0 * c.bm * c.bn * 16.0 / (251.0e9 * c.eff * occ);
+  t += (double)per_sm * lat_knobs().unit_s;   // per-unit epilogue / pipeline refill
   if (ks > 1) t += (double)(ks + 1) * M * N * 8.0 / 5.0e12 + 3.0e-6;
   return t;
 }
@@ -632,12 +655,13 @@ double latency_estimate(const TileCand& c, long long M, long long N, long long K
 // best (candidate index, ks) for a small GEMM, or -1 when the stage is not small
 int latency_choice(const GemmParams& p, bool a_kc, bool b_kc, int& ks_out) {
   if (g_dbg_flags & 8192) return -1;
-  if (2.0 * p.M * p.N * p.K > kLatencyFlops) return -1;
+  if (2.0 * p.M * p.N * p.K > lat_knobs().flops) return -1;
   double best = 1e30;
   int bi = -1;
   const long long KT = (p.K + 15) / 16;
   for (int i = 0; i < (int)(sizeof(kLatencyCands) / sizeof(kLatencyCands[0])); ++i) {
     const TileCand& c = kLatencyCands[i];
+    if (lat_knobs().mask & (1u << i)) continue;
     (void)a_kc; (void)b_kc;   // every candidate's BM, BN are multiples of 16 (any operand layout)
     for (int ks = 1; ks <= 16; ks *= 2) {
       if (ks > 1 && (KT < 2 * ks || g_pscratch == nullptr || (long long)ks * p.M * p.N > g_pscratch_elems))
