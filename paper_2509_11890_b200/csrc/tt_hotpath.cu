@@ -599,7 +599,7 @@ cudaError_t launch_v3_cfg(const GemmParams& p0, cudaStream_t s, bool& ok) {
 // configuration and split-K factor are chosen by a small model over a candidate list:
 //   t = ceil(units / SMs) x k-tiles per unit x 2 BM BN 16 / (251 GF/s x eff x occ)
 //       + ceil(units / SMs) x 3 us + split-K reduction (reads ks M N, writes M N doubles)
-//       + a fixed 3 us if ks > 1,
+//       + a fixed 1 us if ks > 1  (occ = 1 by default; knobs below),
 // eff = the configuration's measured fraction of peak at scale (tools/stage_probe.py, config-5
 // interior shapes) and occ the warp-occupancy factor of a sparsely filled SM (a DMMA blocks
 // its warp ~16 cycles; fewer than 2 warps per sub-partition leave the pipe idle).
@@ -621,7 +621,10 @@ struct LatKnobs {
   // unit_s: a per-unit cost (epilogue, pipeline refill, the smaller tiles' lower efficiency)
   // that favours fewer, larger units; swept on the W34 DAG (tools/w34_knobs.py): config 4
   // 0.808 ms (0 us) -> 0.761 (1 us) -> 0.750 (3 us), config 3 unchanged (0.173-0.176 ms)
-  double flops = kLatencyFlops, unit_s = 3.0e-6;
+  // split_s: fixed cost of a split-K reduction launch; occ_model: the warp-occupancy factor
+  // (off: with the per-unit term it only cost config 3, 0.175 -> 0.165 ms without it)
+  double flops = kLatencyFlops, unit_s = 3.0e-6, split_s = 1.0e-6;
+  int occ_model = 0;
   unsigned mask = 0;
 };
 const LatKnobs& lat_knobs() {
@@ -630,6 +633,8 @@ const LatKnobs& lat_knobs() {
     if (const char* e = getenv("TT_LAT_FLOPS")) r.flops = atof(e);
     if (const char* e = getenv("TT_LAT_UNIT_US")) r.unit_s = atof(e) * 1e-6;
     if (const char* e = getenv("TT_LAT_MASK")) r.mask = (unsigned)strtoul(e, nullptr, 0);
+    if (const char* e = getenv("TT_LAT_SPLIT_US")) r.split_s = atof(e) * 1e-6;
+    if (const char* e = getenv("TT_LAT_OCC")) r.occ_model = atoi(e);
     return r;
   }();
   return k;
@@ -645,10 +650,10 @@ double latency_estimate(const TileCand& c, long long M, long long N, long long K
   const long long per_sm = (units + sms - 1) / sms;
   const long long ctas_per_sm = std::min<long long>(c.minb, (grid + sms - 1) / sms);
   const long long w = ctas_per_sm * c.warps;
-  const double occ = w >= 12 ? 1.0 : w >= 8 ? 0.9 : w >= 4 ? 0.6 : 0.35;
+  const double occ = !lat_knobs().occ_model ? 1.0 : w >= 12 ? 1.0 : w >= 8 ? 0.9 : w >= 4 ? 0.6 : 0.35;
   double t = (double)per_sm * (double)kper * 2.0 * c.bm * c.bn * 16.0 / (251.0e9 * c.eff * occ);
   t += (double)per_sm * lat_knobs().unit_s;   // per-unit epilogue / pipeline refill
-  if (ks > 1) t += (double)(ks + 1) * M * N * 8.0 / 5.0e12 + 3.0e-6;
+  if (ks > 1) t += (double)(ks + 1) * M * N * 8.0 / 5.0e12 + lat_knobs().split_s;
   return t;
 }
 
