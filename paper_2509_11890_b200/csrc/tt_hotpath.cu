@@ -187,9 +187,17 @@ size_t ws_bytes(std::initializer_list<long long> elems) {
 
 thread_local int g_dbg_flags = 0;   // tt_debug_set_flags (bits listed in the header)
 // GEMMs up to this size are launched with PDL (config 3's ~34 MFLOP stages gain 8 %; config
-// 4's ~0.4 GFLOP interior stages lose 6 % in a lone chain: the early-placed dependents
-// unbalance the persistent grid); g_no_pdl (tt_sweep_als scope) disables it.
-constexpr double kPdlFlops = 0.2e9;
+// 4's ~0.16-0.4 GFLOP stages lose: the early-placed dependents unbalance the persistent grid;
+// swept with tools/w34_knobs.py: 0.05 GFLOP gives config 3 0.166 ms and config 4 0.731 ms,
+// 0.2 GFLOP 0.165 / 0.746, no PDL 0.193 / 0.734); g_no_pdl (tt_sweep_als scope) disables it.
+constexpr double kPdlFlopsDefault = 0.05e9;
+double pdl_flops() {   // probe override TT_PDL_FLOPS, read once
+  static const double v = [] {
+    const char* e = getenv("TT_PDL_FLOPS");
+    return e ? atof(e) : kPdlFlopsDefault;
+  }();
+  return v;
+}
 thread_local bool g_no_pdl = false;
 
 // Launch with programmatic stream serialisation (PDL, tt_gemm.cuh pdl_wait/pdl_trigger) when
@@ -235,7 +243,7 @@ cudaError_t launch_cfg(const GemmParams& p0, cudaStream_t s) {
   const long long tiles = tm * p.tiles_n;
   if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
   const long long tr = trace_begin(BN, p.M, p.N, p.K, s);
-  if (cudaError_t e = launch_pdl(2.0 * p.M * p.N * p.K <= kPdlFlops, kern, dim3((unsigned)tiles), dim3(Cfg::kThreads), Cfg::kSmemBytes, s, p))
+  if (cudaError_t e = launch_pdl(2.0 * p.M * p.N * p.K <= pdl_flops(), kern, dim3((unsigned)tiles), dim3(Cfg::kThreads), Cfg::kSmemBytes, s, p))
     return e;
   trace_end(tr, s);
   ++g_launches;
@@ -340,13 +348,13 @@ cudaError_t launch_v2_cfg(const GemmParams& p0, cudaStream_t s) {
   if (ks > 1) p.P = g_pscratch;
   const int grid = (int)std::min<long long>((long long)p.total_units, slots);
   const long long tr = trace_begin(BN + 1000 * ks, p0.M, p0.N, p0.K, s);
-  if (cudaError_t e = launch_pdl(2.0 * p0.M * p0.N * p0.K <= kPdlFlops, kern, dim3(grid), dim3(Cfg::kThreads), Cfg::kSmemBytes, s, p))
+  if (cudaError_t e = launch_pdl(2.0 * p0.M * p0.N * p0.K <= pdl_flops(), kern, dim3(grid), dim3(Cfg::kThreads), Cfg::kSmemBytes, s, p))
     return e;
   if (ks > 1) {
     const long long mn = p0.M * p0.N;
     long long blocks = (mn + 255) / 256;
     if (blocks > 8L * num_sms()) blocks = 8L * num_sms();
-    if (cudaError_t e = launch_pdl(2.0 * p0.M * p0.N * p0.K <= kPdlFlops, tt::splitk_reduce_kernel,
+    if (cudaError_t e = launch_pdl(2.0 * p0.M * p0.N * p0.K <= pdl_flops(), tt::splitk_reduce_kernel,
                                    dim3((unsigned)blocks), dim3(256), 0,
                                    s, (const double*)p.P, p.C, p.M, p.N, ks, p.rowmap, p.colmap,
                                    p.gate))
@@ -574,13 +582,13 @@ cudaError_t launch_v3_cfg(const GemmParams& p0, cudaStream_t s, bool& ok) {
   if (ks > 1) p.P = g_pscratch;
   const int grid = (int)std::min<long long>((long long)p.total_units, slots);
   const long long tr = trace_begin(BN + 1000 * ks + 100000, p0.M, p0.N, p0.K, s);
-  if (cudaError_t e = launch_pdl(2.0 * p0.M * p0.N * p0.K <= kPdlFlops, kern, dim3(grid), dim3(Cfg::kThreads), Cfg::kSmemBytes, s, ta, tb, p))
+  if (cudaError_t e = launch_pdl(2.0 * p0.M * p0.N * p0.K <= pdl_flops(), kern, dim3(grid), dim3(Cfg::kThreads), Cfg::kSmemBytes, s, ta, tb, p))
     return e;
   if (ks > 1) {
     const long long mn = p0.M * p0.N;
     long long blocks = (mn + 255) / 256;
     if (blocks > 8L * num_sms()) blocks = 8L * num_sms();
-    if (cudaError_t e = launch_pdl(2.0 * p0.M * p0.N * p0.K <= kPdlFlops, tt::splitk_reduce_kernel,
+    if (cudaError_t e = launch_pdl(2.0 * p0.M * p0.N * p0.K <= pdl_flops(), tt::splitk_reduce_kernel,
                                    dim3((unsigned)blocks), dim3(256), 0,
                                    s, (const double*)p.P, p.C, p.M, p.N, ks, p.rowmap, p.colmap,
                                    p.gate))

@@ -1,5 +1,5 @@
 """W34 DAG (configs 3, 4) CUDA-graph time under the latency-model knobs in the environment
-(TT_LAT_FLOPS, TT_LAT_UNIT_US, TT_LAT_MASK); one line per process."""
+(TT_LAT_FLOPS, TT_LAT_UNIT_US, TT_LAT_MASK, TT_LAT_SPLIT_US, TT_LAT_OCC, TT_PDL_FLOPS); one line per process."""
 import os
 import statistics
 import sys
@@ -35,5 +35,5 @@ for idx in (3, 4):
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
     out.append(f"c{idx} {statistics.median(ts):.3f} ms")
-knobs = {k: v for k, v in os.environ.items() if k.startswith("TT_LAT")}
+knobs = {k: v for k, v in os.environ.items() if k.startswith(("TT_LAT", "TT_PDL"))}
 print(knobs, " ".join(out), flush=True)
