@@ -35,6 +35,7 @@ struct GemmParamsV3 {
   int M, N, K;
   IndexMap32 rowmap, colmap;
   int tiles_n, total_units, KT, ksplit, kt_per_split;
+  FastDiv tiles_n_div;   // magic division by tiles_n (unit decode)
   int a3d, b3d;     // MN-contiguous operand described by a 3-D map (one TMA per stage)
   int tiles_m, group_m;   // tile order: groups of group_m M-tiles, M fastest inside a group
                           // (group_m = 1: N-fastest rows of tiles)
@@ -197,6 +198,9 @@ dmma_gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     if (fast_units && p.group_m <= 1 && p.tiles_n == 1) {
       tm = tile;
       tn = 0;
+    } else if (fast_units && p.group_m <= 1) {
+      tm = (int)fdiv((uint32_t)tile, p.tiles_n_div);
+      tn = tile - tm * p.tiles_n;
     } else if (p.group_m <= 1) {
       tm = tile / p.tiles_n;
       tn = tile - tm * p.tiles_n;

@@ -542,6 +542,7 @@ cudaError_t launch_v3_cfg(const GemmParams& p0, cudaStream_t s, bool& ok) {
   const long long tn = (p0.N + BN - 1) / BN;
   const long long tiles = tm * tn;
   p.tiles_n = (int)tn;
+  p.tiles_n_div = tt::make_fastdiv((uint32_t)tn);
   p.tiles_m = (int)tm;
   p.group_m = (g_dbg_flags & 512) ? 8 : (g_dbg_flags & 1024) ? (int)tm : 1;
   p.KT = (int)((p0.K + Cfg::BK - 1) / Cfg::BK);
