@@ -731,6 +731,9 @@ cudaError_t launch_v3_l(const GemmParams& p, cudaStream_t s, bool& ok) {
       case 20: return launch_v3_cfg<AK, BK_, 128, 32, 4, 2, 2>(p, s, ok);
       case 21: return launch_v3_cfg<AK, BK_, 64, 144, 4, 2, 2>(p, s, ok);
       case 22: return launch_v3_cfg<AK, BK_, 32, 112, 2, 2, 4>(p, s, ok);
+      case 23: return launch_v3_cfg<AK, BK_, 128, 144, 16, 1, 1>(p, s, ok);
+      case 24: return launch_v3_cfg<AK, BK_, 128, 128, 8, 2, 1>(p, s, ok);
+      case 25: return launch_v3_cfg<AK, BK_, 128, 128, 2, 8, 1>(p, s, ok);
       default: break;
     }
   }
@@ -749,7 +752,8 @@ cudaError_t launch_v3_l(const GemmParams& p, cudaStream_t s, bool& ok) {
   //    128 x 128 tiles (+ split-K), 95% of the DMMA peak;
   //  * wide N with an N-contiguous B (the first stage): one 16-warp CTA per SM, 128 x 128
   //    (two 8-warp CTAs of 128 x 64 were the earlier choice; with the 3-D TMA slabs and L2
-  //    hints the 128 x 128 tile is 1.2 % faster on the whole W5 sweep, tools/flags_ab.py 0 v5).
+  //    hints the 128 x 128 tile is 1.2 % faster on the whole W5 sweep), warps 8 x 2 (16 x 64
+  //    warp tiles: S1 +0.9 %, W5 -0.28 % against 4 x 4, tools/flags_ab.py 0 v6).
   if (p.N <= 16) return launch_v3_cfg<AK, BK_, 64, 16, 8, 1, 2>(p, s, ok);
   if (p.N <= 48) return launch_v3_cfg<AK, BK_, 64, 48, 8, 1, 2>(p, s, ok);
   // small problems: 64-row tiles on two CTAs per SM double the tile count
@@ -764,9 +768,9 @@ cudaError_t launch_v3_l(const GemmParams& p, cudaStream_t s, bool& ok) {
   if (p.N <= 144) return launch_v3_cfg<AK, BK_, 128, 144, 8, 2, 1>(p, s, ok);
   if (BK_) return launch_v3_cfg<AK, BK_, 128, 128, 4, 4, 1>(p, s, ok);
   if (g_variant == 5) return launch_v3_cfg<AK, BK_, 128, 64, 4, 2, 2>(p, s, ok);   // probes
-  if (g_variant == 6) return launch_v3_cfg<AK, BK_, 128, 128, 8, 2, 1>(p, s, ok);
+  if (g_variant == 6) return launch_v3_cfg<AK, BK_, 128, 128, 4, 4, 1>(p, s, ok);
   if (g_variant == 7) return launch_v3_cfg<AK, BK_, 64, 128, 2, 4, 2>(p, s, ok);
-  return launch_v3_cfg<AK, BK_, 128, 128, 4, 4, 1>(p, s, ok);
+  return launch_v3_cfg<AK, BK_, 128, 128, 8, 2, 1>(p, s, ok);
 }
 
 bool aligned16(const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; }
