@@ -499,7 +499,7 @@ cudaError_t launch_v3_cfg(const GemmParams& p0, cudaStream_t s, bool& ok) {
   p.gate = p0.gate;
   // warp skew (tt_gemm_v3.cuh): 1 k-tile for the 16-warp tiles (W5 sweep -0.18 % in a
   // one-process A/B, S1 +0.4 %); debug bit 16384 disables it, bit 32768 sets 2 k-tiles
-  p.skew = (Cfg::kWarps >= 16 && ST >= 4 && !(g_dbg_flags & 16384))
+  p.skew = (Cfg::kWarps >= 12 && ST >= 4 && !(g_dbg_flags & 16384))
                ? ((g_dbg_flags & 32768) ? 2 : 1) : 0;
   p.M = (int)p0.M;
   p.N = (int)p0.N;
@@ -734,6 +734,10 @@ cudaError_t launch_v3_l(const GemmParams& p, cudaStream_t s, bool& ok) {
       case 23: return launch_v3_cfg<AK, BK_, 128, 144, 16, 1, 1>(p, s, ok);
       case 24: return launch_v3_cfg<AK, BK_, 128, 128, 8, 2, 1>(p, s, ok);
       case 25: return launch_v3_cfg<AK, BK_, 128, 128, 2, 8, 1>(p, s, ok);
+      case 26: return launch_v3_cfg<AK, BK_, 128, 144, 4, 3, 1>(p, s, ok);
+      case 27: return launch_v3_cfg<AK, BK_, 128, 144, 2, 6, 1>(p, s, ok);
+      case 29: return launch_v3_cfg<AK, BK_, 128, 96, 4, 3, 1>(p, s, ok);
+      case 31: return launch_v3_cfg<AK, BK_, 128, 128, 4, 2, 1>(p, s, ok);
       default: break;
     }
   }
@@ -753,7 +757,11 @@ cudaError_t launch_v3_l(const GemmParams& p, cudaStream_t s, bool& ok) {
   //  * wide N with an N-contiguous B (the first stage): one 16-warp CTA per SM, 128 x 128
   //    (two 8-warp CTAs of 128 x 64 were the earlier choice; with the 3-D TMA slabs and L2
   //    hints the 128 x 128 tile is 1.2 % faster on the whole W5 sweep), warps 8 x 2 (16 x 64
-  //    warp tiles: S1 +0.9 %, W5 -0.28 % against 4 x 4, tools/flags_ab.py 0 v6).
+  //    warp tiles: S1 +0.9 %, W5 -0.28 % against 4 x 4, tools/flags_ab.py 0 v6); since then
+  //    one 12-warp CTA per SM with a 128 x 144 tile (warps 4 x 3 of 32 x 48), below.
+  //  * 12 warps (3 per sub-partition, up to 168 registers) fit 32 x 48 warp tiles: 10
+  //    fragment loads per 24 DMMAs instead of 10-11 per 16-18 (tools/stage_probe.py 26-31,
+  //    tools/flags_ab.py 0 5242880: W5 sweep 105.65 -> 104.18 ms).
   if (p.N <= 16) return launch_v3_cfg<AK, BK_, 64, 16, 8, 1, 2>(p, s, ok);
   if (p.N <= 48) return launch_v3_cfg<AK, BK_, 64, 48, 8, 1, 2>(p, s, ok);
   // small problems: 64-row tiles on two CTAs per SM double the tile count
@@ -765,12 +773,21 @@ cudaError_t launch_v3_l(const GemmParams& p, cudaStream_t s, bool& ok) {
   }
   if (p.N <= 64) return launch_v3_cfg<AK, BK_, 128, 64, 8, 2, 1>(p, s, ok);
   if (p.N <= 112) return launch_v3_cfg<AK, BK_, 128, 112, 8, 2, 1>(p, s, ok);
-  if (p.N <= 144) return launch_v3_cfg<AK, BK_, 128, 144, 8, 2, 1>(p, s, ok);
+  if (p.N <= 144) {
+    // 12 warps of 32 x 48 (fewer fragment loads per DMMA than 8 x 2 warps of 16 x 72:
+    // operator-core stage 33.5 -> 34.6 TFLOP/s, W5 sweep -0.6 %); bit 20 restores 8 x 2
+    if (g_dbg_flags & 1048576) return launch_v3_cfg<AK, BK_, 128, 144, 8, 2, 1>(p, s, ok);
+    if (g_dbg_flags & 2097152) return launch_v3_cfg<AK, BK_, 128, 144, 2, 6, 1>(p, s, ok);
+    return launch_v3_cfg<AK, BK_, 128, 144, 4, 3, 1>(p, s, ok);
+  }
   if (BK_) return launch_v3_cfg<AK, BK_, 128, 128, 4, 4, 1>(p, s, ok);
   if (g_variant == 5) return launch_v3_cfg<AK, BK_, 128, 64, 4, 2, 2>(p, s, ok);   // probes
   if (g_variant == 6) return launch_v3_cfg<AK, BK_, 128, 128, 4, 4, 1>(p, s, ok);
   if (g_variant == 7) return launch_v3_cfg<AK, BK_, 64, 128, 2, 4, 2>(p, s, ok);
-  return launch_v3_cfg<AK, BK_, 128, 128, 8, 2, 1>(p, s, ok);
+  // 128 x 144 tiles on 12 warps of 32 x 48 (first stage 34.0 -> 35.4 TFLOP/s, W5 sweep
+  // -0.75 % on top of the operator-core change; bit 22 restores 128 x 128 on 8 x 2 warps)
+  if (g_dbg_flags & 4194304) return launch_v3_cfg<AK, BK_, 128, 128, 8, 2, 1>(p, s, ok);
+  return launch_v3_cfg<AK, BK_, 128, 144, 4, 3, 1>(p, s, ok);
 }
 
 bool aligned16(const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; }

@@ -646,7 +646,7 @@ def test_local_gmres_converged_cycle_is_gated(tt):
 # interface update + single-vector matvec vs the oracle.  Guards the 4-warp / 4-CTA-per-SM
 # configurations and the no-empty-split clamp of the split-K planner.
 @pytest.mark.timeout(120)
-@pytest.mark.parametrize("cfg", list(range(10, 23)))
+@pytest.mark.parametrize("cfg", list(range(10, 23)) + [24, 26, 27])
 @pytest.mark.parametrize("ks", [1, 3, 8, 16])
 def test_forced_tile_configs(tt, cfg, ks):
     import oracle
