@@ -622,6 +622,8 @@ constexpr TileCand kLatencyCands[] = {
     {10, 128, 64, 8, 2, 0.90}, {11, 64, 64, 8, 2, 0.83}, {12, 64, 64, 4, 4, 0.85},
     {13, 64, 32, 4, 4, 0.82},  {14, 32, 64, 4, 4, 0.82}, {15, 32, 32, 4, 4, 0.75},
     {16, 64, 112, 8, 2, 0.80}, {21, 64, 144, 8, 2, 0.85}, {17, 64, 48, 8, 2, 0.78},
+    // (12-warp 128 x 144 / 128 x 96 and 6-warp 64 x 144 / 64 x 96 candidates were measured
+    // and dropped: config-4 W34 0.73 -> 0.84 ms; the 6-warp tiles reach only 28 TF/s at scale)
 };
 
 // model knobs (probe overrides: TT_LAT_FLOPS, TT_LAT_UNIT_US, TT_LAT_MASK = candidate bitmask
