@@ -366,6 +366,10 @@ tt_status tt_enrich_right(int64_t rl, int64_t n, int64_t rx, int64_t rz, int64_t
  * x_k with phiL[k], phiR[k+1] for every core (y_cores[k] shaped like x_cores[k]).  The two
  * chains run concurrently and each matvec starts as soon as its two interfaces exist (event
  * dependencies, pool streams, middle cores first); the caller's stream waits for all of it.
+ * The matvec at core k is the same contraction as the left update at core k up to its last
+ * stage (phiL[k], A_k and x_k with one vector), so the left chain keeps its stage-2
+ * intermediate T2_k (r[k] n[k] R[k+1] r[k+1] doubles per core, in the workspace) and the
+ * matvec runs only y_k = T2_k . phiR[k+1] (same results as tt_local_matvec, bit for bit).
  * Asynchronous, graph-capturable.  Workspace: tt_sweep_w34_workspace_size. */
 size_t tt_sweep_w34_workspace_size(int64_t d, const int64_t* n, const int64_t* r,
                                    const int64_t* R);
@@ -392,7 +396,9 @@ void tt_debug_set_variant(int v);
  * dependent launch, bit 13 the small-GEMM latency tile policy, bit 14 the one-k-tile warp skew
  * of the 16-warp GEMM tiles (bit 15: two k-tiles), bit 17 the 32-byte epilogue stores, bit 18
  * the shared-memory column-offset table of single-N-tile GEMMs, bit 19 the division-free unit
- * decode (ksplit == 1 / one N tile).
+ * decode (ksplit == 1 / one N tile), bits 20 / 22 restore the 16-warp (8 x 2) tiles of the
+ * operator-core / first matvec stages (bit 21: 2 x 6 warps), bit 23 runs tt_sweep_w34's
+ * matvecs as three stages instead of reusing the left updates' T2_k.
  * tt_debug_set_variant(v): v >= 10 forces
  * the GEMM tile configuration v % 100 (probe list in tt_hotpath.cu) and split-K factor v / 100. */
 void tt_debug_set_flags(int flags);

@@ -1129,6 +1129,18 @@ struct SplitScratch {   // scopes the split-K scratch to one stage launch
 };
 
 // Local matvec (K columns, Block-TT layout) — stages S1, S2^T, S3.
+// S3: Y(a', i, m, b') = T2[(a' m i), (be b)] . phiR[b', (be b)]^T
+cudaError_t enqueue_matvec_last(const Dims& d, long long K, const double* T2, const double* phiR,
+                                double* Y, double* P, long long pe, cudaStream_t s) {
+  const long long a = d.a, b = d.b, be = d.be, N = d.n;
+  g_stage = TT_ST_MV_S3;
+  SplitScratch scratch(P, pe);
+  return launch_gemm(true, true,
+                     gp(T2, be * b, phiR, be * b, Y, a * K * N, b, be * b,
+                        tt::map3(N, K, K * b, b, N * K * b), tt::map_plain(1)),
+                     s);
+}
+
 cudaError_t enqueue_matvec(const Dims& d, long long K, const double* phiL, const double* A,
                            const double* phiR, const double* X, double* Y, double* T1,
                            double* T2, double* Ah, double* P, long long pe, cudaStream_t s,
@@ -1153,14 +1165,7 @@ cudaError_t enqueue_matvec(const Dims& d, long long K, const double* phiL, const
                      tt::map2(b, 1, N * be * b), tt::map_plain(b)),
                   s);
   if (e != cudaSuccess) return e;
-  // S3: Y(a', i, m, b') = T2[(a' m i), (be b)] . phiR[b', (be b)]^T
-  g_stage = TT_ST_MV_S3;
-  SplitScratch scratch(P, pe);
-  e = launch_gemm(true, true,
-                  gp(T2, be * b, phiR, be * b, Y, a * K * N, b, be * b,
-                     tt::map3(N, K, K * b, b, N * K * b), tt::map_plain(1)),
-                  s);
-  return e;
+  return enqueue_matvec_last(d, K, T2, phiR, Y, P, pe, s);
 }
 
 bool iface_ws_elems(const Dims& d, long long& t1, long long& t2, long long& ah, long long& pe) {
@@ -1184,7 +1189,7 @@ bool iface_ws_elems(const Dims& d, long long& t1, long long& t2, long long& ah, 
 cudaError_t enqueue_left(const Dims& d, const double* phiL, const double* A, const double* x,
                          double* out, double* T1, double* T2, double* Ah, double* P,
                          long long pe, cudaStream_t s, int tag_s1 = TT_ST_IL_S1,
-                         const double* Ah_pre = nullptr) {
+                         const double* Ah_pre = nullptr, cudaEvent_t ev_t2 = nullptr) {
   const long long a = d.a, b = d.b, al = d.al, be = d.be, N = d.n;
   cudaError_t e;
   if (Ah_pre)
@@ -1203,6 +1208,7 @@ cudaError_t enqueue_left(const Dims& d, const double* phiL, const double* A, con
                      tt::map_plain(b)),
                   s);
   if (e != cudaSuccess) return e;
+  if (ev_t2 && (e = cudaEventRecord(ev_t2, s)) != cudaSuccess) return e;   // T2 complete
   g_stage = tag_s1 + 2;
   SplitScratch scratch(P, pe);
   return launch_gemm(false, false,
@@ -1849,7 +1855,8 @@ size_t tt_sweep_als_workspace_size(int64_t d, const int64_t* n, const int64_t* r
 static cudaError_t sweep_left_step(int64_t k, int64_t d, int64_t nvec, void* scratch, const int64_t* n,
                                    const int64_t* r, const int64_t* R, const double* const* xc,
                                    const double* const* Ac, double* const* phiL, void* ws,
-                                   size_t wsb, cudaStream_t s) {
+                                   size_t wsb, cudaStream_t s, double* T2_keep = nullptr,
+                                   cudaEvent_t ev_t2 = nullptr) {
   Dims dk{r[k], n[k], r[k + 1], R[k], R[k + 1]};
   long long t1, t2, ah, pe;
   iface_ws_elems(dk, t1, t2, ah, pe);
@@ -1859,9 +1866,10 @@ static cudaError_t sweep_left_step(int64_t k, int64_t d, int64_t nvec, void* scr
   double* Ah = c.take(ah);
   double* Pp = c.take(pe);
   if (!c.ok) return cudaErrorInvalidValue;
+  if (T2_keep) T2 = T2_keep;
   const Prep pp = prep_ptrs(k, d, n, r, R, nvec, ws);
   return enqueue_left(dk, phiL[k], Ac[k], xc[k], phiL[k + 1], T1, T2, Ah, Pp, pe, s,
-                      TT_ST_IL_S1, pp.Ahl);
+                      TT_ST_IL_S1, pp.Ahl, ev_t2);
 }
 
 static cudaError_t sweep_right_step(int64_t k, int64_t d, int64_t nvec, void* scratch, const int64_t* n,
@@ -2005,12 +2013,27 @@ static size_t w34_mv_scratch(int64_t d, const int64_t* n, const int64_t* r, cons
   return best;
 }
 
+// W34 keeps every left update's stage-2 intermediate T2_k (a', i, be, b): with K = 1 it is
+// also the matvec's stage-2 output at core k (same phiL[k], A_k, x_k), so the matvec is only
+// its last stage, y_k = T2_k . phiR[k+1]^T
+static size_t w34_t2_keep(int64_t d, const int64_t* n, const int64_t* r, const int64_t* R) {
+  size_t tot = 256;
+  for (int64_t k = 0; k < d; ++k) {
+    bool ok = true;
+    const long long e = prod({r[k], n[k], R[k + 1], r[k + 1]}, ok);
+    if (!ok) return 0;
+    tot += align_up((size_t)e * 8, 256);
+  }
+  return tot;
+}
+
 size_t tt_sweep_w34_workspace_size(int64_t d, const int64_t* n, const int64_t* r,
                                    const int64_t* R) {
   if (d <= 0 || !n || !r || !R) return 0;
   const size_t base = sweep_ws(d, n, r, R, 0), mv = w34_mv_scratch(d, n, r, R);
-  if (base == 0 || mv == 0) return 0;
-  return align_up(base, 256) + kPoolStreams * align_up(mv, 256) + 256;
+  const size_t keep = w34_t2_keep(d, n, r, R);
+  if (base == 0 || mv == 0 || keep == 0) return 0;
+  return align_up(base, 256) + kPoolStreams * align_up(mv, 256) + keep + 256;
 }
 
 tt_status tt_sweep_w34(int64_t d, const int64_t* n, const int64_t* r, const int64_t* R,
@@ -2040,10 +2063,22 @@ tt_status tt_sweep_w34(int64_t d, const int64_t* n, const int64_t* r, const int6
   void* ws_side = wsb + align_up(main_b, 256);
   const size_t mv_b = w34_mv_scratch(d, n, r, R);
   char* mv_base = wsb + align_up(sweep_ws(d, n, r, R, 0), 256);
-  if ((e = pool_init(size_t(2 * (d + 1) + kPoolStreams + 4))) != cudaSuccess) return cuda_fail(e, "pool");
+  if ((e = pool_init(size_t(3 * (d + 1) + kPoolStreams + 4))) != cudaSuccess) return cuda_fail(e, "pool");
   cudaEvent_t* evL = g_pool.ev.data();         // evL[k]: phiL[k] ready
   cudaEvent_t* evR = evL + (d + 1);            // evR[k]: phiR[k] ready
-  cudaEvent_t* evJ = evR + (d + 1);            // joins
+  cudaEvent_t* evT = evR + (d + 1);            // evT[k]: the left update's T2_k ready
+  cudaEvent_t* evJ = evT + (d + 1);            // joins
+  // T2 reuse (debug bit 23 restores the three-stage matvecs)
+  const bool reuse = !(g_dbg_flags & 8388608);
+  std::vector<double*> T2k(d, nullptr);
+  if (reuse) {
+    char* kb = mv_base + kPoolStreams * align_up(mv_b, 256);
+    kb += (256 - (reinterpret_cast<uintptr_t>(kb) & 255)) & 255;
+    for (int64_t k = 0; k < d; ++k) {
+      T2k[k] = reinterpret_cast<double*>(kb);
+      kb += align_up((size_t)(r[k] * n[k] * R[k + 1] * r[k + 1]) * 8, 256);
+    }
+  }
   if ((e = launch_prep(d, n, r, R, 0, x_cores, A_cores, workspace, s, phiL[0], phiR[d])) != cudaSuccess)
     return cuda_fail(e, "sweep prep");
   cudaStream_t sr;
@@ -2057,7 +2092,7 @@ tt_status tt_sweep_w34(int64_t d, const int64_t* n, const int64_t* r, const int6
   if ((e = cudaEventRecord(evL[0], sl)) != cudaSuccess) return cuda_fail(e, "event");
   for (int64_t k = 0; k < d; ++k) {
     if ((e = sweep_left_step(k, d, 0, ws_main, n, r, R, x_cores, A_cores, phiL, workspace, main_b,
-                             sl)) != cudaSuccess)
+                             sl, T2k[k], reuse ? evT[k] : nullptr)) != cudaSuccess)
       return cuda_fail(e, "sweep left");
     if ((e = cudaEventRecord(evL[k + 1], sl)) != cudaSuccess) return cuda_fail(e, "event");
   }
@@ -2078,7 +2113,7 @@ tt_status tt_sweep_w34(int64_t d, const int64_t* n, const int64_t* r, const int6
     const int64_t k = order[i];
     const int q = (int)(i % kPoolStreams);
     cudaStream_t ps = g_pool.s[q];
-    if ((e = cudaStreamWaitEvent(ps, evL[k], 0)) != cudaSuccess) return cuda_fail(e, "wait");
+    if ((e = cudaStreamWaitEvent(ps, reuse ? evT[k] : evL[k], 0)) != cudaSuccess) return cuda_fail(e, "wait");
     if ((e = cudaStreamWaitEvent(ps, evR[k + 1], 0)) != cudaSuccess) return cuda_fail(e, "wait");
     Dims dk{r[k], n[k], r[k + 1], R[k], R[k + 1]};
     long long t1, t2, ah, pe;
@@ -2089,6 +2124,11 @@ tt_status tt_sweep_w34(int64_t d, const int64_t* n, const int64_t* r, const int6
     double* Ah = c.take(ah);
     double* Pp = c.take(pe);
     if (!c.ok) return fail(TT_ERR_WORKSPACE, "workspace too small after alignment");
+    if (reuse) {
+      if ((e = enqueue_matvec_last(dk, 1, T2k[k], phiR[k + 1], y_cores[k], Pp, pe, ps)) != cudaSuccess)
+        return cuda_fail(e, "sweep matvec");
+      continue;
+    }
     const Prep pp = prep_ptrs(k, d, n, r, R, 0, workspace);
     if ((e = enqueue_matvec(dk, 1, phiL[k], A_cores[k], phiR[k + 1], x_cores[k], y_cores[k], T1,
                             T2, Ah, Pp, pe, ps, pp.Ahl)) != cudaSuccess)

@@ -563,15 +563,20 @@ def test_block_and_elementwise_jacobi_agree(tt):
 # ----------------------------------------------------------------------------------------
 # W34 as one DAG-scheduled call (tt_sweep_w34)
 # ----------------------------------------------------------------------------------------
+@pytest.mark.parametrize("flags", [0, 8388608])   # T2 reuse / bit 23: three-stage matvecs
 @pytest.mark.parametrize("idx", [1, 2, 3, 4])
-def test_sweep_w34_call_vs_oracle_and_separate_calls(tt, idx):
+def test_sweep_w34_call_vs_oracle_and_separate_calls(tt, idx, flags):
     import oracle
     import ttgen
     inp = ttgen.make_inputs(idx)
     x = [g(c) for c in inp.x]
     A = [g(c) for c in inp.A]
-    y, pl, pr = tt.tt_sweep_w34(x, A)
-    torch.cuda.synchronize()
+    tt.tt_debug_set_flags(flags)
+    try:
+        y, pl, pr = tt.tt_sweep_w34(x, A)
+        torch.cuda.synchronize()
+    finally:
+        tt.tt_debug_set_flags(0)
     # identical to the separate calls (same kernels, deterministic)
     pl2, pr2 = tt.alloc_interfaces(x, A), tt.alloc_interfaces(x, A)
     tt.tt_sweep_interfaces(x, A, pl2, pr2)

@@ -10,6 +10,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2509_11890_b200 as tt  # noqa: E402
 import ttgen  # noqa: E402
 
+tt.tt_debug_set_flags(int(os.environ.get("TT_FLAGS", "0")))   # debug bits (header)
 out = []
 for idx in (3, 4):
     inp = ttgen.make_inputs(idx)
@@ -35,5 +36,5 @@ for idx in (3, 4):
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
     out.append(f"c{idx} {statistics.median(ts):.3f} ms")
-knobs = {k: v for k, v in os.environ.items() if k.startswith(("TT_LAT", "TT_PDL"))}
+knobs = {k: v for k, v in os.environ.items() if k.startswith(("TT_LAT", "TT_PDL", "TT_FLAGS"))}
 print(knobs, " ".join(out), flush=True)
