@@ -398,7 +398,9 @@ void tt_debug_set_variant(int v);
  * the shared-memory column-offset table of single-N-tile GEMMs, bit 19 the division-free unit
  * decode (ksplit == 1 / one N tile), bits 20 / 22 restore the 16-warp (8 x 2) tiles of the
  * operator-core / first matvec stages (bit 21: 2 x 6 warps), bit 23 runs tt_sweep_w34's
- * matvecs as three stages instead of reusing the left updates' T2_k.
+ * matvecs as three stages instead of reusing the left updates' T2_k, bit 25 runs the
+ * operator-core stage with the whole A-hat resident in shared memory (3-deep T1 ring;
+ * measured slower, kept as a probe).
  * tt_debug_set_variant(v): v >= 10 forces
  * the GEMM tile configuration v % 100 (probe list in tt_hotpath.cu) and split-K factor v / 100. */
 void tt_debug_set_flags(int flags);

@@ -127,7 +127,12 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
-template <bool A_KC, bool B_KC, int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, int MINB>
+// B_RES: the whole B operand of a single-N-tile GEMM (the operator-core stage's A-hat,
+// K x N <= kBresMaxKT x 16 x BN doubles) is loaded once per CTA into a resident shared-memory
+// block; the ring then carries only A tiles.
+constexpr int kBresMaxKT = 9;
+template <bool A_KC, bool B_KC, int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, int MINB,
+          bool B_RES = false>
 struct GemmV3Cfg {
   static constexpr int BK = 16, kThreads = WARPS_M * WARPS_N * 32, kWarps = WARPS_M * WARPS_N;
   static constexpr int WTM = BM / WARPS_M, WTN = BN / WARPS_N;
@@ -136,22 +141,24 @@ struct GemmV3Cfg {
   static_assert(B_KC || BN % 16 == 0, "N-contiguous B needs 16-wide boxes");
   static constexpr int MI = WTM / 8, NI = WTN / 8;
   static constexpr int A_BYTES = BM * 128, B_BYTES = BN * 128;   // 16 doubles per row/column
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGE_BYTES = B_RES ? A_BYTES : A_BYTES + B_BYTES;
+  static constexpr int BRES_BYTES = B_RES ? kBresMaxKT * B_BYTES : 0;
   static_assert(A_BYTES % 1024 == 0 || BM % 8 == 0, "");
   // +1024 alignment slack for the 128-byte swizzle atoms
-  static constexpr size_t kSmemBytes = (size_t)STAGES * STAGE_BYTES + 1024;
+  static constexpr size_t kSmemBytes = (size_t)STAGES * STAGE_BYTES + BRES_BYTES + 1024;
 };
 
-template <bool A_KC, bool B_KC, int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, int MINB>
+template <bool A_KC, bool B_KC, int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, int MINB,
+          bool B_RES = false>
 __global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, MINB)
 dmma_gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const GemmParamsV3 p) {
-  using Cfg = GemmV3Cfg<A_KC, B_KC, BM, BN, WARPS_M, WARPS_N, STAGES, MINB>;
+  using Cfg = GemmV3Cfg<A_KC, B_KC, BM, BN, WARPS_M, WARPS_N, STAGES, MINB, B_RES>;
   constexpr int WTM = Cfg::WTM, WTN = Cfg::WTN, MI = Cfg::MI, NI = Cfg::NI;
   constexpr int A_BYTES = Cfg::A_BYTES, STAGE_BYTES = Cfg::STAGE_BYTES;
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES];
+  __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES], bres_bar;
   // align to the 1 KB swizzle atom by integer offset so the compiler keeps the shared
   // address space (generic pointer arithmetic would turn every LDS into a generic LD)
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -176,6 +183,7 @@ dmma_gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], Cfg::kWarps);
     }
+    if constexpr (B_RES) mbar_init(&bres_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
@@ -238,6 +246,7 @@ dmma_gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     unsigned char* bs = as + A_BYTES;
     const int k0 = ps[3] * Cfg::BK, m0 = ps[1], n0 = ps[2];
     mbar_expect_tx(&full_bar[s], STAGE_BYTES);
+    (void)bs;
     if (!(p.dbg & 2)) {
       if (A_KC) {
         if (p.l2_a) tma_load_2d_hint(as, &tmA, k0, m0, &full_bar[s], pol_a);
@@ -251,7 +260,8 @@ dmma_gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           else tma_load_2d(as + b * 2048, &tmA, m0 + 16 * b, k0, &full_bar[s]);
         }
       }
-      if (B_KC) {
+      if constexpr (B_RES) {
+      } else if (B_KC) {
         if (p.l2_b) tma_load_2d_hint(bs, &tmB, k0, n0, &full_bar[s], pol_b);
         else tma_load_2d(bs, &tmB, k0, n0, &full_bar[s]);
       } else if (p.b3d) {
@@ -282,10 +292,17 @@ dmma_gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   // STAGES-1-L k-tiles ahead so that refilling a stage never waits for the trailing half.
   const int skew = p.skew;
   const bool trail = skew > 0 && warp >= Cfg::kWarps / 2;
+  unsigned char* const bres = smem + STAGES * STAGE_BYTES;   // B_RES: resident B k-tiles
   if (tid == 0) {
+    if constexpr (B_RES) {   // the whole B once (one N tile, ksplit 1, KT <= kBresMaxKT)
+      mbar_expect_tx(&bres_bar, (uint32_t)(p.KT * Cfg::B_BYTES));
+      for (int kt = 0; kt < p.KT; ++kt)
+        tma_load_3d(bres + kt * Cfg::B_BYTES, &tmB, 0, kt * Cfg::BK, 0, &bres_bar, pol_b, p.l2_b != 0);
+    }
     for (int s = 0; s < STAGES - 1 - skew; ++s) produce_one();
   }
   if (trail) asm volatile("bar.sync 1, %0;\n" ::"r"(Cfg::kThreads) : "memory");
+  if constexpr (B_RES) mbar_wait(&bres_bar, 0);
 
   // ---- fragment geometry ---------------------------------------------------------------
   auto frag_row = [&](int i) -> int {   // tile row of fragment i, lane group g
@@ -331,7 +348,7 @@ dmma_gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     const int s = (int)(q % STAGES);
     mbar_wait(&full_bar[s], (q / STAGES) & 1);
     const unsigned char* as = smem + s * STAGE_BYTES;
-    const unsigned char* bs = as + A_BYTES;
+    const unsigned char* bs = B_RES ? bres + c_kt * Cfg::B_BYTES : as + A_BYTES;
 #pragma unroll
     for (int kp = 0; kp < 2; ++kp) {   // two pairs of DMMA k-steps per 16-deep k-tile
       // K-contiguous operands: one LDS.128 yields both k-steps of the pair

@@ -463,14 +463,14 @@ int store_mode(bool a_kc, bool b_kc, const GemmParams& p) {
   return 0;
 }
 
-template <bool AK, bool BK_, int BM, int BN, int WM, int WN, int MINB>
+template <bool AK, bool BK_, int BM, int BN, int WM, int WN, int MINB, bool BRES = false>
 cudaError_t launch_v3_cfg(const GemmParams& p0, cudaStream_t s, bool& ok) {
-  using Probe = tt::GemmV3Cfg<AK, BK_, BM, BN, WM, WN, 1, MINB>;
+  using Probe = tt::GemmV3Cfg<AK, BK_, BM, BN, WM, WN, 1, MINB, BRES>;
   constexpr size_t budget = (MINB == 1 ? 224 : MINB == 2 ? 110 : 54) * 1024 - 1024;
-  constexpr int ST0 = (int)(budget / Probe::STAGE_BYTES);
+  constexpr int ST0 = (int)((budget - Probe::BRES_BYTES) / Probe::STAGE_BYTES);
   constexpr int ST = ST0 > 6 ? 6 : ST0;
   static_assert(ST >= 2, "shared memory budget");
-  using Cfg = tt::GemmV3Cfg<AK, BK_, BM, BN, WM, WN, ST, MINB>;
+  using Cfg = tt::GemmV3Cfg<AK, BK_, BM, BN, WM, WN, ST, MINB, BRES>;
   ok = false;
   CUtensorMap ta, tb;
   // A: K-contiguous -> inner K, outer M (box rows BM); M-contiguous -> inner M, outer K (box 16)
@@ -483,8 +483,9 @@ cudaError_t launch_v3_cfg(const GemmParams& p0, cudaStream_t s, bool& ok) {
   if (!b3d &&
       !(BK_ ? make_map(&tb, p0.B, p0.K, p0.N, p0.ldb, BN) : make_map(&tb, p0.B, p0.N, p0.K, p0.ldb, 16)))
     return cudaSuccess;
+  if (BRES && (!b3d || p0.N > BN || (p0.K + 15) / 16 > tt::kBresMaxKT)) return cudaSuccess;
   ok = true;
-  auto kern = tt::dmma_gemm_v3_kernel<AK, BK_, BM, BN, WM, WN, ST, MINB>;
+  auto kern = tt::dmma_gemm_v3_kernel<AK, BK_, BM, BN, WM, WN, ST, MINB, BRES>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
@@ -552,7 +553,8 @@ cudaError_t launch_v3_cfg(const GemmParams& p0, cudaStream_t s, bool& ok) {
   // Big stages rarely split (only to fix wave quantisation); skinny ones (few output tiles,
   // long K — e.g. config 4's last matvec stage, 4 tiles x 200 k-tiles) split up to 64 ways.
   int ks = 1;
-  if (g_force_ks > 0) {   // probe hook (tt_debug_set_variant >= 100)
+  if (BRES) {   // resident B: one N tile, whole K per unit
+  } else if (g_force_ks > 0) {   // probe hook (tt_debug_set_variant >= 100)
     ks = g_force_ks;
     while (ks > 1 && (p.KT < ks || g_pscratch == nullptr ||
                       (long long)ks * p0.M * p0.N > g_pscratch_elems))
@@ -779,6 +781,10 @@ cudaError_t launch_v3_l(const GemmParams& p, cudaStream_t s, bool& ok) {
     // 12 warps of 32 x 48 (fewer fragment loads per DMMA than 8 x 2 warps of 16 x 72:
     // operator-core stage 33.5 -> 34.6 TFLOP/s, W5 sweep -0.6 %); bit 20 restores 8 x 2
     if (g_dbg_flags & 1048576) return launch_v3_cfg<AK, BK_, 128, 144, 8, 2, 1>(p, s, ok);
+    if ((g_dbg_flags & 33554432) && !BK_ && (p.K + 15) / 16 <= tt::kBresMaxKT) {
+      cudaError_t e = launch_v3_cfg<AK, BK_, 128, 144, 4, 3, 1, true>(p, s, ok);
+      if (e != cudaSuccess || ok) return e;
+    }
     if (g_dbg_flags & 2097152) return launch_v3_cfg<AK, BK_, 128, 144, 2, 6, 1>(p, s, ok);
     return launch_v3_cfg<AK, BK_, 128, 144, 4, 3, 1>(p, s, ok);
   }

@@ -696,3 +696,27 @@ def test_latency_policy_w34_vs_default_policy(tt, idx):
         outs.append([h(t) for t in pl + pr + y])
     for a, b in zip(*outs):
         assert rel(a, b) <= TOL
+
+
+# Operator-core stage with the resident-B GEMM variant (debug bit 25: the whole A-hat loaded
+# once per CTA, the ring carries only T1 tiles) and with the ring (default), at a size above
+# the small-GEMM latency path (S2 = 2 x 65536 x 144 x 144 = 2.7 GFLOP) with a ragged last tile.
+@pytest.mark.parametrize("flags", [0, 33554432])
+@pytest.mark.parametrize("shape", [(64, 4, 64, 36, 36, 16), (60, 4, 68, 25, 36, 17)])
+def test_operator_core_stage_resident_b(tt, shape, flags):
+    import oracle
+    rl, n, rr, Rl, Rr, nvec = shape
+    rng = np.random.default_rng(sum(shape) + flags % 7)
+    phiL = rng.standard_normal((rl, Rl, rl))
+    A = rng.standard_normal((Rl, n, n, Rr))
+    phiR = rng.standard_normal((rr, Rr, rr))
+    X = rng.standard_normal((rl, n, nvec, rr))
+    tt.tt_debug_set_flags(flags)
+    try:
+        Y = tt.tt_local_matvec_batched(g(phiL), g(A), g(phiR), g(X))
+        torch.cuda.synchronize()
+    finally:
+        tt.tt_debug_set_flags(0)
+    ref = oracle.local_matvec_batched(phiL, A, phiR, X)
+    for m in range(nvec):
+        assert rel(h(Y)[:, :, m, :], ref[:, :, m, :]) <= TOL

@@ -50,6 +50,8 @@ if __name__ == "__main__":
             sets = ((0, "quad-stores"), (131072, "pair-stores"), (1, "no-stores"), (0, "quad-stores"))
         if os.environ.get("PROBE_SKEW"):
             sets = ((0, "skew0"), (16384, "skew1"), (32768, "skew2"), (0, "skew0"))
+        if os.environ.get("PROBE_BRES"):
+            sets = ((0, "ring-B"), (33554432, "resident-B"), (0, "ring-B"), (33554432, "resident-B"))
         if os.environ.get("PROBE_RASTER"):
             sets = ((0, "n-fastest"), (512, "group-m-8"), (1024, "m-fastest"))
         for flags, name in sets:
