@@ -619,7 +619,10 @@ struct TileCand {
   int id, bm, bn, warps, minb;
   double eff;
 };
-constexpr double kLatencyFlops = 1.5e9;
+// threshold swept on the W5 sweep (TT_LAT_FLOPS, profiles/r01e/latflops.log): 5 GFLOP brings
+// the config-5 interface-update stages (2.7-4.8 GFLOP, 3.5-3.9 waves of default tiles) under
+// the model: update 0.443 -> 0.430 ms, W5 -0.1 %; 3 GFLOP was neutral
+constexpr double kLatencyFlops = 5.0e9;
 constexpr TileCand kLatencyCands[] = {
     {10, 128, 64, 8, 2, 0.90}, {11, 64, 64, 8, 2, 0.83}, {12, 64, 64, 4, 4, 0.85},
     {13, 64, 32, 4, 4, 0.82},  {14, 32, 64, 4, 4, 0.82}, {15, 32, 32, 4, 4, 0.75},
