@@ -619,10 +619,11 @@ struct TileCand {
   int id, bm, bn, warps, minb;
   double eff;
 };
-// threshold swept on the W5 sweep (TT_LAT_FLOPS, profiles/r01e/latflops.log): 5 GFLOP brings
+// threshold swept on the W5 sweep (TT_LAT_FLOPS, profiles/r01e/latflops*.log): 5 GFLOP brings
 // the config-5 interface-update stages (2.7-4.8 GFLOP, 3.5-3.9 waves of default tiles) under
-// the model: update 0.443 -> 0.430 ms, W5 -0.1 %; 3 GFLOP was neutral
-constexpr double kLatencyFlops = 5.0e9;
+// the model: update 0.443 -> 0.430 ms, W5 -0.1 %; 10 GFLOP adds the first stage of cores 3 / 8
+// (9.7 GFLOP, K = 64): W5 another -0.07 %; 3 GFLOP neutral, 25 GFLOP +0.1 %
+constexpr double kLatencyFlops = 1.0e10;
 constexpr TileCand kLatencyCands[] = {
     {10, 128, 64, 8, 2, 0.90}, {11, 64, 64, 8, 2, 0.83}, {12, 64, 64, 4, 4, 0.85},
     {13, 64, 32, 4, 4, 0.82},  {14, 32, 64, 4, 4, 0.82}, {15, 32, 32, 4, 4, 0.75},

@@ -700,10 +700,11 @@ def test_latency_policy_w34_vs_default_policy(tt, idx):
 
 # Operator-core stage with the resident-B GEMM variant (debug bit 25: the whole A-hat loaded
 # once per CTA, the ring carries only T1 tiles) and with the ring (default), at a size above
-# the small-GEMM latency path (S2 = 2 x 131072 x 144 x 144 = 5.4 GFLOP > 5 GFLOP) with a ragged
-# last tile.
+# the small-GEMM latency path (S2 = 2 x 262144 x 144 x 144 = 10.9 GFLOP > 10 GFLOP) with a
+# ragged last tile.
+@pytest.mark.timeout(300)
 @pytest.mark.parametrize("flags", [0, 33554432])
-@pytest.mark.parametrize("shape", [(64, 4, 64, 36, 36, 32), (60, 4, 68, 25, 36, 48)])
+@pytest.mark.parametrize("shape", [(64, 4, 64, 36, 36, 64), (60, 4, 68, 25, 36, 88)])
 def test_operator_core_stage_resident_b(tt, shape, flags):
     import oracle
     rl, n, rr, Rl, Rr, nvec = shape
