@@ -1,17 +1,28 @@
 #!/usr/bin/env python
-"""Benchmark of the B200 FP64 TT hot path (BASELINE.json metric, config 5 = W5 workload).
+"""Benchmark of the B200 FP64 TT hot path (BASELINE.json metric; headline = config 5, W5).
 
 One step = the whole hot path over one batch of synthetic config-5 input, through the C-ABI:
-  tt_sweep_als   (H1-H7: initial right interfaces, L->R sweep with K=32 batched local
-                  matvecs + left interfaces, R->L sweep with batched matvecs + right
-                  interfaces; DESIGN.md §5 workload W5)
+  tt_sweep_als      (H1-H7: initial right interfaces, L->R sweep with K=32 batched local
+                     matvecs + left interfaces, R->L sweep with batched matvecs + right
+                     interfaces; DESIGN.md §5 workload W5)
   tt_operator_apply (H8: full unrounded TT-matrix x TT-vector product)
-Value = algorithmic FP64 GFLOP per step / device time per step (CUDA events, max over ranks).
+Value = algorithmic FP64 GFLOP per step / device time per step (CUDA events, max over ranks),
+with the library's tracer OFF in the timed region.  Per-kernel durations come from a separate
+traced pass after it.  `e2e` times the same step with every input uploaded from pinned host
+memory and EVERY output (Y blocks, the unrounded apply z, all interfaces) downloaded to host
+memory inside the timed region.
+
+Per-config lines (`configs`): configs 1-4 run workload W34 through tt_sweep_w34, config 5 the
+W5 sweep; each reports absolute device time (CUDA graph and eager), launches, GFLOP/s,
+roofline fraction and the max relative parity error against the CPU oracle; the oracle is
+timed on configs 1-4's full workloads and on a bounded config-5 sample (the W5 figure is a
+labelled extrapolation).  `latency` covers the single-vector (K=1) matvec and GMRES of the
+paper's regime at config-3/4 interior shapes.
 
   python bench.py [--gpus N --steps K --warmup W]          # our CUDA path
   python bench.py --impl reference [--steps K --warmup W]  # the CPU oracle, as it stands
 
-Multi-GPU: replicas only — each rank runs the same workload, no collective on
+Multi-GPU: replicas only -- each rank runs the same workload, no collective on
 the data path; the barrier/all-reduce below is timing plumbing.
 """
 from __future__ import annotations
@@ -34,10 +45,18 @@ import ttgen  # noqa: E402
 
 METRIC = "FP64 GFLOP/s + % FP64 roofline of TT local matvec; full-sweep time at d=12"
 UNIT = "GFLOP/s"
+HBM_FALLBACK_GBS = 6650.0   # B200_PROFILING.md fallback when MEASURED_PEAKS.json is absent
+PAPER_CONTEXT = {
+    "hardware": "Intel Core i7-1260P, 32 GB RAM, 16 threads (PAPER.md:683, 687)",
+    "implementation": "Python TT IPM (PAPER.md:683)",
+    "headline": "problems up to 2^12, duality gap ~1e-6, ~1.5 h, < 2 GB (PAPER.md:24)",
+    "note": "end-to-end solver figures on other hardware: context only; the paper publishes "
+            "no timing of this hot path (BASELINE.md §1)",
+}
 
 
 # ----------------------------------------------------------------------------------------
-# algorithmic work (DESIGN.md §5; SURVEY.md §8(d))
+# algorithmic work (DESIGN.md §4.4; SURVEY.md §8(d))
 # ----------------------------------------------------------------------------------------
 def f_local(a, N, b, al, be):
     """FLOPs of one local matvec (per vector) == one interface update: three products."""
@@ -46,6 +65,10 @@ def f_local(a, N, b, al, be):
 
 def b_local_matvec(a, N, b, al, be, K):
     return 8 * (a * a * al + b * b * be + al * N * N * be + 2 * K * a * N * b)
+
+
+def b_interface(a, N, b, al, be):
+    return 8 * (a * a * al + al * N * N * be + a * N * b + b * b * be)
 
 
 def f_apply(a, N, b, al, be):
@@ -62,9 +85,52 @@ def w5_work(cfg):
     iface = sum(f_local(r[k], N, r[k + 1], R[k], R[k + 1]) for k in range(1, d)) * 2 \
         + sum(f_local(r[k], N, r[k + 1], R[k], R[k + 1]) for k in range(0, d - 1))
     ap = sum(f_apply(r[k], N, r[k + 1], R[k], R[k + 1]) for k in range(d))
+    mv_b = sum(2 * b_local_matvec(r[k], N, r[k + 1], R[k], R[k + 1], K) for k in range(d))
+    if_b = sum(b_interface(r[k], N, r[k + 1], R[k], R[k + 1]) for k in range(1, d)) * 2 \
+        + sum(b_interface(r[k], N, r[k + 1], R[k], R[k + 1]) for k in range(0, d - 1))
     ap_bytes = sum(b_apply(r[k], N, r[k + 1], R[k], R[k + 1]) for k in range(d))
     return {"matvec_flops": mv, "interface_flops": iface, "apply_flops": ap,
-            "apply_bytes": ap_bytes, "step_flops": mv + iface + ap}
+            "apply_bytes": ap_bytes, "sweep_bytes": mv_b + if_b, "step_flops": mv + iface + ap}
+
+
+def w34_flops(cfg):
+    """SURVEY §8(d) count of W34: (d-1) right + (d-1) left updates + one three-stage matvec per
+    core."""
+    d, N, r, R = cfg.d, cfg.N, cfg.r, cfg.R
+    f = [f_local(r[k], N, r[k + 1], R[k], R[k + 1]) for k in range(d)]
+    return sum(f[1:]) + sum(f[:-1]) + sum(f)
+
+
+def w34_bytes(cfg):
+    d, N, r, R = cfg.d, cfg.N, cfg.r, cfg.R
+    bi = [b_interface(r[k], N, r[k + 1], R[k], R[k + 1]) for k in range(d)]
+    bm = [b_local_matvec(r[k], N, r[k + 1], R[k], R[k + 1], 1) for k in range(d)]
+    return sum(bi[1:]) + sum(bi[:-1]) + sum(bm)
+
+
+def w34_executed_flops(cfg):
+    """FLOPs tt_sweep_w34 executes: d left and d right interface updates (the chains include
+    the boundary updates giving x^T A x) and, per core, only the matvec's last stage -- its first
+    two stages are the left update's (same phiL[k], A_k, x_k with K = 1), whose T2_k is kept."""
+    d, N, r, R = cfg.d, cfg.N, cfg.r, cfg.R
+    f = [f_local(r[k], N, r[k + 1], R[k], R[k + 1]) for k in range(d)]
+    s3 = [2.0 * r[k] * N * r[k + 1] ** 2 * R[k + 1] for k in range(d)]
+    return 2 * sum(f) + sum(s3)
+
+
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return float(json.load(open(p))["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured)"
+    except Exception:
+        return HBM_FALLBACK_GBS, "B200_PROFILING.md fallback (MEASURED_PEAKS.json absent)"
+
+
+def roof(flops, nbytes, ms, p64_tf, bw_gbs):
+    """t_roof = max(F / P64, B / BW); frac = t_roof / t_measured."""
+    t_roof = max(flops / (p64_tf * 1e12), nbytes / (bw_gbs * 1e9))
+    return {"t_roof_ms": t_roof * 1e3, "frac": t_roof / (ms * 1e-3),
+            "bound": "tensor" if flops / (p64_tf * 1e12) >= nbytes / (bw_gbs * 1e9) else "hbm"}
 
 
 # ----------------------------------------------------------------------------------------
@@ -86,27 +152,12 @@ def whole_job_rate(work_per_step: float, world: int, steps: int, max_ms: float) 
     return work_per_step * world * steps / (max_ms * 1e-3) / 1e9
 
 
-def bench_w34_flops(cfg):
-    """W34 = (d-1) right + (d-1) left interface updates + one local matvec per core."""
-    d, N, r, R = cfg.d, cfg.N, cfg.r, cfg.R
-    f = [f_local(r[k], N, r[k + 1], R[k], R[k + 1]) for k in range(d)]
-    return sum(f[1:]) + sum(f[:-1]) + sum(f)
-
-
-def w34_executed_flops(cfg):
-    """FLOPs tt_sweep_w34 executes: d left and d right interface updates (the chains include
-    the boundary updates giving x^T A x) and, per core, only the matvec's last stage — its first
-    two stages are the left update's (same phiL[k], A_k, x_k with K = 1), whose T2_k is kept."""
-    d, N, r, R = cfg.d, cfg.N, cfg.r, cfg.R
-    f = [f_local(r[k], N, r[k + 1], R[k], R[k + 1]) for k in range(d)]
-    s3 = [2.0 * r[k] * N * r[k + 1] ** 2 * R[k + 1] for k in range(d)]
-    return 2 * sum(f) + sum(s3)
-
-
 def time_sweep(tt, fn, stream, dev, reps=5):
-    """Median/best device time of `fn` run eagerly and replayed from a captured CUDA graph."""
+    """Median/best device time of `fn` run eagerly and replayed from a captured CUDA graph;
+    also the number of library launches one call enqueues."""
     import torch
     fn(stream)
+    launches = tt.tt_last_launch_count()
     torch.cuda.synchronize(dev)
     eager = []
     for _ in range(reps):
@@ -131,8 +182,17 @@ def time_sweep(tt, fn, stream, dev, reps=5):
         e1.record(stream)
         e1.synchronize()
         graphed.append(e0.elapsed_time(e1))
+    del graph
     return {"eager_ms_median": statistics.median(eager), "eager_ms_best": min(eager),
-            "graph_ms_median": statistics.median(graphed), "graph_ms_best": min(graphed)}
+            "graph_ms_median": statistics.median(graphed), "graph_ms_best": min(graphed),
+            "launches": launches}
+
+
+def rel_err(a, b):
+    """DESIGN.md reading A8: ||a - b||_F / ||b||_F (||a||_F if b = 0)."""
+    a = np.asarray(a)
+    nb = np.linalg.norm(b)
+    return float(np.linalg.norm(a - b) / nb) if nb else float(np.linalg.norm(a))
 
 
 # ----------------------------------------------------------------------------------------
@@ -186,7 +246,7 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------------------
-# reference arm: the CPU oracle as it stands
+# the CPU oracle (test infrastructure; only the cpu_baseline leg and --impl reference run it)
 # ----------------------------------------------------------------------------------------
 def oracle_sample_inputs(seed=7):
     """Config-5 interior-core shapes (a=b=256, alpha=beta=36, N=4), seeded random values."""
@@ -217,20 +277,6 @@ class pinned_one_core:
         return False
 
 
-def time_oracle_sample(with_interface=True):
-    import oracle
-    s = oracle_sample_inputs()
-    oracle.build()
-    t0 = time.perf_counter()
-    oracle.local_matvec(s["phiL"], s["A"], s["phiR"], s["x"])
-    flops = f_local(s["a"], s["N"], s["b"], s["al"], s["be"])
-    if with_interface:
-        oracle.interface_left(s["phiL"], s["A"], s["x"])
-        flops += f_local(s["a"], s["N"], s["b"], s["al"], s["be"])
-    dt = time.perf_counter() - t0
-    return flops, dt
-
-
 def cpu_model():
     try:
         for line in open("/proc/cpuinfo"):
@@ -239,6 +285,76 @@ def cpu_model():
     except Exception:
         pass
     return "unknown"
+
+
+def oracle_w34(inp):
+    """W34 on the oracle: every interface of both chains and one local matvec per core."""
+    import oracle
+    pl, pr = oracle.sweep_interfaces(inp.x, inp.A, 3)
+    ys = [oracle.local_matvec(pl[k], inp.A[k], pr[k + 1], inp.x[k]) for k in range(len(inp.x))]
+    return pl, pr, ys
+
+
+def oracle_configs(gpu_out, p64):
+    """Configs 1-4: the oracle (1 thread, pinned) on the full W34 workload, timed, and the max
+    relative Frobenius error of the GPU's W34 outputs against it."""
+    out = {}
+    for idx in (1, 2, 3, 4):
+        cfg = ttgen.CONFIGS[idx]
+        inp = ttgen.make_inputs(idx)
+        t0 = time.perf_counter()
+        pl, pr, ys = oracle_w34(inp)
+        dt = time.perf_counter() - t0
+        g = gpu_out[idx]
+        errs = [rel_err(g["phiL"][k], pl[k]) for k in range(cfg.d + 1)]
+        errs += [rel_err(g["phiR"][k], pr[k]) for k in range(cfg.d + 1)]
+        errs += [rel_err(g["y"][k], ys[k]) for k in range(cfg.d)]
+        f = w34_flops(cfg)
+        out[idx] = {"oracle_s": dt, "oracle_gflops": f / dt / 1e9, "max_rel_err": max(errs)}
+    return out
+
+
+def oracle_config5(gpu5, inp5):
+    """Config-5 parity sample + oracle rate at config-5 shapes: the left chain up to phiL[6],
+    the right chain down to phiR[7] (cores 0-5 / 7-11, including the rank-256 interior updates),
+    two Krylov columns of the core-6 matvec, and the apply z of cores 0-3, 11 plus a row slice
+    of core 6, all against the GPU's step outputs."""
+    import oracle
+    d, k = len(inp5.x), 6
+    t0 = time.perf_counter()
+    pl = [np.ones((1, 1, 1))]
+    for j in range(k):
+        pl.append(oracle.interface_left(pl[-1], inp5.A[j], inp5.x[j]))
+    pr = [np.ones((1, 1, 1))]
+    for j in range(d - 1, k, -1):
+        pr.insert(0, oracle.interface_right(pr[0], inp5.A[j], inp5.x[j]))
+    pr = [None] * (k + 1) + pr          # pr[j] for j = k+1 .. d
+    cols = [0, 21]
+    ycols = {m: oracle.local_matvec(pl[k], inp5.A[k], pr[k + 1],
+                                    np.ascontiguousarray(inp5.X[k][:, :, m, :])) for m in cols}
+    t1 = time.perf_counter()
+    cfg = ttgen.CONFIGS[5]
+    N, r, R = cfg.N, cfg.r, cfg.R
+    flops = sum(f_local(r[j], N, r[j + 1], R[j], R[j + 1]) for j in range(k)) \
+        + sum(f_local(r[j], N, r[j + 1], R[j], R[j + 1]) for j in range(k + 1, d)) \
+        + len(cols) * f_local(r[k], N, r[k + 1], R[k], R[k + 1])
+    errs = {"phiL": max(rel_err(gpu5["phiL"][j], pl[j]) for j in range(1, k + 1)),
+            "phiR": max(rel_err(gpu5["phiR"][j], pr[j]) for j in range(k + 1, d)),
+            "Y_core6_cols": max(rel_err(gpu5["Y6"][:, :, m, :], ycols[m]) for m in cols)}
+    ap = []
+    if gpu5.get("z") is not None:
+        for j in (0, 1, 2, 3, 11):
+            ap.append(rel_err(gpu5["z"][j], oracle.apply_core(inp5.x[j], inp5.A[j])))
+        a0, a1 = 100, 104     # rows (a, alpha) for a in [100, 104) of the core-6 z
+        zs = oracle.apply_core(np.ascontiguousarray(inp5.x[k][a0:a1]), inp5.A[k])
+        ap.append(rel_err(gpu5["z6_rows"], zs))
+        errs["apply_z"] = max(ap)
+    return {"oracle_s": t1 - t0, "oracle_gflop": flops / 1e9, "oracle_gflops": flops / (t1 - t0) / 1e9,
+            "errs": errs, "max_rel_err": max(errs.values()),
+            "sample": "config 5: left chain phiL[1..6] + right chain phiR[7..11] (11 interface "
+                      "updates incl. the rank-256 interior ones) + Krylov columns {0, 21} of the "
+                      "core-6 batched matvec; apply z of cores 0-3, 11 and rows a in [100,104) "
+                      "of core 6 (checked, not timed)"}
 
 
 def run_reference(args, rank):
@@ -272,6 +388,7 @@ def run_reference(args, rank):
                          "pinned_core": pin.core},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
+        "paper_context": PAPER_CONTEXT,
     }
     print(json.dumps(line), flush=True)
 
@@ -289,8 +406,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-apply", action="store_true", help="debug: skip H8 in the step")
-    ap.add_argument("--no-sweeps", action="store_true", help="skip the d=12 sweep timings")
-    ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--no-sweeps", action="store_true", help="skip everything after the e2e leg")
+    ap.add_argument("--no-next", action="store_true", help="skip the SURVEY 8(f) NEXT-row timings")
     ap.add_argument("--variant", type=int, default=-1, help="GEMM tiling variant (benchmark hook)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
@@ -313,6 +430,7 @@ def main():
     torch.cuda.set_device(dev)
     import paper_2509_11890_b200 as tt
     tt.tt_debug_set_variant(args.variant)
+    bw_gbs, bw_src = hbm_peak()
 
     cfg = ttgen.CONFIGS[args.config]
     work = w5_work(cfg)
@@ -329,29 +447,31 @@ def main():
     hx = [pin(c) for c in inp.x]
     hA = [pin(c) for c in inp.A]
     hX = [pin(c) for c in inp.X]
-    xs = [t.to(dev) for t in hx]
-    As = [t.to(dev) for t in hA]
-    Xs = [t.to(dev) for t in hX]
-    Yf = [torch.empty_like(X) for X in Xs]
-    phiL = tt.alloc_interfaces(xs, As)
-    phiR = tt.alloc_interfaces(xs, As)
-    tr = tt._Train(xs, As)
-    ws = torch.empty(tt.tt_sweep_als_workspace_size(tr, cfg.nvec), dtype=torch.uint8, device=dev)
-    zs = None
-    if not args.no_apply:
-        zs = [torch.empty((cfg.r[k] * cfg.R[k], cfg.N, cfg.r[k + 1] * cfg.R[k + 1]),
-                          dtype=torch.float64, device=dev) for k in range(d)]
-    hY = [torch.empty(Y.shape, dtype=torch.float64).pin_memory() for Y in Yf]
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
 
+    def dev_set():
+        s = {"x": [t.to(dev) for t in hx], "A": [t.to(dev) for t in hA],
+             "X": [t.to(dev) for t in hX]}
+        s["Y"] = [torch.empty_like(X) for X in s["X"]]
+        s["phiL"] = tt.alloc_interfaces(s["x"], s["A"])
+        s["phiR"] = tt.alloc_interfaces(s["x"], s["A"])
+        s["z"] = None if args.no_apply else [
+            torch.empty((cfg.r[k] * cfg.R[k], cfg.N, cfg.r[k + 1] * cfg.R[k + 1]),
+                        dtype=torch.float64, device=dev) for k in range(d)]
+        return s
+
+    S0 = dev_set()
+    tr = tt._Train(S0["x"], S0["A"])
+    ws = torch.empty(tt.tt_sweep_als_workspace_size(tr, cfg.nvec), dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
     launches = [0]
 
-    def step(bx=None, bA=None, bX=None, bY=None):
-        bx, bA, bX, bY = bx or xs, bA or As, bX or Xs, bY or Yf
-        tt.tt_sweep_als(bx, bA, bX, bY, None, phiL, phiR, workspace=ws, stream=stream)
+    def step(s, st=None):
+        st = st or stream
+        tt.tt_sweep_als(s["x"], s["A"], s["X"], s["Y"], None, s["phiL"], s["phiR"], workspace=ws,
+                        stream=st)
         n = tt.tt_last_launch_count()
-        if zs is not None:
-            tt.tt_operator_apply(bx, bA, zs, stream=stream)
+        if s["z"] is not None:
+            tt.tt_operator_apply(s["x"], s["A"], s["z"], stream=st)
             n += tt.tt_last_launch_count()
         launches[0] += n
 
@@ -371,11 +491,10 @@ def main():
 
     # ---- warm-up ----------------------------------------------------------------------
     for _ in range(args.warmup):
-        step()
+        step(S0)
     torch.cuda.synchronize(dev)
 
-    # ---- timed region -----------------------------------------------------------------
-    tt.tt_trace_enable(400 * (args.steps + 1))
+    # ---- timed region (library tracer OFF) ----------------------------------------------
     clocks = ClockSampler(local_rank)
     clocks.start()
     launches[0] = 0
@@ -387,7 +506,7 @@ def main():
     for i in range(args.steps):
         flush.zero_()   # L2 flush between timed steps, outside the step's events
         ev[i][0].record(stream)
-        step()
+        step(S0)
         ev[i][1].record(stream)
     torch.cuda.synchronize(dev)
     if world > 1:
@@ -395,14 +514,20 @@ def main():
     step_ms = [a.elapsed_time(b) for a, b in ev]
     clk = clocks.stop()
     gpu_launches = launches[0]
-    recs = [tt.tt_trace_read(i) for i in range(tt.tt_trace_count())]
-    tt.tt_trace_disable()
 
     total_ms = max_over_ranks(sum(step_ms), dev)
     ms_per_step = total_ms / args.steps
     value = whole_job_rate(work["step_flops"], world, args.steps, total_ms)
 
-    # ---- per-stage breakdown from the trace -----------------------------------------------
+    # ---- separate traced pass: per-launch durations (events on each launch's stream) -----
+    n_traced = 2
+    tt.tt_trace_enable(600 * n_traced)
+    for _ in range(n_traced):
+        flush.zero_()
+        step(S0)
+    torch.cuda.synchronize(dev)
+    recs = [tt.tt_trace_read(i) for i in range(tt.tt_trace_count())]
+    tt.tt_trace_disable()
     stages = {}
     for r in recs:
         s = stages.setdefault(r["stage"], {"launches": 0, "ms": 0.0, "flops": 0.0})
@@ -412,12 +537,11 @@ def main():
             s["flops"] += 2.0 * r["M"] * r["N"] * r["K"]
         elif r["stage"] == "apply":
             s["flops"] += 2.0 * r["M"] * r["N"]
-    traced_ms = sum(s["ms"] for s in stages.values())
     for s in stages.values():
-        s["ms_per_step"] = s["ms"] / args.steps
+        s["ms_per_step"] = s["ms"] / n_traced
+        s["launches_per_step"] = s["launches"] / n_traced
         s["tflops"] = s["flops"] / (s["ms"] * 1e-3) / 1e12 if s["ms"] > 0 else None
-        s["share"] = s["ms"] / traced_ms if traced_ms else None
-    dom_name = max((n for n in stages if n != "apply"), key=lambda n: stages[n]["ms"])
+    dom_name = max((n for n in stages if n.startswith("mv_")), key=lambda n: stages[n]["ms"])
     dom = stages[dom_name]
     mv_ms = sum(stages[n]["ms"] for n in ("mv_s1", "mv_s2", "mv_s3") if n in stages)
     mv_flops = sum(stages[n]["flops"] for n in ("mv_s1", "mv_s2", "mv_s3") if n in stages)
@@ -432,6 +556,11 @@ def main():
     roofline = {"bound": "tensor", "kernel": f"dmma_gemm ({dom_name})",
                 "achieved": dom["tflops"], "peak": p64_sustained, "unit": "TFLOP/s",
                 "frac": dom["tflops"] / p64_sustained, "traffic": traffic,
+                "per_launch": {"flops": dom["flops"] / dom["launches"],
+                               "ms": dom["ms"] / dom["launches"], "launches_per_step":
+                               dom["launches_per_step"]},
+                "timing": "separate traced pass after the timed region (tracer off there): CUDA "
+                          "events on the kernel's launch stream around each launch",
                 "peak_source": "FP64 DMMA probe kernel, measured in this run (sustained ~1 s); "
                                "MEASURED_PEAKS.json has no FP64 entry",
                 "peak_burst": p64_burst,
@@ -441,49 +570,72 @@ def main():
                 "frac_vs_datasheet": dom["tflops"] / 37.0}
     apply_detail = None
     if "apply" in stages:
-        ap_ms = stages["apply"]["ms"] / args.steps
+        ap_ms = stages["apply"]["ms_per_step"]
         apply_detail = {"ms_per_step": ap_ms, "bytes": work["apply_bytes"],
-                        "gbs": work["apply_bytes"] / (ap_ms * 1e-3) / 1e9}
+                        "gbs": work["apply_bytes"] / (ap_ms * 1e-3) / 1e9, "peak_gbs": bw_gbs,
+                        "frac": work["apply_bytes"] / (ap_ms * 1e-3) / 1e9 / bw_gbs,
+                        "peak_source": bw_src}
 
-    # ---- end to end through the public API from pinned host buffers ---------------------
-    # Every step copies its inputs (x, A, Krylov block) host->device and its result (the Y
-    # blocks) device->host inside the timed region.  The copies are double-buffered on two
-    # copy streams so that step i+1's upload and step i's download overlap step i's compute.
+    # device outputs of the timed step, for the config-5 parity sample (checked after timing)
+    gpu5 = {"phiL": [p.cpu().numpy() for p in S0["phiL"]],
+            "phiR": [p.cpu().numpy() for p in S0["phiR"]],
+            "Y6": S0["Y"][6].cpu().numpy() if d > 6 else None, "z": None}
+    if S0["z"] is not None:
+        gpu5["z"] = {j: S0["z"][j].cpu().numpy() for j in (0, 1, 2, 3, d - 1)}
+        gpu5["z6_rows"] = S0["z"][6][100 * cfg.R[6]:104 * cfg.R[6]].cpu().numpy()
+
+    # ---- end to end through the public API from/to pinned host buffers -----------------
+    # Every step copies its inputs (x, A, Krylov block) host->device and EVERY output (the Y
+    # blocks, the 12.3 GB unrounded apply z, all interfaces) device->host inside the timed
+    # region; device buffers are double-buffered so step i+1's upload and compute overlap
+    # step i's download on two copy streams.
     e2e = None
     if not args.no_e2e:
+        S1 = dev_set()
+        sets = [S0, S1]
+        outs = lambda s: s["Y"] + (s["z"] or []) + s["phiL"] + s["phiR"]
+        o_numel = [t.numel() for t in outs(S0)]
+        host_out = torch.empty(sum(o_numel), dtype=torch.float64)
+        registered = False
+        try:
+            rc = torch.cuda.cudart().cudaHostRegister(host_out.data_ptr(),
+                                                      host_out.numel() * 8, 0)
+            registered = int(rc) == 0 if not isinstance(rc, tuple) else int(rc[0]) == 0
+        except Exception:
+            registered = False
+        if not registered:
+            host_out = host_out.pin_memory()
+        host_views, off = [], 0
+        for t, nel in zip(outs(S0), o_numel):
+            host_views.append(host_out[off:off + nel].view(t.shape))
+            off += nel
         h2d = sum(t.numel() * 8 for t in hx + hA + hX)
-        d2h = sum(t.numel() * 8 for t in hY)
-        sets = [(xs, As, Xs, Yf),
-                ([torch.empty_like(t) for t in xs], [torch.empty_like(t) for t in As],
-                 [torch.empty_like(t) for t in Xs], [torch.empty_like(t) for t in Yf])]
-        hYs = [hY, [torch.empty(Y.shape, dtype=torch.float64).pin_memory() for Y in Yf]]
+        d2h = sum(o_numel) * 8
         up, down = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-        ev = lambda: torch.cuda.Event()
-        in_ready = [ev(), ev()]
-        done = [ev(), ev()]
-        out_done = [ev(), ev()]
+        evn = lambda: torch.cuda.Event()
+        in_ready, done, out_done = [evn(), evn()], [evn(), evn()], [evn(), evn()]
 
         def upload(i):
-            bx, bA, bX, _ = sets[i % 2]
+            s = sets[i % 2]
             with torch.cuda.stream(up):
                 if i >= 2:
                     up.wait_event(done[i % 2])        # step i-2 finished reading this set
-                for src, dst in zip(hx + hA + hX, bx + bA + bX):
+                for src, dst in zip(hx + hA + hX, s["x"] + s["A"] + s["X"]):
                     dst.copy_(src, non_blocking=True)
                 in_ready[i % 2].record(up)
 
         def run(i, nsteps):
-            bx, bA, bX, bY = sets[i % 2]
+            s = sets[i % 2]
             stream.wait_event(in_ready[i % 2])
             if i >= 2:
-                stream.wait_event(out_done[i % 2])   # step i-2's Y has been downloaded
-            step(bx, bA, bX, bY)
+                stream.wait_event(out_done[i % 2])   # step i-2's outputs have been downloaded
+            step(s)
             done[i % 2].record(stream)
             if i + 1 < nsteps:
                 upload(i + 1)
             with torch.cuda.stream(down):
                 down.wait_event(done[i % 2])
-                for src, dst in zip(bY, hYs[i % 2]):
+                for src, dst in zip(outs(s), host_views):
                     dst.copy_(src, non_blocking=True)
                 out_done[i % 2].record(down)
 
@@ -508,12 +660,126 @@ def main():
         e2e = {"value": whole_job_rate(work["step_flops"], world, args.steps, e_ms),
                "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": e_ms / args.steps,
-               "note": "H2D of x, A and the Krylov block and D2H of the Y blocks every step, "
-                       "double-buffered on two copy streams (overlapping compute)"}
+               "d2h_breakdown_bytes": {"Y": sum(t.numel() for t in S0["Y"]) * 8,
+                                       "z": sum(t.numel() for t in (S0["z"] or [])) * 8,
+                                       "interfaces": sum(t.numel() for t in S0["phiL"] + S0["phiR"]) * 8},
+               "host_buffer": "cudaHostRegister" if registered else "torch pinned",
+               "note": "H2D of x, A and the Krylov block and D2H of every output (Y blocks, the "
+                       "unrounded apply z, all interfaces) every step; device buffers double-"
+                       "buffered, copies on two copy streams overlapping the neighbouring steps' "
+                       "compute; bound by the D2H of z over PCIe"}
+        if registered:
+            torch.cuda.cudart().cudaHostUnregister(host_out.data_ptr())
+        del S1, sets, host_views, host_out
+        torch.cuda.empty_cache()
 
-    # ---- local GMRES on the interior core (m = 10, one cycle) ----------
-    gm = None
+    # ---- per-config lines: W34 for configs 1-4, W5 for config 5 ---------
+    configs = {}
+    gpu_out = {}
+    latency = None
     if not args.no_sweeps:
+        for idx in (1, 2, 3, 4):
+            c = ttgen.CONFIGS[idx]
+            ii = ttgen.make_inputs(idx)
+            xs = [torch.from_numpy(t).to(dev) for t in ii.x]
+            As = [torch.from_numpy(t).to(dev) for t in ii.A]
+            pl, pr = tt.alloc_interfaces(xs, As), tt.alloc_interfaces(xs, As)
+            ys = [torch.empty_like(t) for t in xs]
+            w = torch.empty(tt.tt_sweep_w34_workspace_size(tt._Train(xs, As)), dtype=torch.uint8,
+                            device=dev)
+
+            def w34(st, xs=xs, As=As, pl=pl, pr=pr, ys=ys, w=w):
+                tt.tt_sweep_w34(xs, As, pl, pr, ys, workspace=w, stream=st)
+            t = time_sweep(tt, w34, stream, dev, reps=20)
+            torch.cuda.synchronize(dev)
+            gpu_out[idx] = {"phiL": [p.cpu().numpy() for p in pl],
+                            "phiR": [p.cpu().numpy() for p in pr],
+                            "y": [y.cpu().numpy() for y in ys]}
+            fa, fx, B = w34_flops(c), w34_executed_flops(c), w34_bytes(c)
+            ms = t["graph_ms_median"]
+            line = {"workload": f"W34 (tt_sweep_w34): d={c.d}, r={max(c.r)}, R={max(c.R)}",
+                    "ms_graph": ms, "ms_eager": t["eager_ms_median"],
+                    "ms_graph_best": t["graph_ms_best"], "launches": t["launches"],
+                    "gflop": fa / 1e9, "executed_gflop": fx / 1e9, "algorithmic_mb": B / 1e6,
+                    "gflops": fx / (ms * 1e-3) / 1e9}
+            rx = roof(fx, B, ms, p64_sustained, bw_gbs)
+            ra = roof(fa, B, ms, p64_sustained, bw_gbs)
+            line.update({"frac_of_roofline": rx["frac"], "t_roof_ms": rx["t_roof_ms"],
+                         "bound": rx["bound"], "frac_of_roofline_survey_flops": ra["frac"],
+                         "eager_over_graph": t["eager_ms_median"] / ms})
+            if idx <= 2:
+                line["note"] = "latency-bound (SURVEY §8(d)): absolute time and launches"
+            configs[idx] = line
+            del xs, As, pl, pr, ys, w
+        # config 5: W5 sweep alone (graph / eager) and the timed step
+        def w5(st):
+            tt.tt_sweep_als(S0["x"], S0["A"], S0["X"], S0["Y"], None, S0["phiL"], S0["phiR"],
+                            workspace=ws, stream=st)
+        t = time_sweep(tt, w5, stream, dev, reps=3)
+        sw_f = work["matvec_flops"] + work["interface_flops"]
+        r5 = roof(sw_f, work["sweep_bytes"], t["graph_ms_median"], p64_sustained, bw_gbs)
+        rs = roof(work["step_flops"], work["sweep_bytes"] + work["apply_bytes"], ms_per_step,
+                  p64_sustained, bw_gbs)
+        configs[5] = {"workload": "W5 (tt_sweep_als, K=32) + tt_operator_apply = the bench step",
+                      "step_ms": ms_per_step, "step_launches": gpu_launches / args.steps,
+                      "step_gflops": value / world, "step_frac_of_roofline": rs["frac"],
+                      "w5_ms_graph": t["graph_ms_median"], "w5_ms_eager": t["eager_ms_median"],
+                      "w5_launches": t["launches"], "w5_gflop": sw_f / 1e9,
+                      "w5_gflops": sw_f / (t["graph_ms_median"] * 1e-3) / 1e9,
+                      "w5_frac_of_roofline": r5["frac"],
+                      "batched_matvec_frac_of_p64_traced": mv_tf / p64_sustained}
+
+        # ---- latency regime: K = 1 matvec and GMRES at config-3/4 interior shapes ---------
+        latency = {}
+        for idx, k in ((3, 5), (4, 6)):
+            c = ttgen.CONFIGS[idx]
+            a, b, al, be, N = c.r[k], c.r[k + 1], c.R[k], c.R[k + 1], c.N
+            gen = torch.Generator(device=dev).manual_seed(31 + idx)
+            rnd = lambda *sh: torch.randn(*sh, dtype=torch.float64, device=dev, generator=gen)
+            phL, A_, phR = rnd(a, al, a) / a, rnd(al, N, N, be) / al, rnd(b, be, b) / b
+            # diagonally dominant local operator so GMRES is well posed
+            phL[:, 0, :] += torch.eye(a, dtype=torch.float64, device=dev) * 4
+            phR[:, 0, :] += torch.eye(b, dtype=torch.float64, device=dev)
+            A_[0, :, :, 0] += torch.eye(N, dtype=torch.float64, device=dev)
+            x1 = rnd(a, N, b)
+            y1 = torch.empty_like(x1)
+            wm = torch.empty(tt.tt_local_matvec_workspace_size(a, N, b, al, be, 1),
+                             dtype=torch.uint8, device=dev)
+            t = time_sweep(tt, lambda st: tt.tt_local_matvec(phL, A_, phR, x1, y1, workspace=wm,
+                                                             stream=st), stream, dev, reps=50)
+            f1 = f_local(a, N, b, al, be)
+            b1 = b_local_matvec(a, N, b, al, be, 1)
+            r1 = roof(f1, b1, t["graph_ms_median"], p64_sustained, bw_gbs)
+            ent = {"shape": {"a": a, "b": b, "alpha": al, "beta": be, "N": N, "core": k},
+                   "matvec_k1": {"us_graph": t["graph_ms_median"] * 1e3,
+                                 "us_eager": t["eager_ms_median"] * 1e3,
+                                 "launches": t["launches"], "mflop": f1 / 1e6,
+                                 "gflops": f1 / (t["graph_ms_median"] * 1e-3) / 1e9,
+                                 "frac_of_roofline": r1["frac"]}}
+            m_g = 10
+            F1 = rnd(a, N, 1, b)
+            X1 = torch.zeros_like(F1)
+            wg = torch.empty(tt.tt_local_gmres_workspace_size(a, N, b, al, be, 1, m_g),
+                             dtype=torch.uint8, device=dev)
+            rr_ = torch.empty(1, dtype=torch.float64, device=dev)
+            it_ = torch.empty(1, dtype=torch.int64, device=dev)
+
+            def gm1(st):
+                X1.zero_()
+                tt.tt_local_gmres(phL, A_, phR, F1, X1, m=m_g, cycles=1, tol=0.0, rel_res=rr_,
+                                  iters=it_, workspace=wg, stream=st)
+            t = time_sweep(tt, gm1, stream, dev, reps=10)
+            ent["gmres_k1"] = {"m": m_g, "cycles": 1, "ms_graph": t["graph_ms_median"],
+                               "ms_eager": t["eager_ms_median"], "launches": t["launches"],
+                               "us_per_arnoldi_step": t["graph_ms_median"] * 1e3 / m_g,
+                               "matvec_gflop": (m_g + 1) * f1 / 1e9,
+                               "rel_res": float(rr_.item())}
+            latency[f"config{idx}"] = ent
+
+    # ---- SURVEY 8(f) NEXT rows on the config-5 interior core ----------------------------
+    xs, As, Xs, phiL, phiR, Yf = S0["x"], S0["A"], S0["X"], S0["phiL"], S0["phiR"], S0["Y"]
+    gm = kkt = two = lob = rnd_info = None
+    if not (args.no_sweeps or args.no_next):
         k = cfg.d // 2
         m_g = 10
         rl, nn, rr = cfg.r[k], cfg.N, cfg.r[k + 1]
@@ -539,13 +805,8 @@ def main():
               "tflops": (mv_f + orth_f) / (t["graph_ms_median"] * 1e-3) / 1e12,
               "matvec_share_of_flops": mv_f / (mv_f + orth_f),
               "frac_of_p64": (mv_f + orth_f) / (t["graph_ms_median"] * 1e-3) / 1e12 / p64_sustained}
+        del Xg, wsg
 
-    # ---- SURVEY 8(f) rows 2 and 4 on the interior core: KKT block action, two-site matvec --
-    kkt = two = None
-    if not args.no_sweeps:
-        k = cfg.d // 2
-        rl, nn, rr = cfg.r[k], cfg.N, cfg.r[k + 1]
-        Rl, Rr = cfg.R[k], cfg.R[k + 1]
         gen = torch.Generator(device=dev).manual_seed(11)
         rnd = lambda *sh: torch.randn(*sh, dtype=torch.float64, device=dev, generator=gen)
         ops = [(rnd(rl, Rl, rl), rnd(Rl, nn, nn, Rr), rnd(rr, Rr, rr)) for _ in range(8)]
@@ -562,7 +823,6 @@ def main():
                "ms": t["graph_ms_median"], "gflop": f9 / 1e9,
                "tflops": f9 / (t["graph_ms_median"] * 1e-3) / 1e12,
                "frac_of_p64": f9 / (t["graph_ms_median"] * 1e-3) / 1e12 / p64_sustained}
-        # two-site (DMRG supercore) matvec: 2x2 modes (N = 4), bonds of the interior core
         A1, A2 = rnd(Rl, 2, 2, Rl), rnd(Rl, 2, 2, Rr)
         W2 = rnd(rl, 2, 2, cfg.nvec, rr)
         Y2 = torch.empty_like(W2)
@@ -576,19 +836,13 @@ def main():
         two = {"core": k, "n1": 2, "n2": 2, "nvec": cfg.nvec, "ms": t["graph_ms_median"],
                "gflop": f2 / 1e9, "tflops": f2 / (t["graph_ms_median"] * 1e-3) / 1e12,
                "frac_of_p64": f2 / (t["graph_ms_median"] * 1e-3) / 1e12 / p64_sustained}
+        del ops, wsk, ws2, W2, Y2
 
-    # ---- block LOBPCG of the step-length eigenproblem (interior core) ---
-    lob = None
-    if not args.no_sweeps:
-        k = cfg.d // 2
-        rl, nn, rr = cfg.r[k], cfg.N, cfg.r[k + 1]
-        Rl, Rr = cfg.R[k], cfg.R[k + 1]
         gen = torch.Generator(device=dev).manual_seed(12)
         rnd = lambda *sh: torch.randn(*sh, dtype=torch.float64, device=dev, generator=gen)
         sym_if = lambda r, R: (lambda t: (t + t.transpose(0, 2)) / 2)(rnd(r, R, r))
         sym_core = lambda: (lambda t: (t + t.transpose(1, 2)) / 2)(rnd(Rl, nn, nn, Rr))
         opA = (sym_if(rl, Rl), sym_core(), sym_if(rr, Rr))
-        # L_B = I + 0.01 (symmetric perturbation): SPD, operator ranks as the interior core's
         pLB, ALB, pRB = 0.1 * sym_if(rl, Rl), 0.1 * sym_core(), 0.1 * sym_if(rr, Rr)
         pLB[:, 0, :] += torch.eye(rl, dtype=torch.float64, device=dev)
         pRB[:, 0, :] += torch.eye(rr, dtype=torch.float64, device=dev)
@@ -615,7 +869,6 @@ def main():
                                    refresh=20)
             t = time_sweep(tt, lob_run, stream, dev, reps=3)
             nops = 2 if oB is not None else 1
-            # matvecs: initial (1 block), one per iteration, refresh (2 blocks) every 20
             nblocks = 1 + its_l + 2 * ((its_l - 1) // 20)
             mv_f = nops * nblocks * nb_l * f_local(rl, nn, rr, Rl, Rr)
             lob[name] = {"ms": t["graph_ms_median"], "ms_eager": t["eager_ms_median"],
@@ -624,36 +877,20 @@ def main():
                          "matvec_tflops_over_total_time": mv_f / (t["graph_ms_median"] * 1e-3) / 1e12,
                          "frac_of_p64": mv_f / (t["graph_ms_median"] * 1e-3) / 1e12 / p64_sustained}
 
-    # ---- TT rounding of the config-5 vector train (delta = 1e-4) --------
-    rnd_info = None
-    if not args.no_sweeps:
-        torch.cuda.synchronize(dev)
-        t0 = time.perf_counter()
-        rounded = tt.tt_round(xs, 1e-4)
-        torch.cuda.synchronize(dev)
-        t1 = time.perf_counter()
-        rts = []
-        for _ in range(3):
-            t = time.perf_counter()
-            rounded = tt.tt_round(xs, 1e-4)
-            torch.cuda.synchronize(dev)
-            rts.append((time.perf_counter() - t) * 1e3)
-        rnd_info = {"delta": 1e-4, "ranks_in": list(cfg.r),
-                    "ranks_out": [1] + [int(c.shape[2]) for c in rounded],
-                    "ms": sorted(rts)[1], "ms_all": rts, "ms_first": (t1 - t0) * 1e3,
-                    "note": "synchronous (data-dependent ranks); host wall time, median of 3 "
-                            "after one warm-up call (the first includes allocator growth)"}
-        # the other row-3 steps at the interior core: left orthonormalisation of the train,
-        # the block-index move with the 4-component KKT block index, AMEn enrichment
+        # TT rounding of the config-5 vector train (delta = 1e-4) and the other row-3 steps
         def wall(fn, reps=2):
             fn()
             torch.cuda.synchronize(dev)
-            t = time.perf_counter()
+            t0 = time.perf_counter()
             for _ in range(reps):
                 fn()
             torch.cuda.synchronize(dev)
-            return (time.perf_counter() - t) / reps * 1e3
-        k = cfg.d // 2
+            return (time.perf_counter() - t0) / reps * 1e3
+        rounded = tt.tt_round(xs, 1e-4)
+        rnd_info = {"delta": 1e-4, "ranks_in": list(cfg.r),
+                    "ranks_out": [1] + [int(c.shape[2]) for c in rounded],
+                    "ms": wall(lambda: tt.tt_round(xs, 1e-4), reps=3),
+                    "note": "synchronous (data-dependent ranks); host wall time"}
         gen = torch.Generator(device=dev).manual_seed(13)
         rnd = lambda *sh: torch.randn(*sh, dtype=torch.float64, device=dev, generator=gen)
         Wh = rnd(cfg.r[k], cfg.N, 4, cfg.r[k + 1])
@@ -664,73 +901,31 @@ def main():
         rnd_info["row3_shapes"] = {"block_move": [cfg.r[k], cfg.N, 4, cfg.r[k + 1]],
                                    "enrich": [cfg.r[k], cfg.N, cfg.r[k + 1], 32]}
 
-    # ---- full sweeps at d = 12 (metric's second half), eager and as a CUDA graph ---------
-    sweeps = None
-    if not args.no_sweeps:
-        sweeps = {}
-        # config 5, W5 (tt_sweep_als) without the apply: the timed step's sweep part
-        def w5(st):
-            tt.tt_sweep_als(xs, As, Xs, Yf, None, phiL, phiR, workspace=ws, stream=st)
-        sweeps["config5_W5"] = time_sweep(tt, w5, stream, dev, reps=3)
-        # config 4, W34: all right interfaces, all left interfaces, one matvec per core
-        inp4 = ttgen.make_inputs(4)
-        x4 = [torch.from_numpy(c).to(dev) for c in inp4.x]
-        A4 = [torch.from_numpy(c).to(dev) for c in inp4.A]
-        pl4 = tt.alloc_interfaces(x4, A4)
-        pr4 = tt.alloc_interfaces(x4, A4)
-        y4 = [torch.empty_like(c) for c in x4]
-        tr4 = tt._Train(x4, A4)
-        ws4 = torch.empty(tt.tt_sweep_workspace_size(tr4), dtype=torch.uint8, device=dev)
-        wsm4 = torch.empty(max(tt.tt_local_matvec_workspace_size(c.shape[0], c.shape[1], c.shape[2],
-                                                                 A.shape[0], A.shape[3], 1)
-                               for c, A in zip(x4, A4)), dtype=torch.uint8, device=dev)
-
-        def w34(st):
-            tt.tt_sweep_interfaces(x4, A4, pl4, pr4, workspace=ws4, stream=st)
-            for k in range(len(x4)):
-                tt.tt_local_matvec(pl4[k], A4[k], pr4[k + 1], x4[k], y4[k], workspace=wsm4,
-                                   stream=st)
-        sweeps["config4_W34_separate_calls"] = time_sweep(tt, w34, stream, dev, reps=20)
-        # the same workload as one DAG-scheduled call (matvecs overlap the interface chains)
-        ws34 = torch.empty(tt.tt_sweep_w34_workspace_size(tr4), dtype=torch.uint8, device=dev)
-
-        def w34_dag(st):
-            tt.tt_sweep_w34(x4, A4, pl4, pr4, y4, workspace=ws34, stream=st)
-        sweeps["config4_W34"] = time_sweep(tt, w34_dag, stream, dev, reps=20)
-        f34 = bench_w34_flops(ttgen.CONFIGS[4])
-        x34 = w34_executed_flops(ttgen.CONFIGS[4])
-        sw = sweeps["config4_W34"]
-        sw["gflop"] = f34 / 1e9                     # three-stage matvec per core
-        sw["executed_gflop"] = x34 / 1e9            # matvecs reuse the left updates' T2_k
-        sw["tflops_graph"] = x34 / (sw["graph_ms_median"] * 1e-3) / 1e12
-        sw["frac_of_p64"] = sw["tflops_graph"] / p64_sustained
-        sw["note"] = ("tflops/frac on executed FLOPs; each matvec is its last stage on the kept "
-                      "T2_k of the left update at core k (debug bit 23 restores three stages)")
-        # config 3 (d = 10) W34 as well
-        inp3 = ttgen.make_inputs(3)
-        x3 = [torch.from_numpy(c).to(dev) for c in inp3.x]
-        A3 = [torch.from_numpy(c).to(dev) for c in inp3.A]
-        pl3, pr3 = tt.alloc_interfaces(x3, A3), tt.alloc_interfaces(x3, A3)
-        y3 = [torch.empty_like(c) for c in x3]
-        ws3 = torch.empty(tt.tt_sweep_w34_workspace_size(tt._Train(x3, A3)), dtype=torch.uint8,
-                          device=dev)
-
-        def w34_c3(st):
-            tt.tt_sweep_w34(x3, A3, pl3, pr3, y3, workspace=ws3, stream=st)
-        sweeps["config3_W34"] = time_sweep(tt, w34_c3, stream, dev, reps=20)
-        sweeps["config3_W34"]["gflop"] = bench_w34_flops(ttgen.CONFIGS[3]) / 1e9
-        sweeps["config3_W34"]["executed_gflop"] = w34_executed_flops(ttgen.CONFIGS[3]) / 1e9
-
-    # ---- CPU oracle baseline (rank 0, N=1) ----------------------------------------------
+    # ---- CPU oracle: baseline + per-config timings and parity (rank 0, N=1) ---------------
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config == 5:
+        import oracle
+        oracle.build()
         with pinned_one_core() as pin:
-            fl, dt = time_oracle_sample(True)
-        cpu = {"value": fl / dt / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": "tt_oracle_local_matvec (1 Krylov column) + tt_oracle_interface_left at "
-                         "config-5 interior-core shapes (a=b=256, alpha=beta=36, N=4), "
-                         f"{fl / 1e9:.1f} GFLOP in {dt:.1f} s",
-               "cpu": cpu_model(), "compiler": "gcc -O2 -std=c99", "pinned_core": pin.core}
+            o5 = oracle_config5(gpu5, inp)
+            oc = oracle_configs(gpu_out, p64_sustained) if gpu_out else {}
+        ext_s = work["step_flops"] / (o5["oracle_gflops"] * 1e9)
+        cpu = {"value": o5["oracle_gflops"], "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": o5["sample"] + f"; {o5['oracle_gflop']:.1f} GFLOP in "
+                                        f"{o5['oracle_s']:.1f} s",
+               "cpu": cpu_model(), "compiler": "gcc -O2 -std=c99", "pinned_core": pin.core,
+               "w5_step_extrapolated_s": ext_s,
+               "w5_step_extrapolation_note": "EXTRAPOLATED (not run): the bench step's "
+                                             f"{work['step_flops'] / 1e9:.0f} GFLOP at the "
+                                             "measured config-5 oracle rate"}
+        for idx, o in oc.items():
+            configs[idx].update({"oracle_s": o["oracle_s"], "oracle_gflops": o["oracle_gflops"],
+                                 "max_rel_err": o["max_rel_err"]})
+        if 5 in configs:
+            configs[5].update({"max_rel_err": o5["max_rel_err"], "parity": o5["errs"],
+                               "parity_sample": o5["sample"],
+                               "oracle_gflops": o5["oracle_gflops"],
+                               "oracle_w5_step_s_extrapolated": ext_s})
 
     if rank == 0:
         line = {
@@ -744,26 +939,29 @@ def main():
                        "step_gflop": work["step_flops"] / 1e9,
                        "l2": "flushed between timed steps (256 MiB memset outside step events); "
                              "inputs 0.43 GB > L2",
+                       "tracer": "off in the timed region",
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": gpu_launches,
             "clocks": clk,
-            "sweeps_d12": sweeps,
+            "configs": configs,
+            "latency": latency,
             "local_gmres": gm,
             "kkt_block_action": kkt,
             "two_site_matvec": two,
             "tt_round": rnd_info,
             "local_lobpcg": lob,
+            "paper_context": PAPER_CONTEXT,
             "detail": {
-                "full_sweep_ms": (total_ms / args.steps) - (apply_detail["ms_per_step"]
-                                                            if apply_detail else 0.0),
-                "batched_matvec_tflops": mv_tf,
-                "batched_matvec_frac_of_p64": mv_tf / p64_sustained,
+                "full_sweep_ms": ms_per_step - (apply_detail["ms_per_step"] if apply_detail else 0.0),
+                "batched_matvec_tflops_traced": mv_tf,
+                "batched_matvec_frac_of_p64_traced": mv_tf / p64_sustained,
                 "p64_tflops_sustained": p64_sustained, "p64_tflops_burst": p64_burst,
+                "hbm_gbs": bw_gbs, "hbm_source": bw_src,
                 "apply": apply_detail,
-                "stages": stages,
+                "stages_traced": stages,
                 "step_ms": step_ms,
                 "work_gflop": {k: v / 1e9 for k, v in work.items() if k.endswith("flops")},
             },

@@ -162,6 +162,33 @@ def _dev(t: torch.Tensor, name: str) -> int:
     return t.data_ptr()
 
 
+def _expect(t: torch.Tensor, shape, name: str) -> None:
+    """Shape check before any pointer reaches the library: the C-ABI takes its extents from
+    the x / A arguments, so a wrongly shaped phi / output would be read or written out of
+    bounds."""
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if tuple(t.shape) != tuple(int(v) for v in shape):
+        raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(int(v) for v in shape)}")
+
+
+def _same_device(*ts) -> None:
+    """All tensors of one call must live on one CUDA device."""
+    devs = {t.device for t in ts if isinstance(t, torch.Tensor)}
+    if len(devs) > 1:
+        raise ValueError(f"tensors of one call are on different devices: {sorted(map(str, devs))}")
+
+
+def _check_local(phiL, A, phiR, rl, n, rr, nbra_l=None, nbra_r=None) -> None:
+    """phiL (rl_bra,Rl,rl), A (Rl,n,n,Rr), phiR (rr_bra,Rr,rr) against the core's (rl, n, rr)."""
+    if A.dim() != 4:
+        raise ValueError(f"A must be 4-D (Rl, n, n, Rr), got shape {tuple(A.shape)}")
+    Rl, Rr = A.shape[0], A.shape[3]
+    _expect(A, (Rl, n, n, Rr), "A")
+    _expect(phiL, (rl if nbra_l is None else nbra_l, Rl, rl), "phiL")
+    _expect(phiR, (rr if nbra_r is None else nbra_r, Rr, rr), "phiR")
+
+
 def _stream(stream) -> int:
     if stream is None:
         return torch.cuda.current_stream().cuda_stream
@@ -188,10 +215,15 @@ def tt_interface_workspace_size(rl, n, rr, Rl, Rr) -> int:
 
 def tt_local_matvec(phiL, A, phiR, x, y=None, workspace=None, stream=None):
     """H1-H3: y = local matvec of core x.  Returns y."""
+    if x.dim() != 3:
+        raise ValueError(f"x must be (rl, n, rr), got shape {tuple(x.shape)}")
     rl, n, rr = x.shape
+    _check_local(phiL, A, phiR, rl, n, rr)
     Rl, Rr = A.shape[0], A.shape[3]
     if y is None:
         y = torch.empty_like(x)
+    _expect(y, x.shape, "y")
+    _same_device(phiL, A, phiR, x, y, workspace)
     ws = _ws(tt_local_matvec_workspace_size(rl, n, rr, Rl, Rr, 1), workspace, x.device)
     _check(lib.tt_local_matvec(rl, n, rr, Rl, Rr, _dev(phiL, "phiL"), _dev(A, "A"),
                                _dev(phiR, "phiR"), _dev(x, "x"), _dev(y, "y"), ws.data_ptr(),
@@ -201,10 +233,15 @@ def tt_local_matvec(phiL, A, phiR, x, y=None, workspace=None, stream=None):
 
 def tt_local_matvec_batched(phiL, A, phiR, X, Y=None, workspace=None, stream=None):
     """H4: the local matvec on every column of a Block-TT core X (rl,n,nvec,rr)."""
+    if X.dim() != 4:
+        raise ValueError(f"X must be (rl, n, nvec, rr), got shape {tuple(X.shape)}")
     rl, n, nvec, rr = X.shape
+    _check_local(phiL, A, phiR, rl, n, rr)
     Rl, Rr = A.shape[0], A.shape[3]
     if Y is None:
         Y = torch.empty_like(X)
+    _expect(Y, X.shape, "Y")
+    _same_device(phiL, A, phiR, X, Y, workspace)
     ws = _ws(tt_local_matvec_workspace_size(rl, n, rr, Rl, Rr, nvec), workspace, X.device)
     _check(lib.tt_local_matvec_batched(rl, n, rr, Rl, Rr, nvec, _dev(phiL, "phiL"), _dev(A, "A"),
                                        _dev(phiR, "phiR"), _dev(X, "X"), _dev(Y, "Y"),
@@ -214,10 +251,16 @@ def tt_local_matvec_batched(phiL, A, phiR, X, Y=None, workspace=None, stream=Non
 
 def tt_interface_left(phiL_prev, A, x, out=None, workspace=None, stream=None):
     """H5: phiL_next (rr,Rr,rr) from phiL_prev (rl,Rl,rl), A_k, x_k."""
+    if x.dim() != 3 or A.dim() != 4:
+        raise ValueError("x must be (rl, n, rr) and A (Rl, n, n, Rr)")
     rl, n, rr = x.shape
     Rl, Rr = A.shape[0], A.shape[3]
+    _expect(A, (Rl, n, n, Rr), "A")
+    _expect(phiL_prev, (rl, Rl, rl), "phiL_prev")
     if out is None:
         out = torch.empty((rr, Rr, rr), dtype=x.dtype, device=x.device)
+    _expect(out, (rr, Rr, rr), "phiL_next")
+    _same_device(phiL_prev, A, x, out, workspace)
     ws = _ws(tt_interface_workspace_size(rl, n, rr, Rl, Rr), workspace, x.device)
     _check(lib.tt_interface_left(rl, n, rr, Rl, Rr, _dev(phiL_prev, "phiL_prev"), _dev(A, "A"),
                                  _dev(x, "x"), _dev(out, "phiL_next"), ws.data_ptr(), ws.numel(),
@@ -227,10 +270,16 @@ def tt_interface_left(phiL_prev, A, x, out=None, workspace=None, stream=None):
 
 def tt_interface_right(phiR_next, A, x, out=None, workspace=None, stream=None):
     """H6: phiR_prev (rl,Rl,rl) from phiR_next (rr,Rr,rr), A_k, x_k."""
+    if x.dim() != 3 or A.dim() != 4:
+        raise ValueError("x must be (rl, n, rr) and A (Rl, n, n, Rr)")
     rl, n, rr = x.shape
     Rl, Rr = A.shape[0], A.shape[3]
+    _expect(A, (Rl, n, n, Rr), "A")
+    _expect(phiR_next, (rr, Rr, rr), "phiR_next")
     if out is None:
         out = torch.empty((rl, Rl, rl), dtype=x.dtype, device=x.device)
+    _expect(out, (rl, Rl, rl), "phiR_prev")
+    _same_device(phiR_next, A, x, out, workspace)
     ws = _ws(tt_interface_workspace_size(rl, n, rr, Rl, Rr), workspace, x.device)
     _check(lib.tt_interface_right(rl, n, rr, Rl, Rr, _dev(phiR_next, "phiR_next"), _dev(A, "A"),
                                   _dev(x, "x"), _dev(out, "phiR_prev"), ws.data_ptr(), ws.numel(),
@@ -243,16 +292,58 @@ class _Train:
 
     def __init__(self, x_cores: Sequence[torch.Tensor], A_cores: Sequence[torch.Tensor]):
         self.d = len(x_cores)
-        if len(A_cores) != self.d:
-            raise ValueError("x_cores and A_cores must have the same length")
+        if len(A_cores) != self.d or self.d == 0:
+            raise ValueError("x_cores and A_cores must be non-empty and of the same length")
+        for k in range(self.d):
+            if x_cores[k].dim() != 3 or A_cores[k].dim() != 4:
+                raise ValueError(f"core {k}: x must be (r, n, r') and A (R, n, n, R')")
+            n = x_cores[k].shape[1]
+            if A_cores[k].shape[1] != n or A_cores[k].shape[2] != n:
+                raise ValueError(f"core {k}: A mode sizes {tuple(A_cores[k].shape[1:3])} do not "
+                                 f"match the vector mode size {n}")
+            if k + 1 < self.d:
+                if x_cores[k].shape[2] != x_cores[k + 1].shape[0]:
+                    raise ValueError(f"vector bond {k + 1}: core {k} has {x_cores[k].shape[2]}, "
+                                     f"core {k + 1} has {x_cores[k + 1].shape[0]}")
+                if A_cores[k].shape[3] != A_cores[k + 1].shape[0]:
+                    raise ValueError(f"operator bond {k + 1}: core {k} has {A_cores[k].shape[3]}, "
+                                     f"core {k + 1} has {A_cores[k + 1].shape[0]}")
+        _same_device(*x_cores, *A_cores)
         self.n = [int(c.shape[1]) for c in x_cores]
         self.r = [int(c.shape[0]) for c in x_cores] + [int(x_cores[-1].shape[-1])]
         self.R = [int(c.shape[0]) for c in A_cores] + [int(A_cores[-1].shape[3])]
         self._n = (ctypes.c_int64 * self.d)(*self.n)
         self._r = (ctypes.c_int64 * (self.d + 1))(*self.r)
         self._R = (ctypes.c_int64 * (self.d + 1))(*self.R)
-        self._x = _ptrs(x_cores, "x_cores")
-        self._A = _ptrs(A_cores, "A_cores")
+        self._xc, self._Ac = x_cores, A_cores
+
+    @property
+    def _x(self):   # pointer arrays built at call time, after every shape check
+        return _ptrs(self._xc, "x_cores")
+
+    @property
+    def _A(self):
+        return _ptrs(self._Ac, "A_cores")
+
+
+def _check_interfaces(tr: "_Train", phis, name: str) -> None:
+    if phis is None:
+        return
+    if len(phis) != tr.d + 1:
+        raise ValueError(f"{name} must hold d+1 = {tr.d + 1} interfaces")
+    for k, p in enumerate(phis):
+        _expect(p, (tr.r[k], tr.R[k], tr.r[k]), f"{name}[{k}]")
+
+
+def _check_cores(tr: "_Train", cores, name: str, nvec=None) -> None:
+    if cores is None:
+        return
+    if len(cores) != tr.d:
+        raise ValueError(f"{name} must hold d = {tr.d} cores")
+    for k, c in enumerate(cores):
+        shape = (tr.r[k], tr.n[k], tr.r[k + 1]) if nvec is None else \
+            (tr.r[k], tr.n[k], nvec, tr.r[k + 1])
+        _expect(c, shape, f"{name}[{k}]")
 
 
 def _ptrs(ts: Sequence[torch.Tensor], name: str):
@@ -282,6 +373,8 @@ def tt_sweep_interfaces(x_cores, A_cores, phiL=None, phiR=None, directions=TT_SW
         phiL = alloc_interfaces(x_cores, A_cores)
     if phiR is None and directions & TT_SWEEP_RIGHT:
         phiR = alloc_interfaces(x_cores, A_cores)
+    _check_interfaces(tr, phiL if directions & TT_SWEEP_LEFT else None, "phiL")
+    _check_interfaces(tr, phiR if directions & TT_SWEEP_RIGHT else None, "phiR")
     ws = _ws(tt_sweep_workspace_size(tr), workspace, x_cores[0].device)
     pl = _ptrs(phiL, "phiL") if phiL is not None else None
     pr = _ptrs(phiR, "phiR") if phiR is not None else None
@@ -305,6 +398,9 @@ def tt_sweep_w34(x_cores, A_cores, phiL=None, phiR=None, y_cores=None, workspace
         phiR = alloc_interfaces(x_cores, A_cores)
     if y_cores is None:
         y_cores = [torch.empty_like(c) for c in x_cores]
+    _check_interfaces(tr, phiL, "phiL")
+    _check_interfaces(tr, phiR, "phiR")
+    _check_cores(tr, y_cores, "y_cores")
     ws = _ws(tt_sweep_w34_workspace_size(tr), workspace, x_cores[0].device)
     _check(lib.tt_sweep_w34(tr.d, tr._n, tr._r, tr._R, tr._x, tr._A, _ptrs(phiL, "phiL"),
                             _ptrs(phiR, "phiR"), _ptrs(y_cores, "y_cores"), ws.data_ptr(),
@@ -324,6 +420,11 @@ def tt_sweep_als(x_cores, A_cores, X_blocks, Y_fwd=None, Y_bwd=None, phiL=None, 
         phiL = alloc_interfaces(x_cores, A_cores)
     if phiR is None:
         phiR = alloc_interfaces(x_cores, A_cores)
+    _check_cores(tr, X_blocks, "X_blocks", nvec)
+    _check_cores(tr, Y_fwd, "Y_fwd", nvec)
+    _check_cores(tr, Y_bwd, "Y_bwd", nvec)
+    _check_interfaces(tr, phiL, "phiL")
+    _check_interfaces(tr, phiR, "phiR")
     ws = _ws(tt_sweep_als_workspace_size(tr, nvec), workspace, x_cores[0].device)
     _check(lib.tt_sweep_als(tr.d, tr._n, tr._r, tr._R, nvec, tr._x, tr._A,
                             _ptrs(X_blocks, "X_blocks"), _ptrs(Y_fwd, "Y_fwd"),
@@ -336,6 +437,17 @@ def tt_sweep_als(x_cores, A_cores, X_blocks, Y_fwd=None, Y_bwd=None, phiL=None, 
 def tt_operator_apply(x_cores, A_cores, z_cores=None, stream=None):
     """H8: unrounded TT-matrix x TT-vector product; returns z cores (r R, n_row, r' R')."""
     d = len(x_cores)
+    if len(A_cores) != d or d == 0:
+        raise ValueError("x_cores and A_cores must be non-empty and of the same length")
+    for k in range(d):
+        if x_cores[k].dim() != 3 or A_cores[k].dim() != 4:
+            raise ValueError(f"core {k}: x must be (r, n_col, r') and A (R, n_row, n_col, R')")
+        if A_cores[k].shape[2] != x_cores[k].shape[1]:
+            raise ValueError(f"core {k}: A column mode {A_cores[k].shape[2]} != x mode "
+                             f"{x_cores[k].shape[1]}")
+        if k + 1 < d and (x_cores[k].shape[2] != x_cores[k + 1].shape[0]
+                          or A_cores[k].shape[3] != A_cores[k + 1].shape[0]):
+            raise ValueError(f"bond {k + 1}: neighbouring cores disagree")
     n_row = [int(c.shape[1]) for c in A_cores]
     n_col = [int(c.shape[2]) for c in A_cores]
     r = [int(c.shape[0]) for c in x_cores] + [int(x_cores[-1].shape[2])]
@@ -343,6 +455,11 @@ def tt_operator_apply(x_cores, A_cores, z_cores=None, stream=None):
     if z_cores is None:
         z_cores = [torch.empty((r[k] * R[k], n_row[k], r[k + 1] * R[k + 1]), dtype=torch.float64,
                                device=x_cores[0].device) for k in range(d)]
+    if len(z_cores) != d:
+        raise ValueError(f"z_cores must hold d = {d} cores")
+    for k in range(d):
+        _expect(z_cores[k], (r[k] * R[k], n_row[k], r[k + 1] * R[k + 1]), f"z_cores[{k}]")
+    _same_device(*x_cores, *A_cores, *z_cores)
     a64 = lambda v: (ctypes.c_int64 * len(v))(*v)
     _check(lib.tt_operator_apply(d, a64(n_row), a64(n_col), a64(r), a64(R),
                                  _ptrs(x_cores, "x_cores"), _ptrs(A_cores, "A_cores"),
@@ -406,14 +523,21 @@ def tt_local_gmres(phiL, A, phiR, F, X=None, m=20, cycles=1, tol=0.0, rel_res=No
     operator for every column of the Block-TT right-hand side F (rl, n, nvec, rr)
     (PAPER.md:488).  X: initial guess (zeros if None), overwritten with the iterate.
     Returns (X, rel_res, iters) (device tensors)."""
+    if F.dim() != 4:
+        raise ValueError(f"F must be (rl, n, nvec, rr), got shape {tuple(F.shape)}")
     rl, n, nvec, rr = F.shape
+    _check_local(phiL, A, phiR, rl, n, rr)
     Rl, Rr = A.shape[0], A.shape[3]
     if X is None:
         X = torch.zeros_like(F)
+    _expect(X, F.shape, "X")
     if rel_res is None:
         rel_res = torch.empty(nvec, dtype=torch.float64, device=F.device)
     if iters is None:
         iters = torch.empty(nvec, dtype=torch.int64, device=F.device)
+    _expect(rel_res, (nvec,), "rel_res")
+    _expect(iters, (nvec,), "iters")
+    _same_device(phiL, A, phiR, F, X, rel_res, iters, workspace)
     ws = _ws(tt_local_gmres_workspace_size(rl, n, rr, Rl, Rr, nvec, m, k_aug), workspace, F.device)
     if iters.dtype != torch.int64 or not iters.is_cuda:
         raise TypeError("iters must be a CUDA int64 tensor")
@@ -434,11 +558,16 @@ def tt_local_lobpcg(opA, X, opB=None, maxiter=100, tol=1e-10, lam=None, res=None
     (PAPER.md:556-567).  opA, opB: (phiL, A, phiR) triplets of device tensors; opB None means
     L_B = I.  X (rl, n, nb, rr): initial block, overwritten with the Ritz vectors.
     Returns (X, lam, res, iters, step) (device tensors; step = min(1, 1/lam[0]) or 1)."""
+    if X.dim() != 4:
+        raise ValueError(f"X must be (rl, n, nb, rr), got shape {tuple(X.shape)}")
     rl, n, nb, rr = X.shape
     phiLA, AA, phiRA = opA
+    _check_local(phiLA, AA, phiRA, rl, n, rr)
     RlA, RrA = AA.shape[0], AA.shape[3]
     if opB is not None:
         phiLB, AB, phiRB = opB
+        _check_local(phiLB, AB, phiRB, rl, n, rr)
+        _same_device(phiLB, AB, phiRB)
         RlB, RrB = AB.shape[0], AB.shape[3]
         pB = (_dev(phiLB, "phiL_B"), _dev(AB, "A_B"), _dev(phiRB, "phiR_B"))
     else:
@@ -449,8 +578,13 @@ def tt_local_lobpcg(opA, X, opB=None, maxiter=100, tol=1e-10, lam=None, res=None
     res = torch.empty(nb, dtype=torch.float64, device=dev) if res is None else res
     iters = torch.empty(1, dtype=torch.int64, device=dev) if iters is None else iters
     step = torch.empty(1, dtype=torch.float64, device=dev) if step is None else step
+    _expect(lam, (nb,), "lam")
+    _expect(res, (nb,), "res")
+    _expect(iters, (1,), "iters")
+    _expect(step, (1,), "step")
     if iters.dtype != torch.int64 or not iters.is_cuda:
         raise TypeError("iters must be a CUDA int64 tensor")
+    _same_device(phiLA, AA, phiRA, X, lam, res, iters, step, workspace)
     ws = _ws(tt_local_lobpcg_workspace_size(rl, n, rr, RlA, RrA, RlB, RrB, nb), workspace, dev)
     _check(lib.tt_local_lobpcg(rl, n, rr, RlA, RrA, RlB, RrB, nb, int(maxiter), int(refresh),
                                float(tol),
@@ -463,10 +597,16 @@ def tt_local_lobpcg(opA, X, opB=None, maxiter=100, tol=1e-10, lam=None, res=None
 
 def tt_merge_operator_cores(A1, A2, A12=None, stream=None):
     """Two-site supercore operator A12 (Rl, n1 n2, n1 n2, Rr) from A1 (Rl,n1,n1,Rm), A2 (Rm,n2,n2,Rr)."""
+    if A1.dim() != 4 or A2.dim() != 4:
+        raise ValueError("A1 and A2 must be 4-D operator cores")
     Rl, n1, _, Rm = A1.shape
     _, n2, _, Rr = A2.shape
+    _expect(A1, (Rl, n1, n1, Rm), "A1")
+    _expect(A2, (Rm, n2, n2, Rr), "A2")
     if A12 is None:
         A12 = torch.empty((Rl, n1 * n2, n1 * n2, Rr), dtype=torch.float64, device=A1.device)
+    _expect(A12, (Rl, n1 * n2, n1 * n2, Rr), "A12")
+    _same_device(A1, A2, A12)
     _check(lib.tt_merge_operator_cores(Rl, n1, n2, Rm, Rr, _dev(A1, "A1"), _dev(A2, "A2"),
                                        _dev(A12, "A12"), _stream(stream)))
     return A12
@@ -480,10 +620,18 @@ def tt_local_matvec_two_site(phiL, A1, A2, phiR, W, Y=None, workspace=None, stre
     """Two-site (DMRG supercore) local matvec; W, Y (rl, n1, n2, nvec, rr) or (rl, n1, n2, rr)."""
     single = W.dim() == 4
     Wv = W.unsqueeze(3) if single else W
+    if Wv.dim() != 5 or A1.dim() != 4 or A2.dim() != 4:
+        raise ValueError("W must be (rl, n1, n2, [nvec,] rr), A1/A2 4-D operator cores")
     rl, n1, n2, nvec, rr = Wv.shape
     Rl, Rm, Rr = A1.shape[0], A1.shape[3], A2.shape[3]
+    _expect(A1, (Rl, n1, n1, Rm), "A1")
+    _expect(A2, (Rm, n2, n2, Rr), "A2")
+    _expect(phiL, (rl, Rl, rl), "phiL")
+    _expect(phiR, (rr, Rr, rr), "phiR")
     if Y is None:
         Y = torch.empty_like(W)
+    _expect(Y, W.shape, "Y")
+    _same_device(phiL, A1, A2, phiR, W, Y, workspace)
     ws = _ws(tt_local_matvec_two_site_workspace_size(rl, n1, n2, rr, Rl, Rm, Rr, nvec), workspace,
              W.device)
     _check(lib.tt_local_matvec_two_site(rl, n1, n2, rr, Rl, Rm, Rr, nvec, _dev(phiL, "phiL"),
@@ -501,11 +649,23 @@ def tt_block_local_matvec_workspace_size(rl, n, rr, Rl, Rr) -> int:
 def tt_block_local_matvec(ops, terms, X, Y=None, workspace=None, stream=None):
     """Projected KKT block action.  ops: list of (phiL, A, phiR) device
     tensors sharing the frame; terms: list of (row, col, op, op2, coeff); X (rl, n, nb, rr)."""
+    if X.dim() != 4:
+        raise ValueError(f"X must be (rl, n, nblocks, rr), got shape {tuple(X.shape)}")
     rl, n, nb, rr = X.shape
+    for o, (pL, Ao, pR) in enumerate(ops):
+        try:
+            _check_local(pL, Ao, pR, rl, n, rr)
+        except ValueError as e:
+            raise ValueError(f"operator {o}: {e}") from None
+    for (row, col, op, op2, _cf) in terms:
+        if not (0 <= row < nb and 0 <= col < nb and 0 <= op < len(ops) and -1 <= op2 < len(ops)):
+            raise ValueError(f"term {(row, col, op, op2)} indexes outside {nb} blocks / {len(ops)} ops")
     Rl = [int(o[1].shape[0]) for o in ops]
     Rr = [int(o[1].shape[3]) for o in ops]
     if Y is None:
         Y = torch.empty_like(X)
+    _expect(Y, X.shape, "Y")
+    _same_device(X, Y, workspace, *[t for o in ops for t in o])
     a64 = lambda v: (ctypes.c_int64 * len(v))(*v)
     T = (TTBlockTerm * max(len(terms), 1))(*[TTBlockTerm(int(r), int(c), int(o), int(o2), float(cf))
                                              for (r, c, o, o2, cf) in terms])
@@ -524,6 +684,7 @@ def tt_round(cores, delta, max_rank=0, workspace=None, stream=None):
     accuracy delta.  Synchronous.  Returns the list of rounded cores."""
     d = len(cores)
     a64 = lambda v: (ctypes.c_int64 * len(v))(*v)
+    _check_vector_train(cores)
     n = [int(c.shape[1]) for c in cores]
     r = [int(c.shape[0]) for c in cores] + [int(cores[-1].shape[2])]
     outs = [torch.empty_like(c) for c in cores]
@@ -534,6 +695,18 @@ def tt_round(cores, delta, max_rank=0, workspace=None, stream=None):
     ro = list(rout)
     return [outs[k].reshape(-1)[: ro[k] * n[k] * ro[k + 1]].reshape(ro[k], n[k], ro[k + 1])
             for k in range(d)]
+
+
+def _check_vector_train(cores) -> None:
+    if len(cores) == 0:
+        raise ValueError("empty train")
+    for k, c in enumerate(cores):
+        if c.dim() != 3:
+            raise ValueError(f"core {k} must be (r, n, r'), got shape {tuple(c.shape)}")
+        if k + 1 < len(cores) and c.shape[2] != cores[k + 1].shape[0]:
+            raise ValueError(f"bond {k + 1}: core {k} has {c.shape[2]}, core {k + 1} has "
+                             f"{cores[k + 1].shape[0]}")
+    _same_device(*cores)
 
 
 def tt_orthonormalise_workspace_size(n, r) -> int:
@@ -547,6 +720,7 @@ def tt_orthonormalise(cores, direction=TT_SWEEP_LEFT, workspace=None, stream=Non
     list of cores (bonds shrink only where the train is exactly rank deficient)."""
     d = len(cores)
     a64 = lambda v: (ctypes.c_int64 * len(v))(*v)
+    _check_vector_train(cores)
     n = [int(c.shape[1]) for c in cores]
     r = [int(c.shape[0]) for c in cores] + [int(cores[-1].shape[2])]
     outs = [torch.empty_like(c) for c in cores]
@@ -568,6 +742,9 @@ def tt_block_move_workspace_size(r0, n0, l, r1, n1, r2) -> int:
 def tt_block_move_right(Wk_hat, Wk1, delta=0.0, max_rank=0, workspace=None, stream=None):
     """Move the block index of Wk_hat (r0,n0,l,r1) into Wk1 (r1,n1,r2) by one truncated SVD
     step (PAPER.md:303).  Returns (Wk (r0,n0,s) left-orthonormal, Wk1_hat (s,n1,l,r2))."""
+    if Wk_hat.dim() != 4 or Wk1.dim() != 3 or Wk1.shape[0] != Wk_hat.shape[3]:
+        raise ValueError("Wk_hat must be (r0, n0, l, r1) and Wk1 (r1, n1, r2)")
+    _same_device(Wk_hat, Wk1, workspace)
     r0, n0, l, r1 = Wk_hat.shape
     _, n1, r2 = Wk1.shape
     smax = min(r0 * n0, l * r1)
@@ -586,6 +763,9 @@ def tt_block_move_right(Wk_hat, Wk1, delta=0.0, max_rank=0, workspace=None, stre
 def tt_block_move_left(Wkm1, Wk_hat, delta=0.0, max_rank=0, workspace=None, stream=None):
     """Move the block index of Wk_hat (r1,n1,l,r2) into Wkm1 (r0,n0,r1).
     Returns (Wkm1_hat (r0,n0,l,s), Wk (s,n1,r2) right-orthonormal)."""
+    if Wkm1.dim() != 3 or Wk_hat.dim() != 4 or Wk_hat.shape[0] != Wkm1.shape[2]:
+        raise ValueError("Wkm1 must be (r0, n0, r1) and Wk_hat (r1, n1, l, r2)")
+    _same_device(Wkm1, Wk_hat, workspace)
     r0, n0, r1 = Wkm1.shape
     _, n1, l, r2 = Wk_hat.shape
     smax = min(r1 * l, n1 * r2)
@@ -610,12 +790,17 @@ def tt_local_matvec_pg(phiL, A, phiR, X, Y=None, workspace=None, stream=None):
     phiR (rr_bra, Rr, rr), X (rl, n, nvec, rr) or (rl, n, rr) -> Y (rl_bra, n, [nvec,] rr_bra)."""
     single = X.dim() == 3
     Xv = X.unsqueeze(2) if single else X
+    if Xv.dim() != 4 or phiL.dim() != 3 or phiR.dim() != 3:
+        raise ValueError("X must be (rl, n, [nvec,] rr); phiL, phiR 3-D")
     rl, n, nvec, rr = Xv.shape
     rlb, rrb = phiL.shape[0], phiR.shape[0]
+    _check_local(phiL, A, phiR, rl, n, rr, rlb, rrb)
     Rl, Rr = A.shape[0], A.shape[3]
+    shape = (rlb, n, rrb) if single else (rlb, n, nvec, rrb)
     if Y is None:
-        shape = (rlb, n, rrb) if single else (rlb, n, nvec, rrb)
         Y = torch.empty(shape, dtype=torch.float64, device=X.device)
+    _expect(Y, shape, "Y")
+    _same_device(phiL, A, phiR, X, Y, workspace)
     ws = _ws(tt_pg_workspace_size(rlb, rl, n, rrb, rr, Rl, Rr, nvec), workspace, X.device)
     _check(lib.tt_local_matvec_pg(rlb, rl, n, rrb, rr, Rl, Rr, nvec, _dev(phiL, "phiL"), _dev(A, "A"),
                                   _dev(phiR, "phiR"), _dev(X, "X"), _dev(Y, "Y"), ws.data_ptr(),
@@ -627,8 +812,13 @@ def tt_interface_left_pg(phiL_prev, A, x_bra, x_ket, out=None, workspace=None, s
     rlb, n, rrb = x_bra.shape
     rl, _, rr = x_ket.shape
     Rl, Rr = A.shape[0], A.shape[3]
+    _expect(x_ket, (rl, n, rr), "x_ket")
+    _expect(A, (Rl, n, n, Rr), "A")
+    _expect(phiL_prev, (rlb, Rl, rl), "phiL_prev")
     if out is None:
         out = torch.empty((rrb, Rr, rr), dtype=torch.float64, device=x_ket.device)
+    _expect(out, (rrb, Rr, rr), "phiL_next")
+    _same_device(phiL_prev, A, x_bra, x_ket, out, workspace)
     ws = _ws(tt_pg_workspace_size(rlb, rl, n, rrb, rr, Rl, Rr, 1), workspace, x_ket.device)
     _check(lib.tt_interface_left_pg(rlb, rl, n, rrb, rr, Rl, Rr, _dev(phiL_prev, "phiL_prev"),
                                     _dev(A, "A"), _dev(x_bra, "x_bra"), _dev(x_ket, "x_ket"),
@@ -641,8 +831,13 @@ def tt_interface_right_pg(phiR_next, A, x_bra, x_ket, out=None, workspace=None, 
     rlb, n, rrb = x_bra.shape
     rl, _, rr = x_ket.shape
     Rl, Rr = A.shape[0], A.shape[3]
+    _expect(x_ket, (rl, n, rr), "x_ket")
+    _expect(A, (Rl, n, n, Rr), "A")
+    _expect(phiR_next, (rrb, Rr, rr), "phiR_next")
     if out is None:
         out = torch.empty((rlb, Rl, rl), dtype=torch.float64, device=x_ket.device)
+    _expect(out, (rlb, Rl, rl), "phiR_prev")
+    _same_device(phiR_next, A, x_bra, x_ket, out, workspace)
     ws = _ws(tt_pg_workspace_size(rlb, rl, n, rrb, rr, Rl, Rr, 1), workspace, x_ket.device)
     _check(lib.tt_interface_right_pg(rlb, rl, n, rrb, rr, Rl, Rr, _dev(phiR_next, "phiR_next"),
                                      _dev(A, "A"), _dev(x_bra, "x_bra"), _dev(x_ket, "x_ket"),
@@ -658,8 +853,14 @@ def tt_enrich_right_workspace_size(rl, n, rx, rz, n1, r2) -> int:
 def tt_enrich_right(x_k, z_k, x_k1, delta=0.0, max_rank=0, workspace=None, stream=None):
     """AMEn enrichment: [x_k | z_k] re-orthonormalised, x_{k+1} padded and
     rotated.  Returns (x_k' (rl, n, s) left-orthonormal, x_{k+1}' (s, n1, r2))."""
+    if x_k.dim() != 3 or z_k.dim() != 3 or x_k1.dim() != 3:
+        raise ValueError("x_k, z_k, x_k1 must be 3-D cores")
     rl, n, rx = x_k.shape
     rz = z_k.shape[2]
+    _expect(z_k, (rl, n, rz), "z_k")
+    if x_k1.shape[0] != rx:
+        raise ValueError(f"x_k1 left bond {x_k1.shape[0]} != x_k right bond {rx}")
+    _same_device(x_k, z_k, x_k1, workspace)
     _, n1, r2 = x_k1.shape
     smax = min(rl * n, rx + rz)
     xo = torch.empty(rl * n * smax, dtype=torch.float64, device=x_k.device)
