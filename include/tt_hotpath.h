@@ -402,7 +402,7 @@ void tt_debug_set_variant(int v);
  * operator-core stage with the whole A-hat resident in shared memory (3-deep T1 ring;
  * measured slower, kept as a probe).
  * tt_debug_set_variant(v): v >= 10 forces
- * the GEMM tile configuration v % 100 (probe list in tt_hotpath.cu) and split-K factor v / 100. */
+ * the GEMM tile configuration v % 100 (probe list in csrc/tt_launch_tpl.cuh) and split-K factor v / 100. */
 void tt_debug_set_flags(int flags);
 
 /* ---------------------------------------------------------------------------------------

@@ -175,6 +175,8 @@ def _expect(t: torch.Tensor, shape, name: str) -> None:
 def _same_device(*ts) -> None:
     """All tensors of one call must live on one CUDA device."""
     devs = {t.device for t in ts if isinstance(t, torch.Tensor)}
+    if len(devs) > 1 and any(dv.type != "cuda" for dv in devs):
+        raise TypeError("every tensor must be a CUDA float64 tensor (no CPU fallback)")
     if len(devs) > 1:
         raise ValueError(f"tensors of one call are on different devices: {sorted(map(str, devs))}")
 

@@ -1,0 +1,894 @@
+// tt_api.cu — C-ABI entry points of the hot path (include/tt_hotpath.h): local matvecs,
+// interface updates, sweeps (W34 / W5), the unrounded apply, tracing and the FP64 probe.
+#include "tt_internal.cuh"
+
+using namespace ttint;
+
+namespace ttint {
+// H8: z[(a,al), i, (b,be)] = sum_j A[al,i,j,be] x[a,j,b].  One CTA per (a, al) pair; the
+// x[a,:,:] and A[al,:,:,:] slices are staged in shared memory; the output rows (one per i,
+// each rr*Rr contiguous doubles) are written with streaming (evict-first) stores.
+__global__ void __launch_bounds__(256) apply_kernel(const double* __restrict__ x,
+                                                    const double* __restrict__ A,
+                                                    double* __restrict__ z, int rl, int ni,
+                                                    int nj, int rr, int Rl, int Rr) {
+  extern __shared__ double sm[];
+  double* xs = sm;                       // [nj][rr]
+  double* As = sm + (size_t)nj * rr;     // [ni][nj][Rr]
+  const long long pair = blockIdx.x;     // a * Rl + al
+  const int a = (int)(pair / Rl), al = (int)(pair % Rl);
+  const int xn = nj * rr, an = ni * nj * Rr;
+  for (int e = threadIdx.x; e < xn; e += blockDim.x) xs[e] = x[(long long)a * xn + e];
+  for (int e = threadIdx.x; e < an; e += blockDim.x) As[e] = A[(long long)al * an + e];
+  __syncthreads();
+  const int L = rr * Rr;
+  const int step_b = blockDim.x / Rr, step_be = blockDim.x % Rr;
+  for (int i = 0; i < ni; ++i) {
+    double* zrow = z + (pair * ni + i) * (long long)L;
+    const double* Ai = As + (size_t)i * nj * Rr;
+    int b = threadIdx.x / Rr, be = threadIdx.x % Rr;
+    for (int e = threadIdx.x; e < L; e += blockDim.x) {
+      double s = 0.0;
+      for (int j = 0; j < nj; ++j) s = fma(Ai[j * Rr + be], xs[j * rr + b], s);
+      __stcs(zrow + e, s);
+      b += step_b;
+      be += step_be;
+      if (be >= Rr) {
+        be -= Rr;
+        ++b;
+      }
+    }
+  }
+}
+
+// H8, register-blocked: thread <-> one output column e = (b, beta) of the z rows; the thread
+// keeps x[a, :, b] for AB consecutive a in registers and walks (alpha, i), reading the nj
+// operator values A[alpha, i, :, beta] (L1-resident, coalesced across the warp's betas) once
+// per AB outputs.  Every warp store is 32 consecutive doubles of one z row (evict-first).
+template <int NJ, int AB>
+__global__ void __launch_bounds__(256) apply_reg_kernel(const double* __restrict__ x,
+                                                        const double* __restrict__ A,
+                                                        double* __restrict__ z, int rl, int ni,
+                                                        int rr, int Rl, int Rr, int az) {
+  const long long L = (long long)rr * Rr;
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= L) return;
+  const int b = (int)(e / Rr), be = (int)(e - (long long)b * Rr);
+  const int a0 = blockIdx.y * AB;
+  // operator bond indices [al0, al1): split over blockIdx.z when the core is small
+  const int al0 = blockIdx.z * az, al1 = min(Rl, al0 + az);
+  double xv[AB][NJ];
+#pragma unroll
+  for (int u = 0; u < AB; ++u)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+      xv[u][j] = (a0 + u < rl) ? __ldg(x + ((long long)(a0 + u) * NJ + j) * rr + b) : 0.0;
+  for (int al = al0; al < al1; ++al)
+  for (int i = 0; i < ni; ++i) {
+    double av[NJ];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) av[j] = __ldg(A + ((long long)(al * ni + i) * NJ + j) * Rr + be);
+#pragma unroll
+    for (int u = 0; u < AB; ++u) {
+      if (a0 + u < rl) {
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) s = fma(av[j], xv[u][j], s);
+        __stcs(z + (((long long)(a0 + u) * Rl + al) * ni + i) * L + e, s);
+      }
+    }
+  }
+}
+
+template <int NJ>
+cudaError_t launch_apply_reg(const double* x, const double* A, double* z, long long rl,
+                             long long ni, long long rr, long long Rl, long long Rr,
+                             cudaStream_t s) {
+  constexpr int AB = 4;
+  const long long L = rr * Rr;
+  const long long gx = (L + 255) / 256, gy = (rl + AB - 1) / AB;
+  // enough CTAs to fill the machine, but as many bond indices per thread as possible
+  long long az = (gx * gy * Rl) / 4096;
+  az = az < 1 ? 1 : (az > Rl ? Rl : az);
+  dim3 grid((unsigned)gx, (unsigned)gy, (unsigned)((Rl + az - 1) / az));
+  apply_reg_kernel<NJ, AB><<<grid, 256, 0, s>>>(x, A, z, (int)rl, (int)ni, (int)rr, (int)Rl,
+                                                (int)Rr, (int)az);
+  return cudaGetLastError();
+}
+
+// FP64 DMMA throughput probe: 8 independent accumulator chains per warp.
+__global__ void __launch_bounds__(256) dmma_probe_kernel(double* out, long long iters) {
+  double c[8][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = 0.0;
+  const double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
+  for (long long it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) tt::dmma_8x8x4(c[i], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+  if (s == -1.0) out[threadIdx.x] = s;   // never true; keeps the loop live
+}
+
+}  // namespace ttint
+
+extern "C" {
+
+const char* tt_status_string(tt_status s) {
+  switch (s) {
+    case TT_OK: return "TT_OK";
+    case TT_ERR_INVALID_ARGUMENT: return "TT_ERR_INVALID_ARGUMENT";
+    case TT_ERR_NULL_POINTER: return "TT_ERR_NULL_POINTER";
+    case TT_ERR_ALIASING: return "TT_ERR_ALIASING";
+    case TT_ERR_WORKSPACE: return "TT_ERR_WORKSPACE";
+    case TT_ERR_OVERFLOW: return "TT_ERR_OVERFLOW";
+    case TT_ERR_CUDA: return "TT_ERR_CUDA";
+  }
+  return "TT_UNKNOWN_STATUS";
+}
+
+const char* tt_last_error_message(void) { return g_msg.c_str(); }
+const char* tt_version(void) { return "tt_hotpath 0.1 (sm_100a, FP64 DMMA)"; }
+int64_t tt_last_launch_count(void) { return g_launches_last; }
+void tt_debug_force_v1(int on) { g_force_v1 = on; }
+void tt_debug_set_variant(int v) {
+  g_variant = v;
+  g_force_ks = v >= 10 ? v / 100 : 0;
+}
+void tt_debug_set_flags(int f) {
+  g_dbg_flags = f;
+  g_side_lowprio = (f & 2048) ? 1 : 0;
+}
+
+size_t tt_local_matvec_workspace_size(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t Rr,
+                                      int64_t nvec) {
+  Dims d{rl, n, rr, Rl, Rr};
+  long long t1, t2, ah, pe;
+  if (!dims_valid(d) || nvec <= 0 || !matvec_ws_elems(d, nvec, t1, t2, ah, pe)) return 0;
+  return ws_bytes({t1, t2, ah, pe});
+}
+
+tt_status tt_local_matvec_batched(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t Rr,
+                                  int64_t nvec, const double* phiL, const double* A,
+                                  const double* phiR, const double* X, double* Y,
+                                  void* workspace, size_t workspace_bytes, void* stream) {
+  CallScope scope;
+  Dims d{rl, n, rr, Rl, Rr};
+  tt_status st = check_dims(d);
+  if (st != TT_OK) return st;
+  if (nvec <= 0) return fail(TT_ERR_INVALID_ARGUMENT, "nvec must be positive");
+  if (!phiL || !A || !phiR || !X || !Y) return fail(TT_ERR_NULL_POINTER, "NULL tensor pointer");
+  if (same(Y, phiL) || same(Y, A) || same(Y, phiR) || same(Y, X))
+    return fail(TT_ERR_ALIASING, "output Y aliases an input");
+  long long t1, t2, ah, pe;
+  if (!matvec_ws_elems(d, nvec, t1, t2, ah, pe)) return fail(TT_ERR_OVERFLOW, "workspace overflow");
+  const size_t need = ws_bytes({t1, t2, ah, pe});
+  if (!workspace || workspace_bytes < need)
+    return fail(TT_ERR_WORKSPACE, "workspace NULL or smaller than " + std::to_string(need) + " bytes");
+  if (same(workspace, Y) || same(workspace, X) || same(workspace, phiL) || same(workspace, phiR) ||
+      same(workspace, A))
+    return fail(TT_ERR_ALIASING, "workspace aliases a tensor");
+  Carver c{static_cast<char*>(workspace), workspace_bytes};
+  double* T1 = c.take(t1);
+  double* T2 = c.take(t2);
+  double* Ah = c.take(ah);
+  double* Pp = c.take(pe);
+  if (!c.ok) return fail(TT_ERR_WORKSPACE, "workspace too small after alignment");
+  cudaError_t e = enqueue_matvec(d, nvec, phiL, A, phiR, X, Y, T1, T2, Ah, Pp, pe,
+                                 static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "tt_local_matvec_batched");
+  return TT_OK;
+}
+
+tt_status tt_local_matvec(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t Rr,
+                          const double* phiL, const double* A, const double* phiR,
+                          const double* x, double* y, void* workspace, size_t workspace_bytes,
+                          void* stream) {
+  return tt_local_matvec_batched(rl, n, rr, Rl, Rr, 1, phiL, A, phiR, x, y, workspace,
+                                 workspace_bytes, stream);
+}
+
+size_t tt_interface_workspace_size(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t Rr) {
+  Dims d{rl, n, rr, Rl, Rr};
+  long long t1, t2, ah, pe;
+  if (!dims_valid(d) || !iface_ws_elems(d, t1, t2, ah, pe)) return 0;
+  return ws_bytes({t1, t2, ah, pe});
+}
+
+static tt_status iface_common(bool left, int64_t rl, int64_t n, int64_t rr, int64_t Rl,
+                              int64_t Rr, const double* phi_in, const double* A,
+                              const double* x, double* phi_out, void* workspace,
+                              size_t workspace_bytes, void* stream) {
+  Dims d{rl, n, rr, Rl, Rr};
+  tt_status st = check_dims(d);
+  if (st != TT_OK) return st;
+  if (!phi_in || !A || !x || !phi_out) return fail(TT_ERR_NULL_POINTER, "NULL tensor pointer");
+  if (same(phi_out, phi_in) || same(phi_out, A) || same(phi_out, x))
+    return fail(TT_ERR_ALIASING, "output interface aliases an input");
+  long long t1, t2, ah, pe;
+  if (!iface_ws_elems(d, t1, t2, ah, pe)) return fail(TT_ERR_OVERFLOW, "workspace overflow");
+  const size_t need = ws_bytes({t1, t2, ah, pe});
+  if (!workspace || workspace_bytes < need)
+    return fail(TT_ERR_WORKSPACE, "workspace NULL or smaller than " + std::to_string(need) + " bytes");
+  if (same(workspace, phi_out) || same(workspace, phi_in) || same(workspace, x) ||
+      same(workspace, A))
+    return fail(TT_ERR_ALIASING, "workspace aliases a tensor");
+  Carver c{static_cast<char*>(workspace), workspace_bytes};
+  double* T1 = c.take(t1);
+  double* T2 = c.take(t2);
+  double* Ah = c.take(ah);
+  double* Pp = c.take(pe);
+  if (!c.ok) return fail(TT_ERR_WORKSPACE, "workspace too small after alignment");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = left ? enqueue_left(d, phi_in, A, x, phi_out, T1, T2, Ah, Pp, pe, s)
+                       : (g_dbg_flags & 8) ? enqueue_right(d, phi_in, A, x, phi_out, T1, T2, Ah, Pp, pe, s)
+                                            : enqueue_right_mirror(d, phi_in, A, x, phi_out, T1, T2, Ah, Pp, pe, s);
+  if (e != cudaSuccess) return cuda_fail(e, left ? "tt_interface_left" : "tt_interface_right");
+  return TT_OK;
+}
+
+tt_status tt_interface_left(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t Rr,
+                            const double* phiL_prev, const double* A, const double* x,
+                            double* phiL_next, void* workspace, size_t workspace_bytes,
+                            void* stream) {
+  CallScope scope;
+  return iface_common(true, rl, n, rr, Rl, Rr, phiL_prev, A, x, phiL_next, workspace,
+                      workspace_bytes, stream);
+}
+
+tt_status tt_interface_right(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t Rr,
+                             const double* phiR_next, const double* A, const double* x,
+                             double* phiR_prev, void* workspace, size_t workspace_bytes,
+                             void* stream) {
+  CallScope scope;
+  return iface_common(false, rl, n, rr, Rl, Rr, phiR_next, A, x, phiR_prev, workspace,
+                      workspace_bytes, stream);
+}
+
+// ---- sweeps ------------------------------------------------------------------------------
+static tt_status check_train(int64_t d, const int64_t* n, const int64_t* r, const int64_t* R) {
+  if (d <= 0) return fail(TT_ERR_INVALID_ARGUMENT, "d must be >= 1");
+  if (!n || !r || !R) return fail(TT_ERR_NULL_POINTER, "NULL shape array");
+  if (r[0] != 1 || r[d] != 1) return fail(TT_ERR_INVALID_ARGUMENT, "r_1 and r_{d+1} must be 1");
+  if (R[0] != 1 || R[d] != 1) return fail(TT_ERR_INVALID_ARGUMENT, "R_1 and R_{d+1} must be 1");
+  for (int64_t k = 0; k < d; ++k) {
+    Dims dk{r[k], n[k], r[k + 1], R[k], R[k + 1]};
+    tt_status st = check_dims(dk);
+    if (st != TT_OK) return fail(st, "core " + std::to_string(k) + ": " + g_msg);
+  }
+  return TT_OK;
+}
+
+// Sweep workspace = [per-stage scratch (max over cores and stage kinds)] [prepared operands
+// of every core: Ahl, Ahr (alpha n^2 beta each), xt (r_k n r_{k+1})].
+static long long prep_elems(const Dims& d) {
+  return 2 * d.al * d.n * d.n * d.be + d.a * d.n * d.b;
+}
+static size_t sweep_step_ws(int64_t d, const int64_t* n, const int64_t* r, const int64_t* R,
+                            int64_t nvec);
+// [main-stream scratch: max over cores of the interface / matvec stage scratch]
+// [side-stream scratch: max over cores of the interface stage scratch] [prepared operands]
+static size_t sweep_prep_offset(int64_t d, const int64_t* n, const int64_t* r, const int64_t* R,
+                                int64_t nvec) {
+  const size_t main_b = sweep_step_ws(d, n, r, R, nvec);
+  const size_t side_b = sweep_step_ws(d, n, r, R, 0);
+  if (main_b == 0 || side_b == 0) return 0;
+  return align_up(main_b, 256) + align_up(side_b, 256);
+}
+static size_t sweep_ws(int64_t d, const int64_t* n, const int64_t* r, const int64_t* R,
+                       int64_t nvec) {
+  size_t base = sweep_prep_offset(d, n, r, R, nvec);
+  if (base == 0) return 0;
+  for (int64_t k = 0; k < d; ++k) {
+    Dims dk{r[k], n[k], r[k + 1], R[k], R[k + 1]};
+    base += align_up(size_t(prep_elems(dk)) * sizeof(double), 256) + 256;
+  }
+  return base;
+}
+struct Prep {
+  const double *Ahl, *Ahr, *xt;
+};
+// pointers of core k's prepared operands inside the workspace
+static Prep prep_ptrs(int64_t k, int64_t d, const int64_t* n, const int64_t* r, const int64_t* R,
+                      int64_t nvec, void* ws) {
+  size_t off = sweep_prep_offset(d, n, r, R, nvec);
+  char* base = static_cast<char*>(ws);
+  for (int64_t q = 0; q <= k; ++q) {
+    Dims dq{r[q], n[q], r[q + 1], R[q], R[q + 1]};
+    uintptr_t p = (reinterpret_cast<uintptr_t>(base) + off + 255) & ~uintptr_t(255);
+    if (q == k) {
+      const double* Ahl = reinterpret_cast<const double*>(p);
+      const double* Ahr = Ahl + dq.al * dq.n * dq.n * dq.be;
+      const double* xt = Ahr + dq.al * dq.n * dq.n * dq.be;
+      return Prep{Ahl, Ahr, xt};
+    }
+    off = (p - reinterpret_cast<uintptr_t>(base)) + size_t(prep_elems(dq)) * sizeof(double);
+  }
+  return Prep{nullptr, nullptr, nullptr};
+}
+// one launch per kPrepMax cores (all of them in practice); one0/one1 (nullable) are set to 1
+static cudaError_t launch_prep(int64_t d, const int64_t* n, const int64_t* r, const int64_t* R,
+                               int64_t nvec, const double* const* xc, const double* const* Ac,
+                               void* ws, cudaStream_t s, double* one0 = nullptr,
+                               double* one1 = nullptr) {
+  for (int64_t k0 = 0; k0 < d; k0 += kPrepMax) {
+    PrepTable t;
+    t.cores = (int)std::min<int64_t>(kPrepMax, d - k0);
+    t.one0 = k0 == 0 ? one0 : nullptr;
+    t.one1 = k0 == 0 ? one1 : nullptr;
+    long long blocks = 0, total = 0;
+    for (int c = 0; c < t.cores; ++c) {
+      const int64_t k = k0 + c;
+      Dims dk{r[k], n[k], r[k + 1], R[k], R[k + 1]};
+      Prep pp = prep_ptrs(k, d, n, r, R, nvec, ws);
+      t.A[c] = Ac[k];
+      t.x[c] = xc[k];
+      t.Ahl[c] = const_cast<double*>(pp.Ahl);
+      t.Ahr[c] = const_cast<double*>(pp.Ahr);
+      t.xt[c] = const_cast<double*>(pp.xt);
+      t.al[c] = (int)dk.al; t.n[c] = (int)dk.n; t.be[c] = (int)dk.be;
+      t.a[c] = (int)dk.a; t.b[c] = (int)dk.b;
+      const long long el = prep_elems(dk);
+      total += el;
+      t.start[c] = (int)blocks;
+      blocks += std::min<long long>(2048, (el + 255) / 256);
+    }
+    t.start[t.cores] = (int)blocks;
+    g_stage = TT_ST_PERM;
+    const long long tr = trace_begin(0, total, 0, 0, s);
+    if (cudaError_t e = launch_pdl(true, prep_all_kernel, dim3((unsigned)blocks), dim3(256), 0, s, t))
+      return e;
+    trace_end(tr, s);
+    ++g_launches;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+static size_t sweep_step_ws(int64_t d, const int64_t* n, const int64_t* r, const int64_t* R,
+                            int64_t nvec) {
+  size_t best = 0;
+  for (int64_t k = 0; k < d; ++k) {
+    Dims dk{r[k], n[k], r[k + 1], R[k], R[k + 1]};
+    long long t1, t2, ah, pe;
+    if (!iface_ws_elems(dk, t1, t2, ah, pe)) return 0;
+    size_t s = ws_bytes({t1, t2, ah, pe});
+    if (s > best) best = s;
+    if (nvec > 0) {
+      if (!matvec_ws_elems(dk, nvec, t1, t2, ah, pe)) return 0;
+      s = ws_bytes({t1, t2, ah, pe});
+      if (s > best) best = s;
+    }
+  }
+  return best;
+}
+
+size_t tt_sweep_workspace_size(int64_t d, const int64_t* n, const int64_t* r, const int64_t* R) {
+  if (d <= 0 || !n || !r || !R) return 0;
+  return sweep_ws(d, n, r, R, 0);
+}
+
+size_t tt_sweep_als_workspace_size(int64_t d, const int64_t* n, const int64_t* r,
+                                   const int64_t* R, int64_t nvec) {
+  if (d <= 0 || !n || !r || !R || nvec <= 0) return 0;
+  return sweep_ws(d, n, r, R, nvec);
+}
+
+// carve the workspace for core k (interface or matvec) and enqueue
+static cudaError_t sweep_left_step(int64_t k, int64_t d, int64_t nvec, void* scratch, const int64_t* n,
+                                   const int64_t* r, const int64_t* R, const double* const* xc,
+                                   const double* const* Ac, double* const* phiL, void* ws,
+                                   size_t wsb, cudaStream_t s, double* T2_keep = nullptr,
+                                   cudaEvent_t ev_t2 = nullptr) {
+  Dims dk{r[k], n[k], r[k + 1], R[k], R[k + 1]};
+  long long t1, t2, ah, pe;
+  iface_ws_elems(dk, t1, t2, ah, pe);
+  Carver c{static_cast<char*>(scratch), wsb};
+  double* T1 = c.take(t1);
+  double* T2 = c.take(t2);
+  double* Ah = c.take(ah);
+  double* Pp = c.take(pe);
+  if (!c.ok) return cudaErrorInvalidValue;
+  if (T2_keep) T2 = T2_keep;
+  const Prep pp = prep_ptrs(k, d, n, r, R, nvec, ws);
+  return enqueue_left(dk, phiL[k], Ac[k], xc[k], phiL[k + 1], T1, T2, Ah, Pp, pe, s,
+                      TT_ST_IL_S1, pp.Ahl, ev_t2);
+}
+
+static cudaError_t sweep_right_step(int64_t k, int64_t d, int64_t nvec, void* scratch, const int64_t* n,
+                                    const int64_t* r, const int64_t* R, const double* const* xc,
+                                    const double* const* Ac, double* const* phiR, void* ws,
+                                    size_t wsb, cudaStream_t s) {
+  Dims dk{r[k], n[k], r[k + 1], R[k], R[k + 1]};
+  long long t1, t2, ah, pe;
+  iface_ws_elems(dk, t1, t2, ah, pe);
+  Carver c{static_cast<char*>(scratch), wsb};
+  double* T1 = c.take(t1);
+  double* T2 = c.take(t2);
+  double* Ah = c.take(ah);
+  double* Pp = c.take(pe);
+  if (!c.ok) return cudaErrorInvalidValue;
+  if (g_dbg_flags & 8) return enqueue_right(dk, phiR[k + 1], Ac[k], xc[k], phiR[k], T1, T2, Ah, Pp, pe, s);
+  const Prep pp = prep_ptrs(k, d, n, r, R, nvec, ws);
+  return enqueue_right_mirror(dk, phiR[k + 1], Ac[k], xc[k], phiR[k], T1, T2, Ah, Pp, pe, s,
+                              pp.Ahr, pp.xt);
+}
+
+static cudaError_t sweep_matvec_step(int64_t k, int64_t d, void* scratch, const int64_t* n, const int64_t* r,
+                                     const int64_t* R, int64_t nvec, const double* const* Ac,
+                                     const double* const* Xb, double* const* Yb,
+                                     double* const* phiL, double* const* phiR, void* ws,
+                                     size_t wsb, cudaStream_t s) {
+  Dims dk{r[k], n[k], r[k + 1], R[k], R[k + 1]};
+  long long t1, t2, ah, pe;
+  matvec_ws_elems(dk, nvec, t1, t2, ah, pe);
+  Carver c{static_cast<char*>(scratch), wsb};
+  double* T1 = c.take(t1);
+  double* T2 = c.take(t2);
+  double* Ah = c.take(ah);
+  double* Pp = c.take(pe);
+  if (!c.ok) return cudaErrorInvalidValue;
+  const Prep pp = prep_ptrs(k, d, n, r, R, nvec, ws);
+  return enqueue_matvec(dk, nvec, phiL[k], Ac[k], phiR[k + 1], Xb[k], Yb[k], T1, T2, Ah, Pp, pe,
+                        s, pp.Ahl);
+}
+
+static tt_status check_ptrs(int64_t d, const void* const* arr, int64_t count, const char* what) {
+  if (!arr) return fail(TT_ERR_NULL_POINTER, std::string("NULL array ") + what);
+  for (int64_t k = 0; k < count; ++k)
+    if (!arr[k]) return fail(TT_ERR_NULL_POINTER, std::string("NULL entry in ") + what);
+  (void)d;
+  return TT_OK;
+}
+
+// outputs (phi arrays, Y blocks) must not alias inputs (cores, blocks) nor each other
+static tt_status check_outputs(int64_t d, const double* const* xc, const double* const* Ac,
+                               const double* const* Xb,
+                               std::initializer_list<std::pair<double* const*, int64_t>> outs,
+                               void* ws) {
+  std::vector<const void*> ins;
+  for (int64_t k = 0; k < d; ++k) {
+    ins.push_back(xc[k]);
+    ins.push_back(Ac[k]);
+    if (Xb) ins.push_back(Xb[k]);
+  }
+  std::vector<const void*> os;
+  for (auto& pr : outs)
+    if (pr.first)
+      for (int64_t k = 0; k < pr.second; ++k) os.push_back(pr.first[k]);
+  for (size_t i = 0; i < os.size(); ++i) {
+    for (const void* q : ins)
+      if (os[i] == q) return fail(TT_ERR_ALIASING, "an output aliases an input core");
+    for (size_t j = i + 1; j < os.size(); ++j)
+      if (os[i] == os[j]) return fail(TT_ERR_ALIASING, "two outputs alias");
+    if (ws && os[i] == ws) return fail(TT_ERR_ALIASING, "an output aliases the workspace");
+  }
+  return TT_OK;
+}
+
+tt_status tt_sweep_interfaces(int64_t d, const int64_t* n, const int64_t* r, const int64_t* R,
+                              const double* const* x_cores, const double* const* A_cores,
+                              double* const* phiL, double* const* phiR, int directions,
+                              void* workspace, size_t workspace_bytes, void* stream) {
+  CallScope scope;
+  tt_status st = check_train(d, n, r, R);
+  if (st != TT_OK) return st;
+  if (directions < 1 || directions > 3) return fail(TT_ERR_INVALID_ARGUMENT, "bad directions");
+  if ((st = check_ptrs(d, (const void* const*)x_cores, d, "x_cores")) != TT_OK) return st;
+  if ((st = check_ptrs(d, (const void* const*)A_cores, d, "A_cores")) != TT_OK) return st;
+  const bool doL = (directions & TT_SWEEP_LEFT) && phiL;
+  const bool doR = (directions & TT_SWEEP_RIGHT) && phiR;
+  if (doL && (st = check_ptrs(d, (const void* const*)phiL, d + 1, "phiL")) != TT_OK) return st;
+  if (doR && (st = check_ptrs(d, (const void* const*)phiR, d + 1, "phiR")) != TT_OK) return st;
+  if ((st = check_outputs(d, x_cores, A_cores, nullptr,
+                          {{doL ? phiL : nullptr, d + 1}, {doR ? phiR : nullptr, d + 1}},
+                          workspace)) != TT_OK)
+    return st;
+  const size_t need = sweep_ws(d, n, r, R, 0);
+  if (need == 0) return fail(TT_ERR_OVERFLOW, "workspace overflow");
+  if (!workspace || workspace_bytes < need)
+    return fail(TT_ERR_WORKSPACE, "workspace NULL or smaller than " + std::to_string(need) + " bytes");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  char* wsb = static_cast<char*>(workspace);
+  const size_t main_b = sweep_step_ws(d, n, r, R, 0);
+  void* ws_main = wsb;
+  void* ws_side = wsb + align_up(main_b, 256);
+  if ((doL || doR) && (e = launch_prep(d, n, r, R, 0, x_cores, A_cores, workspace, s,
+                                      doL ? phiL[0] : nullptr, doR ? phiR[d] : nullptr)) != cudaSuccess)
+    return cuda_fail(e, "sweep prep");
+  // the two chains are independent: left on the caller's stream, right on the side stream
+  cudaStream_t sr = s;
+  if (doL && doR) {
+    if ((e = side_stream(&sr)) != cudaSuccess) return cuda_fail(e, "side stream");
+    if ((e = stream_dep(s, sr)) != cudaSuccess) return cuda_fail(e, "fork");
+  }
+  if (doL) {
+    for (int64_t k = 0; k < d; ++k)
+      if ((e = sweep_left_step(k, d, 0, ws_main, n, r, R, x_cores, A_cores, phiL, workspace,
+                               main_b, s)) != cudaSuccess)
+        return cuda_fail(e, "sweep left");
+  }
+  if (doR) {
+    void* wr = (sr == s) ? ws_main : ws_side;
+    for (int64_t k = d - 1; k >= 0; --k)
+      if ((e = sweep_right_step(k, d, 0, wr, n, r, R, x_cores, A_cores, phiR, workspace, main_b,
+                                sr)) != cudaSuccess)
+        return cuda_fail(e, "sweep right");
+  }
+  if (sr != s && (e = stream_dep(sr, s)) != cudaSuccess) return cuda_fail(e, "join");
+  return TT_OK;
+}
+
+// ---- W34 as one DAG-scheduled call: both interface chains and one matvec per core ---------
+// Workspace: [sweep workspace (chain scratch x2, prepared operands)] [kPoolStreams matvec
+// scratches].  The left chain runs on the caller's stream, the right chain on the side
+// stream, and core k's matvec on a pool stream as soon as phiL[k] and phiR[k+1] exist
+// (events), middle cores first -- so the matvecs overlap the chains.
+static size_t w34_mv_scratch(int64_t d, const int64_t* n, const int64_t* r, const int64_t* R) {
+  size_t best = 0;
+  for (int64_t k = 0; k < d; ++k) {
+    Dims dk{r[k], n[k], r[k + 1], R[k], R[k + 1]};
+    long long t1, t2, ah, pe;
+    if (!matvec_ws_elems(dk, 1, t1, t2, ah, pe)) return 0;
+    best = std::max(best, ws_bytes({t1, t2, ah, pe}));
+  }
+  return best;
+}
+
+// W34 keeps every left update's stage-2 intermediate T2_k (a', i, be, b): with K = 1 it is
+// also the matvec's stage-2 output at core k (same phiL[k], A_k, x_k), so the matvec is only
+// its last stage, y_k = T2_k . phiR[k+1]^T
+static size_t w34_t2_keep(int64_t d, const int64_t* n, const int64_t* r, const int64_t* R) {
+  size_t tot = 256;
+  for (int64_t k = 0; k < d; ++k) {
+    bool ok = true;
+    const long long e = prod({r[k], n[k], R[k + 1], r[k + 1]}, ok);
+    if (!ok) return 0;
+    tot += align_up((size_t)e * 8, 256);
+  }
+  return tot;
+}
+
+size_t tt_sweep_w34_workspace_size(int64_t d, const int64_t* n, const int64_t* r,
+                                   const int64_t* R) {
+  if (d <= 0 || !n || !r || !R) return 0;
+  const size_t base = sweep_ws(d, n, r, R, 0), mv = w34_mv_scratch(d, n, r, R);
+  const size_t keep = w34_t2_keep(d, n, r, R);
+  if (base == 0 || mv == 0 || keep == 0) return 0;
+  return align_up(base, 256) + kPoolStreams * align_up(mv, 256) + keep + 256;
+}
+
+tt_status tt_sweep_w34(int64_t d, const int64_t* n, const int64_t* r, const int64_t* R,
+                       const double* const* x_cores, const double* const* A_cores,
+                       double* const* phiL, double* const* phiR, double* const* y_cores,
+                       void* workspace, size_t workspace_bytes, void* stream) {
+  CallScope scope;
+  tt_status st = check_train(d, n, r, R);
+  if (st != TT_OK) return st;
+  if ((st = check_ptrs(d, (const void* const*)x_cores, d, "x_cores")) != TT_OK) return st;
+  if ((st = check_ptrs(d, (const void* const*)A_cores, d, "A_cores")) != TT_OK) return st;
+  if ((st = check_ptrs(d, (const void* const*)phiL, d + 1, "phiL")) != TT_OK) return st;
+  if ((st = check_ptrs(d, (const void* const*)phiR, d + 1, "phiR")) != TT_OK) return st;
+  if ((st = check_ptrs(d, (const void* const*)y_cores, d, "y_cores")) != TT_OK) return st;
+  if ((st = check_outputs(d, x_cores, A_cores, nullptr, {{phiL, d + 1}, {phiR, d + 1}, {y_cores, d}},
+                          workspace)) != TT_OK)
+    return st;
+  const size_t need = tt_sweep_w34_workspace_size(d, n, r, R);
+  if (need == 0) return fail(TT_ERR_OVERFLOW, "workspace overflow");
+  if (!workspace || workspace_bytes < need)
+    return fail(TT_ERR_WORKSPACE, "workspace NULL or smaller than " + std::to_string(need) + " bytes");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  char* wsb = static_cast<char*>(workspace);
+  const size_t main_b = sweep_step_ws(d, n, r, R, 0);
+  void* ws_main = wsb;
+  void* ws_side = wsb + align_up(main_b, 256);
+  const size_t mv_b = w34_mv_scratch(d, n, r, R);
+  char* mv_base = wsb + align_up(sweep_ws(d, n, r, R, 0), 256);
+  if ((e = pool_init(size_t(3 * (d + 1) + kPoolStreams + 4))) != cudaSuccess) return cuda_fail(e, "pool");
+  cudaEvent_t* evL = g_pool.ev.data();         // evL[k]: phiL[k] ready
+  cudaEvent_t* evR = evL + (d + 1);            // evR[k]: phiR[k] ready
+  cudaEvent_t* evT = evR + (d + 1);            // evT[k]: the left update's T2_k ready
+  cudaEvent_t* evJ = evT + (d + 1);            // joins
+  // T2 reuse (debug bit 23 restores the three-stage matvecs)
+  const bool reuse = !(g_dbg_flags & 8388608);
+  std::vector<double*> T2k(d, nullptr);
+  if (reuse) {
+    char* kb = mv_base + kPoolStreams * align_up(mv_b, 256);
+    kb += (256 - (reinterpret_cast<uintptr_t>(kb) & 255)) & 255;
+    for (int64_t k = 0; k < d; ++k) {
+      T2k[k] = reinterpret_cast<double*>(kb);
+      kb += align_up((size_t)(r[k] * n[k] * R[k + 1] * r[k + 1]) * 8, 256);
+    }
+  }
+  if ((e = launch_prep(d, n, r, R, 0, x_cores, A_cores, workspace, s, phiL[0], phiR[d])) != cudaSuccess)
+    return cuda_fail(e, "sweep prep");
+  cudaStream_t sr;
+  if ((e = side_stream(&sr)) != cudaSuccess) return cuda_fail(e, "side stream");
+  if ((e = stream_dep(s, sr)) != cudaSuccess) return cuda_fail(e, "fork");
+  for (int q = 0; q < kPoolStreams; ++q)
+    if ((e = stream_dep(s, g_pool.s[q])) != cudaSuccess) return cuda_fail(e, "fork");
+  // the two chains, on high-priority streams (the critical path)
+  cudaStream_t sl = g_pool.chain;
+  if ((e = stream_dep(s, sl)) != cudaSuccess) return cuda_fail(e, "fork");
+  if ((e = cudaEventRecord(evL[0], sl)) != cudaSuccess) return cuda_fail(e, "event");
+  for (int64_t k = 0; k < d; ++k) {
+    if ((e = sweep_left_step(k, d, 0, ws_main, n, r, R, x_cores, A_cores, phiL, workspace, main_b,
+                             sl, T2k[k], reuse ? evT[k] : nullptr)) != cudaSuccess)
+      return cuda_fail(e, "sweep left");
+    if ((e = cudaEventRecord(evL[k + 1], sl)) != cudaSuccess) return cuda_fail(e, "event");
+  }
+  if ((e = cudaEventRecord(evR[d], sr)) != cudaSuccess) return cuda_fail(e, "event");
+  for (int64_t k = d - 1; k >= 0; --k) {
+    if ((e = sweep_right_step(k, d, 0, ws_side, n, r, R, x_cores, A_cores, phiR, workspace,
+                              main_b, sr)) != cudaSuccess)
+      return cuda_fail(e, "sweep right");
+    if ((e = cudaEventRecord(evR[k], sr)) != cudaSuccess) return cuda_fail(e, "event");
+  }
+  // matvecs in readiness order (core k needs k left steps and d-1-k right steps)
+  std::vector<int64_t> order(d);
+  for (int64_t k = 0; k < d; ++k) order[k] = k;
+  std::stable_sort(order.begin(), order.end(), [&](int64_t p, int64_t q) {
+    return std::max(p, d - 1 - p) < std::max(q, d - 1 - q);
+  });
+  for (int64_t i = 0; i < d; ++i) {
+    const int64_t k = order[i];
+    const int q = (int)(i % kPoolStreams);
+    cudaStream_t ps = g_pool.s[q];
+    if ((e = cudaStreamWaitEvent(ps, reuse ? evT[k] : evL[k], 0)) != cudaSuccess) return cuda_fail(e, "wait");
+    if ((e = cudaStreamWaitEvent(ps, evR[k + 1], 0)) != cudaSuccess) return cuda_fail(e, "wait");
+    Dims dk{r[k], n[k], r[k + 1], R[k], R[k + 1]};
+    long long t1, t2, ah, pe;
+    matvec_ws_elems(dk, 1, t1, t2, ah, pe);
+    Carver c{mv_base + q * align_up(mv_b, 256), mv_b};
+    double* T1 = c.take(t1);
+    double* T2 = c.take(t2);
+    double* Ah = c.take(ah);
+    double* Pp = c.take(pe);
+    if (!c.ok) return fail(TT_ERR_WORKSPACE, "workspace too small after alignment");
+    if (reuse) {
+      if ((e = enqueue_matvec_last(dk, 1, T2k[k], phiR[k + 1], y_cores[k], Pp, pe, ps)) != cudaSuccess)
+        return cuda_fail(e, "sweep matvec");
+      continue;
+    }
+    const Prep pp = prep_ptrs(k, d, n, r, R, 0, workspace);
+    if ((e = enqueue_matvec(dk, 1, phiL[k], A_cores[k], phiR[k + 1], x_cores[k], y_cores[k], T1,
+                            T2, Ah, Pp, pe, ps, pp.Ahl)) != cudaSuccess)
+      return cuda_fail(e, "sweep matvec");
+  }
+  // join everything back into the caller's stream
+  if ((e = cudaEventRecord(evJ[0], sr)) != cudaSuccess || (e = cudaStreamWaitEvent(s, evJ[0], 0)) != cudaSuccess)
+    return cuda_fail(e, "join");
+  if ((e = cudaEventRecord(evJ[1 + kPoolStreams], sl)) != cudaSuccess ||
+      (e = cudaStreamWaitEvent(s, evJ[1 + kPoolStreams], 0)) != cudaSuccess)
+    return cuda_fail(e, "join");
+  for (int q = 0; q < kPoolStreams; ++q)
+    if ((e = cudaEventRecord(evJ[1 + q], g_pool.s[q])) != cudaSuccess ||
+        (e = cudaStreamWaitEvent(s, evJ[1 + q], 0)) != cudaSuccess)
+      return cuda_fail(e, "join");
+  return TT_OK;
+}
+
+tt_status tt_sweep_als(int64_t d, const int64_t* n, const int64_t* r, const int64_t* R,
+                       int64_t nvec, const double* const* x_cores,
+                       const double* const* A_cores, const double* const* X_blocks,
+                       double* const* Y_fwd, double* const* Y_bwd, double* const* phiL,
+                       double* const* phiR, void* workspace, size_t workspace_bytes,
+                       void* stream) {
+  CallScope scope;
+  tt_status st = check_train(d, n, r, R);
+  if (st != TT_OK) return st;
+  if (nvec <= 0) return fail(TT_ERR_INVALID_ARGUMENT, "nvec must be positive");
+  if ((st = check_ptrs(d, (const void* const*)x_cores, d, "x_cores")) != TT_OK) return st;
+  if ((st = check_ptrs(d, (const void* const*)A_cores, d, "A_cores")) != TT_OK) return st;
+  if ((st = check_ptrs(d, (const void* const*)X_blocks, d, "X_blocks")) != TT_OK) return st;
+  if ((st = check_ptrs(d, (const void* const*)Y_fwd, d, "Y_fwd")) != TT_OK) return st;
+  if (Y_bwd && (st = check_ptrs(d, (const void* const*)Y_bwd, d, "Y_bwd")) != TT_OK) return st;
+  if ((st = check_ptrs(d, (const void* const*)phiL, d + 1, "phiL")) != TT_OK) return st;
+  if ((st = check_ptrs(d, (const void* const*)phiR, d + 1, "phiR")) != TT_OK) return st;
+  if ((st = check_outputs(d, x_cores, A_cores, X_blocks,
+                          {{Y_fwd, d}, {Y_bwd, d}, {phiL, d + 1}, {phiR, d + 1}}, workspace)) !=
+      TT_OK)
+    return st;
+  const size_t need = sweep_ws(d, n, r, R, nvec);
+  if (need == 0) return fail(TT_ERR_OVERFLOW, "workspace overflow");
+  if (!workspace || workspace_bytes < need)
+    return fail(TT_ERR_WORKSPACE, "workspace NULL or smaller than " + std::to_string(need) + " bytes");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  double* const* Yb = Y_bwd ? Y_bwd : Y_fwd;
+  char* wsb = static_cast<char*>(workspace);
+  const size_t main_b = sweep_step_ws(d, n, r, R, nvec);
+  const size_t side_b = sweep_step_ws(d, n, r, R, 0);
+  void* ws_main = wsb;
+  void* ws_side = wsb + align_up(main_b, 256);
+  // W5 is throughput-bound: plain launches (PDL measured 0.2 % slower on the whole sweep)
+  struct NoPdl {
+    bool saved = g_no_pdl;
+    NoPdl() { g_no_pdl = true; }
+    ~NoPdl() { g_no_pdl = saved; }
+  } no_pdl;
+  cudaStream_t ss;
+  if ((e = side_stream(&ss)) != cudaSuccess) return cuda_fail(e, "side stream");
+  if ((e = launch_prep(d, n, r, R, nvec, x_cores, A_cores, workspace, s, phiL[0], phiR[d])) !=
+      cudaSuccess)
+    return cuda_fail(e, "als prep");
+  for (int64_t k = d - 1; k >= 1; --k)
+    if ((e = sweep_right_step(k, d, nvec, ws_main, n, r, R, x_cores, A_cores, phiR, workspace,
+                              main_b, s)) != cudaSuccess)
+      return cuda_fail(e, "als initial right");
+  // L->R: the left-interface chain runs on the side stream, one step ahead of the matvecs,
+  // which wait only for the interface they read (matvec(k) needs phiL[k] = IL(k-1)).
+  if ((e = stream_dep(s, ss)) != cudaSuccess) return cuda_fail(e, "fork");
+  for (int64_t k = 0; k < d; ++k) {
+    if (k > 0 && (e = stream_dep(ss, s)) != cudaSuccess) return cuda_fail(e, "dep");
+    if ((e = sweep_matvec_step(k, d, ws_main, n, r, R, nvec, A_cores, X_blocks, Y_fwd, phiL, phiR,
+                               workspace, main_b, s)) != cudaSuccess)
+      return cuda_fail(e, "als matvec L->R");
+    if (k < d - 1 && (e = sweep_left_step(k, d, nvec, ws_side, n, r, R, x_cores, A_cores, phiL,
+                                          workspace, side_b, ss)) != cudaSuccess)
+      return cuda_fail(e, "als left");
+  }
+  // R->L: the right chain recomputes phiR[k] (k = d-1..1) on the side stream; matvec(k)
+  // needs phiR[k+1] = IR(k+1).  Both streams first wait for the whole L->R pass.
+  if ((e = stream_dep(s, ss)) != cudaSuccess) return cuda_fail(e, "fork");
+  for (int64_t k = d - 1; k >= 0; --k) {
+    if (k < d - 1 && (e = stream_dep(ss, s)) != cudaSuccess) return cuda_fail(e, "dep");
+    if ((e = sweep_matvec_step(k, d, ws_main, n, r, R, nvec, A_cores, X_blocks, Yb, phiL, phiR,
+                               workspace, main_b, s)) != cudaSuccess)
+      return cuda_fail(e, "als matvec R->L");
+    if (k > 0 && (e = sweep_right_step(k, d, nvec, ws_side, n, r, R, x_cores, A_cores, phiR,
+                                       workspace, side_b, ss)) != cudaSuccess)
+      return cuda_fail(e, "als right");
+  }
+  if ((e = stream_dep(ss, s)) != cudaSuccess) return cuda_fail(e, "join");
+  return TT_OK;
+}
+
+// ---- H8 ----------------------------------------------------------------------------------
+tt_status tt_operator_apply(int64_t d, const int64_t* n_row, const int64_t* n_col,
+                            const int64_t* r, const int64_t* R, const double* const* x_cores,
+                            const double* const* A_cores, double* const* z_cores, void* stream) {
+  CallScope scope;
+  if (d <= 0) return fail(TT_ERR_INVALID_ARGUMENT, "d must be >= 1");
+  if (!n_row || !n_col || !r || !R) return fail(TT_ERR_NULL_POINTER, "NULL shape array");
+  if (r[0] != 1 || r[d] != 1) return fail(TT_ERR_INVALID_ARGUMENT, "r_1 and r_{d+1} must be 1");
+  if (R[0] != 1 || R[d] != 1) return fail(TT_ERR_INVALID_ARGUMENT, "R_1 and R_{d+1} must be 1");
+  tt_status st;
+  if ((st = check_ptrs(d, (const void* const*)x_cores, d, "x_cores")) != TT_OK) return st;
+  if ((st = check_ptrs(d, (const void* const*)A_cores, d, "A_cores")) != TT_OK) return st;
+  if ((st = check_ptrs(d, (const void* const*)z_cores, d, "z_cores")) != TT_OK) return st;
+  if ((st = check_outputs(d, x_cores, A_cores, nullptr, {{z_cores, d}}, nullptr)) != TT_OK)
+    return st;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int smem_optin = 0;
+  cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  for (int64_t k = 0; k < d; ++k) {
+    if (n_row[k] <= 0 || n_col[k] <= 0 || r[k] <= 0 || R[k] <= 0)
+      return fail(TT_ERR_INVALID_ARGUMENT, "extents must be positive");
+    bool ok = true;
+    prod({r[k], R[k], n_row[k], r[k + 1], R[k + 1]}, ok);
+    prod({R[k], n_row[k], n_col[k], R[k + 1]}, ok);
+    prod({r[k], n_col[k], r[k + 1]}, ok);
+    if (!ok) return fail(TT_ERR_OVERFLOW, "extent product overflows");
+    const long long smem = 8LL * (n_col[k] * r[k + 1] + n_row[k] * n_col[k] * R[k + 1]);
+    if (smem > smem_optin || r[k + 1] * R[k + 1] > 0x7fffffffLL || r[k] * R[k] > 0x7fffffffLL)
+      return fail(TT_ERR_INVALID_ARGUMENT, "core too large for the apply kernel's staging");
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] {
+    attr_err = cudaFuncSetAttribute(apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    smem_optin);
+  });
+  if (attr_err != cudaSuccess) return cuda_fail(attr_err, "tt_operator_apply attr");
+  for (int64_t k = 0; k < d; ++k) {
+    const long long smem = 8LL * (n_col[k] * r[k + 1] + n_row[k] * n_col[k] * R[k + 1]);
+    const long long blocks = r[k] * R[k];
+    g_stage = TT_ST_APPLY;
+    const long long tr = trace_begin(0, r[k] * R[k] * n_row[k] * r[k + 1] * R[k + 1], n_col[k], 0, s);
+    cudaError_t e = cudaSuccess;
+    const long long L = r[k + 1] * R[k + 1];
+    if (n_col[k] <= 4 && L >= 256 && (r[k] + 3) / 4 <= 65535 && R[k] <= 65535) {
+      switch (n_col[k]) {
+        case 1: e = launch_apply_reg<1>(x_cores[k], A_cores[k], z_cores[k], r[k], n_row[k], r[k + 1], R[k], R[k + 1], s); break;
+        case 2: e = launch_apply_reg<2>(x_cores[k], A_cores[k], z_cores[k], r[k], n_row[k], r[k + 1], R[k], R[k + 1], s); break;
+        case 3: e = launch_apply_reg<3>(x_cores[k], A_cores[k], z_cores[k], r[k], n_row[k], r[k + 1], R[k], R[k + 1], s); break;
+        default: e = launch_apply_reg<4>(x_cores[k], A_cores[k], z_cores[k], r[k], n_row[k], r[k + 1], R[k], R[k + 1], s); break;
+      }
+    } else {
+      apply_kernel<<<(unsigned)blocks, 256, (size_t)smem, s>>>(
+          x_cores[k], A_cores[k], z_cores[k], (int)r[k], (int)n_row[k], (int)n_col[k],
+          (int)r[k + 1], (int)R[k], (int)R[k + 1]);
+      e = cudaGetLastError();
+    }
+    trace_end(tr, s);
+    ++g_launches;
+    if (e != cudaSuccess) return cuda_fail(e, "tt_operator_apply");
+  }
+  return TT_OK;
+}
+
+// test hook: symmetric eigendecomposition of an n x n matrix (G overwritten), lam descending
+tt_status tt_debug_sym_eigen(int64_t n, double* G, double* V, double* lam, void* workspace,
+                             size_t workspace_bytes, void* stream) {
+  CallScope scope;
+  if (n <= 0 || n > 2048) return fail(TT_ERR_INVALID_ARGUMENT, "0 < n <= 2048");
+  if (!G || !V || !lam || !workspace) return fail(TT_ERR_NULL_POINTER, "NULL pointer");
+  if (workspace_bytes < (size_t)sym_eigen_scratch(n) * 8) return fail(TT_ERR_WORKSPACE, "workspace");
+  g_eigen_elementwise = (g_dbg_flags & 256) ? 1 : 0;
+  cudaError_t e = launch_sym_eigen(G, V, lam, (int)n, static_cast<double*>(workspace),
+                                   static_cast<cudaStream_t>(stream));
+  g_eigen_elementwise = 0;
+  if (e != cudaSuccess) return cuda_fail(e, "tt_debug_sym_eigen");
+  return TT_OK;
+}
+
+// ---- tracing / probe ----------------------------------------------------------------------
+tt_status tt_trace_enable(int64_t capacity) {
+  g_msg.clear();
+  if (capacity <= 0) return fail(TT_ERR_INVALID_ARGUMENT, "capacity must be positive");
+  tt_trace_disable();
+  g_trace_pool.resize(size_t(2 * capacity));
+  for (auto& ev : g_trace_pool) {
+    cudaError_t e = cudaEventCreate(&ev);
+    if (e != cudaSuccess) {
+      g_trace_pool.clear();
+      return cuda_fail(e, "tt_trace_enable");
+    }
+  }
+  g_trace.clear();
+  g_trace.reserve(size_t(capacity));
+  g_trace_on = true;
+  return TT_OK;
+}
+
+tt_status tt_trace_disable(void) {
+  for (auto& ev : g_trace_pool) cudaEventDestroy(ev);
+  g_trace_pool.clear();
+  g_trace.clear();
+  g_trace_on = false;
+  return TT_OK;
+}
+
+int64_t tt_trace_count(void) { return (int64_t)g_trace.size(); }
+
+tt_status tt_trace_read(int64_t i, int* stage, int* tile, int64_t* M, int64_t* N, int64_t* K,
+                        float* ms) {
+  if (i < 0 || i >= (int64_t)g_trace.size()) return fail(TT_ERR_INVALID_ARGUMENT, "bad index");
+  const TraceRec& r = g_trace[size_t(i)];
+  if (stage) *stage = r.stage;
+  if (tile) *tile = r.tile;
+  if (M) *M = r.M;
+  if (N) *N = r.N;
+  if (K) *K = r.K;
+  if (ms) {
+    cudaError_t e = cudaEventSynchronize(r.e1);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(ms, r.e0, r.e1);
+    if (e != cudaSuccess) return cuda_fail(e, "tt_trace_read");
+  }
+  return TT_OK;
+}
+
+tt_status tt_fp64_peak_probe(int64_t iters, double* flops, void* stream) {
+  CallScope scope;
+  if (iters <= 0) return fail(TT_ERR_INVALID_ARGUMENT, "iters must be positive");
+  if (!flops) return fail(TT_ERR_NULL_POINTER, "flops");
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int blocks = 2 * sms, threads = 256;   // 16 warps per SM
+  dmma_probe_kernel<<<blocks, threads, 0, static_cast<cudaStream_t>(stream)>>>(nullptr, iters);
+  ++g_launches;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "tt_fp64_peak_probe");
+  *flops = 2.0 * 8 * 8 * 4 * 8.0 * double(iters) * blocks * (threads / 32);
+  return TT_OK;
+}
+
+}  // extern "C"

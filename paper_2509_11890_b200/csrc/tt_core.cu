@@ -1,0 +1,571 @@
+// tt_core.cu — internal state, small kernels (operator-core permutations, sweep preparation,
+// the unrounded apply H8) and the three-GEMM stage plans of the TT hot path.
+#include "tt_internal.cuh"
+
+namespace ttint {
+
+thread_local std::string g_msg;
+thread_local int64_t g_launches = 0;
+thread_local int64_t g_launches_last = 0;
+
+// ---- tracing (tt_trace_*): per-launch CUDA events on the launch stream ----------------
+thread_local bool g_trace_on = false;
+thread_local std::vector<TraceRec> g_trace;
+thread_local std::vector<cudaEvent_t> g_trace_pool;
+thread_local int g_stage = TT_ST_PERM;   // stage tag of the next launch
+
+// ---- side stream for the sweeps' concurrent interface chains (per thread, per device) ------
+thread_local SideStream g_side;
+thread_local int g_side_lowprio = 0;
+
+cudaError_t side_stream(cudaStream_t* out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (g_side.dev != dev) {
+    // the side stream carries the interface chains, the sweeps' critical path: give it the
+    // highest priority so its small GEMMs are scheduled ahead of the concurrent matvecs
+    int lo = 0, hi = 0;
+    if ((e = cudaDeviceGetStreamPriorityRange(&lo, &hi)) != cudaSuccess) return e;
+    if ((e = cudaStreamCreateWithPriority(&g_side.s, cudaStreamNonBlocking, hi)) != cudaSuccess)
+      return e;
+    if ((e = cudaStreamCreateWithPriority(&g_side.s_lo, cudaStreamNonBlocking, lo)) != cudaSuccess)
+      return e;
+    for (auto& ev : g_side.ev)
+      if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return e;
+    g_side.dev = dev;
+  }
+  *out = g_side_lowprio ? g_side.s_lo : g_side.s;
+  return cudaSuccess;
+}
+// `to` waits for all work enqueued on `from` so far (graph-capture compatible)
+cudaError_t stream_dep(cudaStream_t from, cudaStream_t to) {
+  cudaEvent_t ev = g_side.ev[g_side.next++ % 64];
+  cudaError_t e = cudaEventRecord(ev, from);
+  if (e != cudaSuccess) return e;
+  return cudaStreamWaitEvent(to, ev, 0);
+}
+
+// ---- stream pool + dependency events for DAG-scheduled sweeps (per thread, per device) ----
+thread_local StreamPool g_pool;
+cudaError_t pool_init(size_t nevents) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (g_pool.dev != dev) {
+    int lo = 0, hi = 0;
+    if ((e = cudaDeviceGetStreamPriorityRange(&lo, &hi)) != cudaSuccess) return e;
+    for (auto& st : g_pool.s)
+      if ((e = cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, lo)) != cudaSuccess) return e;
+    if ((e = cudaStreamCreateWithPriority(&g_pool.chain, cudaStreamNonBlocking, hi)) != cudaSuccess)
+      return e;
+    g_pool.ev.clear();
+    g_pool.dev = dev;
+  }
+  while (g_pool.ev.size() < nevents) {
+    cudaEvent_t ev;
+    if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return e;
+    g_pool.ev.push_back(ev);
+  }
+  return cudaSuccess;
+}
+
+long long trace_begin(int tile, long long M, long long N, long long K, cudaStream_t s) {
+  if (!g_trace_on || 2 * (g_trace.size() + 1) > g_trace_pool.size()) return -1;
+  TraceRec r;
+  r.stage = g_stage;
+  r.tile = tile;
+  r.M = M;
+  r.N = N;
+  r.K = K;
+  r.e0 = g_trace_pool[2 * g_trace.size()];
+  r.e1 = g_trace_pool[2 * g_trace.size() + 1];
+  cudaEventRecord(r.e0, s);
+  g_trace.push_back(r);
+  return (long long)g_trace.size() - 1;
+}
+void trace_end(long long idx, cudaStream_t s) {
+  if (idx >= 0) cudaEventRecord(g_trace[idx].e1, s);
+}
+
+tt_status fail(tt_status s, const std::string& m) {
+  g_msg = m;
+  return s;
+}
+
+constexpr long long kMaxElems = (1LL << 62) / 8;
+
+// checked product of positive extents
+bool mulc(long long& acc, long long v) {
+  if (v <= 0) return false;
+  if (acc > kMaxElems / v) return false;
+  acc *= v;
+  return true;
+}
+
+long long prod(std::initializer_list<long long> xs, bool& ok) {
+  long long p = 1;
+  for (long long v : xs)
+    if (!mulc(p, v)) ok = false;
+  return ok ? p : 0;
+}
+
+
+// Carves 256-byte aligned sub-buffers out of the caller's workspace.
+
+// bytes of workspace for a list of buffers (each padded to 256 B, plus 256 B base slack)
+size_t ws_bytes(std::initializer_list<long long> elems) {
+  size_t s = 256;
+  for (long long e : elems) s += align_up(size_t(e) * sizeof(double), 256);
+  return s;
+}
+
+thread_local int g_dbg_flags = 0;   // tt_debug_set_flags (bits listed in the header)
+// GEMMs up to this size are launched with PDL (config 3's ~34 MFLOP stages gain 8 %; config
+// 4's ~0.16-0.4 GFLOP stages lose: the early-placed dependents unbalance the persistent grid;
+// swept with tools/w34_knobs.py: 0.05 GFLOP gives config 3 0.166 ms and config 4 0.731 ms,
+// 0.2 GFLOP 0.165 / 0.746, no PDL 0.193 / 0.734); g_no_pdl (tt_sweep_als scope) disables it.
+constexpr double kPdlFlopsDefault = 0.05e9;
+double pdl_flops() {   // probe override TT_PDL_FLOPS, read once
+  static const double v = [] {
+    const char* e = getenv("TT_PDL_FLOPS");
+    return e ? atof(e) : kPdlFlopsDefault;
+  }();
+  return v;
+}
+thread_local bool g_no_pdl = false;
+
+
+// ----------------------------------------------------------------------------------------
+// small kernels
+// ----------------------------------------------------------------------------------------
+// Ahat[(al, j), (i, be)] = A[al, i, j, be]   (left / matvec stage S2 operand)
+__global__ void perm_left_kernel(const double* __restrict__ A, double* __restrict__ Ah,
+                                 long long al_n, long long n, long long be_n) {
+  const long long total = al_n * n * n * be_n;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    long long r = e;
+    const long long be = r % be_n; r /= be_n;
+    const long long j = r % n; r /= n;
+    const long long i = r % n; r /= n;
+    const long long al = r;
+    Ah[(al * n + j) * (n * be_n) + i * be_n + be] = A[e];
+  }
+}
+
+// Atil[(j, be), (al, i)] = A[al, i, j, be]   (right interface stage S2'' operand)
+__global__ void perm_right_kernel(const double* __restrict__ A, double* __restrict__ At,
+                                  long long al_n, long long n, long long be_n) {
+  const long long total = al_n * n * n * be_n;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    long long r = e;
+    const long long be = r % be_n; r /= be_n;
+    const long long j = r % n; r /= n;
+    const long long i = r % n; r /= n;
+    const long long al = r;
+    At[(j * be_n + be) * (al_n * n) + al * n + i] = A[e];
+  }
+}
+
+
+// xt[b, j, a] = x[a, j, b]: 32x32 shared-memory tiles per mode index j (coalesced both ways)
+__global__ void transpose_core_kernel(const double* __restrict__ x, double* __restrict__ xt,
+                                      int a_n, int n, int b_n) {
+  __shared__ double tile[32][33];
+  const int j = blockIdx.z;
+  const int a0 = blockIdx.y * 32, b0 = blockIdx.x * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int a = a0 + r, b = b0 + threadIdx.x;
+    if (a < a_n && b < b_n) tile[r][threadIdx.x] = x[((long long)a * n + j) * b_n + b];
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int b = b0 + r, a = a0 + threadIdx.x;
+    if (a < a_n && b < b_n) xt[((long long)b * n + j) * a_n + a] = tile[threadIdx.x][r];
+  }
+}
+
+// All cores of a sweep prepared by ONE launch (a dependent launch costs ~4 us on the
+// critical path of the small-rank sweeps): block range [start[c], start[c+1]) works on core c;
+// the first block also writes the trivial boundary interfaces when given.
+
+__global__ void __launch_bounds__(256) prep_all_kernel(const __grid_constant__ PrepTable t) {
+  tt::pdl_wait();
+  int c = 0;
+  while (c + 1 < t.cores && (int)blockIdx.x >= t.start[c + 1]) ++c;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (t.one0) *t.one0 = 1.0;
+    if (t.one1) *t.one1 = 1.0;
+  }
+  const long long al_n = t.al[c], n = t.n[c], be_n = t.be[c], a_n = t.a[c], b_n = t.b[c];
+  const double* __restrict__ A = t.A[c];
+  const double* __restrict__ x = t.x[c];
+  double* __restrict__ Ahl = t.Ahl[c];
+  double* __restrict__ Ahr = t.Ahr[c];
+  double* __restrict__ xt = t.xt[c];
+  const long long tA = al_n * n * n * be_n, tx = a_n * n * b_n;
+  const long long nb = t.start[c + 1] - t.start[c];
+  for (long long e = (blockIdx.x - t.start[c]) * (long long)blockDim.x + threadIdx.x; e < tA + tx;
+       e += nb * blockDim.x) {
+    if (e < tA) {
+      long long r = e;
+      const long long be = r % be_n; r /= be_n;
+      const long long j = r % n; r /= n;
+      const long long i = r % n;
+      const long long al = r / n;
+      const double v = A[e];
+      Ahl[(al * n + j) * (n * be_n) + i * be_n + be] = v;
+      Ahr[(be * n + j) * (n * al_n) + i * al_n + al] = v;
+    } else {
+      const long long f = e - tA;
+      const long long b = f % b_n, r = f / b_n;
+      const long long j = r % n, a = r / n;
+      xt[(b * n + j) * a_n + a] = x[f];
+    }
+  }
+  tt::pdl_trigger();
+}
+
+// At[be, i, j, al] = A[al, i, j, be]  (operator core with its two bonds swapped)
+__global__ void swap_bonds_kernel(const double* __restrict__ A, double* __restrict__ At,
+                                  long long al_n, long long nn, long long be_n) {
+  const long long total = al_n * nn * be_n;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long be = e % be_n, r = e / be_n;
+    const long long ij = r % nn, al = r / nn;
+    At[(be * nn + ij) * al_n + al] = A[e];
+  }
+}
+
+cudaError_t launch_perm(bool left, const double* A, double* out, long long al, long long n,
+                        long long be, cudaStream_t s) {
+  const long long total = al * n * n * be;
+  const int threads = 256;
+  long long blocks = (total + threads - 1) / threads;
+  if (blocks > 4096) blocks = 4096;
+  const int saved = g_stage;
+  g_stage = TT_ST_PERM;
+  const long long tr = trace_begin(0, total, 0, 0, s);
+  g_stage = saved;
+  if (left)
+    perm_left_kernel<<<(unsigned)blocks, threads, 0, s>>>(A, out, al, n, be);
+  else
+    perm_right_kernel<<<(unsigned)blocks, threads, 0, s>>>(A, out, al, n, be);
+  trace_end(tr, s);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+
+// ----------------------------------------------------------------------------------------
+// stage plans
+// ----------------------------------------------------------------------------------------
+
+bool dims_valid(const Dims& d) { return d.a > 0 && d.n > 0 && d.b > 0 && d.al > 0 && d.be > 0; }
+
+// element counts of the matvec workspace buffers (K columns)
+bool matvec_ws_elems(const Dims& d, long long K, long long& t1, long long& t2, long long& ah,
+                     long long& pe) {
+  bool ok = true;
+  t1 = prod({d.a, d.al, d.n, K, d.b}, ok);
+  t2 = prod({d.a, d.n, K, d.be, d.b}, ok);
+  ah = prod({d.al, d.n, d.n, d.be}, ok);
+  // split-K partials of the last stage: 4 slices, or up to 64 for small outputs (<= 128 MB)
+  {
+    const long long out = prod({d.a, d.n, K, d.b}, ok);
+    pe = std::max(4 * out, std::min(64 * out, 16LL << 20));
+  }
+  return ok;
+}
+
+
+// Local matvec (K columns, Block-TT layout) — stages S1, S2^T, S3.
+// S3: Y(a', i, m, b') = T2[(a' m i), (be b)] . phiR[b', (be b)]^T
+cudaError_t enqueue_matvec_last(const Dims& d, long long K, const double* T2, const double* phiR,
+                                double* Y, double* P, long long pe, cudaStream_t s) {
+  const long long a = d.a, b = d.b, be = d.be, N = d.n;
+  g_stage = TT_ST_MV_S3;
+  SplitScratch scratch(P, pe);
+  return launch_gemm(true, true,
+                     gp(T2, be * b, phiR, be * b, Y, a * K * N, b, be * b,
+                        tt::map3(N, K, K * b, b, N * K * b), tt::map_plain(1)),
+                     s);
+}
+
+cudaError_t enqueue_matvec(const Dims& d, long long K, const double* phiL, const double* A,
+                           const double* phiR, const double* X, double* Y, double* T1,
+                           double* T2, double* Ah, double* P, long long pe, cudaStream_t s,
+                           const double* Ah_pre) {
+  const long long a = d.a, b = d.b, al = d.al, be = d.be, N = d.n;
+  cudaError_t e;
+  if (Ah_pre)
+    Ah = const_cast<double*>(Ah_pre);
+  else if ((e = launch_perm(true, A, Ah, al, N, be, s)) != cudaSuccess)
+    return e;
+  // S1: T1(al, j, a', m, b) = phiL[(a' al), a] . X[a, (j m b)]
+  g_stage = TT_ST_MV_S1;
+  e = launch_gemm(true, false,
+                  gp(phiL, a, X, N * K * b, T1, a * al, N * K * b, a,
+                     tt::map2(al, N * a * K * b, K * b), tt::map2(K * b, 1, a * K * b)),
+                  s);
+  if (e != cudaSuccess) return e;
+  // S2^T: T2(a', m, i, be, b) = T1^T[(a' m b), (al j)] . Ahat[(al j), (i be)]
+  g_stage = TT_ST_MV_S2;
+  e = launch_gemm(false, false,
+                  gp(T1, a * K * b, Ah, N * be, T2, a * K * b, N * be, al * N,
+                     tt::map2(b, 1, N * be * b), tt::map_plain(b)),
+                  s);
+  if (e != cudaSuccess) return e;
+  return enqueue_matvec_last(d, K, T2, phiR, Y, P, pe, s);
+}
+
+bool iface_ws_elems(const Dims& d, long long& t1, long long& t2, long long& ah, long long& pe) {
+  bool ok = true;
+  // ah also holds the mirrored right update's swapped operator core and transposed core
+  {
+    const long long out = std::max(prod({d.b, d.be, d.b}, ok), prod({d.a, d.al, d.a}, ok));
+    pe = std::max(4 * out, std::min(64 * out, 16LL << 20));
+  }
+  t1 = prod({d.a, d.al, d.n, d.b}, ok);
+  long long t1r = prod({d.a, d.n, d.b, d.be}, ok);
+  if (t1r > t1) t1 = t1r;
+  t2 = prod({d.a, d.n, d.be, d.b}, ok);
+  long long t2r = prod({d.a, d.al, d.n, d.b}, ok);
+  if (t2r > t2) t2 = t2r;
+  ah = prod({3, d.al, d.n, d.n, d.be}, ok) + prod({d.a, d.n, d.b}, ok);
+  return ok;
+}
+
+// Left interface: S1, S2^T (K = 1), S3': phiL_next[b', (be b)] = x^T[b', (a' i)] . T2[(a' i), (be b)]
+cudaError_t enqueue_left(const Dims& d, const double* phiL, const double* A, const double* x,
+                         double* out, double* T1, double* T2, double* Ah, double* P,
+                         long long pe, cudaStream_t s, int tag_s1,
+                         const double* Ah_pre, cudaEvent_t ev_t2) {
+  const long long a = d.a, b = d.b, al = d.al, be = d.be, N = d.n;
+  cudaError_t e;
+  if (Ah_pre)
+    Ah = const_cast<double*>(Ah_pre);
+  else if ((e = launch_perm(true, A, Ah, al, N, be, s)) != cudaSuccess)
+    return e;
+  g_stage = tag_s1;
+  e = launch_gemm(true, false,
+                  gp(phiL, a, x, N * b, T1, a * al, N * b, a, tt::map2(al, N * a * b, b),
+                     tt::map2(b, 1, a * b)),
+                  s);
+  if (e != cudaSuccess) return e;
+  g_stage = tag_s1 + 1;
+  e = launch_gemm(false, false,
+                  gp(T1, a * b, Ah, N * be, T2, a * b, N * be, al * N, tt::map2(b, 1, N * be * b),
+                     tt::map_plain(b)),
+                  s);
+  if (e != cudaSuccess) return e;
+  if (ev_t2 && (e = cudaEventRecord(ev_t2, s)) != cudaSuccess) return e;   // T2 complete
+  g_stage = tag_s1 + 2;
+  SplitScratch scratch(P, pe);
+  return launch_gemm(false, false,
+                     gp(x, b, T2, be * b, out, b, be * b, a * N, tt::map_plain(be * b),
+                        tt::map_plain(1)),
+                     s);
+}
+
+// Right interface: S1'': T1(j, be, a, b') = x[(a j), b] . phiR[(b' be), b]^T
+//                  S2'': T2(i, b', al, a) = T1^T[(a b'), (j be)] . Atil[(j be), (al i)]
+//                  S3'': phiR_prev[a', (al a)] = x[a', (i b')] . T2[(i b'), (al a)]
+// Right interface as the mirror image of the left one: with
+// xt[b, j, a] = x[a, j, b] and At[be, i, j, al] = A[al, i, j, be],
+//   phiR_prev[a', al, a] = sum x[a',i,b'] A[al,i,j,be] phiR[b',be,b] x[a,j,b]
+//                        = (left update of phiR through At, xt)[a', al, a],
+// so the right update runs on the left update's stage kernels (their layouts give 16-byte
+// epilogue stores and M/N-contiguous TMA operands).  Ah holds [perm | At | xt].
+cudaError_t enqueue_right_mirror(const Dims& d, const double* phiR, const double* A,
+                                 const double* x, double* out, double* T1, double* T2,
+                                 double* Ah, double* P, long long pe, cudaStream_t s,
+                                 const double* Ahr_pre, const double* xt_pre) {
+  const long long a = d.a, b = d.b, al = d.al, be = d.be, N = d.n;
+  if (Ahr_pre && xt_pre) {
+    const Dims dm{b, N, a, be, al};
+    return enqueue_left(dm, phiR, nullptr, xt_pre, out, T1, T2, Ah, P, pe, s, TT_ST_IR_S1,
+                        Ahr_pre);
+  }
+  double* At = Ah + al * N * N * be;
+  double* xt = At + al * N * N * be;
+  {
+    const long long total = al * N * N * be;
+    long long blocks = (total + 255) / 256;
+    if (blocks > 4096) blocks = 4096;
+    g_stage = TT_ST_PERM;
+    const long long tr = trace_begin(0, total, 0, 0, s);
+    swap_bonds_kernel<<<(unsigned)blocks, 256, 0, s>>>(A, At, al, N * N, be);
+    trace_end(tr, s);
+    ++g_launches;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  {
+    dim3 grid((unsigned)((b + 31) / 32), (unsigned)((a + 31) / 32), (unsigned)N);
+    g_stage = TT_ST_PERM;
+    const long long tr = trace_begin(0, a * N * b, 0, 0, s);
+    transpose_core_kernel<<<grid, dim3(32, 8), 0, s>>>(x, xt, (int)a, (int)N, (int)b);
+    trace_end(tr, s);
+    ++g_launches;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  const Dims dm{b, N, a, be, al};
+  return enqueue_left(dm, phiR, At, xt, out, T1, T2, Ah, P, pe, s, TT_ST_IR_S1);
+}
+
+cudaError_t enqueue_right(const Dims& d, const double* phiR, const double* A, const double* x,
+                          double* out, double* T1, double* T2, double* At, double* P,
+                          long long pe, cudaStream_t s) {
+  const long long a = d.a, b = d.b, al = d.al, be = d.be, N = d.n;
+  cudaError_t e;
+  if ((e = launch_perm(false, A, At, al, N, be, s)) != cudaSuccess) return e;
+  g_stage = TT_ST_IR_S1;
+  e = launch_gemm(true, true,
+                  gp(x, b, phiR, b, T1, a * N, b * be, b, tt::map2(N, be * a * b, b),
+                     tt::map2(be, a * b, 1)),
+                  s);
+  if (e != cudaSuccess) return e;
+  g_stage = TT_ST_IR_S2;
+  e = launch_gemm(false, false,
+                  gp(T1, a * b, At, al * N, T2, a * b, al * N, N * be, tt::map2(b, al * a, 1),
+                     tt::map2(N, b * al * a, a)),
+                  s);
+  if (e != cudaSuccess) return e;
+  g_stage = TT_ST_IR_S3;
+  SplitScratch scratch(P, pe);
+  return launch_gemm(true, false,
+                     gp(x, N * b, T2, al * a, out, a, al * a, N * b, tt::map_plain(al * a),
+                        tt::map_plain(1)),
+                     s);
+}
+
+// ---- Petrov-Galerkin (bra train != ket train) variants --------------------------------------
+// The same three-GEMM stage plans with the bra ranks (ap = a', bp = b') decoupled from the ket
+// ranks (a, b): the local operator Z_{!=k}^T A X_{!=k} of two different trains, the projected
+// right-hand side X_{!=k}^T b (identity operator) and the AMEn residual frame
+// (PAPER.md:303).  Interfaces are [bra, op, ket]: phiL (ap, al, a), phiR (bp, be, b).
+bool dims_pg_valid(const DimsPG& d) {
+  return d.ap > 0 && d.a > 0 && d.n > 0 && d.bp > 0 && d.b > 0 && d.al > 0 && d.be > 0;
+}
+// element counts for the matvec (K columns) and both interface updates
+bool pg_ws_elems(const DimsPG& d, long long K, long long& t1, long long& t2, long long& ah,
+                 long long& pe) {
+  bool ok = true;
+  t1 = std::max({prod({d.ap, d.al, d.n, K, d.b}, ok), prod({d.a, d.n, d.bp, d.be}, ok)});
+  t2 = std::max({prod({d.ap, d.n, K, d.be, d.b}, ok), prod({d.n, d.bp, d.al, d.a}, ok)});
+  ah = prod({d.al, d.n, d.n, d.be}, ok);
+  const long long out = std::max({prod({d.ap, d.n, K, d.bp}, ok), prod({d.bp, d.be, d.b}, ok),
+                                  prod({d.ap, d.al, d.a}, ok)});
+  pe = std::max(4 * out, std::min(64 * out, 16LL << 20));
+  return ok;
+}
+
+// Y (ap, n, K, bp) = phiL (ap, al, a) x A x phiR (bp, be, b) applied to X (a, n, K, b)
+cudaError_t enqueue_matvec_pg(const DimsPG& d, long long K, const double* phiL, const double* A,
+                              const double* phiR, const double* X, double* Y, double* T1,
+                              double* T2, double* Ah, double* P, long long pe, cudaStream_t s) {
+  const long long ap = d.ap, a = d.a, bp = d.bp, b = d.b, al = d.al, be = d.be, N = d.n;
+  cudaError_t e;
+  if ((e = launch_perm(true, A, Ah, al, N, be, s)) != cudaSuccess) return e;
+  // S1: T1(al, j, a', m, b) = phiL[(a' al), a] . X[a, (j m b)]
+  g_stage = TT_ST_MV_S1;
+  e = launch_gemm(true, false,
+                  gp(phiL, a, X, N * K * b, T1, ap * al, N * K * b, a,
+                     tt::map2(al, N * ap * K * b, K * b), tt::map2(K * b, 1, ap * K * b)),
+                  s);
+  if (e != cudaSuccess) return e;
+  // S2: T2(a', m, i, be, b) = T1^T[(a' m b), (al j)] . Ahat[(al j), (i be)]
+  g_stage = TT_ST_MV_S2;
+  e = launch_gemm(false, false,
+                  gp(T1, ap * K * b, Ah, N * be, T2, ap * K * b, N * be, al * N,
+                     tt::map2(b, 1, N * be * b), tt::map_plain(b)),
+                  s);
+  if (e != cudaSuccess) return e;
+  // S3: Y(a', i, m, b') = T2[(a' m i), (be b)] . phiR[b', (be b)]^T
+  g_stage = TT_ST_MV_S3;
+  SplitScratch scratch(P, pe);
+  return launch_gemm(true, true,
+                     gp(T2, be * b, phiR, be * b, Y, ap * K * N, bp, be * b,
+                        tt::map3(N, K, K * bp, bp, N * K * bp), tt::map_plain(1)),
+                     s);
+}
+
+// phiL_next (bp, be, b) = sum x_bra[a', i, b'] phiL[a', al, a] A[al, i, j, be] x_ket[a, j, b]
+cudaError_t enqueue_left_pg(const DimsPG& d, const double* phiL, const double* A,
+                            const double* xb, const double* xk, double* out, double* T1,
+                            double* T2, double* Ah, double* P, long long pe, cudaStream_t s) {
+  const long long ap = d.ap, a = d.a, bp = d.bp, b = d.b, al = d.al, be = d.be, N = d.n;
+  cudaError_t e;
+  if ((e = launch_perm(true, A, Ah, al, N, be, s)) != cudaSuccess) return e;
+  g_stage = TT_ST_IL_S1;   // T1(al, j, a', b) = phiL[(a' al), a] . x_ket[a, (j b)]
+  e = launch_gemm(true, false,
+                  gp(phiL, a, xk, N * b, T1, ap * al, N * b, a, tt::map2(al, N * ap * b, b),
+                     tt::map2(b, 1, ap * b)),
+                  s);
+  if (e != cudaSuccess) return e;
+  g_stage = TT_ST_IL_S2;   // T2(a', i, be, b) = T1^T[(a' b), (al j)] . Ahat[(al j), (i be)]
+  e = launch_gemm(false, false,
+                  gp(T1, ap * b, Ah, N * be, T2, ap * b, N * be, al * N, tt::map2(b, 1, N * be * b),
+                     tt::map_plain(b)),
+                  s);
+  if (e != cudaSuccess) return e;
+  g_stage = TT_ST_IL_S3;   // out[b', (be b)] = x_bra^T[b', (a' i)] . T2[(a' i), (be b)]
+  SplitScratch scratch(P, pe);
+  return launch_gemm(false, false,
+                     gp(xb, bp, T2, be * b, out, bp, be * b, ap * N, tt::map_plain(be * b),
+                        tt::map_plain(1)),
+                     s);
+}
+
+// phiR_prev (ap, al, a) = sum x_bra[a', i, b'] A[al, i, j, be] phiR[b', be, b] x_ket[a, j, b]
+cudaError_t enqueue_right_pg(const DimsPG& d, const double* phiR, const double* A,
+                             const double* xb, const double* xk, double* out, double* T1,
+                             double* T2, double* At, double* P, long long pe, cudaStream_t s) {
+  const long long ap = d.ap, a = d.a, bp = d.bp, b = d.b, al = d.al, be = d.be, N = d.n;
+  cudaError_t e;
+  if ((e = launch_perm(false, A, At, al, N, be, s)) != cudaSuccess) return e;
+  g_stage = TT_ST_IR_S1;   // T1(j, be, a, b') = x_ket[(a j), b] . phiR[(b' be), b]^T
+  e = launch_gemm(true, true,
+                  gp(xk, b, phiR, b, T1, a * N, bp * be, b, tt::map2(N, be * a * bp, bp),
+                     tt::map2(be, a * bp, 1)),
+                  s);
+  if (e != cudaSuccess) return e;
+  g_stage = TT_ST_IR_S2;   // T2(i, b', al, a) = T1^T[(a b'), (j be)] . Atil[(j be), (al i)]
+  e = launch_gemm(false, false,
+                  gp(T1, a * bp, At, al * N, T2, a * bp, al * N, N * be, tt::map2(bp, al * a, 1),
+                     tt::map2(N, bp * al * a, a)),
+                  s);
+  if (e != cudaSuccess) return e;
+  g_stage = TT_ST_IR_S3;   // out[a', (al a)] = x_bra[a', (i b')] . T2[(i b'), (al a)]
+  SplitScratch scratch(P, pe);
+  return launch_gemm(true, false,
+                     gp(xb, N * bp, T2, al * a, out, ap, al * a, N * bp, tt::map_plain(al * a),
+                        tt::map_plain(1)),
+                     s);
+}
+
+tt_status cuda_fail(cudaError_t e, const char* where) {
+  return fail(TT_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+
+tt_status check_dims(const Dims& d) {
+  if (!dims_valid(d)) return fail(TT_ERR_INVALID_ARGUMENT, "extents must be positive");
+  bool ok = true;
+  prod({d.a, d.al, d.n, d.b}, ok);
+  prod({d.a, d.n, d.be, d.b}, ok);
+  prod({d.al, d.n, d.n, d.be}, ok);
+  prod({d.b, d.be, d.b}, ok);
+  prod({d.a, d.al, d.a}, ok);
+  if (!ok) return fail(TT_ERR_OVERFLOW, "extent product overflows");
+  return TT_OK;
+}
+
+bool same(const void* p, const void* q) { return p != nullptr && p == q; }
+
+}  // namespace ttint

@@ -357,7 +357,7 @@ dmma_gemm_v2_kernel(const GemmParamsV2 p) {
 }
 
 // C[rowmap(m) + colmap(n)] = sum_s P[s][m][n]  (split-K reduction, fixed summation order)
-__global__ void __launch_bounds__(256) splitk_reduce_kernel(const double* __restrict__ P,
+static __global__ void __launch_bounds__(256) splitk_reduce_kernel(const double* __restrict__ P,
                                                             double* __restrict__ C, int M, int N,
                                                             int ksplit, IndexMap32 rowmap,
                                                             IndexMap32 colmap,

@@ -9,7 +9,7 @@
 // Gram-Schmidt of the textbook algorithm).  The Hessenberg least-squares problem of every column is updated by Givens
 // rotations in a one-thread-per-column kernel; converged columns are frozen by a device-side
 // flag, so the whole solve is a fixed sequence of launches (asynchronous, graph-capturable).
-// Included by tt_hotpath.cu inside its anonymous namespace.
+// Included by tt_solvers.cu inside namespace ttint.
 
 constexpr int kMaxL = 32;   // basis vectors per reduction pass
 

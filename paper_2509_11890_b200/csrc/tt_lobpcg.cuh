@@ -23,7 +23,7 @@
 // |lam| ||B x||) <= tol) sets a device flag that turns every later launch, the GEMMs of the
 // matvecs included (GemmParams::gate), into a no-op: the solve is a fixed, asynchronous,
 // graph-capturable launch sequence whose iterations after convergence cost launches only.
-// Included by tt_hotpath.cu inside its anonymous namespace.
+// Included by tt_solvers.cu inside namespace ttint.
 
 constexpr int kLobMaxNb = 32;
 // Cholesky pivot floor of the equilibrated Gram matrix (squared norm of the new direction a

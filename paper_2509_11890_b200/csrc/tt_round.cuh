@@ -7,7 +7,7 @@
 // Exactly rank-deficient unfoldings (e.g. the formal sum T + T) are handled: zero singular
 // values are dropped.  The truncation decisions are data dependent, so the host reads the
 // singular values of every core (one synchronisation per core).
-// Included by tt_hotpath.cu inside its anonymous namespace.
+// Included by tt_solvers.cu inside namespace ttint.
 
 // Multi-CTA parallel Jacobi (cooperative launch, one grid barrier per step).  The n x n
 // matrix is embedded in an np x np one (np even; a dummy isolated index if n is odd) and
