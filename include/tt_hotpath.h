@@ -378,7 +378,20 @@ tt_status tt_sweep_w34(int64_t d, const int64_t* n, const int64_t* r, const int6
                        double* const* phiL, double* const* phiR, double* const* y_cores,
                        void* workspace, size_t workspace_bytes, void* stream);
 
-/* Number of kernel launches the last call on this thread enqueued. */
+/* Graph cache for eager calls (default on).  tt_local_matvec(_batched), tt_interface_left/right,
+ * tt_sweep_interfaces, tt_sweep_w34 and tt_sweep_als enqueue several kernels per call; the second
+ * time a call arrives with the same extents, the same device pointers (host pointer arrays
+ * compared by content), the same workspace and the same debug state on the calling thread, it
+ * is captured once on an internal stream into a CUDA graph and from then on replayed with one
+ * cudaGraphLaunch into the caller's stream (same kernels, same results).  Bypassed while the
+ * caller's stream is being captured and while tracing.  Up to 32 graphs per thread (LRU);
+ * tt_set_graph_cache(0) disables the cache and destroys its graphs.  A cached graph keeps
+ * referring to the device buffers of its key: free or reuse them only as with any pending
+ * enqueued work. */
+void tt_set_graph_cache(int enabled);
+
+/* Number of kernel launches the last call on this thread enqueued (for a replayed graph: the
+ * kernels it contains). */
 int64_t tt_last_launch_count(void);
 /* Test hook: on != 0 routes every GEMM stage of the calling thread through the generic
  * (unaligned-capable) kernel instead of the persistent 16-byte-load kernel. */
@@ -404,6 +417,15 @@ void tt_debug_set_variant(int v);
  * tt_debug_set_variant(v): v >= 10 forces
  * the GEMM tile configuration v % 100 (probe list in csrc/tt_launch_tpl.cuh) and split-K factor v / 100. */
 void tt_debug_set_flags(int flags);
+/* Benchmark hook: the experimental persistent DAG executor for tt_sweep_w34 on the calling
+ * thread (one launch for the whole sweep, csrc/tt_dag.cuh): 0 = off (default: the stream/event
+ * version, measured faster), 1 = on with 4-warp 64 x 64 tiles, 2 = 8-warp. */
+void tt_debug_set_dag(int mode);
+/* Measurement hook: while buf != NULL (device, 5 x uint64 per unit, cap_units units) the next
+ * DAG launches of the calling thread record per unit {grab, ready, computed, published,
+ * smid} (%globaltimer ns).  Copies the last DAG's per-task first-unit table into unit0 (host,
+ * cap_tasks entries, + total) and returns (tasks << 32) | units of the last DAG launch. */
+int64_t tt_debug_dag_trace(void* buf, int64_t cap_units, int32_t* unit0, int64_t cap_tasks);
 
 /* ---------------------------------------------------------------------------------------
  * Tracing (measurement support, not part of the math).  While enabled on the calling
@@ -412,14 +434,15 @@ void tt_debug_set_flags(int flags);
  * for non-GEMM kernels N = K = 0 and M = elements written).  Do not enable while capturing
  * a CUDA graph.  tt_trace_read synchronises on record i's end event.
  *   stage: TT_ST_PERM, TT_ST_SET, TT_ST_MV_S1..S3 (local matvec), TT_ST_IL_S1..S3 (left
- *   interface), TT_ST_IR_S1..S3 (right interface), TT_ST_APPLY.  tile = the GEMM tile's BN.
+ *   interface), TT_ST_IR_S1..S3 (right interface), TT_ST_APPLY, TT_ST_DAG (one persistent
+ *   DAG launch: tile = its task count, M = its tile units).  tile = the GEMM tile's BN.
  * ------------------------------------------------------------------------------------- */
 enum {
   TT_ST_PERM = 0, TT_ST_SET = 1,
   TT_ST_MV_S1 = 2, TT_ST_MV_S2 = 3, TT_ST_MV_S3 = 4,
   TT_ST_IL_S1 = 5, TT_ST_IL_S2 = 6, TT_ST_IL_S3 = 7,
   TT_ST_IR_S1 = 8, TT_ST_IR_S2 = 9, TT_ST_IR_S3 = 10,
-  TT_ST_APPLY = 11
+  TT_ST_APPLY = 11, TT_ST_DAG = 12
 };
 tt_status tt_trace_enable(int64_t capacity);
 tt_status tt_trace_disable(void);

@@ -24,7 +24,9 @@ __all__ = [
     "tt_sweep_als", "tt_operator_apply", "tt_last_launch_count",
     "TT_SWEEP_LEFT", "TT_SWEEP_RIGHT", "TT_SWEEP_BOTH", "tt_trace_enable", "tt_trace_disable",
     "tt_trace_count", "tt_trace_read", "tt_fp64_peak_probe", "STAGE_NAMES", "tt_debug_force_v1",
-    "tt_debug_set_variant", "tt_debug_set_flags", "tt_local_gmres", "tt_local_gmres_workspace_size",
+    "tt_debug_set_variant", "tt_debug_set_flags", "tt_debug_set_dag", "tt_debug_dag_trace", "tt_set_graph_cache",
+    "tt_local_gmres",
+    "tt_local_gmres_workspace_size",
     "tt_local_matvec_two_site", "tt_local_matvec_two_site_workspace_size",
     "tt_block_local_matvec", "tt_block_local_matvec_workspace_size", "TTBlockTerm",
     "tt_round", "tt_round_workspace_size", "tt_debug_sym_eigen",
@@ -134,6 +136,12 @@ lib.tt_debug_set_variant.argtypes = [ctypes.c_int]
 lib.tt_debug_set_variant.restype = None
 lib.tt_debug_set_flags.argtypes = [ctypes.c_int]
 lib.tt_debug_set_flags.restype = None
+lib.tt_debug_set_dag.argtypes = [ctypes.c_int]
+lib.tt_debug_set_dag.restype = None
+lib.tt_set_graph_cache.argtypes = [ctypes.c_int]
+lib.tt_set_graph_cache.restype = None
+lib.tt_debug_dag_trace.argtypes = [_p, _i64, _p, _i64]
+lib.tt_debug_dag_trace.restype = ctypes.c_int64
 for _f in ("tt_trace_enable", "tt_trace_disable", "tt_trace_read", "tt_fp64_peak_probe"):
     getattr(lib, _f).restype = ctypes.c_int
 for _f in ("tt_local_matvec", "tt_local_matvec_batched", "tt_interface_left",
@@ -508,6 +516,29 @@ def tt_debug_force_v1(on: bool) -> None:
 def tt_debug_set_variant(v: int) -> None:
     """Benchmark hook: GEMM tiling variant for this thread (-1 default, 0, 1)."""
     lib.tt_debug_set_variant(int(v))
+
+
+def tt_set_graph_cache(enabled: bool) -> None:
+    """Eager multi-launch calls are replayed from a per-thread CUDA graph cache from the second
+    identical call on (default on); False disables it and destroys the cached graphs."""
+    lib.tt_set_graph_cache(1 if enabled else 0)
+
+
+def tt_debug_set_dag(mode: int) -> None:
+    """Benchmark hook: experimental DAG executor for tt_sweep_w34 (0 off = default, 1 / 2 on)."""
+    lib.tt_debug_set_dag(int(mode))
+
+
+def tt_debug_dag_trace(buf=None):
+    """Measurement hook: record per-unit timestamps of the next DAG launches into buf (CUDA
+    uint64 tensor of 5 x units); returns (tasks, units, unit0 list) of the last DAG launch."""
+    import numpy as np
+    u0 = np.zeros(4096, dtype=np.int32)
+    cap = buf.numel() // 5 if buf is not None else 0
+    v = lib.tt_debug_dag_trace(buf.data_ptr() if buf is not None else None, cap,
+                               u0.ctypes.data, len(u0))
+    nt, nu = int(v >> 32), int(v & 0xffffffff)
+    return nt, nu, u0[: nt + 1].tolist()
 
 
 def tt_debug_set_flags(flags: int) -> None:

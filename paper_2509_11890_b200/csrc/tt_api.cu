@@ -137,6 +137,19 @@ void tt_debug_set_variant(int v) {
   g_variant = v;
   g_force_ks = v >= 10 ? v / 100 : 0;
 }
+void tt_debug_set_dag(int mode) { g_dag_mode = mode; }
+void tt_set_graph_cache(int enabled) {
+  g_graph_cache_on = enabled ? 1 : 0;
+  if (!enabled) graph_cache_clear();
+}
+int64_t tt_debug_dag_trace(void* buf, int64_t cap_units, int32_t* unit0, int64_t cap_tasks) {
+  g_dag_trace = static_cast<unsigned long long*>(buf);
+  g_dag_trace_cap = buf ? cap_units : 0;
+  if (unit0)
+    for (int64_t i = 0; i < cap_tasks && i < (int64_t)g_dag_last_unit0.size(); ++i)
+      unit0[i] = g_dag_last_unit0[size_t(i)];
+  return ((int64_t)g_dag_last_tasks << 32) | (int64_t)g_dag_last_units;
+}
 void tt_debug_set_flags(int f) {
   g_dbg_flags = f;
   g_side_lowprio = (f & 2048) ? 1 : 0;
@@ -176,10 +189,14 @@ tt_status tt_local_matvec_batched(int64_t rl, int64_t n, int64_t rr, int64_t Rl,
   double* Ah = c.take(ah);
   double* Pp = c.take(pe);
   if (!c.ok) return fail(TT_ERR_WORKSPACE, "workspace too small after alignment");
-  cudaError_t e = enqueue_matvec(d, nvec, phiL, A, phiR, X, Y, T1, T2, Ah, Pp, pe,
-                                 static_cast<cudaStream_t>(stream));
-  if (e != cudaSuccess) return cuda_fail(e, "tt_local_matvec_batched");
-  return TT_OK;
+  auto body = [&](cudaStream_t s) -> tt_status {
+    cudaError_t e = enqueue_matvec(d, nvec, phiL, A, phiR, X, Y, T1, T2, Ah, Pp, pe, s);
+    return e == cudaSuccess ? TT_OK : cuda_fail(e, "tt_local_matvec_batched");
+  };
+  GraphKey key;
+  key.add(1).add(rl).add(n).add(rr).add(Rl).add(Rr).add(nvec).add(phiL).add(A).add(phiR).add(X)
+      .add(Y).add(workspace).add(workspace_bytes);
+  return graph_cached(key, static_cast<cudaStream_t>(stream), body, "tt_local_matvec_batched");
 }
 
 tt_status tt_local_matvec(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t Rr,
@@ -221,12 +238,17 @@ static tt_status iface_common(bool left, int64_t rl, int64_t n, int64_t rr, int6
   double* Ah = c.take(ah);
   double* Pp = c.take(pe);
   if (!c.ok) return fail(TT_ERR_WORKSPACE, "workspace too small after alignment");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  cudaError_t e = left ? enqueue_left(d, phi_in, A, x, phi_out, T1, T2, Ah, Pp, pe, s)
-                       : (g_dbg_flags & 8) ? enqueue_right(d, phi_in, A, x, phi_out, T1, T2, Ah, Pp, pe, s)
-                                            : enqueue_right_mirror(d, phi_in, A, x, phi_out, T1, T2, Ah, Pp, pe, s);
-  if (e != cudaSuccess) return cuda_fail(e, left ? "tt_interface_left" : "tt_interface_right");
-  return TT_OK;
+  auto body = [&](cudaStream_t s) -> tt_status {
+    cudaError_t e = left ? enqueue_left(d, phi_in, A, x, phi_out, T1, T2, Ah, Pp, pe, s)
+                         : (g_dbg_flags & 8) ? enqueue_right(d, phi_in, A, x, phi_out, T1, T2, Ah, Pp, pe, s)
+                                              : enqueue_right_mirror(d, phi_in, A, x, phi_out, T1, T2, Ah, Pp, pe, s);
+    return e == cudaSuccess ? TT_OK : cuda_fail(e, left ? "tt_interface_left" : "tt_interface_right");
+  };
+  GraphKey key;
+  key.add(left ? 2 : 3).add(rl).add(n).add(rr).add(Rl).add(Rr).add(phi_in).add(A).add(x).add(phi_out)
+      .add(workspace).add(workspace_bytes);
+  return graph_cached(key, static_cast<cudaStream_t>(stream), body,
+                      left ? "tt_interface_left" : "tt_interface_right");
 }
 
 tt_status tt_interface_left(int64_t rl, int64_t n, int64_t rr, int64_t Rl, int64_t Rr,
@@ -490,7 +512,7 @@ tt_status tt_sweep_interfaces(int64_t d, const int64_t* n, const int64_t* r, con
   if (need == 0) return fail(TT_ERR_OVERFLOW, "workspace overflow");
   if (!workspace || workspace_bytes < need)
     return fail(TT_ERR_WORKSPACE, "workspace NULL or smaller than " + std::to_string(need) + " bytes");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  auto body = [&](cudaStream_t s) -> tt_status {
   cudaError_t e;
   char* wsb = static_cast<char*>(workspace);
   const size_t main_b = sweep_step_ws(d, n, r, R, 0);
@@ -520,6 +542,10 @@ tt_status tt_sweep_interfaces(int64_t d, const int64_t* n, const int64_t* r, con
   }
   if (sr != s && (e = stream_dep(sr, s)) != cudaSuccess) return cuda_fail(e, "join");
   return TT_OK;
+  };
+  GraphKey key;
+  key.add(4).add(d).arr(n, d).arr(r, d + 1).arr(R, d + 1).arr(x_cores, d).arr(A_cores, d).arr(phiL, d + 1).arr(phiR, d + 1).add(directions).add(workspace).add(workspace_bytes);
+  return graph_cached(key, static_cast<cudaStream_t>(stream), body, "tt_sweep_interfaces");
 }
 
 // ---- W34 as one DAG-scheduled call: both interface chains and one matvec per core ---------
@@ -552,13 +578,108 @@ static size_t w34_t2_keep(int64_t d, const int64_t* n, const int64_t* r, const i
   return tot;
 }
 
-size_t tt_sweep_w34_workspace_size(int64_t d, const int64_t* n, const int64_t* r,
-                                   const int64_t* R) {
+static size_t w34_stream_ws(int64_t d, const int64_t* n, const int64_t* r, const int64_t* R) {
   if (d <= 0 || !n || !r || !R) return 0;
   const size_t base = sweep_ws(d, n, r, R, 0), mv = w34_mv_scratch(d, n, r, R);
   const size_t keep = w34_t2_keep(d, n, r, R);
   if (base == 0 || mv == 0 || keep == 0) return 0;
   return align_up(base, 256) + kPoolStreams * align_up(mv, 256) + keep + 256;
+}
+
+// W34 on the persistent DAG executor (tt_dag.cuh): the same stage GEMMs as the stream version
+// (left chain = lane 0, right chain = lane 1, core k's matvec = lane 2 + k, waiting on the left
+// update's T2_k task and on the right update that produced phiR[k+1]), recorded into one
+// kernel launch after the preparation kernel.  With ws == nullptr the recording is a dry run
+// that sizes the split-K partials (pointers are only carried, never dereferenced).
+static cudaError_t w34_dag_record(DagBuilder& B, int64_t d, const int64_t* n, const int64_t* r,
+                                  const int64_t* R, const double* const* xc, const double* const* Ac,
+                                  double* const* phiL, double* const* phiR, double* const* yc,
+                                  char* ws, cudaStream_t s) {
+  char* wsb = ws ? ws : reinterpret_cast<char*>(uintptr_t(1) << 40);   // dry run: fake base
+  const size_t main_b = sweep_step_ws(d, n, r, R, 0);
+  void* ws_main = wsb;
+  void* ws_side = wsb + align_up(main_b, 256);
+  const size_t mv_b = w34_mv_scratch(d, n, r, R);
+  char* kb = wsb + align_up(sweep_ws(d, n, r, R, 0), 256) + kPoolStreams * align_up(mv_b, 256);
+  kb += (256 - (reinterpret_cast<uintptr_t>(kb) & 255)) & 255;
+  std::vector<double*> T2k(d);
+  for (int64_t k = 0; k < d; ++k) {
+    T2k[k] = reinterpret_cast<double*>(kb);
+    kb += align_up((size_t)(r[k] * n[k] * R[k + 1] * r[k + 1]) * 8, 256);
+  }
+  double* const* pL = phiL;
+  double* const* pR = phiR;
+  std::vector<double*> fakeL, fakeR, fakeY;
+  std::vector<const double*> fakeX, fakeA;
+  if (!ws) {   // dry run: distinct fake operands and outputs
+    for (int64_t k = 0; k <= d; ++k) {
+      fakeX.push_back(reinterpret_cast<const double*>((uintptr_t(5) << 40) + (uintptr_t)k * 4096));
+      fakeA.push_back(reinterpret_cast<const double*>((uintptr_t(6) << 40) + (uintptr_t)k * 4096));
+      fakeL.push_back(reinterpret_cast<double*>((uintptr_t(2) << 40) + (uintptr_t)k * 4096));
+      fakeR.push_back(reinterpret_cast<double*>((uintptr_t(3) << 40) + (uintptr_t)k * 4096));
+      fakeY.push_back(reinterpret_cast<double*>((uintptr_t(4) << 40) + (uintptr_t)k * 4096));
+    }
+    pL = fakeL.data();
+    pR = fakeR.data();
+    yc = fakeY.data();
+    xc = fakeX.data();
+    Ac = fakeA.data();
+  }
+  DagScope scope(&B);
+  cudaError_t e;
+  std::vector<int> t2_task(d, -1), phiR_task(d + 1, -1);
+  B.set_lane(0);
+  for (int64_t k = 0; k < d; ++k) {
+    const int c0 = B.count();
+    if ((e = sweep_left_step(k, d, 0, ws_main, n, r, R, xc, Ac, pL, wsb, main_b, s, T2k[k])) != cudaSuccess)
+      return e;
+    if (B.count() != c0 + 3) return cudaErrorInvalidValue;
+    t2_task[k] = c0 + 1;
+  }
+  B.set_lane(1);
+  for (int64_t k = d - 1; k >= 0; --k) {
+    if ((e = sweep_right_step(k, d, 0, ws_side, n, r, R, xc, Ac, pR, wsb, main_b, s)) != cudaSuccess)
+      return e;
+    phiR_task[k] = B.last_of(1);
+  }
+  for (int64_t k = 0; k < d; ++k) {
+    B.set_lane(2 + (int)k);
+    B.add_dep(t2_task[k]);
+    B.add_dep(phiR_task[k + 1]);   // -1 (phiR[d] = 1, written by the preparation) is ignored
+    Dims dk{r[k], n[k], r[k + 1], R[k], R[k + 1]};
+    if ((e = enqueue_matvec_last(dk, 1, T2k[k], pR[k + 1], yc[k], nullptr, 0, s)) != cudaSuccess)
+      return e;
+  }
+  return B.ok ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+// split-K partial elements of the W34 DAG (dry recording), -1 when it does not fit the executor
+static long long w34_dag_partials(int64_t d, const int64_t* n, const int64_t* r, const int64_t* R) {
+  // cached per shape (the dry recording costs ~10-40 us of host time per call otherwise)
+  thread_local std::vector<int64_t> key;
+  thread_local long long cached = -2;
+  std::vector<int64_t> k2;
+  k2.push_back(d);
+  k2.insert(k2.end(), n, n + d);
+  k2.insert(k2.end(), r, r + d + 1);
+  k2.insert(k2.end(), R, R + d + 1);
+  if (cached != -2 && k2 == key) return cached;
+  DagBuilder B(nullptr, 0);
+  if (w34_dag_record(B, d, n, r, R, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr) !=
+      cudaSuccess)
+    cached = -1;
+  else
+    cached = B.partials_needed();
+  key = k2;
+  return cached;
+}
+
+size_t tt_sweep_w34_workspace_size(int64_t d, const int64_t* n, const int64_t* r,
+                                   const int64_t* R) {
+  const size_t base = w34_stream_ws(d, n, r, R);
+  if (base == 0) return 0;
+  const long long pe = w34_dag_partials(d, n, r, R);
+  return base + (pe >= 0 ? dag_scratch_bytes(pe) : 0);
 }
 
 tt_status tt_sweep_w34(int64_t d, const int64_t* n, const int64_t* r, const int64_t* R,
@@ -580,16 +701,32 @@ tt_status tt_sweep_w34(int64_t d, const int64_t* n, const int64_t* r, const int6
   if (need == 0) return fail(TT_ERR_OVERFLOW, "workspace overflow");
   if (!workspace || workspace_bytes < need)
     return fail(TT_ERR_WORKSPACE, "workspace NULL or smaller than " + std::to_string(need) + " bytes");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  auto body = [&](cudaStream_t s) -> tt_status {
   cudaError_t e;
   char* wsb = static_cast<char*>(workspace);
+  // persistent DAG executor: one preparation launch + one DAG launch (tt_dag.cuh); debug bits
+  // 3 (direct right update, launches its own permutation) and 23 keep the stream version
+  if (g_dag_mode > 0 && !(g_dbg_flags & (8 | 8388608))) {
+    const long long pe = w34_dag_partials(d, n, r, R);
+    if (pe >= 0) {
+      const size_t base = w34_stream_ws(d, n, r, R);
+      DagBuilder B(wsb + base, workspace_bytes - base);
+      if (!B.ok) return fail(TT_ERR_WORKSPACE, "workspace too small for the DAG scratch");
+      if ((e = w34_dag_record(B, d, n, r, R, x_cores, A_cores, phiL, phiR, y_cores, wsb, s)) != cudaSuccess)
+        return fail(TT_ERR_INVALID_ARGUMENT, "W34 DAG recording failed");
+      if ((e = launch_prep(d, n, r, R, 0, x_cores, A_cores, workspace, s, phiL[0], phiR[d])) != cudaSuccess)
+        return cuda_fail(e, "sweep prep");
+      if ((e = B.launch(s)) != cudaSuccess) return cuda_fail(e, "W34 DAG launch");
+      return TT_OK;
+    }
+  }
   const size_t main_b = sweep_step_ws(d, n, r, R, 0);
   void* ws_main = wsb;
   void* ws_side = wsb + align_up(main_b, 256);
   const size_t mv_b = w34_mv_scratch(d, n, r, R);
   char* mv_base = wsb + align_up(sweep_ws(d, n, r, R, 0), 256);
   if ((e = pool_init(size_t(3 * (d + 1) + kPoolStreams + 4))) != cudaSuccess) return cuda_fail(e, "pool");
-  cudaEvent_t* evL = g_pool.ev.data();         // evL[k]: phiL[k] ready
+  cudaEvent_t* evL = g_res.pool.ev.data();         // evL[k]: phiL[k] ready
   cudaEvent_t* evR = evL + (d + 1);            // evR[k]: phiR[k] ready
   cudaEvent_t* evT = evR + (d + 1);            // evT[k]: the left update's T2_k ready
   cudaEvent_t* evJ = evT + (d + 1);            // joins
@@ -610,9 +747,9 @@ tt_status tt_sweep_w34(int64_t d, const int64_t* n, const int64_t* r, const int6
   if ((e = side_stream(&sr)) != cudaSuccess) return cuda_fail(e, "side stream");
   if ((e = stream_dep(s, sr)) != cudaSuccess) return cuda_fail(e, "fork");
   for (int q = 0; q < kPoolStreams; ++q)
-    if ((e = stream_dep(s, g_pool.s[q])) != cudaSuccess) return cuda_fail(e, "fork");
+    if ((e = stream_dep(s, g_res.pool.s[q])) != cudaSuccess) return cuda_fail(e, "fork");
   // the two chains, on high-priority streams (the critical path)
-  cudaStream_t sl = g_pool.chain;
+  cudaStream_t sl = g_res.pool.chain;
   if ((e = stream_dep(s, sl)) != cudaSuccess) return cuda_fail(e, "fork");
   if ((e = cudaEventRecord(evL[0], sl)) != cudaSuccess) return cuda_fail(e, "event");
   for (int64_t k = 0; k < d; ++k) {
@@ -637,7 +774,7 @@ tt_status tt_sweep_w34(int64_t d, const int64_t* n, const int64_t* r, const int6
   for (int64_t i = 0; i < d; ++i) {
     const int64_t k = order[i];
     const int q = (int)(i % kPoolStreams);
-    cudaStream_t ps = g_pool.s[q];
+    cudaStream_t ps = g_res.pool.s[q];
     if ((e = cudaStreamWaitEvent(ps, reuse ? evT[k] : evL[k], 0)) != cudaSuccess) return cuda_fail(e, "wait");
     if ((e = cudaStreamWaitEvent(ps, evR[k + 1], 0)) != cudaSuccess) return cuda_fail(e, "wait");
     Dims dk{r[k], n[k], r[k + 1], R[k], R[k + 1]};
@@ -666,10 +803,14 @@ tt_status tt_sweep_w34(int64_t d, const int64_t* n, const int64_t* r, const int6
       (e = cudaStreamWaitEvent(s, evJ[1 + kPoolStreams], 0)) != cudaSuccess)
     return cuda_fail(e, "join");
   for (int q = 0; q < kPoolStreams; ++q)
-    if ((e = cudaEventRecord(evJ[1 + q], g_pool.s[q])) != cudaSuccess ||
+    if ((e = cudaEventRecord(evJ[1 + q], g_res.pool.s[q])) != cudaSuccess ||
         (e = cudaStreamWaitEvent(s, evJ[1 + q], 0)) != cudaSuccess)
       return cuda_fail(e, "join");
   return TT_OK;
+  };
+  GraphKey key;
+  key.add(5).add(d).arr(n, d).arr(r, d + 1).arr(R, d + 1).arr(x_cores, d).arr(A_cores, d).arr(phiL, d + 1).arr(phiR, d + 1).arr(y_cores, d).add(workspace).add(workspace_bytes);
+  return graph_cached(key, static_cast<cudaStream_t>(stream), body, "tt_sweep_w34");
 }
 
 tt_status tt_sweep_als(int64_t d, const int64_t* n, const int64_t* r, const int64_t* R,
@@ -697,7 +838,7 @@ tt_status tt_sweep_als(int64_t d, const int64_t* n, const int64_t* r, const int6
   if (need == 0) return fail(TT_ERR_OVERFLOW, "workspace overflow");
   if (!workspace || workspace_bytes < need)
     return fail(TT_ERR_WORKSPACE, "workspace NULL or smaller than " + std::to_string(need) + " bytes");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  auto body = [&](cudaStream_t s) -> tt_status {
   cudaError_t e;
   double* const* Yb = Y_bwd ? Y_bwd : Y_fwd;
   char* wsb = static_cast<char*>(workspace);
@@ -746,6 +887,10 @@ tt_status tt_sweep_als(int64_t d, const int64_t* n, const int64_t* r, const int6
   }
   if ((e = stream_dep(ss, s)) != cudaSuccess) return cuda_fail(e, "join");
   return TT_OK;
+  };
+  GraphKey key;
+  key.add(6).add(d).arr(n, d).arr(r, d + 1).arr(R, d + 1).add(nvec).arr(x_cores, d).arr(A_cores, d).arr(X_blocks, d).arr(Y_fwd, d).arr(Y_bwd, d).arr(phiL, d + 1).arr(phiR, d + 1).add(workspace).add(workspace_bytes);
+  return graph_cached(key, static_cast<cudaStream_t>(stream), body, "tt_sweep_als");
 }
 
 // ---- H8 ----------------------------------------------------------------------------------

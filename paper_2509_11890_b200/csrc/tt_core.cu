@@ -14,60 +14,194 @@ thread_local std::vector<TraceRec> g_trace;
 thread_local std::vector<cudaEvent_t> g_trace_pool;
 thread_local int g_stage = TT_ST_PERM;   // stage tag of the next launch
 
-// ---- side stream for the sweeps' concurrent interface chains (per thread, per device) ------
-thread_local SideStream g_side;
+// ---- per-thread, per-device stream resources (side stream, W34 pool, capture stream) -------
+// Created lazily on the current device; a device switch parks the previous device's set (it is
+// reused when that device becomes current again, never leaked), and everything -- streams,
+// events and the cached graph executables -- is destroyed when the thread exits.
 thread_local int g_side_lowprio = 0;
+thread_local ThreadRes g_res;
+
+void SideStream::release() {
+  for (auto& ev : this->ev)
+    if (ev) cudaEventDestroy(ev);
+  if (s) cudaStreamDestroy(s);
+  if (s_lo) cudaStreamDestroy(s_lo);
+  *this = SideStream{};
+}
+void StreamPool::release() {
+  for (auto& ev : this->ev) cudaEventDestroy(ev);
+  for (auto& st : s)
+    if (st) cudaStreamDestroy(st);
+  if (chain) cudaStreamDestroy(chain);
+  if (capture) cudaStreamDestroy(capture);
+  *this = StreamPool{};
+}
+ThreadRes::~ThreadRes() {
+  for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
+  side.release();
+  pool.release();
+  for (auto& p : side_parked) p.release();
+  for (auto& p : pool_parked) p.release();
+}
 
 cudaError_t side_stream(cudaStream_t* out) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  if (g_side.dev != dev) {
+  SideStream& sd = g_res.side;
+  if (sd.dev != dev) {
+    if (sd.dev >= 0) g_res.side_parked.push_back(sd);
+    sd = SideStream{};
+    for (size_t i = 0; i < g_res.side_parked.size(); ++i)
+      if (g_res.side_parked[i].dev == dev) {
+        sd = g_res.side_parked[i];
+        g_res.side_parked.erase(g_res.side_parked.begin() + (long)i);
+        break;
+      }
+  }
+  if (sd.dev != dev) {
     // the side stream carries the interface chains, the sweeps' critical path: give it the
     // highest priority so its small GEMMs are scheduled ahead of the concurrent matvecs
     int lo = 0, hi = 0;
+    sd.dev = dev;
     if ((e = cudaDeviceGetStreamPriorityRange(&lo, &hi)) != cudaSuccess) return e;
-    if ((e = cudaStreamCreateWithPriority(&g_side.s, cudaStreamNonBlocking, hi)) != cudaSuccess)
+    if ((e = cudaStreamCreateWithPriority(&sd.s, cudaStreamNonBlocking, hi)) != cudaSuccess)
       return e;
-    if ((e = cudaStreamCreateWithPriority(&g_side.s_lo, cudaStreamNonBlocking, lo)) != cudaSuccess)
+    if ((e = cudaStreamCreateWithPriority(&sd.s_lo, cudaStreamNonBlocking, lo)) != cudaSuccess)
       return e;
-    for (auto& ev : g_side.ev)
+    for (auto& ev : sd.ev)
       if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return e;
-    g_side.dev = dev;
   }
-  *out = g_side_lowprio ? g_side.s_lo : g_side.s;
+  *out = g_side_lowprio ? sd.s_lo : sd.s;
   return cudaSuccess;
 }
 // `to` waits for all work enqueued on `from` so far (graph-capture compatible)
 cudaError_t stream_dep(cudaStream_t from, cudaStream_t to) {
-  cudaEvent_t ev = g_side.ev[g_side.next++ % 64];
-  cudaError_t e = cudaEventRecord(ev, from);
+  cudaStream_t dummy;
+  cudaError_t e = side_stream(&dummy);   // events of the current device
+  if (e != cudaSuccess) return e;
+  cudaEvent_t ev = g_res.side.ev[g_res.side.next++ % 64];
+  e = cudaEventRecord(ev, from);
   if (e != cudaSuccess) return e;
   return cudaStreamWaitEvent(to, ev, 0);
 }
 
-// ---- stream pool + dependency events for DAG-scheduled sweeps (per thread, per device) ----
-thread_local StreamPool g_pool;
 cudaError_t pool_init(size_t nevents) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  if (g_pool.dev != dev) {
-    int lo = 0, hi = 0;
-    if ((e = cudaDeviceGetStreamPriorityRange(&lo, &hi)) != cudaSuccess) return e;
-    for (auto& st : g_pool.s)
-      if ((e = cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, lo)) != cudaSuccess) return e;
-    if ((e = cudaStreamCreateWithPriority(&g_pool.chain, cudaStreamNonBlocking, hi)) != cudaSuccess)
-      return e;
-    g_pool.ev.clear();
-    g_pool.dev = dev;
+  StreamPool& pl = g_res.pool;
+  if (pl.dev != dev) {
+    if (pl.dev >= 0) g_res.pool_parked.push_back(pl);
+    pl = StreamPool{};
+    for (size_t i = 0; i < g_res.pool_parked.size(); ++i)
+      if (g_res.pool_parked[i].dev == dev) {
+        pl = g_res.pool_parked[i];
+        g_res.pool_parked.erase(g_res.pool_parked.begin() + (long)i);
+        break;
+      }
   }
-  while (g_pool.ev.size() < nevents) {
+  if (pl.dev != dev) {
+    int lo = 0, hi = 0;
+    pl.dev = dev;
+    if ((e = cudaDeviceGetStreamPriorityRange(&lo, &hi)) != cudaSuccess) return e;
+    for (auto& st : pl.s)
+      if ((e = cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, lo)) != cudaSuccess) return e;
+    if ((e = cudaStreamCreateWithPriority(&pl.chain, cudaStreamNonBlocking, hi)) != cudaSuccess)
+      return e;
+    if ((e = cudaStreamCreateWithFlags(&pl.capture, cudaStreamNonBlocking)) != cudaSuccess) return e;
+  }
+  while (pl.ev.size() < nevents) {
     cudaEvent_t ev;
     if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return e;
-    g_pool.ev.push_back(ev);
+    pl.ev.push_back(ev);
   }
   return cudaSuccess;
+}
+
+// ---- graph cache for eager calls ------------------------------------------------------------
+// A multi-launch call (a sweep, a three-stage matvec or interface update) enqueued eagerly pays
+// one host launch per kernel.  The second time the same call arrives -- same entry point, same
+// extents, same device pointers (host pointer arrays compared by content), same debug state --
+// it is captured once on an internal stream into a CUDA graph, and from then on replayed with
+// one cudaGraphLaunch into the caller's stream.  The graph holds exactly the kernels the direct
+// path enqueues (same results, bit for bit).  Bypassed while the caller's stream is capturing,
+// while tracing, and under tt_set_graph_cache(0).
+thread_local int g_graph_cache_on = 1;
+constexpr size_t kGraphCacheMax = 32;
+
+tt_status graph_cached(GraphKey& key, cudaStream_t s, const std::function<tt_status(cudaStream_t)>& enq,
+                       const char* where) {
+  cudaError_t e;
+  bool bypass = !g_graph_cache_on || g_trace_on || g_gate != nullptr;
+  if (!bypass) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) bypass = true;
+  }
+  int dev = 0;
+  if (!bypass && cudaGetDevice(&dev) != cudaSuccess) bypass = true;
+  if (bypass) return enq(s);
+  key.w.push_back((uint64_t)dev);
+  key.w.push_back((uint64_t)(uint32_t)g_dbg_flags);
+  key.w.push_back((uint64_t)(uint32_t)g_variant);
+  key.w.push_back((uint64_t)(uint32_t)g_force_v1);
+  key.w.push_back((uint64_t)(uint32_t)g_dag_mode);
+  key.w.push_back((uint64_t)(uint32_t)g_side_lowprio);
+  key.w.push_back((uint64_t)(uint32_t)g_eigen_elementwise);
+  auto& G = g_res.graphs;
+  ++g_res.clock;
+  for (auto& g : G)
+    if (g.key.w == key.w) {
+      g.last = g_res.clock;
+      if ((e = cudaGraphLaunch(g.exec, s)) != cudaSuccess) return cuda_fail(e, where);
+      g_launches = g.launches;
+      return TT_OK;
+    }
+  // first sighting: enqueue directly and remember the key; second: capture
+  bool seen = false;
+  for (auto& k : g_res.seen)
+    if (k.w == key.w) seen = true;
+  if (!seen) {
+    if (g_res.seen.size() >= 2 * kGraphCacheMax) g_res.seen.erase(g_res.seen.begin());
+    g_res.seen.push_back(key);
+    return enq(s);
+  }
+  if ((e = pool_init(0)) != cudaSuccess) return cuda_fail(e, where);
+  cudaStream_t cs = g_res.pool.capture;
+  if ((e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
+    return cuda_fail(e, where);
+  const int64_t l0 = g_launches;
+  const tt_status st = enq(cs);
+  cudaGraph_t graph = nullptr;
+  cudaError_t e2 = cudaStreamEndCapture(cs, &graph);
+  if (st != TT_OK || e2 != cudaSuccess) {
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    return st != TT_OK ? st : cuda_fail(e2, where);
+  }
+  GraphEntry ent;
+  ent.key = key;
+  ent.launches = g_launches - l0;
+  ent.last = g_res.clock;
+  e = cudaGraphInstantiateWithFlags(&ent.exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return cuda_fail(e, where);
+  if (G.size() >= kGraphCacheMax) {   // evict the least recently used
+    size_t lru = 0;
+    for (size_t i = 1; i < G.size(); ++i)
+      if (G[i].last < G[lru].last) lru = i;
+    cudaGraphExecDestroy(G[lru].exec);
+    G.erase(G.begin() + (long)lru);
+  }
+  G.push_back(ent);
+  if ((e = cudaGraphLaunch(ent.exec, s)) != cudaSuccess) return cuda_fail(e, where);
+  return TT_OK;
+}
+
+void graph_cache_clear() {
+  for (auto& g : g_res.graphs) cudaGraphExecDestroy(g.exec);
+  g_res.graphs.clear();
+  g_res.seen.clear();
 }
 
 long long trace_begin(int tile, long long M, long long N, long long K, cudaStream_t s) {

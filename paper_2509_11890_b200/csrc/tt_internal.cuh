@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <algorithm>
+#include <functional>
 #include <initializer_list>
 #include <memory>
 #include <mutex>
@@ -18,6 +19,7 @@
 #include "../../include/tt_hotpath.h"
 #include "tt_gemm.cuh"
 #include "tt_gemm_v2.cuh"
+#include "tt_dag.cuh"
 
 using tt::GemmParams;
 using tt::IndexMap;
@@ -39,6 +41,8 @@ extern thread_local const int* g_gate;        // device flag gating the solvers'
 extern thread_local double* g_pscratch;       // split-K scratch of the current stage
 extern thread_local long long g_pscratch_elems;
 extern thread_local int g_force_v1;
+extern thread_local int g_eigen_elementwise;
+extern thread_local int g_dag_mode;
 
 struct TraceRec {
   int stage, tile;
@@ -52,14 +56,47 @@ struct SideStream {
   cudaStream_t s_lo = nullptr;   // same, lowest priority (A/B hook: debug flag 2048)
   cudaEvent_t ev[64] = {};
   unsigned next = 0;
+  void release();
 };
 
 constexpr int kPoolStreams = 4;
 struct StreamPool {
   int dev = -1;
   cudaStream_t s[kPoolStreams] = {};
-  cudaStream_t chain = nullptr;   // high priority (the W34 left chain)
+  cudaStream_t chain = nullptr;     // high priority (the W34 left chain)
+  cudaStream_t capture = nullptr;   // graph-cache capture stream
   std::vector<cudaEvent_t> ev;
+  void release();
+};
+
+struct GraphKey {
+  std::vector<uint64_t> w;
+  GraphKey& add(uint64_t v) { w.push_back(v); return *this; }
+  GraphKey& add(const void* p) { w.push_back((uint64_t)(uintptr_t)p); return *this; }
+  template <typename T>
+  GraphKey& arr(const T* a, int64_t n) {   // host array contents (extents or pointers)
+    w.push_back((uint64_t)(a != nullptr));
+    if (a)
+      for (int64_t i = 0; i < n; ++i) w.push_back((uint64_t)(uintptr_t)a[i]);
+    return *this;
+  }
+};
+struct GraphEntry {
+  GraphKey key;
+  cudaGraphExec_t exec = nullptr;
+  int64_t launches = 0;
+  uint64_t last = 0;
+};
+
+struct ThreadRes {   // tt_core.cu: everything a thread's calls created, destroyed at thread exit
+  SideStream side;
+  StreamPool pool;
+  std::vector<SideStream> side_parked;
+  std::vector<StreamPool> pool_parked;
+  std::vector<GraphEntry> graphs;
+  std::vector<GraphKey> seen;
+  uint64_t clock = 0;
+  ~ThreadRes();
 };
 
 struct Carver {
@@ -122,13 +159,17 @@ struct CallScope {
 
 extern thread_local std::vector<TraceRec> g_trace;
 extern thread_local std::vector<cudaEvent_t> g_trace_pool;
-extern thread_local SideStream g_side;
-extern thread_local StreamPool g_pool;
+extern thread_local ThreadRes g_res;
+extern thread_local int g_graph_cache_on;
 
 // ---- helpers (tt_core.cu) ---------------------------------------------------------------------
 cudaError_t side_stream(cudaStream_t* out);
 cudaError_t stream_dep(cudaStream_t from, cudaStream_t to);
 cudaError_t pool_init(size_t nevents);
+// eager multi-launch calls: replayed from a per-thread CUDA graph cache from the second call on
+tt_status graph_cached(GraphKey& key, cudaStream_t s,
+                       const std::function<tt_status(cudaStream_t)>& enqueue, const char* where);
+void graph_cache_clear();
 long long trace_begin(int tile, long long M, long long N, long long K, cudaStream_t s);
 void trace_end(long long idx, cudaStream_t s);
 tt_status fail(tt_status s, const std::string& m);
@@ -216,5 +257,49 @@ extern thread_local int g_eigen_elementwise;
 long long sym_eigen_scratch(long long n);
 cudaError_t launch_sym_eigen(const double* G, double* V, double* lam, int n, double* scratch,
                              cudaStream_t s);
+
+// ---- persistent DAG executor (tt_dag.cu / tt_dag.cuh) -------------------------------------------
+// While a DagBuilder is active on the thread (g_dag), launch_gemm records a task instead of
+// launching; each task depends on the previous task of the current lane and on add_dep()s.
+constexpr int kDagCounterInts = 1 << 16;   // queue head + per-task tile counters + tickets
+class DagBuilder {
+ public:
+  DagBuilder(void* scratch, size_t bytes);   // counters + split-K partials (dag_scratch_bytes)
+  void set_lane(int lane);
+  int last_of(int lane) const;               // last task recorded on a lane (-1: none)
+  int count() const { return (int)tasks.size(); }
+  void add_dep(int task) { if (task >= 0) pending.push_back(task); }
+  cudaError_t add(bool a_kc, bool b_kc, const GemmParams& p);
+  cudaError_t launch(cudaStream_t s);        // one memset of the counters + one kernel
+  long long partials_needed() const { return part_used; }
+  bool ok = true;
+  long long target_units = 128;              // split-K aims for this many units per task
+
+ private:
+  struct Node {
+    tt::DagTask t;
+    int tiles = 0, units = 0;
+    std::vector<int> deps;
+  };
+  std::vector<Node> tasks;
+  std::vector<int> lane_last, pending;
+  int lane = 0;
+  bool dry = false;
+  int* ctr = nullptr;
+  double* part = nullptr;
+  long long part_cap = 0, part_used = 0, ticks = 0;
+};
+extern thread_local DagBuilder* g_dag;
+extern thread_local int g_dag_mode;
+extern thread_local unsigned long long* g_dag_trace;
+extern thread_local long long g_dag_trace_cap;
+extern thread_local int g_dag_last_units, g_dag_last_tasks;
+extern thread_local std::vector<int> g_dag_last_unit0;   // tt_debug_set_dag: 0 policy, -1 off, 1 force, 2 8-warp tiles
+size_t dag_scratch_bytes(long long partial_elems);
+struct DagScope {   // records launch_gemm calls into b for the scope's lifetime
+  explicit DagScope(DagBuilder* b) : saved(g_dag) { g_dag = b; }
+  ~DagScope() { g_dag = saved; }
+  DagBuilder* saved;
+};
 
 }  // namespace ttint

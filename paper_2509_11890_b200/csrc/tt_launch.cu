@@ -200,6 +200,7 @@ thread_local int g_force_v1 = 0;   // test hook (tt_debug_force_v1)
 
 cudaError_t launch_gemm(bool a_kc, bool b_kc, const GemmParams& p, cudaStream_t s) {
   if (p.M <= 0 || p.N <= 0 || p.K <= 0) return cudaSuccess;
+  if (g_dag) return g_dag->add(a_kc, b_kc, p);   // recording a persistent DAG (tt_dag.cu)
   if (a_kc && b_kc) return launch_layout<true, true>(p, s);
   if (a_kc && !b_kc) return launch_layout<true, false>(p, s);
   if (!a_kc && b_kc) return launch_layout<false, true>(p, s);
