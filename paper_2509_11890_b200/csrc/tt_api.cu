@@ -151,6 +151,9 @@ int64_t tt_debug_dag_trace(void* buf, int64_t cap_units, int32_t* unit0, int64_t
   return ((int64_t)g_dag_last_tasks << 32) | (int64_t)g_dag_last_units;
 }
 void tt_debug_set_flags(int f) {
+#ifndef TT_DEBUG_HOOKS
+  f &= ~3;   // the result-corrupting timing bits (skip stores / loads) need a debug build
+#endif
   g_dbg_flags = f;
   g_side_lowprio = (f & 2048) ? 1 : 0;
 }
@@ -925,13 +928,8 @@ tt_status tt_operator_apply(int64_t d, const int64_t* n_row, const int64_t* n_co
       return fail(TT_ERR_INVALID_ARGUMENT, "core too large for the apply kernel's staging");
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [&] {
-    attr_err = cudaFuncSetAttribute(apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    smem_optin);
-  });
-  if (attr_err != cudaSuccess) return cuda_fail(attr_err, "tt_operator_apply attr");
+  if (cudaError_t attr_err = smem_attr((const void*)apply_kernel, smem_optin))
+    return cuda_fail(attr_err, "tt_operator_apply attr");
   for (int64_t k = 0; k < d; ++k) {
     const long long smem = 8LL * (n_col[k] * r[k + 1] + n_row[k] * n_col[k] * R[k + 1]);
     const long long blocks = r[k] * R[k];

@@ -119,6 +119,22 @@ cudaError_t pool_init(size_t nevents) {
   return cudaSuccess;
 }
 
+// Opt-in dynamic shared memory of a kernel: a function attribute is per device, so it is set
+// once per (kernel, device, size) and thread.
+cudaError_t smem_attr(const void* kern, int bytes) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  struct Rec { const void* k; int dev, bytes; };
+  thread_local std::vector<Rec> done;
+  for (const Rec& r : done)
+    if (r.k == kern && r.dev == dev && r.bytes >= bytes) return cudaSuccess;
+  if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes)) != cudaSuccess)
+    return e;
+  done.push_back(Rec{kern, dev, bytes});
+  return cudaSuccess;
+}
+
 // ---- graph cache for eager calls ------------------------------------------------------------
 // A multi-launch call (a sweep, a three-stage matvec or interface update) enqueued eagerly pays
 // one host launch per kernel.  The second time the same call arrives -- same entry point, same
@@ -260,12 +276,16 @@ thread_local int g_dbg_flags = 0;   // tt_debug_set_flags (bits listed in the he
 // swept with tools/w34_knobs.py: 0.05 GFLOP gives config 3 0.166 ms and config 4 0.731 ms,
 // 0.2 GFLOP 0.165 / 0.746, no PDL 0.193 / 0.734); g_no_pdl (tt_sweep_als scope) disables it.
 constexpr double kPdlFlopsDefault = 0.05e9;
-double pdl_flops() {   // probe override TT_PDL_FLOPS, read once
+double pdl_flops() {
+#ifdef TT_DEBUG_HOOKS   // probe override TT_PDL_FLOPS (debug build), read once
   static const double v = [] {
     const char* e = getenv("TT_PDL_FLOPS");
     return e ? atof(e) : kPdlFlopsDefault;
   }();
   return v;
+#else
+  return kPdlFlopsDefault;
+#endif
 }
 thread_local bool g_no_pdl = false;
 

@@ -166,6 +166,7 @@ extern thread_local int g_graph_cache_on;
 cudaError_t side_stream(cudaStream_t* out);
 cudaError_t stream_dep(cudaStream_t from, cudaStream_t to);
 cudaError_t pool_init(size_t nevents);
+cudaError_t smem_attr(const void* kern, int bytes);   // per device opt-in shared memory
 // eager multi-launch calls: replayed from a per-thread CUDA graph cache from the second call on
 tt_status graph_cached(GraphKey& key, cudaStream_t s,
                        const std::function<tt_status(cudaStream_t)>& enqueue, const char* where);

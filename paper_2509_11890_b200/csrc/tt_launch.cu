@@ -6,16 +6,17 @@
 namespace ttint {
 
 // ---- v2 (persistent, 16 warps, 16-byte loads) --------------------------------------------
-int num_sms() {
-  static int sms = 0;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  });
-  return sms;
+int num_sms() {   // of the current device (cached per device and thread)
+  constexpr int kMaxDev = 64;
+  thread_local int sms[kMaxDev] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return 148;
+  if (sms[dev] <= 0) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    sms[dev] = v > 0 ? v : 148;
+  }
+  return sms[dev];
 }
 
 thread_local int g_variant = -1;
@@ -131,11 +132,13 @@ struct LatKnobs {
 const LatKnobs& lat_knobs() {
   static LatKnobs k = [] {
     LatKnobs r;
+#ifdef TT_DEBUG_HOOKS   // probe overrides exist only in a debug build
     if (const char* e = getenv("TT_LAT_FLOPS")) r.flops = atof(e);
     if (const char* e = getenv("TT_LAT_UNIT_US")) r.unit_s = atof(e) * 1e-6;
     if (const char* e = getenv("TT_LAT_MASK")) r.mask = (unsigned)strtoul(e, nullptr, 0);
     if (const char* e = getenv("TT_LAT_SPLIT_US")) r.split_s = atof(e) * 1e-6;
     if (const char* e = getenv("TT_LAT_OCC")) r.occ_model = atoi(e);
+#endif
     return r;
   }();
   return k;

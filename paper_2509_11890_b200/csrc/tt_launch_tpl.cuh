@@ -42,13 +42,7 @@ template <int BM, int BN, int BK, int WM, int WN, int ST, bool AK, bool BK_>
 cudaError_t launch_cfg(const GemmParams& p0, cudaStream_t s) {
   using Cfg = tt::GemmCfg<BM, BN, BK, WM, WN, ST, AK, BK_>;
   auto kern = tt::dmma_gemm_kernel<BM, BN, BK, WM, WN, ST, AK, BK_>;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [&] {
-    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)Cfg::kSmemBytes);
-  });
-  if (attr_err != cudaSuccess) return attr_err;
+  if (cudaError_t attr_err = smem_attr((const void*)kern, (int)Cfg::kSmemBytes)) return attr_err;
   GemmParams p = p0;
   const long long tm = (p.M + BM - 1) / BM;
   p.tiles_n = (p.N + BN - 1) / BN;
@@ -87,13 +81,7 @@ cudaError_t launch_v2_cfg(const GemmParams& p0, cudaStream_t s) {
   static_assert(ST >= 2, "shared memory budget");
   using Cfg = tt::GemmV2Cfg<AK, BK_, BM, BN, WM, WN, ST, MINB>;
   auto kern = tt::dmma_gemm_v2_kernel<AK, BK_, BM, BN, WM, WN, ST, MINB>;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [&] {
-    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)Cfg::kSmemBytes);
-  });
-  if (attr_err != cudaSuccess) return attr_err;
+  if (cudaError_t attr_err = smem_attr((const void*)kern, (int)Cfg::kSmemBytes)) return attr_err;
   tt::GemmParamsV2 p;
   p.A = p0.A;
   p.B = p0.B;
@@ -201,13 +189,7 @@ cudaError_t launch_v3_cfg(const GemmParams& p0, cudaStream_t s, bool& ok) {
   if (BRES && (!b3d || p0.N > BN || (p0.K + 15) / 16 > tt::kBresMaxKT)) return cudaSuccess;
   ok = true;
   auto kern = tt::dmma_gemm_v3_kernel<AK, BK_, BM, BN, WM, WN, ST, MINB, BRES>;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [&] {
-    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)Cfg::kSmemBytes);
-  });
-  if (attr_err != cudaSuccess) return attr_err;
+  if (cudaError_t attr_err = smem_attr((const void*)kern, (int)Cfg::kSmemBytes)) return attr_err;
   tt::GemmParamsV3 p;
   p.C = p0.C;
   p.P = nullptr;
@@ -247,7 +229,11 @@ cudaError_t launch_v3_cfg(const GemmParams& p0, cudaStream_t s, bool& ok) {
     }
     if (g_dbg_flags & 32) { if (p.l2_a == 2) p.l2_a = 0; if (p.l2_b == 2) p.l2_b = 0; }
     if (g_dbg_flags & 64) { if (p.l2_a == 1) p.l2_a = 0; if (p.l2_b == 1) p.l2_b = 0; }
+#ifdef TT_DEBUG_HOOKS
     static const bool l2_debug = getenv("TT_L2_DEBUG") != nullptr;
+#else
+    constexpr bool l2_debug = false;
+#endif
     if (l2_debug)
       fprintf(stderr, "v3 %dx%d M=%lld N=%lld K=%lld AK=%d BK=%d a=%lldMB(r%lld,p%d) b=%lldMB(r%lld,p%d)\n",
               BM, BN, (long long)p0.M, (long long)p0.N, (long long)p0.K, AK, BK_, a_bytes >> 20,

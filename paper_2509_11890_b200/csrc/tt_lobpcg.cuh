@@ -816,26 +816,17 @@ bool lob_ws_elems(const Dims& d, long long nb, LobWs& w) {
   return ok;
 }
 
-// opt-in shared memory of the kernels that can exceed 48 KB (once per process)
+// opt-in shared memory of the kernels that can exceed 48 KB (per device)
 cudaError_t lob_set_smem_attrs() {
-  static std::once_flag once;
-  static cudaError_t err = cudaSuccess;
-  std::call_once(once, [] {
-    err = cudaFuncSetAttribute(lob_gram_kernel<16, 16, 6, 12>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)GramCfg<16, 16, 6, 12>::smem(kLobMaxS, 2 * kLobMaxS));
+  cudaError_t err = smem_attr((const void*)lob_gram_kernel<16, 16, 6, 12>,
+                              (int)GramCfg<16, 16, 6, 12>::smem(kLobMaxS, 2 * kLobMaxS));
+  if (err == cudaSuccess)
+    err = smem_attr((const void*)lob_gram_kernel<16, 8, 3, 12>, (int)GramCfg<16, 8, 3, 12>::smem(48, 96));
+  if (err == cudaSuccess)
+    err = smem_attr((const void*)lob_rr_kernel, (int)lob_rr_smem(kLobMaxS, kLobMaxNb));
+  for (auto fn : {lob_combine_kernel<16, 1>, lob_combine_kernel<16, 2>, lob_combine_kernel<32, 1>})
     if (err == cudaSuccess)
-      err = cudaFuncSetAttribute(lob_gram_kernel<16, 8, 3, 12>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)GramCfg<16, 8, 3, 12>::smem(48, 96));
-    if (err == cudaSuccess)
-      err = cudaFuncSetAttribute(lob_rr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)lob_rr_smem(kLobMaxS, kLobMaxNb));
-    for (auto fn : {lob_combine_kernel<16, 1>, lob_combine_kernel<16, 2>, lob_combine_kernel<32, 1>})
-      if (err == cudaSuccess)
-        err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)(sizeof(double) * 2 * kLobMaxS * kLobMaxNb));
-  });
+      err = smem_attr((const void*)fn, (int)(sizeof(double) * 2 * kLobMaxS * kLobMaxNb));
   return err;
 }
 

@@ -8,11 +8,12 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 HEADER = os.path.join(ROOT, "include", "tt_hotpath.h")
+DEBUG_HEADER = os.path.join(ROOT, "include", "tt_hotpath_debug.h")
 LIB = os.path.join(ROOT, "paper_2509_11890_b200", "libtt_hotpath.so")
 
 
 def declared_functions():
-    src = open(HEADER).read()
+    src = open(HEADER).read() + open(DEBUG_HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(tt_[a-z_0-9]+)\s*\(", src)))
 
@@ -117,3 +118,18 @@ def test_binding_argtypes_match_header():
         assert len(fn.argtypes) == n, (name, len(fn.argtypes), n)
         checked += 1
     assert checked >= 12
+
+
+def test_debug_hooks_live_in_the_debug_header():
+    """ABI hygiene: the production header declares no tt_debug_* hook; the debug header does."""
+    prod = re.sub(r"/\*.*?\*/", "", open(HEADER).read(), flags=re.S)
+    dbg = re.sub(r"/\*.*?\*/", "", open(DEBUG_HEADER).read(), flags=re.S)
+    assert not re.findall(r"\btt_debug_[a-z_0-9]+\s*\(", prod)
+    assert "tt_debug_set_flags" in dbg and "tt_debug_set_variant" in dbg
+
+
+def test_product_library_reads_no_environment_knobs():
+    """The probe knobs (TT_LAT_*, TT_PDL_FLOPS, TT_L2_DEBUG) exist only in a debug build."""
+    data = open(LIB, "rb").read()
+    for knob in (b"TT_LAT_FLOPS", b"TT_PDL_FLOPS", b"TT_L2_DEBUG", b"TT_LAT_UNIT_US"):
+        assert knob not in data, knob
