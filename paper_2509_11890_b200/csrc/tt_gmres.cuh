@@ -220,6 +220,243 @@ __global__ void gmres_arnoldi_kernel(GmresState st, const double* __restrict__ h
   st.scale[j] = (!done && hn > 0.0) ? 1.0 / hn : 0.0;
 }
 
+// ---- fused Arnoldi step for one right-hand side (K = 1, the paper's GMRES: one matrix-free
+// product per Arnoldi step) -------------------------------------------------------
+// The ~12 dependent launches of an orthogonalisation step (CGS2 dots and updates, norm, Givens,
+// scaling) are latency, not bandwidth, at the ranks of the paper (a vector of r n r <= 2^18
+// doubles).  One thread-block cluster of kOrthCluster CTAs does the whole step: each CTA owns
+// a contiguous segment of the vector, the three reductions (h1 = V^T w, h2 = V^T w after the
+// first update, ||w||^2) combine the CTAs' partial sums through distributed shared memory
+// (every CTA adds the kOrthCluster partials in rank order: identical, deterministic results in
+// all CTAs), CTA 0 performs the Hessenberg / Givens update of gmres_arnoldi_kernel and
+// broadcasts 1 / H[i+1,i], and every CTA writes its segment of v_{i+1}.
+constexpr int kOrthMaxL = 32;
+constexpr long long kOrthMaxS = 1LL << 17;
+
+// Each CTA keeps its segment of w in shared memory for the whole step and reads the basis
+// three times: h1 = V^T w; then (same loaded V values) w -= V h1 and h2 = V^T w; then
+// w -= V h2 and ||w||^2.  Element loops are unrolled by U (2 for L <= 16) so that U (L + 1)
+// independent loads are in flight per thread (the kernel is load-latency bound at these sizes).
+template <int LMAX, int NT, int U>
+__global__ void __launch_bounds__(NT) gmres_orth_cluster_kernel(
+    GmresState st, const double* __restrict__ V, double* __restrict__ W, double* __restrict__ Vnext,
+    long long S, int L, int m, int i, double tol, const int* __restrict__ gate) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank(), ncl = (int)cluster.num_blocks();
+  extern __shared__ double wseg[];   // this CTA's segment of w
+  __shared__ double partA[LMAX], partB[LMAX], partC[1];
+  __shared__ double h1[LMAX], h2[LMAX], wn2;
+  __shared__ double red[NT / 32][LMAX + 1];
+  __shared__ double sh_scale;
+  const bool gated = gate && *gate;   // uniform: written by an earlier, completed launch
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long per = (S + ncl - 1) / ncl;
+  const long long s0 = rank * per, s1 = min(S, s0 + per);
+  const int nseg = (int)max(0LL, s1 - s0);
+
+  // block-reduce acc[0..n) -> part[0..n) (thread l writes part[l])
+  auto block_reduce = [&](double (&acc)[LMAX + 1], int n, double* part) {
+#pragma unroll
+    for (int l = 0; l < LMAX; ++l) {
+      if (l >= n) break;
+      double v = acc[l];
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+      if (lane == 0) red[warp][l] = v;
+    }
+    __syncthreads();
+    if (tid < n) {
+      double v = 0.0;
+      for (int q = 0; q < NT / 32; ++q) v += red[q][tid];
+      part[tid] = v;
+    }
+  };
+  // h[l] = sum over the cluster's CTAs (rank order) of part[l]: identical in every CTA
+  auto combine = [&](double* part, double* h, int n) {
+    cluster.sync();
+    if (tid < n) {
+      double v = 0.0;
+      for (int r = 0; r < ncl; ++r) v += cluster.map_shared_rank(part, r)[tid];
+      h[tid] = v;
+    }
+    __syncthreads();
+  };
+  if (!gated) {
+    double acc[LMAX + 1];
+    // pass 1: w -> shared memory, h1 = V^T w
+#pragma unroll
+    for (int l = 0; l < LMAX; ++l) acc[l] = 0.0;
+    for (int t0 = tid; t0 < nseg; t0 += U * NT) {
+      const int t1 = t0 + NT;
+      const bool ok1 = U == 2 && t1 < nseg;
+      const double w0 = W[s0 + t0], w1 = ok1 ? W[s0 + t1] : 0.0;
+      wseg[t0] = w0;
+      if (ok1) wseg[t1] = w1;
+#pragma unroll
+      for (int l = 0; l < LMAX; ++l)
+        if (l < L) {
+          const double v0 = V[l * S + s0 + t0], v1 = ok1 ? V[l * S + s0 + t1] : 0.0;
+          acc[l] = fma(v1, w1, fma(v0, w0, acc[l]));
+        }
+    }
+    block_reduce(acc, L, partA);
+    combine(partA, h1, L);
+    // pass 2: w -= V h1, h2 = V^T w (one read of V)
+#pragma unroll
+    for (int l = 0; l < LMAX; ++l) acc[l] = 0.0;
+    for (int t0 = tid; t0 < nseg; t0 += U * NT) {
+      const int t1 = t0 + NT;
+      const bool ok1 = U == 2 && t1 < nseg;
+      double vv0[LMAX], vv1[LMAX];
+      double w0 = wseg[t0], w1 = ok1 ? wseg[t1] : 0.0;
+#pragma unroll
+      for (int l = 0; l < LMAX; ++l)
+        if (l < L) {
+          vv0[l] = V[l * S + s0 + t0];
+          vv1[l] = ok1 ? V[l * S + s0 + t1] : 0.0;
+        }
+#pragma unroll
+      for (int l = 0; l < LMAX; ++l)
+        if (l < L) {
+          w0 = fma(-h1[l], vv0[l], w0);
+          w1 = fma(-h1[l], vv1[l], w1);
+        }
+#pragma unroll
+      for (int l = 0; l < LMAX; ++l)
+        if (l < L) acc[l] = fma(vv1[l], w1, fma(vv0[l], w0, acc[l]));
+      wseg[t0] = w0;
+      if (ok1) wseg[t1] = w1;
+    }
+    block_reduce(acc, L, partB);
+    combine(partB, h2, L);
+    // pass 3: w -= V h2, ||w||^2
+    acc[0] = 0.0;
+    for (int t0 = tid; t0 < nseg; t0 += U * NT) {
+      const int t1 = t0 + NT;
+      const bool ok1 = U == 2 && t1 < nseg;
+      double vv0[LMAX], vv1[LMAX];
+      double w0 = wseg[t0], w1 = ok1 ? wseg[t1] : 0.0;
+#pragma unroll
+      for (int l = 0; l < LMAX; ++l)
+        if (l < L) {
+          vv0[l] = V[l * S + s0 + t0];
+          vv1[l] = ok1 ? V[l * S + s0 + t1] : 0.0;
+        }
+#pragma unroll
+      for (int l = 0; l < LMAX; ++l)
+        if (l < L) {
+          w0 = fma(-h2[l], vv0[l], w0);
+          w1 = fma(-h2[l], vv1[l], w1);
+        }
+      acc[0] = fma(w1, w1, fma(w0, w0, acc[0]));
+      wseg[t0] = w0;
+      if (ok1) wseg[t1] = w1;
+    }
+    block_reduce(acc, 1, partC);
+    combine(partC, &wn2, 1);
+    if (rank == 0 && tid == 0) {   // the Hessenberg column, Givens rotations, convergence
+      double scale = 0.0;
+      if (st.active[0]) {
+        double* H = st.H;
+        double* cs = st.cs;
+        double* sn = st.sn;
+        double* gg = st.g;
+        for (int l = 0; l <= i; ++l) H[l * m + i] = h1[l] + h2[l];
+        const double hn = sqrt(wn2);
+        H[(i + 1) * m + i] = hn;
+        for (int l = 0; l < i; ++l) {
+          const double a = H[l * m + i], b = H[(l + 1) * m + i];
+          H[l * m + i] = cs[l] * a + sn[l] * b;
+          H[(l + 1) * m + i] = -sn[l] * a + cs[l] * b;
+        }
+        const double a = H[i * m + i], b = H[(i + 1) * m + i];
+        const double den = hypot(a, b);
+        cs[i] = a / den;
+        sn[i] = b / den;
+        H[i * m + i] = den;
+        H[(i + 1) * m + i] = 0.0;
+        gg[i + 1] = -sn[i] * gg[i];
+        gg[i] = cs[i] * gg[i];
+        st.kcyc[0] = i + 1;
+        st.its[0] += 1;
+        const double rel = fabs(gg[i + 1]) / st.fnorm[0];
+        st.rel[0] = rel;
+        const bool done = (rel <= tol) || !(hn > 0.0);
+        if (done) st.active[0] = 0;
+        scale = (!done && hn > 0.0) ? 1.0 / hn : 0.0;
+      }
+      st.scale[0] = scale;
+      *st.done = !st.active[0];
+      sh_scale = scale;
+    }
+    cluster.sync();
+    const double scale = *cluster.map_shared_rank(&sh_scale, 0);
+    for (int t = tid; t < nseg; t += NT) Vnext[s0 + t] = wseg[t] * scale;
+  }
+  cluster.sync();   // no CTA leaves while another may still read its shared memory
+}
+
+// cluster size: 16 CTAs where the device allows non-portable clusters, else 8 (per device)
+template <int LMAX, int NT, int U>
+cudaError_t orth_launch_t(const GmresState& st, const double* V, double* W, double* Vnext,
+                          long long S, int L, int m, int i, double tol, cudaStream_t s) {
+  auto kern = gmres_orth_cluster_kernel<LMAX, NT, U>;
+  thread_local int cl_dev[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& cl = cl_dev[dev & 63];
+  const size_t smem_max = sizeof(double) * (size_t)((kOrthMaxS + 7) / 8);   // w segment, 8 CTAs
+  if (cl == 0) {
+    cl = 8;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+      cudaLaunchConfig_t q = {};
+      q.gridDim = dim3(16);
+      q.blockDim = dim3(NT);
+      q.dynamicSmemBytes = sizeof(double) * (size_t)((kOrthMaxS + 15) / 16);
+      cudaLaunchAttribute a[1];
+      a[0].id = cudaLaunchAttributeClusterDimension;
+      a[0].val.clusterDim.x = 16;
+      a[0].val.clusterDim.y = 1;
+      a[0].val.clusterDim.z = 1;
+      q.attrs = a;
+      q.numAttrs = 1;
+      int nclusters = 0;
+      if (cudaOccupancyMaxActiveClusters(&nclusters, kern, &q) == cudaSuccess && nclusters > 0) cl = 16;
+    }
+    cudaGetLastError();
+  }
+  if (cudaError_t e = smem_attr((const void*)kern, (int)smem_max)) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cl);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = sizeof(double) * (size_t)((S + cl - 1) / cl);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, st, V, W, Vnext, S, L, m, i, tol, g_gate);
+}
+
+cudaError_t launch_orth_cluster(const GmresState& st, const double* V, double* W, double* Vnext,
+                                long long S, int L, int m, int i, double tol, cudaStream_t s) {
+  ++g_launches;
+  g_stage = TT_ST_SET;
+  const long long tr = trace_begin(-1, S, L, 0, s);
+  cudaError_t e;
+  if (L <= 8)
+    e = orth_launch_t<8, 512, 2>(st, V, W, Vnext, S, L, m, i, tol, s);
+  else if (L <= 16)
+    e = orth_launch_t<16, 256, 2>(st, V, W, Vnext, S, L, m, i, tol, s);
+  else
+    e = orth_launch_t<32, 256, 1>(st, V, W, Vnext, S, L, m, i, tol, s);
+  trace_end(tr, s);
+  return e;
+}
+
 // *done = no column is active (gates the rest of the cycle's Arnoldi steps)
 __global__ void gmres_alldone_kernel(const int* __restrict__ active, int K, int* __restrict__ done) {
   int any = 0;
@@ -390,6 +627,10 @@ cudaError_t enqueue_gmres(const Dims& d, long long K, long long m, long long kau
   double* C = W;   // the correction reuses W after the cycle's last Arnoldi step
   std::vector<int> zorder;   // Z slot indices, newest first
   const int kb = (int)((K + 127) / 128), kt = 128;
+  // K = 1 at the paper's ranks: the fused cluster kernel for the orthogonalisation step
+  // (debug flag 1 << 26 keeps the separate kernels)
+  const bool fused_orth = K == 1 && ms + 1 <= kOrthMaxL && gd.S <= kOrthMaxS &&
+                          !(g_dbg_flags & (1 << 26));
   cudaError_t e;
   g_stage = TT_ST_PERM;
   if ((e = launch_perm(true, A, Ah, d.al, d.n, d.be, s)) != cudaSuccess) return e;
@@ -421,6 +662,12 @@ cudaError_t enqueue_gmres(const Dims& d, long long K, long long m, long long kau
           cudaSuccess)
         return e;
       const int L = (int)(i + 1);
+      if (fused_orth) {   // one cluster launch for the whole orthogonalisation step
+        if ((e = launch_orth_cluster(st, V, W, V + (i + 1) * gd.S, gd.S, L, (int)ms, (int)i, tol, s)) !=
+            cudaSuccess)
+          return e;
+        continue;
+      }
       // CGS2: two classical Gram-Schmidt passes against v_0..v_i
       if ((e = launch_coldots(gd, V, L, W, part, h1, s)) != cudaSuccess) return e;
       if ((e = launch_colaxpy(gd, V, L, h1, -1.0, W, s)) != cudaSuccess) return e;

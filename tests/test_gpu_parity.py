@@ -393,7 +393,10 @@ def _mixed_canonical_system(idx, k, seed=3):
 
 @pytest.mark.parametrize("idx,k,K,m,cycles,kaug", [(2, 3, 4, 12, 2, 0), (4, 5, 3, 8, 1, 0),
                                                   (3, 1, 5, 10, 2, 0), (2, 3, 4, 5, 4, 2),
-                                                  (3, 5, 3, 6, 3, 1)])
+                                                  (3, 5, 3, 6, 3, 1),
+                                                  # K = 1: the fused cluster orthogonalisation
+                                                  (3, 5, 1, 10, 2, 0), (2, 3, 1, 12, 3, 2),
+                                                  (4, 6, 1, 8, 2, 0), (2, 0, 1, 6, 2, 0)])
 def test_local_gmres_vs_oracle(tt, idx, k, K, m, cycles, kaug):
     """Fixed m, cycles (and augmentation k for LGMRES) and tol = 0 on both sides: the
     iterates must agree (<= 1e-11) and take the same number of Arnoldi steps."""
@@ -428,6 +431,28 @@ def test_local_gmres_converges_to_dense_solution(tt):
         ref = np.linalg.solve(L, F[:, :, j, :].ravel())
         assert rel(h(Xg)[:, :, j, :].ravel(), ref) <= 1e-11
     assert (h(relg) <= 1e-13).all()
+
+
+@pytest.mark.parametrize("idx,k,m,kaug", [(3, 5, 10, 0), (4, 6, 12, 2)])
+def test_local_gmres_fused_orth_equals_separate_kernels(tt, idx, k, m, kaug):
+    """K = 1: the one-launch cluster orthogonalisation step (CGS2 + Givens + scaling) against the
+    separate kernels (debug flag 1 << 26): same Arnoldi step counts, iterates within rounding."""
+    mixed, A, phiL, phiR, rng = _mixed_canonical_system(idx, k)
+    rl, n, rr = mixed[k].shape
+    F = rng.standard_normal((rl, n, 1, rr))
+    out = []
+    for flags in (0, 1 << 26):
+        tt.tt_debug_set_flags(flags)
+        try:
+            out.append(tt.tt_local_gmres(g(phiL), g(A[k]), g(phiR), g(F), m=m, cycles=3, tol=1e-12,
+                                         k_aug=kaug))
+            torch.cuda.synchronize()
+        finally:
+            tt.tt_debug_set_flags(0)
+    (Xa, ra, ia), (Xb, rb, ib) = out
+    assert (h(ia) == h(ib)).all()
+    assert rel(h(Xa), h(Xb)) <= 1e-11
+    assert np.allclose(h(ra), h(rb), rtol=1e-6, atol=1e-14)
 
 
 def test_local_gmres_errors(tt):
