@@ -24,7 +24,8 @@ __all__ = [
     "tt_sweep_als", "tt_operator_apply", "tt_last_launch_count",
     "TT_SWEEP_LEFT", "TT_SWEEP_RIGHT", "TT_SWEEP_BOTH", "tt_trace_enable", "tt_trace_disable",
     "tt_trace_count", "tt_trace_read", "tt_fp64_peak_probe", "STAGE_NAMES", "tt_debug_force_v1",
-    "tt_debug_set_variant", "tt_debug_set_flags", "tt_debug_set_dag", "tt_debug_dag_trace", "tt_set_graph_cache",
+    "tt_debug_set_variant", "tt_debug_set_flags", "tt_debug_set_dag", "tt_debug_dag_trace", "tt_set_graph_cache", "prepare",
+    "PreparedCall",
     "tt_local_gmres",
     "tt_local_gmres_workspace_size",
     "tt_local_matvec_two_site", "tt_local_matvec_two_site_workspace_size",
@@ -208,7 +209,59 @@ def _stream(stream) -> int:
 def _ws(nbytes: int, workspace: Optional[torch.Tensor], device) -> torch.Tensor:
     if workspace is not None:
         return workspace
-    return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+    ws = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+    if _RECORD is not None:   # prepare(): the recorded call keeps its workspace alive
+        _RECORD_KEEP.append(ws)
+    return ws
+
+
+
+# ---- prepared calls ------------------------------------------------------------------------
+# prepare(fn, ...) runs a hot-path call once and returns a PreparedCall that re-issues the same
+# C-ABI call (same device buffers, same marshalled pointer / extent arrays) on a given stream
+# with no per-call Python validation or marshalling: the eager-call overhead of an iterative
+# solver's repeated sweeps drops to one ctypes call (and the library's graph cache then replays
+# the call as one CUDA graph launch).  The PreparedCall keeps every tensor and array alive.
+_RECORD: Optional[list] = None
+_RECORD_KEEP: list = []
+
+
+def _invoke(fn, *args) -> None:
+    if _RECORD is not None:
+        _RECORD.append((fn, args))
+    _check(fn(*args))
+
+
+class PreparedCall:
+    """A recorded C-ABI call: ``p()`` / ``p(stream)`` re-issues it; ``p.result`` holds the
+    outputs the first call returned (the buffers every re-issue writes)."""
+
+    def __init__(self, fn, args, keep, result):
+        self._fn, self._args, self._keep, self.result = fn, args[:-1], keep, result
+
+    def __call__(self, stream=None):
+        _check(self._fn(*self._args, _stream(stream)))
+        return self.result
+
+
+def prepare(fn, *args, **kwargs) -> PreparedCall:
+    """prepare(tt_sweep_w34, x, A, ...) etc.: validate and marshal once (see PreparedCall).
+    fn: tt_local_matvec, tt_local_matvec_batched, tt_interface_left / _right,
+    tt_sweep_interfaces, tt_sweep_w34, tt_sweep_als, tt_operator_apply."""
+    global _RECORD
+    rec: list = []
+    _RECORD = rec
+    _RECORD_KEEP.clear()
+    try:
+        result = fn(*args, **kwargs)
+        keep = list(_RECORD_KEEP)
+    finally:
+        _RECORD = None
+        _RECORD_KEEP.clear()
+    if len(rec) != 1:
+        raise ValueError(f"{getattr(fn, '__name__', fn)} is not a single-call hot-path function")
+    lfn, largs = rec[0]
+    return PreparedCall(lfn, largs, (args, kwargs, largs, keep), result)
 
 
 def tt_last_launch_count() -> int:
@@ -235,9 +288,9 @@ def tt_local_matvec(phiL, A, phiR, x, y=None, workspace=None, stream=None):
     _expect(y, x.shape, "y")
     _same_device(phiL, A, phiR, x, y, workspace)
     ws = _ws(tt_local_matvec_workspace_size(rl, n, rr, Rl, Rr, 1), workspace, x.device)
-    _check(lib.tt_local_matvec(rl, n, rr, Rl, Rr, _dev(phiL, "phiL"), _dev(A, "A"),
-                               _dev(phiR, "phiR"), _dev(x, "x"), _dev(y, "y"), ws.data_ptr(),
-                               ws.numel(), _stream(stream)))
+    _invoke(lib.tt_local_matvec, rl, n, rr, Rl, Rr, _dev(phiL, "phiL"), _dev(A, "A"),
+            _dev(phiR, "phiR"), _dev(x, "x"), _dev(y, "y"), ws.data_ptr(), ws.numel(),
+            _stream(stream))
     return y
 
 
@@ -253,9 +306,9 @@ def tt_local_matvec_batched(phiL, A, phiR, X, Y=None, workspace=None, stream=Non
     _expect(Y, X.shape, "Y")
     _same_device(phiL, A, phiR, X, Y, workspace)
     ws = _ws(tt_local_matvec_workspace_size(rl, n, rr, Rl, Rr, nvec), workspace, X.device)
-    _check(lib.tt_local_matvec_batched(rl, n, rr, Rl, Rr, nvec, _dev(phiL, "phiL"), _dev(A, "A"),
+    _invoke(lib.tt_local_matvec_batched, rl, n, rr, Rl, Rr, nvec, _dev(phiL, "phiL"), _dev(A, "A"),
                                        _dev(phiR, "phiR"), _dev(X, "X"), _dev(Y, "Y"),
-                                       ws.data_ptr(), ws.numel(), _stream(stream)))
+                                       ws.data_ptr(), ws.numel(), _stream(stream))
     return Y
 
 
@@ -272,9 +325,9 @@ def tt_interface_left(phiL_prev, A, x, out=None, workspace=None, stream=None):
     _expect(out, (rr, Rr, rr), "phiL_next")
     _same_device(phiL_prev, A, x, out, workspace)
     ws = _ws(tt_interface_workspace_size(rl, n, rr, Rl, Rr), workspace, x.device)
-    _check(lib.tt_interface_left(rl, n, rr, Rl, Rr, _dev(phiL_prev, "phiL_prev"), _dev(A, "A"),
+    _invoke(lib.tt_interface_left, rl, n, rr, Rl, Rr, _dev(phiL_prev, "phiL_prev"), _dev(A, "A"),
                                  _dev(x, "x"), _dev(out, "phiL_next"), ws.data_ptr(), ws.numel(),
-                                 _stream(stream)))
+                                 _stream(stream))
     return out
 
 
@@ -291,9 +344,9 @@ def tt_interface_right(phiR_next, A, x, out=None, workspace=None, stream=None):
     _expect(out, (rl, Rl, rl), "phiR_prev")
     _same_device(phiR_next, A, x, out, workspace)
     ws = _ws(tt_interface_workspace_size(rl, n, rr, Rl, Rr), workspace, x.device)
-    _check(lib.tt_interface_right(rl, n, rr, Rl, Rr, _dev(phiR_next, "phiR_next"), _dev(A, "A"),
+    _invoke(lib.tt_interface_right, rl, n, rr, Rl, Rr, _dev(phiR_next, "phiR_next"), _dev(A, "A"),
                                   _dev(x, "x"), _dev(out, "phiR_prev"), ws.data_ptr(), ws.numel(),
-                                  _stream(stream)))
+                                  _stream(stream))
     return out
 
 
@@ -388,8 +441,8 @@ def tt_sweep_interfaces(x_cores, A_cores, phiL=None, phiR=None, directions=TT_SW
     ws = _ws(tt_sweep_workspace_size(tr), workspace, x_cores[0].device)
     pl = _ptrs(phiL, "phiL") if phiL is not None else None
     pr = _ptrs(phiR, "phiR") if phiR is not None else None
-    _check(lib.tt_sweep_interfaces(tr.d, tr._n, tr._r, tr._R, tr._x, tr._A, pl, pr, directions,
-                                   ws.data_ptr(), ws.numel(), _stream(stream)))
+    _invoke(lib.tt_sweep_interfaces, tr.d, tr._n, tr._r, tr._R, tr._x, tr._A, pl, pr, directions,
+                                   ws.data_ptr(), ws.numel(), _stream(stream))
     return phiL, phiR
 
 
@@ -412,9 +465,9 @@ def tt_sweep_w34(x_cores, A_cores, phiL=None, phiR=None, y_cores=None, workspace
     _check_interfaces(tr, phiR, "phiR")
     _check_cores(tr, y_cores, "y_cores")
     ws = _ws(tt_sweep_w34_workspace_size(tr), workspace, x_cores[0].device)
-    _check(lib.tt_sweep_w34(tr.d, tr._n, tr._r, tr._R, tr._x, tr._A, _ptrs(phiL, "phiL"),
+    _invoke(lib.tt_sweep_w34, tr.d, tr._n, tr._r, tr._R, tr._x, tr._A, _ptrs(phiL, "phiL"),
                             _ptrs(phiR, "phiR"), _ptrs(y_cores, "y_cores"), ws.data_ptr(),
-                            ws.numel(), _stream(stream)))
+                            ws.numel(), _stream(stream))
     return y_cores, phiL, phiR
 
 
@@ -436,11 +489,11 @@ def tt_sweep_als(x_cores, A_cores, X_blocks, Y_fwd=None, Y_bwd=None, phiL=None, 
     _check_interfaces(tr, phiL, "phiL")
     _check_interfaces(tr, phiR, "phiR")
     ws = _ws(tt_sweep_als_workspace_size(tr, nvec), workspace, x_cores[0].device)
-    _check(lib.tt_sweep_als(tr.d, tr._n, tr._r, tr._R, nvec, tr._x, tr._A,
+    _invoke(lib.tt_sweep_als, tr.d, tr._n, tr._r, tr._R, nvec, tr._x, tr._A,
                             _ptrs(X_blocks, "X_blocks"), _ptrs(Y_fwd, "Y_fwd"),
                             _ptrs(Y_bwd, "Y_bwd") if Y_bwd is not None else None,
                             _ptrs(phiL, "phiL"), _ptrs(phiR, "phiR"), ws.data_ptr(), ws.numel(),
-                            _stream(stream)))
+                            _stream(stream))
     return Y_fwd, Y_bwd, phiL, phiR
 
 
@@ -471,9 +524,9 @@ def tt_operator_apply(x_cores, A_cores, z_cores=None, stream=None):
         _expect(z_cores[k], (r[k] * R[k], n_row[k], r[k + 1] * R[k + 1]), f"z_cores[{k}]")
     _same_device(*x_cores, *A_cores, *z_cores)
     a64 = lambda v: (ctypes.c_int64 * len(v))(*v)
-    _check(lib.tt_operator_apply(d, a64(n_row), a64(n_col), a64(r), a64(R),
+    _invoke(lib.tt_operator_apply, d, a64(n_row), a64(n_col), a64(r), a64(R),
                                  _ptrs(x_cores, "x_cores"), _ptrs(A_cores, "A_cores"),
-                                 _ptrs(z_cores, "z_cores"), _stream(stream)))
+                                 _ptrs(z_cores, "z_cores"), _stream(stream))
     return z_cores
 
 

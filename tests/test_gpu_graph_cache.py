@@ -111,3 +111,32 @@ def test_interface_replay_and_user_capture(tt):
     graph.replay()
     torch.cuda.synchronize()
     assert torch.equal(out2, ref)
+
+
+def test_prepared_calls_reissue_the_same_work(tt):
+    """tt.prepare: one validation / marshalling, then re-issues of the identical C-ABI call
+    (its internally allocated workspace stays alive)."""
+    import gc
+    import ttgen
+    inp = ttgen.make_inputs(3)
+    x = [g(c) for c in inp.x]
+    A = [g(c) for c in inp.A]
+    y0, pl0, pr0 = tt.tt_sweep_w34(x, A)
+    p = tt.prepare(tt.tt_sweep_w34, x, A)
+    gc.collect()
+    torch.cuda.empty_cache()
+    for _ in range(3):
+        y, pl, pr = p()
+        torch.cuda.synchronize()
+        for a, b in zip(y + pl + pr, y0 + pl0 + pr0):
+            assert torch.equal(a, b)
+    k = 5
+    rng = np.random.default_rng(11)
+    phL = g(rng.standard_normal((x[k].shape[0], A[k].shape[0], x[k].shape[0])))
+    phR = g(rng.standard_normal((x[k].shape[2], A[k].shape[3], x[k].shape[2])))
+    pm = tt.prepare(tt.tt_local_matvec, phL, A[k], phR, x[k])
+    y1 = pm().clone()
+    x[k].mul_(3.0)
+    y3 = pm()
+    torch.cuda.synchronize()
+    assert torch.allclose(y3, 3.0 * y1, rtol=1e-14, atol=0)

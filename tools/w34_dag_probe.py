@@ -37,6 +37,8 @@ for idx in [int(a) for a in (sys.argv[1:] or ["1", "2", "3", "4"])]:
         tt.tt_debug_set_dag(0 if mode == 9 else mode)
         s = torch.cuda.Stream()
         call = lambda: tt.tt_sweep_w34(x, A, pl, pr, y, workspace=ws, stream=s)
+        if mode == 0:   # prepared call: one ctypes call per sweep
+            call = tt.prepare(tt.tt_sweep_w34, x, A, pl, pr, y, workspace=ws, stream=s)
         with torch.cuda.stream(s):
             for _ in range(3):
                 call()
