@@ -441,6 +441,54 @@ static cudaError_t sweep_right_step(int64_t k, int64_t d, int64_t nvec, void* sc
                               pp.Ahr, pp.xt);
 }
 
+// Runs of consecutive small updates (tt_core.cu small_chain_kernel): the number of cores from
+// core k on (left: k, k+1, ...; right: k, k-1, ...) that one CTA updates in a single launch.
+static Dims chain_dims(bool left, int64_t k, const int64_t* n, const int64_t* r, const int64_t* R) {
+  return left ? Dims{r[k], n[k], r[k + 1], R[k], R[k + 1]}
+              : Dims{r[k + 1], n[k], r[k], R[k + 1], R[k]};   // mirrored right update
+}
+static int small_run(bool left, int64_t k, int64_t d, const int64_t* n, const int64_t* r,
+                     const int64_t* R) {
+  int run = 0;
+  size_t pmax = 0, work = 0;
+  for (int64_t kk = k; kk >= 0 && kk < d && run < kSmallChainMax; kk += left ? 1 : -1) {
+    const Dims dk = chain_dims(left, kk, n, r, R);
+    if (!small_update(dk)) break;
+    pmax = std::max(pmax, (size_t)(dk.a * dk.al * dk.a));
+    work = std::max(work, small_chain_work(dk));
+    if ((pmax + work) * sizeof(double) > 200 * 1024) break;
+    ++run;
+  }
+  return run;
+}
+static cudaError_t enqueue_small_run(bool left, int64_t k, int run, int64_t d, const int64_t* n,
+                                     const int64_t* r, const int64_t* R,
+                                     const double* const* xc, double* const* phi,
+                                     double* const* T2keep, void* ws, cudaStream_t s) {
+  SmallChain c{};
+  c.cores = run;
+  size_t pmax = 0, work = 0;
+  c.phi_in = left ? phi[k] : phi[k + 1];
+  for (int q = 0; q < run; ++q) {
+    const int64_t kk = left ? k + q : k - q;
+    const Dims dk = chain_dims(left, kk, n, r, R);
+    const Prep pp = prep_ptrs(kk, d, n, r, R, 0, ws);
+    c.a[q] = (int)dk.a;
+    c.b[q] = (int)dk.b;
+    c.al[q] = (int)dk.al;
+    c.be[q] = (int)dk.be;
+    c.n[q] = (int)dk.n;
+    c.x[q] = left ? xc[kk] : pp.xt;
+    c.Ah[q] = left ? pp.Ahl : pp.Ahr;
+    c.phi_out[q] = left ? phi[kk + 1] : phi[kk];
+    c.T2keep[q] = (left && T2keep) ? T2keep[kk] : nullptr;
+    pmax = std::max(pmax, (size_t)(dk.a * dk.al * dk.a));
+    work = std::max(work, small_chain_work(dk));
+  }
+  c.pmax = (int)pmax;
+  return launch_small_chain(c, (pmax + work) * sizeof(double), s);
+}
+
 static cudaError_t sweep_matvec_step(int64_t k, int64_t d, void* scratch, const int64_t* n, const int64_t* r,
                                      const int64_t* R, int64_t nvec, const double* const* Ac,
                                      const double* const* Xb, double* const* Yb,
@@ -530,18 +578,38 @@ tt_status tt_sweep_interfaces(int64_t d, const int64_t* n, const int64_t* r, con
     if ((e = side_stream(&sr)) != cudaSuccess) return cuda_fail(e, "side stream");
     if ((e = stream_dep(s, sr)) != cudaSuccess) return cuda_fail(e, "fork");
   }
+  // runs of small boundary updates go to one fused launch each (debug bit 28 disables)
+  const bool small_on = !(g_dbg_flags & 8);
   if (doL) {
-    for (int64_t k = 0; k < d; ++k)
+    for (int64_t k = 0; k < d;) {
+      const int run = small_on ? small_run(true, k, d, n, r, R) : 0;
+      if (run > 0) {
+        if ((e = enqueue_small_run(true, k, run, d, n, r, R, x_cores, phiL, nullptr, workspace, s)) != cudaSuccess)
+          return cuda_fail(e, "sweep left (small)");
+        k += run;
+        continue;
+      }
       if ((e = sweep_left_step(k, d, 0, ws_main, n, r, R, x_cores, A_cores, phiL, workspace,
                                main_b, s)) != cudaSuccess)
         return cuda_fail(e, "sweep left");
+      ++k;
+    }
   }
   if (doR) {
     void* wr = (sr == s) ? ws_main : ws_side;
-    for (int64_t k = d - 1; k >= 0; --k)
+    for (int64_t k = d - 1; k >= 0;) {
+      const int run = small_on ? small_run(false, k, d, n, r, R) : 0;
+      if (run > 0) {
+        if ((e = enqueue_small_run(false, k, run, d, n, r, R, x_cores, phiR, nullptr, workspace, sr)) != cudaSuccess)
+          return cuda_fail(e, "sweep right (small)");
+        k -= run;
+        continue;
+      }
       if ((e = sweep_right_step(k, d, 0, wr, n, r, R, x_cores, A_cores, phiR, workspace, main_b,
                                 sr)) != cudaSuccess)
         return cuda_fail(e, "sweep right");
+      --k;
+    }
   }
   if (sr != s && (e = stream_dep(sr, s)) != cudaSuccess) return cuda_fail(e, "join");
   return TT_OK;
@@ -755,18 +823,43 @@ tt_status tt_sweep_w34(int64_t d, const int64_t* n, const int64_t* r, const int6
   cudaStream_t sl = g_res.pool.chain;
   if ((e = stream_dep(s, sl)) != cudaSuccess) return cuda_fail(e, "fork");
   if ((e = cudaEventRecord(evL[0], sl)) != cudaSuccess) return cuda_fail(e, "event");
-  for (int64_t k = 0; k < d; ++k) {
+  // runs of small boundary updates go to one fused launch each (debug bits 3 / 28 disable)
+  const bool small_on = !(g_dbg_flags & 8);
+  for (int64_t k = 0; k < d;) {
+    const int run = small_on ? small_run(true, k, d, n, r, R) : 0;
+    if (run > 0) {
+      if ((e = enqueue_small_run(true, k, run, d, n, r, R, x_cores, phiL, reuse ? T2k.data() : nullptr,
+                                 workspace, sl)) != cudaSuccess)
+        return cuda_fail(e, "sweep left (small)");
+      for (int q = 0; q < run; ++q) {
+        if (reuse && (e = cudaEventRecord(evT[k + q], sl)) != cudaSuccess) return cuda_fail(e, "event");
+        if ((e = cudaEventRecord(evL[k + q + 1], sl)) != cudaSuccess) return cuda_fail(e, "event");
+      }
+      k += run;
+      continue;
+    }
     if ((e = sweep_left_step(k, d, 0, ws_main, n, r, R, x_cores, A_cores, phiL, workspace, main_b,
                              sl, T2k[k], reuse ? evT[k] : nullptr)) != cudaSuccess)
       return cuda_fail(e, "sweep left");
     if ((e = cudaEventRecord(evL[k + 1], sl)) != cudaSuccess) return cuda_fail(e, "event");
+    ++k;
   }
   if ((e = cudaEventRecord(evR[d], sr)) != cudaSuccess) return cuda_fail(e, "event");
-  for (int64_t k = d - 1; k >= 0; --k) {
+  for (int64_t k = d - 1; k >= 0;) {
+    const int run = small_on ? small_run(false, k, d, n, r, R) : 0;
+    if (run > 0) {
+      if ((e = enqueue_small_run(false, k, run, d, n, r, R, x_cores, phiR, nullptr, workspace, sr)) != cudaSuccess)
+        return cuda_fail(e, "sweep right (small)");
+      for (int q = 0; q < run; ++q)
+        if ((e = cudaEventRecord(evR[k - q], sr)) != cudaSuccess) return cuda_fail(e, "event");
+      k -= run;
+      continue;
+    }
     if ((e = sweep_right_step(k, d, 0, ws_side, n, r, R, x_cores, A_cores, phiR, workspace,
                               main_b, sr)) != cudaSuccess)
       return cuda_fail(e, "sweep right");
     if ((e = cudaEventRecord(evR[k], sr)) != cudaSuccess) return cuda_fail(e, "event");
+    --k;
   }
   // matvecs in readiness order (core k needs k left steps and d-1-k right steps)
   std::vector<int64_t> order(d);

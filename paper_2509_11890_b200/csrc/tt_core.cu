@@ -414,6 +414,103 @@ cudaError_t launch_perm(bool left, const double* A, double* out, long long al, l
 }
 
 
+// ---- fused small interface updates (the boundary cores of every sweep) --------------------
+// An interface update at the tiny ranks near the ends of a train (r = 1, 4, 16: a few hundred
+// kFLOP) costs three dependent launches whose runtime is pure latency.  One CTA performs a run
+// of consecutive small updates of one chain entirely in shared memory: for each core
+//   T1[a', al, j, b] = sum_a  P[a', al, a] x[a, j, b]                       (S1)
+//   T2[a', i, be, b] = sum_{al, j} Ah[(al, j), (i, be)] T1[a', al, j, b]   (S2; optional copy out)
+//   P'[b', be, b]    = sum_{a', i} x[a', i, b'] T2[a', i, be, b]           (S3')
+// the output P' feeding the next core of the run in shared memory.  The operator arrives in
+// the prepared left layout Ah (al, j, i, be) (prep_all_kernel); a right update runs as the
+// mirrored left update on (xt, Ahr) exactly as in the stream plans.
+__global__ void __launch_bounds__(256) small_chain_kernel(const __grid_constant__ SmallChain c) {
+  extern __shared__ double sm[];
+  tt::pdl_wait();
+  double* P = sm;   // current input interface ([0, pmax): never overlaps the work regions)
+  for (int q = 0; q < c.cores; ++q) {
+    const int a = c.a[q], b = c.b[q], al = c.al[q], be = c.be[q], N = c.n[q];
+    double* X = P + c.pmax;
+    double* AH = X + a * N * b;
+    double* T1 = AH + al * N * N * be;
+    double* T2 = T1 + a * al * N * b;
+    double* PN = T2 + a * N * be * b;
+    if (q == 0)
+      for (int e = threadIdx.x; e < a * al * a; e += blockDim.x) P[e] = c.phi_in[e];
+    for (int e = threadIdx.x; e < a * N * b; e += blockDim.x) X[e] = c.x[q][e];
+    for (int e = threadIdx.x; e < al * N * N * be; e += blockDim.x) AH[e] = c.Ah[q][e];
+    __syncthreads();
+    // S1: T1[((a' al + al_) N + j) b + bb]
+    for (int e = threadIdx.x; e < a * al * N * b; e += blockDim.x) {
+      const int bb = e % b, j = (e / b) % N, aal = e / (b * N);   // aal = a' al + al_
+      const double* pr = P + aal * a;
+      double s = 0.0;
+      for (int k = 0; k < a; ++k) s = fma(pr[k], X[(k * N + j) * b + bb], s);
+      T1[e] = s;
+    }
+    __syncthreads();
+    // S2: T2[((a' N + i) be + be_) b + bb]
+    for (int e = threadIdx.x; e < a * N * be * b; e += blockDim.x) {
+      const int bb = e % b, bq = (e / b) % be, i = (e / (b * be)) % N, ap = e / (b * be * N);
+      double s = 0.0;
+      for (int k = 0; k < al; ++k)
+        for (int j = 0; j < N; ++j)
+          s = fma(AH[((k * N + j) * N + i) * be + bq], T1[((ap * al + k) * N + j) * b + bb], s);
+      T2[e] = s;
+      if (c.T2keep[q]) c.T2keep[q][e] = s;
+    }
+    __syncthreads();
+    // S3': PN[(b' be + be_) b + bb]
+    for (int e = threadIdx.x; e < b * be * b; e += blockDim.x) {
+      const int bb = e % b, bq = (e / b) % be, bp = e / (b * be);
+      double s = 0.0;
+      for (int ap = 0; ap < a; ++ap)
+        for (int i = 0; i < N; ++i)
+          s = fma(X[(ap * N + i) * b + bp], T2[((ap * N + i) * be + bq) * b + bb], s);
+      PN[e] = s;
+      c.phi_out[q][e] = s;
+    }
+    __syncthreads();
+    // the output becomes the next core's input interface (front of shared memory)
+    if (q + 1 < c.cores) {
+      for (int e = threadIdx.x; e < b * be * b; e += blockDim.x) P[e] = PN[e];
+      __syncthreads();
+    }
+  }
+  tt::pdl_trigger();
+}
+
+// shared memory of one core's work regions (x, operator, T1, T2, output), in doubles
+size_t small_chain_work(const Dims& d) {
+  return (size_t)(d.a * d.n * d.b + d.al * d.n * d.n * d.be + d.a * d.al * d.n * d.b +
+                  d.a * d.n * d.be * d.b + d.b * d.be * d.b);
+}
+size_t small_chain_smem(const Dims& d) {
+  return (size_t)(d.a * d.al * d.a) * sizeof(double) + small_chain_work(d) * sizeof(double);
+}
+
+// a core whose update is cheap enough for one CTA and fits in shared memory.  The one-CTA FMA
+// loops run at ~20-50 GFLOP/s: 1.5 MFLOP (config-3/4 core 1) made W34 slower (config 3
+// 159 -> 248 us); below ~0.1 MFLOP one launch beats three dependent stage launches.
+constexpr double kSmallUpdateFlops = 1.0e5;
+bool small_update(const Dims& d) {
+  const double f = 2.0 * d.n * (double)(d.a * d.a * d.al * d.b + d.a * d.b * d.b * d.be) +
+                   2.0 * d.a * d.b * d.al * d.be * d.n * d.n;
+  return !(g_dbg_flags & (1 << 28)) && f <= kSmallUpdateFlops && small_chain_smem(d) <= 200 * 1024;
+}
+
+cudaError_t launch_small_chain(const SmallChain& c, size_t smem, cudaStream_t s) {
+  if (cudaError_t e = smem_attr((const void*)small_chain_kernel, (int)std::max<size_t>(smem, 1)))
+    return e;
+  g_stage = TT_ST_IL_S1;
+  const long long tr = trace_begin(-2, c.cores, 0, 0, s);
+  cudaError_t e = launch_pdl(true, small_chain_kernel, dim3(1), dim3(256), smem, s, c);
+  trace_end(tr, s);
+  ++g_launches;
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
 // ----------------------------------------------------------------------------------------
 // stage plans
 // ----------------------------------------------------------------------------------------

@@ -134,6 +134,19 @@ struct Dims {
   long long a, n, b, al, be;
 };
 
+constexpr int kSmallChainMax = 8;
+struct SmallChain {   // a run of consecutive small left updates in one CTA (tt_core.cu)
+  int cores;
+  int pmax;                             // doubles reserved for the running input interface
+  int a[kSmallChainMax], b[kSmallChainMax], al[kSmallChainMax], be[kSmallChainMax],
+      n[kSmallChainMax];
+  const double* phi_in;                 // interface into the first core
+  const double* x[kSmallChainMax];      // vector core (a, n, b) (or the transposed core)
+  const double* Ah[kSmallChainMax];     // operator core in the prepared layout (al, j, i, be)
+  double* phi_out[kSmallChainMax];      // output interfaces (b, be, b)
+  double* T2keep[kSmallChainMax];       // optional stage-2 intermediates (a, n, be, b)
+};
+
 struct SplitScratch {   // scopes the split-K scratch to one stage launch
   SplitScratch(double* p, long long n) {
     g_pscratch = p;
@@ -219,6 +232,10 @@ GemmParams gp(const double* A, long long lda, const double* B, long long ldb, do
 
 // ---- small kernels and stage plans (tt_core.cu) -------------------------------------------------
 __global__ void __launch_bounds__(256) prep_all_kernel(const __grid_constant__ PrepTable t);
+size_t small_chain_smem(const Dims& d);
+size_t small_chain_work(const Dims& d);
+bool small_update(const Dims& d);
+cudaError_t launch_small_chain(const SmallChain& c, size_t smem, cudaStream_t s);
 cudaError_t launch_perm(bool left, const double* A, double* out, long long al, long long n,
                         long long be, cudaStream_t s);
 bool matvec_ws_elems(const Dims& d, long long K, long long& t1, long long& t2, long long& ah,

@@ -455,6 +455,28 @@ def test_local_gmres_fused_orth_equals_separate_kernels(tt, idx, k, m, kaug):
     assert np.allclose(h(ra), h(rb), rtol=1e-6, atol=1e-14)
 
 
+@pytest.mark.parametrize("idx", [1, 2, 3, 4])
+def test_small_boundary_runs_equal_stage_gemms(tt, idx):
+    """Runs of small boundary updates in one fused CTA (default) against the three DMMA stage
+    GEMMs per core (debug bit 28): interfaces and W34 matvecs agree to rounding."""
+    import ttgen
+    inp = ttgen.make_inputs(idx)
+    x = [g(c) for c in inp.x]
+    A = [g(c) for c in inp.A]
+    outs = []
+    for flags in (0, 1 << 28):
+        tt.tt_debug_set_flags(flags)
+        try:
+            pl, pr = tt.tt_sweep_interfaces(x, A)
+            y, ql, qr = tt.tt_sweep_w34(x, A)
+            torch.cuda.synchronize()
+            outs.append(pl + pr + y + ql + qr)
+        finally:
+            tt.tt_debug_set_flags(0)
+    for a, b in zip(*outs):
+        assert rel(h(a), h(b)) <= 1e-13
+
+
 def test_local_gmres_errors(tt):
     F = torch.zeros(2, 4, 65, 2, dtype=torch.float64, device="cuda")
     A = torch.zeros(1, 4, 4, 1, dtype=torch.float64, device="cuda")
@@ -631,10 +653,9 @@ def test_sweep_w34_call_vs_oracle_and_separate_calls(tt, idx, flags, dag):
     tt.tt_sweep_interfaces(x, A, pl2, pr2)
     for k in range(len(x)):
         y2 = tt.tt_local_matvec(pl2[k], A[k], pr2[k + 1], x[k])
-        if dag == 0:
-            assert torch.equal(y[k], y2)
-        else:
-            assert rel(h(y[k]), h(y2)) <= 1e-13
+        # boundary cores: W34 reuses the fused small update's stage-2 intermediate (FMA loops)
+        # where tt_local_matvec runs the DMMA stages -> equal up to rounding order
+        assert rel(h(y[k]), h(y2)) <= 1e-13
     for a, b in zip(pl + pr, pl2 + pr2):
         if dag == 0:
             assert torch.equal(a, b)
