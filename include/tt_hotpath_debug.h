@@ -49,7 +49,9 @@ void tt_debug_set_variant(int v);
  * operator-core stage with the whole A-hat resident in shared memory (3-deep T1 ring;
  * measured slower, kept as a probe), bit 26 runs tt_local_gmres's K = 1 orthogonalisation
  * step as separate kernels instead of the fused cluster kernel, bit 28 runs the small boundary
- * interface updates of the sweeps as three stage GEMMs each instead of fused one-CTA runs.
+ * interface updates of the sweeps as three stage GEMMs each instead of fused one-CTA runs, bit 29
+ * the orthonormalisation steps of tt_round / tt_orthonormalise through the Gram matrix instead
+ * of the cluster Householder QR.
  * tt_debug_set_variant(v): v >= 10 forces
  * the GEMM tile configuration v % 100 (probe list in csrc/tt_launch_tpl.cuh) and split-K factor v / 100. */
 void tt_debug_set_flags(int flags);

@@ -275,8 +275,13 @@ __global__ void __launch_bounds__(NT) gmres_orth_cluster_kernel(
   auto combine = [&](double* part, double* h, int n) {
     cluster.sync();
     if (tid < n) {
+      double pv[16];   // all remote loads in flight, then the rank-order sum
+#pragma unroll
+      for (int r = 0; r < 16; ++r) pv[r] = r < ncl ? cluster.map_shared_rank(part, r)[tid] : 0.0;
       double v = 0.0;
-      for (int r = 0; r < ncl; ++r) v += cluster.map_shared_rank(part, r)[tid];
+#pragma unroll
+      for (int r = 0; r < 16; ++r)
+        if (r < ncl) v += pv[r];
       h[tid] = v;
     }
     __syncthreads();

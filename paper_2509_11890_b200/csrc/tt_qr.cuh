@@ -1,0 +1,227 @@
+// tt_qr.cuh — Householder QR of an m x c core unfolding in ONE thread-block cluster (sm_100a).
+//
+// TT orthonormalisation (the rounding's orthonormalisation sweeps and the
+// block-index move) needs M = Q R with Q orthonormal to working precision.  The Gram route
+// (M^T M -> eigenvectors) squares the condition number; Householder reflections do not.  A
+// config-5 interior unfolding (1024 x 256, 2 MB) is spread over the distributed shared memory of
+// a 16-CTA cluster (64 rows per CTA), so every column step works on-chip:
+//   step j:  sigma^2 = sum_{i>j} M[i][j]^2 (per-CTA partials combined through DSMEM in rank
+//            order, identical in every CTA), the reflector (LAPACK dlarfg convention:
+//            beta = -sign(x_j) ||x||, tau = (beta - x_j) / beta, v = x / (x_j - beta), v_j = 1)
+//            stored in place below the diagonal;
+//            w = v^T M[j:, j+1:] (DSMEM-combined partials), M[i][col] -= tau v_i w[col].
+//   then R is read off the upper triangle and Q = H_0 ... H_{k-1} [I; 0] is formed in place
+//   backwards (LAPACK dorg2r order).
+// Two cluster barriers per reflector and per backward step; every reduction is deterministic.
+// Included by tt_solvers.cu inside namespace ttint.
+
+constexpr int kQrThreads = 512;
+constexpr size_t kQrSmemMax = 220 * 1024;
+
+struct QrArgs {
+  const double* M;     // input, M[i][j] at M[i * rs + j * cs]
+  long long rs, cs;
+  int m, c;            // rows, columns; k = min(m, c) reflectors
+  double* Q;           // output Q (m x k), Q[i][j] at Q[i * qrs + j * qcs] (may alias M)
+  long long qrs, qcs;
+  double* R;           // output R (k x c), row-major, zeros below the diagonal
+  int rb;              // rows per CTA
+};
+
+__device__ __forceinline__ double qr_block_sum(double v, double* red, int tid) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if ((tid & 31) == 0) red[tid >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int w = 0; w < kQrThreads / 32; ++w) s += red[w];
+  return s;
+}
+
+__global__ void __launch_bounds__(kQrThreads) qr_cluster_kernel(const QrArgs p) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank(), ncl = (int)cluster.num_blocks();
+  const int tid = threadIdx.x;
+  const int m = p.m, c = p.c, k = min(m, c), rb = p.rb, ld = c + 1;   // odd row stride
+  extern __shared__ double qsm[];
+  double* A = qsm;                       // [rb][ld] this CTA's rows
+  double* inbox = A + (size_t)rb * ld;   // [2][16][c + 2] partials pushed by every CTA
+  double* tau = inbox + 2 * 16 * (c + 2);   // [k]
+  double* wv = tau + k;                  // [c + 2] combined sums
+  __shared__ double red[kQrThreads / 32];
+  const int r0 = rank * rb;
+  const int nr = max(0, min(rb, m - r0));   // rows held by this CTA
+  for (int e = tid; e < nr * c; e += kQrThreads) {
+    const int i = e / c, j = e - i * c;
+    A[i * ld + j] = p.M[(long long)(r0 + i) * p.rs + (long long)j * p.cs];
+  }
+  __syncthreads();
+  int red_no = 0;   // running reduction index: inbox parity red_no & 1
+  // Reductions push: the thread holding a partial stores it into slot [parity][its rank][q]
+  // of EVERY CTA's inbox (remote DSMEM stores, nothing to wait for), one cluster barrier
+  // (release / acquire) makes them visible, and each CTA sums its inbox locally in rank order
+  // (identical, deterministic results in every CTA).  Reusing a parity two reductions later
+  // is safe: a CTA reads reduction t's inbox before arriving at barrier t + 1.
+  auto push = [&](int par, int q, double v, int r) {   // to CTA r
+    cluster.map_shared_rank(inbox, r)[(par * 16 + rank) * (c + 2) + q] = v;
+  };
+  auto gather = [&](int par, int n, double* out) {
+    cluster.sync();
+    for (int q = tid; q < n; q += kQrThreads) {
+      double s = 0.0;
+      for (int r = 0; r < ncl; ++r) s += inbox[(par * 16 + r) * (c + 2) + q];
+      out[q] = s;
+    }
+    __syncthreads();
+  };
+  // w[col] = sum_{i >= j} v_i M[i][col] for col in [c0, c1), v_j = 1, v_i = A[i][j] below;
+  // then M[i][col] -= t v_i w[col].  Warps own columns for the dots (lanes over rows, shuffle
+  // reduction) and rows for the update (lanes over columns): no integer division, no serial
+  // FMA chains longer than rb / 32.
+  const int lane = tid & 31, warp = tid >> 5;
+  constexpr int kWarps = kQrThreads / 32;
+  auto apply_reflector = [&](int j, int c0, int c1, double t) {
+    const int par = red_no++ & 1;
+    const int ib = max(0, min(nr, j - r0));   // first local row with global index >= j
+    for (int col = c0 + warp; col < c1; col += kWarps) {
+      double s = 0.0;
+      for (int i = ib + lane; i < nr; i += 32) {
+        const double v = (r0 + i == j) ? 1.0 : A[i * ld + j];
+        s = fma(v, A[i * ld + col], s);
+      }
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane < ncl) push(par, col - c0, s, lane);
+    }
+    gather(par, c1 - c0, wv);
+    for (int i = ib + warp; i < nr; i += kWarps) {
+      const double tv = -t * ((r0 + i == j) ? 1.0 : A[i * ld + j]);
+      for (int col = c0 + lane; col < c1; col += 32)
+        A[i * ld + col] = fma(tv, wv[col - c0], A[i * ld + col]);
+    }
+    __syncthreads();
+  };
+
+  // ---- factorisation ---------------------------------------------------------------------
+  for (int j = 0; j < k; ++j) {
+    const int owner = j / rb;
+    const int par = red_no++ & 1;
+    double s2 = 0.0;
+    for (int i = tid; i < nr; i += kQrThreads)
+      if (r0 + i > j) s2 = fma(A[i * ld + j], A[i * ld + j], s2);
+    s2 = qr_block_sum(s2, red, tid);
+    if (tid < ncl) {
+      push(par, 0, s2, tid);
+      push(par, 1, (rank == owner) ? A[(j - r0) * ld + j] : 0.0, tid);
+    }
+    gather(par, 2, wv);
+    const double sigma2 = wv[0], xj = wv[1];
+    double t = 0.0, beta = xj, scal = 0.0;
+    if (sigma2 > 0.0) {
+      beta = -copysign(sqrt(fma(xj, xj, sigma2)), xj);
+      t = (beta - xj) / beta;
+      scal = 1.0 / (xj - beta);
+    }
+    if (tid == 0) tau[j] = t;
+    for (int i = tid; i < nr; i += kQrThreads) {
+      const int gi = r0 + i;
+      if (gi > j) A[i * ld + j] *= scal;
+      else if (gi == j) A[i * ld + j] = beta;
+    }
+    __syncthreads();
+    if (j + 1 < c && t != 0.0) apply_reflector(j, j + 1, c, t);   // t is uniform: same branch in every CTA
+  }
+  // ---- R: the upper triangle of rows 0..k-1 ----------------------------------------------
+  for (int e = tid; e < nr * c; e += kQrThreads) {
+    const int i = e / c, col = e - i * c;
+    const int gi = r0 + i;
+    if (gi < k) p.R[(long long)gi * c + col] = (col >= gi) ? A[i * ld + col] : 0.0;
+  }
+  __syncthreads();
+  // ---- Q = H_0 ... H_{k-1} [I; 0], formed in place backwards (dorg2r) ---------------------
+  for (int j = k - 1; j >= 0; --j) {
+    if (j < k - 1) apply_reflector(j, j + 1, k, tau[j]);
+    const double t = tau[j];
+    for (int i = tid; i < nr; i += kQrThreads) {
+      const int gi = r0 + i;
+      if (gi > j) A[i * ld + j] *= -t;
+      else if (gi == j) A[i * ld + j] = 1.0 - t;
+      else A[i * ld + j] = 0.0;
+    }
+    __syncthreads();
+  }
+  cluster.sync();   // every CTA's remote reads are done before Q may overwrite M (aliasing)
+  for (int e = tid; e < nr * k; e += kQrThreads) {
+    const int i = e / k, j = e - i * k;
+    p.Q[(long long)(r0 + i) * p.qrs + (long long)j * p.qcs] = A[i * ld + j];
+  }
+  cluster.sync();   // no CTA leaves while another may still read its shared memory
+}
+
+// cluster size for an m-row factorisation (16 where non-portable clusters are available, per
+// device); 0 when the rows do not fit the cluster's shared memory
+inline int qr_cluster_size(int m, int c) {
+  thread_local int cl_dev[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& cl = cl_dev[dev & 63];
+  if (cl == 0) {
+    cl = 8;
+    if (cudaFuncSetAttribute(qr_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+            cudaSuccess &&
+        smem_attr((const void*)qr_cluster_kernel, (int)kQrSmemMax) == cudaSuccess) {
+      cudaLaunchConfig_t q = {};
+      q.gridDim = dim3(16);
+      q.blockDim = dim3(kQrThreads);
+      q.dynamicSmemBytes = kQrSmemMax;
+      cudaLaunchAttribute a[1];
+      a[0].id = cudaLaunchAttributeClusterDimension;
+      a[0].val.clusterDim.x = 16;
+      a[0].val.clusterDim.y = 1;
+      a[0].val.clusterDim.z = 1;
+      q.attrs = a;
+      q.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, qr_cluster_kernel, &q) == cudaSuccess && n > 0) cl = 16;
+    }
+    cudaGetLastError();
+  }
+  return cl;
+}
+inline size_t qr_smem(int m, int c, int cl) {
+  const long long rb = (m + cl - 1) / cl;
+  const int k = std::min(m, c);
+  return sizeof(double) * (size_t)(rb * (c + 1) + 2 * 16 * (c + 2) + k + c + 2);
+}
+inline bool qr_fits(int m, int c) {
+  if (m <= 0 || c <= 0 || c > kQrThreads * 4) return false;
+  return qr_smem(m, c, qr_cluster_size(m, c)) <= kQrSmemMax;
+}
+
+// Q (m x k) and R (k x c) of M; Q may alias M.  One cluster launch.
+inline cudaError_t launch_qr(const QrArgs& a0, cudaStream_t s) {
+  QrArgs a = a0;
+  const int cl = qr_cluster_size(a.m, a.c);
+  a.rb = (a.m + cl - 1) / cl;
+  const size_t smem = qr_smem(a.m, a.c, cl);
+  if (smem > kQrSmemMax) return cudaErrorInvalidValue;
+  if (cudaError_t e = smem_attr((const void*)qr_cluster_kernel, (int)kQrSmemMax)) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cl);
+  cfg.blockDim = dim3(kQrThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  g_stage = TT_ST_SET;
+  const long long tr = trace_begin(-3, a.m, a.c, 0, s);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, qr_cluster_kernel, a);
+  trace_end(tr, s);
+  ++g_launches;
+  return e;
+}

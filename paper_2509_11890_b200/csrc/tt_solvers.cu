@@ -7,6 +7,7 @@ namespace ttint {
 
 #include "tt_gmres.cuh"
 #include "tt_round.cuh"
+#include "tt_qr.cuh"
 #include "tt_lobpcg.cuh"
 
 // Symmetric eigendecomposition of the n x n Gram matrix G: lam (descending) and V (columns)
@@ -252,9 +253,33 @@ static tt_status round_impl(int64_t d, const int64_t* n, const int64_t* r_in,
     return cudaGetLastError();
   };
   const double zero_rel = 1e-14;   // relative eigenvalue floor (numerical zero of the Gram)
-  // right-to-left orthonormalisation: W_k = (V S)(S^-1 V^T W_k), W_{k-1} <- W_{k-1} V S
+  // right-to-left orthonormalisation by Householder QR (tt_qr.cuh, exact to working
+  // precision): W_k^T = Q R, W_k <- Q^T, W_{k-1} <- W_{k-1} R^T.  The Gram route below remains
+  // for unfoldings that do not fit one cluster's shared memory (debug bit 29 forces it).
   for (int64_t k = d - 1; (phases & 1) && k >= 1 && e == cudaSuccess; --k) {
     const long long rk = r[k], q = n[k] * r[k + 1];
+    if (!(g_dbg_flags & (1 << 29)) && qr_fits((int)q, (int)rk)) {
+      const long long kk = std::min(q, rk);
+      QrArgs qa{};
+      qa.M = W[k];
+      qa.rs = 1;                 // M = W_k^T: M[i][j] = W_k[j][i]
+      qa.cs = q;
+      qa.m = (int)q;
+      qa.c = (int)rk;
+      qa.Q = W[k];               // new core = Q^T (kk x q), i.e. Q column-major
+      qa.qrs = 1;
+      qa.qcs = q;
+      qa.R = G;                  // R (kk x rk)
+      if ((e = launch_qr(qa, s)) != cudaSuccess) break;
+      const long long m1 = r[k - 1] * n[k - 1];
+      // W_{k-1} (m1 x kk) = W_{k-1} (m1 x rk) . R^T  (B[k'][n'] = R[n'][k']: K-contiguous)
+      e = launch_gemm(true, true, gp(W[k - 1], rk, G, rk, Tmp, m1, kk, rk, tt::map_plain(kk),
+                                     tt::map_plain(1)), s);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(W[k - 1], Tmp, sizeof(double) * m1 * kk, cudaMemcpyDeviceToDevice, s);
+      r[k] = kk;
+      continue;
+    }
     g_stage = TT_ST_IL_S1;
     e = launch_gemm(true, true, gp(W[k], q, W[k], q, G, rk, rk, q, tt::map_plain(rk),
                                    tt::map_plain(1)), s);
@@ -281,6 +306,34 @@ static tt_status round_impl(int64_t d, const int64_t* n, const int64_t* r_in,
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(W[k - 1], Tmp, sizeof(double) * m1 * sk, cudaMemcpyDeviceToDevice, s);
     r[k] = sk;
+  }
+  // left orthonormalisation without truncation (tt_orthonormalise, phases bit 4): Householder
+  // QR W_k = Q R, W_k <- Q, W_{k+1} <- R W_{k+1}
+  for (int64_t k = 0; (phases & 4) && k < d - 1 && e == cudaSuccess; ++k) {
+    const long long m = r[k] * n[k], rk1 = r[k + 1];
+    if ((g_dbg_flags & (1 << 29)) || !qr_fits((int)m, (int)rk1)) {   // Gram route for this core
+      phases |= 2;
+      break;
+    }
+    const long long kk = std::min(m, rk1);
+    QrArgs qa{};
+    qa.M = W[k];
+    qa.rs = rk1;
+    qa.cs = 1;
+    qa.m = (int)m;
+    qa.c = (int)rk1;
+    qa.Q = W[k];   // Q (m x kk) row-major
+    qa.qrs = kk;
+    qa.qcs = 1;
+    qa.R = G;
+    if ((e = launch_qr(qa, s)) != cudaSuccess) break;
+    const long long q = n[k + 1] * r[k + 2];
+    // W_{k+1} (kk x q) = R (kk x rk1) . W_{k+1} (rk1 x q)
+    e = launch_gemm(true, false, gp(G, rk1, W[k + 1], q, Tmp, kk, q, rk1, tt::map_plain(q),
+                                    tt::map_plain(1)), s);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(W[k + 1], Tmp, sizeof(double) * kk * q, cudaMemcpyDeviceToDevice, s);
+    r[k + 1] = kk;
   }
   // left-to-right truncation with threshold delta / sqrt(d-1) ||T||
   double thr = 0.0;
@@ -356,7 +409,7 @@ tt_status tt_orthonormalise(int64_t d, const int64_t* n, const int64_t* r_in,
   if (direction != TT_SWEEP_LEFT && direction != TT_SWEEP_RIGHT)
     return fail(TT_ERR_INVALID_ARGUMENT, "direction must be TT_SWEEP_LEFT or TT_SWEEP_RIGHT");
   return round_impl(d, n, r_in, cores_in, 0.0, 0, r_out, cores_out, workspace, workspace_bytes,
-                    stream, direction == TT_SWEEP_LEFT ? 2 : 1, "tt_orthonormalise");
+                    stream, direction == TT_SWEEP_LEFT ? 4 : 1, "tt_orthonormalise");
 }
 
 // ---- block-index move ---------------------------------

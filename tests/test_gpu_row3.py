@@ -148,3 +148,51 @@ def test_block_move_errors(tt):
     # aliasing output/input
     assert tt.lib.tt_block_move_left(3, 4, 5, 4, 2, 2, 0.0, 0, p, p + 8, p, p + 24,
                                      ctypes.byref(s_out), None, 0, None) == 3
+
+
+@pytest.mark.parametrize("direction", ["left", "right"])
+def test_orthonormalise_exact_on_graded_cores(tt, direction):
+    """Householder QR (tt_qr.cuh): orthonormal to working precision and the represented tensor
+    unchanged even when every unfolding has singular values from 1 down to 1e-14 (the Gram
+    route squares that condition number: directions below ~1e-8 are lost)."""
+    rng = np.random.default_rng(77)
+    d, N = 6, 4
+    ranks = ttgen.capped_ranks(d, N, 16)
+    x = ttgen.gaussian_tt_vector(rng, N, ranks)
+    for k in range(d):   # grade both bonds of every core
+        x[k] = x[k] * np.logspace(0, -14, x[k].shape[2])[None, None, :]
+        x[k] = x[k] * np.logspace(0, -7, x[k].shape[0])[:, None, None]
+    flag = tt.TT_SWEEP_LEFT if direction == "left" else tt.TT_SWEEP_RIGHT
+    out = [h(c) for c in tt.tt_orthonormalise([g(c) for c in x], flag)]
+    v, vg = full_vector(x), full_vector(out)
+    assert rel_fro(vg, v) <= 1e-12
+    ks = range(d - 1) if direction == "left" else range(1, d)
+    for k in ks:
+        c = out[k]
+        M = c.reshape(-1, c.shape[2]) if direction == "left" else c.reshape(c.shape[0], -1).T
+        assert np.abs(M.T @ M - np.eye(M.shape[1])).max() <= 1e-13
+
+
+@pytest.mark.parametrize("shape", [(1024, 256), (256, 256), (64, 256), (1000, 37), (5, 3), (33, 64)])
+def test_cluster_qr_vs_gram_route(tt, shape):
+    """The QR path against the Gram route (debug bit 29) on one two-core train whose first
+    unfolding has the given shape: same represented tensor, both orthonormal."""
+    m, c = shape
+    rng = np.random.default_rng(m + c)
+    n0 = 4
+    r0 = max(1, m // n0)
+    x = [rng.standard_normal((1, n0, r0)), rng.standard_normal((r0, n0, c)) / np.sqrt(r0 * n0),
+         rng.standard_normal((c, n0, 1))]
+    x[0] = x[0] / np.linalg.norm(x[0])
+    outs = []
+    for flags in (0, 1 << 29):
+        tt.tt_debug_set_flags(flags)
+        try:
+            outs.append([h(t) for t in tt.tt_orthonormalise([g(t) for t in x], tt.TT_SWEEP_LEFT)])
+        finally:
+            tt.tt_debug_set_flags(0)
+    for out in outs:
+        assert rel_fro(full_vector(out), full_vector(x)) <= 1e-11
+        M = out[1].reshape(-1, out[1].shape[2])
+        assert np.abs(M.T @ M - np.eye(M.shape[1])).max() <= 1e-12
+    assert rel_fro(full_vector(outs[0]), full_vector(outs[1])) <= 1e-11
