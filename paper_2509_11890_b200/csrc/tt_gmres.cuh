@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(NT) gmres_orth_cluster_kernel(
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank(), ncl = (int)cluster.num_blocks();
   extern __shared__ double wseg[];   // this CTA's segment of w
-  __shared__ double partA[LMAX], partB[LMAX], partC[1];
+  __shared__ double inA[16][LMAX], inB[16][LMAX], inC[16][1];   // partials pushed by every CTA
   __shared__ double h1[LMAX], h2[LMAX], wn2;
   __shared__ double red[NT / 32][LMAX + 1];
   __shared__ double sh_scale;
@@ -255,8 +255,10 @@ __global__ void __launch_bounds__(NT) gmres_orth_cluster_kernel(
   const long long s0 = rank * per, s1 = min(S, s0 + per);
   const int nseg = (int)max(0LL, s1 - s0);
 
-  // block-reduce acc[0..n) -> part[0..n) (thread l writes part[l])
-  auto block_reduce = [&](double (&acc)[LMAX + 1], int n, double* part) {
+  // block-reduce acc[0..n), then thread l pushes the CTA's partial l into slot [rank][l] of
+  // EVERY CTA's inbox (remote DSMEM stores, nothing to wait for); after one cluster barrier
+  // each CTA sums its inbox locally in rank order (identical, deterministic in every CTA)
+  auto block_reduce = [&](double (&acc)[LMAX + 1], int n, double* inbox, int ldi) {
 #pragma unroll
     for (int l = 0; l < LMAX; ++l) {
       if (l >= n) break;
@@ -268,20 +270,14 @@ __global__ void __launch_bounds__(NT) gmres_orth_cluster_kernel(
     if (tid < n) {
       double v = 0.0;
       for (int q = 0; q < NT / 32; ++q) v += red[q][tid];
-      part[tid] = v;
+      for (int r = 0; r < ncl; ++r) cluster.map_shared_rank(inbox, r)[rank * ldi + tid] = v;
     }
   };
-  // h[l] = sum over the cluster's CTAs (rank order) of part[l]: identical in every CTA
-  auto combine = [&](double* part, double* h, int n) {
+  auto combine = [&](const double* inbox, int ldi, double* h, int n) {
     cluster.sync();
     if (tid < n) {
-      double pv[16];   // all remote loads in flight, then the rank-order sum
-#pragma unroll
-      for (int r = 0; r < 16; ++r) pv[r] = r < ncl ? cluster.map_shared_rank(part, r)[tid] : 0.0;
       double v = 0.0;
-#pragma unroll
-      for (int r = 0; r < 16; ++r)
-        if (r < ncl) v += pv[r];
+      for (int r = 0; r < ncl; ++r) v += inbox[r * ldi + tid];
       h[tid] = v;
     }
     __syncthreads();
@@ -304,8 +300,8 @@ __global__ void __launch_bounds__(NT) gmres_orth_cluster_kernel(
           acc[l] = fma(v1, w1, fma(v0, w0, acc[l]));
         }
     }
-    block_reduce(acc, L, partA);
-    combine(partA, h1, L);
+    block_reduce(acc, L, &inA[0][0], LMAX);
+    combine(&inA[0][0], LMAX, h1, L);
     // pass 2: w -= V h1, h2 = V^T w (one read of V)
 #pragma unroll
     for (int l = 0; l < LMAX; ++l) acc[l] = 0.0;
@@ -332,8 +328,8 @@ __global__ void __launch_bounds__(NT) gmres_orth_cluster_kernel(
       wseg[t0] = w0;
       if (ok1) wseg[t1] = w1;
     }
-    block_reduce(acc, L, partB);
-    combine(partB, h2, L);
+    block_reduce(acc, L, &inB[0][0], LMAX);
+    combine(&inB[0][0], LMAX, h2, L);
     // pass 3: w -= V h2, ||w||^2
     acc[0] = 0.0;
     for (int t0 = tid; t0 < nseg; t0 += U * NT) {
@@ -357,8 +353,8 @@ __global__ void __launch_bounds__(NT) gmres_orth_cluster_kernel(
       wseg[t0] = w0;
       if (ok1) wseg[t1] = w1;
     }
-    block_reduce(acc, 1, partC);
-    combine(partC, &wn2, 1);
+    block_reduce(acc, 1, &inC[0][0], 1);
+    combine(&inC[0][0], 1, &wn2, 1);
     if (rank == 0 && tid == 0) {   // the Hessenberg column, Givens rotations, convergence
       double scale = 0.0;
       if (st.active[0]) {
