@@ -409,7 +409,8 @@ cudaError_t orth_launch_t(const GmresState& st, const double* V, double* W, doub
   const size_t smem_max = sizeof(double) * (size_t)((kOrthMaxS + 7) / 8);   // w segment, 8 CTAs
   if (cl == 0) {
     cl = 8;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
+        smem_attr((const void*)kern, (int)smem_max) == cudaSuccess) {
       cudaLaunchConfig_t q = {};
       q.gridDim = dim3(16);
       q.blockDim = dim3(NT);
