@@ -51,7 +51,8 @@ void tt_debug_set_variant(int v);
  * step as separate kernels instead of the fused cluster kernel, bit 28 runs the small boundary
  * interface updates of the sweeps as three stage GEMMs each instead of fused one-CTA runs, bit 29
  * the orthonormalisation steps of tt_round / tt_orthonormalise through the Gram matrix instead
- * of the cluster Householder QR.
+ * of the cluster Householder QR, bit 27 the operator apply with the register-blocked kernel instead
+ * of the operator-stationary row-block kernel.
  * tt_debug_set_variant(v): v >= 10 forces
  * the GEMM tile configuration v % 100 (probe list in csrc/tt_launch_tpl.cuh) and split-K factor v / 100. */
 void tt_debug_set_flags(int flags);

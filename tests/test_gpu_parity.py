@@ -798,3 +798,25 @@ def test_operator_core_stage_resident_b(tt, shape, flags):
     ref = oracle.local_matvec_batched(phiL, A, phiR, X)
     for m in range(nvec):
         assert rel(h(Y)[:, :, m, :], ref[:, :, m, :]) <= TOL
+
+
+@pytest.mark.parametrize("idx", [1, 3, 5])
+def test_apply_register_blocked_path(tt, idx):
+    """The register-blocked apply kernel (debug bit 27) against the default row-block kernel and
+    the oracle (config 5: cores 0-3 and 11 in full, which cover both kernels' boundary cases)."""
+    import oracle
+    import ttgen
+    inp = ttgen.make_inputs(idx)
+    x = [g(c) for c in inp.x]
+    A = [g(c) for c in inp.A]
+    ks = range(len(x)) if idx != 5 else [0, 1, 2, 3, len(x) - 1]
+    zd = tt.tt_operator_apply(x, A)
+    tt.tt_debug_set_flags(1 << 27)
+    try:
+        zr = tt.tt_operator_apply(x, A)
+        torch.cuda.synchronize()
+    finally:
+        tt.tt_debug_set_flags(0)
+    for k in ks:
+        assert torch.equal(zd[k], zr[k])   # same FMA order per output: bit-identical
+        assert rel(h(zr[k]), oracle.apply_core(inp.x[k], inp.A[k])) <= TOL

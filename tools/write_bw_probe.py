@@ -43,3 +43,9 @@ p = tt.prepare(tt.tt_operator_apply, x, A, z)
 ms = t(lambda: p())
 nb = sum(v.numel() * 8 for v in z) + sum(v.numel() * 8 for v in x) + sum(v.numel() * 8 for v in A)
 print(f"apply config 5: {ms:.3f} ms, {nb / ms / 1e6:.0f} GB/s")
+for flags, name in [(0, "default: row-block kernel"), (1 << 27, "register-blocked kernel (debug bit 27)")]:
+    tt.tt_debug_set_flags(flags)
+    p = tt.prepare(tt.tt_operator_apply, x, A, z)
+    ms = t(lambda: p())
+    print(f"apply config 5 [{name}]: {ms:.3f} ms, {nb / ms / 1e6:.0f} GB/s", flush=True)
+tt.tt_debug_set_flags(0)
