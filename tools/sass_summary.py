@@ -24,6 +24,7 @@ for line in res.splitlines():
 pats = collections.OrderedDict([
     ("DMMA", r"\bDMMA\."), ("HMMA/UTC", r"\b(HMMA|UTCHMMA|UTCQMMA)"), ("UTMALDG", r"\bUTMALDG"),
     ("UBLKCP", r"\bUBLKCP"), ("LDGSTS", r"\bLDGSTS"), ("LDS", r"\bLDS\b|\bLDS\."),
+    ("LDS.128", r"\bLDS\.128"), ("LDSM", r"\bLDSM"),
     ("STS", r"\bSTS\b|\bSTS\."), ("LDG", r"\bLDG\."), ("STG", r"\bSTG\."), ("STG.256", r"STG\.E[^ ]*\.256"),
     ("DFMA", r"\bDFMA\b"), ("SYNCS", r"\bSYNCS\."), ("BAR", r"\bBAR\."), ("ATOM/RED", r"\b(ATOMG|RED)\."),
 ])
