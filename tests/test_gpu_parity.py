@@ -779,8 +779,8 @@ def test_latency_policy_w34_vs_default_policy(tt, idx):
 # the small-GEMM latency path (S2 = 2 x 262144 x 144 x 144 = 10.9 GFLOP > 10 GFLOP) with a
 # ragged last tile.
 @pytest.mark.timeout(300)
-@pytest.mark.parametrize("flags", [0, 33554432])
-@pytest.mark.parametrize("shape", [(64, 4, 64, 36, 36, 64), (60, 4, 68, 25, 36, 88)])
+@pytest.mark.parametrize("flags", [0, 33554432 | 8192])   # bit 13 (8192): no latency policy, so
+@pytest.mark.parametrize("shape", [(64, 4, 64, 36, 36, 64), (60, 4, 68, 25, 36, 88)])   # B_RES runs
 def test_operator_core_stage_resident_b(tt, shape, flags):
     import oracle
     rl, n, rr, Rl, Rr, nvec = shape
