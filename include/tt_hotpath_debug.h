@@ -47,7 +47,8 @@ void tt_debug_set_variant(int v);
  * operator-core / first matvec stages (bit 21: 2 x 6 warps), bit 23 runs tt_sweep_w34's
  * matvecs as three stages instead of reusing the left updates' T2_k, bit 25 runs the
  * operator-core stage with the whole A-hat resident in shared memory (3-deep T1 ring;
- * measured slower, kept as a probe), bit 26 runs tt_local_gmres's K = 1 orthogonalisation
+ * measured slower, kept as a probe), bit 24 forces tt_round's accurate truncation route
+ * (Householder QR + cluster one-sided Jacobi SVD, otherwise used for delta / sqrt(d-1) < 1e-7), bit 26 runs tt_local_gmres's K = 1 orthogonalisation
  * step as separate kernels instead of the fused cluster kernel, bit 28 runs the small boundary
  * interface updates of the sweeps as three stage GEMMs each instead of fused one-CTA runs, bit 29
  * the orthonormalisation steps of tt_round / tt_orthonormalise through the Gram matrix instead
@@ -65,6 +66,13 @@ void tt_debug_set_dag(int mode);
  * smid} (%globaltimer ns).  Copies the last DAG's per-task first-unit table into unit0 (host,
  * cap_tasks entries, + total) and returns (tasks << 32) | units of the last DAG launch. */
 int64_t tt_debug_dag_trace(void* buf, int64_t cap_units, int32_t* unit0, int64_t cap_tasks);
+
+/* Test hook: one-sided Jacobi SVD of a rows x c row-major matrix B (rows, c <= 256) in one
+ * thread-block cluster (csrc/tt_qr.cuh): BJ = B J (rows x c, columns u_j sigma_j, unsorted),
+ * J (c x c orthogonal), sigma (c), *sweeps (int32, device) the Jacobi sweeps run.  Device
+ * pointers, asynchronous. */
+tt_status tt_debug_svd(int64_t rows, int64_t c, const double* B, double* BJ, double* J,
+                       double* sigma, int32_t* sweeps, void* stream);
 
 #ifdef __cplusplus
 }

@@ -30,7 +30,7 @@ __all__ = [
     "tt_local_gmres_workspace_size",
     "tt_local_matvec_two_site", "tt_local_matvec_two_site_workspace_size",
     "tt_block_local_matvec", "tt_block_local_matvec_workspace_size", "TTBlockTerm",
-    "tt_round", "tt_round_workspace_size", "tt_debug_sym_eigen",
+    "tt_round", "tt_round_workspace_size", "tt_debug_sym_eigen", "tt_debug_svd",
     "tt_local_lobpcg", "tt_local_lobpcg_workspace_size", "tt_merge_operator_cores",
     "tt_orthonormalise", "tt_orthonormalise_workspace_size", "tt_block_move_right",
     "tt_block_move_left", "tt_block_move_workspace_size", "tt_pg_workspace_size",
@@ -87,6 +87,8 @@ lib.tt_round.argtypes = [_i64, _p, _p, _p, ctypes.c_double, _i64, _p, _p, _p, _s
 lib.tt_round.restype = ctypes.c_int
 lib.tt_debug_sym_eigen.argtypes = [_i64, _p, _p, _p, _p, _sz, _p]
 lib.tt_debug_sym_eigen.restype = ctypes.c_int
+lib.tt_debug_svd.argtypes = [_i64, _i64, _p, _p, _p, _p, _p, _p]
+lib.tt_debug_svd.restype = ctypes.c_int
 lib.tt_block_local_matvec_workspace_size.restype = _sz
 lib.tt_block_local_matvec_workspace_size.argtypes = [_i64] * 4 + [_p, _p]
 lib.tt_block_local_matvec.argtypes = [_i64] * 5 + [_p] * 5 + [_i64, _p, _p, _p, _p, _sz, _p]
@@ -964,6 +966,20 @@ def tt_enrich_right(x_k, z_k, x_k1, delta=0.0, max_rank=0, workspace=None, strea
 def tt_round_workspace_size(n, r) -> int:
     a64 = lambda v: (ctypes.c_int64 * len(v))(*v)
     return int(lib.tt_round_workspace_size(len(n), a64(n), a64(r)))
+
+
+def tt_debug_svd(B, stream=None):
+    """Test hook: one-sided Jacobi SVD of B (rows x c, <= 256) in one thread-block cluster.
+    Returns (BJ, J, sigma, sweeps) with B J = BJ (columns u_j sigma_j, unsorted)."""
+    rows, c = B.shape
+    Bc = B.contiguous()
+    BJ = torch.empty_like(Bc)
+    J = torch.empty((c, c), dtype=torch.float64, device=B.device)
+    sig = torch.empty(c, dtype=torch.float64, device=B.device)
+    sw = torch.zeros(1, dtype=torch.int32, device=B.device)
+    _check(lib.tt_debug_svd(rows, c, _dev(Bc, "B"), _dev(BJ, "BJ"), _dev(J, "J"), _dev(sig, "sigma"),
+                            sw.data_ptr(), _stream(stream)))
+    return BJ, J, sig, sw
 
 
 def tt_debug_sym_eigen(G, stream=None):

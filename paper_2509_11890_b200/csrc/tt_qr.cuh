@@ -225,3 +225,189 @@ inline cudaError_t launch_qr(const QrArgs& a0, cudaStream_t s) {
   ++g_launches;
   return e;
 }
+
+// ---- one-sided (Hestenes) Jacobi SVD of a small rows x c matrix in one cluster ------------------
+// B = R of the core's QR (rows = min(m, c) <= 256, c <= 256).  Columns are owned by the CTAs
+// (cpb consecutive columns each) and stay there; in every round-robin step each column meets one
+// partner, and BOTH owners compute the pair's rotation from the same canonical sums
+// (alpha_p = ||b_p||^2, alpha_q = ||b_q||^2, gamma = b_p . b_q, p < q, identical code and
+// summation order, so identical bits), each updating only its own column of B and of the
+// accumulated rotation J; the partner's columns are read through distributed shared memory from
+// the previous step's buffer (double-buffered, one cluster barrier per step).  Relative accuracy
+// of the singular values does not depend on the condition number (Demmel & Veselic 1992): there
+// is no squared-condition floor.  Output: B J (columns u_j sigma_j), J, sigma_j = ||(B J)_j||.
+constexpr int kSvdMaxC = 256, kSvdMaxRows = 256, kSvdMaxSweeps = 60;
+struct SvdArgs {
+  const double* B;   // rows x c, row-major (bt = 0) or column-major (bt = 1)
+  int rows, c, cpb;  // columns per CTA
+  int bt;
+  double* BJ;        // rows x c row-major (output)
+  double* J;         // c x c row-major (output)
+  double* sigma;     // c (output)
+  int* sweeps;       // (output) sweeps run
+};
+
+__global__ void __launch_bounds__(kQrThreads) svd_jacobi_cluster_kernel(const SvdArgs p) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank(), ncl = (int)cluster.num_blocks();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int kWarps = kQrThreads / 32;
+  const int rows = p.rows, c = p.c, cpb = p.cpb, P = (c + 1) & ~1;
+  extern __shared__ double ssm[];
+  // [2 buffers][cpb columns][rows] of B, then of J (columns contiguous)
+  double* Bb = ssm;
+  double* Jb = Bb + 2 * (size_t)cpb * rows;
+  int* partner = reinterpret_cast<int*>(Jb + 2 * (size_t)cpb * c);   // [P]
+  __shared__ double offmax[16];
+  __shared__ double sweep_off;
+  const int j0 = rank * cpb;
+  const int nown = max(0, min(cpb, c - j0));
+  for (int e = tid; e < nown * rows; e += kQrThreads) {
+    const int lj = e / rows, i = e - lj * rows;
+    Bb[lj * rows + i] = p.bt ? p.B[(long long)(j0 + lj) * rows + i] : p.B[(long long)i * c + j0 + lj];
+  }
+  for (int e = tid; e < nown * c; e += kQrThreads) {
+    const int lj = e / c, i = e - lj * c;
+    Jb[lj * c + i] = (i == j0 + lj) ? 1.0 : 0.0;
+  }
+  cluster.sync();
+  const double tol = 1e-15 * rows;
+  int cur = 0, sw = 0;
+  for (; sw < kSvdMaxSweeps; ++sw) {
+    double my_off = 0.0;
+    for (int step = 0; step < P - 1; ++step) {
+      for (int k = tid; k < P / 2; k += kQrThreads) {   // the step's pairs (chess tournament)
+        int a = (k == 0) ? 0 : 1 + (k - 1 + step) % (P - 1);
+        int b = 1 + (P - 2 - k + step) % (P - 1);
+        partner[a] = b;
+        partner[b] = a;
+      }
+      __syncthreads();
+      const double* Bc = Bb + (size_t)cur * cpb * rows;
+      const double* Jc = Jb + (size_t)cur * cpb * c;
+      double* Bn = Bb + (size_t)(cur ^ 1) * cpb * rows;
+      double* Jn = Jb + (size_t)(cur ^ 1) * cpb * c;
+      for (int lj = warp; lj < nown; lj += kWarps) {
+        const int j = j0 + lj, q = partner[j];
+        const double* bj = Bc + lj * rows;
+        const double* jj = Jc + lj * c;
+        if (q >= c) {   // dummy partner (odd c): unchanged
+          for (int i = lane; i < rows; i += 32) Bn[lj * rows + i] = bj[i];
+          for (int i = lane; i < c; i += 32) Jn[lj * c + i] = jj[i];
+          continue;
+        }
+        const int oq = q / cpb, lq = q - oq * cpb;
+        const double* bq = cluster.map_shared_rank(Bb, oq) + (size_t)cur * cpb * rows + lq * rows;
+        const double* jq = cluster.map_shared_rank(Jb, oq) + (size_t)cur * cpb * c + lq * c;
+        const bool lo = j < q;   // canonical pair (p, q) = (min, max)
+        const double* bp_ = lo ? bj : bq;
+        const double* bq_ = lo ? bq : bj;
+        double sp = 0.0, sq = 0.0, g = 0.0;
+        for (int i = lane; i < rows; i += 32) {
+          const double x = bp_[i], y = bq_[i];
+          sp = fma(x, x, sp);
+          sq = fma(y, y, sq);
+          g = fma(x, y, g);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+          sp += __shfl_xor_sync(0xffffffffu, sp, o);
+          sq += __shfl_xor_sync(0xffffffffu, sq, o);
+          g += __shfl_xor_sync(0xffffffffu, g, o);
+        }
+        double cs = 1.0, sn = 0.0;
+        const double den = sqrt(sp * sq);
+        if (den > 0.0 && fabs(g) > tol * den) {
+          my_off = fmax(my_off, fabs(g) / den);
+          const double zeta = (sq - sp) / (2.0 * g);
+          const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+          cs = 1.0 / sqrt(fma(t, t, 1.0));
+          sn = cs * t;
+        }
+        // [b_p', b_q'] = [b_p, b_q] [[cs, sn], [-sn, cs]]
+        for (int i = lane; i < rows; i += 32) {
+          const double x = lo ? bj[i] : bq[i], y = lo ? bq[i] : bj[i];
+          Bn[lj * rows + i] = lo ? fma(-sn, y, cs * x) : fma(sn, x, cs * y);
+        }
+        for (int i = lane; i < c; i += 32) {
+          const double x = lo ? jj[i] : jq[i], y = lo ? jq[i] : jj[i];
+          Jn[lj * c + i] = lo ? fma(-sn, y, cs * x) : fma(sn, x, cs * y);
+        }
+      }
+      cluster.sync();   // every read of the cur buffers is done; nxt is complete
+      cur ^= 1;
+    }
+    // convergence: the largest rotated pair of the sweep, over the cluster (rank order)
+    for (int o = 16; o > 0; o >>= 1) my_off = fmax(my_off, __shfl_xor_sync(0xffffffffu, my_off, o));
+    __shared__ double wmax[kQrThreads / 32];
+    if (lane == 0) wmax[warp] = my_off;
+    __syncthreads();
+    if (tid == 0) {
+      double mx = 0.0;
+      for (int w = 0; w < kWarps; ++w) mx = fmax(mx, wmax[w]);
+      for (int r = 0; r < ncl; ++r) cluster.map_shared_rank(offmax, r)[rank] = mx;
+    }
+    cluster.sync();
+    if (tid == 0) {
+      double mx = 0.0;
+      for (int r = 0; r < ncl; ++r) mx = fmax(mx, offmax[r]);
+      sweep_off = mx;
+    }
+    __syncthreads();
+    if (sweep_off == 0.0) break;   // no rotation in the whole sweep: converged
+  }
+  const double* Bc = Bb + (size_t)cur * cpb * rows;
+  const double* Jc = Jb + (size_t)cur * cpb * c;
+  for (int lj = warp; lj < nown; lj += kWarps) {
+    double s = 0.0;
+    for (int i = lane; i < rows; i += 32) s = fma(Bc[lj * rows + i], Bc[lj * rows + i], s);
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) p.sigma[j0 + lj] = sqrt(s);
+  }
+  for (int e = tid; e < nown * rows; e += kQrThreads) {
+    const int lj = e / rows, i = e - lj * rows;
+    p.BJ[(long long)i * c + j0 + lj] = Bc[lj * rows + i];
+  }
+  for (int e = tid; e < nown * c; e += kQrThreads) {
+    const int lj = e / c, i = e - lj * c;
+    p.J[(long long)i * c + j0 + lj] = Jc[lj * c + i];
+  }
+  if (rank == 0 && tid == 0 && p.sweeps) *p.sweeps = sw;
+  cluster.sync();
+}
+
+inline size_t svd_smem(int rows, int c, int cpb) {
+  return sizeof(double) * (size_t)(2 * cpb * rows + 2 * cpb * c) + sizeof(int) * (size_t)(c + 2);
+}
+inline bool svd_fits(int rows, int c) {
+  if (rows <= 0 || c <= 0 || rows > kSvdMaxRows || c > kSvdMaxC) return false;
+  const int cl = qr_cluster_size(rows, c);
+  const int cpb = (c + cl - 1) / cl;
+  return svd_smem(rows, c, cpb) <= kQrSmemMax;
+}
+inline cudaError_t launch_svd(SvdArgs a, cudaStream_t s) {
+  const int cl = qr_cluster_size(a.rows, a.c);
+  a.cpb = (a.c + cl - 1) / cl;
+  const size_t smem = svd_smem(a.rows, a.c, a.cpb);
+  if (smem > kQrSmemMax) return cudaErrorInvalidValue;
+  if (cudaError_t e = smem_attr((const void*)svd_jacobi_cluster_kernel, (int)kQrSmemMax)) return e;
+  cudaFuncSetAttribute(svd_jacobi_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cl);
+  cfg.blockDim = dim3(kQrThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  g_stage = TT_ST_SET;
+  const long long tr = trace_begin(-5, a.rows, a.c, 0, s);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, svd_jacobi_cluster_kernel, a);
+  trace_end(tr, s);
+  ++g_launches;
+  return e;
+}

@@ -191,6 +191,23 @@ size_t tt_round_workspace_size(int64_t d, const int64_t* n, const int64_t* r) {
 
 // phases: bit 0 = right-to-left orthonormalisation, bit 1 = left-to-right truncation
 // (delta = 0, max_rank = 0: plain left-to-right orthonormalisation)
+// the selected singular triplets of the accurate truncation (cluster Jacobi SVD of R):
+// Usel[r][i] = BJ[r][perm[i]] / sigma[perm[i]] (kk x sk), SJt[i][col] = sigma[perm[i]] J[col][perm[i]]
+__global__ void svd_select_kernel(const double* __restrict__ BJ, const double* __restrict__ J,
+                                  const int* __restrict__ perm, int kk, int rk1, int sk,
+                                  double* __restrict__ Usel, double* __restrict__ SJt) {
+  // R^T J = BJ (columns U_R sigma) => R = J BJ^T: left vectors J, sigma-scaled right vectors BJ
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < kk * sk) {
+    const int r = e / sk, i = e - r * sk;
+    Usel[e] = J[(long long)r * kk + perm[i]];
+  }
+  if (e < sk * rk1) {
+    const int i = e / rk1, col = e - i * rk1;
+    SJt[e] = BJ[(long long)col * kk + perm[i]];
+  }
+}
+
 static tt_status round_impl(int64_t d, const int64_t* n, const int64_t* r_in,
                             const double* const* cores_in, double delta, int64_t max_rank,
                             int64_t* r_out, double* const* cores_out, void* workspace,
@@ -337,7 +354,90 @@ static tt_status round_impl(int64_t d, const int64_t* n, const int64_t* r_in,
   }
   // left-to-right truncation with threshold delta / sqrt(d-1) ||T||
   double thr = 0.0;
-  for (int64_t k = 0; (phases & 2) && k < d - 1 && e == cudaSuccess; ++k) {
+  // Accurate route (Householder QR + one-sided Jacobi SVD of R^T, no squared-condition floor;
+  // Jacobi on R^T rather than R converges in ~8 sweeps at any condition, as in LAPACK's
+  // preconditioned dgejsv, where R's own columns need 11-26+ growing with the condition)
+  // where the Gram route's floor (singular values below ~1e-8 sigma_max unresolved) reaches the
+  // per-core threshold: delta / sqrt(d-1) < 1e-7, delta = 0 included; debug bit 24 forces it.
+  const bool accurate = (phases & 2) &&
+      ((g_dbg_flags & (1 << 24)) || delta / std::sqrt((double)std::max<int64_t>(d - 1, 1)) < 1e-7);
+  int64_t kstart = 0;   // the Gram route continues from the first core the accurate one left
+  for (int64_t k = 0; accurate && k < d - 1 && e == cudaSuccess; ++k) {
+    const long long m = r[k] * n[k], rk1 = r[k + 1], kk = std::min(m, rk1);
+    if (!qr_fits((int)m, (int)rk1) || !svd_fits((int)rk1, (int)kk)) break;   // Gram from here
+    QrArgs qa{};
+    qa.M = W[k];
+    qa.rs = rk1;
+    qa.cs = 1;
+    qa.m = (int)m;
+    qa.c = (int)rk1;
+    qa.Q = W[k];   // Q (m x kk) row-major
+    qa.qrs = kk;
+    qa.qcs = 1;
+    qa.R = G;      // R (kk x rk1)
+    if ((e = launch_qr(qa, s)) != cudaSuccess) break;
+    SvdArgs sa{};
+    sa.B = G;      // R (kk x rk1) row-major = R^T (rk1 x kk) column-major
+    sa.bt = 1;
+    sa.rows = (int)rk1;
+    sa.c = (int)kk;
+    sa.BJ = Bm;    // R^T J (rk1 x kk)
+    sa.J = V;      // J (kk x kk)
+    sa.sigma = lam;
+    sa.sweeps = nullptr;
+    if ((e = launch_svd(sa, s)) != cudaSuccess) break;
+    std::vector<double> sg(kk);
+    if ((e = cudaMemcpyAsync(sg.data(), lam, sizeof(double) * kk, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+        (e = cudaStreamSynchronize(s)) != cudaSuccess)
+      break;
+    std::vector<int> perm(kk);
+    for (int i = 0; i < (int)kk; ++i) perm[i] = i;
+    std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return sg[a] > sg[b]; });
+    if (k == 0) {
+      double nrm2 = 0.0;
+      for (long long i = 0; i < kk; ++i) nrm2 += sg[i] * sg[i];
+      thr = delta / std::sqrt((double)std::max<int64_t>(d - 1, 1)) * std::sqrt(nrm2);
+    }
+    // numerical zeros: sigma <= rk1 eps sigma_max (the QR's backward error)
+    const double smax = sg[perm[0]];
+    int nz = 0;
+    for (long long i = 0; i < kk; ++i)
+      if (sg[perm[i]] > (double)rk1 * 1.1e-16 * smax) ++nz;
+    if (nz == 0) nz = 1;
+    int sk = nz;
+    double tail = 0.0;
+    for (int i = nz - 1; i >= 1; --i) {
+      tail += sg[perm[i]] * sg[perm[i]];
+      if (std::sqrt(tail) <= thr) sk = i; else break;
+    }
+    if (max_rank > 0 && sk > max_rank) sk = (int)max_rank;
+    // Usel (kk x sk) = J[:, perm], SJt (sk x rk1) = (R^T J)[:, perm]^T = sigma U_R^T
+    double* Usel = esc;
+    double* SJt = esc + rmax * rmax;
+    int* dperm = reinterpret_cast<int*>(esc + 2 * rmax * rmax);
+    if ((e = cudaMemcpyAsync(dperm, perm.data(), sizeof(int) * sk, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+      break;
+    const long long nsel = std::max(kk, rk1) * sk;
+    svd_select_kernel<<<(unsigned)((nsel + 255) / 256), 256, 0, s>>>(Bm, V, dperm, (int)kk,
+                                                                      (int)rk1, sk, Usel, SJt);
+    ++g_launches;
+    if ((e = cudaGetLastError()) != cudaSuccess) break;
+    // new core (m x sk) = Q (m x kk) . Usel
+    e = launch_gemm(true, false, gp(W[k], kk, Usel, sk, Tmp, m, sk, kk, tt::map_plain(sk),
+                                    tt::map_plain(1)), s);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(W[k], Tmp, sizeof(double) * m * sk, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) break;
+    // W_{k+1} (sk x q) = SJt (sk x rk1) . W_{k+1} (rk1 x q)
+    const long long q = n[k + 1] * r[k + 2];
+    e = launch_gemm(true, false, gp(SJt, rk1, W[k + 1], q, Tmp, sk, q, rk1, tt::map_plain(q),
+                                    tt::map_plain(1)), s);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(W[k + 1], Tmp, sizeof(double) * sk * q, cudaMemcpyDeviceToDevice, s);
+    r[k + 1] = sk;
+    kstart = k + 1;
+  }
+  for (int64_t k = kstart; (phases & 2) && k < d - 1 && e == cudaSuccess; ++k) {
     const long long m = r[k] * n[k], rk1 = r[k + 1];
     g_stage = TT_ST_IL_S2;
     e = launch_gemm(false, false, gp(W[k], rk1, W[k], rk1, G, rk1, rk1, m, tt::map_plain(rk1),
@@ -410,6 +510,25 @@ tt_status tt_orthonormalise(int64_t d, const int64_t* n, const int64_t* r_in,
     return fail(TT_ERR_INVALID_ARGUMENT, "direction must be TT_SWEEP_LEFT or TT_SWEEP_RIGHT");
   return round_impl(d, n, r_in, cores_in, 0.0, 0, r_out, cores_out, workspace, workspace_bytes,
                     stream, direction == TT_SWEEP_LEFT ? 4 : 1, "tt_orthonormalise");
+}
+
+tt_status tt_debug_svd(int64_t rows, int64_t c, const double* B, double* BJ, double* J,
+                       double* sigma, int32_t* sweeps, void* stream) {
+  CallScope scope;
+  if (rows <= 0 || c <= 0) return fail(TT_ERR_INVALID_ARGUMENT, "extents must be positive");
+  if (!B || !BJ || !J || !sigma) return fail(TT_ERR_NULL_POINTER, "NULL pointer");
+  if (!svd_fits((int)rows, (int)c)) return fail(TT_ERR_INVALID_ARGUMENT, "rows, c <= 256");
+  SvdArgs a{};
+  a.B = B;
+  a.rows = (int)rows;
+  a.c = (int)c;
+  a.BJ = BJ;
+  a.J = J;
+  a.sigma = sigma;
+  a.sweeps = reinterpret_cast<int*>(sweeps);
+  cudaError_t e = launch_svd(a, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "tt_debug_svd");
+  return TT_OK;
 }
 
 // ---- block-index move ---------------------------------

@@ -196,3 +196,63 @@ def test_cluster_qr_vs_gram_route(tt, shape):
         M = out[1].reshape(-1, out[1].shape[2])
         assert np.abs(M.T @ M - np.eye(M.shape[1])).max() <= 1e-12
     assert rel_fro(full_vector(outs[0]), full_vector(outs[1])) <= 1e-11
+
+
+@pytest.mark.parametrize("rows,c,kappa,pre", [
+    (256, 256, 1e2, False), (256, 256, 1e2, True), (256, 256, 1e14, True), (64, 200, 1e10, True),
+    (37, 37, 1e15, True), (256, 100, 1e12, True), (256, 100, 1e6, False), (5, 3, 1e3, False)])
+def test_cluster_jacobi_svd_relative_accuracy(tt, rows, c, kappa, pre):
+    """One-sided Jacobi (tt_qr.cuh): B J has orthogonal columns, J is orthogonal, B = BJ J^T, and
+    the singular values are relatively accurate even at condition 1e14-1e15 (the Gram route
+    resolves nothing below ~1e-8 of the largest).  B = U diag(s) V^T with known s; with `pre`,
+    B is replaced by R^T of B's QR (same singular values) as tt_round's accurate route does:
+    there Jacobi converges in a few sweeps at any condition (on B itself the count grows with
+    the condition, 11 -> 26 sweeps from 1e2 to 1e14 for n = 64 in a numpy model of the order)."""
+    rng = np.random.default_rng(rows * 7 + c)
+    k = min(rows, c)
+    s = np.logspace(0, -np.log10(kappa), k)
+    U = np.linalg.qr(rng.standard_normal((rows, k)))[0]
+    V = np.linalg.qr(rng.standard_normal((c, k)))[0]
+    B = (U * s) @ V.T
+    if pre:
+        B = np.ascontiguousarray(np.linalg.qr(B)[1].T)
+        rows, c = B.shape
+    BJ, J, sig, sw = tt.tt_debug_svd(g(B))
+    BJ, J, sig = h(BJ), h(J), h(sig)
+    assert int(h(sw)[0]) <= (12 if pre else 40)
+    # J is ~c * sweeps rotations per column, each within eps of orthogonal
+    assert np.abs(J.T @ J - np.eye(c)).max() <= max(1e-13, 1e-15 * c)
+    assert np.linalg.norm(BJ @ J.T - B) <= 1e-14 * np.linalg.norm(B) * max(rows, c)
+    got = np.sort(sig)[::-1][:k]
+    # the exact singular values of the rounded B are s up to the representation error of B
+    # (~eps ||B||): relative accuracy for every sigma above ~1e3 eps sigma_max
+    big = s > 1e3 * np.finfo(float).eps * s[0]
+    assert np.all(np.abs(got[big] - s[big]) <= 1e-8 * s[big] + 1e2 * np.finfo(float).eps * s[0])
+
+
+@pytest.mark.parametrize("delta", [0.0, 1e-9, 1e-2])
+def test_tt_round_accurate_route(tt, delta):
+    """tt_round's accurate truncation (QR + cluster Jacobi SVD; automatic for delta / sqrt(d-1)
+    < 1e-7, forced at 1e-2 by debug bit 24): on a train whose unfoldings are graded down to
+    1e-13, delta = 0 reconstructs to 1e-12 (the Gram route drops everything below ~1e-7), and
+    the error bound ||T - round(T)|| <= delta ||T|| holds with ranks equal to the oracle's."""
+    from oracle.rounding import tt_round as oracle_round
+    rng = np.random.default_rng(91)
+    d, N = 6, 4
+    x = ttgen.gaussian_tt_vector(rng, N, ttgen.capped_ranks(d, N, 12))
+    for k in range(d):
+        x[k] = x[k] * np.logspace(0, -13, x[k].shape[2])[None, None, :]
+    flags = (1 << 24) if delta >= 1e-7 else 0
+    tt.tt_debug_set_flags(flags)
+    try:
+        out = [h(c) for c in tt.tt_round([g(c) for c in x], delta)]
+    finally:
+        tt.tt_debug_set_flags(0)
+    v, vg = full_vector(x), full_vector(out)
+    err = rel_fro(vg, v)
+    if delta == 0.0:
+        assert err <= 1e-12
+    else:
+        assert err <= delta * (1 + 1e-6)
+        ref = oracle_round(x, delta)
+        assert [c.shape for c in out] == [c.shape for c in ref]
