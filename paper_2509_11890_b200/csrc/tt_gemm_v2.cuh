@@ -356,21 +356,55 @@ dmma_gemm_v2_kernel(const GemmParamsV2 p) {
   cp_async_wait<0>();
 }
 
-// C[rowmap(m) + colmap(n)] = sum_s P[s][m][n]  (split-K reduction, fixed summation order)
+// C[rowmap(m) + colmap(n)] = sum_s P[s][m][n]  (split-K reduction, fixed summation order).
+// Streaming: the partials are read once (evict-first), two adjacent columns per thread when N
+// is even (16-byte loads; one 16-byte store where the column map keeps the pair adjacent and
+// aligned), the row/column split by a host-built magic divisor instead of a 64-bit division.
 static __global__ void __launch_bounds__(256) splitk_reduce_kernel(const double* __restrict__ P,
                                                             double* __restrict__ C, int M, int N,
                                                             int ksplit, IndexMap32 rowmap,
-                                                            IndexMap32 colmap,
+                                                            IndexMap32 colmap, FastDiv ndiv,
                                                             const int* gate) {
   pdl_wait();
   if (gate && *gate) return;
   const long long MN = (long long)M * N;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < MN;
-       e += (long long)gridDim.x * blockDim.x) {
-    double s = P[e];
-    for (int q = 1; q < ksplit; ++q) s += P[q * MN + e];
-    const int m = (int)(e / N), n = (int)(e - (long long)m * N);
-    stg_cs(C + apply_map32(rowmap, (uint32_t)m) + apply_map32(colmap, (uint32_t)n), s);
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  if ((N & 1) == 0 && MN < (1LL << 31) && !(reinterpret_cast<uintptr_t>(P) & 15)) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; 2 * t < MN; t += stride) {
+      const uint32_t e = (uint32_t)(2 * t);
+      double2 acc = __ldcs(reinterpret_cast<const double2*>(P + e));
+      int q = 1;
+      for (; q + 1 < ksplit; q += 2) {
+        const double2 v0 = __ldcs(reinterpret_cast<const double2*>(P + (long long)q * MN + e));
+        const double2 v1 = __ldcs(reinterpret_cast<const double2*>(P + (long long)(q + 1) * MN + e));
+        acc.x += v0.x;
+        acc.y += v0.y;
+        acc.x += v1.x;
+        acc.y += v1.y;
+      }
+      if (q < ksplit) {
+        const double2 v0 = __ldcs(reinterpret_cast<const double2*>(P + (long long)q * MN + e));
+        acc.x += v0.x;
+        acc.y += v0.y;
+      }
+      const uint32_t m = fdiv(e, ndiv), n = e - m * (uint32_t)N;
+      double* row = C + apply_map32(rowmap, m);
+      const long long c0 = apply_map32(colmap, n), c1 = apply_map32(colmap, n + 1);
+      double* d0 = row + c0;
+      if (c1 == c0 + 1 && !(reinterpret_cast<uintptr_t>(d0) & 15)) {
+        asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};\n" ::"l"(d0), "d"(acc.x), "d"(acc.y));
+      } else {
+        stg_cs(d0, acc.x);
+        stg_cs(row + c1, acc.y);
+      }
+    }
+  } else {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < MN; e += stride) {
+      double sum = P[e];
+      for (int q = 1; q < ksplit; ++q) sum += P[q * MN + e];
+      const int m = (int)(e / N), n = (int)(e - (long long)m * N);
+      stg_cs(C + apply_map32(rowmap, (uint32_t)m) + apply_map32(colmap, (uint32_t)n), sum);
+    }
   }
   pdl_trigger();
 }

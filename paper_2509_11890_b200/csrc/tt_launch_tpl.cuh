@@ -130,12 +130,13 @@ cudaError_t launch_v2_cfg(const GemmParams& p0, cudaStream_t s) {
     return e;
   if (ks > 1) {
     const long long mn = p0.M * p0.N;
-    long long blocks = (mn + 255) / 256;
+    long long blocks = (mn / 2 + 255) / 256;   // two columns per thread
     if (blocks > 8L * num_sms()) blocks = 8L * num_sms();
+    if (blocks < 1) blocks = 1;
     if (cudaError_t e = launch_pdl(2.0 * p0.M * p0.N * p0.K <= pdl_flops(), tt::splitk_reduce_kernel,
                                    dim3((unsigned)blocks), dim3(256), 0,
                                    s, (const double*)p.P, p.C, p.M, p.N, ks, p.rowmap, p.colmap,
-                                   p.gate))
+                                   tt::make_fastdiv((uint32_t)p.N), p.gate))
       return e;
     ++g_launches;
   }
@@ -290,12 +291,13 @@ cudaError_t launch_v3_cfg(const GemmParams& p0, cudaStream_t s, bool& ok) {
     return e;
   if (ks > 1) {
     const long long mn = p0.M * p0.N;
-    long long blocks = (mn + 255) / 256;
+    long long blocks = (mn / 2 + 255) / 256;   // two columns per thread
     if (blocks > 8L * num_sms()) blocks = 8L * num_sms();
+    if (blocks < 1) blocks = 1;
     if (cudaError_t e = launch_pdl(2.0 * p0.M * p0.N * p0.K <= pdl_flops(), tt::splitk_reduce_kernel,
                                    dim3((unsigned)blocks), dim3(256), 0,
                                    s, (const double*)p.P, p.C, p.M, p.N, ks, p.rowmap, p.colmap,
-                                   p.gate))
+                                   tt::make_fastdiv((uint32_t)p.N), p.gate))
       return e;
     ++g_launches;
   }

@@ -61,21 +61,13 @@ LobDims lob_dims(const Dims& d, long long nb) {
   return L;
 }
 
-// W = AX - BX diag(lam)
-__global__ void lob_resid_kernel(const double* __restrict__ AX, const double* __restrict__ BX,
-                                 const double* __restrict__ lam, double* __restrict__ W,
-                                 long long S, int nb, int rr, const int* __restrict__ gate) {
-  if (gate && *gate) return;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < S;
-       e += (long long)gridDim.x * blockDim.x)
-    W[e] = fma(-lam[(e / rr) % nb], BX[e], AX[e]);
-}
-
+// Residual and column norms in one pass: W = AX - BX diag(lam) is written, and
 // part[(t*nb + j)*chunks + c] = sum over chunk c of the squared entries of column j of block t
 // (t < 3: W, AX, BX).  Grid (chunks, nb).
-__global__ void __launch_bounds__(256) lob_colnorm_kernel(const double* __restrict__ B0,
-                                                          const double* __restrict__ B1,
-                                                          const double* __restrict__ B2,
+__global__ void __launch_bounds__(256) lob_colnorm_kernel(double* __restrict__ W,
+                                                          const double* __restrict__ AX,
+                                                          const double* __restrict__ BX,
+                                                          const double* __restrict__ lam,
                                                           long long rows, int nb, int rr,
                                                           long long rows_per_chunk,
                                                           double* __restrict__ part,
@@ -83,10 +75,13 @@ __global__ void __launch_bounds__(256) lob_colnorm_kernel(const double* __restri
   if (gate && *gate) return;
   const int c = blockIdx.x, j = blockIdx.y, chunks = gridDim.x;
   const long long r0 = c * rows_per_chunk, r1 = min(rows, r0 + rows_per_chunk);
+  const double lj = lam[j];
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
   for (long long t = threadIdx.x; t < (r1 - r0) * rr; t += blockDim.x) {
     const long long e = ((r0 + t / rr) * nb + j) * rr + (t % rr);
-    const double x0 = B0[e], x1 = B1[e], x2 = B2[e];
+    const double x1 = AX[e], x2 = BX[e];
+    const double x0 = fma(-lj, x2, x1);
+    W[e] = x0;
     a0 = fma(x0, x0, a0);
     a1 = fma(x1, x1, a1);
     a2 = fma(x2, x2, a2);
@@ -120,20 +115,27 @@ struct LobState {
   double* step;     // optional: min(1, 1 / lam_0) if lam_0 > 0 else 1
 };
 
-// Residual norms -> relative residuals, the normalisation of W, convergence; one block.
-__global__ void lob_check_kernel(const double* __restrict__ part, int chunks, int nb,
-                                 LobState st, double tol, int final_pass) {
+// Residual norms -> relative residuals, the normalisation of W, convergence; one block of
+// 1024 threads: warp w sums the chunk partials of (array, column) pairs w, w + 32, ... (lanes
+// over chunks, a fixed shuffle tree: deterministic), then the first nb threads finish.
+__global__ void __launch_bounds__(1024) lob_check_kernel(const double* __restrict__ part, int chunks,
+                                                         int nb, LobState st, double tol,
+                                                         int final_pass) {
   if (!final_pass && *st.done) return;
+  __shared__ double sums[3 * kLobMaxNb];
   __shared__ double rmax[kLobMaxNb];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int q = warp; q < 3 * nb; q += nw) {
+    double v = 0.0;
+    for (int c = lane; c < chunks; c += 32) v += part[(long long)q * chunks + c];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) sums[q] = v;
+  }
+  __syncthreads();
   const int j = threadIdx.x;
   double rel = 0.0;
   if (j < nb) {
-    double w = 0.0, a = 0.0, b = 0.0;
-    for (int c = 0; c < chunks; ++c) {
-      w += part[((long long)0 * nb + j) * chunks + c];
-      a += part[((long long)1 * nb + j) * chunks + c];
-      b += part[((long long)2 * nb + j) * chunks + c];
-    }
+    const double w = sums[j], a = sums[nb + j], b = sums[2 * nb + j];
     const double wn = sqrt(w), den = sqrt(a) + fabs(st.lam[j]) * sqrt(b);
     rel = den > 0.0 ? wn / den : 0.0;
     st.res[j] = rel;
@@ -152,14 +154,6 @@ __global__ void lob_check_kernel(const double* __restrict__ part, int chunks, in
   }
 }
 
-__global__ void lob_colscale_kernel(double* __restrict__ W, const double* __restrict__ sc,
-                                    long long S, int nb, int rr, const int* __restrict__ gate) {
-  if (gate && *gate) return;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < S;
-       e += (long long)gridDim.x * blockDim.x)
-    W[e] *= sc[(e / rr) % nb];
-}
-
 // Gram partial sums: part[c][p][m] = sum over the contraction indices k = (row, b) of chunk c
 // of U_{p / nb}[row, p % nb, b] * V_{m / nb}[row, m % nb, b],  p < nu nb, m < nv nb.
 struct GramArgs {
@@ -168,6 +162,8 @@ struct GramArgs {
   int nu, nv, nb, rr;
   long long kt, k_per_chunk;
   const int* gate;
+  tt::FastDiv rrdiv;   // k -> (row, b) with 32-bit magic division when kt < 2^31 (k32)
+  int k32;
 };
 
 // Thread layout: G = 256 / (TU TV) groups split the 32 contraction indices of a staged chunk;
@@ -220,7 +216,15 @@ __global__ void __launch_bounds__(256) lob_gram_kernel(const GramArgs g, double*
   auto stage_chunk = [&](long long kb, double* buf) {
     const long long k = kb + bb_t;
     const bool in = k < k1;
-    const long long off = in ? (k / g.rr) * (long long)g.nb * g.rr + (k % g.rr) : 0;
+    long long off = 0;
+    if (in) {
+      if (g.k32) {   // the division of every staged index is the kernel's largest cost otherwise
+        const uint32_t row = tt::fdiv((uint32_t)k, g.rrdiv);
+        off = (long long)row * g.nb * g.rr + ((uint32_t)k - row * (uint32_t)g.rr);
+      } else {
+        off = (k / g.rr) * (long long)g.nb * g.rr + (k % g.rr);
+      }
+    }
     for (int r = r_t; r < su + sv; r += 8) {
       double* dst = (r < su ? buf + r * LD : buf + su * LD + (r - su) * LD) + bb_t;
       tt::cp_async8(dst, rptr[r] + off, in);
@@ -294,12 +298,20 @@ __global__ void lob_gram_finish_kernel(const double* __restrict__ part, int chun
 // Cyclic parallel Jacobi on a symmetric np x np matrix (np even) in shared memory, one CTA:
 // round-robin pairs, rotation angles from the current matrix, then J^T M J applied in 2x2
 // blocks (each block owns its four entries, so the update is in place) and V <- V J.
+// The step is latency-bound (one dependent chain per step: pair -> angle -> update ->
+// barrier), so the chain is kept short: the round-robin pair of a step needs no division
+// (one conditional subtraction), the angle is t = sgn(d) e / (|d| + hypot(d, e)) with
+// d = a_qq - a_pp, e = 2 a_pq (one sqrt, one division, one rsqrt instead of three divisions
+// and two square roots), the rotation flag is a plain store, and every thread walks its
+// update items with incremental indices (no integer division inside the step loop).
 __device__ void lob_jacobi_cta(double* M, double* V, int np, double* cs, double* sn, int* pp,
                                int* qq, double* red) {
-  const int tid = threadIdx.x, nt = blockDim.x, h = np / 2;
+  const int tid = threadIdx.x, nt = blockDim.x, h = np / 2, n1 = np - 1;
   __shared__ int nrot;
   for (int e = tid; e < np * np; e += nt) V[e] = (e / np == e % np) ? 1.0 : 0.0;
   if (tid == 0) nrot = 1;
+  // first update items of this thread and the stride between its items, as (row, col) pairs
+  const int m_r0 = tid / h, m_c0 = tid - m_r0 * h, st_r = nt / h, st_c = nt - st_r * h;
   __syncthreads();
   for (int sw = 0; sw < 60; ++sw) {
     // a sweep that applied no rotation (every off-diagonal entry negligible against its
@@ -326,50 +338,67 @@ __device__ void lob_jacobi_cta(double* M, double* V, int np, double* cs, double*
     }
     __syncthreads();
     if (!(offs > 1e-30 * dias)) break;   // also stops on an all-zero matrix
+    // an entry is negligible below 1e-15 sqrt(|a_pp a_qq|) (the classical threshold: relative
+    // accuracy) or below 1e-17 ||M||_F (rounding noise of the matrix itself)
+    const double floor_abs = 1e-17 * sqrt(offs + dias);
     if (tid == 0) nrot = 0;
     __syncthreads();
-    for (int step = 0; step < np - 1; ++step) {
+    for (int step = 0; step < n1; ++step) {
       for (int k = tid; k < h; k += nt) {
-        int a = (k == 0) ? 0 : 1 + (k - 1 + step) % (np - 1);
-        int b = 1 + (np - 2 - k + step) % (np - 1);
+        int a = 0, b;
+        if (k > 0) {
+          a = k - 1 + step;
+          if (a >= n1) a -= n1;
+          a += 1;
+        }
+        b = n1 - 1 - k + step;
+        if (b >= n1) b -= n1;
+        b += 1;
         if (a > b) { const int t = a; a = b; b = t; }
         pp[k] = a;
         qq[k] = b;
         double c = 1.0, s = 0.0;
         const double apq = M[a * np + b], app = M[a * np + a], aqq = M[b * np + b];
-        if (fabs(apq) > 1e-18 * sqrt(fabs(app * aqq))) {
-          const double tau = (aqq - app) / (2.0 * apq);
-          const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+        if (apq * apq > 1e-30 * fabs(app * aqq) && fabs(apq) > floor_abs) {
+          const double d = aqq - app, e2 = 2.0 * apq;
+          const double r = sqrt(fma(d, d, e2 * e2));
+          const double t = (d >= 0.0 ? e2 : -e2) / (fabs(d) + r);
           if (t != 0.0) {
-            c = 1.0 / sqrt(1.0 + t * t);
+            c = rsqrt(fma(t, t, 1.0));
             s = t * c;
-            atomicAdd(&nrot, 1);
+            nrot = 1;
           }
         }
         cs[k] = c;
         sn[k] = s;
       }
       __syncthreads();
-      for (int e = tid; e < h * h; e += nt) {
-        const int kr = e / h, kc = e - kr * h;
+      for (int kr = m_r0, kc = m_c0; kr < h;) {
         const int p = pp[kr], q = qq[kr], u = pp[kc], w = qq[kc];
         const double cr = cs[kr], sr = sn[kr], cc = cs[kc], sc = sn[kc];
-        if (sr == 0.0 && sc == 0.0) continue;
-        const double mpu = M[p * np + u], mpw = M[p * np + w];
-        const double mqu = M[q * np + u], mqw = M[q * np + w];
-        const double rpu = cr * mpu - sr * mqu, rpw = cr * mpw - sr * mqw;
-        const double rqu = sr * mpu + cr * mqu, rqw = sr * mpw + cr * mqw;
-        M[p * np + u] = cc * rpu - sc * rpw;
-        M[p * np + w] = sc * rpu + cc * rpw;
-        M[q * np + u] = cc * rqu - sc * rqw;
-        M[q * np + w] = sc * rqu + cc * rqw;
+        if (sr != 0.0 || sc != 0.0) {
+          const double mpu = M[p * np + u], mpw = M[p * np + w];
+          const double mqu = M[q * np + u], mqw = M[q * np + w];
+          const double rpu = cr * mpu - sr * mqu, rpw = cr * mpw - sr * mqw;
+          const double rqu = sr * mpu + cr * mqu, rqw = sr * mpw + cr * mqw;
+          M[p * np + u] = cc * rpu - sc * rpw;
+          M[p * np + w] = sc * rpu + cc * rpw;
+          M[q * np + u] = cc * rqu - sc * rqw;
+          M[q * np + w] = sc * rqu + cc * rqw;
+        }
+        kr += st_r;
+        kc += st_c;
+        if (kc >= h) { kc -= h; ++kr; }
       }
-      for (int e = tid; e < np * h; e += nt) {
-        const int i = e / h, kc = e - i * h;
+      // V <- V J: items (row i, pair kc) over np x h, the same incremental walk
+      for (int i = m_r0, kc = m_c0; i < np;) {
         const int u = pp[kc], w = qq[kc];
         const double vu = V[i * np + u], vw = V[i * np + w];
         V[i * np + u] = cs[kc] * vu - sn[kc] * vw;
         V[i * np + w] = sn[kc] * vu + cs[kc] * vw;
+        i += st_r;
+        kc += st_c;
+        if (kc >= h) { kc -= h; ++i; }
       }
       __syncthreads();
     }
@@ -680,6 +709,8 @@ __global__ void __launch_bounds__(256) lob_rr_kernel(const double* __restrict__ 
 // Linear combinations: for every family f (X, AX, BX images) and position (row, b):
 //   Xn_f[row, m, b] = sum_q sum_p S_f,q[row, p, b] Y[q nb + p, m]     (q over X, W, P)
 //   Pn_f[row, m, b] = sum_q sum_p S_f,q[row, p, b] Yp[q nb + p, m]    (if Yp)
+// In place (Xn_f = S_f,0, Pn_f = S_f,2): a thread reads every S_f,q[row, :, b] of its (row, b)
+// positions before it writes Xn_f / Pn_f there, and no other thread touches them.
 struct CombineArgs {
   const double* S[3][3];
   double* Xn[3];
@@ -717,7 +748,9 @@ __global__ void __launch_bounds__(128) lob_combine_kernel(const CombineArgs a) {
         for (int t = 0; t < TB; ++t) ax[m][t] = ap[m][t] = 0.0;
       for (int q = 0; q < a.nblk; ++q) {
         const double* src = a.S[f][q] + row * nb * a.rr + b;
-        for (int p = 0; p < nb; ++p) {
+#pragma unroll
+        for (int p = 0; p < NBT; ++p) {
+          if (p >= nb) break;
           double v[TB];
           if (TB == 2) {
             const double2 w = *reinterpret_cast<const double2*>(src + (long long)p * a.rr);
@@ -759,53 +792,55 @@ __global__ void __launch_bounds__(128) lob_combine_kernel(const CombineArgs a) {
   }
 }
 
-// W[row, m, b] -= sum_p X[row, p, b] C[p, m]   (in place; one thread per (row, b))
+// W[row, m, b] -= sum_p X[row, p, b] C[p, m]   (in place; one thread per (row, b)).  NBT: a
+// compile-time bound on nb, so the loads of a thread's nb values are unrolled and independent.
+// With sc != nullptr the result columns are then scaled: W[:, m, :] *= sc[m] (the residual
+// normalisation folded into the first pass: (W - X C) D = W D - X (C D)).
+template <int NBT>
 __global__ void __launch_bounds__(128) lob_orth_kernel(const double* __restrict__ X,
                                                        const double* __restrict__ C,
                                                        double* __restrict__ W, long long rows,
-                                                       int nb, int rr, const int* __restrict__ gate) {
+                                                       int nb, int rr, const double* __restrict__ sc,
+                                                       const int* __restrict__ gate) {
   if (gate && *gate) return;
-  __shared__ double Cs[kLobMaxNb * kLobMaxNb];
-  for (int i = threadIdx.x; i < nb * nb; i += blockDim.x) Cs[i] = C[i];
+  __shared__ double Cs[NBT * NBT];
+  __shared__ double Ds[NBT];
+  for (int i = threadIdx.x; i < NBT * NBT; i += blockDim.x) {
+    const int p = i / NBT, m = i - p * NBT;
+    Cs[i] = (p < nb && m < nb) ? C[p * nb + m] : 0.0;
+  }
+  for (int i = threadIdx.x; i < NBT; i += blockDim.x) Ds[i] = (sc && i < nb) ? sc[i] : 1.0;
   __syncthreads();
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < rows * rr;
        e += (long long)gridDim.x * blockDim.x) {
     const long long row = e / rr, b = e - row * rr;
     const double* x = X + row * nb * rr + b;
     double* w = W + row * nb * rr + b;
-    double acc[kLobMaxNb];
+    double xv[NBT], acc[NBT];
 #pragma unroll
-    for (int m = 0; m < kLobMaxNb; ++m) acc[m] = 0.0;
-    for (int p = 0; p < nb; ++p) {
-      const double v = x[(long long)p * rr];
+    for (int p = 0; p < NBT; ++p) xv[p] = p < nb ? x[(long long)p * rr] : 0.0;
 #pragma unroll
-      for (int m = 0; m < kLobMaxNb; ++m)
-        if (m < nb) acc[m] = fma(v, Cs[p * nb + m], acc[m]);
-    }
+    for (int m = 0; m < NBT; ++m) acc[m] = m < nb ? w[(long long)m * rr] : 0.0;
 #pragma unroll
-    for (int m = 0; m < kLobMaxNb; ++m)
-      if (m < nb) w[(long long)m * rr] -= acc[m];
+    for (int p = 0; p < NBT; ++p)
+#pragma unroll
+      for (int m = 0; m < NBT; ++m) acc[m] = fma(-xv[p], Cs[p * NBT + m], acc[m]);
+#pragma unroll
+    for (int m = 0; m < NBT; ++m)
+      if (m < nb) w[(long long)m * rr] = acc[m] * Ds[m];
   }
-}
-
-__global__ void lob_copy_kernel(const double* __restrict__ src, double* __restrict__ dst,
-                                long long S, const int* __restrict__ gate) {
-  if (gate && *gate) return;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < S;
-       e += (long long)gridDim.x * blockDim.x)
-    dst[e] = src[e];
 }
 
 // workspace element counts beyond the matvec's (T1, T2, Pp shared; one Ahat per operator)
 struct LobWs {
-  long long blocks;   // 14 blocks of S: AX BX W AW BW P AP BP + 6 combination temporaries
+  long long blocks;   // 8 blocks of S: AX BX W AW BW P AP BP (the combination is in place)
   long long part, gpart, G, Y, small;
 };
 
 bool lob_ws_elems(const Dims& d, long long nb, LobWs& w) {
   bool ok = true;
   const long long S = prod({d.a, d.n, nb, d.b}, ok);
-  w.blocks = prod({14, S}, ok);
+  w.blocks = prod({8, S}, ok);
   const LobDims L = lob_dims(d, nb);
   const long long s = 3 * nb;
   w.part = 3 * nb * (long long)L.chunks;
@@ -870,12 +905,6 @@ cudaError_t enqueue_lobpcg(const Dims& dA, const Dims& dB, bool has_B, long long
   double* P = blk + 5 * S;
   double* AP = blk + 6 * S;
   double* BP = blk + 7 * S;
-  double* nX = blk + 8 * S;   // temporaries of the combination
-  double* nAX = blk + 9 * S;
-  double* nBX = blk + 10 * S;
-  double* nP = blk + 11 * S;
-  double* nAP = blk + 12 * S;
-  double* nBP = blk + 13 * S;
   if (!has_B) {   // B = I: the B images are the blocks themselves
     BX = X;
     BW = W;
@@ -923,8 +952,13 @@ cudaError_t enqueue_lobpcg(const Dims& dA, const Dims& dB, bool has_B, long long
     ga.kt = L.rows * L.rr;
     ga.k_per_chunk = L.k_per_gchunk;
     ga.gate = gate;
+    ga.k32 = ga.kt < (1LL << 31) ? 1 : 0;
+    ga.rrdiv = tt::make_fastdiv((uint32_t)L.rr);
     const int su = nu * (int)nb, sv = nv * (int)nb;
-    if (su <= 12 && sv <= 24) {
+    if (su <= 8 && sv <= 8) {   // the orthogonalisation Gram X^T B W: 8 x 8 exactly, 32 groups
+      using C = GramCfg<4, 2, 2, 4>;
+      lob_gram_kernel<4, 2, 2, 4><<<L.gchunks, 256, C::smem(su, sv), s>>>(ga, gpart);
+    } else if (su <= 12 && sv <= 24) {
       using C = GramCfg<4, 4, 3, 6>;
       lob_gram_kernel<4, 4, 3, 6><<<L.gchunks, 256, C::smem(su, sv), s>>>(ga, gpart);
     } else if (su <= 24 && sv <= 48) {
@@ -963,8 +997,8 @@ cudaError_t enqueue_lobpcg(const Dims& dA, const Dims& dB, bool has_B, long long
   auto combine = [&](int nblk) -> cudaError_t {
     CombineArgs ca;
     const double* fam[3][3] = {{X, W, P}, {AX, AW, AP}, {BX, BW, BP}};
-    double* xn[3] = {nX, nAX, nBX};
-    double* pn[3] = {nP, nAP, nBP};
+    double* xn[3] = {X, AX, BX};   // in place (lob_combine_kernel)
+    double* pn[3] = {P, AP, BP};
     ca.nfam = has_B ? 3 : 2;
     for (int f = 0; f < 3; ++f) {
       for (int q = 0; q < 3; ++q) ca.S[f][q] = fam[f][q];
@@ -993,25 +1027,15 @@ cudaError_t enqueue_lobpcg(const Dims& dA, const Dims& dB, bool has_B, long long
     else lob_combine_kernel<32, 1><<<(unsigned)cb2, 128, smem, s>>>(ca);
 #undef LOB_COMBINE
     ++g_launches;
-    double* dst[6] = {X, AX, BX, P, AP, BP};
-    double* src[6] = {nX, nAX, nBX, nP, nAP, nBP};
-    for (int i = 0; i < 6; ++i) {
-      if (!has_B && (i == 2 || i == 5)) continue;
-      if (nblk == 1 && i >= 3) continue;
-      lob_copy_kernel<<<(unsigned)eb, 256, 0, s>>>(src[i], dst[i], S, gate);
-      ++g_launches;
-    }
     return cudaGetLastError();
   };
   auto check = [&](int final_pass) -> cudaError_t {
     const int* g2 = final_pass ? nullptr : gate;
-    lob_resid_kernel<<<(unsigned)eb, 256, 0, s>>>(AX, BX, lam, W, S, (int)nb, L.rr, g2);
-    ++g_launches;
     dim3 grid(L.chunks, (unsigned)nb);
-    lob_colnorm_kernel<<<grid, 256, 0, s>>>(W, AX, BX, L.rows, (int)nb, L.rr, L.rows_per_chunk,
-                                            part, g2);
+    lob_colnorm_kernel<<<grid, 256, 0, s>>>(W, AX, BX, lam, L.rows, (int)nb, L.rr,
+                                            L.rows_per_chunk, part, g2);
     ++g_launches;
-    lob_check_kernel<<<1, kLobMaxNb, 0, s>>>(part, L.chunks, (int)nb, st, tol, final_pass);
+    lob_check_kernel<<<1, 1024, 0, s>>>(part, L.chunks, (int)nb, st, tol, final_pass);
     ++g_launches;
     return cudaGetLastError();
   };
@@ -1026,13 +1050,15 @@ cudaError_t enqueue_lobpcg(const Dims& dA, const Dims& dB, bool has_B, long long
       if ((e = matvecs(P, AP, BP)) != cudaSuccess) return e;
     }
     if ((e = check(0)) != cudaSuccess) return e;
-    lob_colscale_kernel<<<(unsigned)eb, 256, 0, s>>>(W, st.scale, S, (int)nb, L.rr, gate);
-    ++g_launches;
-    for (int pass = 0; pass < 2; ++pass) {   // W <- W - X (B X)^T W, twice
+    for (int pass = 0; pass < 2; ++pass) {   // W <- W - X (B X)^T W, twice (pass 0 also scales)
       const double* U[1] = {BX};
       const double* V[1] = {W};
+      const double* scp = pass == 0 ? st.scale : nullptr;
       if ((e = gram(1, U, 1, V, Cw)) != cudaSuccess) return e;
-      lob_orth_kernel<<<(unsigned)cb, 128, 0, s>>>(X, Cw, W, L.rows, (int)nb, L.rr, gate);
+      if (nb <= 4) lob_orth_kernel<4><<<(unsigned)cb, 128, 0, s>>>(X, Cw, W, L.rows, (int)nb, L.rr, scp, gate);
+      else if (nb <= 8) lob_orth_kernel<8><<<(unsigned)cb, 128, 0, s>>>(X, Cw, W, L.rows, (int)nb, L.rr, scp, gate);
+      else if (nb <= 16) lob_orth_kernel<16><<<(unsigned)cb, 128, 0, s>>>(X, Cw, W, L.rows, (int)nb, L.rr, scp, gate);
+      else lob_orth_kernel<32><<<(unsigned)cb, 128, 0, s>>>(X, Cw, W, L.rows, (int)nb, L.rr, scp, gate);
       ++g_launches;
     }
     if ((e = matvecs(W, AW, BW)) != cudaSuccess) return e;

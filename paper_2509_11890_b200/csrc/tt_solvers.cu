@@ -834,7 +834,8 @@ size_t tt_block_local_matvec_workspace_size(int64_t rl, int64_t n, int64_t rr, i
   if (nops <= 0 || !Rl || !Rr) return 0;
   long long t1, t2, ah, pe, vec;
   if (!block_ws(rl, n, rr, nops, Rl, Rr, t1, t2, ah, pe, vec)) return 0;
-  return ws_bytes({t1, t2, ah, pe, vec, vec, vec});
+  // one matvec lane per pool stream: the terms' matvecs run concurrently
+  return (size_t)kPoolStreams * ws_bytes({t1, t2, ah, pe, vec, vec, vec});
 }
 
 tt_status tt_block_local_matvec(int64_t rl, int64_t n, int64_t rr, int64_t nblocks, int64_t nops,
@@ -865,43 +866,90 @@ tt_status tt_block_local_matvec(int64_t rl, int64_t n, int64_t rr, int64_t nbloc
   long long t1, t2, ah, pe, vec;
   if (!block_ws(rl, n, rr, nops, Rl, Rr, t1, t2, ah, pe, vec))
     return fail(TT_ERR_OVERFLOW, "workspace overflow");
-  const size_t need = ws_bytes({t1, t2, ah, pe, vec, vec, vec});
+  const size_t lane_b = ws_bytes({t1, t2, ah, pe, vec, vec, vec});
+  const size_t need = (size_t)kPoolStreams * lane_b;
   if (!workspace || workspace_bytes < need)
     return fail(TT_ERR_WORKSPACE, "workspace NULL or smaller than " + std::to_string(need) + " bytes");
-  Carver c{static_cast<char*>(workspace), workspace_bytes};
-  double* T1 = c.take(t1);
-  double* T2 = c.take(t2);
-  double* Ah = c.take(ah);
-  double* Pp = c.take(pe);
-  double* G = c.take(vec);
-  double* G2 = c.take(vec);
-  double* Tv = c.take(vec);
-  if (!c.ok) return fail(TT_ERR_WORKSPACE, "workspace too small after alignment");
+  // Terms are independent K = 1 matvecs (~12 GFLOP each at the config-5 interior core: stage
+  // GEMMs of 2.7-4.8 GFLOP that quantise badly on 148 SMs), so they run on up to kPoolStreams
+  // lanes concurrently, each with its own scratch; the accumulation Y[row] += coeff T_t stays
+  // in term order per row block (each scatter waits for the previous scatter into its row:
+  // deterministic and race-free).  Lanes are assigned greedily by cost (2 for a product term).
+  struct Lane {
+    double *T1, *T2, *Ah, *Pp, *G, *G2, *Tv;
+  };
+  const int lanes = (int)std::min<int64_t>(kPoolStreams, std::max<int64_t>(nterms, 1));
+  std::vector<Lane> L(size_t(lanes), Lane{});
+  for (int q = 0; q < lanes; ++q) {
+    Carver c{static_cast<char*>(workspace) + (size_t)q * lane_b, lane_b};
+    L[q].T1 = c.take(t1);
+    L[q].T2 = c.take(t2);
+    L[q].Ah = c.take(ah);
+    L[q].Pp = c.take(pe);
+    L[q].G = c.take(vec);
+    L[q].G2 = c.take(vec);
+    L[q].Tv = c.take(vec);
+    if (!c.ok) return fail(TT_ERR_WORKSPACE, "workspace too small after alignment");
+  }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const long long rows = rl * n;
   long long blocks = (vec + 255) / 256;
   if (blocks > 4L * num_sms()) blocks = 4L * num_sms();
   cudaError_t e = cudaMemsetAsync(Y, 0, sizeof(double) * rows * nblocks * rr, s);
-  for (int64_t t = 0; t < nterms && e == cudaSuccess; ++t) {
-    const tt_block_term& tm = terms[t];
-    gather_col_kernel<<<(unsigned)blocks, 256, 0, s>>>(X, G, rows, (int)nblocks, (int)rr,
-                                                       (int)tm.col);
+  if (e != cudaSuccess) return cuda_fail(e, "tt_block_local_matvec");
+  auto term = [&](const tt_block_term& tm, const Lane& ln, cudaStream_t ps) -> cudaError_t {
+    gather_col_kernel<<<(unsigned)blocks, 256, 0, ps>>>(X, ln.G, rows, (int)nblocks, (int)rr,
+                                                        (int)tm.col);
     ++g_launches;
-    const double* in = G;
+    const double* in = ln.G;
+    cudaError_t r = cudaSuccess;
     if (tm.op2 >= 0) {
       const Dims d2{rl, n, rr, Rl[tm.op2], Rr[tm.op2]};
-      e = enqueue_matvec(d2, 1, phiL[tm.op2], A[tm.op2], phiR[tm.op2], G, G2, T1, T2, Ah, Pp, pe, s);
-      in = G2;
+      r = enqueue_matvec(d2, 1, phiL[tm.op2], A[tm.op2], phiR[tm.op2], ln.G, ln.G2, ln.T1, ln.T2,
+                         ln.Ah, ln.Pp, pe, ps);
+      in = ln.G2;
     }
-    if (e != cudaSuccess) break;
+    if (r != cudaSuccess) return r;
     const Dims d1{rl, n, rr, Rl[tm.op], Rr[tm.op]};
-    e = enqueue_matvec(d1, 1, phiL[tm.op], A[tm.op], phiR[tm.op], in, Tv, T1, T2, Ah, Pp, pe, s);
-    if (e != cudaSuccess) break;
-    scatter_add_col_kernel<<<(unsigned)blocks, 256, 0, s>>>(Tv, Y, rows, (int)nblocks, (int)rr,
-                                                            (int)tm.row, tm.coeff);
+    return enqueue_matvec(d1, 1, phiL[tm.op], A[tm.op], phiR[tm.op], in, ln.Tv, ln.T1, ln.T2,
+                          ln.Ah, ln.Pp, pe, ps);
+  };
+  auto scatter = [&](const tt_block_term& tm, const Lane& ln, cudaStream_t ps) -> cudaError_t {
+    scatter_add_col_kernel<<<(unsigned)blocks, 256, 0, ps>>>(ln.Tv, Y, rows, (int)nblocks,
+                                                             (int)rr, (int)tm.row, tm.coeff);
     ++g_launches;
-    e = cudaGetLastError();
+    return cudaGetLastError();
+  };
+  if (lanes <= 1 || (g_dbg_flags & 8)) {   // one lane on the caller's stream (debug bit 3: A/B)
+    for (int64_t t = 0; t < nterms && e == cudaSuccess; ++t) {
+      e = term(terms[t], L[0], s);
+      if (e == cudaSuccess) e = scatter(terms[t], L[0], s);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "tt_block_local_matvec");
+    return TT_OK;
   }
+  if ((e = pool_init(size_t(nterms + kPoolStreams + 2))) != cudaSuccess) return cuda_fail(e, "pool");
+  cudaEvent_t* ev = g_res.pool.ev.data();   // ev[t]: term t's scatter done; ev[nterms + q]: joins
+  for (int q = 0; q < lanes && e == cudaSuccess; ++q) e = stream_dep(s, g_res.pool.s[q]);
+  std::vector<int> cost(size_t(lanes), 0);
+  std::vector<int64_t> last_in_row(size_t(nblocks), -1);
+  for (int64_t t = 0; t < nterms && e == cudaSuccess; ++t) {
+    const tt_block_term& tm = terms[t];
+    int q = 0;
+    for (int i = 1; i < lanes; ++i)
+      if (cost[size_t(i)] < cost[size_t(q)]) q = i;
+    cost[size_t(q)] += tm.op2 >= 0 ? 2 : 1;
+    cudaStream_t ps = g_res.pool.s[q];
+    if ((e = term(tm, L[size_t(q)], ps)) != cudaSuccess) break;
+    const int64_t prev = last_in_row[size_t(tm.row)];
+    if (prev >= 0 && (e = cudaStreamWaitEvent(ps, ev[prev], 0)) != cudaSuccess) break;
+    if ((e = scatter(tm, L[size_t(q)], ps)) != cudaSuccess) break;
+    if ((e = cudaEventRecord(ev[t], ps)) != cudaSuccess) break;
+    last_in_row[size_t(tm.row)] = t;
+  }
+  for (int q = 0; q < lanes && e == cudaSuccess; ++q)
+    if ((e = cudaEventRecord(ev[nterms + q], g_res.pool.s[q])) == cudaSuccess)
+      e = cudaStreamWaitEvent(s, ev[nterms + q], 0);
   if (e != cudaSuccess) return cuda_fail(e, "tt_block_local_matvec");
   return TT_OK;
 }
