@@ -61,6 +61,10 @@ void tt_debug_set_flags(int flags);
  * thread (one launch for the whole sweep, csrc/tt_dag.cuh): 0 = off (default: the stream/event
  * version, measured faster), 1 = on with 4-warp 64 x 64 tiles, 2 = 8-warp. */
 void tt_debug_set_dag(int mode);
+/* Benchmark / test hook: the fused S1 -> S2 matvec kernel (csrc/tt_fused12.cuh: T1 stays in
+ * shared memory) on the calling thread: 0 = policy (default), -1 = never, 1 = whenever the
+ * shape is eligible (warp-group skew 1 k-tile), 2 / 3 = eligible with skew 0 / 2. */
+void tt_debug_set_fused(int mode);
 /* Measurement hook: while buf != NULL (device, 5 x uint64 per unit, cap_units units) the next
  * DAG launches of the calling thread record per unit {grab, ready, computed, published,
  * smid} (%globaltimer ns).  Copies the last DAG's per-task first-unit table into unit0 (host,

@@ -186,6 +186,7 @@ void tt_debug_set_variant(int v) {
   g_force_ks = v >= 10 ? v / 100 : 0;
 }
 void tt_debug_set_dag(int mode) { g_dag_mode = mode; }
+void tt_debug_set_fused(int mode) { g_fused_mode = mode; }
 void tt_set_graph_cache(int enabled) {
   g_graph_cache_on = enabled ? 1 : 0;
   if (!enabled) graph_cache_clear();

@@ -162,6 +162,7 @@ tt_status graph_cached(GraphKey& key, cudaStream_t s, const std::function<tt_sta
   key.w.push_back((uint64_t)(uint32_t)g_variant);
   key.w.push_back((uint64_t)(uint32_t)g_force_v1);
   key.w.push_back((uint64_t)(uint32_t)g_dag_mode);
+  key.w.push_back((uint64_t)(uint32_t)g_fused_mode);
   key.w.push_back((uint64_t)(uint32_t)g_side_lowprio);
   key.w.push_back((uint64_t)(uint32_t)g_eigen_elementwise);
   auto& G = g_res.graphs;
@@ -556,6 +557,13 @@ cudaError_t enqueue_matvec(const Dims& d, long long K, const double* phiL, const
     Ah = const_cast<double*>(Ah_pre);
   else if ((e = launch_perm(true, A, Ah, al, N, be, s)) != cudaSuccess)
     return e;
+  // fused S1 -> S2 (tt_fused12.cuh): T1 stays in shared memory
+  if (fused12_wanted(d, K)) {
+    bool ok = false;
+    e = launch_fused12(d, K, phiL, Ah, X, T2, s, ok);
+    if (e != cudaSuccess) return e;
+    if (ok) return enqueue_matvec_last(d, K, T2, phiR, Y, P, pe, s);
+  }
   // S1: T1(al, j, a', m, b) = phiL[(a' al), a] . X[a, (j m b)]
   g_stage = TT_ST_MV_S1;
   e = launch_gemm(true, false,

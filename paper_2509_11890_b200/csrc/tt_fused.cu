@@ -1,0 +1,93 @@
+// tt_fused.cu — launcher of the fused S1 -> S2 matvec kernel (tt_fused12.cuh): eligibility,
+// the three tensor maps, unit count.  Called from enqueue_matvec (tt_core.cu).
+#include "tt_internal.cuh"
+#include "tt_launch_tpl.cuh"
+#include "tt_fused12.cuh"
+
+namespace ttint {
+
+// tt_debug_set_fused: 0 policy (default), -1 never, m > 0 whenever eligible with warp-group
+// skew {1, 0, 2}[(m - 1) % 3] k-tiles and option bits (m - 1) / 3 (tt_fused12.cuh)
+thread_local int g_fused_mode = 0;
+
+// 5-D FP64 view of the Krylov block X (a, j, m, b) for the phase-1 B operand: dims
+// {16 (b lo), a (k), b / 16 (b hi), 4 (j), K (m)}, box {16, 16, 1, 4, 1}: one TMA brings the
+// four swizzled 16 x 16 slabs (one per mode index j) of a k-tile.
+static bool make_map_x(CUtensorMap* m, const double* X, long long a, long long N, long long K,
+                       long long b) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[5] = {16u, (cuuint64_t)a, (cuuint64_t)(b / 16), (cuuint64_t)N, (cuuint64_t)K};
+  cuuint64_t strides[4] = {(cuuint64_t)(N * K * b * 8), 128u, (cuuint64_t)(K * b * 8),
+                           (cuuint64_t)(b * 8)};
+  cuuint32_t box[5] = {16u, 16u, 1u, (cuuint32_t)N, 1u};
+  cuuint32_t estr[5] = {1u, 1u, 1u, 1u, 1u};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double*>(X), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+bool fused12_shape_ok(const Dims& d, long long K) {
+  if (d.n != 4 || d.al > 36 || d.be > 36 || (4 * d.be) % 16 != 0) return false;
+  if (d.b % 16 != 0 || d.a % 2 != 0 || K <= 0) return false;
+  const long long units = ((d.a + 3) / 4) * (d.b / 16) * K;
+  return units > 0 && units < (1LL << 31) - 1024 && d.a * d.al < (1LL << 31) &&
+         d.a * K * 4 * d.be * d.b < (1LL << 62);
+}
+
+// policy: the fused kernel where the T1 round trip is the larger cost -- both bonds wide
+// enough that the three-stage path would stream T1 through HBM (it no longer fits in L2)
+bool fused12_wanted(const Dims& d, long long K) {
+  if (g_fused_mode < 0) return false;
+  if (!fused12_shape_ok(d, K)) return false;
+  if (g_fused_mode > 0) return true;
+  return false;   // policy default decided by measurement
+}
+
+cudaError_t launch_fused12(const Dims& d, long long K, const double* phiL, const double* Ah,
+                           const double* X, double* T2, cudaStream_t s, bool& ok) {
+  ok = false;
+  if (!fused12_shape_ok(d, K)) return cudaSuccess;
+  if (!aligned16(phiL) || !aligned16(Ah) || !aligned16(X) || !aligned16(T2)) return cudaSuccess;
+  CUtensorMap tl, tx, ta;
+  if (!make_map(&tl, phiL, d.a, d.a * d.al, d.a, 72)) return cudaSuccess;
+  if (!make_map_x(&tx, X, d.a, d.n, K, d.b)) return cudaSuccess;
+  if (!make_map3(&ta, Ah, d.n * d.be, d.al * d.n, d.n * d.be, 9)) return cudaSuccess;
+  ok = true;
+  if (cudaError_t e = smem_attr((const void*)tt::fused_s12_kernel, (int)tt::kF12SmemBytes)) return e;
+  tt::Fused12Params p;
+  p.T2 = T2;
+  p.a = (int)d.a;
+  p.b = (int)d.b;
+  p.al = (int)d.al;
+  p.be = (int)d.be;
+  p.K = (int)K;
+  p.nag = (int)((d.a + 3) / 4);
+  p.nbt = (int)(d.b / 16);
+  p.total_units = (int)((long long)p.nag * p.nbt * K);
+  p.KT1 = (int)((d.a + 15) / 16);
+  p.KT2 = (int)((4 * d.al + 15) / 16);
+  p.nag_div = tt::make_fastdiv((uint32_t)p.nag);
+  p.nbt_div = tt::make_fastdiv((uint32_t)p.nbt);
+  {
+    const int m = g_fused_mode > 0 ? g_fused_mode - 1 : 1;   // policy default: skew 0
+    const int sk[3] = {1, 0, 2};
+    p.skew = sk[m % 3];
+    p.opt = m / 3;
+  }
+  p.dbg = g_dbg_flags;
+  p.gate = g_gate;
+  const int grid = (int)std::min<long long>(p.total_units, num_sms());
+  g_stage = TT_ST_MV_S1;
+  // traced as one record with 2 M N K = the flops of both stages
+  const long long tr = trace_begin(-12, d.a * K * d.b, 4 * d.al, d.a + 4 * d.be, s);
+  if (cudaError_t e = launch_pdl(false, tt::fused_s12_kernel, dim3(grid), dim3(tt::kF12Threads),
+                                 tt::kF12SmemBytes, s, tl, tx, ta, p))
+    return e;
+  trace_end(tr, s);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+}  // namespace ttint

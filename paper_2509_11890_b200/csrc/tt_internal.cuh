@@ -270,6 +270,13 @@ cudaError_t enqueue_right_pg(const DimsPG& d, const double* phiR, const double* 
                              const double* xb, const double* xk, double* out, double* T1,
                              double* T2, double* At, double* P, long long pe, cudaStream_t s);
 
+// ---- fused S1 -> S2 matvec kernel (tt_fused.cu / tt_fused12.cuh) ---------------------------------
+extern thread_local int g_fused_mode;
+bool fused12_shape_ok(const Dims& d, long long K);
+bool fused12_wanted(const Dims& d, long long K);
+cudaError_t launch_fused12(const Dims& d, long long K, const double* phiL, const double* Ah,
+                           const double* X, double* T2, cudaStream_t s, bool& ok);
+
 // ---- symmetric eigensolver (tt_solvers.cu) ------------------------------------------------------
 extern thread_local int g_eigen_elementwise;
 long long sym_eigen_scratch(long long n);
