@@ -24,7 +24,7 @@ __all__ = [
     "tt_sweep_als", "tt_operator_apply", "tt_last_launch_count",
     "TT_SWEEP_LEFT", "TT_SWEEP_RIGHT", "TT_SWEEP_BOTH", "tt_trace_enable", "tt_trace_disable",
     "tt_trace_count", "tt_trace_read", "tt_fp64_peak_probe", "STAGE_NAMES", "tt_debug_force_v1",
-    "tt_debug_set_variant", "tt_debug_set_flags", "tt_debug_set_dag", "tt_debug_set_fused", "tt_debug_dag_trace", "tt_set_graph_cache", "prepare",
+    "tt_debug_set_variant", "tt_debug_set_flags", "tt_debug_set_dag", "tt_debug_set_fused", "tt_debug_dag_trace", "tt_set_graph_cache", "tt_set_matvec_mode", "prepare",
     "PreparedCall",
     "tt_local_gmres",
     "tt_local_gmres_workspace_size",
@@ -141,6 +141,8 @@ lib.tt_debug_set_flags.argtypes = [ctypes.c_int]
 lib.tt_debug_set_flags.restype = None
 lib.tt_debug_set_dag.argtypes = [ctypes.c_int]
 lib.tt_debug_set_dag.restype = None
+lib.tt_set_matvec_mode.argtypes = [ctypes.c_int]
+lib.tt_set_matvec_mode.restype = ctypes.c_int
 lib.tt_debug_set_fused.argtypes = [ctypes.c_int]
 lib.tt_debug_set_fused.restype = None
 lib.tt_set_graph_cache.argtypes = [ctypes.c_int]
@@ -579,6 +581,16 @@ def tt_set_graph_cache(enabled: bool) -> None:
     """Eager multi-launch calls are replayed from a per-thread CUDA graph cache from the second
     identical call on (default on); False disables it and destroys the cached graphs."""
     lib.tt_set_graph_cache(1 if enabled else 0)
+
+
+_MATVEC_MODES = {"auto": 0, "three_stage": 1, "fused": 2}
+
+
+def tt_set_matvec_mode(mode) -> None:
+    """Evaluation of the local matvec on the calling thread: "auto" (default), "three_stage" or
+    "fused" (T1 kept in shared memory: about half the workspace and HBM traffic, same results;
+    include/tt_hotpath.h tt_set_matvec_mode).  Workspace sizes follow the mode."""
+    _check(lib.tt_set_matvec_mode(int(_MATVEC_MODES.get(mode, mode))))
 
 
 def tt_debug_set_fused(mode: int) -> None:

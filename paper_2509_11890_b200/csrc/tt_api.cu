@@ -187,6 +187,13 @@ void tt_debug_set_variant(int v) {
 }
 void tt_debug_set_dag(int mode) { g_dag_mode = mode; }
 void tt_debug_set_fused(int mode) { g_fused_mode = mode; }
+tt_status tt_set_matvec_mode(int mode) {
+  if (mode != TT_MATVEC_AUTO && mode != TT_MATVEC_THREE_STAGE && mode != TT_MATVEC_FUSED)
+    return fail(TT_ERR_INVALID_ARGUMENT, "tt_set_matvec_mode: unknown mode");
+  // (variant 2 of tt_debug_set_fused: the 12-warp kernel, no warp-group skew)
+  g_fused_mode = mode == TT_MATVEC_FUSED ? 2 : mode == TT_MATVEC_THREE_STAGE ? -1 : 0;
+  return TT_OK;
+}
 void tt_set_graph_cache(int enabled) {
   g_graph_cache_on = enabled ? 1 : 0;
   if (!enabled) graph_cache_clear();

@@ -289,6 +289,7 @@ double pdl_flops() {
 #endif
 }
 thread_local bool g_no_pdl = false;
+thread_local bool g_fused_misaligned = false;
 
 
 // ----------------------------------------------------------------------------------------
@@ -522,7 +523,8 @@ bool dims_valid(const Dims& d) { return d.a > 0 && d.n > 0 && d.b > 0 && d.al > 
 bool matvec_ws_elems(const Dims& d, long long K, long long& t1, long long& t2, long long& ah,
                      long long& pe) {
   bool ok = true;
-  t1 = prod({d.a, d.al, d.n, K, d.b}, ok);
+  // the fused S1 -> S2 kernel keeps T1 in shared memory (tt_fused12.cuh)
+  t1 = fused12_wanted(d, K) ? 0 : prod({d.a, d.al, d.n, K, d.b}, ok);
   t2 = prod({d.a, d.n, K, d.be, d.b}, ok);
   ah = prod({d.al, d.n, d.n, d.be}, ok);
   // split-K partials of the last stage: 4 slices, or up to 64 for small outputs (<= 128 MB)
@@ -563,6 +565,8 @@ cudaError_t enqueue_matvec(const Dims& d, long long K, const double* phiL, const
     e = launch_fused12(d, K, phiL, Ah, X, T2, s, ok);
     if (e != cudaSuccess) return e;
     if (ok) return enqueue_matvec_last(d, K, T2, phiR, Y, P, pe, s);
+    g_fused_misaligned = true;           // the workspace was sized without T1 (cuda_fail)
+    return cudaErrorMisalignedAddress;
   }
   // S1: T1(al, j, a', m, b) = phiL[(a' al), a] . X[a, (j m b)]
   g_stage = TT_ST_MV_S1;
@@ -809,6 +813,11 @@ cudaError_t enqueue_right_pg(const DimsPG& d, const double* phiR, const double* 
 }
 
 tt_status cuda_fail(cudaError_t e, const char* where) {
+  if (g_fused_misaligned) {   // set by enqueue_matvec: not a device fault
+    g_fused_misaligned = false;
+    return fail(TT_ERR_INVALID_ARGUMENT,
+                std::string(where) + ": TT_MATVEC_FUSED needs 16-byte aligned phiL and X");
+  }
   return fail(TT_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 

@@ -45,6 +45,27 @@ bool fused12_wanted(const Dims& d, long long K) {
   return false;   // policy default decided by measurement
 }
 
+template <int G>
+static cudaError_t launch_fused12_g(const Dims& d, long long K, tt::Fused12Params p,
+                                    const CUtensorMap& tl, const CUtensorMap& tx,
+                                    const CUtensorMap& ta, cudaStream_t s) {
+  using Cfg = tt::F12Cfg<G>;
+  if (cudaError_t e = smem_attr((const void*)tt::fused_s12_kernel<G>, (int)Cfg::kSmemBytes)) return e;
+  p.nag = (int)((d.a + 2 * G - 1) / (2 * G));
+  p.total_units = (int)((long long)p.nag * p.nbt * K);
+  p.nag_div = tt::make_fastdiv((uint32_t)p.nag);
+  const int grid = (int)std::min<long long>(p.total_units, (long long)num_sms() * (3 - G));
+  g_stage = TT_ST_MV_S1;
+  // traced as one record with 2 M N K = the flops of both stages
+  const long long tr = trace_begin(-12 - (G == 1), d.a * K * d.b, 4 * d.al, d.a + 4 * d.be, s);
+  if (cudaError_t e = launch_pdl(false, tt::fused_s12_kernel<G>, dim3(grid), dim3(Cfg::kThreads),
+                                 Cfg::kSmemBytes, s, tl, tx, ta, p))
+    return e;
+  trace_end(tr, s);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_fused12(const Dims& d, long long K, const double* phiL, const double* Ah,
                            const double* X, double* T2, cudaStream_t s, bool& ok) {
   ok = false;
@@ -55,7 +76,6 @@ cudaError_t launch_fused12(const Dims& d, long long K, const double* phiL, const
   if (!make_map_x(&tx, X, d.a, d.n, K, d.b)) return cudaSuccess;
   if (!make_map3(&ta, Ah, d.n * d.be, d.al * d.n, d.n * d.be, 9)) return cudaSuccess;
   ok = true;
-  if (cudaError_t e = smem_attr((const void*)tt::fused_s12_kernel, (int)tt::kF12SmemBytes)) return e;
   tt::Fused12Params p;
   p.T2 = T2;
   p.a = (int)d.a;
@@ -63,12 +83,9 @@ cudaError_t launch_fused12(const Dims& d, long long K, const double* phiL, const
   p.al = (int)d.al;
   p.be = (int)d.be;
   p.K = (int)K;
-  p.nag = (int)((d.a + 3) / 4);
   p.nbt = (int)(d.b / 16);
-  p.total_units = (int)((long long)p.nag * p.nbt * K);
   p.KT1 = (int)((d.a + 15) / 16);
   p.KT2 = (int)((4 * d.al + 15) / 16);
-  p.nag_div = tt::make_fastdiv((uint32_t)p.nag);
   p.nbt_div = tt::make_fastdiv((uint32_t)p.nbt);
   {
     const int m = g_fused_mode > 0 ? g_fused_mode - 1 : 1;   // policy default: skew 0
@@ -78,16 +95,9 @@ cudaError_t launch_fused12(const Dims& d, long long K, const double* phiL, const
   }
   p.dbg = g_dbg_flags;
   p.gate = g_gate;
-  const int grid = (int)std::min<long long>(p.total_units, num_sms());
-  g_stage = TT_ST_MV_S1;
-  // traced as one record with 2 M N K = the flops of both stages
-  const long long tr = trace_begin(-12, d.a * K * d.b, 4 * d.al, d.a + 4 * d.be, s);
-  if (cudaError_t e = launch_pdl(false, tt::fused_s12_kernel, dim3(grid), dim3(tt::kF12Threads),
-                                 tt::kF12SmemBytes, s, tl, tx, ta, p))
-    return e;
-  trace_end(tr, s);
-  ++g_launches;
-  return cudaGetLastError();
+  // option bit 1: two independent 6-warp CTAs per SM instead of one 12-warp CTA
+  if (p.opt & 2) return launch_fused12_g<1>(d, K, p, tl, tx, ta, s);
+  return launch_fused12_g<2>(d, K, p, tl, tx, ta, s);
 }
 
 }  // namespace ttint

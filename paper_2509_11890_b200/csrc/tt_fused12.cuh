@@ -24,23 +24,31 @@
 
 namespace tt {
 
-constexpr int kF12Threads = 384, kF12Warps = 12, kF12Stages = 5;
 constexpr int kF12ABytes = 72 * 128;                       // Phi_L rows of one warp group
 constexpr int kF12XBytes = 4 * 2048;                       // X tile: 4 slabs (j) of 16 k x 16 b
-constexpr int kF12StageBytes = 2 * kF12ABytes + kF12XBytes;   // 26624 (phase-1 k-tile)
 constexpr int kF12AhBytes = 9 * 2048;                      // phase-2 k-tile: 16 k x 144 columns
 // T1 of one a': 9 k-tiles (144 k-rows) x 16 b, the 2 KB slabs 16 bytes apart so that the
 // hand-over stores of fragment rows g and g + 1 (k-rows 16 apart) fall on different banks
 constexpr int kF12T1Slab = 2048 + 16;
 constexpr int kF12T1PerA = 9 * kF12T1Slab;
-constexpr int kF12T1Bytes = 4 * kF12T1PerA;
-constexpr size_t kF12SmemBytes = (size_t)kF12Stages * kF12StageBytes + kF12T1Bytes + 1024;
-static_assert(kF12AhBytes <= kF12StageBytes, "phase-2 k-tile fits a ring stage");
+// G warp groups of 6 warps per CTA, each owning two a' of the unit: G = 2 is one 12-warp CTA
+// per SM (4 a' per unit, X tile and Ahat k-tiles shared by the groups, 5 stages); G = 1 is two
+// independent 6-warp CTAs per SM (2 a' per unit, own 4-stage rings: twice the X / Ahat reads
+// from L2, but one CTA's hand-over and epilogue fall on the other's DMMA stream).
+template <int G>
+struct F12Cfg {
+  static constexpr int kThreads = 192 * G, kWarps = 6 * G;
+  static constexpr int kPhase1Bytes = G * kF12ABytes + kF12XBytes;
+  static constexpr int kStageBytes = kPhase1Bytes > kF12AhBytes ? kPhase1Bytes : kF12AhBytes;
+  static constexpr int kStages = G == 2 ? 5 : 4;
+  static constexpr int kT1Bytes = 2 * G * kF12T1PerA;
+  static constexpr size_t kSmemBytes = (size_t)kStages * kStageBytes + kT1Bytes + 1024;
+};
 
 struct Fused12Params {
   double* T2;        // (a, K, 4, be, b)
   int a, b, al, be, K;
-  int nag, nbt;      // groups of 4 a', tiles of 16 b
+  int nag, nbt;      // groups of 2 G a', tiles of 16 b
   int total_units;   // nag * nbt * K, a' group fastest
   int KT1, KT2;      // k-tiles of 16: ceil(a / 16), ceil(4 al / 16)
   FastDiv nag_div, nbt_div;
@@ -69,10 +77,13 @@ __device__ __forceinline__ void bar_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(n) : "memory");
 }
 
-__global__ void __launch_bounds__(kF12Threads, 1)
+template <int G>
+__global__ void __launch_bounds__(192 * G, 3 - G)
 fused_s12_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_constant__ CUtensorMap tmX,
                  const __grid_constant__ CUtensorMap tmA, const Fused12Params p) {
-  constexpr int ST = kF12Stages;
+  using Cfg = F12Cfg<G>;
+  constexpr int ST = Cfg::kStages, kF12StageBytes = Cfg::kStageBytes, kF12Threads = Cfg::kThreads;
+  constexpr int kF12Warps = Cfg::kWarps, kF12T1Bytes = Cfg::kT1Bytes;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[ST], empty_bar[ST];
   __shared__ int prod_state[6];   // u, ag, bt, m, kt, q
@@ -81,7 +92,7 @@ fused_s12_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_constant_
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int gm = warp / 6, wl = warp - 6 * gm;   // warp group, warp within the group
+  const int gm = G == 1 ? 0 : warp / 6, wl = warp - 6 * gm;   // warp group, warp within the group
   const int wr = wl >> 1, wc = wl & 1;           // phase 1: 3 x 2 warps of 24 rows x 32 columns
   const int wa = wl / 3, wn2 = wl - 3 * wa;      // phase 2: 2 (a') x 3 warps of 16 rows x 48 columns
 
@@ -128,12 +139,21 @@ fused_s12_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_constant_
     if (lq >= (uint32_t)ST) mbar_wait(&empty_bar[s], ((lq / ST) - 1) & 1);
     unsigned char* st = smem + s * kF12StageBytes;
     const int kt = ps[4];
+#ifdef TT_DEBUG_HOOKS
+    if (p.opt & 4) {   // timing probe: no loads, the transaction count completed locally
+      const uint32_t nbytes = kt < p.KT1 ? Cfg::kPhase1Bytes : kF12AhBytes;
+      mbar_expect_tx(&full_bar[s], nbytes);
+      asm volatile("mbarrier.complete_tx.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&full_bar[s])),
+                   "r"(nbytes)
+                   : "memory");
+    } else
+#endif
     if (kt < p.KT1) {
-      const int k0 = kt * 16, r0 = ps[1] * 4 * p.al;
-      mbar_expect_tx(&full_bar[s], kF12StageBytes);
+      const int k0 = kt * 16, r0 = ps[1] * 2 * G * p.al;
+      mbar_expect_tx(&full_bar[s], Cfg::kPhase1Bytes);
       tma_load_2d_hint(st, &tmL, k0, r0, &full_bar[s], pol_keep);
-      tma_load_2d_hint(st + kF12ABytes, &tmL, k0, r0 + 2 * p.al, &full_bar[s], pol_keep);
-      tma_load_5d(st + 2 * kF12ABytes, &tmX, 0, k0, ps[2], 0, ps[3], &full_bar[s]);
+      if (G == 2) tma_load_2d_hint(st + kF12ABytes, &tmL, k0, r0 + 2 * p.al, &full_bar[s], pol_keep);
+      tma_load_5d(st + G * kF12ABytes, &tmX, 0, k0, ps[2], 0, ps[3], &full_bar[s]);
     } else {
       mbar_expect_tx(&full_bar[s], kF12AhBytes);
       tma_load_3d(st, &tmA, 0, (kt - p.KT1) * 16, 0, &full_bar[s], pol_keep, true);
@@ -145,7 +165,7 @@ fused_s12_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_constant_
       if (ps[0] < p.total_units) decode(ps[0], ps[1], ps[2], ps[3]);
     }
   };
-  const int skew = p.skew;
+  const int skew = G == 2 ? p.skew : 0;
   const bool trail = skew > 0 && gm == 1;
   if (tid == 0)
     for (int s = 0; s < ST - 1 - skew; ++s) produce_one();
@@ -159,7 +179,7 @@ fused_s12_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_constant_
   const int mn0 = (2 * t) * 128 + ((g ^ (2 * t)) << 4);
   const int mn1 = (2 * t + 1) * 128 + ((g ^ (2 * t + 1)) << 4);
   // phase 1 B (X tile): slabs j = 2 wc + q;  phase 2 B (Ahat k-tile): slabs 3 wn2 + q
-  const int x_off = 2 * kF12ABytes + wc * 2 * 2048;
+  const int x_off = G * kF12ABytes + wc * 2 * 2048;
   const int ah_off = wn2 * 3 * 2048;
   // phase 2 A: the T1 block of this warp's a' (= 2 gm + wa), one slab per k-tile
   const unsigned char* const t1a = t1s + (2 * gm + wa) * kF12T1PerA;
@@ -226,6 +246,9 @@ fused_s12_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_constant_
     // ring guarantees it (the load of this unit's last phase-1 k-tile was issued only after
     // all 12 warps released a stage of this unit's phase 1), otherwise a barrier does.
     if (pre_barrier) bar_sync(1 + gm, 192);
+#ifdef TT_DEBUG_HOOKS
+    if (!(p.opt & 16))   // timing probe: no hand-over stores
+#endif
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
       const int lr = wr * 24 + 8 * i + Rg;           // Phi_L row within the group: (a', al)
@@ -288,7 +311,15 @@ fused_s12_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_constant_
       }
     }
     // ================= epilogue: T2(a', m, i, be, b0 + 2g .. 2g + 1) =================
-    const int ap = ag * 4 + 2 * gm + wa;
+    const int ap = ag * 2 * G + 2 * gm + wa;
+#ifdef TT_DEBUG_HOOKS
+    if (p.opt & 8) {   // timing probe: no T2 stores (accumulators kept live)
+      double sink = 0.0;
+#pragma unroll
+      for (int j = 0; j < 6; ++j) sink += ac2[0][j][0] + ac2[0][j][1] + ac2[1][j][0] + ac2[1][j][1];
+      if (sink == 1.2345e-300) p.T2[0] = sink;
+    } else
+#endif
     if (ap < p.a) {
       double* rowp = p.T2 + ((long long)ap * p.K + m) * ((long long)NB * p.b) + bt * 16 + 2 * g;
 #pragma unroll

@@ -272,6 +272,7 @@ cudaError_t enqueue_right_pg(const DimsPG& d, const double* phiR, const double* 
 
 // ---- fused S1 -> S2 matvec kernel (tt_fused.cu / tt_fused12.cuh) ---------------------------------
 extern thread_local int g_fused_mode;
+extern thread_local bool g_fused_misaligned;
 bool fused12_shape_ok(const Dims& d, long long K);
 bool fused12_wanted(const Dims& d, long long K);
 cudaError_t launch_fused12(const Dims& d, long long K, const double* phiL, const double* Ah,

@@ -133,3 +133,29 @@ def test_product_library_reads_no_environment_knobs():
     data = open(LIB, "rb").read()
     for knob in (b"TT_LAT_FLOPS", b"TT_PDL_FLOPS", b"TT_L2_DEBUG", b"TT_LAT_UNIT_US"):
         assert knob not in data, knob
+
+
+def test_matvec_mode_sizes_the_workspace(lib):
+    """tt_set_matvec_mode (host logic only): an unknown mode is rejected; under TT_MATVEC_FUSED
+    the workspace of an eligible core drops T1 = rl Rl n nvec rr doubles, an ineligible core
+    (n != 4, rr % 16 != 0, Rr % 4 != 0, Rl > 36, odd rl) keeps it; AUTO restores the size."""
+    import ctypes
+    f = lib.tt_local_matvec_workspace_size
+    f.restype = ctypes.c_size_t
+    f.argtypes = [ctypes.c_int64] * 6
+    lib.tt_set_matvec_mode.restype = ctypes.c_int
+    lib.tt_set_matvec_mode.argtypes = [ctypes.c_int]
+    assert lib.tt_set_matvec_mode(7) != 0
+    elig = (256, 4, 256, 36, 36, 32)
+    inelig = [(256, 3, 256, 36, 36, 32), (256, 4, 250, 36, 36, 32), (256, 4, 256, 36, 35, 32),
+              (256, 4, 256, 40, 36, 32), (255, 4, 256, 36, 36, 32)]
+    full = f(*elig)
+    full_in = [f(*s) for s in inelig]
+    assert lib.tt_set_matvec_mode(2) == 0
+    try:
+        t1 = 8 * 256 * 36 * 4 * 32 * 256
+        assert full - t1 - 4096 <= f(*elig) <= full - t1
+        assert [f(*s) for s in inelig] == full_in
+    finally:
+        assert lib.tt_set_matvec_mode(0) == 0
+    assert f(*elig) == full

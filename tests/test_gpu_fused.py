@@ -49,7 +49,7 @@ FUSED_SHAPES = [
 ]
 
 
-@pytest.mark.parametrize("mode", [1, 2, 3, 5])
+@pytest.mark.parametrize("mode", [1, 2, 3, 5, 8])
 @pytest.mark.parametrize("shape", FUSED_SHAPES)
 def test_fused_matvec_vs_oracle(tt, shape, mode):
     import oracle
@@ -69,7 +69,7 @@ def test_fused_matvec_vs_oracle(tt, shape, mode):
     finally:
         tt.tt_debug_set_fused(0)
     # the fused kernel ran (one mv_s1 record tagged -12) and no separate S2 launch
-    assert any(r["stage"] == "mv_s1" and r["tile"] == -12 for r in recs), recs
+    assert any(r["stage"] == "mv_s1" and r["tile"] in (-12, -13) for r in recs), recs
     assert not any(r["stage"] == "mv_s2" for r in recs), recs
     for m in range(nvec):
         assert rel(Y[:, :, m, :], ref[:, :, m, :]) <= TOL, (shape, m)
@@ -100,5 +100,87 @@ def test_fused_ineligible_shapes_fall_back(tt):
             tt.tt_trace_disable()
         finally:
             tt.tt_debug_set_fused(0)
-        assert not any(r["tile"] == -12 for r in recs)
+        assert not any(r["tile"] in (-12, -13) for r in recs)
         assert rel(Y, oracle.local_matvec_batched(phiL, A, phiR, X)) <= TOL
+
+
+def test_public_fused_mode_halves_workspace_and_matches(tt):
+    """tt_set_matvec_mode("fused"): the workspace query drops T1, the call runs the fused kernel
+    with that smaller workspace and returns bit-identical results; "three_stage" restores both."""
+    rl, rr, Rl, Rr, nvec = 64, 64, 36, 36, 4
+    rng = np.random.default_rng(11)
+    phiL, A = g(rng.standard_normal((rl, Rl, rl))), g(rng.standard_normal((Rl, 4, 4, Rr)))
+    phiR, X = g(rng.standard_normal((rr, Rr, rr))), g(rng.standard_normal((rl, 4, nvec, rr)))
+    full = tt.lib.tt_local_matvec_workspace_size(rl, 4, rr, Rl, Rr, nvec)
+    Y3 = tt.tt_local_matvec_batched(phiL, A, phiR, X)
+    tt.tt_set_matvec_mode("fused")
+    try:
+        compact = tt.lib.tt_local_matvec_workspace_size(rl, 4, rr, Rl, Rr, nvec)
+        t1_bytes = 8 * rl * Rl * 4 * nvec * rr
+        assert full - t1_bytes - 4096 <= compact <= full - t1_bytes
+        tt.tt_trace_enable(16)
+        Yf = tt.tt_local_matvec_batched(phiL, A, phiR, X)
+        recs = [tt.tt_trace_read(i) for i in range(tt.tt_trace_count())]
+        tt.tt_trace_disable()
+        assert any(r["tile"] == -12 for r in recs)
+        # an ineligible core keeps its T1
+        assert tt.lib.tt_local_matvec_workspace_size(rl, 3, rr, Rl, Rr, nvec) >= 8 * rl * Rl * 3 * nvec * rr
+    finally:
+        tt.tt_set_matvec_mode("auto")
+    assert tt.lib.tt_local_matvec_workspace_size(rl, 4, rr, Rl, Rr, nvec) == full
+    assert torch.equal(Yf, Y3)
+
+
+def test_fused_mode_rejects_misaligned_operands(tt):
+    rl, rr, Rl, Rr, nvec = 8, 16, 4, 4, 1
+    base = torch.randn(rl * 4 * nvec * rr + 1, dtype=torch.float64, device="cuda")
+    X = base[1:].view(rl, 4, nvec, rr)   # 8-byte aligned only
+    phiL = torch.randn(rl, Rl, rl, dtype=torch.float64, device="cuda")
+    A = torch.randn(Rl, 4, 4, Rr, dtype=torch.float64, device="cuda")
+    phiR = torch.randn(rr, Rr, rr, dtype=torch.float64, device="cuda")
+    ref = tt.tt_local_matvec_batched(phiL, A, phiR, X)      # three-stage handles it
+    tt.tt_set_matvec_mode("fused")
+    try:
+        with pytest.raises(tt.TTError) as ei:
+            tt.tt_local_matvec_batched(phiL, A, phiR, X)
+        assert "16-byte aligned" in str(ei.value)
+        # the thread stays usable
+        Y = tt.tt_local_matvec_batched(phiL, A, phiR, X.clone())
+    finally:
+        tt.tt_set_matvec_mode("auto")
+    assert float((Y - ref).norm() / ref.norm()) <= 1e-13   # (the misaligned reference ran the generic kernel)
+
+def test_fused_config5_interior_bit_identical(tt):
+    """Full-size config-5 interior core (a = b = 256, al = be = 36, K = 32), the launch
+    configuration tools/fused_probe.py and bench.py time: the fused evaluation equals the
+    three-stage one bit for bit (same k order in every DMMA accumulator), so the oracle parity
+    of test_gpu_parity.py::test_config5_w5_sampled carries over."""
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    r = lambda *s: torch.randn(*s, dtype=torch.float64, device="cuda", generator=gen)
+    phiL, A, phiR, X = r(256, 36, 256), r(36, 4, 4, 36), r(256, 36, 256), r(256, 4, 32, 256)
+    Y3 = tt.tt_local_matvec_batched(phiL, A, phiR, X)
+    tt.tt_set_matvec_mode("fused")
+    try:
+        Yf = tt.tt_local_matvec_batched(phiL, A, phiR, X)
+    finally:
+        tt.tt_set_matvec_mode("auto")
+    assert torch.equal(Yf, Y3)
+
+
+def test_fused_sweep_als_matches_three_stage(tt):
+    """tt_sweep_als (the W5 launch configuration) at a reduced config-5 shape under both modes."""
+    d, nvec = 6, 4
+    r = [1, 4, 16, 64, 16, 4, 1]
+    R = [1, 4, 36, 36, 36, 4, 1]
+    rng = np.random.default_rng(17)
+    xs = [g(rng.standard_normal((r[k], 4, r[k + 1]))) for k in range(d)]
+    As = [g(rng.standard_normal((R[k], 4, 4, R[k + 1])) / 6) for k in range(d)]
+    Xs = [g(rng.standard_normal((r[k], 4, nvec, r[k + 1]))) for k in range(d)]
+    out3 = tt.tt_sweep_als(xs, As, Xs)
+    tt.tt_set_matvec_mode("fused")
+    try:
+        outf = tt.tt_sweep_als(xs, As, Xs)
+    finally:
+        tt.tt_set_matvec_mode("auto")
+    for y3, yf in zip(out3[0], outf[0]):
+        assert torch.equal(y3, yf)
