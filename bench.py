@@ -673,6 +673,66 @@ def main():
         del S1, sets, host_views, host_out
         torch.cuda.empty_cache()
 
+    # ---- the same W5 sweep under TT_MATVEC_FUSED (T1 kept in shared memory) ---------------
+    fused = None
+    if not args.no_sweeps:
+        tt.tt_set_matvec_mode("fused")
+        try:
+            ws_f = torch.empty(tt.tt_sweep_als_workspace_size(tr, cfg.nvec), dtype=torch.uint8,
+                               device=dev)
+            Y_f = [torch.empty_like(X) for X in S0["X"]]
+
+            def sweep_f():
+                tt.tt_sweep_als(S0["x"], S0["A"], S0["X"], Y_f, None, S0["phiL"], S0["phiR"],
+                                workspace=ws_f, stream=stream)
+            for _ in range(2):
+                sweep_f()
+            torch.cuda.synchronize(dev)
+            evf = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(3)]
+            for a, b in evf:
+                flush.zero_()
+                a.record(stream)
+                sweep_f()
+                b.record(stream)
+            torch.cuda.synchronize(dev)
+            f_ms = sum(a.elapsed_time(b) for a, b in evf) / len(evf)
+            tt.tt_trace_enable(600)
+            flush.zero_()
+            sweep_f()
+            torch.cuda.synchronize(dev)
+            frecs = [tt.tt_trace_read(i) for i in range(tt.tt_trace_count())]
+            tt.tt_trace_disable()
+            fk = [r for r in frecs if r["stage"] == "mv_s1" and r["tile"] == -12]
+            fk_ms = sum(r["ms"] for r in fk)
+            fk_fl = sum(2.0 * r["M"] * r["N"] * r["K"] for r in fk)
+            same = all(torch.equal(a, b) for a, b in zip(Y_f, S0["Y"]))
+            tj = {}
+            try:
+                tj = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+            except Exception:
+                pass
+            w5_fl = work["step_flops"] - work["apply_flops"]
+            fused = {
+                "mode": "tt_set_matvec_mode(TT_MATVEC_FUSED): S1 -> S2 in one kernel, T1 in shared "
+                        "memory (csrc/tt_fused12.cuh); opt-in, the default is the three-stage path",
+                "w5_ms": f_ms, "w5_gflops": w5_fl / (f_ms * 1e-3) / 1e9,
+                "w5_frac_of_roofline": w5_fl / (f_ms * 1e-3) / 1e12 / p64_sustained,
+                "fused_launches": len(fk), "all_matvec_launches_fused": len(fk) == 2 * d,
+                "fused_kernel_tflops_traced": fk_fl / (fk_ms * 1e-3) / 1e12 if fk_ms > 0 else None,
+                "workspace_bytes": int(ws_f.numel()), "workspace_bytes_three_stage": int(ws.numel()),
+                "bit_identical_to_three_stage": bool(same),
+                "dram_bytes_interior_matvec": {
+                    "three_stage": (tj.get("mv_s1", 0) + tj.get("mv_s2", 0) + tj.get("mv_s3", 0)) or None,
+                    "fused": (tj.get("mv_fused12", 0) + tj.get("mv_s3", 0)) or None,
+                    "algorithmic": b_local_matvec(cfg.r[d // 2], cfg.N, cfg.r[d // 2 + 1],
+                                                  cfg.R[d // 2], cfg.R[d // 2 + 1], cfg.nvec),
+                    "source": "profiles/ncu_traffic.json (ncu --set full, config-5 interior core)"},
+            }
+            del ws_f, Y_f
+        finally:
+            tt.tt_set_matvec_mode("auto")
+
     # ---- per-config lines: W34 for configs 1-4, W5 for config 5 ---------
     configs = {}
     gpu_out = {}
@@ -956,6 +1016,7 @@ def main():
             "gpu_launches": gpu_launches,
             "clocks": clk,
             "configs": configs,
+            "fused_matvec": fused,
             "latency": latency,
             "local_gmres": gm,
             "kkt_block_action": kkt,
