@@ -847,7 +847,7 @@ def main():
 
     # ---- SURVEY 8(f) NEXT rows on the config-5 interior core ----------------------------
     xs, As, Xs, phiL, phiR, Yf = S0["x"], S0["A"], S0["X"], S0["phiL"], S0["phiR"], S0["Y"]
-    gm = kkt = two = lob = rnd_info = None
+    gm = kkt = two = lob = rnd_info = single = None
     if not (args.no_sweeps or args.no_next):
         k = cfg.d // 2
         m_g = 10
@@ -892,6 +892,27 @@ def main():
                "ms": t["graph_ms_median"], "gflop": f9 / 1e9,
                "tflops": f9 / (t["graph_ms_median"] * 1e-3) / 1e12,
                "frac_of_p64": f9 / (t["graph_ms_median"] * 1e-3) / 1e12 / p64_sustained}
+        # one interface update / one single-vector matvec of the interior core, alone on the GPU
+        # (TT_MATVEC_AUTO runs their first two products in the fused kernel)
+        wsi = torch.empty(tt.tt_interface_workspace_size(rl, nn, rr, Rl, Rr), dtype=torch.uint8,
+                          device=dev)
+        pl_out, pr_out = torch.empty_like(phiL[k + 1]), torch.empty_like(phiR[k])
+        y1 = torch.empty_like(xs[k])
+        wsm = torch.empty(tt.tt_local_matvec_workspace_size(rl, nn, rr, Rl, Rr, 1),
+                          dtype=torch.uint8, device=dev)
+        f1 = f_local(rl, nn, rr, Rl, Rr)
+        single = {"core": k, "gflop": f1 / 1e9}
+        for nm, fn in (("interface_left", lambda st: tt.tt_interface_left(
+                            phiL[k], As[k], xs[k], pl_out, workspace=wsi, stream=st)),
+                       ("interface_right", lambda st: tt.tt_interface_right(
+                            phiR[k + 1], As[k], xs[k], pr_out, workspace=wsi, stream=st)),
+                       ("matvec_k1", lambda st: tt.tt_local_matvec(
+                            phiL[k], As[k], phiR[k + 1], xs[k], y1, workspace=wsm, stream=st))):
+            t = time_sweep(tt, fn, stream, dev, reps=10)
+            single[nm] = {"ms": t["graph_ms_median"], "launches": t["launches"],
+                          "tflops": f1 / (t["graph_ms_median"] * 1e-3) / 1e12,
+                          "frac_of_p64": f1 / (t["graph_ms_median"] * 1e-3) / 1e12 / p64_sustained}
+        del wsi, wsm
         A1, A2 = rnd(Rl, 2, 2, Rl), rnd(Rl, 2, 2, Rr)
         W2 = rnd(rl, 2, 2, cfg.nvec, rr)
         Y2 = torch.empty_like(W2)
@@ -1019,6 +1040,7 @@ def main():
             "fused_matvec": fused,
             "latency": latency,
             "local_gmres": gm,
+            "single_core_k1": single,
             "kkt_block_action": kkt,
             "two_site_matvec": two,
             "tt_round": rnd_info,

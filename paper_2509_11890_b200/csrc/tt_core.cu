@@ -560,13 +560,15 @@ cudaError_t enqueue_matvec(const Dims& d, long long K, const double* phiL, const
   else if ((e = launch_perm(true, A, Ah, al, N, be, s)) != cudaSuccess)
     return e;
   // fused S1 -> S2 (tt_fused12.cuh): T1 stays in shared memory
-  if (fused12_wanted(d, K)) {
+  if (fused12_wanted(d, K) || fused12_auto(d, K)) {
     bool ok = false;
     e = launch_fused12(d, K, phiL, Ah, X, T2, s, ok);
     if (e != cudaSuccess) return e;
     if (ok) return enqueue_matvec_last(d, K, T2, phiR, Y, P, pe, s);
-    g_fused_misaligned = true;           // the workspace was sized without T1 (cuda_fail)
-    return cudaErrorMisalignedAddress;
+    if (fused12_wanted(d, K)) {
+      g_fused_misaligned = true;         // the workspace was sized without T1 (cuda_fail)
+      return cudaErrorMisalignedAddress;
+    }
   }
   // S1: T1(al, j, a', m, b) = phiL[(a' al), a] . X[a, (j m b)]
   g_stage = TT_ST_MV_S1;
@@ -613,18 +615,25 @@ cudaError_t enqueue_left(const Dims& d, const double* phiL, const double* A, con
     Ah = const_cast<double*>(Ah_pre);
   else if ((e = launch_perm(true, A, Ah, al, N, be, s)) != cudaSuccess)
     return e;
-  g_stage = tag_s1;
-  e = launch_gemm(true, false,
-                  gp(phiL, a, x, N * b, T1, a * al, N * b, a, tt::map2(al, N * a * b, b),
-                     tt::map2(b, 1, a * b)),
-                  s);
-  if (e != cudaSuccess) return e;
-  g_stage = tag_s1 + 1;
-  e = launch_gemm(false, false,
-                  gp(T1, a * b, Ah, N * be, T2, a * b, N * be, al * N, tt::map2(b, 1, N * be * b),
-                     tt::map_plain(b)),
-                  s);
-  if (e != cudaSuccess) return e;
+  // the first two stages are the matvec's with one column: fused when wanted (tt_fused12.cuh)
+  bool fused = false;
+  if (fused12_iface_wanted(d)) {
+    if ((e = launch_fused12(d, 1, phiL, Ah, x, T2, s, fused, tag_s1)) != cudaSuccess) return e;
+  }
+  if (!fused) {
+    g_stage = tag_s1;
+    e = launch_gemm(true, false,
+                    gp(phiL, a, x, N * b, T1, a * al, N * b, a, tt::map2(al, N * a * b, b),
+                       tt::map2(b, 1, a * b)),
+                    s);
+    if (e != cudaSuccess) return e;
+    g_stage = tag_s1 + 1;
+    e = launch_gemm(false, false,
+                    gp(T1, a * b, Ah, N * be, T2, a * b, N * be, al * N, tt::map2(b, 1, N * be * b),
+                       tt::map_plain(b)),
+                    s);
+    if (e != cudaSuccess) return e;
+  }
   if (ev_t2 && (e = cudaEventRecord(ev_t2, s)) != cudaSuccess) return e;   // T2 complete
   g_stage = tag_s1 + 2;
   SplitScratch scratch(P, pe);

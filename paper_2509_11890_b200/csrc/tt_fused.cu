@@ -9,6 +9,7 @@ namespace ttint {
 // tt_debug_set_fused: 0 policy (default), -1 never, m > 0 whenever eligible with warp-group
 // skew {1, 0, 2}[(m - 1) % 3] k-tiles and option bits (m - 1) / 3 (tt_fused12.cuh)
 thread_local int g_fused_mode = 0;
+thread_local bool g_fused_auto_ctx = false;
 
 // 5-D FP64 view of the Krylov block X (a, j, m, b) for the phase-1 B operand: dims
 // {16 (b lo), a (k), b / 16 (b hi), 4 (j), K (m)}, box {16, 16, 1, 4, 1}: one TMA brings the
@@ -36,17 +37,32 @@ bool fused12_shape_ok(const Dims& d, long long K) {
          d.a * K * 4 * d.be * d.b < (1LL << 62);
 }
 
-// policy: the fused kernel where the T1 round trip is the larger cost -- both bonds wide
-// enough that the three-stage path would stream T1 through HBM (it no longer fits in L2)
+// The workspace is sized without T1 only under an explicit fused mode (TT_MATVEC_FUSED or a
+// forced tt_debug_set_fused variant): there a misaligned operand is an error.
 bool fused12_wanted(const Dims& d, long long K) {
-  if (g_fused_mode < 0) return false;
-  if (!fused12_shape_ok(d, K)) return false;
-  if (g_fused_mode > 0) return true;
-  return false;   // policy default decided by measurement
+  return g_fused_mode > 0 && fused12_shape_ok(d, K);
+}
+
+// TT_MATVEC_AUTO: the fused kernel where it was measured faster than the two stage GEMMs
+// (tools/fused_probe.py, tools/iface_probe.py): few Krylov columns -- the
+// single-vector matvecs and every interface update -- where the stage GEMMs are a few waves of
+// tiles (r = 256, R = 36: K = 1 -7 %, K = 2 -4 %, K = 4 -1 %, K >= 8 slower; r = 512, K = 1
+// -2 %), and an operator bond that fills the kernel's 36-row a' blocks (R = 16 / 20 / 24: the
+// padded rows cost more than the launch saves).  The workspace keeps T1, so a misaligned
+// operand falls back to the stage GEMMs.
+bool fused12_auto(const Dims& d, long long K) {
+  if (g_fused_mode != 0 || !g_fused_auto_ctx || !fused12_shape_ok(d, K)) return false;
+  return d.al >= 28 && d.a * d.b * K <= 300000 && d.a >= 64 && d.b >= 64;
+}
+
+// interface updates (their workspace always holds T1, so a misaligned operand just falls back)
+bool fused12_iface_wanted(const Dims& d) {
+  if (g_fused_mode < 0 || !fused12_shape_ok(d, 1)) return false;
+  return g_fused_mode > 0 || fused12_auto(d, 1);
 }
 
 template <int G>
-static cudaError_t launch_fused12_g(const Dims& d, long long K, tt::Fused12Params p,
+static cudaError_t launch_fused12_g(const Dims& d, long long K, int stage_tag, tt::Fused12Params p,
                                     const CUtensorMap& tl, const CUtensorMap& tx,
                                     const CUtensorMap& ta, cudaStream_t s) {
   using Cfg = tt::F12Cfg<G>;
@@ -55,7 +71,7 @@ static cudaError_t launch_fused12_g(const Dims& d, long long K, tt::Fused12Param
   p.total_units = (int)((long long)p.nag * p.nbt * K);
   p.nag_div = tt::make_fastdiv((uint32_t)p.nag);
   const int grid = (int)std::min<long long>(p.total_units, (long long)num_sms() * (3 - G));
-  g_stage = TT_ST_MV_S1;
+  g_stage = stage_tag;
   // traced as one record with 2 M N K = the flops of both stages
   const long long tr = trace_begin(-12 - (G == 1), d.a * K * d.b, 4 * d.al, d.a + 4 * d.be, s);
   if (cudaError_t e = launch_pdl(false, tt::fused_s12_kernel<G>, dim3(grid), dim3(Cfg::kThreads),
@@ -67,7 +83,7 @@ static cudaError_t launch_fused12_g(const Dims& d, long long K, tt::Fused12Param
 }
 
 cudaError_t launch_fused12(const Dims& d, long long K, const double* phiL, const double* Ah,
-                           const double* X, double* T2, cudaStream_t s, bool& ok) {
+                           const double* X, double* T2, cudaStream_t s, bool& ok, int stage_tag) {
   ok = false;
   if (!fused12_shape_ok(d, K)) return cudaSuccess;
   if (!aligned16(phiL) || !aligned16(Ah) || !aligned16(X) || !aligned16(T2)) return cudaSuccess;
@@ -96,8 +112,8 @@ cudaError_t launch_fused12(const Dims& d, long long K, const double* phiL, const
   p.dbg = g_dbg_flags;
   p.gate = g_gate;
   // option bit 1: two independent 6-warp CTAs per SM instead of one 12-warp CTA
-  if (p.opt & 2) return launch_fused12_g<1>(d, K, p, tl, tx, ta, s);
-  return launch_fused12_g<2>(d, K, p, tl, tx, ta, s);
+  if (p.opt & 2) return launch_fused12_g<1>(d, K, stage_tag, p, tl, tx, ta, s);
+  return launch_fused12_g<2>(d, K, stage_tag, p, tl, tx, ta, s);
 }
 
 }  // namespace ttint

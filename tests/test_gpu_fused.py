@@ -184,3 +184,53 @@ def test_fused_sweep_als_matches_three_stage(tt):
         tt.tt_set_matvec_mode("auto")
     for y3, yf in zip(out3[0], outf[0]):
         assert torch.equal(y3, yf)
+
+
+def _stages(tt, fn):
+    tt.tt_trace_enable(64)
+    out = fn()
+    recs = [tt.tt_trace_read(i) for i in range(tt.tt_trace_count())]
+    tt.tt_trace_disable()
+    return out, recs
+
+
+def test_auto_policy_selects_fused_for_few_columns(tt):
+    """TT_MATVEC_AUTO (default): single-core calls with few Krylov columns and an operator bond
+    that fills the kernel's 36-row blocks run the fused kernel (with the full workspace as the
+    fallback); large Krylov blocks and narrow operator bonds keep the three stages."""
+    import oracle
+    rng = np.random.default_rng(23)
+    rl = rr = 64
+    for Rl, Rr, nvec, want in [(36, 36, 1, True), (36, 36, 4, True), (36, 36, 128, False),
+                               (16, 16, 1, False), (28, 32, 2, True)]:
+        phiL = rng.standard_normal((rl, Rl, rl))
+        A = rng.standard_normal((Rl, 4, 4, Rr))
+        phiR = rng.standard_normal((rr, Rr, rr))
+        X = rng.standard_normal((rl, 4, nvec, rr))
+        Y, recs = _stages(tt, lambda: tt.tt_local_matvec_batched(g(phiL), g(A), g(phiR), g(X)))
+        assert any(r["tile"] == -12 for r in recs) == want, (Rl, Rr, nvec, recs)
+        ref = oracle.local_matvec_batched(phiL, A, phiR, X[:, :, :2, :])
+        assert rel(h(Y)[:, :, :2, :], ref) <= TOL
+
+
+@pytest.mark.parametrize("mode", [0, 2])
+def test_interface_updates_through_fused_kernel(tt, mode):
+    """Left and right interface updates whose first two products run in the
+    fused kernel (AUTO policy at Rl = 36, or forced) against the oracle."""
+    import oracle
+    rng = np.random.default_rng(29)
+    for rl, rr, Rl, Rr in [(64, 80, 36, 32), (96, 64, 28, 36)]:
+        A = rng.standard_normal((Rl, 4, 4, Rr))
+        x = rng.standard_normal((rl, 4, rr))
+        pl = rng.standard_normal((rl, Rl, rl))
+        pr = rng.standard_normal((rr, Rr, rr))
+        tt.tt_debug_set_fused(mode)
+        try:
+            outL, recL = _stages(tt, lambda: tt.tt_interface_left(g(pl), g(A), g(x)))
+            outR, recR = _stages(tt, lambda: tt.tt_interface_right(g(pr), g(A), g(x)))
+        finally:
+            tt.tt_debug_set_fused(0)
+        assert any(r["tile"] == -12 and r["stage"] == "il_s1" for r in recL), recL
+        assert any(r["tile"] == -12 and r["stage"] == "ir_s1" for r in recR), recR
+        assert rel(h(outL), oracle.interface_left(pl, A, x)) <= TOL
+        assert rel(h(outR), oracle.interface_right(pr, A, x)) <= TOL

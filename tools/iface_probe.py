@@ -16,6 +16,8 @@ g = torch.Generator(device="cuda").manual_seed(0)
 r = lambda *s: torch.randn(*s, dtype=torch.float64, device="cuda", generator=g)
 phiL, A, phiR, x = r(a, al, a), r(al, n, n, be), r(b, be, b), r(a, n, b)
 wi = torch.empty(tt.tt_interface_workspace_size(a, n, b, al, be), dtype=torch.uint8, device="cuda")
+mode = int(sys.argv[3]) if len(sys.argv) > 3 else 0   # tt_debug_set_fused
+tt.tt_debug_set_fused(mode)
 for name, fn in (("left", lambda: tt.tt_interface_left(phiL, A, x, workspace=wi)),
                  ("right", lambda: tt.tt_interface_right(phiR, A, x, workspace=wi))):
     fn()
