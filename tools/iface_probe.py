@@ -18,6 +18,8 @@ phiL, A, phiR, x = r(a, al, a), r(al, n, n, be), r(b, be, b), r(a, n, b)
 wi = torch.empty(tt.tt_interface_workspace_size(a, n, b, al, be), dtype=torch.uint8, device="cuda")
 mode = int(sys.argv[3]) if len(sys.argv) > 3 else 0   # tt_debug_set_fused
 tt.tt_debug_set_fused(mode)
+if len(sys.argv) > 4:
+    tt.tt_debug_set_variant(int(sys.argv[4]))   # forced tile configuration (tt_launch_tpl.cuh)
 for name, fn in (("left", lambda: tt.tt_interface_left(phiL, A, x, workspace=wi)),
                  ("right", lambda: tt.tt_interface_right(phiR, A, x, workspace=wi))):
     fn()
