@@ -385,18 +385,17 @@ void tt_set_graph_cache(int enabled);
 
 /* Evaluation of the local matvec's three products on the calling thread.
  *   TT_MATVEC_THREE_STAGE: three GEMM launches, both intermediates T1 (a, Rl, n, nvec, b) and
- *     T2 (a, nvec, n, Rr, b) in the workspace (the fastest evaluation of large Krylov blocks:
- *     DESIGN.md §4.10).
+ *     T2 (a, nvec, n, Rr, b) in the workspace.
  *   TT_MATVEC_FUSED: the first two products in one kernel, T1 kept in shared memory tile by
  *     tile (csrc/tt_fused12.cuh): the workspace holds no T1 (about half the bytes) and the
  *     matvec's HBM traffic loses the T1 round trip; same results bit for bit.  Applies to cores
  *     with n = 4, Rl <= 36, Rr <= 36 with Rr % 4 == 0, rr % 16 == 0, rl even and 16-byte aligned
  *     phiL and X; other cores keep the three-stage evaluation and its workspace (a misaligned
  *     phiL / X on an eligible shape returns TT_ERR_INVALID_ARGUMENT in this mode).
- *   TT_MATVEC_AUTO (default): the workspace of TT_MATVEC_THREE_STAGE; the fused kernel where it
- *     was measured faster -- eligible cores with Rl >= 28, rl, rr >= 64 and rl rr nvec <= 300000
- *     (single-vector matvecs, small Krylov blocks, every interface update of such a core) --
- *     the three stages elsewhere and whenever phiL / X are not 16-byte aligned.
+ *   TT_MATVEC_AUTO (default): the workspace of TT_MATVEC_THREE_STAGE; the fused kernel on every
+ *     eligible core where it was measured faster -- Rl >= 28 and rl, rr >= 64 (the config-5
+ *     interior cores: matvecs with any number of columns and every interface update) -- the
+ *     three stages elsewhere and whenever phiL / X are not 16-byte aligned.
  * Every *_workspace_size query and every call of the thread (tt_local_matvec(_batched),
  * tt_sweep_als, tt_sweep_w34, tt_block_local_matvec, the local solvers) follows the mode set
  * at the time of the query / call: size the workspace under the mode the call will run in.

@@ -249,7 +249,6 @@ tt_status tt_local_matvec_batched(int64_t rl, int64_t n, int64_t rr, int64_t Rl,
   double* Pp = c.take(pe);
   if (!c.ok) return fail(TT_ERR_WORKSPACE, "workspace too small after alignment");
   auto body = [&](cudaStream_t s) -> tt_status {
-    FusedAutoScope fused_auto;
     cudaError_t e = enqueue_matvec(d, nvec, phiL, A, phiR, X, Y, T1, T2, Ah, Pp, pe, s);
     return e == cudaSuccess ? TT_OK : cuda_fail(e, "tt_local_matvec_batched");
   };
@@ -299,7 +298,6 @@ static tt_status iface_common(bool left, int64_t rl, int64_t n, int64_t rr, int6
   double* Pp = c.take(pe);
   if (!c.ok) return fail(TT_ERR_WORKSPACE, "workspace too small after alignment");
   auto body = [&](cudaStream_t s) -> tt_status {
-    FusedAutoScope fused_auto;
     cudaError_t e = left ? enqueue_left(d, phi_in, A, x, phi_out, T1, T2, Ah, Pp, pe, s)
                          : (g_dbg_flags & 8) ? enqueue_right(d, phi_in, A, x, phi_out, T1, T2, Ah, Pp, pe, s)
                                               : enqueue_right_mirror(d, phi_in, A, x, phi_out, T1, T2, Ah, Pp, pe, s);

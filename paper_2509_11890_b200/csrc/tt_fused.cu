@@ -9,7 +9,6 @@ namespace ttint {
 // tt_debug_set_fused: 0 policy (default), -1 never, m > 0 whenever eligible with warp-group
 // skew {1, 0, 2}[(m - 1) % 3] k-tiles and option bits (m - 1) / 3 (tt_fused12.cuh)
 thread_local int g_fused_mode = 0;
-thread_local bool g_fused_auto_ctx = false;
 
 // 5-D FP64 view of the Krylov block X (a, j, m, b) for the phase-1 B operand: dims
 // {16 (b lo), a (k), b / 16 (b hi), 4 (j), K (m)}, box {16, 16, 1, 4, 1}: one TMA brings the
@@ -44,15 +43,14 @@ bool fused12_wanted(const Dims& d, long long K) {
 }
 
 // TT_MATVEC_AUTO: the fused kernel where it was measured faster than the two stage GEMMs
-// (tools/fused_probe.py, tools/iface_probe.py): few Krylov columns -- the
-// single-vector matvecs and every interface update -- where the stage GEMMs are a few waves of
-// tiles (r = 256, R = 36: K = 1 -7 %, K = 2 -4 %, K = 4 -1 %, K >= 8 slower; r = 512, K = 1
-// -2 %), and an operator bond that fills the kernel's 36-row a' blocks (R = 16 / 20 / 24: the
-// padded rows cost more than the launch saves).  The workspace keeps T1, so a misaligned
-// operand falls back to the stage GEMMs.
+// (tools/fused_probe.py, tools/iface_probe.py, tools/w5_fused_probe.py):
+// every eligible core whose operator bond fills the kernel's 36-row a' blocks (Rl >= 28; at
+// R = 16 / 20 / 24 the padded rows cost more than the fusion saves) and whose bonds give the
+// 148 CTAs enough units.  The workspace keeps T1, so a misaligned operand falls back to the
+// stage GEMMs.
 bool fused12_auto(const Dims& d, long long K) {
-  if (g_fused_mode != 0 || !g_fused_auto_ctx || !fused12_shape_ok(d, K)) return false;
-  return d.al >= 28 && d.a * d.b * K <= 300000 && d.a >= 64 && d.b >= 64;
+  if (g_fused_mode != 0 || !fused12_shape_ok(d, K)) return false;
+  return d.al >= 28 && d.a >= 64 && d.b >= 64;
 }
 
 // interface updates (their workspace always holds T1, so a misaligned operand just falls back)
@@ -61,20 +59,20 @@ bool fused12_iface_wanted(const Dims& d) {
   return g_fused_mode > 0 || fused12_auto(d, 1);
 }
 
-template <int G>
+template <int G, bool PW, bool RR = false>
 static cudaError_t launch_fused12_g(const Dims& d, long long K, int stage_tag, tt::Fused12Params p,
                                     const CUtensorMap& tl, const CUtensorMap& tx,
                                     const CUtensorMap& ta, cudaStream_t s) {
   using Cfg = tt::F12Cfg<G>;
-  if (cudaError_t e = smem_attr((const void*)tt::fused_s12_kernel<G>, (int)Cfg::kSmemBytes)) return e;
+  if (cudaError_t e = smem_attr((const void*)tt::fused_s12_kernel<G, PW, RR>, (int)Cfg::kSmemBytes)) return e;
   p.nag = (int)((d.a + 2 * G - 1) / (2 * G));
   p.total_units = (int)((long long)p.nag * p.nbt * K);
   p.nag_div = tt::make_fastdiv((uint32_t)p.nag);
   const int grid = (int)std::min<long long>(p.total_units, (long long)num_sms() * (3 - G));
   g_stage = stage_tag;
   // traced as one record with 2 M N K = the flops of both stages
-  const long long tr = trace_begin(-12 - (G == 1), d.a * K * d.b, 4 * d.al, d.a + 4 * d.be, s);
-  if (cudaError_t e = launch_pdl(false, tt::fused_s12_kernel<G>, dim3(grid), dim3(Cfg::kThreads),
+  const long long tr = trace_begin(-12 - (G == 1) - 2 * (G == 2 && !RR ? 1 : 0), d.a * K * d.b, 4 * d.al, d.a + 4 * d.be, s);
+  if (cudaError_t e = launch_pdl(false, tt::fused_s12_kernel<G, PW, RR>, dim3(grid), dim3(Cfg::kThreads + (PW ? 32 : 0)),
                                  Cfg::kSmemBytes, s, tl, tx, ta, p))
     return e;
   trace_end(tr, s);
@@ -112,8 +110,13 @@ cudaError_t launch_fused12(const Dims& d, long long K, const double* phiL, const
   p.dbg = g_dbg_flags;
   p.gate = g_gate;
   // option bit 1: two independent 6-warp CTAs per SM instead of one 12-warp CTA
-  if (p.opt & 2) return launch_fused12_g<1>(d, K, stage_tag, p, tl, tx, ta, s);
-  return launch_fused12_g<2>(d, K, stage_tag, p, tl, tx, ta, s);
+  if (p.opt & 2) return launch_fused12_g<1, false>(d, K, stage_tag, p, tl, tx, ta, s);
+  // Producer placement (config-5 interior core, K = 32): thread 0 of the first consumer warp
+  // 7.00-7.15 ms (option bit 5), a 13th producer warp 6.84 ms (bit 6; 13 warps cap the kernel at
+  // 128 registers), the refill rotating over the 12 consumer warps 6.80 ms (default).
+  if (p.opt & 32) return launch_fused12_g<2, false>(d, K, stage_tag, p, tl, tx, ta, s);
+  if (p.opt & 64) return launch_fused12_g<2, true>(d, K, stage_tag, p, tl, tx, ta, s);
+  return launch_fused12_g<2, false, true>(d, K, stage_tag, p, tl, tx, ta, s);
 }
 
 }  // namespace ttint

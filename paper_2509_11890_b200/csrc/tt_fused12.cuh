@@ -77,12 +77,17 @@ __device__ __forceinline__ void bar_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(n) : "memory");
 }
 
-template <int G>
-__global__ void __launch_bounds__(192 * G, 3 - G)
+// PW: a 13th warp whose lane 0 is the TMA producer (G = 2 only), so that no consumer warp
+// carries the refill on its critical path.
+// RR: no producer warp; the refill rotates over the consumer warps (tt_gemm_v3.cuh RR).
+template <int G, bool PW = false, bool RR = false>
+__global__ void __launch_bounds__(192 * G + (PW ? 32 : 0), 3 - G)
 fused_s12_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_constant__ CUtensorMap tmX,
                  const __grid_constant__ CUtensorMap tmA, const Fused12Params p) {
   using Cfg = F12Cfg<G>;
   constexpr int ST = Cfg::kStages, kF12StageBytes = Cfg::kStageBytes, kF12Threads = Cfg::kThreads;
+  constexpr int kProdTid = PW ? kF12Threads : 0;   // the thread that issues the TMA loads
+  __shared__ volatile int prod_turn;   // RR: the k-tile whose refill is due next
   constexpr int kF12Warps = Cfg::kWarps, kF12T1Bytes = Cfg::kT1Bytes;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[ST], empty_bar[ST];
@@ -109,7 +114,7 @@ fused_s12_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_constant_
   }
   // the k-rows of T1 past 4 al (the last phase-2 k-tile's padding) stay zero for the whole run
   static_assert(kF12T1Bytes % 16 == 0, "");
-  for (int e = tid; e < kF12T1Bytes / 16; e += kF12Threads)
+  for (int e = tid; e < kF12T1Bytes / 16; e += (int)blockDim.x)
     *reinterpret_cast<double2*>(t1s + 16 * e) = make_double2(0.0, 0.0);
   __syncthreads();
   pdl_wait();
@@ -122,9 +127,9 @@ fused_s12_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_constant_
     bt = rest - m * p.nbt;
   };
 
-  const uint64_t pol_keep = tid == 0 ? l2_policy(1) : 0;   // Phi_L and Ahat: re-read by every unit
+  const uint64_t pol_keep = (RR ? lane == 0 : tid == kProdTid) ? l2_policy(1) : 0;   // Phi_L and Ahat: re-read by every unit
   const int KTU = p.KT1 + p.KT2;
-  if (tid == 0) {
+  if (tid == kProdTid) {
     int* ps = prod_state;
     ps[0] = blockIdx.x;
     ps[4] = 0;
@@ -167,8 +172,17 @@ fused_s12_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_constant_
   };
   const int skew = G == 2 ? p.skew : 0;
   const bool trail = skew > 0 && gm == 1;
-  if (tid == 0)
+  if (PW) {
+    if (warp == kF12Warps) {   // producer warp: runs as far ahead as the ring allows
+      if (lane == 0)
+        while (prod_state[0] < p.total_units) produce_one();
+      return;
+    }
+  } else if (tid == 0) {
     for (int s = 0; s < ST - 1 - skew; ++s) produce_one();
+    prod_turn = 0;
+  }
+  if (RR) __syncthreads();
   if (trail) bar_sync(3, kF12Threads);
 
   // ---- per-lane shared-memory byte offsets (tt_gemm_v3.cuh fragment geometry) ------------
@@ -233,7 +247,18 @@ fused_s12_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_constant_
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_bar[s]);
-      if (tid == 0) produce_one();
+      if (RR) {
+        if (lane == 0 && (int)(q % kF12Warps) == warp) {
+          while (prod_turn != (int)q) {
+          }
+          __threadfence_block();
+          produce_one();
+          __threadfence_block();
+          prod_turn = (int)q + 1;
+        }
+      } else if (!PW && tid == 0) {
+        produce_one();
+      }
       __syncwarp();
       ++q;
       if (!released && q == (uint32_t)skew) {
@@ -302,7 +327,18 @@ fused_s12_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_constant_
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_bar[s]);
-      if (tid == 0) produce_one();
+      if (RR) {
+        if (lane == 0 && (int)(q % kF12Warps) == warp) {
+          while (prod_turn != (int)q) {
+          }
+          __threadfence_block();
+          produce_one();
+          __threadfence_block();
+          prod_turn = (int)q + 1;
+        }
+      } else if (!PW && tid == 0) {
+        produce_one();
+      }
       __syncwarp();
       ++q;
       if (!released && q == (uint32_t)skew) {

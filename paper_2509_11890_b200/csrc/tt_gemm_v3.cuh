@@ -148,8 +148,13 @@ struct GemmV3Cfg {
   static constexpr size_t kSmemBytes = (size_t)STAGES * STAGE_BYTES + BRES_BYTES + 1024;
 };
 
+// RR: the refill of the ring (an empty-barrier wait plus the TMA issue) rotates over the warps
+// -- the warp q mod kWarps issues the load that follows k-tile q, in stream order through a
+// shared turn counter -- instead of always falling on warp 0, whose critical path it lengthened
+// (an extra producer warp costs a quarter of the register file: 13 warps put 4 on one
+// sub-partition, 128 registers per thread).
 template <bool A_KC, bool B_KC, int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, int MINB,
-          bool B_RES = false>
+          bool B_RES = false, bool RR = false>
 __global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, MINB)
 dmma_gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const GemmParamsV3 p) {
@@ -166,6 +171,8 @@ dmma_gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp / WARPS_N, wn = warp % WARPS_N;
   const int g = lane >> 2, t = lane & 3;
+  constexpr int kProdTid = 0;   // the thread that issues the prologue's TMA loads
+  __shared__ volatile int prod_turn;   // RR: the k-tile whose refill is due next
 
   // Column offsets of the output map: when the whole N extent is one tile (the operator-core
   // stage, N = n R <= 144) every unit has c_n0 = 0, so the BN offsets are evaluated once into
@@ -226,11 +233,12 @@ dmma_gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     ke = min(p.KT, kb + p.kt_per_split);
   };
 
-  const uint64_t pol_a = (tid == 0 && p.l2_a) ? l2_policy(p.l2_a) : 0;
-  const uint64_t pol_b = (tid == 0 && p.l2_b) ? l2_policy(p.l2_b) : 0;
+  const bool may_produce = RR ? lane == 0 : tid == kProdTid;
+  const uint64_t pol_a = (may_produce && p.l2_a) ? l2_policy(p.l2_a) : 0;
+  const uint64_t pol_b = (may_produce && p.l2_b) ? l2_policy(p.l2_b) : 0;
   // ---- producer state (thread 0 only; kept in shared memory to spare registers) ---------
   __shared__ int prod_state[7];   // u, m0, n0, kt, ke, split, q
-  if (tid == 0) {
+  if (tid == kProdTid) {
     int* ps = prod_state;
     ps[0] = blockIdx.x;
     ps[6] = 0;
@@ -293,14 +301,16 @@ dmma_gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   const int skew = p.skew;
   const bool trail = skew > 0 && warp >= Cfg::kWarps / 2;
   unsigned char* const bres = smem + STAGES * STAGE_BYTES;   // B_RES: resident B k-tiles
-  if (tid == 0) {
+  if (tid == kProdTid) {
     if constexpr (B_RES) {   // the whole B once (one N tile, ksplit 1, KT <= kBresMaxKT)
       mbar_expect_tx(&bres_bar, (uint32_t)(p.KT * Cfg::B_BYTES));
       for (int kt = 0; kt < p.KT; ++kt)
         tma_load_3d(bres + kt * Cfg::B_BYTES, &tmB, 0, kt * Cfg::BK, 0, &bres_bar, pol_b, p.l2_b != 0);
     }
     for (int s = 0; s < STAGES - 1 - skew; ++s) produce_one();
+    prod_turn = 0;
   }
+  if constexpr (RR) __syncthreads();   // the prologue's producer state is visible to every warp
   if (trail) asm volatile("bar.sync 1, %0;\n" ::"r"(Cfg::kThreads) : "memory");
   if constexpr (B_RES) mbar_wait(&bres_bar, 0);
 
@@ -410,7 +420,18 @@ dmma_gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     // release the stage (one arrival per warp), then thread 0 refills the stream
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_bar[s]);
-    if (tid == 0) produce_one();
+    if constexpr (RR) {
+      if (lane == 0 && (int)(q % Cfg::kWarps) == warp) {
+        while (prod_turn != (int)q) {
+        }
+        __threadfence_block();
+        produce_one();
+        __threadfence_block();
+        prod_turn = (int)q + 1;
+      }
+    } else {
+      if (tid == 0) produce_one();
+    }
     __syncwarp();
     ++q;
     if (skew > 0 && !trail && q == (uint32_t)skew)

@@ -273,15 +273,6 @@ cudaError_t enqueue_right_pg(const DimsPG& d, const double* phiR, const double* 
 // ---- fused S1 -> S2 matvec kernel (tt_fused.cu / tt_fused12.cuh) ---------------------------------
 extern thread_local int g_fused_mode;
 extern thread_local bool g_fused_misaligned;
-// The AUTO policy applies inside the single-core entry points only (tt_local_matvec(_batched),
-// tt_interface_left / right): in the sweeps and the block action several chains share the SMs
-// and the one-CTA-per-SM fused kernel was measured slightly slower there.
-extern thread_local bool g_fused_auto_ctx;
-struct FusedAutoScope {
-  bool saved;
-  FusedAutoScope() : saved(g_fused_auto_ctx) { g_fused_auto_ctx = true; }
-  ~FusedAutoScope() { g_fused_auto_ctx = saved; }
-};
 bool fused12_shape_ok(const Dims& d, long long K);
 bool fused12_wanted(const Dims& d, long long K);   // explicit fused mode: no T1 in the workspace
 bool fused12_auto(const Dims& d, long long K);     // AUTO policy (T1 kept as the fallback)
