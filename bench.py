@@ -530,6 +530,10 @@ def main():
     tt.tt_trace_disable()
     stages = {}
     for r in recs:
+        # the fused S1 -> S2 kernel is traced as one mv_s1 record tagged -12 (its 2 M N K = the
+        # flops of both products): reported as its own stage mv_s12
+        if r["stage"] == "mv_s1" and r["tile"] in (-12, -13, -14):
+            r["stage"] = "mv_s12"
         s = stages.setdefault(r["stage"], {"launches": 0, "ms": 0.0, "flops": 0.0})
         s["launches"] += 1
         s["ms"] += r["ms"]
@@ -543,19 +547,25 @@ def main():
         s["tflops"] = s["flops"] / (s["ms"] * 1e-3) / 1e12 if s["ms"] > 0 else None
     dom_name = max((n for n in stages if n.startswith("mv_")), key=lambda n: stages[n]["ms"])
     dom = stages[dom_name]
-    mv_ms = sum(stages[n]["ms"] for n in ("mv_s1", "mv_s2", "mv_s3") if n in stages)
-    mv_flops = sum(stages[n]["flops"] for n in ("mv_s1", "mv_s2", "mv_s3") if n in stages)
+    mv_names = ("mv_s1", "mv_s2", "mv_s12", "mv_s3")
+    mv_ms = sum(stages[n]["ms"] for n in mv_names if n in stages)
+    mv_flops = sum(stages[n]["flops"] for n in mv_names if n in stages)
     mv_tf = mv_flops / (mv_ms * 1e-3) / 1e12
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(dom_name)
+            traffic = json.load(open(tpath)).get("mv_fused12" if dom_name == "mv_s12" else dom_name)
         except Exception:
             traffic = None
-    roofline = {"bound": "tensor", "kernel": f"dmma_gemm ({dom_name})",
+    roofline = {"bound": "tensor",
+                "kernel": "fused_s12_kernel (mv_s12: matvec stages S1 + S2 in one kernel)"
+                if dom_name == "mv_s12" else f"dmma_gemm ({dom_name})",
                 "achieved": dom["tflops"], "peak": p64_sustained, "unit": "TFLOP/s",
                 "frac": dom["tflops"] / p64_sustained, "traffic": traffic,
+                "traffic_note": "ncu dram__bytes_read.sum + dram__bytes_write.sum of ONE launch at the "
+                                "config-5 interior core (profiles/ncu_traffic.json); per_launch "
+                                "below averages over the step's launches (boundary cores included)",
                 "per_launch": {"flops": dom["flops"] / dom["launches"],
                                "ms": dom["ms"] / dom["launches"], "launches_per_step":
                                dom["launches_per_step"]},
@@ -703,7 +713,7 @@ def main():
             torch.cuda.synchronize(dev)
             frecs = [tt.tt_trace_read(i) for i in range(tt.tt_trace_count())]
             tt.tt_trace_disable()
-            fk = [r for r in frecs if r["stage"] == "mv_s1" and r["tile"] == -12]
+            fk = [r for r in frecs if r["stage"] == "mv_s1" and r["tile"] in (-12, -13, -14)]
             fk_ms = sum(r["ms"] for r in fk)
             fk_fl = sum(2.0 * r["M"] * r["N"] * r["K"] for r in fk)
             same = all(torch.equal(a, b) for a, b in zip(Y_f, S0["Y"]))

@@ -167,8 +167,11 @@ cudaError_t launch_v2_l(const GemmParams& p, cudaStream_t s) {
 }
 
 
+// RR (round-robin producer, tt_gemm_v3.cuh) by default on tiles of 8 and more warps: the
+// 4-warp latency tiles of configs 2 / 3 lost 3 % with it (W34 87 -> 90 us, 152 -> 156 us; its
+// extra block barrier after the prologue), the 8- to 16-warp tiles gain 1-2 %.
 template <bool AK, bool BK_, int BM, int BN, int WM, int WN, int MINB, bool BRES = false,
-          bool RR = false>
+          bool RR = (WM * WN >= 8)>
 cudaError_t launch_v3_cfg(const GemmParams& p0, cudaStream_t s, bool& ok) {
   using Probe = tt::GemmV3Cfg<AK, BK_, BM, BN, WM, WN, 1, MINB, BRES>;
   constexpr size_t budget = (MINB == 1 ? 224 : MINB == 2 ? 110 : 54) * 1024 - 1024;
@@ -401,19 +404,19 @@ cudaError_t launch_v3_l(const GemmParams& p, cudaStream_t s, bool& ok) {
     if (g_dbg_flags & 2097152) return launch_v3_cfg<AK, BK_, 128, 144, 2, 6, 1>(p, s, ok);
     // round-robin producer (tt_gemm_v3.cuh RR): S1 / S2 / S3 of the config-5 interior matvec
     // 4.379 / 2.515 / 4.425 -> 4.328 / 2.466 / 4.360 ms; debug bit 30 restores thread 0
-    if (g_dbg_flags & (1 << 30)) return launch_v3_cfg<AK, BK_, 128, 144, 4, 3, 1>(p, s, ok);
-    return launch_v3_cfg<AK, BK_, 128, 144, 4, 3, 1, false, true>(p, s, ok);
+    if (g_dbg_flags & (1 << 30)) return launch_v3_cfg<AK, BK_, 128, 144, 4, 3, 1, false, false>(p, s, ok);
+    return launch_v3_cfg<AK, BK_, 128, 144, 4, 3, 1>(p, s, ok);
   }
-  if (BK_ && (g_dbg_flags & (1 << 30))) return launch_v3_cfg<AK, BK_, 128, 128, 4, 4, 1>(p, s, ok);
-  if (BK_) return launch_v3_cfg<AK, BK_, 128, 128, 4, 4, 1, false, true>(p, s, ok);
+  if (BK_ && (g_dbg_flags & (1 << 30))) return launch_v3_cfg<AK, BK_, 128, 128, 4, 4, 1, false, false>(p, s, ok);
+  if (BK_) return launch_v3_cfg<AK, BK_, 128, 128, 4, 4, 1>(p, s, ok);
   if (g_variant == 5) return launch_v3_cfg<AK, BK_, 128, 64, 4, 2, 2>(p, s, ok);   // probes
   if (g_variant == 6) return launch_v3_cfg<AK, BK_, 128, 128, 4, 4, 1>(p, s, ok);
   if (g_variant == 7) return launch_v3_cfg<AK, BK_, 64, 128, 2, 4, 2>(p, s, ok);
   // 128 x 144 tiles on 12 warps of 32 x 48 (first stage 34.0 -> 35.4 TFLOP/s, W5 sweep
   // -0.75 % on top of the operator-core change; bit 22 restores 128 x 128 on 8 x 2 warps)
   if (g_dbg_flags & 4194304) return launch_v3_cfg<AK, BK_, 128, 128, 8, 2, 1>(p, s, ok);
-  if (g_dbg_flags & (1 << 30)) return launch_v3_cfg<AK, BK_, 128, 144, 4, 3, 1>(p, s, ok);
-  return launch_v3_cfg<AK, BK_, 128, 144, 4, 3, 1, false, true>(p, s, ok);
+  if (g_dbg_flags & (1 << 30)) return launch_v3_cfg<AK, BK_, 128, 144, 4, 3, 1, false, false>(p, s, ok);
+  return launch_v3_cfg<AK, BK_, 128, 144, 4, 3, 1>(p, s, ok);
 }
 
 
