@@ -15,7 +15,7 @@ def main(path, per_step=None, skip=0):
     ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
     for r in rd:
         name = r[ki]
-        if not re.search(r"dmma_gemm|apply_|perm_|set_one|splitk|prep_all|prep_core|transpose_core|swap_bonds", name):
+        if not re.search(r"dmma_gemm|fused_s12|small_chain|apply_|perm_|set_one|splitk|prep_all|prep_core|transpose_core|swap_bonds", name):
             continue
         v = float(r[vi].replace(",", ""))
         v = v / 1e6 if r[ui] == "ns" else (v / 1e3 if r[ui] == "us" else v)
