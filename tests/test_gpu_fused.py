@@ -234,3 +234,61 @@ def test_interface_updates_through_fused_kernel(tt, mode):
         assert any(r["tile"] == -12 and r["stage"] == "ir_s1" for r in recR), recR
         assert rel(h(outL), oracle.interface_left(pl, A, x)) <= TOL
         assert rel(h(outR), oracle.interface_right(pr, A, x)) <= TOL
+
+
+@pytest.mark.parametrize("mode", ["auto", "fused"])
+@pytest.mark.parametrize("shape", [(66, 80, 28, 36, 3), (64, 64, 36, 36, 1), (70, 96, 33, 8, 2)])
+def test_fused_kernel_writes_stay_in_bounds(tt, shape, mode):
+    """Guard zones (compute-sanitizer is closed on this pool): the output Y and the workspace --
+    under "fused" the compact one without T1 -- sit inside larger sentinel-filled buffers; after
+    a matvec and both interface updates through the fused kernel the guards are untouched, the
+    inputs unchanged and the results equal to the oracle.  Ragged a' groups (66, 70), k-tile
+    padding in both phases (Rl = 33: 132 of 144 k-rows; rl = 66: 66 of 80)."""
+    import oracle
+    rl, rr, Rl, Rr, nvec = shape
+    SENT, GUARD, WGUARD = 4321.5, 512, 1 << 16
+    rng = np.random.default_rng(sum(shape) + 3)
+    pl, A = rng.standard_normal((rl, Rl, rl)), rng.standard_normal((Rl, 4, 4, Rr))
+    pr, X = rng.standard_normal((rr, Rr, rr)), rng.standard_normal((rl, 4, nvec, rr))
+    ins = [g(pl), g(A), g(pr), g(X)]
+    before = [t.clone() for t in ins]
+
+    def guarded(shp):
+        n = int(np.prod(shp))
+        big = torch.full((2 * GUARD + n,), SENT, dtype=torch.float64, device="cuda")
+        return big, big[GUARD:GUARD + n].view(*shp)
+
+    def intact(big, shp):
+        n = int(np.prod(shp))
+        return bool((big[:GUARD] == SENT).all()) and bool((big[GUARD + n:] == SENT).all())
+
+    tt.tt_set_matvec_mode(mode)
+    try:
+        need = tt.lib.tt_local_matvec_workspace_size(rl, 4, rr, Rl, Rr, nvec)
+        bigW = torch.full((need + WGUARD,), 0xAB, dtype=torch.uint8, device="cuda")
+        bigY, Y = guarded((rl, 4, nvec, rr))
+        tt.tt_trace_enable(16)
+        tt.tt_local_matvec_batched(*ins, Y, workspace=bigW[:need])
+        torch.cuda.synchronize()
+        recs = [tt.tt_trace_read(i) for i in range(tt.tt_trace_count())]
+        tt.tt_trace_disable()
+        assert any(r["tile"] == -12 for r in recs)
+        assert intact(bigY, Y.shape) and bool((bigW[need:] == 0xAB).all())
+        assert rel(h(Y), oracle.local_matvec_batched(pl, A, pr, X)) <= TOL
+        # interface updates of the same core
+        x = np.ascontiguousarray(X[:, :, 0, :])
+        needi = tt.lib.tt_interface_workspace_size(rl, 4, rr, Rl, Rr)
+        bigWi = torch.full((needi + WGUARD,), 0xAB, dtype=torch.uint8, device="cuda")
+        bigL, outL = guarded((rr, Rr, rr))
+        bigR, outR = guarded((rl, Rl, rl))
+        tt.tt_interface_left(ins[0], ins[1], g(x), outL, workspace=bigWi[:needi])
+        tt.tt_interface_right(ins[2], ins[1], g(x), outR, workspace=bigWi[:needi])
+        torch.cuda.synchronize()
+        assert intact(bigL, outL.shape) and intact(bigR, outR.shape)
+        assert bool((bigWi[needi:] == 0xAB).all())
+        assert rel(h(outL), oracle.interface_left(pl, A, x)) <= TOL
+        assert rel(h(outR), oracle.interface_right(pr, A, x)) <= TOL
+    finally:
+        tt.tt_set_matvec_mode("auto")
+    for a, b in zip(ins, before):
+        assert torch.equal(a, b)
