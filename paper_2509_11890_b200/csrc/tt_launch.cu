@@ -171,8 +171,12 @@ int latency_choice(const GemmParams& p, bool a_kc, bool b_kc, int& ks_out) {
   for (int i = 0; i < (int)(sizeof(kLatencyCands) / sizeof(kLatencyCands[0])); ++i) {
     const TileCand& c = kLatencyCands[i];
     if (lat_knobs().mask & (1u << i)) continue;
+    // the one-CTA-per-SM 128 x 128 tile only for the multi-GFLOP stages (config-5 interior,
+    // K = 1): under config 4's concurrent chains it cost 10 % (W34 597 -> 654 us)
+    if (c.id == 18 && 2.0 * p.M * p.N * p.K < 2.0e9) continue;
     (void)a_kc; (void)b_kc;   // every candidate's BM, BN are multiples of 16 (any operand layout)
-    for (int ks = 1; ks <= 16; ks *= 2) {
+    static const int kSplits[] = {1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 12, 14, 16};
+    for (int ks : kSplits) {
       if (ks > 1 && (KT < 2 * ks || g_pscratch == nullptr || (long long)ks * p.M * p.N > g_pscratch_elems))
         break;
       const double t = latency_estimate(c, p.M, p.N, p.K, ks);

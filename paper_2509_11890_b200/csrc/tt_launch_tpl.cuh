@@ -30,6 +30,9 @@ constexpr TileCand kLatencyCands[] = {
     {10, 128, 64, 8, 2, 0.90}, {11, 64, 64, 8, 2, 0.83}, {12, 64, 64, 4, 4, 0.85},
     {13, 64, 32, 4, 4, 0.82},  {14, 32, 64, 4, 4, 0.82}, {15, 32, 32, 4, 4, 0.75},
     {16, 64, 112, 8, 2, 0.80}, {21, 64, 144, 8, 2, 0.85}, {17, 64, 48, 8, 2, 0.78},
+    // one 16-warp CTA per SM: with a non-power-of-two split it fills 144 of 148 SMs where the
+    // 128 x 64 tiles reach 128 (the K = 1 matvec's last stage at r = 256: 16 tiles x 9 splits)
+    {18, 128, 128, 16, 1, 0.93},
     // (12-warp 128 x 144 / 128 x 96 and 6-warp 64 x 144 / 64 x 96 candidates were measured
     // and dropped: config-4 W34 0.73 -> 0.84 ms; the 6-warp tiles reach only 28 TF/s at scale)
 };
@@ -332,6 +335,7 @@ cudaError_t launch_v3_l(const GemmParams& p, cudaStream_t s, bool& ok) {
         case 16: return launch_v3_cfg<AK, BK_, 64, 112, 8, 1, 2>(p, s, ok);
         case 17: return launch_v3_cfg<AK, BK_, 64, 48, 8, 1, 2>(p, s, ok);
         case 21: return launch_v3_cfg<AK, BK_, 64, 144, 4, 2, 2>(p, s, ok);
+        case 18: return launch_v3_cfg<AK, BK_, 128, 128, 4, 4, 1>(p, s, ok);
         default: break;
       }
     }
