@@ -53,7 +53,8 @@ void tt_debug_set_variant(int v);
  * interface updates of the sweeps as three stage GEMMs each instead of fused one-CTA runs, bit 29
  * the orthonormalisation steps of tt_round / tt_orthonormalise through the Gram matrix instead
  * of the cluster Householder QR, bit 27 the operator apply with the register-blocked kernel instead
- * of the operator-stationary row-block kernel.
+ * of the operator-stationary row-block kernel, bit 30 the 12- and 16-warp stage GEMM tiles with
+ * thread 0 as the TMA producer instead of the round-robin producer (same results).
  * tt_debug_set_variant(v): v >= 10 forces
  * the GEMM tile configuration v % 100 (probe list in csrc/tt_launch_tpl.cuh) and split-K factor v / 100. */
 void tt_debug_set_flags(int flags);
@@ -62,8 +63,13 @@ void tt_debug_set_flags(int flags);
  * version, measured faster), 1 = on with 4-warp 64 x 64 tiles, 2 = 8-warp. */
 void tt_debug_set_dag(int mode);
 /* Benchmark / test hook: the fused S1 -> S2 matvec kernel (csrc/tt_fused12.cuh: T1 stays in
- * shared memory) on the calling thread: 0 = policy (default), -1 = never, 1 = whenever the
- * shape is eligible (warp-group skew 1 k-tile), 2 / 3 = eligible with skew 0 / 2. */
+ * shared memory) on the calling thread: 0 = policy (default: TT_MATVEC_AUTO), -1 = never,
+ * m > 0 = whenever the shape is eligible (workspaces sized without T1), with warp-group skew
+ * {1, 0, 2}[(m - 1) % 3] k-tiles and option bits (m - 1) / 3: bit 0 keeps the barrier before
+ * the hand-over, bit 1 two 6-warp CTAs per SM, bit 5 thread 0 as the TMA producer, bit 6 a
+ * 13th producer warp (default: round-robin over the consumer warps); bits 2-4 are timing
+ * probes of a debug build (no loads / no T2 stores / no hand-over: WRONG results).
+ * m = 2 is what tt_set_matvec_mode(TT_MATVEC_FUSED) selects. */
 void tt_debug_set_fused(int mode);
 /* Measurement hook: while buf != NULL (device, 5 x uint64 per unit, cap_units units) the next
  * DAG launches of the calling thread record per unit {grab, ready, computed, published,

@@ -292,3 +292,25 @@ def test_fused_kernel_writes_stay_in_bounds(tt, shape, mode):
         tt.tt_set_matvec_mode("auto")
     for a, b in zip(ins, before):
         assert torch.equal(a, b)
+
+
+def test_round_robin_producer_equals_thread0_producer(tt):
+    """The stage GEMMs with the round-robin TMA producer (default on tiles of 8+ warps) and with
+    thread 0 as the producer (debug bit 30) run the same arithmetic: bit-identical results on a
+    shape that takes the 12-warp 128 x 144 and the 16-warp 128 x 128 tiles (three-stage path),
+    and the fused kernel's three producer placements agree bit for bit as well."""
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    r = lambda *s: torch.randn(*s, dtype=torch.float64, device="cuda", generator=gen)
+    phiL, A, phiR, X = r(256, 36, 256), r(36, 4, 4, 36), r(256, 36, 256), r(256, 4, 8, 256)
+    outs = {}
+    for name, fused, flags in [("rr", -1, 0), ("t0", -1, 1 << 30), ("f_rr", 2, 0), ("f_t0", 98, 0),
+                               ("f_pw", 194, 0)]:
+        tt.tt_debug_set_fused(fused)
+        tt.tt_debug_set_flags(flags)
+        try:
+            outs[name] = tt.tt_local_matvec_batched(phiL, A, phiR, X)
+        finally:
+            tt.tt_debug_set_fused(0)
+            tt.tt_debug_set_flags(0)
+    for name in ("t0", "f_rr", "f_t0", "f_pw"):
+        assert torch.equal(outs[name], outs["rr"]), name
