@@ -13,9 +13,14 @@
 //   phase 2: per a': T2 tile (16 b) x (4 be), K = 4 al, B = the prepared operator core
 //            Ahat[(al j), (i be)] streamed through the same ring (k-tiles of 16 x 144).
 // 12 warps in two groups of 6; a group owns two of the four a' in both phases, so the
-// hand-over needs only group-local named barriers and one group's epilogues fall on the other
-// group's DMMA stream (the trailing group starts `skew` k-tiles late).  The k-tile stream is
-// continuous across phases and units (persistent CTAs, one per SM).
+// hand-over needs only a group-local named barrier.  The k-tile stream is continuous across
+// phases and units (persistent CTAs, one per SM); the refill of the ring rotates over the 12
+// consumer warps (template RR: warp q mod 12 issues the load that follows k-tile q, in stream
+// order through a shared turn counter) -- with thread 0 of warp 0 as the only producer that
+// warp's critical path set the pace of the whole CTA (7.15 ms against 6.80 ms at the config-5
+// interior core, K = 32; a 13th producer warp, template PW: 6.84 ms at 128 registers).
+// Probe variants kept for A/B: G = 1 (two 6-warp CTAs per SM), a start skew
+// between the two groups, the barrier before the hand-over.
 //
 // Preconditions (host-checked in tt_fused.cu, else the three-stage path): n = 4, al <= 36,
 // be <= 36 with 4 be a multiple of 16, b a multiple of 16, a even, 16-byte aligned bases.

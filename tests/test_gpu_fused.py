@@ -314,3 +314,22 @@ def test_round_robin_producer_equals_thread0_producer(tt):
             tt.tt_debug_set_flags(0)
     for name in ("t0", "f_rr", "f_t0", "f_pw"):
         assert torch.equal(outs[name], outs["rr"]), name
+
+
+def test_auto_falls_back_for_misaligned_operands(tt):
+    """TT_MATVEC_AUTO keeps T1 in the workspace: an 8-byte-aligned X (or phiL) on an eligible
+    core silently takes the stage GEMMs and still matches the oracle."""
+    import oracle
+    rl, rr, Rl, Rr, nvec = 64, 64, 36, 36, 2
+    rng = np.random.default_rng(41)
+    phiL, A = rng.standard_normal((rl, Rl, rl)), rng.standard_normal((Rl, 4, 4, Rr))
+    phiR, X = rng.standard_normal((rr, Rr, rr)), rng.standard_normal((rl, 4, nvec, rr))
+    base = torch.empty(X.size + 1, dtype=torch.float64, device="cuda")
+    Xm = base[1:].view(rl, 4, nvec, rr)
+    Xm.copy_(g(X))
+    Y, recs = _stages(tt, lambda: tt.tt_local_matvec_batched(g(phiL), g(A), g(phiR), Xm))
+    assert not any(r["tile"] == -12 for r in recs)
+    assert rel(h(Y), oracle.local_matvec_batched(phiL, A, phiR, X)) <= TOL
+    Y2, recs2 = _stages(tt, lambda: tt.tt_local_matvec_batched(g(phiL), g(A), g(phiR), g(X)))
+    assert any(r["tile"] == -12 for r in recs2)
+    assert rel(h(Y2), h(Y)) <= 1e-13
