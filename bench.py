@@ -991,6 +991,12 @@ def main():
                     "ranks_out": [1] + [int(c.shape[2]) for c in rounded],
                     "ms": wall(lambda: tt.tt_round(xs, 1e-4), reps=3),
                     "note": "synchronous (data-dependent ranks); host wall time"}
+        pad, rk_dev = tt.tt_round_async(xs, 1e-4)
+        rnd_info["async"] = {"ms": wall(lambda: tt.tt_round_async(xs, 1e-4), reps=3),
+                             "ranks_equal_sync": [int(v) for v in rk_dev.tolist()] == rnd_info["ranks_out"],
+                             "note": "tt_round_async: device-side rank decisions into zero-padded "
+                                     "max-rank cores, no host synchronisation (graph-capturable)"}
+        del pad
         gen = torch.Generator(device=dev).manual_seed(13)
         rnd = lambda *sh: torch.randn(*sh, dtype=torch.float64, device=dev, generator=gen)
         Wh = rnd(cfg.r[k], cfg.N, 4, cfg.r[k + 1])

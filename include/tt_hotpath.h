@@ -163,6 +163,24 @@ tt_status tt_round(int64_t d, const int64_t* n, const int64_t* r_in,
                    double* const* cores_out, void* workspace, size_t workspace_bytes,
                    void* stream);
 
+/* tt_round_async: the same rounding with every truncation decision taken on
+ * the device -- no host read of a singular value, no synchronisation, graph-capturable.  The
+ * cores keep host-known STORAGE ranks r_storage[d+1] (host, written before the call returns:
+ * r_in, except that a bond wider than its unfolding's other side shrinks to it) and are
+ * zero-padded: cores_out[k] is a contiguous (r_storage[k], n[k], r_storage[k+1]) array whose
+ * entries with a bond index >= the effective rank are exactly 0, so the padded train
+ * represents the rounded tensor as it stands and can be passed to every other entry point;
+ * r_dev[d+1] (DEVICE int64) receives the effective ranks (r_dev[0] = r_dev[d] = 1), equal to
+ * tt_round's r_out (same formulas and summation order).  A consumer that wants compact cores
+ * reads r_dev when convenient and slices.  Truncation goes through the Gram matrix as in
+ * tt_round's default route, so delta / sqrt(d-1) >= 1e-7 is required (TT_ERR_INVALID_ARGUMENT
+ * otherwise; use tt_round).  Other arguments, workspace (tt_round_workspace_size) and
+ * errors as tt_round.  The work is that of an untruncated pass (max-rank GEMMs). */
+tt_status tt_round_async(int64_t d, const int64_t* n, const int64_t* r_in,
+                         const double* const* cores_in, double delta, int64_t max_rank,
+                         int64_t* r_storage, int64_t* r_dev, double* const* cores_out,
+                         void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---------------------------------------------------------------------------------------
  * projected KKT block system action: several
  * operators sharing one frame W_{!=k} act on a Block-TT core whose block index is the KKT

@@ -30,7 +30,7 @@ __all__ = [
     "tt_local_gmres_workspace_size",
     "tt_local_matvec_two_site", "tt_local_matvec_two_site_workspace_size",
     "tt_block_local_matvec", "tt_block_local_matvec_workspace_size", "TTBlockTerm",
-    "tt_round", "tt_round_workspace_size", "tt_debug_sym_eigen", "tt_debug_svd",
+    "tt_round", "tt_round_async", "tt_compact", "tt_round_workspace_size", "tt_debug_sym_eigen", "tt_debug_svd",
     "tt_local_lobpcg", "tt_local_lobpcg_workspace_size", "tt_merge_operator_cores",
     "tt_orthonormalise", "tt_orthonormalise_workspace_size", "tt_block_move_right",
     "tt_block_move_left", "tt_block_move_workspace_size", "tt_pg_workspace_size",
@@ -85,6 +85,8 @@ lib.tt_round_workspace_size.restype = _sz
 lib.tt_round_workspace_size.argtypes = [_i64, _p, _p]
 lib.tt_round.argtypes = [_i64, _p, _p, _p, ctypes.c_double, _i64, _p, _p, _p, _sz, _p]
 lib.tt_round.restype = ctypes.c_int
+lib.tt_round_async.argtypes = [_i64, _p, _p, _p, ctypes.c_double, _i64, _p, _p, _p, _p, _sz, _p]
+lib.tt_round_async.restype = ctypes.c_int
 lib.tt_debug_sym_eigen.argtypes = [_i64, _p, _p, _p, _p, _sz, _p]
 lib.tt_debug_sym_eigen.restype = ctypes.c_int
 lib.tt_debug_svd.argtypes = [_i64, _i64, _p, _p, _p, _p, _p, _p]
@@ -802,6 +804,39 @@ def tt_round(cores, delta, max_rank=0, workspace=None, stream=None):
     ro = list(rout)
     return [outs[k].reshape(-1)[: ro[k] * n[k] * ro[k + 1]].reshape(ro[k], n[k], ro[k + 1])
             for k in range(d)]
+
+
+def tt_round_async(cores, delta, max_rank=0, workspace=None, stream=None, ranks=None):
+    """Asynchronous TT rounding: device-side rank decisions, no host
+    synchronisation, graph-capturable.  Returns (padded_cores, ranks): zero-padded cores with
+    the host-known storage ranks and a device int64 tensor (d + 1) of the effective ranks;
+    tt_compact(padded_cores, ranks) slices them (that reads the ranks: a synchronisation)."""
+    d = len(cores)
+    a64 = lambda v: (ctypes.c_int64 * len(v))(*v)
+    _check_vector_train(cores)
+    n = [int(c.shape[1]) for c in cores]
+    r = [int(c.shape[0]) for c in cores] + [int(cores[-1].shape[2])]
+    outs = [torch.empty_like(c) for c in cores]
+    if ranks is None:
+        ranks = torch.empty(d + 1, dtype=torch.int64, device=cores[0].device)
+    elif ranks.dtype != torch.int64 or ranks.numel() != d + 1 or ranks.device != cores[0].device:
+        raise ValueError("ranks must be a device int64 tensor of d + 1 entries")
+    rst = (ctypes.c_int64 * (d + 1))()
+    ws = _ws(int(lib.tt_round_workspace_size(d, a64(n), a64(r))), workspace, cores[0].device)
+    _check(lib.tt_round_async(d, a64(n), a64(r), _ptrs(cores, "cores"), float(delta),
+                              int(max_rank), rst, ranks.data_ptr(), _ptrs(outs, "cores_out"),
+                              ws.data_ptr(), ws.numel(), _stream(stream)))
+    rs = list(rst)
+    padded = [outs[k].reshape(-1)[: rs[k] * n[k] * rs[k + 1]].reshape(rs[k], n[k], rs[k + 1])
+              for k in range(d)]
+    return padded, ranks
+
+
+def tt_compact(padded_cores, ranks):
+    """Slice the zero-padded cores of tt_round_async to their effective ranks (reads `ranks`
+    from the device: synchronises)."""
+    ro = [int(v) for v in ranks.tolist()]
+    return [c[: ro[k], :, : ro[k + 1]].contiguous() for k, c in enumerate(padded_cores)]
 
 
 def _check_vector_train(cores) -> None:

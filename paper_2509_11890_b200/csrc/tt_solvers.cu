@@ -208,10 +208,69 @@ __global__ void svd_select_kernel(const double* __restrict__ BJ, const double* _
   }
 }
 
+// Device-side truncation decision of the asynchronous rounding (tt_round_async): from the
+// descending Gram eigenvalues lam[0..m) it drops the numerical zeros (lam <= zero_rel lam_0),
+// then -- with use_thr -- the longest tail whose Frobenius norm sqrt(sum lam) stays <= thr
+// (first core: thr = fac * sqrt(sum lam) is computed here and kept in thr_dev for the later
+// cores), caps at max_rank, writes the rank to *r_dev and the two zero-padded m x m factors
+// Bm1 = V[:, :sk] diag(lam^-1/2), Bm2 = V[:, :sk] diag(lam^1/2) (columns >= sk exactly zero).
+// Same formulas, summation order and IEEE operations as the host loop of tt_round.
+__global__ void __launch_bounds__(256) trunc_decide_kernel(
+    const double* __restrict__ lam, const double* __restrict__ V, int m, int use_thr, int first,
+    double fac, long long max_rank, double zero_rel, double* __restrict__ thr_dev,
+    long long* __restrict__ r_dev, double* __restrict__ Bm1, double* __restrict__ Bm2) {
+  __shared__ int s_sk;
+  if (threadIdx.x == 0) {
+    const double l0 = lam[0];
+    int nz = 0;
+    for (int i = 0; i < m; ++i)
+      if (lam[i] > zero_rel * l0 && lam[i] > 0.0) ++nz;
+    if (nz == 0) nz = 1;
+    int sk = nz;
+    if (use_thr) {
+      double thr;
+      if (first) {
+        double nrm2 = 0.0;
+        for (int i = 0; i < m; ++i) nrm2 += fmax(lam[i], 0.0);
+        thr = fac * sqrt(nrm2);
+        *thr_dev = thr;
+      } else {
+        thr = *thr_dev;
+      }
+      double tail = 0.0;
+      for (int i = nz - 1; i >= 1; --i) {
+        tail += fmax(lam[i], 0.0);
+        if (sqrt(tail) <= thr) sk = i; else break;
+      }
+      if (max_rank > 0 && sk > max_rank) sk = (int)max_rank;
+    }
+    s_sk = sk;
+    if (r_dev) *r_dev = sk;
+  }
+  __syncthreads();
+  const int sk = s_sk;
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+    const int c = e % m;
+    double a = 0.0, b = 0.0;
+    if (c < sk) {
+      const double v = V[e];
+      a = v * (1.0 / sqrt(fmax(lam[c], 1e-300)));
+      b = v * sqrt(fmax(lam[c], 0.0));
+    }
+    Bm1[e] = a;
+    Bm2[e] = b;
+  }
+}
+__global__ void set_rank_kernel(long long* r_dev, long long idx, long long val) { r_dev[idx] = val; }
+
 static tt_status round_impl(int64_t d, const int64_t* n, const int64_t* r_in,
                             const double* const* cores_in, double delta, int64_t max_rank,
                             int64_t* r_out, double* const* cores_out, void* workspace,
-                            size_t workspace_bytes, void* stream, int phases, const char* who) {
+                            size_t workspace_bytes, void* stream, int phases, const char* who,
+                            int64_t* r_dev = nullptr) {
+  // r_dev != nullptr: asynchronous mode (tt_round_async) -- no host read of any singular value;
+  // r_out receives the STORAGE ranks (host-known), r_dev (device) the effective ranks
+  const bool async = r_dev != nullptr;
   if (d <= 0) return fail(TT_ERR_INVALID_ARGUMENT, "d must be >= 1");
   if (!n || !r_in || !cores_in || !r_out || !cores_out) return fail(TT_ERR_NULL_POINTER, "NULL array");
   if (r_in[0] != 1 || r_in[d] != 1) return fail(TT_ERR_INVALID_ARGUMENT, "r_1 and r_{d+1} must be 1");
@@ -300,6 +359,26 @@ static tt_status round_impl(int64_t d, const int64_t* n, const int64_t* r_in,
     g_stage = TT_ST_IL_S1;
     e = launch_gemm(true, true, gp(W[k], q, W[k], q, G, rk, rk, q, tt::map_plain(rk),
                                    tt::map_plain(1)), s);
+    if (async) {   // full-size zero-padded factors, the rank stays on the device
+      if (e == cudaSuccess) e = launch_sym_eigen(G, V, lam, (int)rk, esc, s);
+      if (e != cudaSuccess) break;
+      trunc_decide_kernel<<<1, 256, 0, s>>>(lam, V, (int)rk, 0, 0, 0.0, 0, zero_rel, dg, nullptr,
+                                            Bm, G);
+      ++g_launches;
+      if ((e = cudaGetLastError()) != cudaSuccess) break;
+      // Tmp (rk x q) = (V S^-1)^T W_k (rows >= rank zero)
+      e = launch_gemm(false, false, gp(Bm, rk, W[k], q, Tmp, rk, q, rk, tt::map_plain(q),
+                                       tt::map_plain(1)), s);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(W[k], Tmp, sizeof(double) * rk * q, cudaMemcpyDeviceToDevice, s);
+      if (e != cudaSuccess) break;
+      const long long m1a = r[k - 1] * n[k - 1];
+      e = launch_gemm(true, false, gp(W[k - 1], rk, G, rk, Tmp, m1a, rk, rk, tt::map_plain(rk),
+                                      tt::map_plain(1)), s);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(W[k - 1], Tmp, sizeof(double) * m1a * rk, cudaMemcpyDeviceToDevice, s);
+      continue;
+    }
     if (e == cudaSuccess) e = eig((int)rk);
     if (e != cudaSuccess) break;
     int sk = 0;
@@ -359,7 +438,7 @@ static tt_status round_impl(int64_t d, const int64_t* n, const int64_t* r_in,
   // preconditioned dgejsv, where R's own columns need 11-26+ growing with the condition)
   // where the Gram route's floor (singular values below ~1e-8 sigma_max unresolved) reaches the
   // per-core threshold: delta / sqrt(d-1) < 1e-7, delta = 0 included; debug bit 24 forces it.
-  const bool accurate = (phases & 2) &&
+  const bool accurate = !async && (phases & 2) &&
       ((g_dbg_flags & (1 << 24)) || delta / std::sqrt((double)std::max<int64_t>(d - 1, 1)) < 1e-7);
   int64_t kstart = 0;   // the Gram route continues from the first core the accurate one left
   for (int64_t k = 0; accurate && k < d - 1 && e == cudaSuccess; ++k) {
@@ -442,6 +521,29 @@ static tt_status round_impl(int64_t d, const int64_t* n, const int64_t* r_in,
     g_stage = TT_ST_IL_S2;
     e = launch_gemm(false, false, gp(W[k], rk1, W[k], rk1, G, rk1, rk1, m, tt::map_plain(rk1),
                                      tt::map_plain(1)), s);
+    if (async) {   // device-side rank decision, full-size zero-padded update GEMMs
+      if (e == cudaSuccess) e = launch_sym_eigen(G, V, lam, (int)rk1, esc, s);
+      if (e != cudaSuccess) break;
+      const double fac = delta / std::sqrt((double)std::max<int64_t>(d - 1, 1));
+      trunc_decide_kernel<<<1, 256, 0, s>>>(lam, V, (int)rk1, 1, k == 0 ? 1 : 0, fac,
+                                            (long long)max_rank, zero_rel, dg,
+                                            reinterpret_cast<long long*>(r_dev) + k + 1, Bm, G);
+      ++g_launches;
+      if ((e = cudaGetLastError()) != cudaSuccess) break;
+      // U (m x rk1) = W_k . (V S^-1) (columns >= rank zero)
+      e = launch_gemm(true, false, gp(W[k], rk1, Bm, rk1, Tmp, m, rk1, rk1, tt::map_plain(rk1),
+                                      tt::map_plain(1)), s);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(W[k], Tmp, sizeof(double) * m * rk1, cudaMemcpyDeviceToDevice, s);
+      if (e != cudaSuccess) break;
+      // W_{k+1} (rk1 x q) = (V S)^T . W_{k+1} (rows >= rank zero)
+      const long long qa2 = n[k + 1] * r[k + 2];
+      e = launch_gemm(false, false, gp(G, rk1, W[k + 1], qa2, Tmp, rk1, qa2, rk1, tt::map_plain(qa2),
+                                       tt::map_plain(1)), s);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(W[k + 1], Tmp, sizeof(double) * rk1 * qa2, cudaMemcpyDeviceToDevice, s);
+      continue;
+    }
     if (e == cudaSuccess) e = eig((int)rk1);
     if (e != cudaSuccess) break;
     if (k == 0) {
@@ -482,7 +584,14 @@ static tt_status round_impl(int64_t d, const int64_t* n, const int64_t* r_in,
   for (int64_t k = 0; k < d && e == cudaSuccess; ++k)
     e = cudaMemcpyAsync(cores_out[k], W[k], sizeof(double) * r[k] * n[k] * r[k + 1],
                         cudaMemcpyDeviceToDevice, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (async && e == cudaSuccess) {
+    set_rank_kernel<<<1, 1, 0, s>>>(reinterpret_cast<long long*>(r_dev), 0, 1);
+    set_rank_kernel<<<1, 1, 0, s>>>(reinterpret_cast<long long*>(r_dev), d, 1);
+    g_launches += 2;
+    e = cudaGetLastError();
+  } else if (e == cudaSuccess) {
+    e = cudaStreamSynchronize(s);
+  }
   if (e != cudaSuccess) return cuda_fail(e, who);
   for (int64_t k = 0; k <= d; ++k) r_out[k] = r[k];
   return TT_OK;
@@ -495,6 +604,20 @@ tt_status tt_round(int64_t d, const int64_t* n, const int64_t* r_in,
   CallScope scope;
   return round_impl(d, n, r_in, cores_in, delta, max_rank, r_out, cores_out, workspace,
                     workspace_bytes, stream, 3, "tt_round");
+}
+
+tt_status tt_round_async(int64_t d, const int64_t* n, const int64_t* r_in,
+                         const double* const* cores_in, double delta, int64_t max_rank,
+                         int64_t* r_storage, int64_t* r_dev, double* const* cores_out,
+                         void* workspace, size_t workspace_bytes, void* stream) {
+  CallScope scope;
+  if (!r_dev) return fail(TT_ERR_NULL_POINTER, "r_dev is NULL");
+  if (!(delta >= 0.0) || delta / std::sqrt((double)std::max<int64_t>(d - 1, 1)) < 1e-7)
+    return fail(TT_ERR_INVALID_ARGUMENT,
+                "tt_round_async truncates through the Gram matrix: delta / sqrt(d-1) must be "
+                ">= 1e-7 (use tt_round for tighter tolerances)");
+  return round_impl(d, n, r_in, cores_in, delta, max_rank, r_storage, cores_out, workspace,
+                    workspace_bytes, stream, 3, "tt_round_async", r_dev);
 }
 
 size_t tt_orthonormalise_workspace_size(int64_t d, const int64_t* n, const int64_t* r) {

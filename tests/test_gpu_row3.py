@@ -256,3 +256,113 @@ def test_tt_round_accurate_route(tt, delta):
         assert err <= delta * (1 + 1e-6)
         ref = oracle_round(x, delta)
         assert [c.shape for c in out] == [c.shape for c in ref]
+
+
+# ----------------------------------------------------------------------------------------
+# tt_round_async: device-side rank decisions into zero-padded max-rank cores
+# ----------------------------------------------------------------------------------------
+def _sum_train(a, b):
+    d, out = len(a), []
+    for k in range(d):
+        ca, cb = a[k], b[k]
+        if k == 0:
+            out.append(np.concatenate([ca, cb], axis=2))
+        elif k == d - 1:
+            out.append(np.concatenate([ca, cb], axis=0))
+        else:
+            c = np.zeros((ca.shape[0] + cb.shape[0], ca.shape[1], ca.shape[2] + cb.shape[2]))
+            c[:ca.shape[0], :, :ca.shape[2]] = ca
+            c[ca.shape[0]:, :, ca.shape[2]:] = cb
+            out.append(c)
+    return out
+
+
+def _async_case(case):
+    rng = np.random.default_rng(77)
+    if case == "random":
+        return ttgen.gaussian_tt_vector(rng, 4, [1, 4, 12, 16, 9, 3, 1])
+    if case == "sum":       # exactly rank-deficient formal sum T + S + T
+        base = ttgen.gaussian_tt_vector(rng, 4, [1, 4, 6, 6, 4, 1])
+        x = _sum_train(base, ttgen.gaussian_tt_vector(rng, 4, [1, 3, 5, 5, 3, 1]))
+        return _sum_train(x, base)
+    if case == "wide":      # bonds wider than their unfoldings: the storage ranks shrink
+        return ttgen.gaussian_tt_vector(rng, 2, [1, 5, 9, 20, 7, 1])
+    return ttgen.make_inputs(3).x
+
+
+@pytest.mark.parametrize("case", ["random", "sum", "wide", "config3"])
+@pytest.mark.parametrize("delta", [1e-2, 1e-5])
+def test_tt_round_async_equals_sync_and_oracle(tt, case, delta):
+    """The asynchronous rounding takes the oracle's ranks on the device, its padding is exactly
+    zero, the padded train is the rounded tensor as it stands, and the compacted cores agree
+    with the synchronous call and the oracle (dense reconstructions)."""
+    from oracle.rounding import tt_round as oracle_round
+    x = _async_case(case)
+    xg = [g(c) for c in x]
+    padded, ranks = tt.tt_round_async(xg, delta)
+    sync = [h(c) for c in tt.tt_round(xg, delta)]
+    ro = [int(v) for v in ranks.tolist()]
+    assert ro == [1] + [c.shape[2] for c in sync]
+    yo = oracle_round(x, delta)
+    assert ro == [1] + [c.shape[2] for c in yo]
+    for k, c in enumerate(padded):   # storage ranks chain, padding exactly zero
+        assert c.shape[0] >= ro[k] and c.shape[2] >= ro[k + 1]
+        if k + 1 < len(padded):
+            assert c.shape[2] == padded[k + 1].shape[0]
+        ch = h(c)
+        assert not ch[ro[k]:, :, :].any() and not ch[:, :, ro[k + 1]:].any()
+    comp = [h(c) for c in tt.tt_compact(padded, ranks)]
+    assert [c.shape for c in comp] == [c.shape for c in sync]
+    v = full_vector(x)
+    vp, vc, vs, vo = (full_vector([h(c) for c in padded]), full_vector(comp), full_vector(sync),
+                      full_vector(yo))
+    assert np.array_equal(vp, vc) or rel_fro(vp, vc) <= 1e-15
+    assert rel_fro(vc, vs) <= 1e-10 and rel_fro(vc, vo) <= 1e-10
+    assert np.linalg.norm(vc - v) / np.linalg.norm(v) <= delta * (1 + 1e-6)
+
+
+def test_tt_round_async_max_rank_and_errors(tt):
+    rng = np.random.default_rng(78)
+    x = [g(c) for c in ttgen.gaussian_tt_vector(rng, 4, [1, 4, 12, 16, 9, 3, 1])]
+    padded, ranks = tt.tt_round_async(x, 1e-3, max_rank=5)
+    sync = tt.tt_round(x, 1e-3, max_rank=5)
+    assert [int(v) for v in ranks.tolist()] == [1] + [c.shape[2] for c in sync]
+    assert max(int(v) for v in ranks.tolist()) == 5
+    comp = tt.tt_compact(padded, ranks)
+    assert rel_fro(full_vector([h(c) for c in comp]), full_vector([h(c) for c in sync])) <= 1e-10
+    with pytest.raises(tt.TTError):      # below the Gram route's floor: tt_round's job
+        tt.tt_round_async(x, 1e-9)
+    with pytest.raises(tt.TTError):
+        tt.tt_round_async(x, 0.0)
+
+
+def test_tt_round_async_graph_capture(tt):
+    """No host synchronisation inside: the call is captured into a CUDA graph and the replay
+    follows new core values in the same buffers."""
+    rng = np.random.default_rng(79)
+    ranks_in = [1, 4, 10, 12, 6, 1]
+    x0 = ttgen.gaussian_tt_vector(rng, 4, ranks_in)
+    low = ttgen.gaussian_tt_vector(rng, 4, [1, 2, 3, 3, 2, 1])
+    x1 = _sum_train(low, low)                      # rank-deficient: other ranks, same shapes?
+    x1 = [np.pad(c, [(0, a.shape[0] - c.shape[0]), (0, 0), (0, a.shape[2] - c.shape[2])])
+          for c, a in zip(x1, x0)]
+    bufs = [g(c) for c in x0]
+    n = [4] * len(bufs)
+    ws = torch.empty(tt.tt_round_workspace_size(n, ranks_in), dtype=torch.uint8, device="cuda")
+    rk = torch.zeros(len(bufs) + 1, dtype=torch.int64, device="cuda")
+    s = torch.cuda.Stream()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        tt.tt_round_async(bufs, 1e-4, workspace=ws, stream=s, ranks=rk)   # warm (attributes)
+        s.synchronize()
+        with torch.cuda.graph(graph, stream=s):
+            padded, rk2 = tt.tt_round_async(bufs, 1e-4, workspace=ws, stream=s, ranks=rk)
+    for xs in (x1, x0):
+        for b, c in zip(bufs, xs):
+            b.copy_(g(c))
+        graph.replay()
+        torch.cuda.synchronize()
+        ref = tt.tt_round([g(c) for c in xs], 1e-4)
+        assert [int(v) for v in rk.tolist()] == [1] + [c.shape[2] for c in ref]
+        comp = tt.tt_compact(padded, rk)
+        assert rel_fro(full_vector([h(c) for c in comp]), full_vector([h(c) for c in ref])) <= 1e-10
