@@ -18,10 +18,10 @@ extern "C" {
 #endif
 
 /* Test hook: eigendecomposition of a symmetric n x n matrix G (overwritten; n <= 2048) by the
- * rounding's parallel Jacobi solver (element-wise for n <= 64, block Jacobi above; debug flag
+ * rounding's parallel Jacobi solver (element-wise for n < 24, block Jacobi above; debug flag
  * 256 forces the element-wise kernel): V columns = eigenvectors, lam descending.  Workspace
- * >= max(4 ne^2, 2 nb^2 + 32 nb) + 8200 doubles, ne = n rounded up to even, nb = n rounded
- * up to a multiple of 32. */
+ * >= max(4 ne^2, 2 nb^2 + 64 nb) + 8200 doubles, ne = n rounded up to even, nb = n rounded
+ * up to a multiple of 64. */
 tt_status tt_debug_sym_eigen(int64_t n, double* G, double* V, double* lam, void* workspace,
                              size_t workspace_bytes, void* stream);
 
@@ -35,7 +35,9 @@ void tt_debug_set_variant(int v);
  * become WRONG; times the main loop / epilogue / load path in isolation) -- these two bits are
  * honoured only by a debug build (-DTT_DEBUG_HOOKS, `TT_DEBUG_HOOKS=1` at build time) and
  * masked off otherwise; bit 3 computes the
- * right interface update directly instead of as the mirrored left update (same result); bit 4
+ * right interface update directly instead of as the mirrored left update (same result); bit 16
+ * runs the Jacobi eigensolver's first block kernel (full inner sweeps, textbook rotations,
+ * scalar updates) and bit 2 the current one with blocks of 32 instead of 16; bit 4
  * disables the TMA L2 cache-policy hints, bit 5 only the evict_first ones, bit 6 only the
  * evict_last ones, bit 7 issues M/N-contiguous tiles as 2-D boxes, bits 9/10 order the tiles
  * M-grouped by 8 / M-fastest, bit 8 forces the element-wise Jacobi (same results), bit 11

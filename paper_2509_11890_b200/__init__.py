@@ -1043,8 +1043,8 @@ def tt_debug_sym_eigen(G, stream=None):
     Gc = G.clone()
     V = torch.empty_like(Gc)
     lam = torch.empty(n, dtype=torch.float64, device=G.device)
-    npe, npb = (n + 1) // 2 * 2, (n + 31) // 32 * 32
-    elems = max(4 * npe * npe, 2 * npb * npb + (npb // 32) * 1024) + 2 * 4096 + 8
+    npe, npb = (n + 1) // 2 * 2, (n + 63) // 64 * 64
+    elems = max(4 * npe * npe, 2 * npb * npb + 64 * npb) + 2 * 4096 + 8
     ws = torch.empty(elems * 8, dtype=torch.uint8, device=G.device)
     _check(lib.tt_debug_sym_eigen(n, _dev(Gc, "G"), _dev(V, "V"), _dev(lam, "lam"), ws.data_ptr(),
                                   ws.numel(), _stream(stream)))

@@ -11,17 +11,36 @@ namespace ttint {
 #include "tt_lobpcg.cuh"
 
 // Symmetric eigendecomposition of the n x n Gram matrix G: lam (descending) and V (columns)
-// in the caller's buffers.  n <= 64: element-wise cooperative Jacobi (4 padded np x np
+// in the caller's buffers.  n < 24: element-wise cooperative Jacobi (4 padded np x np
 // buffers, np = n rounded up to even); larger n: block Jacobi (G and V padded to a multiple
-// of 32 plus the per-pair rotations).  Scratch: sym_eigen_scratch(n) doubles.
-constexpr int kBlockJacobiMin = 65;
+// of 32 -- 64 for the BS = 32 probe variant -- plus the per-pair rotations).  Scratch:
+// sym_eigen_scratch(n) doubles.
+constexpr int kBlockJacobiMin = 24;   // below: the element-wise kernel (measured faster)
+constexpr int kJBig = 64;             // padding granularity of the block kernels (2 BS, BS = 32)
 long long sym_eigen_scratch(long long n) {
   const long long np = (n + 1) & ~1LL;
-  const long long nb = (n + kJB2 - 1) / kJB2 * kJB2;
-  const long long elem = 4 * np * np, blk = 2 * nb * nb + (nb / kJB2) * kJB2 * kJB2;
+  const long long nb = (n + kJBig - 1) / kJBig * kJBig;
+  const long long elem = 4 * np * np, blk = 2 * nb * nb + nb * kJBig;
   return std::max(elem, blk) + 2 * 4096 + 8;
 }
 thread_local int g_eigen_elementwise = 0;   // test hook: force the element-wise kernel
+template <int BS>
+static cudaError_t launch_block2(double* G0, double* V0, int np, double* Rbuf, double* part,
+                                 cudaStream_t s) {
+  using C = Jb2<BS>;
+  int per_sm = 0;
+  if (cudaError_t e = smem_attr((const void*)jacobi_block2_kernel<BS>, (int)C::kSmem)) return e;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_block2_kernel<BS>, C::kLaunch,
+                                                C::kSmem);
+  const int m = np / C::B2;
+  int grid = num_sms() * std::max(per_sm, 1);
+  const int tasks = 2 * m * m;
+  if (grid > tasks) grid = tasks;
+  int sweeps = 40;
+  void* args[] = {&G0, &V0, (void*)&np, &sweeps, &Rbuf, &part};
+  return cudaLaunchCooperativeKernel((const void*)jacobi_block2_kernel<BS>, grid, C::kLaunch,
+                                     args, C::kSmem, s);
+}
 cudaError_t launch_sym_eigen(const double* G, double* V, double* lam, int n, double* scratch,
                              cudaStream_t s) {
   g_stage = TT_ST_PERM;
@@ -30,27 +49,36 @@ cudaError_t launch_sym_eigen(const double* G, double* V, double* lam, int n, dou
   cudaGetDevice(&dev);
   cudaError_t e;
   if (n >= kBlockJacobiMin && !g_eigen_elementwise) {
-    const int np = (n + kJB2 - 1) / kJB2 * kJB2;
+    // debug bit 16: the first block kernel (BS = 16, full inner sweeps, scalar updates);
+    // bit 2: the second kernel with BS = 32 instead of 16 (measured slower below n = 1024)
+    const bool v1 = (g_dbg_flags & (1 << 16)) != 0, bs16 = v1 || (g_dbg_flags & (1 << 2)) == 0;
+    const int gran = bs16 ? kJB2 : kJBig;
+    const int np = (n + gran - 1) / gran * gran;
     const long long NN = (long long)np * np;
     double* G0 = scratch;
     double* V0 = G0 + NN;
     double* Rbuf = V0 + NN;
-    const int m = np / kJB2;   // block pairs per step
-    double* part = Rbuf + (long long)m * kJB2 * kJB2;
+    const int m = np / gran;   // block pairs per step
+    double* part = Rbuf + (long long)m * gran * gran;
     int* which = reinterpret_cast<int*>(part + 2 * 4096);
     long long eb = std::min<long long>(4096, (NN + 255) / 256);
     embed_kernel<<<(unsigned)eb, 256, 0, s>>>(G, G0, n, np);
     ++g_launches;
     if ((e = cudaMemsetAsync(which, 0, sizeof(int), s)) != cudaSuccess) return e;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_block_coop_kernel, 256, 0);
-    int grid = num_sms() * std::max(per_sm, 1);
-    const int tasks = m * m + (np / kJB2) * m;
-    if (grid > tasks) grid = tasks;
-    if (grid > 4096) grid = 4096;
-    int sweeps = 40;
-    int npi = np;
-    void* args[] = {&G0, &V0, (void*)&npi, &sweeps, &Rbuf, &part};
-    e = cudaLaunchCooperativeKernel((const void*)jacobi_block_coop_kernel, grid, 256, args, 0, s);
+    if (v1) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_block_coop_kernel, 256, 0);
+      int grid = num_sms() * std::max(per_sm, 1);
+      const int tasks = m * m + (np / kJB2) * m;
+      if (grid > tasks) grid = tasks;
+      if (grid > 4096) grid = 4096;
+      int sweeps = 40;
+      int npi = np;
+      void* args[] = {&G0, &V0, (void*)&npi, &sweeps, &Rbuf, &part};
+      e = cudaLaunchCooperativeKernel((const void*)jacobi_block_coop_kernel, grid, 256, args, 0, s);
+    } else {
+      e = bs16 ? launch_block2<16>(G0, V0, np, Rbuf, part, s)
+               : launch_block2<32>(G0, V0, np, Rbuf, part, s);
+    }
     ++g_launches;
     if (e != cudaSuccess) return e;
     sort_padded_kernel<<<(n + 255) / 256, 256, 0, s>>>(G0, G0, V0, V0, which, V, lam, n, np);
