@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(256) jacobi_block_coop_kernel(double* __restri
 //  * the 2BS x 2BS x 2BS products of the update phase on the FP64 tensor cores (DMMA.8x8x4;
 //    the scalar version made n >= 512 shared-memory bound), all three operands of a task
 //    loaded in one round trip, T = S R_cols written over S for the second product.
-// Dynamic shared memory: 3 (2BS)(2BS + 1) doubles.
+// Dynamic shared memory: 3 (2BS)(2BS + 4) doubles.
 __device__ __forceinline__ void jb2_rotation(double app, double aqq, double apq, double& c,
                                              double& s) {
   // (c, s) annihilating apq, |theta| <= pi/4, without the textbook three divisions and two
@@ -365,12 +365,13 @@ __device__ __forceinline__ void jb2_dmma(double (&c)[2], double a, double b) {
 }
 template <int BS>
 struct Jb2 {
-  static constexpr int B2 = 2 * BS, LD = B2 + 1;
+  static constexpr int B2 = 2 * BS, LD = B2 + 1;        // odd stride: the inner sweeps' accesses
+  static constexpr int LDB = B2 + 4;                    // update phase: conflict-free DMMA fragments
   static constexpr int kThreads = BS * 16;              // update warps: 256 / 512 threads
   static constexpr int kLaunch = kThreads + 32;         // + the rotation warp of the inner sweeps
   static constexpr int kRowTiles = B2 / 8;              // 8-row DMMA tiles of a block
   static constexpr int kNT = B2 / 16;                   // 8-column tiles per warp (half a block)
-  static constexpr size_t kSmem = 3 * (size_t)B2 * LD * sizeof(double);
+  static constexpr size_t kSmem = 3 * (size_t)B2 * LDB * sizeof(double);
 };
 template <int BS>
 __global__ void __launch_bounds__(Jb2<BS>::kLaunch) jacobi_block2_kernel(
@@ -380,9 +381,13 @@ __global__ void __launch_bounds__(Jb2<BS>::kLaunch) jacobi_block2_kernel(
   constexpr int B2 = C::B2, LD = C::LD, NTL = C::kNT;
   cooperative_groups::grid_group grid = cooperative_groups::this_grid();
   extern __shared__ double jsm[];
+  constexpr int LDB = C::LDB;
   double (*S)[LD] = reinterpret_cast<double (*)[LD]>(jsm);
-  double (*R)[LD] = reinterpret_cast<double (*)[LD]>(jsm + B2 * LD);
-  double (*R2)[LD] = reinterpret_cast<double (*)[LD]>(jsm + 2 * B2 * LD);
+  double (*R)[LD] = reinterpret_cast<double (*)[LD]>(jsm + B2 * LDB);
+  double (*R2)[LD] = reinterpret_cast<double (*)[LD]>(jsm + 2 * B2 * LDB);
+  double (*Sb)[LDB] = reinterpret_cast<double (*)[LDB]>(jsm);               // update-phase views
+  double (*Rb)[LDB] = reinterpret_cast<double (*)[LDB]>(jsm + B2 * LDB);
+  double (*R2b)[LDB] = reinterpret_cast<double (*)[LDB]>(jsm + 2 * B2 * LDB);
   __shared__ double cs[2][BS], sn[2][BS];
   __shared__ int pp[2][BS], qq[2][BS], pos[2][B2];
   __shared__ double red[2 * C::kLaunch / 32];
@@ -579,9 +584,9 @@ __global__ void __launch_bounds__(Jb2<BS>::kLaunch) jacobi_block2_kernel(
           int gi;
           if (isG) gi = (i < BS ? Pr * BS + i : Qr * BS + i - BS);
           else gi = rb * B2 + i;
-          S[i][j] = isG ? G[(long long)gi * np + gj] : V[(long long)gi * np + gj];
-          R[i][j] = Rc[e];
-          if (isG) R2[i][j] = Rr[e];
+          Sb[i][j] = isG ? G[(long long)gi * np + gj] : V[(long long)gi * np + gj];
+          Rb[i][j] = Rc[e];
+          if (isG) R2b[i][j] = Rr[e];
         }
         __syncthreads();
         const bool mmaw = warp < C::kThreads / 32;   // the rotation warp only helps with loads
@@ -590,24 +595,24 @@ __global__ void __launch_bounds__(Jb2<BS>::kLaunch) jacobi_block2_kernel(
         for (int t = 0; t < NTL; ++t) c[t][0] = c[t][1] = 0.0;
 #pragma unroll 4
         for (int kk = 0; mmaw && kk < B2 / 4; ++kk) {   // T = S R_cols
-          const double a = S[fr][4 * kk + fk];
+          const double a = Sb[fr][4 * kk + fk];
 #pragma unroll
-          for (int t = 0; t < NTL; ++t) jb2_dmma(c[t], a, R[4 * kk + fk][fc + 8 * t]);
+          for (int t = 0; t < NTL; ++t) jb2_dmma(c[t], a, Rb[4 * kk + fk][fc + 8 * t]);
         }
         if (isG) {   // S <- T, then out = R_rows^T T
           __syncthreads();
 #pragma unroll
           for (int t = 0; mmaw && t < NTL; ++t) {
-            S[fr][oc + 8 * t] = c[t][0];
-            S[fr][oc + 8 * t + 1] = c[t][1];
+            Sb[fr][oc + 8 * t] = c[t][0];
+            Sb[fr][oc + 8 * t + 1] = c[t][1];
             c[t][0] = c[t][1] = 0.0;
           }
           __syncthreads();
 #pragma unroll 4
           for (int kk = 0; mmaw && kk < B2 / 4; ++kk) {
-            const double a = R2[4 * kk + fk][fr];
+            const double a = R2b[4 * kk + fk][fr];
 #pragma unroll
-            for (int t = 0; t < NTL; ++t) jb2_dmma(c[t], a, S[4 * kk + fk][fc + 8 * t]);
+            for (int t = 0; t < NTL; ++t) jb2_dmma(c[t], a, Sb[4 * kk + fk][fc + 8 * t]);
           }
         }
         if (mmaw) {   // the thread's outputs: row fr, columns oc + 8 t, + 1 (one BS-column half)
