@@ -622,6 +622,47 @@ def test_block_and_elementwise_jacobi_agree(tt):
         assert np.allclose(G @ V, V * lam, atol=1e-10 * 5)
 
 
+@pytest.mark.parametrize("flags", [0, 1 << 2, 1 << 16])
+@pytest.mark.parametrize("n", [24, 33, 64, 100, 256])
+def test_block_jacobi_kernels_agree_with_lapack(tt, n, flags):
+    """Every block-Jacobi kernel (default: cross-pair inner sweeps + two-rsqrt rotations + DMMA
+    updates, blocks of 16; bit 2: blocks of 32; bit 16: the first kernel) against LAPACK on a
+    Gram matrix graded over 12 decades, including sizes that pad (33, 100)."""
+    rng = np.random.default_rng(1000 + n)
+    Q = np.linalg.qr(rng.standard_normal((n, n)))[0]
+    lamv = np.logspace(0, -12, n)
+    G = (Q * lamv) @ Q.T
+    G = (G + G.T) / 2
+    tt.tt_debug_set_flags(flags)
+    try:
+        lam, V = tt.tt_debug_sym_eigen(g(G))
+        torch.cuda.synchronize()
+    finally:
+        tt.tt_debug_set_flags(0)
+    ref = np.linalg.eigvalsh(G)[::-1]
+    assert np.allclose(h(lam), ref, rtol=0, atol=8 * n * 2.2e-16)   # both sides err ~ n eps
+    Vh = h(V)
+    assert np.abs(Vh.T @ Vh - np.eye(n)).max() <= 1e-12
+    assert np.abs(G @ Vh - Vh * h(lam)).max() <= 1e-13
+
+
+@pytest.mark.parametrize("scale", [1e-60, 1.0, 1e60])
+def test_block_jacobi_scale_invariance(tt, scale):
+    """The rotations are computed from power-of-two-scaled entries: the eigenvectors of s G are
+    those of G and the eigenvalues scale, for s far from 1 (|s G|^2 still representable)."""
+    rng = np.random.default_rng(77)
+    n = 96
+    M = rng.standard_normal((3 * n, n))
+    G = M.T @ M
+    lam1, V1 = tt.tt_debug_sym_eigen(g(G))
+    lams, Vs = tt.tt_debug_sym_eigen(g(G * scale))
+    torch.cuda.synchronize()
+    assert np.allclose(h(lams) / scale, h(lam1), rtol=1e-13)
+    Vh = h(Vs)
+    assert np.abs(Vh.T @ Vh - np.eye(n)).max() <= 1e-12
+    assert np.abs((G * scale) @ Vh - Vh * h(lams)).max() <= 1e-12 * scale * h(lam1)[0]
+
+
 # ----------------------------------------------------------------------------------------
 # W34 as one DAG-scheduled call (tt_sweep_w34)
 # ----------------------------------------------------------------------------------------
