@@ -5,14 +5,15 @@
 // (M^T M -> eigenvectors) squares the condition number; Householder reflections do not.  A
 // config-5 interior unfolding (1024 x 256, 2 MB) is spread over the distributed shared memory of
 // a 16-CTA cluster (64 rows per CTA), so every column step works on-chip:
-//   step j:  sigma^2 = sum_{i>j} M[i][j]^2 (per-CTA partials combined through DSMEM in rank
+//   step j:  sigma^2 = sum_{i>j} M[i][j]^2 and the dots of the column with the trailing ones
+//            (per-CTA partials combined through DSMEM in rank
 //            order, identical in every CTA), the reflector (LAPACK dlarfg convention:
 //            beta = -sign(x_j) ||x||, tau = (beta - x_j) / beta, v = x / (x_j - beta), v_j = 1)
 //            stored in place below the diagonal;
 //            w = v^T M[j:, j+1:] (DSMEM-combined partials), M[i][col] -= tau v_i w[col].
 //   then R is read off the upper triangle and Q = H_0 ... H_{k-1} [I; 0] is formed in place
 //   backwards (LAPACK dorg2r order).
-// Two cluster barriers per reflector and per backward step; every reduction is deterministic.
+// One cluster barrier per reflector and per backward step; every reduction is deterministic.
 // Included by tt_solvers.cu inside namespace ttint.
 
 constexpr int kQrThreads = 512;
@@ -28,16 +29,6 @@ struct QrArgs {
   int rb;              // rows per CTA
 };
 
-__device__ __forceinline__ double qr_block_sum(double v, double* red, int tid) {
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-  __syncthreads();
-  if ((tid & 31) == 0) red[tid >> 5] = v;
-  __syncthreads();
-  double s = 0.0;
-  for (int w = 0; w < kQrThreads / 32; ++w) s += red[w];
-  return s;
-}
-
 __global__ void __launch_bounds__(kQrThreads) qr_cluster_kernel(const QrArgs p) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
@@ -49,7 +40,7 @@ __global__ void __launch_bounds__(kQrThreads) qr_cluster_kernel(const QrArgs p) 
   double* inbox = A + (size_t)rb * ld;   // [2][16][c + 2] partials pushed by every CTA
   double* tau = inbox + 2 * 16 * (c + 2);   // [k]
   double* wv = tau + k;                  // [c + 2] combined sums
-  __shared__ double red[kQrThreads / 32];
+  double* rowj = wv + (c + 2);           // [2][c] row j of the current reflector (from its owner)
   const int r0 = rank * rb;
   const int nr = max(0, min(rb, m - r0));   // rows held by this CTA
   for (int e = tid; e < nr * c; e += kQrThreads) {
@@ -103,19 +94,33 @@ __global__ void __launch_bounds__(kQrThreads) qr_cluster_kernel(const QrArgs p) 
   };
 
   // ---- factorisation ---------------------------------------------------------------------
+  // ONE cluster reduction per reflector: with x = M[j:, j], every CTA pushes its partials of
+  // y[q] = sum_{i > j} x_i M[i][j + q], q = 0 .. c - j - 1 (q = 0: sigma^2, the squared norm
+  // below the diagonal), and the owner of row j broadcasts M[j][j:]; after the barrier each
+  // CTA derives beta, tau, the scaling of v and w = v^T M[j:, j+1:] = M[j][col] + scal y[col]
+  // locally (v_j = 1, v_i = scal x_i) -- the same reflector as the two-reduction form (norm,
+  // then v^T M), the sums in another order.
   for (int j = 0; j < k; ++j) {
     const int owner = j / rb;
     const int par = red_no++ & 1;
-    double s2 = 0.0;
-    for (int i = tid; i < nr; i += kQrThreads)
-      if (r0 + i > j) s2 = fma(A[i * ld + j], A[i * ld + j], s2);
-    s2 = qr_block_sum(s2, red, tid);
-    if (tid < ncl) {
-      push(par, 0, s2, tid);
-      push(par, 1, (rank == owner) ? A[(j - r0) * ld + j] : 0.0, tid);
+    const int ib1 = max(0, min(nr, j + 1 - r0));   // first local row with global index > j
+    const int ncol = c - j;
+    for (int col = j + warp; col < c; col += kWarps) {
+      double s = 0.0;
+      for (int i = ib1 + lane; i < nr; i += 32) s = fma(A[i * ld + j], A[i * ld + col], s);
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane < ncl) push(par, col - j, s, lane);
     }
-    gather(par, 2, wv);
-    const double sigma2 = wv[0], xj = wv[1];
+    if (rank == owner) {
+      const double* row = A + (size_t)(j - r0) * ld + j;
+      for (int e = tid; e < ncol * ncl; e += kQrThreads) {
+        const int r = e / ncol, q = e - r * ncol;
+        cluster.map_shared_rank(rowj, r)[par * c + q] = row[q];
+      }
+    }
+    gather(par, ncol, wv);
+    const double* rj = rowj + par * c;
+    const double sigma2 = wv[0], xj = rj[0];
     double t = 0.0, beta = xj, scal = 0.0;
     if (sigma2 > 0.0) {
       beta = -copysign(sqrt(fma(xj, xj, sigma2)), xj);
@@ -123,13 +128,24 @@ __global__ void __launch_bounds__(kQrThreads) qr_cluster_kernel(const QrArgs p) 
       scal = 1.0 / (xj - beta);
     }
     if (tid == 0) tau[j] = t;
-    for (int i = tid; i < nr; i += kQrThreads) {
-      const int gi = r0 + i;
-      if (gi > j) A[i * ld + j] *= scal;
-      else if (gi == j) A[i * ld + j] = beta;
+    for (int q = 1 + tid; q < ncol; q += kQrThreads) wv[q] = fma(scal, wv[q], rj[q]);   // w
+    __syncthreads();
+    for (int i = ib1 + warp; i < nr; i += kWarps) {   // rows below j: v_i = scal x_i
+      const double vi = A[i * ld + j] * scal;
+      const double tv = -t * vi;
+      if (t != 0.0)
+        for (int col = j + 1 + lane; col < c; col += 32)
+          A[i * ld + col] = fma(tv, wv[col - j], A[i * ld + col]);
+      __syncwarp();
+      if (lane == 0) A[i * ld + j] = vi;
+    }
+    if (rank == owner) {   // row j: v_j = 1
+      double* row = A + (size_t)(j - r0) * ld;
+      if (t != 0.0)
+        for (int col = j + 1 + tid; col < c; col += kQrThreads) row[col] = fma(-t, wv[col - j], row[col]);
+      if (tid == 0) row[j] = beta;
     }
     __syncthreads();
-    if (j + 1 < c && t != 0.0) apply_reflector(j, j + 1, c, t);   // t is uniform: same branch in every CTA
   }
   // ---- R: the upper triangle of rows 0..k-1 ----------------------------------------------
   for (int e = tid; e < nr * c; e += kQrThreads) {
@@ -191,7 +207,7 @@ inline int qr_cluster_size(int m, int c) {
 inline size_t qr_smem(int m, int c, int cl) {
   const long long rb = (m + cl - 1) / cl;
   const int k = std::min(m, c);
-  return sizeof(double) * (size_t)(rb * (c + 1) + 2 * 16 * (c + 2) + k + c + 2);
+  return sizeof(double) * (size_t)(rb * (c + 1) + 2 * 16 * (c + 2) + k + c + 2 + 2 * c);
 }
 inline bool qr_fits(int m, int c) {
   if (m <= 0 || c <= 0 || c > kQrThreads * 4) return false;
