@@ -66,29 +66,68 @@ __global__ void __launch_bounds__(kQrThreads) qr_cluster_kernel(const QrArgs p) 
     }
     __syncthreads();
   };
-  // w[col] = sum_{i >= j} v_i M[i][col] for col in [c0, c1), v_j = 1, v_i = A[i][j] below;
-  // then M[i][col] -= t v_i w[col].  Warps own columns for the dots (lanes over rows, shuffle
-  // reduction) and rows for the update (lanes over columns): no integer division, no serial
-  // FMA chains longer than rb / 32.
   const int lane = tid & 31, warp = tid >> 5;
   constexpr int kWarps = kQrThreads / 32;
+  // Partial dots of column j with the columns [c0, c1), local rows with global index > j:
+  //   s[col] = sum_i A[i][j] A[i][col]  (+ A[j][col] in the owner of row j when unit_diag),
+  // pushed to slot col - c0 of every CTA's inbox.  A half-warp owns 16 consecutive columns
+  // (conflict-free row reads, the A[i][j] factor a broadcast) and one row parity; the row
+  // loop carries two independent accumulators and no shuffles except the final parity add.
+  auto dots = [&](int par, int j, int c0, int c1, bool unit_diag) {
+    const int ib1 = max(0, min(nr, j + 1 - r0));   // first local row with global index > j
+    const int h = lane >> 4;
+    const bool diag_here = unit_diag && j >= r0 && j < r0 + nr;
+    for (int q0 = c0; q0 < c1; q0 += kWarps * 16) {
+      const int col = q0 + warp * 16 + (lane & 15);
+      const bool on = col < c1;
+      double s0 = 0.0, s1 = 0.0;
+      if (on) {
+        const double* a = A + col;
+        const double* x = A + j;
+        int i = ib1 + h;
+#pragma unroll 2
+        for (; i + 2 < nr; i += 4) {
+          s0 = fma(x[i * ld], a[i * ld], s0);
+          s1 = fma(x[(i + 2) * ld], a[(i + 2) * ld], s1);
+        }
+        if (i < nr) s0 = fma(x[i * ld], a[i * ld], s0);
+        if (diag_here && h == 0) s1 += a[(j - r0) * ld];
+      }
+      double sv = s0 + s1;
+      sv += __shfl_xor_sync(0xffffffffu, sv, 16);
+      if (on)
+        for (int r = h; r < ncl; r += 2) push(par, col - c0, sv, r);
+    }
+  };
+  // A[i][col] += tv w[col - wo] for col in [c0, c1): one row per warp, eight columns per lane
+  // loaded before any store (the compiler cannot reorder shared-memory loads across the stores
+  // of a rolled loop, which serialised the latencies)
+  auto row_axpy = [&](double* row, double tv, int c0, int c1, const double* w, int wo) {
+    for (int cb = c0; cb < c1; cb += 256) {
+      double a[8], ww[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int col = cb + lane + 32 * u;
+        a[u] = col < c1 ? row[col] : 0.0;
+        ww[u] = col < c1 ? w[col - wo] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int col = cb + lane + 32 * u;
+        if (col < c1) row[col] = fma(tv, ww[u], a[u]);
+      }
+    }
+  };
+  // w[col] = sum_{i >= j} v_i M[i][col] for col in [c0, c1), v_j = 1, v_i = A[i][j] below;
+  // then M[i][col] -= t v_i w[col]
   auto apply_reflector = [&](int j, int c0, int c1, double t) {
     const int par = red_no++ & 1;
     const int ib = max(0, min(nr, j - r0));   // first local row with global index >= j
-    for (int col = c0 + warp; col < c1; col += kWarps) {
-      double s = 0.0;
-      for (int i = ib + lane; i < nr; i += 32) {
-        const double v = (r0 + i == j) ? 1.0 : A[i * ld + j];
-        s = fma(v, A[i * ld + col], s);
-      }
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane < ncl) push(par, col - c0, s, lane);
-    }
+    dots(par, j, c0, c1, true);
     gather(par, c1 - c0, wv);
     for (int i = ib + warp; i < nr; i += kWarps) {
       const double tv = -t * ((r0 + i == j) ? 1.0 : A[i * ld + j]);
-      for (int col = c0 + lane; col < c1; col += 32)
-        A[i * ld + col] = fma(tv, wv[col - c0], A[i * ld + col]);
+      row_axpy(A + (size_t)i * ld, tv, c0, c1, wv, c0);
     }
     __syncthreads();
   };
@@ -105,17 +144,12 @@ __global__ void __launch_bounds__(kQrThreads) qr_cluster_kernel(const QrArgs p) 
     const int par = red_no++ & 1;
     const int ib1 = max(0, min(nr, j + 1 - r0));   // first local row with global index > j
     const int ncol = c - j;
-    for (int col = j + warp; col < c; col += kWarps) {
-      double s = 0.0;
-      for (int i = ib1 + lane; i < nr; i += 32) s = fma(A[i * ld + j], A[i * ld + col], s);
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane < ncl) push(par, col - j, s, lane);
-    }
+    dots(par, j, j, c, false);
     if (rank == owner) {
       const double* row = A + (size_t)(j - r0) * ld + j;
-      for (int e = tid; e < ncol * ncl; e += kQrThreads) {
-        const int r = e / ncol, q = e - r * ncol;
-        cluster.map_shared_rank(rowj, r)[par * c + q] = row[q];
+      for (int q = tid; q < ncol; q += kQrThreads) {
+        const double v = row[q];
+        for (int r = 0; r < ncl; ++r) cluster.map_shared_rank(rowj, r)[par * c + q] = v;
       }
     }
     gather(par, ncol, wv);
@@ -132,10 +166,7 @@ __global__ void __launch_bounds__(kQrThreads) qr_cluster_kernel(const QrArgs p) 
     __syncthreads();
     for (int i = ib1 + warp; i < nr; i += kWarps) {   // rows below j: v_i = scal x_i
       const double vi = A[i * ld + j] * scal;
-      const double tv = -t * vi;
-      if (t != 0.0)
-        for (int col = j + 1 + lane; col < c; col += 32)
-          A[i * ld + col] = fma(tv, wv[col - j], A[i * ld + col]);
+      if (t != 0.0) row_axpy(A + (size_t)i * ld, -t * vi, j + 1, c, wv, j);
       __syncwarp();
       if (lane == 0) A[i * ld + j] = vi;
     }
