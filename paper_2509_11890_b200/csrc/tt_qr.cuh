@@ -348,11 +348,23 @@ __global__ void __launch_bounds__(kQrThreads) svd_jacobi_cluster_kernel(const Sv
         const double* bq = cluster.map_shared_rank(Bb, oq) + (size_t)cur * cpb * rows + lq * rows;
         const double* jq = cluster.map_shared_rank(Jb, oq) + (size_t)cur * cpb * c + lq * c;
         const bool lo = j < q;   // canonical pair (p, q) = (min, max)
-        const double* bp_ = lo ? bj : bq;
-        const double* bq_ = lo ? bq : bj;
+        // both columns of B and of J (own: local, partner: DSMEM) go into registers in ONE
+        // round of loads -- rows, c <= 256, eight per lane -- and serve the sums and both
+        // updates; loops that re-read the partner between stores paid its remote latency
+        // once per 32 rows
+        double bo[8], bp[8], jo[8], jp[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = lane + 32 * u;
+          bo[u] = i < rows ? bj[i] : 0.0;
+          bp[u] = i < rows ? bq[i] : 0.0;
+          jo[u] = i < c ? jj[i] : 0.0;
+          jp[u] = i < c ? jq[i] : 0.0;
+        }
         double sp = 0.0, sq = 0.0, g = 0.0;
-        for (int i = lane; i < rows; i += 32) {
-          const double x = bp_[i], y = bq_[i];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {   // same order as a lane-strided loop (zeros beyond rows)
+          const double x = lo ? bo[u] : bp[u], y = lo ? bp[u] : bo[u];
           sp = fma(x, x, sp);
           sq = fma(y, y, sq);
           g = fma(x, y, g);
@@ -363,22 +375,25 @@ __global__ void __launch_bounds__(kQrThreads) svd_jacobi_cluster_kernel(const Sv
           g += __shfl_xor_sync(0xffffffffu, g, o);
         }
         double cs = 1.0, sn = 0.0;
-        const double den = sqrt(sp * sq);
-        if (den > 0.0 && fabs(g) > tol * den) {
-          my_off = fmax(my_off, fabs(g) / den);
-          const double zeta = (sq - sp) / (2.0 * g);
-          const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-          cs = 1.0 / sqrt(fma(t, t, 1.0));
-          sn = cs * t;
+        const double pq = sp * sq;
+        if (pq > 0.0 && g * g > (tol * tol) * pq) {
+          // rotation from two reciprocal square roots (jb2_rotation, tt_round.cuh): the same
+          // angle as zeta = (sq - sp) / 2g, t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2))
+          jb2_rotation(sp, sq, g, cs, sn);
+          my_off = fmax(my_off, fabs(g) * rsqrt(pq));
         }
         // [b_p', b_q'] = [b_p, b_q] [[cs, sn], [-sn, cs]]
-        for (int i = lane; i < rows; i += 32) {
-          const double x = lo ? bj[i] : bq[i], y = lo ? bq[i] : bj[i];
-          Bn[lj * rows + i] = lo ? fma(-sn, y, cs * x) : fma(sn, x, cs * y);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = lane + 32 * u;
+          const double x = lo ? bo[u] : bp[u], y = lo ? bp[u] : bo[u];
+          if (i < rows) Bn[lj * rows + i] = lo ? fma(-sn, y, cs * x) : fma(sn, x, cs * y);
         }
-        for (int i = lane; i < c; i += 32) {
-          const double x = lo ? jj[i] : jq[i], y = lo ? jq[i] : jj[i];
-          Jn[lj * c + i] = lo ? fma(-sn, y, cs * x) : fma(sn, x, cs * y);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = lane + 32 * u;
+          const double x = lo ? jo[u] : jp[u], y = lo ? jp[u] : jo[u];
+          if (i < c) Jn[lj * c + i] = lo ? fma(-sn, y, cs * x) : fma(sn, x, cs * y);
         }
       }
       cluster.sync();   // every read of the cur buffers is done; nxt is complete
