@@ -997,6 +997,9 @@ def main():
                              "note": "tt_round_async: device-side rank decisions into zero-padded "
                                      "max-rank cores, no host synchronisation (graph-capturable)"}
         del pad
+        rnd_info["accurate_route_ms"] = wall(lambda: tt.tt_round(xs, 1e-10), reps=2)
+        rnd_info["accurate_route_note"] = ("delta = 1e-10: Householder QR + cluster one-sided Jacobi SVD of "
+                                           "R^T per core (no Gram floor; automatic for delta / sqrt(d-1) < 1e-7)")
         gen = torch.Generator(device=dev).manual_seed(13)
         rnd = lambda *sh: torch.randn(*sh, dtype=torch.float64, device=dev, generator=gen)
         Wh = rnd(cfg.r[k], cfg.N, 4, cfg.r[k + 1])

@@ -149,10 +149,14 @@ tt_status tt_operator_apply(int64_t d, const int64_t* n_row, const int64_t* n_co
  * block index between cores): Oseledets' algorithm, right-to-left
  * orthonormalisation then left-to-right truncation with per-core threshold
  * delta / sqrt(d-1) * ||T||_F (optionally capped at max_rank > 0), so that
- * ||T - round(T)||_F <= delta ||T||_F.  Every SVD is taken through the core unfolding's Gram
- * matrix (DMMA GEMM + a one-CTA parallel Jacobi eigensolver); numerically zero directions
- * (Gram eigenvalue <= 1e-14 of the largest) are dropped, which bounds the attainable
- * accuracy at ~1e-7 relative (fine for the paper's delta = 1e-4).
+ * ||T - round(T)||_F <= delta ||T||_F.  The orthonormalisation sweep is Householder QR (one
+ * thread-block cluster per core, exact to working precision).  The truncating SVDs go through
+ * the core unfolding's Gram matrix (DMMA GEMM + a block-Jacobi eigensolver on all SMs) when
+ * delta / sqrt(d-1) >= 1e-7 -- numerically zero directions (Gram eigenvalue <= 1e-14 of the
+ * largest) are dropped; that route resolves singular values down to ~1e-8 of the largest,
+ * ample for the paper's delta = 1e-4 -- and through Householder QR + a
+ * one-sided Jacobi SVD of R^T (no squared-condition floor) for tighter tolerances, delta = 0
+ * included.
  * cores_in[k] (r_in[k], n[k], r_in[k+1]) device, not modified; cores_out[k] device buffers of
  * at least the input core's size; r_out[d+1] (host) receives the new ranks.  Ranks <= 512.
  * SYNCHRONOUS: the truncation ranks are data dependent (one host read per core).
