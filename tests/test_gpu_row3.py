@@ -321,6 +321,33 @@ def test_tt_round_async_equals_sync_and_oracle(tt, case, delta):
     assert np.linalg.norm(vc - v) / np.linalg.norm(v) <= delta * (1 + 1e-6)
 
 
+@pytest.mark.parametrize("case", ["random", "sum", "wide"])
+def test_tt_round_async_gram_orthonormalisation(tt, case):
+    """Debug bit 29 sends the right-to-left orthonormalisation through the Gram matrix (the
+    route of unfoldings too large for one cluster): in the asynchronous call that sweep also
+    keeps full-size zero-padded factors and no host read."""
+    from oracle.rounding import tt_round as oracle_round
+    x = _async_case(case)
+    xg = [g(c) for c in x]
+    delta = 1e-4
+    tt.tt_debug_set_flags(1 << 29)
+    try:
+        padded, ranks = tt.tt_round_async(xg, delta)
+        torch.cuda.synchronize()
+    finally:
+        tt.tt_debug_set_flags(0)
+    yo = oracle_round(x, delta)
+    ro = [int(v) for v in ranks.tolist()]
+    assert ro == [1] + [c.shape[2] for c in yo]
+    for k, c in enumerate(padded):
+        ch = h(c)
+        assert not ch[ro[k]:, :, :].any() and not ch[:, :, ro[k + 1]:].any()
+    comp = [h(c) for c in tt.tt_compact(padded, ranks)]
+    v, vc, vo = full_vector(x), full_vector(comp), full_vector(yo)
+    assert rel_fro(vc, vo) <= 1e-9          # Gram route on both sweeps: ~eps kappa^2
+    assert np.linalg.norm(vc - v) / np.linalg.norm(v) <= delta * (1 + 1e-6)
+
+
 def test_tt_round_async_max_rank_and_errors(tt):
     rng = np.random.default_rng(78)
     x = [g(c) for c in ttgen.gaussian_tt_vector(rng, 4, [1, 4, 12, 16, 9, 3, 1])]
