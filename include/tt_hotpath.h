@@ -299,9 +299,14 @@ tt_status tt_merge_operator_cores(int64_t Rl, int64_t n1, int64_t n2, int64_t Rm
  * tt_orthonormalise: left- (TT_SWEEP_LEFT: cores 0..d-2 left-orthonormal, sum_{a,i}
  * x[a,i,b] x[a,i,b'] = delta_{bb'}, the norm carried into core d-1) or right-
  * (TT_SWEEP_RIGHT: cores 1..d-1 right-orthonormal, the norm carried into core 0)
- * orthonormalisation of a TT vector, the represented tensor unchanged.  Every factorisation
- * goes through the unfolding's Gram matrix and its eigendecomposition (as tt_round); exactly
- * rank-deficient bonds shrink (r_out).  Arguments and workspace as tt_round.  Synchronous.
+ * orthonormalisation of a TT vector, the represented tensor unchanged.  Every unfolding is
+ * factorised by Householder QR in one thread-block cluster (orthonormal to working precision;
+ * a bond wider than the unfolding's other side shrinks to it, r_out); the call is then
+ * ASYNCHRONOUS and graph-capturable (r_out is host-known).  An unfolding too large for one
+ * cluster's shared memory goes through its Gram matrix and eigendecomposition instead (as
+ * tt_round: orthonormal to ~eps kappa^2, exactly rank-deficient bonds shrink); that route
+ * reads the ranks on the host, so the call returns synchronised (and cannot be captured).
+ * Arguments and workspace as tt_round.
  *
  * tt_block_move_right / _left: "move the block index l to W_{k+1} or W_{k-1} ... by realising
  * one step of the TT rounding procedure".  Right: Wk_hat (r0,n0,l,r1) and

@@ -340,7 +340,12 @@ static tt_status round_impl(int64_t d, const int64_t* n, const int64_t* r_in,
     e = cudaMemcpyAsync(W[k], cores_in[k], sizeof(double) * r[k] * n[k] * r[k + 1],
                         cudaMemcpyDeviceToDevice, s);
   std::vector<double> hl(rmax);
+  // tt_round reads singular values on the host and returns synchronised; a pure cluster-QR
+  // orthonormalisation (tt_orthonormalise with every unfolding on the QR path) reads nothing
+  // and stays asynchronous
+  bool host_sync = (phases & 2) != 0;
   auto eig = [&](int m) -> cudaError_t {   // G (m x m) -> V, lam (host copy in hl)
+    host_sync = true;
     cudaError_t er = launch_sym_eigen(G, V, lam, m, esc, s);
     if (er != cudaSuccess) return er;
     er = cudaMemcpyAsync(hl.data(), lam, sizeof(double) * m, cudaMemcpyDeviceToHost, s);
@@ -617,7 +622,7 @@ static tt_status round_impl(int64_t d, const int64_t* n, const int64_t* r_in,
     set_rank_kernel<<<1, 1, 0, s>>>(reinterpret_cast<long long*>(r_dev), d, 1);
     g_launches += 2;
     e = cudaGetLastError();
-  } else if (e == cudaSuccess) {
+  } else if (e == cudaSuccess && (host_sync || (phases & 2))) {
     e = cudaStreamSynchronize(s);
   }
   if (e != cudaSuccess) return cuda_fail(e, who);
