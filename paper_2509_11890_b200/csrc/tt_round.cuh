@@ -1,12 +1,16 @@
 // tt_round.cuh — TT rounding on the GPU.
 //
-// Oseledets' TT-rounding (right-to-left orthonormalisation, left-to-right truncated SVD)
-// with every SVD taken through the Gram matrix of the core unfolding:
-//   G = M^T M (a DMMA GEMM of the engine) = V diag(sigma^2) V^T   (parallel cyclic Jacobi
-//   eigensolver on all SMs, cooperative launch, n <= 512), U = M V diag(1/sigma) (a GEMM).
+// Oseledets' TT-rounding (right-to-left orthonormalisation -- cluster Householder QR,
+// tt_qr.cuh -- then left-to-right truncated SVD).  This header holds the Gram route of the
+// truncating SVDs (and of orthonormalisations too large for one cluster):
+//   G = M^T M (a DMMA GEMM of the engine) = V diag(sigma^2) V^T   (parallel Jacobi
+//   eigensolver on all SMs, cooperative launch), U = M V diag(1/sigma) (a GEMM).
 // Exactly rank-deficient unfoldings (e.g. the formal sum T + T) are handled: zero singular
-// values are dropped.  The truncation decisions are data dependent, so the host reads the
-// singular values of every core (one synchronisation per core).
+// values are dropped.  The truncation decisions are data dependent: tt_round reads the
+// singular values of every core on the host (one synchronisation per core), tt_round_async
+// takes them on the device (trunc_decide_kernel, tt_solvers.cu).
+// Kernels: jacobi_coop_kernel (element-wise, n < 24), jacobi_block2_kernel (block Jacobi,
+// the default), jacobi_block_coop_kernel (the first block kernel, kept for A/B).
 // Included by tt_solvers.cu inside namespace ttint.
 
 // Multi-CTA parallel Jacobi (cooperative launch, one grid barrier per step).  The n x n
