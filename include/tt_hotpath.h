@@ -319,7 +319,14 @@ tt_status tt_merge_operator_cores(int64_t Rl, int64_t n1, int64_t n2, int64_t Rm
  * with the returned extent s (*s_out, host); the caller sizes them for s = min of the
  * unfolding's sides.  The smaller side must be <= 2048.  Synchronous (data-dependent s).
  * Workspace: tt_block_move_workspace_size(r0, n0, l, r1, n1, r2) for the right move with
- * those extents; for the left move pass (r0, n0, l, r1, n1, r2) of its own arguments.
+ * those extents; for the left move pass (r0, n0, l, r1, n1, r2) of its own arguments. *
+ * tt_block_move_right_async / _left_async: the same moves with the truncation decided on the
+ * device (no host read, no synchronisation, graph-capturable -- a half-sweep of block moves
+ * can be one CUDA graph).  The outputs keep the host-known STORAGE extent
+ * *s_storage = min of the unfolding's sides and are zero-padded: entries with the new bond
+ * index >= the effective rank are exactly 0 (the padded pair represents the same block
+ * tensors); *s_dev (DEVICE int64) receives the effective rank, equal to the synchronous
+ * call's *s_out.  The work is that of an untruncated move.
  * ------------------------------------------------------------------------------------- */
 size_t tt_orthonormalise_workspace_size(int64_t d, const int64_t* n, const int64_t* r);
 tt_status tt_orthonormalise(int64_t d, const int64_t* n, const int64_t* r_in,
@@ -338,6 +345,16 @@ tt_status tt_block_move_left(int64_t r0, int64_t n0, int64_t r1, int64_t n1, int
                              const double* Wk_hat, double* Wkm1_hat_out, double* Wk_out,
                              int64_t* s_out, void* workspace, size_t workspace_bytes,
                              void* stream);
+tt_status tt_block_move_right_async(int64_t r0, int64_t n0, int64_t l, int64_t r1, int64_t n1,
+                                    int64_t r2, double delta, int64_t max_rank,
+                                    const double* Wk_hat, const double* Wk1, double* Wk_out,
+                                    double* Wk1_hat_out, int64_t* s_storage, int64_t* s_dev,
+                                    void* workspace, size_t workspace_bytes, void* stream);
+tt_status tt_block_move_left_async(int64_t r0, int64_t n0, int64_t r1, int64_t n1, int64_t l,
+                                   int64_t r2, double delta, int64_t max_rank, const double* Wkm1,
+                                   const double* Wk_hat, double* Wkm1_hat_out, double* Wk_out,
+                                   int64_t* s_storage, int64_t* s_dev, void* workspace,
+                                   size_t workspace_bytes, void* stream);
 
 /* -------------------------------------------------------------------------------------
  * Petrov-Galerkin local operations: the bra train Z differs from the ket train X (ranks

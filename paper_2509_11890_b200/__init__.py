@@ -33,7 +33,7 @@ __all__ = [
     "tt_round", "tt_round_async", "tt_compact", "tt_round_workspace_size", "tt_debug_sym_eigen", "tt_debug_svd",
     "tt_local_lobpcg", "tt_local_lobpcg_workspace_size", "tt_merge_operator_cores",
     "tt_orthonormalise", "tt_orthonormalise_workspace_size", "tt_block_move_right",
-    "tt_block_move_left", "tt_block_move_workspace_size", "tt_pg_workspace_size",
+    "tt_block_move_left", "tt_block_move_right_async", "tt_block_move_left_async", "tt_block_move_workspace_size", "tt_pg_workspace_size",
     "tt_local_matvec_pg", "tt_interface_left_pg", "tt_interface_right_pg", "tt_enrich_right",
     "tt_enrich_right_workspace_size", "tt_sweep_w34", "tt_sweep_w34_workspace_size",
 ]
@@ -118,6 +118,10 @@ lib.tt_block_move_right.argtypes = [_i64] * 6 + [ctypes.c_double, _i64] + [_p] *
 lib.tt_block_move_right.restype = ctypes.c_int
 lib.tt_block_move_left.argtypes = [_i64] * 6 + [ctypes.c_double, _i64] + [_p] * 6 + [_sz, _p]
 lib.tt_block_move_left.restype = ctypes.c_int
+lib.tt_block_move_right_async.argtypes = [_i64] * 6 + [ctypes.c_double, _i64] + [_p] * 7 + [_sz, _p]
+lib.tt_block_move_right_async.restype = ctypes.c_int
+lib.tt_block_move_left_async.argtypes = [_i64] * 6 + [ctypes.c_double, _i64] + [_p] * 7 + [_sz, _p]
+lib.tt_block_move_left_async.restype = ctypes.c_int
 lib.tt_sweep_w34_workspace_size.restype = _sz
 lib.tt_sweep_w34_workspace_size.argtypes = [_i64, _p, _p, _p]
 lib.tt_sweep_w34.argtypes = [_i64, _p, _p, _p, _p, _p, _p, _p, _p, _p, _sz, _p]
@@ -900,6 +904,58 @@ def tt_block_move_right(Wk_hat, Wk1, delta=0.0, max_rank=0, workspace=None, stre
                                    ws.numel(), _stream(stream)))
     sk = s_out.value
     return (Wk[: r0 * n0 * sk].reshape(r0, n0, sk), W1[: sk * n1 * l * r2].reshape(sk, n1, l, r2))
+
+
+def tt_block_move_right_async(Wk_hat, Wk1, delta=0.0, max_rank=0, workspace=None, stream=None,
+                              rank=None):
+    """tt_block_move_right with the truncation decided on the device (no synchronisation,
+    graph-capturable).  Returns (Wk (r0,n0,S), Wk1_hat (S,n1,l,r2), rank): zero-padded to the
+    storage extent S = min(r0 n0, l r1), `rank` a device int64 tensor (1) with the effective
+    rank s; Wk[..., :s] and Wk1_hat[:s] are the synchronous call's outputs."""
+    if Wk_hat.dim() != 4 or Wk1.dim() != 3 or Wk1.shape[0] != Wk_hat.shape[3]:
+        raise ValueError("Wk_hat must be (r0, n0, l, r1) and Wk1 (r1, n1, r2)")
+    _same_device(Wk_hat, Wk1, workspace)
+    r0, n0, l, r1 = Wk_hat.shape
+    _, n1, r2 = Wk1.shape
+    smax = min(r0 * n0, l * r1)
+    Wk = torch.empty(r0, n0, smax, dtype=torch.float64, device=Wk_hat.device)
+    W1 = torch.empty(smax, n1, l, r2, dtype=torch.float64, device=Wk_hat.device)
+    if rank is None:
+        rank = torch.empty(1, dtype=torch.int64, device=Wk_hat.device)
+    s_st = ctypes.c_int64()
+    ws = _ws(tt_block_move_workspace_size(r0, n0, l, r1, n1, r2), workspace, Wk_hat.device)
+    _check(lib.tt_block_move_right_async(r0, n0, l, r1, n1, r2, float(delta), int(max_rank),
+                                         _dev(Wk_hat, "Wk_hat"), _dev(Wk1, "Wk1"),
+                                         _dev(Wk, "Wk_out"), _dev(W1, "Wk1_hat_out"),
+                                         ctypes.byref(s_st), rank.data_ptr(), ws.data_ptr(),
+                                         ws.numel(), _stream(stream)))
+    assert s_st.value == smax
+    return Wk, W1, rank
+
+
+def tt_block_move_left_async(Wkm1, Wk_hat, delta=0.0, max_rank=0, workspace=None, stream=None,
+                             rank=None):
+    """tt_block_move_left with the truncation decided on the device.  Returns
+    (Wkm1_hat (r0,n0,l,S), Wk (S,n1,r2), rank), zero-padded to S = min(r1 l, n1 r2)."""
+    if Wkm1.dim() != 3 or Wk_hat.dim() != 4 or Wk_hat.shape[0] != Wkm1.shape[2]:
+        raise ValueError("Wkm1 must be (r0, n0, r1) and Wk_hat (r1, n1, l, r2)")
+    _same_device(Wkm1, Wk_hat, workspace)
+    r0, n0, r1 = Wkm1.shape
+    _, n1, l, r2 = Wk_hat.shape
+    smax = min(r1 * l, n1 * r2)
+    Wh = torch.empty(r0, n0, l, smax, dtype=torch.float64, device=Wk_hat.device)
+    Wk = torch.empty(smax, n1, r2, dtype=torch.float64, device=Wk_hat.device)
+    if rank is None:
+        rank = torch.empty(1, dtype=torch.int64, device=Wk_hat.device)
+    s_st = ctypes.c_int64()
+    ws = _ws(tt_block_move_workspace_size(r0, n0, l, r1, n1, r2), workspace, Wk_hat.device)
+    _check(lib.tt_block_move_left_async(r0, n0, r1, n1, l, r2, float(delta), int(max_rank),
+                                        _dev(Wkm1, "Wkm1"), _dev(Wk_hat, "Wk_hat"),
+                                        _dev(Wh, "Wkm1_hat_out"), _dev(Wk, "Wk_out"),
+                                        ctypes.byref(s_st), rank.data_ptr(), ws.data_ptr(),
+                                        ws.numel(), _stream(stream)))
+    assert s_st.value == smax
+    return Wh, Wk, rank
 
 
 def tt_block_move_left(Wkm1, Wk_hat, delta=0.0, max_rank=0, workspace=None, stream=None):

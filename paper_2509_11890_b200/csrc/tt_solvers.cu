@@ -700,8 +700,46 @@ static long long svd_ws_elems(long long m, long long q) {
   // G, E (<= k^2 + big k), lam, eigen scratch, f, Us + Vs (<= 2 big k), alignment slack
   return 2 * k * k + 3 * big * k + 3 * k + 128 + sym_eigen_scratch(k) + 12 * 32;
 }
+// Device-side truncation decision of the asynchronous block moves: the rule of svd_gram's
+// host loop (same formulas and summation order) from the descending Gram eigenvalues; writes
+// the rank, the k x k singular vectors of the Gram side with the columns >= rank zeroed and
+// the column factors 1 / sigma (0 beyond the rank), so every later GEMM keeps extent k.
+__global__ void __launch_bounds__(256) svd_decide_kernel(const double* __restrict__ lam,
+                                                         const double* __restrict__ E, int k,
+                                                         double delta, long long max_rank,
+                                                         long long* __restrict__ s_dev,
+                                                         double* __restrict__ side,
+                                                         double* __restrict__ fin) {
+  __shared__ int s_sk;
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    int nz = 0;
+    for (int i = 0; i < k; ++i) {
+      tot += fmax(lam[i], 0.0);
+      if (lam[i] > 1e-14 * lam[0] && lam[i] > 0.0) ++nz;
+    }
+    if (nz == 0) nz = 1;
+    const double thr = delta * sqrt(tot);
+    int sk = nz;
+    double tail = 0.0;
+    for (int i = nz - 1; i >= 1; --i) {
+      tail += fmax(lam[i], 0.0);
+      if (sqrt(tail) <= thr) sk = i; else break;
+    }
+    if (max_rank > 0 && sk > max_rank) sk = (int)max_rank;
+    s_sk = sk;
+    *s_dev = sk;
+  }
+  __syncthreads();
+  const int sk = s_sk;
+  for (int e = threadIdx.x; e < k * k; e += blockDim.x) side[e] = (e % k) < sk ? E[e] : 0.0;
+  for (int c = threadIdx.x; c < k; c += blockDim.x)
+    fin[c] = c < sk ? 1.0 / sqrt(fmax(lam[c], 1e-300)) : 0.0;
+}
+
 static cudaError_t svd_gram(const double* M, long long m, long long q, double delta,
-                            long long max_rank, SvdBufs& b, int& s_out, cudaStream_t s) {
+                            long long max_rank, SvdBufs& b, int& s_out, cudaStream_t s,
+                            int64_t* s_dev = nullptr) {
   const bool left = m <= q;   // Gram of the smaller side
   const long long k = left ? m : q;
   cudaError_t e;
@@ -712,6 +750,26 @@ static cudaError_t svd_gram(const double* M, long long m, long long q, double de
     e = launch_gemm(false, false, gp(M, q, M, q, b.G, q, q, m, tt::map_plain(q), tt::map_plain(1)), s);
   if (e != cudaSuccess) return e;
   if ((e = launch_sym_eigen(b.G, b.E, b.lam, (int)k, b.esc, s)) != cudaSuccess) return e;
+  if (s_dev) {   // asynchronous: rank on the device, every extent stays k (zero padding)
+    double* side = left ? b.Us : b.Vs;
+    double* fin = b.f + 32 * ((k + 31) / 32);
+    svd_decide_kernel<<<1, 256, 0, s>>>(b.lam, b.E, (int)k, delta, max_rank,
+                                        reinterpret_cast<long long*>(s_dev), side, fin);
+    ++g_launches;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    s_out = (int)k;
+    double* other = left ? b.Vs : b.Us;
+    if (left)   // Vs (q x k) = M^T (q x m) . Us (m x k)
+      e = launch_gemm(false, false, gp(M, q, b.Us, k, b.E, q, k, m, tt::map_plain(k), tt::map_plain(1)), s);
+    else        // Us (m x k) = M (m x q) . Vs (q x k)
+      e = launch_gemm(true, false, gp(M, q, b.Vs, k, b.E, m, k, q, tt::map_plain(k), tt::map_plain(1)), s);
+    if (e != cudaSuccess) return e;
+    const long long ob = left ? q : m;
+    scale_cols_ld_kernel<<<(unsigned)std::min<long long>(4096, (ob * k + 255) / 256), 256, 0, s>>>(
+        b.E, k, fin, other, ob, (int)k);
+    ++g_launches;
+    return cudaGetLastError();
+  }
   std::vector<double> hl(k);
   if ((e = cudaMemcpyAsync(hl.data(), b.lam, sizeof(double) * k, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
     return e;
@@ -779,12 +837,11 @@ size_t tt_block_move_workspace_size(int64_t r0, int64_t n0, int64_t l, int64_t r
   return ws_bytes({std::max(a, b)});
 }
 
-tt_status tt_block_move_right(int64_t r0, int64_t n0, int64_t l, int64_t r1, int64_t n1,
+static tt_status block_move_right_impl(int64_t r0, int64_t n0, int64_t l, int64_t r1, int64_t n1,
                               int64_t r2, double delta, int64_t max_rank, const double* Wk_hat,
                               const double* Wk1, double* Wk_out, double* Wk1_hat_out,
                               int64_t* s_out, void* workspace, size_t workspace_bytes,
-                              void* stream) {
-  CallScope scope;
+                              void* stream, int64_t* s_dev) {
   if (r0 <= 0 || n0 <= 0 || l <= 0 || r1 <= 0 || n1 <= 0 || r2 <= 0)
     return fail(TT_ERR_INVALID_ARGUMENT, "extents must be positive");
   if (!(delta >= 0.0) || max_rank < 0) return fail(TT_ERR_INVALID_ARGUMENT, "need delta >= 0, max_rank >= 0");
@@ -813,7 +870,7 @@ tt_status tt_block_move_right(int64_t r0, int64_t n0, int64_t l, int64_t r1, int
   double* C = c.take(k * q);
   if (!c.ok) return fail(TT_ERR_WORKSPACE, "workspace too small after alignment");
   int sk = 0;
-  cudaError_t e = svd_gram(Wk_hat, m, q, delta, max_rank, b, sk, s);
+  cudaError_t e = svd_gram(Wk_hat, m, q, delta, max_rank, b, sk, s, s_dev);
   // Wk_out = Us (m x sk);  C (sk x q) = Us^T M
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(Wk_out, b.Us, sizeof(double) * m * sk, cudaMemcpyDeviceToDevice, s);
@@ -825,18 +882,36 @@ tt_status tt_block_move_right(int64_t r0, int64_t n0, int64_t l, int64_t r1, int
   if (e == cudaSuccess)
     e = launch_gemm(true, false, gp(C, r1, Wk1, n1 * r2, Wk1_hat_out, sk * l, n1 * r2, r1,
                                     tt::map2(l, r2, n1 * l * r2), tt::map2(r2, 1, l * r2)), s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e == cudaSuccess && !s_dev) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return cuda_fail(e, "tt_block_move_right");
   *s_out = sk;
   return TT_OK;
 }
+tt_status tt_block_move_right(int64_t r0, int64_t n0, int64_t l, int64_t r1, int64_t n1,
+                              int64_t r2, double delta, int64_t max_rank, const double* Wk_hat,
+                              const double* Wk1, double* Wk_out, double* Wk1_hat_out,
+                              int64_t* s_out, void* workspace, size_t workspace_bytes,
+                              void* stream) {
+  CallScope scope;
+  return block_move_right_impl(r0, n0, l, r1, n1, r2, delta, max_rank, Wk_hat, Wk1, Wk_out,
+                               Wk1_hat_out, s_out, workspace, workspace_bytes, stream, nullptr);
+}
+tt_status tt_block_move_right_async(int64_t r0, int64_t n0, int64_t l, int64_t r1, int64_t n1,
+                                    int64_t r2, double delta, int64_t max_rank,
+                                    const double* Wk_hat, const double* Wk1, double* Wk_out,
+                                    double* Wk1_hat_out, int64_t* s_storage, int64_t* s_dev,
+                                    void* workspace, size_t workspace_bytes, void* stream) {
+  CallScope scope;
+  if (!s_dev) return fail(TT_ERR_NULL_POINTER, "s_dev is NULL");
+  return block_move_right_impl(r0, n0, l, r1, n1, r2, delta, max_rank, Wk_hat, Wk1, Wk_out,
+                               Wk1_hat_out, s_storage, workspace, workspace_bytes, stream, s_dev);
+}
 
-tt_status tt_block_move_left(int64_t r0, int64_t n0, int64_t r1, int64_t n1, int64_t l,
+static tt_status block_move_left_impl(int64_t r0, int64_t n0, int64_t r1, int64_t n1, int64_t l,
                              int64_t r2, double delta, int64_t max_rank, const double* Wkm1,
                              const double* Wk_hat, double* Wkm1_hat_out, double* Wk_out,
                              int64_t* s_out, void* workspace, size_t workspace_bytes,
-                             void* stream) {
-  CallScope scope;
+                             void* stream, int64_t* s_dev) {
   if (r0 <= 0 || n0 <= 0 || l <= 0 || r1 <= 0 || n1 <= 0 || r2 <= 0)
     return fail(TT_ERR_INVALID_ARGUMENT, "extents must be positive");
   if (!(delta >= 0.0) || max_rank < 0) return fail(TT_ERR_INVALID_ARGUMENT, "need delta >= 0, max_rank >= 0");
@@ -871,7 +946,7 @@ tt_status tt_block_move_left(int64_t r0, int64_t n0, int64_t r1, int64_t n1, int
   ++g_launches;
   int sk = 0;
   cudaError_t e = cudaGetLastError();
-  if (e == cudaSuccess) e = svd_gram(Mp, m, q, delta, max_rank, b, sk, s);
+  if (e == cudaSuccess) e = svd_gram(Mp, m, q, delta, max_rank, b, sk, s, s_dev);
   // Wk_out (sk x q) = Vs^T;  C (m x sk) = M Vs = Us Sigma
   if (e == cudaSuccess) {
     transpose2d_kernel<<<(unsigned)std::min<long long>(4096, (q * sk + 255) / 256), 256, 0, s>>>(
@@ -887,10 +962,29 @@ tt_status tt_block_move_left(int64_t r0, int64_t n0, int64_t r1, int64_t n1, int
   if (e == cudaSuccess)
     e = launch_gemm(true, false, gp(Wkm1, r1, C, l * sk, Wkm1_hat_out, r0 * n0, l * sk, r1,
                                     tt::map_plain(l * sk), tt::map_plain(1)), s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e == cudaSuccess && !s_dev) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return cuda_fail(e, "tt_block_move_left");
   *s_out = sk;
   return TT_OK;
+}
+tt_status tt_block_move_left(int64_t r0, int64_t n0, int64_t r1, int64_t n1, int64_t l,
+                             int64_t r2, double delta, int64_t max_rank, const double* Wkm1,
+                             const double* Wk_hat, double* Wkm1_hat_out, double* Wk_out,
+                             int64_t* s_out, void* workspace, size_t workspace_bytes,
+                             void* stream) {
+  CallScope scope;
+  return block_move_left_impl(r0, n0, r1, n1, l, r2, delta, max_rank, Wkm1, Wk_hat, Wkm1_hat_out,
+                              Wk_out, s_out, workspace, workspace_bytes, stream, nullptr);
+}
+tt_status tt_block_move_left_async(int64_t r0, int64_t n0, int64_t r1, int64_t n1, int64_t l,
+                                   int64_t r2, double delta, int64_t max_rank, const double* Wkm1,
+                                   const double* Wk_hat, double* Wkm1_hat_out, double* Wk_out,
+                                   int64_t* s_storage, int64_t* s_dev, void* workspace,
+                                   size_t workspace_bytes, void* stream) {
+  CallScope scope;
+  if (!s_dev) return fail(TT_ERR_NULL_POINTER, "s_dev is NULL");
+  return block_move_left_impl(r0, n0, r1, n1, l, r2, delta, max_rank, Wkm1, Wk_hat, Wkm1_hat_out,
+                              Wk_out, s_storage, workspace, workspace_bytes, stream, s_dev);
 }
 
 // ---- AMEn enrichment ("enrichment of the TT cores by TT cores of the

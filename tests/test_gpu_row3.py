@@ -426,3 +426,76 @@ def test_orthonormalise_is_asynchronous_and_capturable(tt, direction):
         for a, b in zip(out, ref):
             assert torch.equal(a, b)
         assert rel_fro(full_vector([h(c) for c in out]), full_vector(xs)) <= 1e-12
+
+
+# ----------------------------------------------------------------------------------------
+# asynchronous block moves: device-side rank into zero-padded outputs
+# ----------------------------------------------------------------------------------------
+@pytest.mark.parametrize("delta", [1e-2, 1e-4, 1e-6])
+@pytest.mark.parametrize("m_lt_q", [True, False])
+def test_block_move_right_async_equals_sync(tt, delta, m_lt_q):
+    rng = np.random.default_rng(91)
+    r0, n0, l, r1, n1, r2 = (4, 4, 4, 8, 4, 3) if m_lt_q else (16, 4, 2, 6, 4, 3)
+    sig = np.array([3.0, 2.0, 1.0, 0.5, 1e-3, 5e-4, 1e-6, 1e-7])
+    Wk_hat = _graded(rng, r0 * n0, l * r1, sig).reshape(r0, n0, l, r1)
+    Wk1 = rng.standard_normal((r1, n1, r2))
+    Wk_s, W1_s = (h(t) for t in tt.tt_block_move_right(g(Wk_hat), g(Wk1), delta))
+    Wk_a, W1_a, rank = tt.tt_block_move_right_async(g(Wk_hat), g(Wk1), delta)
+    s = int(rank.item())
+    Wk_a, W1_a = h(Wk_a), h(W1_a)
+    assert s == Wk_s.shape[2] == block_move_right(Wk_hat, Wk1, delta)[0].shape[2]
+    assert Wk_a.shape[2] == min(r0 * n0, l * r1) and W1_a.shape[0] == Wk_a.shape[2]
+    assert not Wk_a[:, :, s:].any() and not W1_a[s:].any()      # exact zero padding
+    T_s = np.einsum("ais,sjlc->ailjc", Wk_s, W1_s)
+    T_a = np.einsum("ais,sjlc->ailjc", Wk_a, W1_a)                # the padded pair as it stands
+    assert rel_fro(T_a, T_s) <= 1e-12
+    P_a, P_s = Wk_a[:, :, :s].reshape(r0 * n0, s), Wk_s.reshape(r0 * n0, s)
+    assert np.abs(P_a @ P_a.T - P_s @ P_s.T).max() <= 1e-12
+
+
+@pytest.mark.parametrize("delta", [0.0, 1e-3])
+@pytest.mark.parametrize("shape", [(2, 4, 5, 4, 3, 6), (8, 4, 32, 4, 4, 8)])
+def test_block_move_left_async_equals_sync(tt, shape, delta):
+    r0, n0, r1, n1, l, r2 = shape
+    rng = np.random.default_rng(92)
+    Wkm1 = rng.standard_normal((r0, n0, r1))
+    k = min(r1 * l, n1 * r2)
+    sig = np.logspace(0, -5, k)
+    Wk_hat = _graded(rng, r1 * l, n1 * r2, sig).reshape(r1, l, n1, r2).transpose(0, 2, 1, 3).copy()
+    Wh_s, Wk_s = (h(t) for t in tt.tt_block_move_left(g(Wkm1), g(Wk_hat), delta))
+    Wh_a, Wk_a, rank = tt.tt_block_move_left_async(g(Wkm1), g(Wk_hat), delta)
+    s = int(rank.item())
+    Wh_a, Wk_a = h(Wh_a), h(Wk_a)
+    assert s == Wk_s.shape[0] == block_move_left(Wkm1, Wk_hat, delta)[1].shape[0]
+    assert not Wh_a[..., s:].any() and not Wk_a[s:].any()
+    T_s = np.einsum("ails,sjc->ailjc", Wh_s, Wk_s)
+    T_a = np.einsum("ails,sjc->ailjc", Wh_a, Wk_a)
+    assert rel_fro(T_a, T_s) <= 1e-12
+
+
+def test_block_move_async_graph_capture(tt):
+    """No host read inside: a right move followed by the left move back is one CUDA graph whose
+    replay follows new values (the synchronous calls cannot be captured)."""
+    rng = np.random.default_rng(93)
+    r0, n0, l, r1, n1, r2 = 6, 4, 3, 5, 4, 7
+    Wk_hat, Wk1 = g(rng.standard_normal((r0, n0, l, r1))), g(rng.standard_normal((r1, n1, r2)))
+    ws = torch.empty(tt.tt_block_move_workspace_size(r0, n0, l, r1, n1, r2), dtype=torch.uint8,
+                     device="cuda")
+    rk = torch.zeros(1, dtype=torch.int64, device="cuda")
+    s = torch.cuda.Stream()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        tt.tt_block_move_right_async(Wk_hat, Wk1, 1e-8, workspace=ws, stream=s, rank=rk)   # warm
+        s.synchronize()
+        with torch.cuda.graph(graph, stream=s):
+            Wk, W1, _ = tt.tt_block_move_right_async(Wk_hat, Wk1, 1e-8, workspace=ws, stream=s,
+                                                     rank=rk)
+    for seed in (1, 2):
+        r2g = np.random.default_rng(seed)
+        Wk_hat.copy_(g(r2g.standard_normal((r0, n0, l, r1))))
+        Wk1.copy_(g(r2g.standard_normal((r1, n1, r2))))
+        graph.replay()
+        torch.cuda.synchronize()
+        T0 = np.einsum("ailb,bjc->ailjc", h(Wk_hat), h(Wk1))
+        assert rel_fro(np.einsum("ais,sjlc->ailjc", h(Wk), h(W1)), T0) <= 1e-9
+        assert int(rk.item()) == tt.tt_block_move_right(Wk_hat, Wk1, 1e-8)[0].shape[2]
