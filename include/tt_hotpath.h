@@ -397,6 +397,15 @@ tt_status tt_enrich_right(int64_t rl, int64_t n, int64_t rx, int64_t rz, int64_t
                           double delta, int64_t max_rank, const double* x_k, const double* z_k,
                           const double* x_k1, double* x_k_out, double* x_k1_out, int64_t* s_out,
                           void* workspace, size_t workspace_bytes, void* stream);
+/* tt_enrich_right_async: the same enrichment with the truncation decided on the device (as
+ * tt_block_move_right_async): x_k_out (rl, n, S) and x_k1_out (S, n1, r2) zero-padded to the
+ * storage extent *s_storage = S = min(rl n, rx + rz) (host), the effective rank in *s_dev
+ * (DEVICE int64).  Asynchronous, graph-capturable. */
+tt_status tt_enrich_right_async(int64_t rl, int64_t n, int64_t rx, int64_t rz, int64_t n1,
+                                int64_t r2, double delta, int64_t max_rank, const double* x_k,
+                                const double* z_k, const double* x_k1, double* x_k_out,
+                                double* x_k1_out, int64_t* s_storage, int64_t* s_dev,
+                                void* workspace, size_t workspace_bytes, void* stream);
 
 /* Workload W34 as one call: all interfaces (as
  * tt_sweep_interfaces with TT_SWEEP_BOTH: phiL[0..d], phiR[0..d]) and y_k = local matvec of

@@ -35,6 +35,7 @@ __all__ = [
     "tt_orthonormalise", "tt_orthonormalise_workspace_size", "tt_block_move_right",
     "tt_block_move_left", "tt_block_move_right_async", "tt_block_move_left_async", "tt_block_move_workspace_size", "tt_pg_workspace_size",
     "tt_local_matvec_pg", "tt_interface_left_pg", "tt_interface_right_pg", "tt_enrich_right",
+    "tt_enrich_right_async",
     "tt_enrich_right_workspace_size", "tt_sweep_w34", "tt_sweep_w34_workspace_size",
 ]
 
@@ -138,6 +139,8 @@ lib.tt_enrich_right_workspace_size.restype = _sz
 lib.tt_enrich_right_workspace_size.argtypes = [_i64] * 6
 lib.tt_enrich_right.argtypes = [_i64] * 6 + [ctypes.c_double, _i64] + [_p] * 7 + [_sz, _p]
 lib.tt_enrich_right.restype = ctypes.c_int
+lib.tt_enrich_right_async.argtypes = [_i64] * 6 + [ctypes.c_double, _i64] + [_p] * 8 + [_sz, _p]
+lib.tt_enrich_right_async.restype = ctypes.c_int
 lib.tt_merge_operator_cores.restype = ctypes.c_int
 lib.tt_debug_force_v1.argtypes = [ctypes.c_int]
 lib.tt_debug_force_v1.restype = None
@@ -1071,6 +1074,34 @@ def tt_enrich_right(x_k, z_k, x_k1, delta=0.0, max_rank=0, workspace=None, strea
                                ws.numel(), _stream(stream)))
     sk = s_out.value
     return xo[: rl * n * sk].reshape(rl, n, sk), x1o[: sk * n1 * r2].reshape(sk, n1, r2)
+
+
+def tt_enrich_right_async(x_k, z_k, x_k1, delta=0.0, max_rank=0, workspace=None, stream=None,
+                          rank=None):
+    """tt_enrich_right with the truncation decided on the device (graph-capturable).  Returns
+    (x_k' (rl, n, S), x_{k+1}' (S, n1, r2), rank): zero-padded to S = min(rl n, rx + rz), `rank`
+    a device int64 tensor (1) with the effective rank."""
+    if x_k.dim() != 3 or z_k.dim() != 3 or x_k1.dim() != 3:
+        raise ValueError("x_k, z_k, x_k1 must be 3-D cores")
+    rl, n, rx = x_k.shape
+    rz = z_k.shape[2]
+    _expect(z_k, (rl, n, rz), "z_k")
+    if x_k1.shape[0] != rx:
+        raise ValueError(f"x_k1 left bond {x_k1.shape[0]} != x_k right bond {rx}")
+    _same_device(x_k, z_k, x_k1, workspace)
+    _, n1, r2 = x_k1.shape
+    smax = min(rl * n, rx + rz)
+    xo = torch.empty(rl, n, smax, dtype=torch.float64, device=x_k.device)
+    x1o = torch.empty(smax, n1, r2, dtype=torch.float64, device=x_k.device)
+    if rank is None:
+        rank = torch.empty(1, dtype=torch.int64, device=x_k.device)
+    s_st = ctypes.c_int64()
+    ws = _ws(tt_enrich_right_workspace_size(rl, n, rx, rz, n1, r2), workspace, x_k.device)
+    _check(lib.tt_enrich_right_async(rl, n, rx, rz, n1, r2, float(delta), int(max_rank),
+                                     _dev(x_k, "x_k"), _dev(z_k, "z_k"), _dev(x_k1, "x_k1"),
+                                     _dev(xo, "x_k_out"), _dev(x1o, "x_k1_out"), ctypes.byref(s_st),
+                                     rank.data_ptr(), ws.data_ptr(), ws.numel(), _stream(stream)))
+    return xo, x1o, rank
 
 
 def tt_round_workspace_size(n, r) -> int:

@@ -1022,11 +1022,10 @@ size_t tt_enrich_right_workspace_size(int64_t rl, int64_t n, int64_t rx, int64_t
   return mv + ws_bytes({cat, cat1});
 }
 
-tt_status tt_enrich_right(int64_t rl, int64_t n, int64_t rx, int64_t rz, int64_t n1, int64_t r2,
+static tt_status enrich_right_impl(int64_t rl, int64_t n, int64_t rx, int64_t rz, int64_t n1, int64_t r2,
                           double delta, int64_t max_rank, const double* x_k, const double* z_k,
                           const double* x_k1, double* x_k_out, double* x_k1_out, int64_t* s_out,
-                          void* workspace, size_t workspace_bytes, void* stream) {
-  CallScope scope;
+                          void* workspace, size_t workspace_bytes, void* stream, int64_t* s_dev) {
   if (rl <= 0 || n <= 0 || rx <= 0 || rz <= 0 || n1 <= 0 || r2 <= 0)
     return fail(TT_ERR_INVALID_ARGUMENT, "extents must be positive");
   if (!x_k || !z_k || !x_k1 || !x_k_out || !x_k1_out || !s_out)
@@ -1053,11 +1052,31 @@ tt_status tt_enrich_right(int64_t rl, int64_t n, int64_t rx, int64_t rz, int64_t
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "tt_enrich_right");
   const int64_t launches = g_launches;
-  tt_status st = tt_block_move_right(rl, n, 1, r, n1, r2, delta, max_rank, cat, cat1, x_k_out,
-                                     x_k1_out, s_out, base, mv, stream);
+  tt_status st = s_dev ? tt_block_move_right_async(rl, n, 1, r, n1, r2, delta, max_rank, cat, cat1,
+                                                   x_k_out, x_k1_out, s_out, s_dev, base, mv, stream)
+                       : tt_block_move_right(rl, n, 1, r, n1, r2, delta, max_rank, cat, cat1,
+                                             x_k_out, x_k1_out, s_out, base, mv, stream);
   g_launches += launches;
   g_launches_last = g_launches;
   return st;
+}
+tt_status tt_enrich_right(int64_t rl, int64_t n, int64_t rx, int64_t rz, int64_t n1, int64_t r2,
+                          double delta, int64_t max_rank, const double* x_k, const double* z_k,
+                          const double* x_k1, double* x_k_out, double* x_k1_out, int64_t* s_out,
+                          void* workspace, size_t workspace_bytes, void* stream) {
+  CallScope scope;
+  return enrich_right_impl(rl, n, rx, rz, n1, r2, delta, max_rank, x_k, z_k, x_k1, x_k_out,
+                           x_k1_out, s_out, workspace, workspace_bytes, stream, nullptr);
+}
+tt_status tt_enrich_right_async(int64_t rl, int64_t n, int64_t rx, int64_t rz, int64_t n1,
+                                int64_t r2, double delta, int64_t max_rank, const double* x_k,
+                                const double* z_k, const double* x_k1, double* x_k_out,
+                                double* x_k1_out, int64_t* s_storage, int64_t* s_dev,
+                                void* workspace, size_t workspace_bytes, void* stream) {
+  CallScope scope;
+  if (!s_dev) return fail(TT_ERR_NULL_POINTER, "s_dev is NULL");
+  return enrich_right_impl(rl, n, rx, rz, n1, r2, delta, max_rank, x_k, z_k, x_k1, x_k_out,
+                           x_k1_out, s_storage, workspace, workspace_bytes, stream, s_dev);
 }
 
 // ---- projected KKT block system action -----------------------------

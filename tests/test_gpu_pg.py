@@ -88,6 +88,28 @@ def test_enrich_right_vs_oracle(tt):
         assert np.abs(P @ c - c).max() <= 1e-10 * np.abs(c).max()
 
 
+def test_enrich_right_async_equals_sync(tt):
+    """Device-side rank into zero-padded outputs: the padded pair is the enriched train as it
+    stands, the rank equals the synchronous call's; a rank-deficient residual (z_k inside the
+    span of x_k) is truncated away on the device."""
+    rng = np.random.default_rng(75)
+    x = ttgen.gaussian_tt_vector(rng, 4, [1, 4, 16, 24, 16, 4, 1])
+    k = 2
+    for zk in (rng.standard_normal((16, 4, 5)),
+               np.einsum("aib,bc->aic", x[k], rng.standard_normal((24, 3)))):
+        xs, x1s = (h(t) for t in tt.tt_enrich_right(g(x[k]), g(zk), g(x[k + 1]), 1e-10))
+        xa, x1a, rank = tt.tt_enrich_right_async(g(x[k]), g(zk), g(x[k + 1]), 1e-10)
+        s = int(rank.item())
+        xa, x1a = h(xa), h(x1a)
+        assert s == xs.shape[2]
+        assert xa.shape[2] == min(64, 24 + zk.shape[2]) == x1a.shape[0]
+        assert not xa[:, :, s:].any() and not x1a[s:].any()
+        y = x[:k] + [xa, x1a] + x[k + 2:]
+        assert rel_fro(full_vector(y), full_vector(x)) <= 1e-11
+        M = xa[:, :, :s].reshape(64, s)
+        assert np.abs(M.T @ M - np.eye(s)).max() <= 1e-9
+
+
 def test_amen_residual_enrichment_step(tt):
     """One AMEn enrichment step at core k of a left-to-right sweep: the residual
     core r_k = X^{<k},Z^{>k}-projection of (b - A x) -- the projected right-hand side minus the
