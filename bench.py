@@ -997,6 +997,23 @@ def main():
                              "note": "tt_round_async: device-side rank decisions into zero-padded "
                                      "max-rank cores, no host synchronisation (graph-capturable)"}
         del pad
+        try:   # the asynchronous call as a CUDA graph (what a host read per core rules out)
+            n_r = [int(c.shape[1]) for c in xs]
+            r_r = [int(c.shape[0]) for c in xs] + [1]
+            ws_r = torch.empty(tt.tt_round_workspace_size(n_r, r_r), dtype=torch.uint8, device=dev)
+            rk_r = torch.zeros(len(xs) + 1, dtype=torch.int64, device=dev)
+            st_r = torch.cuda.Stream(device=dev)
+            gr_r = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(st_r):
+                tt.tt_round_async(xs, 1e-4, workspace=ws_r, stream=st_r, ranks=rk_r)
+                st_r.synchronize()
+                with torch.cuda.graph(gr_r, stream=st_r):
+                    tt.tt_round_async(xs, 1e-4, workspace=ws_r, stream=st_r, ranks=rk_r)
+            rnd_info["async"]["graph_replay_ms"] = wall(gr_r.replay, reps=3)
+            del gr_r, ws_r
+        except Exception as exc:   # reported, never fatal for the bench line
+            rnd_info["async"]["graph_replay_ms"] = None
+            rnd_info["async"]["graph_error"] = str(exc)[:200]
         rnd_info["accurate_route_ms"] = wall(lambda: tt.tt_round(xs, 1e-10), reps=2)
         rnd_info["accurate_route_note"] = ("delta = 1e-10: Householder QR + cluster one-sided Jacobi SVD of "
                                            "R^T per core (no Gram floor; automatic for delta / sqrt(d-1) < 1e-7)")
@@ -1007,6 +1024,10 @@ def main():
         rnd_info["orthonormalise_left_ms"] = wall(lambda: tt.tt_orthonormalise(xs, tt.TT_SWEEP_LEFT))
         rnd_info["block_move_right_ms"] = wall(lambda: tt.tt_block_move_right(Wh, xs[k + 1], 1e-6))
         rnd_info["enrich_right_ms"] = wall(lambda: tt.tt_enrich_right(xs[k], zk, xs[k + 1]))
+        rnd_info["block_move_right_async_ms"] = wall(
+            lambda: tt.tt_block_move_right_async(Wh, xs[k + 1], 1e-6))
+        rnd_info["enrich_right_async_ms"] = wall(
+            lambda: tt.tt_enrich_right_async(xs[k], zk, xs[k + 1]))
         rnd_info["row3_shapes"] = {"block_move": [cfg.r[k], cfg.N, 4, cfg.r[k + 1]],
                                    "enrich": [cfg.r[k], cfg.N, cfg.r[k + 1], 32]}
 
