@@ -702,13 +702,11 @@ static long long svd_ws_elems(long long m, long long q) {
 }
 // Device-side truncation decision of the asynchronous block moves: the rule of svd_gram's
 // host loop (same formulas and summation order) from the descending Gram eigenvalues; writes
-// the rank, the k x k singular vectors of the Gram side with the columns >= rank zeroed and
-// the column factors 1 / sigma (0 beyond the rank), so every later GEMM keeps extent k.
-__global__ void __launch_bounds__(256) svd_decide_kernel(const double* __restrict__ lam,
-                                                         const double* __restrict__ E, int k,
+// the rank and the column factors 1 / sigma (0 beyond the rank); svd_mask_kernel then zeroes
+// the columns >= rank of the Gram side's singular vectors, so every later GEMM keeps extent k.
+__global__ void __launch_bounds__(256) svd_decide_kernel(const double* __restrict__ lam, int k,
                                                          double delta, long long max_rank,
                                                          long long* __restrict__ s_dev,
-                                                         double* __restrict__ side,
                                                          double* __restrict__ fin) {
   __shared__ int s_sk;
   if (threadIdx.x == 0) {
@@ -732,9 +730,17 @@ __global__ void __launch_bounds__(256) svd_decide_kernel(const double* __restric
   }
   __syncthreads();
   const int sk = s_sk;
-  for (int e = threadIdx.x; e < k * k; e += blockDim.x) side[e] = (e % k) < sk ? E[e] : 0.0;
   for (int c = threadIdx.x; c < k; c += blockDim.x)
     fin[c] = c < sk ? 1.0 / sqrt(fmax(lam[c], 1e-300)) : 0.0;
+}
+// side = E with the columns >= *s_dev zeroed (k x k, all SMs)
+__global__ void svd_mask_kernel(const double* __restrict__ E, int k,
+                                const long long* __restrict__ s_dev, double* __restrict__ side) {
+  const int sk = (int)*s_dev;
+  const long long kk = (long long)k * k;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < kk;
+       e += (long long)gridDim.x * blockDim.x)
+    side[e] = (int)(e % k) < sk ? E[e] : 0.0;
 }
 
 static cudaError_t svd_gram(const double* M, long long m, long long q, double delta,
@@ -753,9 +759,11 @@ static cudaError_t svd_gram(const double* M, long long m, long long q, double de
   if (s_dev) {   // asynchronous: rank on the device, every extent stays k (zero padding)
     double* side = left ? b.Us : b.Vs;
     double* fin = b.f + 32 * ((k + 31) / 32);
-    svd_decide_kernel<<<1, 256, 0, s>>>(b.lam, b.E, (int)k, delta, max_rank,
-                                        reinterpret_cast<long long*>(s_dev), side, fin);
-    ++g_launches;
+    svd_decide_kernel<<<1, 256, 0, s>>>(b.lam, (int)k, delta, max_rank,
+                                        reinterpret_cast<long long*>(s_dev), fin);
+    svd_mask_kernel<<<(unsigned)std::min<long long>(4096, (k * k + 255) / 256), 256, 0, s>>>(
+        b.E, (int)k, reinterpret_cast<const long long*>(s_dev), side);
+    g_launches += 2;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     s_out = (int)k;
     double* other = left ? b.Vs : b.Us;
