@@ -176,10 +176,11 @@ tt_status tt_round(int64_t d, const int64_t* n, const int64_t* r_in,
  * represents the rounded tensor as it stands and can be passed to every other entry point;
  * r_dev[d+1] (DEVICE int64) receives the effective ranks (r_dev[0] = r_dev[d] = 1), equal to
  * tt_round's r_out (same formulas and summation order).  A consumer that wants compact cores
- * reads r_dev when convenient and slices.  Truncation goes through the Gram matrix as in
- * tt_round's default route, so delta / sqrt(d-1) >= 1e-7 is required (TT_ERR_INVALID_ARGUMENT
- * otherwise; use tt_round).  Other arguments, workspace (tt_round_workspace_size) and
- * errors as tt_round.  The work is that of an untruncated pass (max-rank GEMMs). */
+ * reads r_dev when convenient and slices.  The truncation route is chosen as in tt_round
+ * (Gram matrix for delta / sqrt(d-1) >= 1e-7; below, delta = 0 included, Householder QR + the
+ * cluster Jacobi SVD with the singular values ranked and selected on the device).  Other
+ * arguments, workspace (tt_round_workspace_size) and errors as tt_round.  The work is that
+ * of an untruncated pass (max-rank GEMMs). */
 tt_status tt_round_async(int64_t d, const int64_t* n, const int64_t* r_in,
                          const double* const* cores_in, double delta, int64_t max_rank,
                          int64_t* r_storage, int64_t* r_dev, double* const* cores_out,

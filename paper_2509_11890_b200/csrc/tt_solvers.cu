@@ -291,6 +291,73 @@ __global__ void __launch_bounds__(256) trunc_decide_kernel(
 }
 __global__ void set_rank_kernel(long long* r_dev, long long idx, long long val) { r_dev[idx] = val; }
 
+// Device-side decision of the accurate truncation (tt_round_async below the Gram floor): the
+// unsorted singular values sg[0..kk) of the cluster Jacobi SVD are ranked by counting (the
+// stable descending order of the host's std::stable_sort), then thread 0 applies the host
+// loop's rule (numerical zeros sigma <= rk1 eps sigma_max, the delta tail, max_rank) with the
+// same formulas and summation order.  perm[0..kk) = the sorted order, perm[kk] = the rank.
+__global__ void __launch_bounds__(256) acc_decide_kernel(const double* __restrict__ sg, int kk,
+                                                         int rk1, int first, double fac,
+                                                         long long max_rank,
+                                                         double* __restrict__ thr_dev,
+                                                         long long* __restrict__ r_dev,
+                                                         int* __restrict__ perm) {
+  __shared__ int s_perm[256];
+  __shared__ int s_sk;
+  for (int i = threadIdx.x; i < kk; i += blockDim.x) {
+    const double v = sg[i];
+    int rk = 0;
+    for (int j = 0; j < kk; ++j) rk += (sg[j] > v) || (sg[j] == v && j < i);
+    s_perm[rk] = i;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double thr;
+    if (first) {
+      double nrm2 = 0.0;
+      for (int i = 0; i < kk; ++i) nrm2 += sg[i] * sg[i];
+      thr = fac * sqrt(nrm2);
+      *thr_dev = thr;
+    } else {
+      thr = *thr_dev;
+    }
+    const double smax = sg[s_perm[0]];
+    int nz = 0;
+    for (int i = 0; i < kk; ++i)
+      if (sg[s_perm[i]] > (double)rk1 * 1.1e-16 * smax) ++nz;
+    if (nz == 0) nz = 1;
+    int sk = nz;
+    double tail = 0.0;
+    for (int i = nz - 1; i >= 1; --i) {
+      tail += sg[s_perm[i]] * sg[s_perm[i]];
+      if (sqrt(tail) <= thr) sk = i; else break;
+    }
+    if (max_rank > 0 && sk > max_rank) sk = (int)max_rank;
+    s_sk = sk;
+    *r_dev = sk;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kk; i += blockDim.x) perm[i] = s_perm[i];
+  if (threadIdx.x == 0) perm[kk] = s_sk;
+}
+// the selected singular triplets zero-padded to the full width kk (rank = perm[kk]):
+// Usel (kk x kk) = J[:, perm] with columns >= rank zero, SJt (kk x rk1) = (R^T J)[:, perm]^T
+// with rows >= rank zero
+__global__ void svd_select_padded_kernel(const double* __restrict__ BJ, const double* __restrict__ J,
+                                         const int* __restrict__ perm, int kk, int rk1,
+                                         double* __restrict__ Usel, double* __restrict__ SJt) {
+  const int sk = perm[kk];
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < kk * kk) {
+    const int r = e / kk, i = e - r * kk;
+    Usel[e] = i < sk ? J[(long long)r * kk + perm[i]] : 0.0;
+  }
+  if (e < kk * rk1) {
+    const int i = e / rk1, col = e - i * rk1;
+    SJt[e] = i < sk ? BJ[(long long)col * kk + perm[i]] : 0.0;
+  }
+}
+
 static tt_status round_impl(int64_t d, const int64_t* n, const int64_t* r_in,
                             const double* const* cores_in, double delta, int64_t max_rank,
                             int64_t* r_out, double* const* cores_out, void* workspace,
@@ -471,7 +538,7 @@ static tt_status round_impl(int64_t d, const int64_t* n, const int64_t* r_in,
   // preconditioned dgejsv, where R's own columns need 11-26+ growing with the condition)
   // where the Gram route's floor (singular values below ~1e-8 sigma_max unresolved) reaches the
   // per-core threshold: delta / sqrt(d-1) < 1e-7, delta = 0 included; debug bit 24 forces it.
-  const bool accurate = !async && (phases & 2) &&
+  const bool accurate = (phases & 2) &&
       ((g_dbg_flags & (1 << 24)) || delta / std::sqrt((double)std::max<int64_t>(d - 1, 1)) < 1e-7);
   int64_t kstart = 0;   // the Gram route continues from the first core the accurate one left
   for (int64_t k = 0; accurate && k < d - 1 && e == cudaSuccess; ++k) {
@@ -498,6 +565,33 @@ static tt_status round_impl(int64_t d, const int64_t* n, const int64_t* r_in,
     sa.sigma = lam;
     sa.sweeps = nullptr;
     if ((e = launch_svd(sa, s)) != cudaSuccess) break;
+    if (async) {   // rank, order and selection on the device; every extent stays kk
+      double* Usel = esc;
+      double* SJt = esc + rmax * rmax;
+      int* dperm = reinterpret_cast<int*>(esc + 2 * rmax * rmax);
+      const double fac = delta / std::sqrt((double)std::max<int64_t>(d - 1, 1));
+      acc_decide_kernel<<<1, 256, 0, s>>>(lam, (int)kk, (int)rk1, k == 0 ? 1 : 0, fac,
+                                          (long long)max_rank, dg,
+                                          reinterpret_cast<long long*>(r_dev) + k + 1, dperm);
+      const long long nsel = std::max(kk, rk1) * kk;
+      svd_select_padded_kernel<<<(unsigned)((nsel + 255) / 256), 256, 0, s>>>(
+          Bm, V, dperm, (int)kk, (int)rk1, Usel, SJt);
+      g_launches += 2;
+      if ((e = cudaGetLastError()) != cudaSuccess) break;
+      e = launch_gemm(true, false, gp(W[k], kk, Usel, kk, Tmp, m, kk, kk, tt::map_plain(kk),
+                                      tt::map_plain(1)), s);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(W[k], Tmp, sizeof(double) * m * kk, cudaMemcpyDeviceToDevice, s);
+      if (e != cudaSuccess) break;
+      const long long qa3 = n[k + 1] * r[k + 2];
+      e = launch_gemm(true, false, gp(SJt, rk1, W[k + 1], qa3, Tmp, kk, qa3, rk1, tt::map_plain(qa3),
+                                      tt::map_plain(1)), s);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(W[k + 1], Tmp, sizeof(double) * kk * qa3, cudaMemcpyDeviceToDevice, s);
+      r[k + 1] = kk;
+      kstart = k + 1;
+      continue;
+    }
     std::vector<double> sg(kk);
     if ((e = cudaMemcpyAsync(sg.data(), lam, sizeof(double) * kk, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
         (e = cudaStreamSynchronize(s)) != cudaSuccess)
@@ -645,10 +739,6 @@ tt_status tt_round_async(int64_t d, const int64_t* n, const int64_t* r_in,
                          void* workspace, size_t workspace_bytes, void* stream) {
   CallScope scope;
   if (!r_dev) return fail(TT_ERR_NULL_POINTER, "r_dev is NULL");
-  if (!(delta >= 0.0) || delta / std::sqrt((double)std::max<int64_t>(d - 1, 1)) < 1e-7)
-    return fail(TT_ERR_INVALID_ARGUMENT,
-                "tt_round_async truncates through the Gram matrix: delta / sqrt(d-1) must be "
-                ">= 1e-7 (use tt_round for tighter tolerances)");
   return round_impl(d, n, r_in, cores_in, delta, max_rank, r_storage, cores_out, workspace,
                     workspace_bytes, stream, 3, "tt_round_async", r_dev);
 }

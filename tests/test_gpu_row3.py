@@ -357,10 +357,38 @@ def test_tt_round_async_max_rank_and_errors(tt):
     assert max(int(v) for v in ranks.tolist()) == 5
     comp = tt.tt_compact(padded, ranks)
     assert rel_fro(full_vector([h(c) for c in comp]), full_vector([h(c) for c in sync])) <= 1e-10
-    with pytest.raises(tt.TTError):      # below the Gram route's floor: tt_round's job
-        tt.tt_round_async(x, 1e-9)
     with pytest.raises(tt.TTError):
-        tt.tt_round_async(x, 0.0)
+        tt.tt_round_async(x, -1.0)
+
+
+@pytest.mark.parametrize("delta", [0.0, 1e-9, 1e-2])
+def test_tt_round_async_accurate_route(tt, delta):
+    """Below the Gram floor (delta / sqrt(d-1) < 1e-7, delta = 0 included; forced at 1e-2 by
+    debug bit 24) the asynchronous call takes the accurate route too -- cluster QR + cluster
+    Jacobi SVD, the singular values ranked and selected on the device: the ranks of the
+    synchronous call, exact zero padding, delta = 0 reconstructs the graded train to 1e-12."""
+    rng = np.random.default_rng(91)
+    d, N = 6, 4
+    x = ttgen.gaussian_tt_vector(rng, N, ttgen.capped_ranks(d, N, 12))
+    for k in range(d):
+        x[k] = x[k] * np.logspace(0, -13, x[k].shape[2])[None, None, :]
+    xg = [g(c) for c in x]
+    tt.tt_debug_set_flags((1 << 24) if delta >= 1e-7 else 0)
+    try:
+        sync = [h(c) for c in tt.tt_round(xg, delta)]
+        padded, ranks = tt.tt_round_async(xg, delta)
+        torch.cuda.synchronize()
+    finally:
+        tt.tt_debug_set_flags(0)
+    ro = [int(v) for v in ranks.tolist()]
+    assert ro == [1] + [c.shape[2] for c in sync]
+    for k, c in enumerate(padded):
+        ch = h(c)
+        assert not ch[ro[k]:, :, :].any() and not ch[:, :, ro[k + 1]:].any()
+    comp = [h(c) for c in tt.tt_compact(padded, ranks)]
+    v, vc, vs = full_vector(x), full_vector(comp), full_vector(sync)
+    assert rel_fro(vc, vs) <= 1e-12
+    assert rel_fro(vc, v) <= (1e-12 if delta == 0.0 else delta * (1 + 1e-6))
 
 
 def test_tt_round_async_graph_capture(tt):
