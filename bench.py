@@ -1015,6 +1015,7 @@ def main():
             rnd_info["async"]["graph_replay_ms"] = None
             rnd_info["async"]["graph_error"] = str(exc)[:200]
         rnd_info["accurate_route_ms"] = wall(lambda: tt.tt_round(xs, 1e-10), reps=2)
+        rnd_info["accurate_route_async_ms"] = wall(lambda: tt.tt_round_async(xs, 1e-10), reps=2)
         rnd_info["accurate_route_note"] = ("delta = 1e-10: Householder QR + cluster one-sided Jacobi SVD of "
                                            "R^T per core (no Gram floor; automatic for delta / sqrt(d-1) < 1e-7)")
         gen = torch.Generator(device=dev).manual_seed(13)
